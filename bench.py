@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""FP64 RSVD truncations/sec on B200 (BASELINE.json metric).
+
+Default workload: config C4 of BASELINE.json — a batch of 32 independent
+4096 x 4096 FP64 bond matrices (chi=256, d=16), A = U diag(sigma) V^T with
+Haar factors and sigma_i = exp(-0.02 i)(1 + 0.1 g_i), truncated to k=256 with
+p=20 (l = 276) and q=2.  It is "4096^2, k=256", fits one GPU and shards by
+item: under torchrun every rank factorizes its own 32 matrices (items
+rank*32 .. rank*32+31), no collective on the data path -> scaling "weak".
+
+  value  : truncations/s over all ranks, inputs resident in HBM, device time
+           (CUDA events on the launching stream, max over ranks).
+  e2e    : same metric through the public API with pinned HOST buffers
+           (H2D of A and D2H of U, S, Vt inside every timed step).
+  roofline: the dominant kernel (the DMMA A-pass GEMM) against the measured
+           FP64 tensor peak.
+  cpu_baseline: the CPU oracle (restated reference rsvd, OpenBLAS/LAPACK) on
+           the host cores, rank 0 at N=1, on a bounded sample.
+
+`--impl reference` times the reference's CPU implementation of the path
+(the oracle port; the reference itself needs Eigen and cannot be built here)
+on the same config with all host threads.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1  # measured: mma.sync f64 probe, profiles/r01_fp64_peak.txt
+FP64_PEAK_SOURCE = ("measured DMMA (mma.sync .f64) throughput on this pool's B200, "
+                    "profiles/r01_fp64_peak.txt; MEASURED_PEAKS.json has no FP64 figure "
+                    "(cuBLAS DGEMM 8192^3 measured 35.5)")
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def f_alg(m, n, k, ell, q):
+    """LAPACK-nominal flops per truncation."""
+    return (4 * (q + 1) * m * n * ell + 2 * m * ell * k
+            + (q + 1) * (4 * m * ell ** 2 - 4 * ell ** 3 / 3)
+            + q * (4 * n * ell ** 2 - 4 * ell ** 3 / 3) + 6 * n * ell ** 2 + 20 * ell ** 3)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, ValueError):
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def make_inputs(cfg, items, first_item, device):
+    from paper_1710_01463_b200 import synth
+
+    return synth.make_batch(cfg, device=device, batch=items, first_item=first_item)
+
+
+def cpu_oracle_rsvd(A_items, cfg, seeds, threads):
+    """Time the oracle rsvd on host copies of the given items; returns
+    (seconds per truncation list)."""
+    from oracle import oracle
+
+    oracle.set_threads(threads)
+    times = []
+    for a, s in zip(A_items, seeds):
+        t0 = time.perf_counter()
+        oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+
+    from paper_1710_01463_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    threads = host_threads()
+    sample = max(1, args.ref_sample)
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    gauss = None
+    if dev == "cpu":
+        from oracle import oracle
+        gauss = lambda seed, count: torch.from_numpy(oracle.fill_gaussian(seed, count))  # noqa
+    A = synth.make_batch(cfg, device=dev, batch=sample, gauss=gauss)
+    mats = [np.asfortranarray(A[i].cpu().numpy()) for i in range(sample)]
+    del A
+    seeds = synth.omega_seeds(cfg, batch=sample)
+    for _ in range(args.warmup):
+        cpu_oracle_rsvd(mats[:1], cfg, seeds[:1], threads)
+    t = 0.0
+    for _ in range(args.steps):
+        t += sum(cpu_oracle_rsvd(mats, cfg, seeds, threads))
+    value = args.steps * sample / t
+    line = {
+        "impl": "reference",
+        "metric": "FP64 RSVD truncations/sec (4096^2, k=256)",
+        "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json C4 recipe, seeded CounterRng)",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": cfg.batch,
+                   "rank_k": cfg.rank, "ell": cfg.ell, "power_q": cfg.power,
+                   "step": f"{sample} truncation(s) of the workload (bounded CPU sample)"},
+        "cpu_baseline": {"value": value, "unit": "truncations/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{sample} of the {cfg.batch} {cfg.m}x{cfg.n} matrices per step, "
+                                   "oracle rsvd (restated reference, OpenBLAS 0.3.31 LAPACK)"},
+        "e2e": {"value": value, "unit": "truncations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_01463_b200 import Handle, RsvdParams, _lib, rsvd_batched, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    B = cfg.batch if args.batch is None else args.batch
+    first = rank * B
+    A = make_inputs(cfg, B, first, dev)
+    seeds = synth.omega_seeds(cfg, batch=B, first_item=first)
+    params = RsvdParams(cfg.rank, cfg.ell, cfg.power, 0)
+    h = Handle(local_rank)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        rsvd_batched(A, params, seeds, handle=h)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region --------------------------------
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.kernel_launches()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        f = rsvd_batched(A, params, seeds, handle=h)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    value = B * world * args.steps / (ms / 1000.0)
+    ranks_ok = all(r == cfg.rank for r in f.ranks)
+
+    # ---- per-stage profile pass (events around each stage) ------------
+    _lib.profile_enable(h, True)
+    prof_steps = max(1, min(2, args.steps))
+    for _ in range(prof_steps):
+        rsvd_batched(A, params, seeds, handle=h)
+    torch.cuda.synchronize()
+    prof = _lib.profile_read(h)
+    _lib.profile_enable(h, False)
+    sweeps = _lib.last_jacobi_sweeps(h)
+    ap_ms = prof["apass_nn"][0] + prof["apass_tn"][0]
+    ap_calls = prof["apass_nn"][1] + prof["apass_tn"][1]
+    ap_flops_per_launch = 2.0 * cfg.m * cfg.n * cfg.ell * B  # algorithmic: one pass over A per item
+    achieved = ap_flops_per_launch / (ap_ms / ap_calls / 1000.0) / 1e12 if ap_calls else None
+    step_ms_prof = sum(v[0] for v in prof.values()) / prof_steps
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("apass_dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- end-to-end through the public API with pinned host buffers ---
+    A_host = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, pin_memory=True)
+    A_host.copy_(A)
+    del A
+    torch.cuda.empty_cache()
+    rsvd_batched(A_host, params, seeds, handle=h)  # warm the host-path workspace
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fe = rsvd_batched(A_host, params, seeds, handle=h)
+        _ = fe.sigma[0, 0].item()  # result read on the host
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = B * world * args.steps / t_e2e
+    k = max(cfg.rank, 1)
+    h2d = B * cfg.m * cfg.n * 8 + B * 8
+    d2h = B * (cfg.m * k + k + k * cfg.n) * 8 + B * 16
+
+    # ---- CPU baseline (rank 0, N=1) -----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_cpu = max(1, args.cpu_sample)
+        mats = [np.asfortranarray(A_host[i].numpy()) for i in range(min(n_cpu, B))]
+        times = cpu_oracle_rsvd(mats, cfg, seeds[:len(mats)], threads)
+        cpu = {"value": len(times) / sum(times), "unit": "truncations/s", "cores": threads,
+               "kind": "port",
+               "sample": f"{len(times)} of the {B} {cfg.m}x{cfg.n} matrices, oracle rsvd "
+                         "(restated reference: cblas_dgemm + dgeqrf/dorgqr + dgesdd, "
+                         "OpenBLAS 0.3.31), all host threads"}
+
+    if rank == 0:
+        falg = f_alg(cfg.m, cfg.n, cfg.rank, cfg.ell, cfg.power)
+        line = {
+            "metric": "FP64 RSVD truncations/sec (4096^2, k=256)",
+            "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE.json config recipe, seeded CounterRng, Haar factors)",
+            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": B,
+                       "global_batch": B * world, "rank_k": cfg.rank, "ell": cfg.ell,
+                       "power_q": cfg.power, "parallelism": f"batch split dp{world}",
+                       "l2": "inputs larger than L2 (%.1f GB per rank)" % (B * cfg.m * cfg.n * 8 / 1e9)},
+            "e2e": {"value": e2e_value, "unit": "truncations/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
+                         "traffic": traffic,
+                         "kernel": "dgemm_kernel A-pass (Y=A X / Z=A^T Y), batched over the step",
+                         "algorithmic_flops_per_launch": ap_flops_per_launch,
+                         "peak_source": FP64_PEAK_SOURCE,
+                         "apass_share_of_step": ap_ms / prof_steps / step_ms_prof},
+            "pipeline": {"tflops_alg": falg * B * world * args.steps / (ms / 1000) / 1e12 / world,
+                         "frac_fp64_peak": falg * B * args.steps / (ms / 1000) / 1e12 / FP64_PEAK_TFLOPS,
+                         "stage_ms_per_step": {k2: v[0] / prof_steps for k2, v in prof.items()},
+                         "jacobi_sweeps": sweeps, "ranks_ok": ranks_ok},
+            "clocks": clk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--batch", type=int, default=None, help="override items per rank")
+    ap.add_argument("--cpu-sample", type=int, default=2)
+    ap.add_argument("--ref-sample", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

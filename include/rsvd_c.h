@@ -1,0 +1,137 @@
+/*
+ * rsvd_c.h — C ABI of the B200-native randomized truncated SVD engine
+ * (librsvd_b200.so, built from paper_1710_01463_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's factorization path
+ * (rlftn, /root/reference/proj).  Every entry point names the reference
+ * interface it replaces.  Plain pointers and sizes only: no torch or Eigen
+ * types cross this boundary.  Matrices are column-major with an explicit
+ * leading dimension, the layout of Eigen's default storage that the reference
+ * hands to LAPACK (types.hpp:12-13, lapack.cpp:122).
+ *
+ * Pointers are host or device memory as selected by `flags`
+ * (RSVD_PTR_HOST / RSVD_PTR_DEVICE).  With host pointers the call copies in,
+ * computes on the handle's stream and copies out before returning.  With
+ * device pointers the call is stream-ordered on the handle's stream; scalar
+ * outputs (rank, discarded weight) are still returned synchronously.
+ *
+ * Return codes mirror the reference's exception classes:
+ *   RSVD_OK            0
+ *   RSVD_ERR_INVALID   1  std::invalid_argument (factorize.cpp:44-45,56-59,79-83)
+ *   RSVD_ERR_NUMERICAL 2  std::runtime_error("lapack: ... failed", lapack.cpp:52-55)
+ *   RSVD_ERR_CUDA      3  device / driver failure (no reference analogue)
+ * rsvd_last_error() returns the message of the handle's last failure, using
+ * the reference's wording for the argument errors.
+ */
+#ifndef RSVD_C_H_
+#define RSVD_C_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSVD_OK 0
+#define RSVD_ERR_INVALID 1
+#define RSVD_ERR_NUMERICAL 2
+#define RSVD_ERR_CUDA 3
+
+#define RSVD_PTR_HOST 0
+#define RSVD_PTR_DEVICE 1
+
+typedef struct rsvd_context* rsvd_handle;
+
+/* Library / handle lifecycle.  A handle owns the device workspace (grow-only,
+ * like the reference's thread_local LAPACK Workspace, lapack.cpp:23-50), a
+ * stream and its last-error string.  One handle per host thread (the
+ * reference's functions are re-entrant). */
+int rsvd_create(rsvd_handle* handle, int device);
+int rsvd_destroy(rsvd_handle handle);
+const char* rsvd_last_error(rsvd_handle handle);
+/* Use a caller-owned cudaStream_t (e.g. torch's current stream); NULL = the
+ * handle's own stream. */
+int rsvd_set_stream(rsvd_handle handle, void* cuda_stream);
+/* Release the cached workspace. */
+int rsvd_trim(rsvd_handle handle);
+/* Library version string. */
+const char* rsvd_version(void);
+
+/* rlftn::mix64 / derive_seed (rng.hpp:11-22). */
+uint64_t rsvd_mix64(uint64_t z);
+uint64_t rsvd_derive_seed(uint64_t seed, uint64_t tag);
+
+/* rlftn::CounterRng(seed).fill_gaussian(out, count) (rng.hpp:62-64), computed
+ * on the device.  64-bit words are bit-exact; normals use the device libm
+ * (see DESIGN.md for the measured ulp distance to glibc). */
+int rsvd_fill_gaussian_f64(rsvd_handle handle, uint64_t seed, double* out, int64_t count,
+                           int flags);
+
+/* rlftn::rsvd<double>(a, RsvdParams{rank, oversample, power, seed})
+ * (factorize.hpp:62-63, factorize.cpp:76-95).
+ *   oversample is the total sample width l (0 -> min(2*rank, min(m,n)));
+ *   U: m x rank (ldu >= m), S: rank, Vt: rank x n (ldvt >= rank).
+ *   Only the leading *out_rank columns / values / rows are meaningful; the
+ *   rest of the caller's buffers is zeroed.  *discarded_weight is the sum of
+ *   squares of the sampled but dropped values (discarded_exact = false). */
+int rsvd_f64(rsvd_handle handle, const double* A, int64_t m, int64_t n, int64_t lda,
+             int64_t rank, int64_t oversample, int power, uint64_t seed, double* U, int64_t ldu,
+             double* S, double* Vt, int64_t ldvt, int64_t* out_rank, double* discarded_weight,
+             int flags);
+
+/* Batched rsvd over `batch` independent matrices of one shape (a TEBD layer's
+ * disjoint bonds, mps.cpp:448-457; the sector loop of block_factorize,
+ * blocks.cpp:60-84).  Matrix b starts at A + b*strideA, U + b*strideU,
+ * S + b*strideS, Vt + b*strideVt and uses seeds[b] (host array).
+ * out_rank / discarded_weight are host arrays of length batch. */
+int rsvd_f64_batched(rsvd_handle handle, int64_t batch, const double* A, int64_t m, int64_t n,
+                     int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
+                     const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
+                     int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
+                     int64_t* out_rank, double* discarded_weight, int flags);
+
+/* rlftn::randomized_range<double>(a, ell, power, seed) (factorize.hpp:56-57,
+ * factorize.cpp:52-74): Q (m x ell, ldq >= m) with orthonormal columns
+ * spanning the sampled dominant range. */
+int rsvd_randomized_range_f64(rsvd_handle handle, const double* A, int64_t m, int64_t n,
+                              int64_t lda, int64_t ell, int power, uint64_t seed, double* Q,
+                              int64_t ldq, int flags);
+
+/* rlftn::reconstruction_error(a, f, ErrorNorm::frobenius) (factorize.cpp:97-104):
+ * ||A - U diag(S) Vt||_F for a rank-r factorization. */
+int rsvd_reconstruction_error_f64(rsvd_handle handle, const double* A, int64_t m, int64_t n,
+                                  int64_t lda, const double* U, int64_t ldu, const double* S,
+                                  const double* Vt, int64_t ldvt, int64_t r, double* out,
+                                  int flags);
+
+/* Argument validation of rlftn::rsvd + randomized_range with the reference's
+ * order and messages (factorize.cpp:79-83, 56-59); host-only, usable without a
+ * GPU.  On success *ell_out is the resolved sample width. */
+int rsvd_validate_params(int64_t m, int64_t n, int64_t rank, int64_t oversample, int power,
+                         int64_t* ell_out, char* msg, int64_t msg_len);
+
+/* Diagnostics (no reference analogue; the reference only brackets the
+ * factorization with steady_clock, mps.cpp:275-277).
+ *   rsvd_kernel_launches: engine kernels launched by this process so far.
+ *   rsvd_profile_enable:  per-stage CUDA-event timing of subsequent calls.
+ *   rsvd_profile_read:    accumulated ms / call counts per stage; returns the
+ *                         number of stages (names via rsvd_profile_stage_name).
+ *   rsvd_last_jacobi_sweeps: max one-sided Jacobi sweeps of the last rsvd. */
+uint64_t rsvd_kernel_launches(void);
+int rsvd_profile_enable(rsvd_handle handle, int on);
+int rsvd_profile_read(rsvd_handle handle, double* ms, int64_t* calls, int n);
+const char* rsvd_profile_stage_name(int i);
+int rsvd_last_jacobi_sweeps(rsvd_handle handle);
+
+/* Testing hook (not part of the reference surface): the engine's batched FP64
+ * GEMM, C = op(A) B, on device pointers; trans_a selects A^T (A stored K x M). */
+int rsvd_testing_dgemm(rsvd_handle handle, int trans_a, int64_t M, int64_t N, int64_t K,
+                       const double* A, int64_t lda, int64_t strideA, const double* B,
+                       int64_t ldb, int64_t strideB, double* C, int64_t ldc, int64_t strideC,
+                       int64_t batch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSVD_C_H_ */

@@ -1,0 +1,26 @@
+"""B200-native randomized truncated SVD (RSVD) engine.
+
+Drop-in for the factorization path of rlftn (arXiv 1710.01463's
+TEBD bond compression): ``rsvd``, ``randomized_range``,
+``reconstruction_error`` and the seed/RNG contract, computed by hand-written
+sm_100a CUDA kernels in ``librsvd_b200.so`` behind the C ABI of
+``include/rsvd_c.h``.
+"""
+from ._lib import DeviceError, Handle, InvalidArgument, LibraryMissing, NumericalError
+from .factorize import (
+    BatchedFactorization,
+    ErrorNorm,
+    RsvdParams,
+    TruncatedFactorization,
+    randomized_range,
+    reconstruction_error,
+    rsvd,
+    rsvd_batched,
+)
+from .rng import CounterRng, derive_seed, mix64, seed_tag
+
+__all__ = [
+    "BatchedFactorization", "CounterRng", "DeviceError", "ErrorNorm", "Handle", "InvalidArgument",
+    "LibraryMissing", "NumericalError", "RsvdParams", "TruncatedFactorization", "derive_seed",
+    "mix64", "randomized_range", "reconstruction_error", "rsvd", "rsvd_batched", "seed_tag",
+]

@@ -1,0 +1,201 @@
+"""ctypes binding of librsvd_b200.so (the C ABI declared in include/rsvd_c.h).
+
+The product path has no CPU fallback: if the CUDA library is missing or fails
+to load, every entry point raises.  Build it with ``python -c "import
+__graft_entry__ as g; g.build()"`` (or ``make -C paper_1710_01463_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsvd_b200.so")
+
+RSVD_OK = 0
+RSVD_ERR_INVALID = 1
+RSVD_ERR_NUMERICAL = 2
+RSVD_ERR_CUDA = 3
+PTR_HOST = 0
+PTR_DEVICE = 1
+
+# Every symbol include/rsvd_c.h declares, with its ctypes signature.
+_c_i64 = ctypes.c_int64
+_c_u64 = ctypes.c_uint64
+_c_int = ctypes.c_int
+_c_vp = ctypes.c_void_p
+_c_dp = ctypes.c_void_p  # double* passed as raw addresses (host or device)
+
+SIGNATURES = {
+    "rsvd_create": (_c_int, [ctypes.POINTER(_c_vp), _c_int]),
+    "rsvd_destroy": (_c_int, [_c_vp]),
+    "rsvd_last_error": (ctypes.c_char_p, [_c_vp]),
+    "rsvd_set_stream": (_c_int, [_c_vp, _c_vp]),
+    "rsvd_trim": (_c_int, [_c_vp]),
+    "rsvd_version": (ctypes.c_char_p, []),
+    "rsvd_mix64": (_c_u64, [_c_u64]),
+    "rsvd_derive_seed": (_c_u64, [_c_u64, _c_u64]),
+    "rsvd_fill_gaussian_f64": (_c_int, [_c_vp, _c_u64, _c_dp, _c_i64, _c_int]),
+    "rsvd_f64": (
+        _c_int,
+        [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_u64, _c_dp, _c_i64,
+         _c_dp, _c_dp, _c_i64, ctypes.POINTER(_c_i64), ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
+    "rsvd_f64_batched": (
+        _c_int,
+        [_c_vp, _c_i64, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
+         ctypes.POINTER(_c_u64), _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_dp, _c_i64, _c_i64,
+         ctypes.POINTER(_c_i64), ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
+    "rsvd_randomized_range_f64": (
+        _c_int, [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_u64, _c_dp, _c_i64, _c_int]
+    ),
+    "rsvd_validate_params": (
+        _c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_int, ctypes.POINTER(_c_i64), ctypes.c_char_p,
+                 _c_i64]
+    ),
+    "rsvd_kernel_launches": (_c_u64, []),
+    "rsvd_profile_enable": (_c_int, [_c_vp, _c_int]),
+    "rsvd_profile_read": (_c_int, [_c_vp, ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(_c_i64), _c_int]),
+    "rsvd_profile_stage_name": (ctypes.c_char_p, [_c_int]),
+    "rsvd_last_jacobi_sweeps": (_c_int, [_c_vp]),
+    "rsvd_testing_dgemm": (
+        _c_int,
+        [_c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
+         _c_i64, _c_i64, _c_i64],
+    ),
+    "rsvd_reconstruction_error_f64": (
+        _c_int,
+        [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_dp, _c_dp, _c_i64, _c_i64,
+         ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def load() -> ctypes.CDLL:
+    """Load librsvd_b200.so (once).  Raises LibraryMissing when absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} not built: run `make -C paper_1710_01463_b200/csrc` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+class InvalidArgument(ValueError):
+    """Mirrors the reference's std::invalid_argument."""
+
+
+class NumericalError(RuntimeError):
+    """Mirrors the reference's std::runtime_error from LAPACK failures."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / driver failure inside the engine."""
+
+
+def raise_for(rc: int, handle) -> None:
+    if rc == RSVD_OK:
+        return
+    msg = load().rsvd_last_error(handle)
+    msg = msg.decode() if msg else ""
+    if rc == RSVD_ERR_INVALID:
+        raise InvalidArgument(msg)
+    if rc == RSVD_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    raise DeviceError(msg or f"rsvd error code {rc}")
+
+
+class Handle:
+    """Owns one rsvd_handle (device workspace + stream).  One per thread."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        h = ctypes.c_void_p()
+        rc = lib.rsvd_create(ctypes.byref(h), int(device))
+        if rc != RSVD_OK:
+            msg = lib.rsvd_last_error(h) if h else b"rsvd_create failed"
+            if h:
+                lib.rsvd_destroy(h)
+            raise DeviceError((msg or b"").decode())
+        self._h = h
+        self.device = device
+
+    @property
+    def raw(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().rsvd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_handles = threading.local()
+
+
+def default_handle(device: int = 0) -> Handle:
+    d = getattr(_handles, "by_device", None)
+    if d is None:
+        d = _handles.by_device = {}
+    h = d.get(device)
+    if h is None:
+        h = d[device] = Handle(device)
+    return h
+
+
+def validate_params(m: int, n: int, rank: int, oversample: int, power: int) -> int:
+    """Host-only argument check (rsvd_validate_params); returns l or raises
+    InvalidArgument with the reference's message."""
+    lib = load()
+    ell = ctypes.c_int64(0)
+    buf = ctypes.create_string_buffer(256)
+    rc = lib.rsvd_validate_params(m, n, rank, oversample, power, ctypes.byref(ell), buf, 256)
+    if rc != RSVD_OK:
+        raise InvalidArgument(buf.value.decode())
+    return ell.value
+
+
+def kernel_launches() -> int:
+    return int(load().rsvd_kernel_launches())
+
+
+def profile_enable(handle: Handle, on: bool = True) -> None:
+    raise_for(load().rsvd_profile_enable(handle.raw, int(on)), handle.raw)
+
+
+def profile_read(handle: Handle) -> dict:
+    lib = load()
+    n = 16
+    ms = (ctypes.c_double * n)()
+    calls = (ctypes.c_int64 * n)()
+    k = lib.rsvd_profile_read(handle.raw, ms, calls, n)
+    return {lib.rsvd_profile_stage_name(i).decode(): (ms[i], int(calls[i])) for i in range(k)}
+
+
+def last_jacobi_sweeps(handle: Handle) -> int:
+    return int(load().rsvd_last_jacobi_sweeps(handle.raw))

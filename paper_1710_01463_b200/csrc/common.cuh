@@ -1,0 +1,109 @@
+// Shared device/host helpers for the B200 RSVD engine (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace rsvd {
+
+// Strided batch of column-major matrices: element (i, j) of item b lives at
+// base[b * stride + i + j * ld].
+struct MatRef {
+  double* base;
+  int64_t ld;
+  int64_t stride;
+  __host__ __device__ double* item(int64_t b) const { return base + b * stride; }
+};
+struct CMatRef {
+  const double* base;
+  int64_t ld;
+  int64_t stride;
+  __host__ __device__ const double* item(int64_t b) const { return base + b * stride; }
+  CMatRef() = default;
+  __host__ __device__ CMatRef(const double* p, int64_t l, int64_t s) : base(p), ld(l), stride(s) {}
+  __host__ __device__ CMatRef(const MatRef& m) : base(m.base), ld(m.ld), stride(m.stride) {}
+};
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+// Number of engine kernels launched by this process (reported by bench.py as
+// gpu_launches; every launch site goes through RSVD_LAUNCH).
+extern std::atomic<uint64_t> g_kernel_launches;
+#define RSVD_CUDA(call) ::rsvd::check_cuda((call), #call)
+#define RSVD_LAUNCH(what)                                                  \
+  do {                                                                     \
+    ::rsvd::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);     \
+    ::rsvd::check_cuda(cudaGetLastError(), what);                          \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+// ---------------------------------------------------------------- kernels
+// Launch wrappers (defined in the .cu files).  All are batched and
+// stream-ordered; none synchronizes.
+
+// rng.cu — CounterRng Gaussian fill of `rows x cols` (column-major, ld) per
+// item, seeds[b] per item (device array); columns >= valid_cols are zeroed.
+void launch_fill_gaussian(MatRef out, int64_t rows, int64_t cols, int64_t valid_cols,
+                          const uint64_t* seeds_dev, int64_t batch, cudaStream_t st);
+void launch_fill_gaussian_flat(double* out, int64_t count, uint64_t seed, cudaStream_t st);
+
+// gemm_f64.cu — C = op(A) * B with op(A) = A (NN) or A^T (TN, A stored K x M).
+// When splits > 1 the partial products go to `partial` (splits*batch items
+// of M x N, ld M) and are reduced in fixed order into C (deterministic).
+void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
+           int64_t batch, double* partial, int64_t partial_capacity, cudaStream_t st);
+int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
+
+// chol.cu — pivoted / plain Cholesky of SPD Grams (ell x ell, ld ell).
+void launch_pchol(const double* G, double* T, double* Rfull, int* rank, int* perm, int64_t ell,
+                  int64_t ellp, double tau, int64_t batch, cudaStream_t st);
+
+// jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
+// columns live), accumulating J; sweeps until converged.
+void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                   int64_t batch, cudaStream_t st);
+
+// aux.cu
+void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
+                           const uint64_t* seeds_dev, uint64_t tag, int64_t batch,
+                           cudaStream_t st);
+void launch_transpose(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_t batch,
+                      cudaStream_t st);
+void launch_set_identity(MatRef out, int64_t n, int64_t batch, cudaStream_t st);
+void launch_finalize_spectrum(const double* HJ, int64_t ellp, int64_t ell, int64_t k,
+                              int64_t m, int64_t n, double* sigma_out, int* perm, int* rank,
+                              double* discarded, int64_t batch, cudaStream_t st);
+void launch_gather_scale_columns(const double* src, int64_t ld_src, int64_t stride_src,
+                                 const int* perm, int64_t ellp_perm, const double* sigma,
+                                 int64_t sigma_stride, const int* rank, int64_t rows, int64_t k,
+                                 double* dst,
+                                 int64_t ld_dst, int64_t stride_dst, int64_t batch,
+                                 cudaStream_t st);
+void launch_zero_columns_from_rank(MatRef X, int64_t rows, int64_t cols, const int* rank,
+                                   int64_t batch, cudaStream_t st);
+void launch_zero_rows_from_rank(MatRef X, int64_t rows, int64_t cols, const int* rank,
+                                int64_t batch, cudaStream_t st);
+void launch_copy_matrix(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_t batch,
+                        cudaStream_t st);
+void launch_scale_columns(MatRef X, int64_t rows, int64_t cols, const double* sc, cudaStream_t st);
+void launch_residual_sumsq(CMatRef A, CMatRef R, int64_t rows, int64_t cols, double* partial,
+                           int64_t nparts, cudaStream_t st);
+
+}  // namespace rsvd

@@ -1,0 +1,721 @@
+// Host-side orchestration of the B200 RSVD pipeline and the C ABI
+// (include/rsvd_c.h).
+//
+// One call runs the reference's rsvd (factorize.cpp:76-95) for a whole batch
+// of equally shaped matrices, every stage a batched kernel over all items:
+//
+//   Omega      = CounterRng(seed_b) Gaussians            rng.cu       (factorize.cpp:61-63)
+//   Y          = A Omega                                  gemm NN      (:68)
+//   Q          = orth(Y)                                  CholeskyQR2  (lapack.cpp:180-201)
+//   q times:   Z = A^T Q; Q' = orth(Z); Y = A Q'; Q = orth(Y)           (:69-72)
+//   B^T        = A^T Q            (B = Q^T A, :86, never formed)
+//   B^T        = Qb Rt                                    CholeskyQR2 with R
+//   H = Rt^T;  H J = U~ Sigma                             one-sided Jacobi (lapack.cpp:112-128)
+//   rank cut, discarded weight                            (:17-38, :91)
+//   U = Q U~[:, :r];  Vt = (Qb J[:, :r])^T                gemm NN      (:92)
+//
+// orth() is CholeskyQR2 with a diagonally pivoted first Cholesky: columns
+// whose pivot falls below tau * max pivot (rank deficiency) are replaced by
+// a deterministic Gaussian completion that the second pass orthonormalises,
+// so the result always has l orthonormal columns (lapack.hpp:18-20).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rsvd_c.h"
+#include "common.cuh"
+
+namespace rsvd {
+namespace {
+
+constexpr double kPivotTau = 1e-13;   // relative pivot floor of the CholeskyQR Gram
+constexpr int kMaxSweeps = 40;        // one-sided Jacobi sweep cap
+constexpr uint64_t kCompletionTag = 0x436f6d706c657465ull;  // "Complete"
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+// Grow-only device arena, the analogue of the reference's thread_local
+// LAPACK workspace (lapack.cpp:23-50).  Contents do not persist across calls.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  void reserve(size_t bytes) {
+    if (bytes <= cap) return;
+    if (base) RSVD_CUDA(cudaFree(base));
+    base = nullptr;
+    cap = 0;
+    RSVD_CUDA(cudaMalloc(&base, bytes));
+    cap = bytes;
+  }
+  void release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = 0;
+  }
+};
+
+// Two-phase carve: measure with base == nullptr, then allocate and carve.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+std::atomic<uint64_t> g_kernel_launches{0};
+
+// Per-stage device-time accounting (CUDA events on the launching stream),
+// enabled by rsvd_profile_enable; read back with rsvd_profile_read.
+enum Stage : int {
+  kStOmega = 0,   // Omega generation
+  kStApassNN,     // Y = A X               (A-pass, NN)
+  kStApassTN,     // Z = A^T Y             (A-pass, TN)
+  kStGram,        // G = Y^T Y             (CholeskyQR Gram)
+  kStChol,        // pivoted Cholesky + triangular inverse
+  kStApply,       // Y T, completion, Rf2 Rf1
+  kStJacobi,      // one-sided Jacobi on the l x l factor
+  kStLift,        // spectrum, gathers, U = Q U~, V = Qb J, transposes
+  kNumStages
+};
+const char* const kStageNames[kNumStages] = {"omega", "apass_nn", "apass_tn", "gram",
+                                             "chol",  "apply",    "jacobi",   "lift"};
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> marks;  // (stage, index of start event)
+  double ms[kNumStages] = {};
+  int64_t calls[kNumStages] = {};
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      RSVD_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  // Call after the stream has been synchronized.
+  void collect() {
+    for (auto& [st, i] : marks) {
+      float t = 0.f;
+      RSVD_CUDA(cudaEventElapsedTime(&t, pool[i], pool[i + 1]));
+      ms[st] += t;
+      calls[st] += 1;
+    }
+    marks.clear();
+    used = 0;
+  }
+  void reset() {
+    for (int i = 0; i < kNumStages; ++i) ms[i] = 0.0, calls[i] = 0;
+  }
+  void destroy() {
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+  }
+};
+
+struct Scope {
+  Prof* p;
+  cudaStream_t st;
+  size_t idx = 0;
+  Scope(Prof* prof, int stage, cudaStream_t s) : p(prof && prof->on ? prof : nullptr), st(s) {
+    if (!p) return;
+    idx = p->used;
+    RSVD_CUDA(cudaEventRecord(p->get(), st));
+    p->get();
+    p->marks.emplace_back(stage, idx);
+  }
+  ~Scope() {
+    if (p) cudaEventRecord(p->pool[idx + 1], st);
+  }
+};
+
+}  // namespace rsvd
+
+struct rsvd_context {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  rsvd::Arena arena;
+  rsvd::Prof prof;
+  int last_sweeps = 0;
+  std::vector<int> h_int;
+  std::vector<double> h_dbl;
+};
+
+namespace rsvd {
+namespace {
+
+struct Shape {
+  int64_t m, n, batch, k, ell, ellp, q;
+};
+
+struct Buffers {
+  uint64_t* seeds;
+  double *X, *X2, *Y, *Y2;
+  double *G, *T, *Rf1, *Rf2, *Rt, *H, *Jm;
+  double *Ut, *Jr, *Vb;
+  double* sig;
+  double* dw;
+  int *rank1, *rank2, *rankF, *perm, *permS, *sweeps;
+  double* partial;
+  int64_t partial_cap;
+  // staging for host-pointer calls
+  double *Ah, *Uh, *Vth, *Sh;
+  Prof* prof;
+};
+
+int64_t partial_need(const Shape& s) {
+  const int64_t b = s.batch, lp = s.ellp;
+  int64_t need = 0;
+  auto upd = [&](bool t, int64_t M, int64_t N, int64_t K) {
+    need = std::max(need, dgemm_partial_elems(t, M, N, K, b));
+  };
+  upd(false, s.m, lp, s.n);
+  upd(true, lp, lp, s.m);
+  upd(true, lp, lp, s.n);
+  upd(false, s.m, lp, lp);
+  upd(false, s.n, lp, lp);
+  upd(true, s.n, lp, s.m);
+  upd(false, lp, lp, lp);
+  upd(false, s.m, s.k, lp);
+  upd(false, s.n, s.k, lp);
+  return need;
+}
+
+Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
+  Buffers B{};
+  const int64_t b = s.batch, lp = s.ellp;
+  B.seeds = c.take<uint64_t>(b);
+  B.X = c.take<double>(b * s.n * lp);
+  B.X2 = c.take<double>(b * s.n * lp);
+  B.Y = c.take<double>(b * s.m * lp);
+  B.Y2 = c.take<double>(b * s.m * lp);
+  B.G = c.take<double>(b * lp * lp);
+  B.T = c.take<double>(b * lp * lp);
+  B.Rf1 = c.take<double>(b * lp * lp);
+  B.Rf2 = c.take<double>(b * lp * lp);
+  B.rank1 = c.take<int>(b);
+  B.rank2 = c.take<int>(b);
+  B.perm = c.take<int>(b * lp);
+  if (want_svd) {
+    B.Rt = c.take<double>(b * lp * lp);
+    B.H = c.take<double>(b * lp * lp);
+    B.Jm = c.take<double>(b * lp * lp);
+    B.Ut = c.take<double>(b * lp * s.k);
+    B.Jr = c.take<double>(b * lp * s.k);
+    B.Vb = c.take<double>(b * s.n * s.k);
+    B.sig = c.take<double>(b * s.k);
+    B.dw = c.take<double>(b);
+    B.rankF = c.take<int>(b);
+    B.permS = c.take<int>(b * lp);
+    B.sweeps = c.take<int>(b);
+  }
+  B.partial_cap = partial_need(s);
+  B.partial = c.take<double>(std::max<int64_t>(B.partial_cap, 1));
+  if (host_io) {
+    B.Ah = c.take<double>(b * s.m * s.n);
+    B.Uh = c.take<double>(b * s.m * std::max<int64_t>(s.k, s.ell));
+    if (want_svd) {
+      B.Vth = c.take<double>(b * s.k * s.n);
+      B.Sh = c.take<double>(b * s.k);
+    }
+  }
+  return B;
+}
+
+// CholeskyQR2 of Y (rows x ellp per item) in place, Tmp as scratch.  When
+// Rt is given, also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
+void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, double* Rt,
+          uint64_t tag, cudaStream_t st) {
+  const int64_t lp = s.ellp, b = s.batch;
+  const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
+  const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
+  Prof* P = B.prof;
+  for (int pass = 0; pass < 2; ++pass) {
+    const MatRef& in = pass == 0 ? Y : Tm;
+    const MatRef& out = pass == 0 ? Tm : Y;
+    double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
+    int* rk = pass == 0 ? B.rank1 : B.rank2;
+    {
+      Scope sc(P, kStGram, st);
+      dgemm(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, st);
+    }
+    {
+      Scope sc(P, kStChol, st);
+      launch_pchol(B.G, B.T, Rf, rk, B.perm, s.ell, lp, kPivotTau, b, st);
+    }
+    Scope sc(P, kStApply, st);
+    dgemm(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, st);
+    launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, st);
+  }
+  if (Rt) {
+    Scope sc(P, kStApply, st);
+    dgemm(false, lp, lp, lp, MatRef{B.Rf2, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp},
+          MatRef{Rt, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+  }
+}
+
+// randomized_range (factorize.cpp:52-74): leaves Q in B.Y (m x ellp).
+void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
+  const int64_t lp = s.ellp, b = s.batch;
+  const MatRef X{B.X, s.n, s.n * lp}, Y{B.Y, s.m, s.m * lp};
+  Prof* P = B.prof;
+  {
+    Scope sc(P, kStOmega, st);
+    launch_fill_gaussian(X, s.n, lp, s.ell, B.seeds, b, st);
+  }
+  auto nn = [&] {
+    Scope sc(P, kStApassNN, st);
+    dgemm(false, s.m, lp, s.n, A, X, Y, b, B.partial, B.partial_cap, st);
+  };
+  auto tn = [&] {
+    Scope sc(P, kStApassTN, st);
+    dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
+  };
+  nn();
+  uint64_t tag = kCompletionTag;
+  orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, st);
+  tag += 2;
+  for (int64_t t = 0; t < s.q; ++t) {
+    tn();
+    orth(s, B, B.X, B.X2, s.n, nullptr, tag, st);
+    tag += 2;
+    nn();
+    orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, st);
+    tag += 2;
+  }
+}
+
+// Projection + small SVD + lift (factorize.cpp:86-93).  Outputs go to
+// U (m x k), S (k per item, contiguous stride sS), Vt (k x n).
+void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64_t sS, MatRef Vt,
+               cudaStream_t st) {
+  const int64_t lp = s.ellp, b = s.batch, k = s.k;
+  const MatRef X{B.X, s.n, s.n * lp}, Y{B.Y, s.m, s.m * lp};
+  Prof* P = B.prof;
+  // B^T = A^T Q (n x ellp), then B^T = Qb Rt.
+  {
+    Scope sc(P, kStApassTN, st);
+    dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
+  }
+  orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, st);
+  {
+    Scope sc(P, kStJacobi, st);
+    launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
+    launch_jacobi(B.H, B.Jm, s.ell, lp, kMaxSweeps, B.sweeps, b, st);
+  }
+  Scope sc(P, kStLift, st);
+  launch_finalize_spectrum(B.H, lp, s.ell, k, s.m, s.n, B.sig, B.permS, B.rankF, B.dw, b, st);
+  // U~ = W Sigma^{-1} restricted to the kept columns, then U = Q U~.
+  launch_gather_scale_columns(B.H, lp, lp * lp, B.permS, lp, B.sig, k, B.rankF, lp, k, B.Ut, lp,
+                              lp * k, b, st);
+  dgemm(false, s.m, k, lp, Y, MatRef{B.Ut, lp, lp * k}, U, b, B.partial, B.partial_cap, st);
+  // V = Qb J[:, perm[:r]], Vt = V^T.
+  launch_gather_scale_columns(B.Jm, lp, lp * lp, B.permS, lp, nullptr, k, B.rankF, lp, k, B.Jr,
+                              lp, lp * k, b, st);
+  dgemm(false, s.n, k, lp, X, MatRef{B.Jr, lp, lp * k}, MatRef{B.Vb, s.n, s.n * k}, b, B.partial,
+        B.partial_cap, st);
+  launch_transpose(MatRef{B.Vb, s.n, s.n * k}, s.n, k, Vt, b, st);
+  launch_copy_matrix(MatRef{B.sig, k, k}, k, 1, MatRef{S, k, sS}, b, st);
+}
+
+// ------------------------------------------------------------ validation
+// Same checks, order and messages as the reference.
+void validate_rsvd(int64_t m, int64_t n, int64_t rank, int64_t oversample, int power,
+                   int64_t& ell) {
+  if (m <= 0 || n <= 0) throw InvalidArgument("rsvd: empty matrix");              // :79
+  if (rank < 1) throw InvalidArgument("rsvd: rank must be >= 1");                 // :80
+  ell = oversample;
+  if (ell == 0) ell = std::min(2 * rank, std::min(m, n));                         // :82
+  if (ell < rank) throw InvalidArgument("rsvd: oversample must be >= rank");      // :83
+  if (ell < 1 || ell > std::min(m, n))                                            // :57-58
+    throw InvalidArgument("randomized_range: need 1 <= ell <= min(m, n)");
+  if (power < 0) throw InvalidArgument("randomized_range: power must be >= 0");   // :59
+}
+
+void validate_range(int64_t m, int64_t n, int64_t ell, int power) {
+  if (m <= 0 || n <= 0) throw InvalidArgument("randomized_range: empty matrix");
+  if (ell < 1 || ell > std::min(m, n))
+    throw InvalidArgument("randomized_range: need 1 <= ell <= min(m, n)");
+  if (power < 0) throw InvalidArgument("randomized_range: power must be >= 0");
+}
+
+void check_flags(int flags) {
+  if (flags != RSVD_PTR_HOST && flags != RSVD_PTR_DEVICE)
+    throw InvalidArgument("rsvd: flags must be RSVD_PTR_HOST or RSVD_PTR_DEVICE");
+}
+
+void copy_2d(void* dst, int64_t dpitch_elems, const void* src, int64_t spitch_elems, int64_t rows,
+             int64_t cols, cudaMemcpyKind kind, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  RSVD_CUDA(cudaMemcpy2DAsync(dst, dpitch_elems * sizeof(double), src,
+                              spitch_elems * sizeof(double), rows * sizeof(double), cols, kind,
+                              st));
+}
+
+// Core batched rsvd on device or host pointers.
+void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n,
+                       int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
+                       const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
+                       int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
+                       int64_t* out_rank, double* dw, int flags) {
+  check_flags(flags);
+  int64_t ell = 0;
+  validate_rsvd(m, n, rank, oversample, power, ell);
+  if (batch < 0) throw InvalidArgument("rsvd: batch must be >= 0");
+  if (batch == 0) return;
+  if (!A || !U || !S || !Vt || !seeds || !out_rank || !dw)
+    throw InvalidArgument("rsvd: null pointer argument");
+  if (lda < m || ldu < m || ldvt < rank) throw InvalidArgument("rsvd: leading dimension too small");
+  const bool host = flags == RSVD_PTR_HOST;
+  RSVD_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+
+  Shape s{m, n, batch, rank, ell, round_up(ell, 8), power};
+  Carver meas{nullptr};
+  carve(meas, s, host, true);
+  h->arena.reserve(meas.off + 256);
+  Carver cv{h->arena.base};
+  Buffers B = carve(cv, s, host, true);
+
+  RSVD_CUDA(cudaMemcpyAsync(B.seeds, seeds, sizeof(uint64_t) * batch, cudaMemcpyHostToDevice, st));
+  CMatRef Ad{A, lda, strideA};
+  MatRef Ud{U, ldu, strideU}, Vtd{Vt, ldvt, strideVt};
+  double* Sd = S;
+  int64_t sS = strideS;
+  if (host) {
+    for (int64_t b = 0; b < batch; ++b)
+      copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, st);
+    Ad = CMatRef{B.Ah, m, m * n};
+    Ud = MatRef{B.Uh, m, m * rank};
+    Vtd = MatRef{B.Vth, rank, rank * n};
+    Sd = B.Sh;
+    sS = rank;
+  }
+  B.prof = &h->prof;
+  range_finder(s, B, Ad, st);
+  svd_stage(s, B, Ad, Ud, Sd, sS, Vtd, st);
+
+  h->h_int.resize(2 * batch);
+  h->h_dbl.resize(batch);
+  RSVD_CUDA(cudaMemcpyAsync(h->h_int.data(), B.rankF, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  RSVD_CUDA(cudaMemcpyAsync(h->h_int.data() + batch, B.sweeps, sizeof(int) * batch,
+                            cudaMemcpyDeviceToHost, st));
+  RSVD_CUDA(cudaMemcpyAsync(h->h_dbl.data(), B.dw, sizeof(double) * batch, cudaMemcpyDeviceToHost, st));
+  if (host) {
+    for (int64_t b = 0; b < batch; ++b) {
+      copy_2d(U + b * strideU, ldu, B.Uh + b * m * rank, m, m, rank, cudaMemcpyDeviceToHost, st);
+      copy_2d(Vt + b * strideVt, ldvt, B.Vth + b * rank * n, rank, rank, n, cudaMemcpyDeviceToHost,
+              st);
+      RSVD_CUDA(cudaMemcpyAsync(S + b * strideS, B.Sh + b * rank, sizeof(double) * rank,
+                                cudaMemcpyDeviceToHost, st));
+    }
+  }
+  RSVD_CUDA(cudaStreamSynchronize(st));
+  if (h->prof.on) h->prof.collect();
+  h->last_sweeps = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    out_rank[b] = h->h_int[b];
+    dw[b] = h->h_dbl[b];
+    h->last_sweeps = std::max(h->last_sweeps, h->h_int[batch + b]);
+  }
+}
+
+void range_impl(rsvd_context* h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t ell,
+                int power, uint64_t seed, double* Q, int64_t ldq, int flags) {
+  check_flags(flags);
+  validate_range(m, n, ell, power);
+  if (!A || !Q) throw InvalidArgument("randomized_range: null pointer argument");
+  if (lda < m || ldq < m) throw InvalidArgument("randomized_range: leading dimension too small");
+  const bool host = flags == RSVD_PTR_HOST;
+  RSVD_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  Shape s{m, n, 1, ell, ell, round_up(ell, 8), power};
+  Carver meas{nullptr};
+  carve(meas, s, host, false);
+  h->arena.reserve(meas.off + 256);
+  Carver cv{h->arena.base};
+  Buffers B = carve(cv, s, host, false);
+  RSVD_CUDA(cudaMemcpyAsync(B.seeds, &seed, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CMatRef Ad{A, lda, 0};
+  if (host) {
+    copy_2d(B.Ah, m, A, lda, m, n, cudaMemcpyHostToDevice, st);
+    Ad = CMatRef{B.Ah, m, m * n};
+  }
+  B.prof = &h->prof;
+  range_finder(s, B, Ad, st);
+  copy_2d(Q, ldq, B.Y, m, m, ell, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st);
+  RSVD_CUDA(cudaStreamSynchronize(st));
+  if (h->prof.on) h->prof.collect();
+}
+
+void recon_impl(rsvd_context* h, const double* A, int64_t m, int64_t n, int64_t lda,
+                const double* U, int64_t ldu, const double* S, const double* Vt, int64_t ldvt,
+                int64_t r, double* out, int flags) {
+  check_flags(flags);
+  if (m <= 0 || n <= 0) throw InvalidArgument("reconstruction_error: empty matrix");
+  if (r < 0) throw InvalidArgument("reconstruction_error: rank must be >= 0");
+  if (!A || !out || (r > 0 && (!U || !S || !Vt)))
+    throw InvalidArgument("reconstruction_error: null pointer argument");
+  const bool host = flags == RSVD_PTR_HOST;
+  RSVD_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const int64_t rr = std::max<int64_t>(r, 1);
+  const int64_t nparts = 4 * kNumSMs;
+  Carver meas{nullptr};
+  auto layout = [&](Carver& c, double*& Ad, double*& Us, double*& Vd, double*& Sd, double*& R,
+                    double*& part, double*& pg) {
+    Ad = c.take<double>(m * n);
+    Us = c.take<double>(m * rr);
+    Vd = c.take<double>(rr * n);
+    Sd = c.take<double>(rr);
+    R = c.take<double>(m * n);
+    part = c.take<double>(nparts);
+    pg = c.take<double>(std::max<int64_t>(dgemm_partial_elems(false, m, n, rr, 1), 1));
+  };
+  double *Ad, *Us, *Vd, *Sd, *R, *part, *pg;
+  layout(meas, Ad, Us, Vd, Sd, R, part, pg);
+  h->arena.reserve(meas.off + 256);
+  Carver cv{h->arena.base};
+  layout(cv, Ad, Us, Vd, Sd, R, part, pg);
+  const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  copy_2d(Ad, m, A, lda, m, n, kin, st);
+  if (r > 0) {
+    copy_2d(Us, m, U, ldu, m, r, kin, st);
+    copy_2d(Vd, r, Vt, ldvt, r, n, kin, st);
+    RSVD_CUDA(cudaMemcpyAsync(Sd, S, sizeof(double) * r, kin, st));
+    launch_scale_columns(MatRef{Us, m, 0}, m, r, Sd, st);  // U diag(S)
+    dgemm(false, m, n, r, CMatRef{Us, m, 0}, CMatRef{Vd, r, 0}, MatRef{R, m, 0}, 1, pg,
+          dgemm_partial_elems(false, m, n, rr, 1), st);
+  } else {
+    RSVD_CUDA(cudaMemsetAsync(R, 0, sizeof(double) * m * n, st));
+  }
+  launch_residual_sumsq(CMatRef{Ad, m, 0}, CMatRef{R, m, 0}, m, n, part, nparts, st);
+  std::vector<double> hp(nparts);
+  RSVD_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * nparts, cudaMemcpyDeviceToHost, st));
+  RSVD_CUDA(cudaStreamSynchronize(st));
+  double sum = 0.0;
+  for (double v : hp) sum += v;
+  *out = std::sqrt(sum);
+}
+
+template <class F>
+int guarded(rsvd_context* h, F&& f) {
+  if (!h) return RSVD_ERR_INVALID;
+  try {
+    f();
+    h->err.clear();
+    return RSVD_OK;
+  } catch (const InvalidArgument& e) {
+    h->err = e.what();
+    return RSVD_ERR_INVALID;
+  } catch (const NumericalError& e) {
+    h->err = e.what();
+    return RSVD_ERR_NUMERICAL;
+  } catch (const CudaError& e) {
+    h->err = e.what();
+    return RSVD_ERR_CUDA;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return RSVD_ERR_CUDA;
+  }
+}
+
+uint64_t mix64_host(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+}  // namespace rsvd
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* rsvd_version(void) { return "rsvd_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+uint64_t rsvd_mix64(uint64_t z) { return rsvd::mix64_host(z); }
+uint64_t rsvd_derive_seed(uint64_t seed, uint64_t tag) { return seed ^ rsvd::mix64_host(tag); }
+
+int rsvd_create(rsvd_handle* out, int device) {
+  if (!out) return RSVD_ERR_INVALID;
+  *out = nullptr;
+  auto* h = new rsvd_context();
+  h->device = device;
+  const int rc = rsvd::guarded(h, [&] {
+    int count = 0;
+    RSVD_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw rsvd::InvalidArgument("rsvd_create: bad device index");
+    RSVD_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    RSVD_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw rsvd::CudaError("rsvd_create: this build targets sm_100a (B200); device is sm_" +
+                            std::to_string(prop.major * 10 + prop.minor));
+    RSVD_CUDA(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking));
+    h->stream = h->own;
+  });
+  if (rc != RSVD_OK) {
+    // Keep the handle so the caller can read the message, then destroy it.
+    *out = h;
+    return rc;
+  }
+  *out = h;
+  return RSVD_OK;
+}
+
+uint64_t rsvd_kernel_launches(void) { return rsvd::g_kernel_launches.load(); }
+
+int rsvd_profile_enable(rsvd_handle h, int on) {
+  return rsvd::guarded(h, [&] {
+    h->prof.on = on != 0;
+    h->prof.reset();
+  });
+}
+
+int rsvd_profile_read(rsvd_handle h, double* ms, int64_t* calls, int n) {
+  if (!h) return -1;
+  const int k = std::min<int>(n, rsvd::kNumStages);
+  for (int i = 0; i < k; ++i) {
+    if (ms) ms[i] = h->prof.ms[i];
+    if (calls) calls[i] = h->prof.calls[i];
+  }
+  return rsvd::kNumStages;
+}
+
+const char* rsvd_profile_stage_name(int i) {
+  return (i >= 0 && i < rsvd::kNumStages) ? rsvd::kStageNames[i] : "";
+}
+
+int rsvd_last_jacobi_sweeps(rsvd_handle h) { return h ? h->last_sweeps : -1; }
+
+int rsvd_destroy(rsvd_handle h) {
+  if (!h) return RSVD_ERR_INVALID;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->prof.destroy();
+  h->arena.release();
+  if (h->own) cudaStreamDestroy(h->own);
+  delete h;
+  return RSVD_OK;
+}
+
+const char* rsvd_last_error(rsvd_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+int rsvd_set_stream(rsvd_handle h, void* stream) {
+  return rsvd::guarded(h, [&] {
+    h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own;
+  });
+}
+
+int rsvd_trim(rsvd_handle h) {
+  return rsvd::guarded(h, [&] {
+    RSVD_CUDA(cudaStreamSynchronize(h->stream));
+    h->arena.release();
+  });
+}
+
+int rsvd_fill_gaussian_f64(rsvd_handle h, uint64_t seed, double* out, int64_t count, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::check_flags(flags);
+    if (count < 0) throw rsvd::InvalidArgument("fill_gaussian: count must be >= 0");
+    if (count == 0) return;
+    if (!out) throw rsvd::InvalidArgument("fill_gaussian: null pointer argument");
+    RSVD_CUDA(cudaSetDevice(h->device));
+    double* dst = out;
+    if (flags == RSVD_PTR_HOST) {
+      h->arena.reserve(sizeof(double) * count + 256);
+      dst = reinterpret_cast<double*>(h->arena.base);
+    }
+    rsvd::launch_fill_gaussian_flat(dst, count, seed, h->stream);
+    if (flags == RSVD_PTR_HOST)
+      RSVD_CUDA(cudaMemcpyAsync(out, dst, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                                h->stream));
+    RSVD_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int rsvd_f64(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t rank,
+             int64_t oversample, int power, uint64_t seed, double* U, int64_t ldu, double* S,
+             double* Vt, int64_t ldvt, int64_t* out_rank, double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::rsvd_batched_impl(h, 1, A, m, n, lda, 0, rank, oversample, power, &seed, U, ldu, 0, S,
+                            0, Vt, ldvt, 0, out_rank, discarded_weight, flags);
+  });
+}
+
+int rsvd_f64_batched(rsvd_handle h, int64_t batch, const double* A, int64_t m, int64_t n,
+                     int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
+                     const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
+                     int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
+                     int64_t* out_rank, double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::rsvd_batched_impl(h, batch, A, m, n, lda, strideA, rank, oversample, power, seeds, U,
+                            ldu, strideU, S, strideS, Vt, ldvt, strideVt, out_rank,
+                            discarded_weight, flags);
+  });
+}
+
+int rsvd_randomized_range_f64(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                              int64_t ell, int power, uint64_t seed, double* Q, int64_t ldq,
+                              int flags) {
+  return rsvd::guarded(h, [&] { rsvd::range_impl(h, A, m, n, lda, ell, power, seed, Q, ldq, flags); });
+}
+
+int rsvd_validate_params(int64_t m, int64_t n, int64_t rank, int64_t oversample, int power,
+                         int64_t* ell_out, char* msg, int64_t msg_len) {
+  try {
+    int64_t ell = 0;
+    rsvd::validate_rsvd(m, n, rank, oversample, power, ell);
+    if (ell_out) *ell_out = ell;
+    if (msg && msg_len > 0) msg[0] = 0;
+    return RSVD_OK;
+  } catch (const std::exception& e) {
+    if (msg && msg_len > 0) {
+      std::strncpy(msg, e.what(), static_cast<size_t>(msg_len - 1));
+      msg[msg_len - 1] = 0;
+    }
+    return RSVD_ERR_INVALID;
+  }
+}
+
+int rsvd_testing_dgemm(rsvd_handle h, int trans_a, int64_t M, int64_t N, int64_t K,
+                       const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                       int64_t strideB, double* C, int64_t ldc, int64_t strideC, int64_t batch) {
+  return rsvd::guarded(h, [&] {
+    RSVD_CUDA(cudaSetDevice(h->device));
+    const int64_t need = rsvd::dgemm_partial_elems(trans_a != 0, M, N, K, batch);
+    h->arena.reserve(sizeof(double) * std::max<int64_t>(need, 1) + 256);
+    rsvd::dgemm(trans_a != 0, M, N, K, rsvd::CMatRef{A, lda, strideA},
+                rsvd::CMatRef{B, ldb, strideB}, rsvd::MatRef{C, ldc, strideC}, batch,
+                reinterpret_cast<double*>(h->arena.base), need, h->stream);
+    RSVD_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int rsvd_reconstruction_error_f64(rsvd_handle h, const double* A, int64_t m, int64_t n,
+                                  int64_t lda, const double* U, int64_t ldu, const double* S,
+                                  const double* Vt, int64_t ldvt, int64_t r, double* out,
+                                  int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::recon_impl(h, A, m, n, lda, U, ldu, S, Vt, ldvt, r, out, flags);
+  });
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,200 @@
+"""GPU parity of the RSVD path against the CPU oracle (restated reference).
+
+Tolerances (BASELINE.json north_star): singular values 1e-10 relative,
+reconstruction error 1e-10 relative, subspace distance <= 1e-8 for gapped
+spectra; factor isometry 1e-12 (test_factorize.cpp:73-83)."""
+import numpy as np
+import pytest
+
+from tests.helpers import (isometry_err, matrix_with_spectrum, rel_sigma_err, spectrum_family,
+                           subspace_distance)
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-10
+REC_TOL = 1e-10
+SUB_TOL = 1e-8
+ISO_TOL = 1e-12
+
+
+def _gapped_prefix(S, k, rel_gap=1e-3):
+    """Largest j <= k such that sigma_{j-1} - sigma_j is a relative gap: the
+    leading j-dimensional subspace is well defined."""
+    for j in range(min(k, len(S) - 1), 0, -1):
+        if (S[j - 1] - S[j]) > rel_gap * S[0]:
+            return j
+    return 0
+
+
+def check_against(a, f, ref, label=""):
+    from paper_1710_01463_b200 import reconstruction_error
+
+    U, S, Vt, dw = ref
+    assert f.rank() == len(S), (label, f.rank(), len(S))
+    assert rel_sigma_err(f.sigma, S) < SIG_TOL, label
+    left = np.asarray(f.left)
+    right = np.asarray(f.right_adj)
+    assert isometry_err(left) < ISO_TOL, label
+    assert isometry_err(right.T) < ISO_TOL, label
+    e_gpu = reconstruction_error(a, f)
+    e_ref = float(np.linalg.norm(a - (U * S[None, :]) @ Vt))
+    if e_ref > 1e-12 * np.linalg.norm(a):
+        assert abs(e_gpu - e_ref) / e_ref < REC_TOL, (label, e_gpu, e_ref)
+    else:
+        assert e_gpu <= 1e-10 * np.linalg.norm(a), label
+    j = _gapped_prefix(S, f.rank())
+    if j:
+        assert subspace_distance(left[:, :j], U[:, :j]) < SUB_TOL, label
+        assert subspace_distance(right[:j].T, Vt[:j].T) < SUB_TOL, label
+    if len(S) < f.rank() or True:
+        assert f.discarded_weight == pytest.approx(dw, rel=1e-9, abs=1e-28), label
+
+
+def test_golden_small_cases(cuda, golden_small):
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    names = sorted({k.split("/")[0] for k in golden_small.files})
+    for name in names:
+        a = golden_small[f"{name}/a"]
+        k, ell, q, seed = (int(x) for x in golden_small[f"{name}/params"])
+        f = rsvd(a, RsvdParams(k, ell, q, seed))
+        ref = (golden_small[f"{name}/U"], golden_small[f"{name}/S"], golden_small[f"{name}/Vt"],
+               float(golden_small[f"{name}/dw"][0]))
+        check_against(a, f, ref, name)
+
+
+def test_device_pointers_match_host_pointers(cuda, golden_small):
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = golden_small["exp_200x160/a"]
+    k, ell, q, seed = (int(x) for x in golden_small["exp_200x160/params"])
+    fh = rsvd(a, RsvdParams(k, ell, q, seed))
+    ad = torch.from_numpy(np.asfortranarray(a)).to(cuda)
+    ad = ad.t().contiguous().t()
+    fd = rsvd(ad, RsvdParams(k, ell, q, seed))
+    assert np.array_equal(fh.sigma, fd.sigma.cpu().numpy())
+    assert np.array_equal(fh.left, fd.left.cpu().numpy())
+    assert np.array_equal(fh.right_adj, fd.right_adj.cpu().numpy())
+
+
+def test_rsvd_matches_tsvd_fast_decay(cuda, oracle_mod):  # test_factorize.cpp:85-103
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
+
+    sigma = spectrum_family(0, 30)
+    a = matrix_with_spectrum(oracle_mod, 3, 50, 30, sigma)
+    Ut, St, Vtt, dwt = oracle_mod.tsvd(a, 10)
+    f = rsvd(a, RsvdParams(10, 20, 4, 123))
+    assert f.rank() == 10 and not f.discarded_exact
+    assert rel_sigma_err(f.sigma, St) < 1e-10
+    et = float(np.linalg.norm(a - (Ut * St) @ Vtt))
+    assert reconstruction_error(a, f) / et <= 1.01
+    assert 0.0 < f.discarded_weight <= dwt * (1 + 1e-8)
+
+
+@pytest.mark.parametrize("r", [3, 7])
+def test_exact_rank_reconstructs(cuda, oracle_mod, r):  # test_factorize.cpp:105-120
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
+
+    sigma = [5.0 / (1.0 + k) for k in range(r)]
+    a = matrix_with_spectrum(oracle_mod, 17 + r, 60, 40, sigma)
+    f = rsvd(a, RsvdParams(10, 20, 4, 5))
+    assert reconstruction_error(a, f) <= 1e-10 * np.linalg.norm(a)
+    assert f.rank() <= 10
+    ref = oracle_mod.rsvd(a, 10, 20, 4, 5)
+    assert f.rank() == len(ref[1])
+    assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
+
+
+def test_zero_matrix(cuda):  # test_factorize.cpp:199-207
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
+
+    a = np.zeros((10, 6))
+    f = rsvd(a, RsvdParams(3, 6, 2, 1))
+    assert f.rank() == 0
+    assert reconstruction_error(a, f) == 0.0
+
+
+def test_deterministic_in_seed(cuda, oracle_mod):  # test_factorize.cpp:135-146
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = oracle_mod.gaussian_matrix(101, 48, 32)
+    f1 = rsvd(a, RsvdParams(6, 12, 4, 77))
+    f2 = rsvd(a, RsvdParams(6, 12, 4, 77))
+    assert np.array_equal(f1.sigma, f2.sigma)
+    assert np.array_equal(f1.left, f2.left)
+    assert np.array_equal(f1.right_adj, f2.right_adj)
+    f3 = rsvd(a, RsvdParams(6, 12, 4, 78))
+    assert np.max(np.abs(f1.left - f3.left)) > 1e-12
+
+
+def test_randomized_range_exact_rank(cuda, oracle_mod):  # test_factorize.cpp:163-173
+    from paper_1710_01463_b200 import randomized_range
+
+    a = matrix_with_spectrum(oracle_mod, 4, 30, 20, [4.0, 2.0, 1.0, 0.5, 0.25])
+    q = randomized_range(a, 8, 2, 31)
+    assert q.shape == (30, 8)
+    assert isometry_err(q) < 1e-12
+    assert np.linalg.norm(a - q @ (q.T @ a)) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_invalid_arguments(cuda):  # test_factorize.cpp:175-184
+    from paper_1710_01463_b200 import InvalidArgument, RsvdParams, randomized_range, rsvd
+
+    a = np.eye(4)
+    with pytest.raises(InvalidArgument, match="rank must be >= 1"):
+        rsvd(a, RsvdParams(0, 0, 4, 1))
+    with pytest.raises(InvalidArgument, match="oversample must be >= rank"):
+        rsvd(a, RsvdParams(3, 2, 4, 1))
+    with pytest.raises(InvalidArgument, match="need 1 <= ell"):
+        randomized_range(a, 0, 1, 1)
+    with pytest.raises(InvalidArgument, match="need 1 <= ell"):
+        randomized_range(a, 5, 1, 1)
+    with pytest.raises(InvalidArgument, match="power must be >= 0"):
+        randomized_range(a, 2, -1, 1)
+    with pytest.raises(InvalidArgument, match="empty matrix"):
+        rsvd(np.zeros((0, 3)), RsvdParams(1, 0, 1, 1))
+
+
+def test_power_iterations_monotone(cuda, oracle_mod):  # test_factorize.cpp:209-226
+    from paper_1710_01463_b200 import randomized_range
+
+    sigma = 1.0 / np.arange(1, 25)
+    mean = np.zeros(4)
+    for trial in range(10):
+        a = matrix_with_spectrum(oracle_mod, 1000 + trial, 40, 24, sigma)
+        for i, q in enumerate([0, 1, 2, 4]):
+            Q = randomized_range(a, 8, q, 7000 + trial)
+            mean[i] += np.linalg.norm(a - Q @ (Q.T @ a)) / 10
+    assert np.all(mean[1:] <= mean[:-1] * (1 + 1e-12))
+
+
+def test_same_omega_as_oracle(cuda, oracle_mod):
+    """Feeding the oracle the reference Omega vs its own gives the same
+    answer to within the Omega ulp noise: parity is not an artefact of Omega."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = matrix_with_spectrum(oracle_mod, 77, 300, 250, np.exp(-np.arange(250) / 20.0))
+    f = rsvd(a, RsvdParams(40, 50, 2, 4242))
+    ref = oracle_mod.rsvd(a, 40, 50, 2, 4242)
+    check_against(a, f, ref, "omega")
+
+
+def test_batched_matches_single(cuda, oracle_mod):
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, rsvd, rsvd_batched
+
+    m, n, bsz = 120, 90, 5
+    mats = [matrix_with_spectrum(oracle_mod, 500 + b, m, n, 0.9 ** np.arange(90)) for b in
+            range(bsz)]
+    seeds = [1000 + b for b in range(bsz)]
+    A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
+    bf = rsvd_batched(A, RsvdParams(20, 30, 2, 0), seeds)
+    for b in range(bsz):
+        ref = oracle_mod.rsvd(mats[b], 20, 30, 2, seeds[b])
+        fb = bf.item(b)
+        fb.left, fb.sigma, fb.right_adj = (x.cpu().numpy() for x in (fb.left, fb.sigma,
+                                                                    fb.right_adj))
+        check_against(mats[b], fb, ref, f"batch{b}")
+        single = rsvd(mats[b], RsvdParams(20, 30, 2, seeds[b]))
+        assert rel_sigma_err(single.sigma, fb.sigma) < 1e-13
