@@ -50,7 +50,8 @@ int rsvd_create(rsvd_handle* handle, int device);
 int rsvd_destroy(rsvd_handle handle);
 const char* rsvd_last_error(rsvd_handle handle);
 /* Use a caller-owned cudaStream_t (e.g. torch's current stream); NULL = the
- * handle's own stream. */
+ * handle's own (non-blocking) stream.  Pass cudaStreamLegacy ((void*)1) for
+ * the legacy default stream, which torch reports as stream 0. */
 int rsvd_set_stream(rsvd_handle handle, void* cuda_stream);
 /* Release the cached workspace. */
 int rsvd_trim(rsvd_handle handle);

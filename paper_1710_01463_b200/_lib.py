@@ -180,6 +180,34 @@ def validate_params(m: int, n: int, rank: int, oversample: int, power: int) -> i
     return ell.value
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream
+
+
+def torch_stream_ptr() -> int:
+    """torch's current stream as a cudaStream_t for rsvd_set_stream.  torch
+    reports its default stream as 0; NULL means "the handle's own stream" to
+    the engine, so the legacy default stream is passed explicitly."""
+    import torch
+
+    s = torch.cuda.current_stream().cuda_stream
+    return s if s else CUDA_STREAM_LEGACY
+
+
+class on_torch_stream:
+    """Context manager: run engine calls of `handle` on torch's current stream."""
+
+    def __init__(self, handle: "Handle"):
+        self.h = handle
+
+    def __enter__(self):
+        load().rsvd_set_stream(self.h.raw, ctypes.c_void_p(torch_stream_ptr()))
+        return self.h
+
+    def __exit__(self, *exc):
+        load().rsvd_set_stream(self.h.raw, None)
+        return False
+
+
 def kernel_launches() -> int:
     return int(load().rsvd_kernel_launches())
 

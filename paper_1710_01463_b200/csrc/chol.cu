@@ -2,11 +2,11 @@
 // step of CholeskyQR that replaces Householder geqrf+orgqr
 // (lapack.cpp:146-201, orthonormal_columns lapack.cpp:211-215).
 //
-// For each batch item (one CTA of 1024 threads):
+// For each batch item (one CTA):
 //   P^T G P ~= R^T R with R (r x l) upper trapezoidal in pivoted order,
 //   stopping at the first pivot <= tau * max(diag G): the numerical rank r of
-//   Y (LAPACK dpstf2 semantics).  Outputs
-//     T     (l x l): Q1 = Y * T has the r orthonormal-ish leading columns
+//   Y (LAPACK dpstrf semantics).  Outputs
+//     T     (l x l): Q1 = Y * T has the r leading columns
 //                    (T = P[:, :r] R11^{-1}); columns >= r are zero and get
 //                    filled by the basis completion (aux.cu), which is how
 //                    the reference's "always l orthonormal columns, arbitrary
@@ -14,188 +14,355 @@
 //                    (lapack.hpp:18-20) is honoured without Householder;
 //     Rfull (l x l): [R11 R12; 0] P^T, so that Y ~= Q1 * Rfull;
 //     rank, perm.
-// The matrix lives in shared memory when it fits (l <= 156), otherwise it is
-// factored in place in global memory (L2-resident for l <= ~600).
-#include <algorithm>
+//
+// Algorithm (blocked, swap-free, dpstrf-like):
+//   * panels of PB = 32 pivots; inside a panel the pivot search runs on the
+//     lazily updated diagonal d - work (one warp), pivots are swapped
+//     *logically* through a position -> storage map, and row j of R is formed
+//     from the panel-start Schur column minus the in-panel rank-jj correction
+//     (shared-memory panel buffer);
+//   * at the end of a panel the trailing Schur complement is rebuilt in a
+//     second buffer in the new pivot order with a rank-32 DMMA update
+//     (mma.sync m16n8k4 f64), so no row/column swap ever touches global memory;
+//   * R rows are written in original column order, which is Rfull directly;
+//   * R11^{-1} by a blocked DMMA inverse (blocked_upper_inverse below).
+#include <cfloat>
 
 #include "common.cuh"
 
 namespace rsvd {
 namespace {
 
-constexpr int kCholThreads = 1024;
+constexpr int kCholThreads = 512;
 constexpr int kCholWarps = kCholThreads / 32;
+constexpr int PB = 32;  // panel width (pivots per panel)
 
-// Block-wide argmax of d[i] over i in [lo, hi) with ties to the smallest i.
-__device__ void block_argmax(const double* W, int ld, int lo, int hi, double* s_val, int* s_idx,
-                             double& best_val, int& best_idx) {
-  double v = -1.0;
-  int ix = 0x7fffffff;
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const double d = W[i + static_cast<int64_t>(i) * ld];
-    if (d > v || (d == v && i < ix)) v = d, ix = i;
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, ix, off);
-    if (ov > v || (ov == v && oi < ix)) v = ov, ix = oi;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s_val[warp] = v, s_idx[warp] = ix;
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < kCholWarps ? s_val[lane] : -1.0;
-    ix = lane < kCholWarps ? s_idx[lane] : 0x7fffffff;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, ix, off);
-      if (ov > v || (ov == v && oi < ix)) v = ov, ix = oi;
-    }
-    if (lane == 0) s_val[32] = v, s_idx[32] = ix;
-  }
-  __syncthreads();
-  best_val = s_val[32];
-  best_idx = s_idx[32];
-  __syncthreads();
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <bool IN_SMEM>
+constexpr int kInvWarps = 8;      // warps active in the blocked inverse
+constexpr int kInvPitch = 36;     // 32 x 36 per-warp tile: 4 mod 16 words, conflict free
+constexpr int kInvSmem = kInvWarps * 32 * kInvPitch;  // doubles of shared scratch needed
+
+// X = R^{-1} for an upper-triangular R of order nbk*32 (column-major, ld),
+// by the whole CTA.  Stage A: each diagonal block inverted by one warp, lane
+// c owning column c (fully unrolled backward substitution, R_II broadcast
+// from shared memory).  Stage B: block diagonals d = 1..nbk-1 in order;
+// X_IJ = -X_II (sum_{K=I+1..J} R_IK X_KJ), one warp per block, both
+// products on DMMA (mma.sync m16n8k4 f64).
+__device__ void blocked_upper_inverse(const double* __restrict__ R, double* __restrict__ X, int ld,
+                                      int nbk, double* smem, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double* S = smem + warp * 32 * kInvPitch;
+  if (warp < kInvWarps) {
+    for (int I = warp; I < nbk; I += kInvWarps) {
+      const int o = I * 32;
+      for (int e = lane; e < 1024; e += 32) {
+        const int c = e >> 5, i = e & 31;
+        S[i * kInvPitch + c] = R[(o + i) + static_cast<int64_t>(o + c) * ld];
+      }
+      __syncwarp();
+      const int c = lane;
+      double x[32];
+#pragma unroll
+      for (int i = 31; i >= 0; --i) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = i + 1; k < 32; ++k) s = fma(S[i * kInvPitch + k], x[k], s);
+        const double rii = S[i * kInvPitch + i];
+        x[i] = (i == c) ? 1.0 / rii : ((i < c) ? -s / rii : 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) X[(o + i) + static_cast<int64_t>(o + c) * ld] = x[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int dg = 1; dg < nbk; ++dg) {
+    if (warp < kInvWarps) {
+      for (int I = warp; I + dg < nbk; I += kInvWarps) {
+        const int J = I + dg;
+        const int oI = I * 32, oJ = J * 32;
+        double acc[2][4][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[a][n][q] = 0.0;
+        for (int k0 = oI + 32; k0 < oJ + 32; k0 += 4) {
+          const double* rc = R + static_cast<int64_t>(k0 + t) * ld + oI + g;
+          const double a00 = rc[0], a01 = rc[8], a10 = rc[16], a11 = rc[24];
+          double bf[4];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) bf[n] = X[(k0 + t) + static_cast<int64_t>(oJ + n * 8 + g) * ld];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            dmma_16x8x4(acc[0][n], a00, a01, bf[n]);
+            dmma_16x8x4(acc[1][n], a10, a11, bf[n]);
+          }
+        }
+        // S (row k, col c) = acc
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int i = a * 16 + g + ((q & 2) ? 8 : 0), c = n * 8 + 2 * t + (q & 1);
+              S[i * kInvPitch + c] = acc[a][n][q];
+              acc[a][n][q] = 0.0;
+            }
+        __syncwarp();
+        // X_IJ = -X_II * S
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          const double* xc = X + static_cast<int64_t>(oI + k0 + t) * ld + oI + g;
+          const double a00 = xc[0], a01 = xc[8], a10 = xc[16], a11 = xc[24];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            const double b0 = S[(k0 + t) * kInvPitch + n * 8 + g];
+            dmma_16x8x4(acc[0][n], a00, a01, b0);
+            dmma_16x8x4(acc[1][n], a10, a11, b0);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int i = a * 16 + g + ((q & 2) ? 8 : 0), c = n * 8 + 2 * t + (q & 1);
+              X[(oI + i) + static_cast<int64_t>(oJ + c) * ld] = -acc[a][n][q];
+            }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kCholThreads)
     pchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
-                 int* __restrict__ rank_out, int* __restrict__ perm_out, int ell, int ellp,
-                 double tau) {
+                 double* __restrict__ scratch, int* __restrict__ rank_out,
+                 int* __restrict__ perm_out, int ell, int ellp, double tau) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double s_val[33];
-  __shared__ int s_idx[33];
+  __shared__ double s_piv;
+  __shared__ int s_stop;
   const int64_t b = blockIdx.x;
   const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  double* Gb = G + b * sq;
-  double* W = IN_SMEM ? sm : Gb;
-  double* colbuf = IN_SMEM ? sm + sq : sm;  // kCholWarps x ellp scratch for the inverse
-  double* rrow = colbuf + static_cast<int64_t>(kCholWarps) * ellp;  // current row of R
-  int* perm = reinterpret_cast<int*>(rrow + ellp);
-  const int tid = threadIdx.x;
   const int ld = ellp;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  if (IN_SMEM)
-    for (int64_t e = tid; e < sq; e += blockDim.x) W[e] = Gb[e];
-  for (int i = tid; i < ellp; i += blockDim.x) perm[i] = i;
+  // Shared layout.  The panel pitch is 4 or 12 mod 16 words (ellp is a
+  // multiple of 8), which makes the DMMA fragment loads conflict free, and
+  // >= ellp + 16 so 16-wide tiles never read past zeroed storage.
+  const int rp_pitch = ellp + 20;
+  const int64_t big = max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
+  double* Rp = sm;                                 // PB x rp_pitch (panel rows of R)
+  double* d = sm + big;                            // panel-start Schur diagonal (by position)
+  double* work = d + ellp;                         // in-panel sum of R[k][x]^2
+  double* diag = work + ellp;                      // diagonal of R11 (by position)
+  int* loc = reinterpret_cast<int*>(diag + ellp);  // position -> storage row/col (this panel)
+  int* pos2orig = loc + ellp;                      // position -> original index
+
+  double* Wcur = G + b * sq;
+  double* Wnext = scratch + b * 2 * sq;
+  double* Rorig = Rfull ? Rfull + b * sq : scratch + b * 2 * sq + sq;  // row j: R[j][orig]
+
+  for (int i = tid; i < ellp; i += blockDim.x) {
+    d[i] = i < ell ? Wcur[i + static_cast<int64_t>(i) * ld] : 0.0;
+    pos2orig[i] = i;
+  }
+  for (int64_t e = tid; e < sq; e += blockDim.x) Rorig[e] = 0.0;
   __syncthreads();
 
-  double dmax0;
-  int p;
-  block_argmax(W, ld, 0, ell, s_val, s_idx, dmax0, p);
-  int r = ell;
-  if (!(dmax0 > 0.0)) r = 0;
-  for (int j = 0; j < r; ++j) {
-    double piv;
-    block_argmax(W, ld, j, ell, s_val, s_idx, piv, p);
-    if (!(piv > tau * dmax0)) {
-      r = j;
-      break;
+  if (warp == 0) {  // max diagonal
+    double v = 0.0;
+    for (int i = lane; i < ell; i += 32) v = fmax(v, d[i]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) {
+      s_piv = v;
+      s_stop = !(v > 0.0);
     }
-    if (p != j) {  // symmetric swap of rows and columns j <-> p
-      for (int i = tid; i < ell; i += blockDim.x) {
-        const double x = W[j + static_cast<int64_t>(i) * ld];
-        W[j + static_cast<int64_t>(i) * ld] = W[p + static_cast<int64_t>(i) * ld];
-        W[p + static_cast<int64_t>(i) * ld] = x;
+  }
+  __syncthreads();
+  const double thresh = tau * s_piv;
+  int r = s_stop ? 0 : ell;
+
+  for (int j0 = 0; j0 < r; j0 += PB) {
+    const int jb = min(PB, ell - j0);
+    for (int i = tid; i < ellp; i += blockDim.x) {
+      work[i] = 0.0;
+      loc[i] = i;
+    }
+    for (int e = tid; e < PB * rp_pitch; e += blockDim.x) Rp[e] = 0.0;
+    __syncthreads();
+    int jdone = jb;
+    for (int jj = 0; jj < jb; ++jj) {
+      const int j = j0 + jj;
+      if (warp == 0) {
+        // pivot: argmax over positions >= j of d - work (ties -> lowest position)
+        double v = -DBL_MAX;
+        int ix = 0x7fffffff;
+        for (int x = j + lane; x < ell; x += 32) {
+          const double dv = d[x] - work[x];
+          if (dv > v || (dv == v && x < ix)) v = dv, ix = x;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, ix, off);
+          if (ov > v || (ov == v && oi < ix)) v = ov, ix = oi;
+        }
+        const bool stop = !(v > thresh);
+        if (!stop && ix != j) {  // logical swap of positions j and ix
+          for (int k = lane; k < jj; k += 32) {
+            const double t0 = Rp[k * rp_pitch + j];
+            Rp[k * rp_pitch + j] = Rp[k * rp_pitch + ix];
+            Rp[k * rp_pitch + ix] = t0;
+          }
+          if (lane == 0) {
+            double t = d[j];
+            d[j] = d[ix];
+            d[ix] = t;
+            t = work[j];
+            work[j] = work[ix];
+            work[ix] = t;
+            int u = loc[j];
+            loc[j] = loc[ix];
+            loc[ix] = u;
+            u = pos2orig[j];
+            pos2orig[j] = pos2orig[ix];
+            pos2orig[ix] = u;
+          }
+        }
+        if (lane == 0) {
+          s_piv = v;
+          s_stop = stop;
+        }
       }
       __syncthreads();
-      for (int i = tid; i < ell; i += blockDim.x) {
-        const double x = W[i + static_cast<int64_t>(j) * ld];
-        W[i + static_cast<int64_t>(j) * ld] = W[i + static_cast<int64_t>(p) * ld];
-        W[i + static_cast<int64_t>(p) * ld] = x;
+      if (s_stop) {
+        jdone = jj;
+        r = j;
+        break;
+      }
+      const double rjj = sqrt(s_piv);
+      const double inv = 1.0 / rjj;
+      const double* wcol = Wcur + static_cast<int64_t>(loc[j]) * ld;
+      for (int x = j + 1 + tid; x < ell; x += blockDim.x) {
+        double s = wcol[loc[x]];
+        for (int k = 0; k < jj; ++k) s -= Rp[k * rp_pitch + j] * Rp[k * rp_pitch + x];
+        const double v = s * inv;
+        Rp[jj * rp_pitch + x] = v;
+        work[x] += v * v;
+        Rorig[j + static_cast<int64_t>(pos2orig[x]) * ld] = v;
       }
       if (tid == 0) {
-        const int x = perm[j];
-        perm[j] = perm[p];
-        perm[p] = x;
+        Rp[jj * rp_pitch + j] = rjj;
+        diag[j] = rjj;
+        Rorig[j + static_cast<int64_t>(pos2orig[j]) * ld] = rjj;
       }
       __syncthreads();
     }
-    const double rjj = sqrt(piv);
-    const double inv = 1.0 / rjj;
-    // Row j of R: W[j][c] / rjj for c > j.  Column j below the diagonal is
-    // updated to match so the trailing block stays symmetric.
-    for (int c = j + 1 + tid; c < ell; c += blockDim.x) {
-      const double v = W[j + static_cast<int64_t>(c) * ld] * inv;
-      W[j + static_cast<int64_t>(c) * ld] = v;
-      rrow[c] = v;
-    }
-    if (tid == 0) W[j + static_cast<int64_t>(j) * ld] = rjj;
-    __syncthreads();
-    // Trailing update W[a][c] -= R[j][a] R[j][c], a, c > j: one warp per
-    // column, lanes along the contiguous rows.
-    {
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int c = j + 1 + warp; c < ell; c += kCholWarps) {
-        const double rc = rrow[c];
-        double* col = W + static_cast<int64_t>(c) * ld;
-        for (int a = j + 1 + lane; a < ell; a += 32) col[a] -= rrow[a] * rc;
+    const int j1 = j0 + jdone;
+    if (jdone < jb || j1 >= ell) break;  // rank found, or finished
+    // Trailing rebuild: Wnext[x][y] = Wcur[loc x][loc y] - sum_k Rp[k][x] Rp[k][y]
+    // for positions x, y in [j1, ell): 16 x 16 DMMA tiles, one per warp.
+    const int nt = ell - j1;
+    const int tiles = (nt + 15) / 16;
+    const int g = lane >> 2, t = lane & 3;
+    for (int tile = warp; tile < tiles * tiles; tile += kCholWarps) {
+      const int tx = tile % tiles, ty = tile / tiles;
+      const int x0 = j1 + tx * 16, y0 = j1 + ty * 16;
+      double acc[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[h][q] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < PB; k0 += 4) {
+        const double a0 = Rp[(k0 + t) * rp_pitch + x0 + g];
+        const double a1 = Rp[(k0 + t) * rp_pitch + x0 + g + 8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double b0 = Rp[(k0 + t) * rp_pitch + y0 + h * 8 + g];
+          dmma_16x8x4(acc[h], a0, a1, b0);
+        }
       }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int x = x0 + g + ((q & 2) ? 8 : 0);
+          const int y = y0 + h * 8 + 2 * t + (q & 1);
+          if (x < ell && y < ell) {
+            const double w = Wcur[loc[x] + static_cast<int64_t>(loc[y]) * ld];
+            Wnext[x + static_cast<int64_t>(y) * ld] = w - acc[h][q];
+          }
+        }
     }
     __syncthreads();
-  }
-
-  // Outputs: Rfull[i][perm[c]] = R[i][c] (i < r, c >= i), zero elsewhere.
-  double* Tb = T + b * sq;
-  double* Rb = Rfull ? Rfull + b * sq : nullptr;
-  for (int64_t e = tid; e < sq; e += blockDim.x) {
-    Tb[e] = 0.0;
-    if (Rb) Rb[e] = 0.0;
+    for (int x = j1 + tid; x < ell; x += blockDim.x)
+      d[x] = Wnext[x + static_cast<int64_t>(x) * ld];
+    double* tmp = Wcur;
+    Wcur = Wnext;
+    Wnext = tmp;
+    __syncthreads();
   }
   __syncthreads();
-  if (Rb) {
-    for (int64_t e = tid; e < static_cast<int64_t>(r) * ell; e += blockDim.x) {
-      const int c = static_cast<int>(e / r), i = static_cast<int>(e - static_cast<int64_t>(c) * r);
-      if (c >= i) Rb[i + static_cast<int64_t>(perm[c]) * ld] = W[i + static_cast<int64_t>(c) * ld];
-    }
+
+  // ---- T = P[:, :r] R11^{-1} ---------------------------------------------
+  // R11 in position order, column-contiguous, padded to whole 32-blocks with
+  // an identity tail: C11[i + c*ld] = Rorig[i][pos2orig[c]] (i <= c < r).
+  double* C11 = Wnext;  // both trailing buffers are free now
+  double* X = Wcur;     // R11^{-1}, position order
+  const int nbk = (r + 31) / 32;
+  const int rp = nbk * 32;  // <= ellp (ellp is a multiple of 32)
+  for (int64_t e = tid; e < static_cast<int64_t>(rp) * rp; e += blockDim.x) {
+    const int c = static_cast<int>(e / rp), i = static_cast<int>(e - static_cast<int64_t>(c) * rp);
+    double v = 0.0;
+    if (c < r) v = i <= c ? Rorig[i + static_cast<int64_t>(pos2orig[c]) * ld] : 0.0;
+    else if (i == c) v = 1.0;
+    C11[i + static_cast<int64_t>(c) * ld] = v;
   }
-  // T = P[:, :r] R11^{-1}: column c of R11^{-1} by backward substitution on
-  // x = e_c (one warp per column, axpy form so lanes work in parallel).
-  const int warp = tid >> 5, lane = tid & 31;
-  double* x = colbuf + static_cast<int64_t>(warp) * ellp;
-  for (int c = warp; c < r; c += kCholWarps) {
-    for (int i = lane; i <= c; i += 32) x[i] = (i == c) ? 1.0 : 0.0;
-    __syncwarp();
-    for (int k = c; k >= 0; --k) {
-      const double xk = x[k] / W[k + static_cast<int64_t>(k) * ld];
-      __syncwarp();
-      if (lane == 0) x[k] = xk;
-      for (int i = lane; i < k; i += 32) x[i] -= W[i + static_cast<int64_t>(k) * ld] * xk;
-      __syncwarp();
-    }
-    for (int i = lane; i <= c; i += 32) Tb[perm[i] + static_cast<int64_t>(c) * ld] = x[i];
-    __syncwarp();
+  __syncthreads();
+  blocked_upper_inverse(C11, X, ld, nbk, sm, warp, lane);
+  double* Tb = T + b * sq;
+  for (int64_t e = tid; e < sq; e += blockDim.x) Tb[e] = 0.0;
+  __syncthreads();
+  for (int64_t e = tid; e < static_cast<int64_t>(r) * r; e += blockDim.x) {
+    const int c = static_cast<int>(e / r), i = static_cast<int>(e - static_cast<int64_t>(c) * r);
+    if (i <= c)
+      Tb[pos2orig[i] + static_cast<int64_t>(c) * ld] = X[i + static_cast<int64_t>(c) * ld];
   }
-  if (tid < ellp && perm_out) perm_out[b * ellp + tid] = perm[tid];
+  if (perm_out)
+    for (int i = tid; i < ellp; i += blockDim.x) perm_out[b * ellp + i] = pos2orig[i];
   if (tid == 0) rank_out[b] = r;
 }
 
 }  // namespace
 
-void launch_pchol(const double* G, double* T, double* Rfull, int* rank, int* perm, int64_t ell,
-                  int64_t ellp, double tau, int64_t batch, cudaStream_t st) {
-  const int64_t sq_bytes = ellp * ellp * static_cast<int64_t>(sizeof(double));
-  const int64_t scratch =
-      (kCholWarps + 1) * ellp * static_cast<int64_t>(sizeof(double)) + ellp * 4 + 16;
-  const bool in_smem = sq_bytes + scratch <= 220 * 1024;
-  double* Gm = const_cast<double*>(G);  // factored in place when not in shared memory
-  if (in_smem) {
-    const int bytes = static_cast<int>(sq_bytes + scratch);
-    RSVD_CUDA(cudaFuncSetAttribute(pchol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   bytes));
-    pchol_kernel<true><<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
-        Gm, T, Rfull, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
-  } else {
-    const int bytes = static_cast<int>(scratch);
-    RSVD_CUDA(cudaFuncSetAttribute(pchol_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    pchol_kernel<false><<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
-        Gm, T, Rfull, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
-  }
+int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ellp * batch; }
+
+void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
+                  int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st) {
+  if (batch <= 0) return;
+  if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
+  const int64_t pitch = ellp + 20;
+  const int64_t big = std::max<int64_t>(PB * pitch, kInvSmem);
+  const int64_t bytes = big * 8 + 3 * ellp * 8 + 2 * ellp * 4 + 64;
+  RSVD_CUDA(cudaFuncSetAttribute(pchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  pchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
+      G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
   RSVD_LAUNCH("pchol_kernel");
 }
 

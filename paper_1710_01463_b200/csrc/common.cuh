@@ -72,13 +72,20 @@ void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, 
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
 
 // chol.cu — pivoted / plain Cholesky of SPD Grams (ell x ell, ld ell).
-void launch_pchol(const double* G, double* T, double* Rfull, int* rank, int* perm, int64_t ell,
-                  int64_t ellp, double tau, int64_t batch, cudaStream_t st);
+// G is consumed (used as factorization storage); scratch holds
+// pchol_scratch_elems(ellp, batch) doubles.
+int64_t pchol_scratch_elems(int64_t ellp, int64_t batch);
+void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
+                  int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st);
 
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.
+// flags: jacobi_flag_elems(batch) unsigned ints of workspace.
+int64_t jacobi_flag_elems(int64_t batch);
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                   int64_t batch, cudaStream_t st);
+                   unsigned* flags, int64_t batch, cudaStream_t st);
+void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
+                           int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st);
 
 // aux.cu
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,

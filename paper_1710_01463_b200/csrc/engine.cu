@@ -167,11 +167,12 @@ struct Shape {
 struct Buffers {
   uint64_t* seeds;
   double *X, *X2, *Y, *Y2;
-  double *G, *T, *Rf1, *Rf2, *Rt, *H, *Jm;
+  double *G, *T, *Rf1, *Rf2, *Rt, *H, *Jm, *cscratch;
   double *Ut, *Jr, *Vb;
   double* sig;
   double* dw;
   int *rank1, *rank2, *rankF, *perm, *permS, *sweeps;
+  unsigned* jflags;
   double* partial;
   int64_t partial_cap;
   // staging for host-pointer calls
@@ -209,6 +210,7 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   B.T = c.take<double>(b * lp * lp);
   B.Rf1 = c.take<double>(b * lp * lp);
   B.Rf2 = c.take<double>(b * lp * lp);
+  B.cscratch = c.take<double>(pchol_scratch_elems(lp, b));
   B.rank1 = c.take<int>(b);
   B.rank2 = c.take<int>(b);
   B.perm = c.take<int>(b * lp);
@@ -224,6 +226,7 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
     B.rankF = c.take<int>(b);
     B.permS = c.take<int>(b * lp);
     B.sweeps = c.take<int>(b);
+    B.jflags = c.take<unsigned>(jacobi_flag_elems(b));
   }
   B.partial_cap = partial_need(s);
   B.partial = c.take<double>(std::max<int64_t>(B.partial_cap, 1));
@@ -257,7 +260,7 @@ void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, dou
     }
     {
       Scope sc(P, kStChol, st);
-      launch_pchol(B.G, B.T, Rf, rk, B.perm, s.ell, lp, kPivotTau, b, st);
+      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, b, st);
     }
     Scope sc(P, kStApply, st);
     dgemm(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, st);
@@ -317,7 +320,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   {
     Scope sc(P, kStJacobi, st);
     launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
-    launch_jacobi(B.H, B.Jm, s.ell, lp, kMaxSweeps, B.sweeps, b, st);
+    launch_jacobi(B.H, B.Jm, s.ell, lp, kMaxSweeps, B.sweeps, B.jflags, b, st);
   }
   Scope sc(P, kStLift, st);
   launch_finalize_spectrum(B.H, lp, s.ell, k, s.m, s.n, B.sig, B.permS, B.rankF, B.dw, b, st);
@@ -386,7 +389,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   RSVD_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
 
-  Shape s{m, n, batch, rank, ell, round_up(ell, 8), power};
+  Shape s{m, n, batch, rank, ell, round_up(ell, 32), power};
   Carver meas{nullptr};
   carve(meas, s, host, true);
   h->arena.reserve(meas.off + 256);
@@ -445,7 +448,7 @@ void range_impl(rsvd_context* h, const double* A, int64_t m, int64_t n, int64_t 
   const bool host = flags == RSVD_PTR_HOST;
   RSVD_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
-  Shape s{m, n, 1, ell, ell, round_up(ell, 8), power};
+  Shape s{m, n, 1, ell, ell, round_up(ell, 32), power};
   Carver meas{nullptr};
   carve(meas, s, host, false);
   h->arena.reserve(meas.off + 256);

@@ -22,6 +22,7 @@
 // second kernel sums in fixed order: no atomics, bitwise reproducible.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -290,6 +291,7 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   int64_t splits = 1;
   if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / 256));
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
+  if (const char* env = std::getenv("RSVD_MAX_SPLITS")) splits = std::min<int64_t>(splits, std::atoi(env));
   int64_t kps = round_up(ceil_div(K, splits), kBK);
   splits = ceil_div(K, kps);
   c.splits = static_cast<int>(std::max<int64_t>(1, splits));

@@ -13,6 +13,8 @@
 // no rotation above tol = sqrt(l) * eps (dgesvj's convergence test) ends the
 // iteration.  One CTA per batch item; H and J live in shared memory when both
 // fit, otherwise in global memory (L2-resident).
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "common.cuh"
@@ -120,21 +122,198 @@ __global__ void __launch_bounds__(kJacThreads)
   if (tid == 0 && sweeps_out) sweeps_out[b] = sweep + 1;
 }
 
+// ---------------------------------------------------------------------------
+// Block-pair one-sided Jacobi for l too large for one CTA's shared memory.
+//
+// Columns are grouped into nb blocks of W (nb even, trailing blocks may be
+// partly or wholly beyond l).  One outer step pairs the blocks round-robin;
+// each pair (2W columns of H and J, rows < l) is staged in shared memory by
+// one CTA, which runs `inner` cyclic sweeps over the 2W local columns (one
+// warp per column pair, W warps) and writes them back.  Every column pair
+// meets in each outer sweep, so the outer sweep is a superset of a scalar
+// cyclic sweep.  A persistent cooperative grid walks the (item, pair) tasks of
+// a step, grid-syncs, and items whose whole sweep rotated nothing (same
+// sqrt(l) eps test as above) drop out.
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+    jacobi_blocked_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp,
+                          int nb, int64_t batch, int max_sweeps, int inner,
+                          unsigned* __restrict__ flags, int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  constexpr int NC = 2 * W;
+  const int pitch = ell + (ell & 1);
+  double* Hs = sm;                  // NC x pitch
+  double* Js = sm + NC * pitch;     // NC x pitch
+  int* conv = reinterpret_cast<int*>(Js + NC * pitch);  // per-item converged (batch ints)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+
+  // J = I, flags cleared.
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
+    for (int s = 0; s < nb - 1; ++s) {
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        const int p = rr_player(k, s, nb), q = rr_player(nb - 1 - k, s, nb);
+        const int bp = min(p, q), bq = max(p, q);
+        if (bp * W >= ell) continue;  // both blocks are padding
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        // stage: local column c < W from block bp, c >= W from block bq
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = (c < W ? bp * W + c : bq * W + (c - W));
+          const bool ok = gc < ell && r < ell;
+          Hs[e] = ok ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
+          Js[e] = ok ? __ldcg(Jg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
+        }
+        if (tid == 0) s_rot = 0;
+        __syncthreads();
+        int rotated = 0;
+        for (int it = 0; it < inner; ++it) {
+          for (int s2 = 0; s2 < NC - 1; ++s2) {
+            const int a = rr_player(warp, s2, NC), bb2 = rr_player(NC - 1 - warp, s2, NC);
+            const int i = min(a, bb2), jx = max(a, bb2);
+            double* hi = Hs + i * pitch;
+            double* hj = Hs + jx * pitch;
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int r = lane; r < ell; r += 32) {
+              const double x = hi[r], y = hj[r];
+              al = fma(x, x, al);
+              be = fma(y, y, be);
+              ga = fma(x, y, ga);
+            }
+            al = warp_sum(al);
+            be = warp_sum(be);
+            ga = warp_sum(ga);
+            if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+              const double zeta = (be - al) / (2.0 * ga);
+              const double tt =
+                  (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double c = 1.0 / sqrt(1.0 + tt * tt);
+              const double sn = c * tt;
+              for (int r = lane; r < ell; r += 32) {
+                const double x = hi[r], y = hj[r];
+                hi[r] = c * x - sn * y;
+                hj[r] = sn * x + c * y;
+              }
+              double* ji = Js + i * pitch;
+              double* jj = Js + jx * pitch;
+              for (int r = lane; r < ell; r += 32) {
+                const double x = ji[r], y = jj[r];
+                ji[r] = c * x - sn * y;
+                jj[r] = sn * x + c * y;
+              }
+              rotated = 1;
+            }
+            __syncthreads();
+          }
+        }
+        if (rotated && lane == 0) atomicOr(&s_rot, 1);
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = (c < W ? bp * W + c : bq * W + (c - W));
+          if (gc < ell && r < ell) {
+            Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
+            Jg[r + static_cast<int64_t>(gc) * ellp] = Js[e];
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
+      }
+      grid.sync();
+    }
+    // Items whose sweep rotated nothing are converged (same view in every CTA).
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const unsigned f = __ldcg(fl + i);
+      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || f == 0u);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (__ldcg(fl + i) == 0u) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int W>
+void launch_blocked_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
+                      int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
+  const int pitch = static_cast<int>(ell + (ell & 1));
+  const size_t bytes = 2 * (2 * W) * pitch * sizeof(double) + batch * sizeof(int) + 16;
+  auto kern = jacobi_blocked_kernel<W>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, bytes));
+  if (per_sm < 1) throw CudaError("jacobi_blocked_kernel: does not fit on an SM");
+  int dev = 0, sms = 0;
+  RSVD_CUDA(cudaGetDevice(&dev));
+  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int nb = static_cast<int>((ell + W - 1) / W);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp), inner = 1;
+  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &inner, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(W * 32),
+                                        args, bytes, st));
+  RSVD_LAUNCH("jacobi_blocked_kernel");
+}
+
 }  // namespace
 
+int64_t jacobi_flag_elems(int64_t batch) { return 3 * batch; }
+
+void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
+                           int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
+  if (4 * 16 * ell * 8 <= 200 * 1024)
+    launch_blocked_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  else if (4 * 8 * ell * 8 <= 200 * 1024)
+    launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  else
+    launch_blocked_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+}
+
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                   int64_t batch, cudaStream_t st) {
+                   unsigned* flags, int64_t batch, cudaStream_t st) {
   const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
   if (bytes <= 220 * 1024) {
+    // Whole problem fits one CTA's shared memory: one CTA per item.
     RSVD_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(bytes)));
     jacobi_kernel<true><<<static_cast<unsigned>(batch), kJacThreads, bytes, st>>>(
         H, J, static_cast<int>(ell), static_cast<int>(ellp), max_sweeps, sweeps);
-  } else {
-    jacobi_kernel<false><<<static_cast<unsigned>(batch), kJacThreads, 0, st>>>(
-        H, J, static_cast<int>(ell), static_cast<int>(ellp), max_sweeps, sweeps);
+    RSVD_LAUNCH("jacobi_kernel");
+    return;
   }
-  RSVD_LAUNCH("jacobi_kernel");
+  launch_jacobi_blocked(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
 }
 
 }  // namespace rsvd

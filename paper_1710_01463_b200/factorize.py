@@ -81,7 +81,7 @@ def _torch_stream_guard(h):
     import torch
 
     lib = _lib.load()
-    lib.rsvd_set_stream(h.raw, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    lib.rsvd_set_stream(h.raw, ctypes.c_void_p(_lib.torch_stream_ptr()))
 
 
 def _resolve_ell(m: int, n: int, p: RsvdParams) -> int:

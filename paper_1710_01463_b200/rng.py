@@ -62,7 +62,7 @@ class CounterRng:
             if out.dtype.itemsize != 8 or not out.is_contiguous():
                 raise _lib.InvalidArgument("fill_gaussian: need a contiguous float64 tensor")
             import torch
-            lib.rsvd_set_stream(h.raw, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            lib.rsvd_set_stream(h.raw, ctypes.c_void_p(_lib.torch_stream_ptr()))
             rc = lib.rsvd_fill_gaussian_f64(h.raw, self.key, out.data_ptr(), n, _lib.PTR_DEVICE)
             lib.rsvd_set_stream(h.raw, None)
         else:

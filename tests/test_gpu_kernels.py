@@ -53,7 +53,7 @@ def _dgemm(trans_a, A, B, M, N, K, batch, lda, ldb, sA, sB):
     h = _lib.default_handle()
     C = torch.zeros(batch * M * N + 7, dtype=torch.float64, device=A.device)
     lib = _lib.load()
-    lib.rsvd_set_stream(h.raw, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    lib.rsvd_set_stream(h.raw, ctypes.c_void_p(_lib.torch_stream_ptr()))
     try:
         rc = lib.rsvd_testing_dgemm(h.raw, int(trans_a), M, N, K, A.data_ptr(), lda, sA,
                                     B.data_ptr(), ldb, sB, C.data_ptr(), M, M * N, batch)
