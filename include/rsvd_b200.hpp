@@ -1,0 +1,146 @@
+// rsvd_b200.hpp — header-only C++ drop-in for rlftn's factorization API over
+// the C ABI of include/rsvd_c.h.
+//
+// Mirrors proj/include/rlftn/factorize.hpp: RsvdParams (hpp:40-45),
+// TruncatedFactorization (hpp:15-31), rsvd (hpp:62-63), randomized_range
+// (hpp:56-57), reconstruction_error (hpp:68-70), and rng.hpp's mix64 /
+// derive_seed / seed_tag.  Errors are rethrown as the reference's exception
+// types with the reference's messages (std::invalid_argument for argument
+// errors, std::runtime_error otherwise).  The matrix type is an owning
+// column-major buffer with lda == rows, i.e. exactly the storage Eigen hands
+// to LAPACK (types.hpp:12-13), so an Eigen caller passes a.data()/a.rows()/
+// a.cols().
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rsvd_c.h"
+
+namespace rlftn_b200 {
+
+using Index = std::int64_t;
+
+struct MatrixR {
+  Index r = 0, c = 0;
+  std::vector<double> v;
+  MatrixR() = default;
+  MatrixR(Index rows, Index cols) : r(rows), c(cols), v(static_cast<size_t>(rows * cols), 0.0) {}
+  Index rows() const { return r; }
+  Index cols() const { return c; }
+  double* data() { return v.data(); }
+  const double* data() const { return v.data(); }
+  double& operator()(Index i, Index j) { return v[static_cast<size_t>(i + j * r)]; }
+  double operator()(Index i, Index j) const { return v[static_cast<size_t>(i + j * r)]; }
+};
+
+struct RsvdParams {
+  Index rank = 0;
+  Index oversample = 0;  // total sample width l; 0 -> min(2*rank, min(m, n))
+  int power = 4;
+  std::uint64_t seed = 0;
+};
+
+struct TruncatedFactorization {
+  MatrixR left;                // m x r
+  std::vector<double> sigma;   // r
+  MatrixR right_adj;           // r x n
+  double discarded_weight = 0.0;
+  bool discarded_exact = true;
+  Index rank() const { return static_cast<Index>(sigma.size()); }
+};
+
+namespace seed_tag {
+inline constexpr std::uint64_t initial_state = 1;
+inline constexpr std::uint64_t rsvd_stream = 2;
+inline constexpr std::uint64_t bench_matrix = 3;
+}  // namespace seed_tag
+
+inline std::uint64_t mix64(std::uint64_t z) { return rsvd_mix64(z); }
+inline std::uint64_t derive_seed(std::uint64_t s, std::uint64_t t) { return rsvd_derive_seed(s, t); }
+
+// One engine handle per thread (the reference is re-entrant).
+class Engine {
+ public:
+  explicit Engine(int device = 0) {
+    const int rc = rsvd_create(&h_, device);
+    if (rc != RSVD_OK) {
+      const std::string msg = h_ ? rsvd_last_error(h_) : "rsvd_create failed";
+      if (h_) rsvd_destroy(h_);
+      h_ = nullptr;
+      throw std::runtime_error(msg);
+    }
+  }
+  ~Engine() {
+    if (h_) rsvd_destroy(h_);
+  }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+  rsvd_handle raw() const { return h_; }
+
+  void check(int rc) const {
+    if (rc == RSVD_OK) return;
+    const std::string msg = rsvd_last_error(h_);
+    if (rc == RSVD_ERR_INVALID) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+  }
+
+ private:
+  rsvd_handle h_ = nullptr;
+};
+
+inline Engine& default_engine() {
+  thread_local Engine e(0);
+  return e;
+}
+
+// rlftn::rsvd<double> (factorize.cpp:76-95) on the GPU.
+inline TruncatedFactorization rsvd(const MatrixR& a, const RsvdParams& p,
+                                   Engine& e = default_engine()) {
+  const Index m = a.rows(), n = a.cols();
+  const Index k = p.rank > 0 ? p.rank : 1;
+  MatrixR u(m, k), vt(k, n);
+  std::vector<double> s(static_cast<size_t>(k));
+  std::int64_t r = 0;
+  double dw = 0.0;
+  e.check(rsvd_f64(e.raw(), a.data(), m, n, m > 0 ? m : 1, p.rank, p.oversample, p.power, p.seed,
+                   u.data(), m > 0 ? m : 1, s.data(), vt.data(), k, &r, &dw, RSVD_PTR_HOST));
+  TruncatedFactorization f;
+  f.left = MatrixR(m, r);
+  for (Index j = 0; j < r; ++j)
+    for (Index i = 0; i < m; ++i) f.left(i, j) = u(i, j);
+  f.sigma.assign(s.begin(), s.begin() + r);
+  f.right_adj = MatrixR(r, n);
+  for (Index j = 0; j < n; ++j)
+    for (Index i = 0; i < r; ++i) f.right_adj(i, j) = vt(i, j);
+  f.discarded_weight = dw;
+  f.discarded_exact = false;
+  return f;
+}
+
+// rlftn::randomized_range<double> (factorize.cpp:52-74).
+inline MatrixR randomized_range(const MatrixR& a, Index ell, int power, std::uint64_t seed,
+                                Engine& e = default_engine()) {
+  MatrixR q(a.rows(), ell > 0 ? ell : 0);
+  e.check(rsvd_randomized_range_f64(e.raw(), a.data(), a.rows(), a.cols(),
+                                    a.rows() > 0 ? a.rows() : 1, ell, power, seed, q.data(),
+                                    a.rows() > 0 ? a.rows() : 1, RSVD_PTR_HOST));
+  return q;
+}
+
+// rlftn::reconstruction_error(a, f, ErrorNorm::frobenius) (factorize.cpp:97-104).
+inline double reconstruction_error(const MatrixR& a, const TruncatedFactorization& f,
+                                   Engine& e = default_engine()) {
+  double out = 0.0;
+  const Index r = f.rank();
+  e.check(rsvd_reconstruction_error_f64(e.raw(), a.data(), a.rows(), a.cols(), a.rows(),
+                                        r ? f.left.data() : nullptr, a.rows(),
+                                        r ? f.sigma.data() : nullptr,
+                                        r ? f.right_adj.data() : nullptr, r > 0 ? r : 1, r,
+                                        &out, RSVD_PTR_HOST));
+  return out;
+}
+
+}  // namespace rlftn_b200
