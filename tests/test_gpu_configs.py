@@ -1,0 +1,115 @@
+"""Parity on BASELINE.json's five full-size configurations.
+
+The same A bytes (generated on the GPU by paper_1710_01463_b200.synth, copied
+to the host) go to the engine and to the CPU oracle (restated reference rsvd,
+OpenBLAS LAPACK, all host threads); the oracle draws its own Omega from the
+same CounterRng seed.  Batched configs check a sample of items against the
+oracle and the whole batch through size-independent properties (isometry,
+ordering, Eckart-Young, determinism)."""
+import numpy as np
+import pytest
+
+from tests.helpers import isometry_err, rel_sigma_err, subspace_distance
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-10
+REC_TOL = 1e-10
+SUB_TOL = 1e-8
+
+
+def gapped_prefix(S, k, rel_gap=1e-6):
+    for j in range(min(k, len(S) - 1), 0, -1):
+        if (S[j - 1] - S[j]) >= rel_gap * S[0]:
+            return j
+    return 0
+
+
+def compare(a, U, S, Vt, dw, ref, label):
+    Ur, Sr, Vtr, dwr = ref
+    assert len(S) == len(Sr), (label, len(S), len(Sr))
+    assert rel_sigma_err(S, Sr) < SIG_TOL, (label, rel_sigma_err(S, Sr))
+    assert isometry_err(U) < 1e-12, label
+    assert isometry_err(Vt.T) < 1e-12, label
+    e = float(np.linalg.norm(a - (U * S[None, :]) @ Vt))
+    er = float(np.linalg.norm(a - (Ur * Sr[None, :]) @ Vtr))
+    assert abs(e - er) / er < REC_TOL, (label, e, er)
+    j = gapped_prefix(Sr, len(Sr))
+    if j:
+        assert subspace_distance(U[:, :j], Ur[:, :j]) < SUB_TOL, label
+        assert subspace_distance(Vt[:j].T, Vtr[:j].T) < SUB_TOL, label
+    assert dw == pytest.approx(dwr, rel=1e-8), label
+    return {"sig": rel_sigma_err(S, Sr), "rec": abs(e - er) / er, "j": j}
+
+
+def run_config(name, cuda, oracle_mod, items):
+    import torch
+
+    from paper_1710_01463_b200 import RsvdParams, rsvd_batched, synth
+
+    cfg = synth.CONFIGS[name]
+    A = synth.make_batch(cfg, device=cuda)
+    seeds = synth.omega_seeds(cfg)
+    p = RsvdParams(cfg.rank, cfg.ell, cfg.power, 0)
+    f = rsvd_batched(A, p, seeds)
+    torch.cuda.synchronize()
+    out = {}
+    for b in items:
+        a = np.asfortranarray(A[b].cpu().numpy())
+        ref = oracle_mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, seeds[b])
+        r = f.ranks[b]
+        U = f.left[b][:, :r].cpu().numpy()
+        S = f.sigma[b][:r].cpu().numpy()
+        Vt = f.right_adj[b][:r, :].cpu().numpy()
+        out[b] = compare(a, U, S, Vt, f.discarded_weight[b], ref, f"{name}[{b}]")
+    return A, f, out
+
+
+def test_c1(cuda, oracle_mod):
+    run_config("C1", cuda, oracle_mod, [0])
+
+
+def test_c2_batch(cuda, oracle_mod):
+    import torch
+
+    A, f, _ = run_config("C2", cuda, oracle_mod, [0, 97, 255])
+    # whole batch: isometry and ordering of every item
+    for b in range(A.shape[0]):
+        r = f.ranks[b]
+        U = f.left[b][:, :r]
+        eye = torch.eye(r, dtype=torch.float64, device=U.device)
+        assert (U.t() @ U - eye).abs().max().item() < 1e-12
+        s = f.sigma[b][:r]
+        assert bool((s[1:] <= s[:-1]).all())
+
+
+@pytest.mark.parametrize("name", ["C3", "C3q3"])
+def test_c3(cuda, oracle_mod, name):
+    run_config(name, cuda, oracle_mod, [0])
+
+
+def test_c4_batch(cuda, oracle_mod):
+    import torch
+
+    from paper_1710_01463_b200 import RsvdParams, rsvd_batched, synth
+
+    A, f, _ = run_config("C4", cuda, oracle_mod, [0, 31])
+    cfg = synth.CONFIGS["C4"]
+    # determinism of the whole batch: bitwise equal on a second call
+    f2 = rsvd_batched(A, RsvdParams(cfg.rank, cfg.ell, cfg.power, 0), synth.omega_seeds(cfg))
+    assert torch.equal(f.sigma, f2.sigma)
+    assert torch.equal(f.left, f2.left)
+    assert torch.equal(f.right_adj, f2.right_adj)
+    # Eckart-Young: no rank-k factorization beats the exact tail
+    a = A[5]
+    s_exact = torch.linalg.svdvals(a)
+    tail = torch.sqrt((s_exact[cfg.rank:] ** 2).sum()).item()
+    r = f.ranks[5]
+    rec = (f.left[5][:, :r] * f.sigma[5][:r]) @ f.right_adj[5][:r]
+    err = torch.linalg.norm(a - rec).item()
+    assert tail * (1 - 1e-12) <= err <= tail * 1.10
+
+
+@pytest.mark.slow
+def test_c5(cuda, oracle_mod):
+    run_config("C5", cuda, oracle_mod, [0])
