@@ -6,8 +6,9 @@
 //   P^T G P ~= R^T R with R (r x l) upper trapezoidal in pivoted order,
 //   stopping at the first pivot <= tau * max(diag G): the numerical rank r of
 //   Y (LAPACK dpstrf semantics).  Outputs
-//     T     (l x l): Q1 = Y * T has the r leading columns
-//                    (T = P[:, :r] R11^{-1}); columns >= r are zero and get
+//     T     (l x l): R11^{-1} in pivot order, upper triangular; Q1 = (Y P) T
+//                    (Y's columns gathered through perm) has the r leading
+//                    columns; columns >= r are zero and get
 //                    filled by the basis completion (aux.cu), which is how
 //                    the reference's "always l orthonormal columns, arbitrary
 //                    completion when rank deficient" contract
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kCholThreads)
   }
   __syncthreads();
 
-  // ---- T = P[:, :r] R11^{-1} ---------------------------------------------
+  // ---- T = R11^{-1} (pivot order; the apply GEMM gathers Y's columns) ----
   // R11 in position order, column-contiguous, padded to whole 32-blocks with
   // an identity tail: C11[i + c*ld] = Rorig[i][pos2orig[c]] (i <= c < r).
   double* C11 = Wnext;  // both trailing buffers are free now
@@ -340,8 +341,7 @@ __global__ void __launch_bounds__(kCholThreads)
   __syncthreads();
   for (int64_t e = tid; e < static_cast<int64_t>(r) * r; e += blockDim.x) {
     const int c = static_cast<int>(e / r), i = static_cast<int>(e - static_cast<int64_t>(c) * r);
-    if (i <= c)
-      Tb[pos2orig[i] + static_cast<int64_t>(c) * ld] = X[i + static_cast<int64_t>(c) * ld];
+    if (i <= c) Tb[i + static_cast<int64_t>(c) * ld] = X[i + static_cast<int64_t>(c) * ld];
   }
   if (perm_out)
     for (int i = tid; i < ellp; i += blockDim.x) perm_out[b * ellp + i] = pos2orig[i];

@@ -69,6 +69,18 @@ void launch_fill_gaussian_flat(double* out, int64_t count, uint64_t seed, cudaSt
 // of M x N, ld M) and are reduced in fixed order into C (deterministic).
 void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
            int64_t batch, double* partial, int64_t partial_capacity, cudaStream_t st);
+// Structured variants: NN with a per-item column map on A (A(:, k) =
+// A_stored(:, colmapA[item*colmap_stride + k])), upper-triangular B (skips the
+// zero K-range per output tile), and symmetric C (upper tiles only, mirrored).
+struct GemmOpts {
+  const int* colmapA = nullptr;
+  int64_t colmap_stride = 0;
+  bool b_upper = false;
+  bool c_upper = false;
+};
+void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
+              int64_t batch, double* partial, int64_t partial_capacity, const GemmOpts& opt,
+              cudaStream_t st);
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
 
 // chol.cu — pivoted / plain Cholesky of SPD Grams (ell x ell, ld ell).

@@ -256,14 +256,21 @@ void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, dou
     int* rk = pass == 0 ? B.rank1 : B.rank2;
     {
       Scope sc(P, kStGram, st);
-      dgemm(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, st);
+      GemmOpts sym;
+      sym.c_upper = true;
+      dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
     }
     {
       Scope sc(P, kStChol, st);
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, b, st);
     }
     Scope sc(P, kStApply, st);
-    dgemm(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, st);
+    // out = (in P) R11^{-1}: pivot-gathered columns, upper-triangular right factor.
+    GemmOpts tri;
+    tri.colmapA = B.perm;
+    tri.colmap_stride = lp;
+    tri.b_upper = true;
+    dgemm_ex(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, tri, st);
     launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, st);
   }
   if (Rt) {

@@ -69,6 +69,14 @@ struct GemmArgs {
   int64_t batch;
   int splits;
   int64_t k_per_split;  // multiple of BK
+  // Optional structure flags:
+  //   colmapA (NN only): A(i, k) = A_stored(i, colmapA[item*colmap_stride + k])
+  //   b_upper: B is upper triangular, output tile [n0, n0+BN) needs k < n0+BN
+  //   c_upper: only tiles touching the upper triangle of C are computed
+  const int* colmapA;
+  int64_t colmap_stride;
+  int b_upper;
+  int c_upper;
 };
 
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC>
@@ -90,8 +98,9 @@ struct GemmCfg {
   static constexpr size_t kSmemBytes = sizeof(double) * kStageElems * STAGES;
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC,
+          int MINB>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     dgemm_kernel(const GemmArgs p) {
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC>;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
@@ -108,12 +117,15 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
   const int64_t bz = blockIdx.z;
   const int64_t item = bz / p.splits;
   const int split = static_cast<int>(bz % p.splits);
+  if (p.c_upper && m0 >= n0 + BN) return;  // tile strictly below the diagonal
   const int64_t k_begin = split * p.k_per_split;
-  const int64_t k_end = min(p.K, k_begin + p.k_per_split);
+  int64_t k_end = min(p.K, k_begin + p.k_per_split);
+  if (p.b_upper) k_end = min(k_end, n0 + BN);  // rows >= n0+BN of an upper B are zero
   const int64_t num_k_tiles = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
 
   const double* __restrict__ Ab = p.A + item * p.strideA;
   const double* __restrict__ Bb = p.B + item * p.strideB;
+  const int* __restrict__ cmap = p.colmapA ? p.colmapA + item * p.colmap_stride : nullptr;
 
   // ---- global -> shared staging of one K-slab --------------------------
   auto load_stage = [&](int stage, int64_t k0) {
@@ -129,7 +141,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
         const int ii = (c % kChunksPerCol) * VEC;
         const int64_t gi = m0 + ii, gk = k0 + kk;
         const bool ok = (gi < p.M) && (gk < k_end);
-        const double* src = ok ? Ab + gi + gk * p.lda : Ab;
+        const int64_t col = (ok && cmap) ? cmap[gk] : gk;
+        const double* src = ok ? Ab + gi + col * p.lda : Ab;
         cp_async<VEC * 8>(sA + kk * Cfg::kPitchA + ii, src, ok);
       }
     } else {
@@ -251,10 +264,23 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int64_t
   }
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC>
+// C(r, c) = C(c, r) for r > c (square items).
+__global__ void mirror_upper_kernel(double* __restrict__ C, int64_t n, int64_t ldc,
+                                    int64_t strideC, int64_t batch) {
+  const int64_t per = n * n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < per * batch;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t item = e / per, rem = e - item * per;
+    const int64_t c = rem / n, r = rem - c * n;
+    if (r > c) C[item * strideC + r + c * ldc] = C[item * strideC + c + r * ldc];
+  }
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC,
+          int MINB = 1>
 void launch_cfg(const GemmArgs& a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC>;
-  auto kern = dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC>;
+  auto kern = dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC, MINB>;
   static bool attr_set = false;
   if (!attr_set) {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -299,10 +325,33 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   return c;
 }
 
+int tuning_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RSVD_GEMM_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <bool TRANS_A, int VEC>
 void dispatch(const Choice& c, const GemmArgs& a, cudaStream_t st) {
-  if (c.bm == 128 && c.bn == 96)
-    launch_cfg<128, 96, kBK, 4, 2, kStages, TRANS_A, VEC>(a, st);
+  // Tuning variants for the large aligned A-pass shapes (RSVD_GEMM_VARIANT).
+  if constexpr (VEC == 2) {
+    const int v = tuning_variant();
+    if (v != 0 && c.bm == 128 && c.bn == 96 && a.splits == 1) {
+      switch (v) {
+        case 1: return launch_cfg<128, 96, 16, 4, 2, 3, TRANS_A, VEC, 2>(a, st);
+        case 2: return launch_cfg<128, 96, 32, 4, 2, 2, TRANS_A, VEC, 1>(a, st);
+        case 3: return launch_cfg<128, 144, 16, 4, 3, 3, TRANS_A, VEC, 1>(a, st);
+        case 4: return launch_cfg<128, 96, 16, 4, 2, 4, TRANS_A, VEC, 1>(a, st);
+        case 5: return launch_cfg<64, 96, 16, 2, 2, 3, TRANS_A, VEC, 3>(a, st);
+        case 6: return launch_cfg<192, 96, 16, 6, 2, 3, TRANS_A, VEC, 1>(a, st);
+        default: break;
+      }
+    }
+  }
+  if (c.bm == 128 && c.bn == 96)  // 128 registers: two CTAs per SM (profiles/r01_gemm_tune.txt)
+    launch_cfg<128, 96, kBK, 4, 2, kStages, TRANS_A, VEC, 2>(a, st);
   else if (c.bm == 128 && c.bn == 64)
     launch_cfg<128, 64, kBK, 4, 2, kStages, TRANS_A, VEC>(a, st);
   else if (c.bm == 128 && c.bn == 32)
@@ -326,6 +375,12 @@ int64_t dgemm_partial_elems(bool, int64_t M, int64_t N, int64_t K, int64_t batch
 
 void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
            int64_t batch, double* partial, int64_t partial_capacity, cudaStream_t st) {
+  dgemm_ex(trans_a, M, N, K, A, B, C, batch, partial, partial_capacity, GemmOpts{}, st);
+}
+
+void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
+              int64_t batch, double* partial, int64_t partial_capacity, const GemmOpts& opt,
+              cudaStream_t st) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   Choice c = choose(M, N, K, batch);
   if (K <= 0) c.splits = 1, c.kps = kBK;
@@ -341,6 +396,10 @@ void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, 
   a.batch = batch;
   a.splits = c.splits;
   a.k_per_split = c.kps;
+  a.colmapA = trans_a ? nullptr : opt.colmapA;
+  a.colmap_stride = opt.colmap_stride;
+  a.b_upper = opt.b_upper ? 1 : 0;
+  a.c_upper = (opt.c_upper && M == N) ? 1 : 0;
   if (c.splits > 1) {
     a.C = partial, a.ldc = M, a.strideC = M * N;
   } else {
@@ -364,6 +423,12 @@ void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, 
     splitk_reduce_kernel<<<blocks, threads, 0, st>>>(partial, M, N, c.splits, batch, C.base, C.ld,
                                                      C.stride);
     RSVD_LAUNCH("splitk_reduce_kernel");
+  }
+  if (a.c_upper) {  // symmetric result: mirror the upper triangle
+    const int64_t total = M * M * batch;
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
+    mirror_upper_kernel<<<blocks, 256, 0, st>>>(C.base, M, C.ld, C.stride, batch);
+    RSVD_LAUNCH("mirror_upper_kernel");
   }
 }
 

@@ -15,6 +15,8 @@
 // fit, otherwise in global memory (L2-resident).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include <cfloat>
 
 #include "common.cuh"
@@ -293,7 +295,13 @@ int64_t jacobi_flag_elems(int64_t batch) { return 3 * batch; }
 
 void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
                            int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
-  if (4 * 16 * ell * 8 <= 200 * 1024)
+  const char* env = std::getenv("RSVD_JACOBI_W");
+  const int wforce = env ? std::atoi(env) : 0;
+  if (wforce == 8 && 4 * 8 * ell * 8 <= 200 * 1024)
+    launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  else if (wforce == 4)
+    launch_blocked_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  else if (4 * 16 * ell * 8 <= 200 * 1024)
     launch_blocked_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
   else if (4 * 8 * ell * 8 <= 200 * 1024)
     launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
