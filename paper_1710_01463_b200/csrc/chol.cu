@@ -151,7 +151,7 @@ __device__ void blocked_upper_inverse(const double* __restrict__ R, double* __re
 __global__ void __launch_bounds__(kCholThreads)
     pchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
                  double* __restrict__ scratch, int* __restrict__ rank_out,
-                 int* __restrict__ perm_out, int ell, int ellp, double tau) {
+                 int* __restrict__ perm_out, int ell, int ellp, double tau, int pivot) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_piv;
   __shared__ int s_stop;
@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(kCholThreads)
           const double ov = __shfl_xor_sync(0xffffffffu, v, off);
           const int oi = __shfl_xor_sync(0xffffffffu, ix, off);
           if (ov > v || (ov == v && oi < ix)) v = ov, ix = oi;
+        }
+        if (!pivot) {  // plain Cholesky: keep the order, still test the pivot floor
+          ix = j;
+          v = d[j] - work[j];
         }
         const bool stop = !(v > thresh);
         if (!stop && ix != j) {  // logical swap of positions j and ix
@@ -353,7 +357,8 @@ __global__ void __launch_bounds__(kCholThreads)
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ellp * batch; }
 
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
-                  int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st) {
+                  int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
+                  cudaStream_t st) {
   if (batch <= 0) return;
   if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
   const int64_t pitch = ellp + 20;
@@ -362,7 +367,8 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   RSVD_CUDA(cudaFuncSetAttribute(pchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));
   pchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
-      G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
+      G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau,
+      pivot ? 1 : 0);
   RSVD_LAUNCH("pchol_kernel");
 }
 

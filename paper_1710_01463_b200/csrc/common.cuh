@@ -88,7 +88,8 @@ int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64
 // pchol_scratch_elems(ellp, batch) doubles.
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch);
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
-                  int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st);
+                  int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
+                  cudaStream_t st);
 
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.

@@ -241,6 +241,11 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   return B;
 }
 
+bool pivot_pass2() {
+  static const bool v = std::getenv("RSVD_PIVOT_PASS2") != nullptr;
+  return v;
+}
+
 // CholeskyQR2 of Y (rows x ellp per item) in place, Tmp as scratch.  When
 // Rt is given, also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
 void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, double* Rt,
@@ -262,7 +267,10 @@ void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, dou
     }
     {
       Scope sc(P, kStChol, st);
-      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, b, st);
+      // Pass 1 pivots (rank revealing, QRCP order for the Jacobi); pass 2 sees
+      // a Gram ~ I and keeps the order so Rt = R2 R1 stays graded.
+      const bool pivot = pass == 0 || pivot_pass2();
+      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
     }
     Scope sc(P, kStApply, st);
     // out = (in P) R11^{-1}: pivot-gathered columns, upper-triangular right factor.

@@ -283,10 +283,231 @@ void launch_blocked_t(double* H, double* J, int64_t ell, int64_t ellp, int max_s
   const int64_t tasks = batch * (nb / 2);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
   int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp), inner = 1;
+  if (const char* e = std::getenv("RSVD_JACOBI_INNER")) inner = std::max(1, std::atoi(e));
   void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &inner, &flags, &sweeps};
   RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(W * 32),
                                         args, bytes, st));
   RSVD_LAUNCH("jacobi_blocked_kernel");
+}
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Block-pair one-sided Jacobi, second generation.  Same schedule as
+// jacobi_blocked_kernel, but per task only the 2W columns of H are staged in
+// shared memory; the inner sweep's rotations are accumulated into a small
+// 2W x 2W orthogonal V (shared memory) and J's block-pair columns are
+// updated once per task, J_pair <- J_pair V, with DMMA straight from/to
+// global memory.  Column norms are computed once at staging and tracked
+// through each exact 2 x 2 rotation (alpha' = alpha - t gamma,
+// beta' = beta + t gamma), so an inner step needs one dot product.  The
+// smaller footprint (H pair + V) fits two CTAs per SM.
+template <int W>
+__global__ void __launch_bounds__(W * 32, 2)
+    jacobi_pairv_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                        int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                        int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  constexpr int NC = 2 * W;
+  constexpr int VP = NC + 4;  // V pitch (column-major V[c*VP + k]), 4 mod 16 words
+  const int pitch = ell + (ell & 1);
+  double* Hs = sm;                          // NC x pitch
+  double* Vs = sm + NC * pitch;             // NC x VP
+  double* nrm = Vs + NC * VP;               // NC column norms^2
+  int* conv = reinterpret_cast<int*>(nrm + NC);  // batch ints
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
+    for (int s = 0; s < nb - 1; ++s) {
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        const int p = rr_player(k, s, nb), q = rr_player(nb - 1 - k, s, nb);
+        const int bp = min(p, q), bq = max(p, q);
+        if (bp * W >= ell) continue;  // both blocks are padding
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = gcol(c);
+          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
+        }
+        for (int e = tid; e < NC * VP; e += blockDim.x) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) s_rot = 0;
+        __syncthreads();
+        for (int c = warp; c < NC; c += W) {
+          double a = 0.0;
+          for (int r = lane; r < ell; r += 32) a = fma(Hs[c * pitch + r], Hs[c * pitch + r], a);
+          a = warp_sum(a);
+          if (lane == 0) nrm[c] = a;
+        }
+        __syncthreads();
+        int rotated = 0;
+        for (int s2 = 0; s2 < NC - 1; ++s2) {
+          const int a0 = rr_player(warp, s2, NC), b0 = rr_player(NC - 1 - warp, s2, NC);
+          const int i = min(a0, b0), jx = max(a0, b0);
+          double* hi = Hs + i * pitch;
+          double* hj = Hs + jx * pitch;
+          double ga = 0.0;
+          for (int r = lane; r < ell; r += 32) ga = fma(hi[r], hj[r], ga);
+          ga = warp_sum(ga);
+          const double al = nrm[i], be = nrm[jx];
+          if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + tt * tt);
+            const double sn = c * tt;
+            for (int r = lane; r < ell; r += 32) {
+              const double x = hi[r], y = hj[r];
+              hi[r] = c * x - sn * y;
+              hj[r] = sn * x + c * y;
+            }
+            if (lane < NC) {
+              double* vi = Vs + i * VP;
+              double* vj = Vs + jx * VP;
+              const double x = vi[lane], y = vj[lane];
+              vi[lane] = c * x - sn * y;
+              vj[lane] = sn * x + c * y;
+            }
+            __syncwarp();
+            if (lane == 0) {
+              nrm[i] = al - tt * ga;
+              nrm[jx] = be + tt * ga;
+            }
+            rotated = 1;
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) atomicOr(&s_rot, 1);
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = gcol(c);
+          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
+        }
+        // J_pair <- J_pair V: warp per 16-row slab, A fragments straight from global.
+        __syncthreads();
+        if (s_rot) {
+          const int slabs = (ell + 15) / 16;
+          for (int sl = warp; sl < slabs; sl += W) {
+            const int r0 = sl * 16;
+            double acc[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+            constexpr int KH = NC / 8;  // k-steps per half
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              double afr[KH][2];
+#pragma unroll
+              for (int kq = 0; kq < KH; ++kq) {
+                const int gc = gcol((h2 * KH + kq) * 4 + t4);
+                const bool okc = gc < ell;
+                const int ra = r0 + g, rb = r0 + g + 8;
+                afr[kq][0] =
+                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
+                afr[kq][1] =
+                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
+              }
+#pragma unroll
+              for (int kq = 0; kq < KH; ++kq)
+#pragma unroll
+                for (int n = 0; n < NC / 8; ++n) {
+                  const double bv = Vs[(n * 8 + g) * VP + (h2 * KH + kq) * 4 + t4];
+                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                const int c = n * 8 + 2 * t4 + (qq & 1);
+                const int gc = gcol(c);
+                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
+              }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
+      }
+      grid.sync();
+    }
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const unsigned f = __ldcg(fl + i);
+      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || f == 0u);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (__ldcg(fl + i) == 0u) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int W>
+void launch_pairv_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                    unsigned* flags, int64_t batch, cudaStream_t st) {
+  constexpr int NC = 2 * W;
+  const int pitch = static_cast<int>(ell + (ell & 1));
+  const size_t bytes =
+      (static_cast<size_t>(NC) * pitch + NC * (NC + 4) + NC) * sizeof(double) +
+      batch * sizeof(int) + 16;
+  auto kern = jacobi_pairv_kernel<W>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, bytes));
+  if (per_sm < 1) throw CudaError("jacobi_pairv_kernel: does not fit on an SM");
+  int dev = 0, sms = 0;
+  RSVD_CUDA(cudaGetDevice(&dev));
+  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int nb = static_cast<int>((ell + W - 1) / W);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
+  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(W * 32),
+                                        args, bytes, st));
+  RSVD_LAUNCH("jacobi_pairv_kernel");
 }
 
 }  // namespace
@@ -297,6 +518,11 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
                            int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
   const char* env = std::getenv("RSVD_JACOBI_W");
   const int wforce = env ? std::atoi(env) : 0;
+  if (!std::getenv("RSVD_JACOBI_OLD")) {
+    if (wforce != 8 && 32 * ell * 8 <= 100 * 1024)
+      return launch_pairv_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    return launch_pairv_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  }
   if (wforce == 8 && 4 * 8 * ell * 8 <= 200 * 1024)
     launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
   else if (wforce == 4)
