@@ -22,6 +22,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rsvd_c.h"
@@ -143,6 +144,41 @@ struct Scope {
   }
 };
 
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  bool failed = false;
+};
+
+// Pinned host staging for the per-call scalars (seeds in; ranks, sweeps,
+// discarded weights out): stable addresses, so captured graphs can replay.
+struct Pinned {
+  uint64_t* seeds = nullptr;
+  int* ints = nullptr;
+  double* dbls = nullptr;
+  int64_t cap = 0;
+  bool reserve(int64_t n) {  // true when the buffers moved
+    if (n <= cap) return false;
+    release();
+    const int64_t c = std::max<int64_t>(n, 64);
+    RSVD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&seeds), sizeof(uint64_t) * c, 0));
+    RSVD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ints), sizeof(int) * 2 * c, 0));
+    RSVD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&dbls), sizeof(double) * c, 0));
+    cap = c;
+    return true;
+  }
+  void release() {
+    if (seeds) cudaFreeHost(seeds);
+    if (ints) cudaFreeHost(ints);
+    if (dbls) cudaFreeHost(dbls);
+    seeds = nullptr, ints = nullptr, dbls = nullptr, cap = 0;
+  }
+};
+
+bool graphs_enabled() {
+  static const bool v = std::getenv("RSVD_NO_GRAPH") == nullptr;
+  return v;
+}
+
 }  // namespace rsvd
 
 struct rsvd_context {
@@ -152,9 +188,15 @@ struct rsvd_context {
   std::string err;
   rsvd::Arena arena;
   rsvd::Prof prof;
+  rsvd::Pinned pin;
+  std::unordered_map<std::string, rsvd::GraphEntry> graphs;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int last_sweeps = 0;
-  std::vector<int> h_int;
-  std::vector<double> h_dbl;
+  void drop_graphs() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
 };
 
 namespace rsvd {
@@ -246,15 +288,26 @@ bool pivot_pass2() {
   return v;
 }
 
-// CholeskyQR2 of Y (rows x ellp per item) in place, Tmp as scratch.  When
-// Rt is given, also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
-void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, double* Rt,
-          uint64_t tag, cudaStream_t st) {
+bool full_orth() {
+  static const bool v = std::getenv("RSVD_FULL_ORTH") != nullptr;
+  return v;
+}
+
+// CholeskyQR of Y (rows x ellp per item): `passes` = 2 is CholeskyQR2 (the
+// result is orthonormal to working precision); 1 pass gives Q1 = (Y P) R11^-1,
+// an exact-span, well-conditioned basis (kappa(Q1)^2 - 1 = O(u kappa(Y)^2) with
+// kappa(Y) <= tau^-1/2 by the pivot floor), which is all an intermediate
+// power-iteration step consumes: the next product only sees span(Q).  The
+// result is left in *Yb (the two buffers are swapped when passes is odd).
+// When Rt is given (passes = 2), also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
+void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, double* Rt,
+          uint64_t tag, int passes, cudaStream_t st) {
   const int64_t lp = s.ellp, b = s.batch;
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
-  for (int pass = 0; pass < 2; ++pass) {
+  if (full_orth()) passes = 2;
+  for (int pass = 0; pass < passes; ++pass) {
     const MatRef& in = pass == 0 ? Y : Tm;
     const MatRef& out = pass == 0 ? Tm : Y;
     double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
@@ -286,35 +339,39 @@ void orth(const Shape& s, Buffers& B, double* Yb, double* Tmp, int64_t rows, dou
     dgemm(false, lp, lp, lp, MatRef{B.Rf2, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp},
           MatRef{Rt, lp, lp * lp}, b, B.partial, B.partial_cap, st);
   }
+  if (passes % 2 == 1) std::swap(Yb, Tmp);
 }
 
-// randomized_range (factorize.cpp:52-74): leaves Q in B.Y (m x ellp).
+// randomized_range (factorize.cpp:52-74): leaves Q (orthonormal) in B.Y.
 void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
   const int64_t lp = s.ellp, b = s.batch;
-  const MatRef X{B.X, s.n, s.n * lp}, Y{B.Y, s.m, s.m * lp};
   Prof* P = B.prof;
   {
     Scope sc(P, kStOmega, st);
-    launch_fill_gaussian(X, s.n, lp, s.ell, B.seeds, b, st);
+    launch_fill_gaussian(MatRef{B.X, s.n, s.n * lp}, s.n, lp, s.ell, B.seeds, b, st);
   }
   auto nn = [&] {
     Scope sc(P, kStApassNN, st);
-    dgemm(false, s.m, lp, s.n, A, X, Y, b, B.partial, B.partial_cap, st);
+    dgemm(false, s.m, lp, s.n, A, MatRef{B.X, s.n, s.n * lp}, MatRef{B.Y, s.m, s.m * lp}, b,
+          B.partial, B.partial_cap, st);
   };
   auto tn = [&] {
     Scope sc(P, kStApassTN, st);
-    dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
+    dgemm(true, s.n, lp, s.m, A, MatRef{B.Y, s.m, s.m * lp}, MatRef{B.X, s.n, s.n * lp}, b,
+          B.partial, B.partial_cap, st);
   };
   nn();
   uint64_t tag = kCompletionTag;
-  orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, st);
+  // Only the last orthonormalisation feeds B = Q^T A and U = Q U~; the
+  // intermediate ones need a well-conditioned basis of the span (one pass).
+  orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, s.q == 0 ? 2 : 1, st);
   tag += 2;
   for (int64_t t = 0; t < s.q; ++t) {
     tn();
-    orth(s, B, B.X, B.X2, s.n, nullptr, tag, st);
+    orth(s, B, B.X, B.X2, s.n, nullptr, tag, 1, st);
     tag += 2;
     nn();
-    orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, st);
+    orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, t + 1 == s.q ? 2 : 1, st);
     tag += 2;
   }
 }
@@ -331,7 +388,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
   }
-  orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, st);
+  orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, 2, st);
   {
     Scope sc(P, kStJacobi, st);
     launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
@@ -407,18 +464,19 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   Shape s{m, n, batch, rank, ell, round_up(ell, 32), power};
   Carver meas{nullptr};
   carve(meas, s, host, true);
+  char* const arena_before = h->arena.base;
   h->arena.reserve(meas.off + 256);
+  if (h->arena.base != arena_before) h->drop_graphs();
   Carver cv{h->arena.base};
   Buffers B = carve(cv, s, host, true);
 
-  RSVD_CUDA(cudaMemcpyAsync(B.seeds, seeds, sizeof(uint64_t) * batch, cudaMemcpyHostToDevice, st));
+  if (h->pin.reserve(batch)) h->drop_graphs();
+  std::memcpy(h->pin.seeds, seeds, sizeof(uint64_t) * batch);
   CMatRef Ad{A, lda, strideA};
   MatRef Ud{U, ldu, strideU}, Vtd{Vt, ldvt, strideVt};
   double* Sd = S;
   int64_t sS = strideS;
   if (host) {
-    for (int64_t b = 0; b < batch; ++b)
-      copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, st);
     Ad = CMatRef{B.Ah, m, m * n};
     Ud = MatRef{B.Uh, m, m * rank};
     Vtd = MatRef{B.Vth, rank, rank * n};
@@ -426,16 +484,23 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
     sS = rank;
   }
   B.prof = &h->prof;
-  range_finder(s, B, Ad, st);
-  svd_stage(s, B, Ad, Ud, Sd, sS, Vtd, st);
+  // The device part of the call: pinned seeds in, pipeline, small results out.
+  auto enqueue = [&](cudaStream_t q) {
+    RSVD_CUDA(cudaMemcpyAsync(B.seeds, h->pin.seeds, sizeof(uint64_t) * batch,
+                              cudaMemcpyHostToDevice, q));
+    Buffers Bq = B;  // range_finder swaps ping-pong buffers in its copy
+    range_finder(s, Bq, Ad, q);
+    svd_stage(s, Bq, Ad, Ud, Sd, sS, Vtd, q);
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints, B.rankF, sizeof(int) * batch, cudaMemcpyDeviceToHost, q));
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch, B.sweeps, sizeof(int) * batch,
+                              cudaMemcpyDeviceToHost, q));
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls, B.dw, sizeof(double) * batch, cudaMemcpyDeviceToHost, q));
+  };
 
-  h->h_int.resize(2 * batch);
-  h->h_dbl.resize(batch);
-  RSVD_CUDA(cudaMemcpyAsync(h->h_int.data(), B.rankF, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
-  RSVD_CUDA(cudaMemcpyAsync(h->h_int.data() + batch, B.sweeps, sizeof(int) * batch,
-                            cudaMemcpyDeviceToHost, st));
-  RSVD_CUDA(cudaMemcpyAsync(h->h_dbl.data(), B.dw, sizeof(double) * batch, cudaMemcpyDeviceToHost, st));
   if (host) {
+    for (int64_t b = 0; b < batch; ++b)
+      copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, st);
+    enqueue(st);
     for (int64_t b = 0; b < batch; ++b) {
       copy_2d(U + b * strideU, ldu, B.Uh + b * m * rank, m, m, rank, cudaMemcpyDeviceToHost, st);
       copy_2d(Vt + b * strideVt, ldvt, B.Vth + b * rank * n, rank, rank, n, cudaMemcpyDeviceToHost,
@@ -443,14 +508,61 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
       RSVD_CUDA(cudaMemcpyAsync(S + b * strideS, B.Sh + b * rank, sizeof(double) * rank,
                                 cudaMemcpyDeviceToHost, st));
     }
+    RSVD_CUDA(cudaStreamSynchronize(st));
+  } else if (!h->prof.on && graphs_enabled()) {
+    // Replay a captured CUDA graph of the whole pipeline (one host launch per
+    // call); captured on the handle's own stream and ordered after / before the
+    // caller's stream with events.
+    char keybuf[512];
+    std::snprintf(keybuf, sizeof(keybuf), "%p|%p|%p|%p|%p|%p|%p|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d",
+                  (const void*)A, (void*)U, (void*)S, (void*)Vt, (void*)h->arena.base,
+                  (void*)h->pin.seeds, (void*)h->pin.ints, (long long)m, (long long)n,
+                  (long long)lda, (long long)strideA, (long long)batch, (long long)rank,
+                  (long long)ell, (long long)ldu, (long long)strideU, (long long)strideS,
+                  (long long)ldvt * 1000003LL + strideVt, power);
+    GraphEntry& ge = h->graphs[std::string(keybuf)];
+    if (!ge.exec && !ge.failed) {
+      cudaGraph_t g = nullptr;
+      RSVD_CUDA(cudaStreamBeginCapture(h->own, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue(h->own);
+      } catch (...) {
+        cudaStreamEndCapture(h->own, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        ge.failed = true;
+      }
+      if (!ge.failed) {
+        const cudaError_t e = cudaStreamEndCapture(h->own, &g);
+        if (e != cudaSuccess || !g || cudaGraphInstantiate(&ge.exec, g, 0) != cudaSuccess) {
+          ge.failed = true;
+          ge.exec = nullptr;
+          cudaGetLastError();
+        }
+        if (g) cudaGraphDestroy(g);
+      }
+    }
+    if (ge.exec) {
+      RSVD_CUDA(cudaEventRecord(h->ev_in, st));
+      RSVD_CUDA(cudaStreamWaitEvent(h->own, h->ev_in, 0));
+      RSVD_CUDA(cudaGraphLaunch(ge.exec, h->own));
+      RSVD_CUDA(cudaEventRecord(h->ev_out, h->own));
+      RSVD_CUDA(cudaStreamWaitEvent(st, h->ev_out, 0));
+      RSVD_CUDA(cudaStreamSynchronize(h->own));
+    } else {
+      enqueue(st);
+      RSVD_CUDA(cudaStreamSynchronize(st));
+    }
+  } else {
+    enqueue(st);
+    RSVD_CUDA(cudaStreamSynchronize(st));
   }
-  RSVD_CUDA(cudaStreamSynchronize(st));
   if (h->prof.on) h->prof.collect();
   h->last_sweeps = 0;
   for (int64_t b = 0; b < batch; ++b) {
-    out_rank[b] = h->h_int[b];
-    dw[b] = h->h_dbl[b];
-    h->last_sweeps = std::max(h->last_sweeps, h->h_int[batch + b]);
+    out_rank[b] = h->pin.ints[b];
+    dw[b] = h->pin.dbls[b];
+    h->last_sweeps = std::max(h->last_sweeps, h->pin.ints[batch + b]);
   }
 }
 
@@ -587,6 +699,8 @@ int rsvd_create(rsvd_handle* out, int device) {
       throw rsvd::CudaError("rsvd_create: this build targets sm_100a (B200); device is sm_" +
                             std::to_string(prop.major * 10 + prop.minor));
     RSVD_CUDA(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking));
+    RSVD_CUDA(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    RSVD_CUDA(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
     h->stream = h->own;
   });
   if (rc != RSVD_OK) {
@@ -627,6 +741,10 @@ int rsvd_destroy(rsvd_handle h) {
   if (!h) return RSVD_ERR_INVALID;
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->prof.destroy();
+  h->drop_graphs();
+  h->pin.release();
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   h->arena.release();
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
@@ -644,6 +762,7 @@ int rsvd_set_stream(rsvd_handle h, void* stream) {
 int rsvd_trim(rsvd_handle h) {
   return rsvd::guarded(h, [&] {
     RSVD_CUDA(cudaStreamSynchronize(h->stream));
+    h->drop_graphs();
     h->arena.release();
   });
 }
