@@ -81,6 +81,11 @@ struct GemmOpts {
 void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
               int64_t batch, double* partial, int64_t partial_capacity, const GemmOpts& opt,
               cudaStream_t st);
+// gemm_tma.cu — TMA/mbarrier-fed variant of the 128 x 96 tile (no column map);
+// returns false (nothing launched) when the operands do not qualify.
+bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
+               int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
+               bool b_upper, cudaStream_t st);
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
 
 // chol.cu — pivoted / plain Cholesky of SPD Grams (ell x ell, ld ell).

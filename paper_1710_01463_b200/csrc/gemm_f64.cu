@@ -306,11 +306,12 @@ struct Choice {
 Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   Choice c{128, 64, 1, 0};
   // Prefer a BN that covers N with little padding waste.
-  const int64_t w64 = round_up(N, 64), w96 = round_up(N, 96), w32 = round_up(N, 32);
+  // The 128 x 96 tile (TMA path) is the efficient one: take it unless 64-wide
+  // tiles cover N with strictly less padding.
+  const int64_t w64 = round_up(N, 64), w96 = round_up(N, 96);
   if (N <= 32) c.bn = 32;
-  else if (w96 < w64 && w96 <= w32 + 16) c.bn = 96;
-  else if (w64 <= w32 + 16) c.bn = 64;
-  else c.bn = 32;
+  else if (N <= 64) c.bn = 64;
+  else c.bn = (w96 <= w64) ? 96 : 64;
   c.bm = (M <= 64) ? 64 : 128;
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
   const int64_t target = 2 * kNumSMs;  // two resident CTAs per SM
@@ -409,7 +410,11 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool vec2 = aligned16(A.base) && aligned16(B.base) && (A.ld % 2 == 0) &&
                     (B.ld % 2 == 0) && (A.stride % 2 == 0) && (B.stride % 2 == 0) &&
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
-  if (trans_a) {
+  const bool tma_done = !a.colmapA && c.bm == 128 && c.bn == 96 &&
+                        dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
+                                  c.kps, a.c_upper != 0, a.b_upper != 0, st);
+  if (tma_done) {
+  } else if (trans_a) {
     if (vec2) dispatch<true, 2>(c, a, st);
     else dispatch<true, 1>(c, a, st);
   } else {
