@@ -311,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
                          "unit": "TFLOP/s",
                          "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
                          "traffic": traffic,
-                         "kernel": "dgemm_kernel A-pass (Y=A X / Z=A^T Y), batched over the step",
+                         "kernel": "dgemm_tma_kernel A-pass (Y=A X / Z=A^T Y; TMA-fed DMMA), batched over the step",
                          "algorithmic_flops_per_launch": ap_flops_per_launch,
                          "peak_source": FP64_PEAK_SOURCE,
                          "apass_share_of_step": ap_ms / prof_steps / step_ms_prof},
