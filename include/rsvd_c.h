@@ -91,6 +91,29 @@ int rsvd_f64_batched(rsvd_handle handle, int64_t batch, const double* A, int64_t
                      int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
                      int64_t* out_rank, double* discarded_weight, int flags);
 
+/* Row-sharded rsvd of ONE large matrix over P ranks (C3/C5): this
+ * rank holds rows [row_offset, row_offset + m_local) of the m_global x n matrix
+ * A (A_local, ld lda) and receives the matching rows of U (U_local, ldu);
+ * S and Vt (replicated) and out_rank / discarded_weight are identical on every
+ * rank.  The only exchanges are sum all-reduces of the m-side l x l Grams and
+ * of the n x l panels A^T Q, through the communicator attached to the handle:
+ *   rsvd_attach_nccl   one process per GPU, ncclAllReduce on the handle stream;
+ *   rsvd_attach_group  in-process ranks (one host thread + handle each), host
+ *                      barriers only — P ranks may share one GPU.
+ * Validation follows rsvd with m = m_global. */
+typedef struct rsvd_group_s* rsvd_group;
+int rsvd_group_create(rsvd_group* group, int nranks);
+int rsvd_group_destroy(rsvd_group group);
+int rsvd_attach_group(rsvd_handle handle, rsvd_group group, int rank);
+int rsvd_nccl_unique_id(unsigned char* id128);
+int rsvd_attach_nccl(rsvd_handle handle, int nranks, int rank, const unsigned char* id128);
+int rsvd_detach(rsvd_handle handle);
+int rsvd_f64_rowsharded(rsvd_handle handle, const double* A_local, int64_t m_local, int64_t n,
+                        int64_t lda, int64_t m_global, int64_t row_offset, int64_t rank,
+                        int64_t oversample, int power, uint64_t seed, double* U_local,
+                        int64_t ldu, double* S, double* Vt, int64_t ldvt, int64_t* out_rank,
+                        double* discarded_weight, int flags);
+
 /* rlftn::randomized_range<double>(a, ell, power, seed) (factorize.hpp:56-57,
  * factorize.cpp:52-74): Q (m x ell, ldq >= m) with orthonormal columns
  * spanning the sampled dominant range. */

@@ -55,6 +55,18 @@ SIGNATURES = {
         _c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_int, ctypes.POINTER(_c_i64), ctypes.c_char_p,
                  _c_i64]
     ),
+    "rsvd_group_create": (_c_int, [ctypes.POINTER(_c_vp), _c_int]),
+    "rsvd_group_destroy": (_c_int, [_c_vp]),
+    "rsvd_attach_group": (_c_int, [_c_vp, _c_vp, _c_int]),
+    "rsvd_nccl_unique_id": (_c_int, [ctypes.c_char_p]),
+    "rsvd_attach_nccl": (_c_int, [_c_vp, _c_int, _c_int, ctypes.c_char_p]),
+    "rsvd_detach": (_c_int, [_c_vp]),
+    "rsvd_f64_rowsharded": (
+        _c_int,
+        [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_u64,
+         _c_dp, _c_i64, _c_dp, _c_dp, _c_i64, ctypes.POINTER(_c_i64),
+         ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
     "rsvd_kernel_launches": (_c_u64, []),
     "rsvd_profile_enable": (_c_int, [_c_vp, _c_int]),
     "rsvd_profile_read": (_c_int, [_c_vp, ctypes.POINTER(ctypes.c_double),

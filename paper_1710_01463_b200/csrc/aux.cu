@@ -23,19 +23,22 @@ __device__ __forceinline__ double uniform_from(uint64_t w) {
 // orthonormalises them against the retained span.  The reference's Householder
 // Q completes such bases "arbitrarily" (lapack.hpp:18-20); this completion is
 // arbitrary too, but deterministic per seed.
+// Rows are indexed globally (row_offset + i of rows_global) so a row-sharded
+// basis gets the same completion as the unsharded one.
 __global__ void complete_basis_kernel(double* __restrict__ Q, int64_t ld, int64_t stride,
                                       int64_t rows, int64_t ell, const int* __restrict__ rank,
-                                      const uint64_t* __restrict__ seeds, uint64_t tag) {
+                                      const uint64_t* __restrict__ seeds, uint64_t tag,
+                                      int64_t row_offset, int64_t rows_global) {
   const int64_t b = blockIdx.y;
   const int r = rank[b];
   if (r >= ell) return;
   const uint64_t key = seeds[b] ^ mix64(tag);
-  const double scale = 1.0 / sqrt(static_cast<double>(rows));
+  const double scale = 1.0 / sqrt(static_cast<double>(rows_global));
   const int64_t total = rows * (ell - r);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = r + e / rows, i = e % rows;
-    const uint64_t idx = static_cast<uint64_t>(i + j * rows);
+    const uint64_t idx = static_cast<uint64_t>(row_offset + i + j * rows_global);
     const double u1 = uniform_from(mix64(key + (2 * idx + 1) * 0x9e3779b97f4a7c15ull));
     const double u2 = uniform_from(mix64(key + (2 * idx + 2) * 0x9e3779b97f4a7c15ull));
     const double z = sqrt(-2.0 * log(u1)) * cos((2.0 * 3.141592653589793) * u2);
@@ -246,11 +249,11 @@ unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
 
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
                            const uint64_t* seeds_dev, uint64_t tag, int64_t batch,
-                           cudaStream_t st) {
+                           int64_t row_offset, int64_t rows_global, cudaStream_t st) {
   if (batch <= 0 || rows <= 0) return;
   dim3 grid(grid1(rows * ell, 256, 2), static_cast<unsigned>(batch));
   complete_basis_kernel<<<grid, 256, 0, st>>>(Q.base, Q.ld, Q.stride, rows, ell, rank, seeds_dev,
-                                              tag);
+                                              tag, row_offset, rows_global);
   RSVD_LAUNCH("complete_basis_kernel");
 }
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 
@@ -108,7 +109,22 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
 // aux.cu
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
                            const uint64_t* seeds_dev, uint64_t tag, int64_t batch,
-                           cudaStream_t st);
+                           int64_t row_offset, int64_t rows_global, cudaStream_t st);
+
+// Sum all-reduce across the ranks of a row-sharded factorization (NCCL or an
+// in-process group); stream-ordered on `st`.
+struct Reducer {
+  virtual ~Reducer() = default;
+  virtual void allreduce_sum(double* buf, int64_t count, cudaStream_t st) = 0;
+  virtual bool capturable() const = 0;  // safe inside CUDA-graph capture
+};
+// shard.cu
+struct Group;
+Group* group_create(int nranks);
+void group_destroy(Group* g);
+std::unique_ptr<Reducer> make_group_reducer(Group* g, int rank);
+std::unique_ptr<Reducer> make_nccl_reducer(int nranks, int rank, const unsigned char* id);
+void nccl_unique_id(unsigned char* out);
 void launch_transpose(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_t batch,
                       cudaStream_t st);
 void launch_set_identity(MatRef out, int64_t n, int64_t batch, cudaStream_t st);

@@ -191,6 +191,7 @@ struct rsvd_context {
   rsvd::Pinned pin;
   std::unordered_map<std::string, rsvd::GraphEntry> graphs;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::unique_ptr<rsvd::Reducer> red;  // row-sharded calls (NCCL or in-process group)
   int last_sweeps = 0;
   void drop_graphs() {
     for (auto& kv : graphs)
@@ -204,6 +205,9 @@ namespace {
 
 struct Shape {
   int64_t m, n, batch, k, ell, ellp, q;
+  // Row sharding: this rank holds rows [row_off, row_off + m) of m_global.
+  int64_t m_global = 0, row_off = 0;
+  int64_t mg() const { return m_global > 0 ? m_global : m; }
 };
 
 struct Buffers {
@@ -220,6 +224,7 @@ struct Buffers {
   // staging for host-pointer calls
   double *Ah, *Uh, *Vth, *Sh;
   Prof* prof;
+  Reducer* red;  // non-null for a row-sharded call
 };
 
 int64_t partial_need(const Shape& s) {
@@ -300,9 +305,13 @@ bool full_orth() {
 // power-iteration step consumes: the next product only sees span(Q).  The
 // result is left in *Yb (the two buffers are swapped when passes is odd).
 // When Rt is given (passes = 2), also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
+// m_side: Y has the (possibly row-sharded) m rows of A; its Gram is then
+// all-reduced across ranks and the completion uses global row indices.
 void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, double* Rt,
-          uint64_t tag, int passes, cudaStream_t st) {
+          uint64_t tag, int passes, bool m_side, cudaStream_t st) {
   const int64_t lp = s.ellp, b = s.batch;
+  const bool sharded = m_side && B.red;
+  const int64_t row_off = m_side ? s.row_off : 0, rows_global = m_side ? s.mg() : rows;
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
@@ -317,6 +326,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       GemmOpts sym;
       sym.c_upper = true;
       dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
+      if (sharded) B.red->allreduce_sum(B.G, b * lp * lp, st);  // G = sum_p Y_p^T Y_p
     }
     {
       Scope sc(P, kStChol, st);
@@ -332,7 +342,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     tri.colmap_stride = lp;
     tri.b_upper = true;
     dgemm_ex(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, tri, st);
-    launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, st);
+    launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global, st);
   }
   if (Rt) {
     Scope sc(P, kStApply, st);
@@ -359,19 +369,20 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, MatRef{B.Y, s.m, s.m * lp}, MatRef{B.X, s.n, s.n * lp}, b,
           B.partial, B.partial_cap, st);
+    if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // Z = sum_p A_p^T Q_p
   };
   nn();
   uint64_t tag = kCompletionTag;
   // Only the last orthonormalisation feeds B = Q^T A and U = Q U~; the
   // intermediate ones need a well-conditioned basis of the span (one pass).
-  orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, s.q == 0 ? 2 : 1, st);
+  orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, s.q == 0 ? 2 : 1, true, st);
   tag += 2;
   for (int64_t t = 0; t < s.q; ++t) {
     tn();
-    orth(s, B, B.X, B.X2, s.n, nullptr, tag, 1, st);
+    orth(s, B, B.X, B.X2, s.n, nullptr, tag, 1, false, st);
     tag += 2;
     nn();
-    orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, t + 1 == s.q ? 2 : 1, st);
+    orth(s, B, B.Y, B.Y2, s.m, nullptr, tag, t + 1 == s.q ? 2 : 1, true, st);
     tag += 2;
   }
 }
@@ -387,15 +398,16 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   {
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
+    if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
   }
-  orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, 2, st);
+  orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, 2, false, st);
   {
     Scope sc(P, kStJacobi, st);
     launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
     launch_jacobi(B.H, B.Jm, s.ell, lp, kMaxSweeps, B.sweeps, B.jflags, b, st);
   }
   Scope sc(P, kStLift, st);
-  launch_finalize_spectrum(B.H, lp, s.ell, k, s.m, s.n, B.sig, B.permS, B.rankF, B.dw, b, st);
+  launch_finalize_spectrum(B.H, lp, s.ell, k, s.mg(), s.n, B.sig, B.permS, B.rankF, B.dw, b, st);
   // U~ = W Sigma^{-1} restricted to the kept columns, then U = Q U~.
   launch_gather_scale_columns(B.H, lp, lp * lp, B.permS, lp, B.sig, k, B.rankF, lp, k, B.Ut, lp,
                               lp * k, b, st);
@@ -448,10 +460,16 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
                        int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
                        const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
                        int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
-                       int64_t* out_rank, double* dw, int flags) {
+                       int64_t* out_rank, double* dw, int flags, int64_t m_global = 0,
+                       int64_t row_off = 0, bool sharded = false) {
   check_flags(flags);
   int64_t ell = 0;
-  validate_rsvd(m, n, rank, oversample, power, ell);
+  validate_rsvd(sharded ? m_global : m, n, rank, oversample, power, ell);
+  if (sharded) {
+    if (!h->red) throw InvalidArgument("rsvd_rowsharded: no group / communicator attached");
+    if (m < 1 || row_off < 0 || row_off + m > m_global)
+      throw InvalidArgument("rsvd_rowsharded: local rows out of range");
+  }
   if (batch < 0) throw InvalidArgument("rsvd: batch must be >= 0");
   if (batch == 0) return;
   if (!A || !U || !S || !Vt || !seeds || !out_rank || !dw)
@@ -462,6 +480,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   cudaStream_t st = h->stream;
 
   Shape s{m, n, batch, rank, ell, round_up(ell, 32), power};
+  if (sharded) s.m_global = m_global, s.row_off = row_off;
   Carver meas{nullptr};
   carve(meas, s, host, true);
   char* const arena_before = h->arena.base;
@@ -484,6 +503,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
     sS = rank;
   }
   B.prof = &h->prof;
+  B.red = sharded ? h->red.get() : nullptr;
   // The device part of the call: pinned seeds in, pipeline, small results out.
   auto enqueue = [&](cudaStream_t q) {
     RSVD_CUDA(cudaMemcpyAsync(B.seeds, h->pin.seeds, sizeof(uint64_t) * batch,
@@ -509,17 +529,19 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
                                 cudaMemcpyDeviceToHost, st));
     }
     RSVD_CUDA(cudaStreamSynchronize(st));
-  } else if (!h->prof.on && graphs_enabled()) {
+  } else if (!h->prof.on && graphs_enabled() && (!B.red || B.red->capturable())) {
     // Replay a captured CUDA graph of the whole pipeline (one host launch per
     // call); captured on the handle's own stream and ordered after / before the
     // caller's stream with events.
     char keybuf[512];
-    std::snprintf(keybuf, sizeof(keybuf), "%p|%p|%p|%p|%p|%p|%p|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d",
+    std::snprintf(keybuf, sizeof(keybuf),
+                  "%p|%p|%p|%p|%p|%p|%p|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d|%p|%lld|%lld",
                   (const void*)A, (void*)U, (void*)S, (void*)Vt, (void*)h->arena.base,
                   (void*)h->pin.seeds, (void*)h->pin.ints, (long long)m, (long long)n,
                   (long long)lda, (long long)strideA, (long long)batch, (long long)rank,
                   (long long)ell, (long long)ldu, (long long)strideU, (long long)strideS,
-                  (long long)ldvt * 1000003LL + strideVt, power);
+                  (long long)ldvt * 1000003LL + strideVt, power, (void*)B.red,
+                  (long long)s.m_global, (long long)s.row_off);
     GraphEntry& ge = h->graphs[std::string(keybuf)];
     if (!ge.exec && !ge.failed) {
       cudaGraph_t g = nullptr;
@@ -754,9 +776,11 @@ int rsvd_destroy(rsvd_handle h) {
 const char* rsvd_last_error(rsvd_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 int rsvd_set_stream(rsvd_handle h, void* stream) {
-  return rsvd::guarded(h, [&] {
-    h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own;
-  });
+  // Does not touch the last-error string: callers restore the stream after a
+  // failed call and still read its message.
+  if (!h) return RSVD_ERR_INVALID;
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own;
+  return RSVD_OK;
 }
 
 int rsvd_trim(rsvd_handle h) {
@@ -805,6 +829,68 @@ int rsvd_f64_batched(rsvd_handle h, int64_t batch, const double* A, int64_t m, i
     rsvd::rsvd_batched_impl(h, batch, A, m, n, lda, strideA, rank, oversample, power, seeds, U,
                             ldu, strideU, S, strideS, Vt, ldvt, strideVt, out_rank,
                             discarded_weight, flags);
+  });
+}
+
+int rsvd_group_create(rsvd_group* g, int nranks) {
+  if (!g) return RSVD_ERR_INVALID;
+  try {
+    *g = reinterpret_cast<rsvd_group>(rsvd::group_create(nranks));
+    return RSVD_OK;
+  } catch (...) {
+    *g = nullptr;
+    return RSVD_ERR_INVALID;
+  }
+}
+
+int rsvd_group_destroy(rsvd_group g) {
+  rsvd::group_destroy(reinterpret_cast<rsvd::Group*>(g));
+  return RSVD_OK;
+}
+
+int rsvd_attach_group(rsvd_handle h, rsvd_group g, int rank) {
+  return rsvd::guarded(h, [&] {
+    h->drop_graphs();
+    h->red = rsvd::make_group_reducer(reinterpret_cast<rsvd::Group*>(g), rank);
+  });
+}
+
+int rsvd_nccl_unique_id(unsigned char* id128) {
+  if (!id128) return RSVD_ERR_INVALID;
+  try {
+    rsvd::nccl_unique_id(id128);
+    return RSVD_OK;
+  } catch (...) {
+    return RSVD_ERR_CUDA;
+  }
+}
+
+int rsvd_attach_nccl(rsvd_handle h, int nranks, int rank, const unsigned char* id128) {
+  return rsvd::guarded(h, [&] {
+    if (!id128 || nranks < 1 || rank < 0 || rank >= nranks)
+      throw rsvd::InvalidArgument("rsvd_attach_nccl: bad arguments");
+    RSVD_CUDA(cudaSetDevice(h->device));
+    h->drop_graphs();
+    h->red = rsvd::make_nccl_reducer(nranks, rank, id128);
+  });
+}
+
+int rsvd_detach(rsvd_handle h) {
+  return rsvd::guarded(h, [&] {
+    h->drop_graphs();
+    h->red.reset();
+  });
+}
+
+int rsvd_f64_rowsharded(rsvd_handle h, const double* A_local, int64_t m_local, int64_t n,
+                        int64_t lda, int64_t m_global, int64_t row_offset, int64_t rank,
+                        int64_t oversample, int power, uint64_t seed, double* U_local, int64_t ldu,
+                        double* S, double* Vt, int64_t ldvt, int64_t* out_rank,
+                        double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::rsvd_batched_impl(h, 1, A_local, m_local, n, lda, 0, rank, oversample, power, &seed,
+                            U_local, ldu, 0, S, 0, Vt, ldvt, 0, out_rank, discarded_weight, flags,
+                            m_global, row_offset, true);
   });
 }
 
