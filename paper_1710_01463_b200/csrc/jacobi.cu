@@ -510,6 +510,239 @@ void launch_pairv_t(double* H, double* J, int64_t ell, int64_t ellp, int max_swe
   RSVD_LAUNCH("jacobi_pairv_kernel");
 }
 
+// Block-cyclic one-sided Jacobi (third generation).  Columns in blocks of 16;
+// one outer sweep = one "diagonal" phase (every block rotates its own 120
+// intra-block pairs, 15 steps of 8 disjoint pairs per block) + nb-1 phases in
+// which round-robin block pairs (p, q) rotate their 256 inter-block pairs
+// (16 steps, warp w pairs column p_w with q_{(w+t) mod 16}).  Every column pair
+// is rotated exactly once per sweep — a cyclic-by-blocks sweep — instead of
+// re-rotating intra-block pairs in every phase.  Within a step a warp keeps its
+// two columns in registers (R = ceil(l/32) rows per lane) from the dot
+// product through the update; norms are tracked through the exact 2 x 2
+// rotation; rotations accumulate into V and J_pair <- J_pair V runs once per
+// task on DMMA straight from global memory.
+template <int R, int MINB>
+__global__ void __launch_bounds__(512, MINB)
+    jacobi_cyc_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                      int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int W = 16, NC = 32, VP = NC + 4;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  const int pitch = 32 * R;
+  double* Hs = sm;                  // NC x pitch
+  double* Vs = sm + NC * pitch;     // NC x VP, column-major V[c*VP + k]
+  double* nrm = Vs + NC * VP;       // NC
+  int* conv = reinterpret_cast<int*>(nrm + NC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
+          bp = min(p, q), bq = max(p, q);
+        }
+        if (bp * W >= ell) continue;  // both blocks are padding
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = gcol(c);
+          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
+        }
+        for (int e = tid; e < NC * VP; e += blockDim.x) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) s_rot = 0;
+        __syncthreads();
+        for (int c = warp; c < NC; c += W) {
+          double a = 0.0;
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            const double x = Hs[c * pitch + lane + 32 * u];
+            a = fma(x, x, a);
+          }
+          a = warp_sum(a);
+          if (lane == 0) nrm[c] = a;
+        }
+        __syncthreads();
+        int rotated = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int i, jx;
+          if (diag) {
+            const int blk = warp >> 3, pi = warp & 7;
+            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
+            i = blk * 16 + min(a0, b0);
+            jx = blk * 16 + max(a0, b0);
+          } else {
+            i = warp;
+            jx = 16 + ((warp + s2) & 15);
+          }
+          double* hi = Hs + i * pitch;
+          double* hj = Hs + jx * pitch;
+          double xi[R], xj[R];
+          double ga = 0.0;
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            xi[u] = hi[lane + 32 * u];
+            xj[u] = hj[lane + 32 * u];
+            ga = fma(xi[u], xj[u], ga);
+          }
+          ga = warp_sum(ga);
+          const double al = nrm[i], be = nrm[jx];
+          if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + tt * tt);
+            const double sn = c * tt;
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+              hi[lane + 32 * u] = c * xi[u] - sn * xj[u];
+              hj[lane + 32 * u] = sn * xi[u] + c * xj[u];
+            }
+            {
+              double* vi = Vs + i * VP;
+              double* vj = Vs + jx * VP;
+              const double x = vi[lane], y = vj[lane];
+              vi[lane] = c * x - sn * y;
+              vj[lane] = sn * x + c * y;
+            }
+            __syncwarp();
+            if (lane == 0) {
+              nrm[i] = al - tt * ga;
+              nrm[jx] = be + tt * ga;
+            }
+            rotated = 1;
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) atomicOr(&s_rot, 1);
+        for (int e = tid; e < NC * pitch; e += blockDim.x) {
+          const int c = e / pitch, r = e - c * pitch;
+          const int gc = gcol(c);
+          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
+        }
+        __syncthreads();
+        if (s_rot) {  // J_pair <- J_pair V (warp per 16-row slab, DMMA)
+          const int slabs = (ell + 15) / 16;
+          for (int sl = warp; sl < slabs; sl += W) {
+            const int r0 = sl * 16;
+            double acc[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              double afr[4][2];
+#pragma unroll
+              for (int kq = 0; kq < 4; ++kq) {
+                const int gc = gcol((h2 * 4 + kq) * 4 + t4);
+                const bool okc = gc < ell;
+                const int ra = r0 + g, rb = r0 + g + 8;
+                afr[kq][0] =
+                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
+                afr[kq][1] =
+                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
+              }
+#pragma unroll
+              for (int kq = 0; kq < 4; ++kq)
+#pragma unroll
+                for (int n = 0; n < NC / 8; ++n) {
+                  const double bv = Vs[(n * 8 + g) * VP + (h2 * 4 + kq) * 4 + t4];
+                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                const int c = n * 8 + 2 * t4 + (qq & 1);
+                const int gc = gcol(c);
+                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
+              }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
+      }
+      grid.sync();
+    }
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const unsigned f = __ldcg(fl + i);
+      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || f == 0u);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (__ldcg(fl + i) == 0u) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int R, int MINB>
+void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                  unsigned* flags, int64_t batch, cudaStream_t st) {
+  const size_t bytes = (static_cast<size_t>(32) * 32 * R + 32 * 36 + 32) * sizeof(double) +
+                       batch * sizeof(int) + 16;
+  auto kern = jacobi_cyc_kernel<R, MINB>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
+  if (per_sm < 1) throw CudaError("jacobi_cyc_kernel: does not fit on an SM");
+  int dev = 0, sms = 0;
+  RSVD_CUDA(cudaGetDevice(&dev));
+  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
+  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512),
+                                        args, bytes, st));
+  RSVD_LAUNCH("jacobi_cyc_kernel");
+}
+
 }  // namespace
 
 int64_t jacobi_flag_elems(int64_t batch) { return 3 * batch; }
@@ -518,6 +751,13 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
                            int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
   const char* env = std::getenv("RSVD_JACOBI_W");
   const int wforce = env ? std::atoi(env) : 0;
+  if (!std::getenv("RSVD_JACOBI_OLD") && !std::getenv("RSVD_JACOBI_PAIRV")) {
+    if (ell <= 32 * 9 && std::getenv("RSVD_JACOBI_MINB1"))
+      return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    if (ell <= 32 * 9) return launch_cyc_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    if (ell <= 32 * 18)
+      return launch_cyc_t<18, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  }
   if (!std::getenv("RSVD_JACOBI_OLD")) {
     if (wforce != 8 && 32 * ell * 8 <= 100 * 1024)
       return launch_pairv_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
