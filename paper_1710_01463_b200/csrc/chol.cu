@@ -28,6 +28,7 @@
 //   * R rows are written in original column order, which is Rfull directly;
 //   * R11^{-1} by a blocked DMMA inverse (blocked_upper_inverse below).
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -96,17 +97,26 @@ __device__ void blocked_upper_inverse(const double* __restrict__ R, double* __re
           for (int n = 0; n < 4; ++n)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[a][n][q] = 0.0;
-        for (int k0 = oI + 32; k0 < oJ + 32; k0 += 4) {
-          const double* rc = R + static_cast<int64_t>(k0 + t) * ld + oI + g;
-          const double a00 = rc[0], a01 = rc[8], a10 = rc[16], a11 = rc[24];
-          double bf[4];
+        // K runs over whole 32-blocks; operands are fetched 16 k at a time
+        // (all loads issued before the MMAs) to overlap the L2 latency.
+        for (int kc = oI + 32; kc < oJ + 32; kc += 16) {
+          double af[4][4], bf[4][4];
 #pragma unroll
-          for (int n = 0; n < 4; ++n) bf[n] = X[(k0 + t) + static_cast<int64_t>(oJ + n * 8 + g) * ld];
+          for (int s4 = 0; s4 < 4; ++s4) {
+            const int k0 = kc + s4 * 4;
+            const double* rc = R + static_cast<int64_t>(k0 + t) * ld + oI + g;
+            af[s4][0] = rc[0], af[s4][1] = rc[8], af[s4][2] = rc[16], af[s4][3] = rc[24];
 #pragma unroll
-          for (int n = 0; n < 4; ++n) {
-            dmma_16x8x4(acc[0][n], a00, a01, bf[n]);
-            dmma_16x8x4(acc[1][n], a10, a11, bf[n]);
+            for (int n = 0; n < 4; ++n)
+              bf[s4][n] = X[(k0 + t) + static_cast<int64_t>(oJ + n * 8 + g) * ld];
           }
+#pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+              dmma_16x8x4(acc[0][n], af[s4][0], af[s4][1], bf[s4][n]);
+              dmma_16x8x4(acc[1][n], af[s4][2], af[s4][3], bf[s4][n]);
+            }
         }
         // S (row k, col c) = acc
 #pragma unroll
@@ -352,6 +362,244 @@ __global__ void __launch_bounds__(kCholThreads)
   if (tid == 0) rank_out[b] = r;
 }
 
+// One warp factors the 32 x 32 diagonal block whose current values lane c
+// holds in a[0..31] (column c), writes R_JJ (upper) to W and Rd and its
+// inverse to Dt; returns the in-block breakdown index (32 = none).  Columns
+// at or beyond `ell` arrive as identity columns.
+__device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld, int ell, int o,
+                                 double thresh, double* Rd, double* Dt, int lane) {
+  int brk = 32;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double akk = __shfl_sync(0xffffffffu, a[k], k);
+    if (brk == 32 && o + k < ell && !(akk > thresh)) brk = k;
+    if (brk == 32) {
+      const double rkk = sqrt(akk);
+      const double rk = (lane == k) ? rkk : (lane > k ? a[k] / rkk : 0.0);
+      a[k] = rk;
+#pragma unroll
+      for (int i = k + 1; i < 32; ++i) {
+        const double rki = __shfl_sync(0xffffffffu, rk, i);
+        if (lane > k) a[i] -= rki * rk;
+      }
+    } else {
+      a[k] = (lane == k) ? 1.0 : 0.0;  // beyond the breakdown: keep R_JJ invertible
+    }
+  }
+  const bool colok = o + lane < ell;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double v = (k <= lane) ? a[k] : 0.0;
+    Rd[k * kInvPitch + lane] = v;
+    if (colok && o + k < ell && k <= lane) W[(o + k) + static_cast<int64_t>(o + lane) * ld] = v;
+  }
+  __syncwarp();
+  double x[32];
+#pragma unroll
+  for (int i = 31; i >= 0; --i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) s = fma(Rd[i * kInvPitch + k], x[k], s);
+    const double rii = Rd[i * kInvPitch + i];
+    x[i] = (i == lane) ? 1.0 / rii : ((i < lane) ? -s / rii : 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Dt[i * kInvPitch + lane] = x[i];
+  __syncwarp();
+  return brk;
+}
+
+// Unpivoted blocked Cholesky with breakdown detection (same outputs as
+// pchol_kernel with the identity permutation).  Right-looking over 32-column
+// blocks: one warp factors the 32 x 32 diagonal block in registers (lane =
+// column, row k broadcast by shuffles) and inverts it; the block row of R
+// right of it is R_JJ^{-T} A_J,right on DMMA; the trailing matrix takes a
+// rank-32 DMMA update in place.  A pivot <= tau * max(diag G) stops the
+// factorization at the numerical rank r (the remaining columns are completed
+// by the caller), which for the generic bases of the power iteration (Gaussian
+// mixing) coincides with the pivoted rank.  Used wherever the pivot order is
+// not consumed: every CholeskyQR pass except the first pass on B^T.
+__global__ void __launch_bounds__(kCholThreads)
+    uchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
+                 double* __restrict__ scratch, int* __restrict__ rank_out,
+                 int* __restrict__ perm_out, int ell, int ellp, double tau) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double s_thresh;
+  __shared__ int s_r;
+  const int64_t b = blockIdx.x;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const int ld = ellp;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rp_pitch = ellp + 20;
+  const int64_t big = max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
+  double* Rp = sm;                  // 32 x rp_pitch: row block J of R, columns >= o + 32
+  double* Rd = sm + big;            // R_JJ,        Rd[i * 36 + c]
+  double* Dt = Rd + 32 * kInvPitch;  // R_JJ^{-1},  Dt[i * 36 + c]
+  double* W = G + b * sq;
+  double* C11 = scratch + b * 2 * sq;
+  double* X = C11 + sq;
+
+  if (warp == 0) {
+    double v = 0.0;
+    for (int i = lane; i < ell; i += 32) v = fmax(v, W[i + static_cast<int64_t>(i) * ld]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) {
+      s_thresh = tau * v;
+      s_r = (v > 0.0) ? ell : 0;
+    }
+  }
+  __syncthreads();
+  const double thresh = s_thresh;
+  int r = s_r;
+  const int nbk_all = (ell + 31) / 32;
+  for (int e = tid; e < PB * rp_pitch; e += blockDim.x) Rp[e] = 0.0;
+  __syncthreads();
+  // Prologue: the first diagonal block.
+  if (warp == 0 && r == ell) {
+    double a[32];
+    const bool colok = lane < ell;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      a[i] = (colok && i < ell) ? W[i + static_cast<int64_t>(lane) * ld] : (i == lane ? 1.0 : 0.0);
+    const int brk = factor_diag_block(a, W, ld, ell, 0, thresh, Rd, Dt, lane);
+    if (lane == 0 && brk < 32) s_r = brk;
+  }
+  __syncthreads();
+  r = s_r;
+  // Iteration J: panel J (all warps); then, with lookahead, warp 0 updates and
+  // factors diagonal block J+1 while warps 1.. apply the rest of the rank-32
+  // trailing update.
+  for (int J = 0; J < nbk_all; ++J) {
+    const int o = J * 32;
+    // Block row J of R right of the diagonal: X = R_JJ^{-T} A_J,chunk (DMMA).
+    const int nchunk = (ell - o - 32 + 31) / 32;
+    for (int ch = warp; ch < nchunk; ch += kCholWarps) {
+      const int cs = o + 32 + ch * 32;
+      double acc[2][4][4];
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[a2][n][q] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < 32; k0 += 4) {
+        // A operand (R_JJ^{-T})[i][k] = Rinv[k][i]
+        const double a00 = Dt[(k0 + t) * kInvPitch + g], a01 = Dt[(k0 + t) * kInvPitch + g + 8];
+        const double a10 = Dt[(k0 + t) * kInvPitch + g + 16],
+                     a11 = Dt[(k0 + t) * kInvPitch + g + 24];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const int c = cs + n * 8 + g;
+          const double bv = (c < ell) ? W[(o + k0 + t) + static_cast<int64_t>(c) * ld] : 0.0;
+          dmma_16x8x4(acc[0][n], a00, a01, bv);
+          dmma_16x8x4(acc[1][n], a10, a11, bv);
+        }
+      }
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = a2 * 16 + g + ((q & 2) ? 8 : 0);
+            const int c = cs + n * 8 + 2 * t + (q & 1);
+            if (c < ell) {
+              Rp[i * rp_pitch + c] = acc[a2][n][q];
+              W[(o + i) + static_cast<int64_t>(c) * ld] = acc[a2][n][q];
+            }
+          }
+    }
+    __syncthreads();
+    if (r < ell) break;  // rank found: the trailing matrix is not needed
+    const int j1 = o + 32;
+    if (j1 >= ell) break;
+    if (warp == 0) {
+      // Lookahead: A_{J+1,J+1} -= R_{J,J+1}^T R_{J,J+1}, then factor it.
+      double a[32];
+      const bool colok = j1 + lane < ell;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double v = (colok && j1 + i < ell) ? W[(j1 + i) + static_cast<int64_t>(j1 + lane) * ld]
+                                           : (i == lane ? 1.0 : 0.0);
+        if (colok && j1 + i < ell) {
+          double s = 0.0;
+#pragma unroll 8
+          for (int k = 0; k < PB; ++k) s = fma(Rp[k * rp_pitch + j1 + i], Rp[k * rp_pitch + j1 + lane], s);
+          v -= s;
+        }
+        a[i] = v;
+      }
+      const int brk = factor_diag_block(a, W, ld, ell, j1, thresh, Rd, Dt, lane);
+      if (lane == 0 && brk < 32) s_r = j1 + brk;
+    }
+    // Trailing update W[x][y] -= sum_k Rp[k][x] Rp[k][y], x, y in [j1, ell),
+    // minus the diagonal block J+1 (warp 0 owns it), on warps 1..
+    {
+      const int nt = ell - j1;
+      const int tiles = (nt + 15) / 16;
+      for (int tile = warp - 1; warp > 0 && tile < tiles * tiles; tile += kCholWarps - 1) {
+        const int tx = tile % tiles, ty = tile / tiles;
+        const int x0 = j1 + tx * 16, y0 = j1 + ty * 16;
+        if (x0 < j1 + 32 && y0 < j1 + 32) continue;
+        double acc[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[h][q] = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < PB; k0 += 4) {
+          const double a0 = Rp[(k0 + t) * rp_pitch + x0 + g];
+          const double a1 = Rp[(k0 + t) * rp_pitch + x0 + g + 8];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double b0 = Rp[(k0 + t) * rp_pitch + y0 + h * 8 + g];
+            dmma_16x8x4(acc[h], a0, a1, b0);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int xx = x0 + g + ((q & 2) ? 8 : 0);
+            const int yy = y0 + h * 8 + 2 * t + (q & 1);
+            if (xx < ell && yy < ell) W[xx + static_cast<int64_t>(yy) * ld] -= acc[h][q];
+          }
+      }
+    }
+    __syncthreads();
+    r = s_r;
+  }
+  // Rfull (rows < r of R in original order) and T = R11^{-1}.
+  double* Rb = Rfull ? Rfull + b * sq : nullptr;
+  if (Rb)
+    for (int64_t e = tid; e < sq; e += blockDim.x) {
+      const int c = static_cast<int>(e / ld), i = static_cast<int>(e - static_cast<int64_t>(c) * ld);
+      Rb[e] = (i < r && i <= c && c < ell) ? W[e] : 0.0;
+    }
+  const int nbk = (r + 31) / 32;
+  const int rpad = nbk * 32;
+  for (int64_t e = tid; e < static_cast<int64_t>(rpad) * rpad; e += blockDim.x) {
+    const int c = static_cast<int>(e / rpad), i = static_cast<int>(e - static_cast<int64_t>(c) * rpad);
+    double v = 0.0;
+    if (c < r) v = i <= c ? W[i + static_cast<int64_t>(c) * ld] : 0.0;
+    else if (i == c) v = 1.0;
+    C11[i + static_cast<int64_t>(c) * ld] = v;
+  }
+  __syncthreads();
+  blocked_upper_inverse(C11, X, ld, nbk, sm, warp, lane);
+  double* Tb = T + b * sq;
+  for (int64_t e = tid; e < sq; e += blockDim.x) {
+    const int c = static_cast<int>(e / ld), i = static_cast<int>(e - static_cast<int64_t>(c) * ld);
+    Tb[e] = (c < r && i <= c) ? X[e] : 0.0;
+  }
+  if (perm_out)
+    for (int i = tid; i < ellp; i += blockDim.x) perm_out[b * ellp + i] = i;
+  if (tid == 0) rank_out[b] = r;
+}
+
 }  // namespace
 
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ellp * batch; }
@@ -363,6 +611,15 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
   const int64_t pitch = ellp + 20;
   const int64_t big = std::max<int64_t>(PB * pitch, kInvSmem);
+  if (!pivot && !std::getenv("RSVD_PIVOT_ALWAYS")) {
+    const int64_t ub = big * 8 + 2 * 32 * kInvPitch * 8 + 64;
+    RSVD_CUDA(cudaFuncSetAttribute(uchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(ub)));
+    uchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, ub, st>>>(
+        G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
+    RSVD_LAUNCH("uchol_kernel");
+    return;
+  }
   const int64_t bytes = big * 8 + 3 * ellp * 8 + 2 * ellp * 4 + 64;
   RSVD_CUDA(cudaFuncSetAttribute(pchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));

@@ -318,6 +318,10 @@ bool pivot_pass2() {
   static const bool v = std::getenv("RSVD_PIVOT_PASS2") != nullptr;
   return v;
 }
+bool pivot_all() {
+  static const bool v = std::getenv("RSVD_PIVOT_ALL") != nullptr;
+  return v;
+}
 
 bool full_orth() {
   static const bool v = std::getenv("RSVD_FULL_ORTH") != nullptr;
@@ -358,7 +362,10 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       Scope sc(P, kStChol, st);
       // Pass 1 pivots (rank revealing, QRCP order for the Jacobi); pass 2 sees
       // a Gram ~ I and keeps the order so Rt = R2 R1 stays graded.
-      const bool pivot = pass == 0 || pivot_pass2();
+      // Only the first pass on B^T needs the pivot order (it grades Rt for
+      // the Jacobi); elsewhere the unpivoted blocked kernel with breakdown
+      // detection gives the same span (RSVD_PIVOT_ALL=1 pivots every pass 1).
+      const bool pivot = (pass == 0 && (Rt || pivot_all())) || pivot_pass2();
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
     }
     Scope sc(P, kStApply, st);
