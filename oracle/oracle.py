@@ -51,6 +51,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_orthonormal_columns.argtypes = [vp, i64, i64, vp]
         L.oracle_singular_values.argtypes = [vp, i64, i64, vp]
         L.oracle_sector_request.argtypes = [ctypes.c_int, i64, i64, vp, i64, vp]
+        L.oracle_block_factorize.argtypes = [i64, vp, vp, vp, vp, i64, ctypes.c_int, i64,
+                                             ctypes.c_int, i64, ctypes.c_int, u64, i64, vp, vp, vp,
+                                             vp, vp, ctypes.POINTER(dbl),
+                                             ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -192,6 +196,42 @@ def sector_request(maximal: bool, chi: int, slack: int, dims) -> np.ndarray:
     _check(lib().oracle_sector_request(int(maximal), chi, slack, d.ctypes.data, len(d),
                                        out.ctypes.data))
     return out
+
+
+def block_factorize(blocks, charges, chi: int, maximal: bool = False, slack: int = -1,
+                    kind: str = "tsvd", oversample: int = 0, power: int = 4, seed: int = 0,
+                    min_dim: int = 32):
+    """rlftn::block_factorize (blocks.cpp:38-118).  Returns
+    (factors [(U, S, Vt, dw) per sector], total_dw, exact)."""
+    bl = [_f(b) for b in blocks]
+    ns = len(bl)
+    ch = np.asarray(charges, dtype=np.int64)
+    rows = np.asarray([b.shape[0] for b in bl], dtype=np.int64)
+    cols = np.asarray([b.shape[1] for b in bl], dtype=np.int64)
+    us = [np.zeros(max(int(r) * int(min(r, c)), 1)) for r, c in zip(rows, cols)]
+    vts = [np.zeros(max(int(c) * int(min(r, c)), 1)) for r, c in zip(rows, cols)]
+    P = ctypes.c_void_p * max(ns, 1)
+    bp = P(*[b.ctypes.data if b.size else None for b in bl])
+    up = P(*[u.ctypes.data for u in us])
+    vp_ = P(*[v.ctypes.data for v in vts])
+    ranks = np.zeros(max(ns, 1), dtype=np.int64)
+    dws = np.zeros(max(ns, 1))
+    sig = np.zeros(max(int(np.minimum(rows, cols).sum()), 1))
+    tot = ctypes.c_double(0.0)
+    ex = ctypes.c_int(0)
+    _check(lib().oracle_block_factorize(ns, ch.ctypes.data, bp, rows.ctypes.data, cols.ctypes.data,
+                                        chi, int(maximal), slack, 1 if kind == "rsvd" else 0,
+                                        oversample, power, seed & ((1 << 64) - 1), min_dim,
+                                        ranks.ctypes.data, dws.ctypes.data, sig.ctypes.data, up,
+                                        vp_, ctypes.byref(tot), ctypes.byref(ex)))
+    out, off = [], 0
+    for s in range(ns):
+        k, m, n = int(ranks[s]), int(rows[s]), int(cols[s])
+        U = us[s][:m * k].reshape(k, m).T.copy(order="F")
+        Vt = vts[s][:k * n].reshape(n, k).T.copy(order="F")
+        out.append((U, sig[off:off + k].copy(), Vt, float(dws[s])))
+        off += k
+    return out, tot.value, bool(ex.value)
 
 
 def haar(seed: int, rows: int, cols: int) -> np.ndarray:

@@ -366,6 +366,89 @@ std::vector<std::int64_t> sector_request(int maximal, std::int64_t chi, std::int
   return out;
 }
 
+struct BlockResult {
+  std::vector<Factorization> factors;
+  double discarded_weight = 0.0;
+  bool discarded_exact = true;
+};
+
+// blocks.cpp:38-118: per-sector rsvd (kind == 1 and min dim >= min_dim) or
+// tsvd, then the global top-chi selection, ties by charge then position.
+BlockResult block_factorize(const std::vector<Mat>& blocks, const std::vector<std::int64_t>& charges,
+                            std::int64_t chi, int maximal, std::int64_t slack, int kind,
+                            std::int64_t oversample, int power, std::uint64_t seed,
+                            std::int64_t min_dim) {
+  if (blocks.size() != charges.size())
+    throw std::invalid_argument("block_factorize: charges/blocks size mismatch");
+  if (blocks.empty()) throw std::invalid_argument("block_factorize: no sectors");
+  {
+    std::vector<std::int64_t> c = charges;
+    std::sort(c.begin(), c.end());
+    if (std::adjacent_find(c.begin(), c.end()) != c.end())
+      throw std::invalid_argument("block_factorize: duplicate sector charge");
+  }
+  std::vector<std::int64_t> dims(blocks.size());
+  for (std::size_t s = 0; s < blocks.size(); ++s) dims[s] = std::min(blocks[s].rows, blocks[s].cols);
+  const std::vector<std::int64_t> want = sector_request(maximal, chi, slack, dims);
+
+  BlockResult out;
+  out.factors.resize(blocks.size());
+  for (std::size_t s = 0; s < blocks.size(); ++s) {
+    Factorization& f = out.factors[s];
+    if (want[s] == 0 || dims[s] == 0) {
+      f.left = Mat(blocks[s].rows, 0);
+      f.sigma.clear();
+      f.right_adj = Mat(0, blocks[s].cols);
+      double sq = 0.0;
+      for (double v : blocks[s].d) sq += v * v;
+      f.discarded_weight = sq;
+      continue;
+    }
+    if (kind == 1 && dims[s] >= min_dim) {
+      const std::int64_t ell = oversample > 0 ? std::min(std::max(oversample, want[s]), dims[s])
+                                              : std::min(2 * want[s], dims[s]);
+      f = rsvd(blocks[s], want[s], ell, power,
+               derive_seed(seed, static_cast<std::uint64_t>(charges[s])));
+      out.discarded_exact = false;
+    } else {
+      f = tsvd(blocks[s], want[s]);
+    }
+  }
+  struct Cand {
+    double sigma;
+    std::int64_t charge, pos;
+    std::size_t sector;
+  };
+  std::vector<Cand> cand;
+  for (std::size_t s = 0; s < out.factors.size(); ++s)
+    for (std::size_t k = 0; k < out.factors[s].sigma.size(); ++k)
+      cand.push_back({out.factors[s].sigma[k], charges[s], static_cast<std::int64_t>(k), s});
+  std::sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) {
+    if (x.sigma != y.sigma) return x.sigma > y.sigma;
+    if (x.charge != y.charge) return x.charge < y.charge;
+    return x.pos < y.pos;
+  });
+  std::vector<std::int64_t> keep(out.factors.size(), 0);
+  for (std::size_t i = 0; i < cand.size() && static_cast<std::int64_t>(i) < chi; ++i)
+    ++keep[cand[i].sector];
+  for (std::size_t s = 0; s < out.factors.size(); ++s) {
+    Factorization& f = out.factors[s];
+    const std::int64_t r = keep[s];
+    for (std::size_t k = static_cast<std::size_t>(r); k < f.sigma.size(); ++k)
+      f.discarded_weight += f.sigma[k] * f.sigma[k];
+    Mat l(f.left.rows, r), ra(r, f.right_adj.cols);
+    for (std::int64_t j = 0; j < r; ++j)
+      for (std::int64_t i = 0; i < l.rows; ++i) l(i, j) = f.left(i, j);
+    for (std::int64_t j = 0; j < ra.cols; ++j)
+      for (std::int64_t i = 0; i < r; ++i) ra(i, j) = f.right_adj(i, j);
+    f.left = l;
+    f.right_adj = ra;
+    f.sigma.resize(static_cast<std::size_t>(r));
+    out.discarded_weight += f.discarded_weight;
+  }
+  return out;
+}
+
 }  // namespace oracle
 
 // ------------------------------------------------------------- C ABI ---
@@ -496,6 +579,43 @@ int oracle_sector_request(int maximal, std::int64_t chi, std::int64_t slack, con
     const std::vector<std::int64_t> d(dims, dims + ns);
     const auto r = oracle::sector_request(maximal, chi, slack, d);
     std::memcpy(out, r.data(), sizeof(std::int64_t) * r.size());
+  });
+}
+
+// block_factorize over ns sectors; block s is rows[s] x cols[s] column-major at
+// blocks[s].  Outputs per sector: ranks[s], dws[s]; sigma values concatenated
+// in sector order into sigma_out (capacity sum of min dims); u_out[s] /
+// vt_out[s] (optional, may be null) receive rows[s] x rank and rank x cols[s]
+// column-major factors (ld rows[s] and rank).
+int oracle_block_factorize(std::int64_t ns, const std::int64_t* charges, const double* const* blocks,
+                           const std::int64_t* rows, const std::int64_t* cols, std::int64_t chi,
+                           int maximal, std::int64_t slack, int kind, std::int64_t oversample,
+                           int power, std::uint64_t seed, std::int64_t min_dim,
+                           std::int64_t* ranks, double* dws, double* sigma_out,
+                           double* const* u_out, double* const* vt_out, double* total_dw,
+                           int* exact) {
+  return guarded([&] {
+    std::vector<oracle::Mat> bl;
+    for (std::int64_t s = 0; s < ns; ++s) bl.push_back(wrap(blocks[s], rows[s], cols[s], rows[s]));
+    const std::vector<std::int64_t> ch(charges, charges + ns);
+    const oracle::BlockResult r = oracle::block_factorize(bl, ch, chi, maximal, slack, kind,
+                                                          oversample, power, seed, min_dim);
+    std::int64_t off = 0;
+    for (std::int64_t s = 0; s < ns; ++s) {
+      const oracle::Factorization& f = r.factors[static_cast<std::size_t>(s)];
+      const std::int64_t k = static_cast<std::int64_t>(f.sigma.size());
+      ranks[s] = k;
+      dws[s] = f.discarded_weight;
+      std::memcpy(sigma_out + off, f.sigma.data(), sizeof(double) * static_cast<std::size_t>(k));
+      off += k;
+      if (u_out && u_out[s])
+        std::memcpy(u_out[s], f.left.data(), sizeof(double) * static_cast<std::size_t>(f.left.size()));
+      if (vt_out && vt_out[s])
+        std::memcpy(vt_out[s], f.right_adj.data(),
+                    sizeof(double) * static_cast<std::size_t>(f.right_adj.size()));
+    }
+    *total_dw = r.discarded_weight;
+    *exact = r.discarded_exact ? 1 : 0;
   });
 }
 

@@ -2,7 +2,8 @@
 
 Drop-in for the factorization path of rlftn (arXiv 1710.01463's
 TEBD bond compression): ``rsvd``, ``randomized_range``,
-``reconstruction_error`` and the seed/RNG contract, computed by hand-written
+``reconstruction_error``, ``tsvd``, ``block_factorize`` and the seed/RNG
+contract, computed by hand-written
 sm_100a CUDA kernels in ``librsvd_b200.so`` behind the C ABI of
 ``include/rsvd_c.h``.
 """
@@ -16,11 +17,17 @@ from .factorize import (
     reconstruction_error,
     rsvd,
     rsvd_batched,
+    tsvd,
+    tsvd_batched,
 )
+from .blocks import (BlockDiagMatrix, BlockFactorization, BlockMethod, RankPolicy,
+                     SectorRankRequest, block_factorize, sector_request)
 from .rng import CounterRng, derive_seed, mix64, seed_tag
 
 __all__ = [
     "BatchedFactorization", "CounterRng", "DeviceError", "ErrorNorm", "Handle", "InvalidArgument",
     "LibraryMissing", "NumericalError", "RsvdParams", "TruncatedFactorization", "derive_seed",
     "mix64", "randomized_range", "reconstruction_error", "rsvd", "rsvd_batched", "seed_tag",
+    "tsvd", "tsvd_batched", "BlockDiagMatrix", "BlockFactorization", "BlockMethod", "RankPolicy",
+    "SectorRankRequest", "block_factorize", "sector_request",
 ]

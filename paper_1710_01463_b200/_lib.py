@@ -55,6 +55,17 @@ SIGNATURES = {
         _c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_int, ctypes.POINTER(_c_i64), ctypes.c_char_p,
                  _c_i64]
     ),
+    "rsvd_tsvd_f64": (
+        _c_int,
+        [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_dp, _c_dp, _c_i64,
+         ctypes.POINTER(_c_i64), ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
+    "rsvd_tsvd_f64_batched": (
+        _c_int,
+        [_c_vp, _c_i64, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64,
+         _c_dp, _c_i64, _c_dp, _c_i64, _c_i64, ctypes.POINTER(_c_i64),
+         ctypes.POINTER(ctypes.c_double), _c_int],
+    ),
     "rsvd_group_create": (_c_int, [ctypes.POINTER(_c_vp), _c_int]),
     "rsvd_group_destroy": (_c_int, [_c_vp]),
     "rsvd_attach_group": (_c_int, [_c_vp, _c_vp, _c_int]),

@@ -28,8 +28,10 @@ __device__ __forceinline__ double uniform_from(uint64_t w) {
 __global__ void complete_basis_kernel(double* __restrict__ Q, int64_t ld, int64_t stride,
                                       int64_t rows, int64_t ell, const int* __restrict__ rank,
                                       const uint64_t* __restrict__ seeds, uint64_t tag,
-                                      int64_t row_offset, int64_t rows_global) {
+                                      int64_t row_offset, int64_t rows_global,
+                                      const int* __restrict__ mask) {
   const int64_t b = blockIdx.y;
+  if (mask && !mask[b]) return;
   const int r = rank[b];
   if (r >= ell) return;
   const uint64_t key = seeds[b] ^ mix64(tag);
@@ -240,6 +242,28 @@ __global__ void scale_columns_kernel(double* __restrict__ X, int64_t ld, int64_t
   }
 }
 
+__global__ void identity_rect_kernel(double* __restrict__ X, int64_t ld, int64_t stride,
+                                     int64_t rows, int64_t cols) {
+  const int64_t b = blockIdx.y;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / rows, i = e % rows;
+    X[b * stride + i + c * ld] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void masked_copy_kernel(const int* __restrict__ mask, const double* __restrict__ src,
+                                   int64_t lds, int64_t ss, double* __restrict__ dst, int64_t ldd,
+                                   int64_t sd, int64_t rows, int64_t cols) {
+  const int64_t b = blockIdx.y;
+  if (!mask[b]) return;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / rows, i = e - c * rows;
+    dst[b * sd + i + c * ldd] = src[b * ss + i + c * lds];
+  }
+}
+
 unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
   return static_cast<unsigned>(
       std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * kNumSMs)));
@@ -249,11 +273,12 @@ unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
 
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
                            const uint64_t* seeds_dev, uint64_t tag, int64_t batch,
-                           int64_t row_offset, int64_t rows_global, cudaStream_t st) {
+                           int64_t row_offset, int64_t rows_global, cudaStream_t st,
+                           const int* mask) {
   if (batch <= 0 || rows <= 0) return;
   dim3 grid(grid1(rows * ell, 256, 2), static_cast<unsigned>(batch));
   complete_basis_kernel<<<grid, 256, 0, st>>>(Q.base, Q.ld, Q.stride, rows, ell, rank, seeds_dev,
-                                              tag, row_offset, rows_global);
+                                              tag, row_offset, rows_global, mask);
   RSVD_LAUNCH("complete_basis_kernel");
 }
 
@@ -265,6 +290,23 @@ void launch_transpose(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in.base, in.ld, in.stride, rows, cols, out.base,
                                                  out.ld, out.stride);
   RSVD_LAUNCH("transpose_kernel");
+}
+
+void launch_set_identity_rect(MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                              cudaStream_t st) {
+  if (batch <= 0 || rows <= 0 || cols <= 0) return;
+  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  identity_rect_kernel<<<grid, 256, 0, st>>>(out.base, out.ld, out.stride, rows, cols);
+  RSVD_LAUNCH("identity_rect_kernel");
+}
+
+void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, int64_t cols,
+                        int64_t batch, cudaStream_t st) {
+  if (batch <= 0 || rows <= 0 || cols <= 0) return;
+  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  masked_copy_kernel<<<grid, 256, 0, st>>>(mask, src.base, src.ld, src.stride, dst.base, dst.ld,
+                                           dst.stride, rows, cols);
+  RSVD_LAUNCH("masked_copy_kernel");
 }
 
 void launch_set_identity(MatRef out, int64_t n, int64_t batch, cudaStream_t st) {

@@ -422,10 +422,11 @@ __device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld
 __global__ void __launch_bounds__(kCholThreads)
     uchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
                  double* __restrict__ scratch, int* __restrict__ rank_out,
-                 int* __restrict__ perm_out, int ell, int ellp, double tau) {
+                 int* __restrict__ perm_out, int ell, int ellp, double tau, const CholOpts o) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_thresh;
   __shared__ int s_r;
+  __shared__ int s_go;
   const int64_t b = blockIdx.x;
   const int64_t sq = static_cast<int64_t>(ellp) * ellp;
   const int ld = ellp;
@@ -439,6 +440,36 @@ __global__ void __launch_bounds__(kCholThreads)
   double* W = G + b * sq;
   double* C11 = scratch + b * 2 * sq;
   double* X = C11 + sq;
+
+  // Gating (CholOpts): the shifted retry runs only for items whose first
+  // factorization stopped short of full rank, and records them in ill_out.
+  if (tid == 0) {
+    int go = 1;
+    if (o.gate_rank) {
+      go = o.gate_rank[b] < ell;
+      if (o.ill_out) o.ill_out[b] = go;
+    }
+    if (o.mask && !o.mask[b]) go = 0;
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  if (o.Gsrc) {
+    const double* src = o.Gsrc + b * sq;
+    for (int64_t e = tid; e < sq; e += blockDim.x) W[e] = src[e];
+    __syncthreads();
+  }
+  if (o.shift_coef > 0.0) {  // G += s I, s = coef * tr(G) (shifted CholeskyQR)
+    if (warp == 0) {
+      double tr = 0.0;
+      for (int i = lane; i < ell; i += 32) tr += W[i + static_cast<int64_t>(i) * ld];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, off);
+      const double sh = o.shift_coef * tr;
+      for (int i = lane; i < ell; i += 32) W[i + static_cast<int64_t>(i) * ld] += sh;
+    }
+    __syncthreads();
+  }
 
   if (warp == 0) {
     double v = 0.0;
@@ -606,17 +637,18 @@ int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ell
 
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
-                  cudaStream_t st) {
+                  cudaStream_t st, const CholOpts* opts) {
   if (batch <= 0) return;
   if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
   const int64_t pitch = ellp + 20;
   const int64_t big = std::max<int64_t>(PB * pitch, kInvSmem);
-  if (!pivot && !std::getenv("RSVD_PIVOT_ALWAYS")) {
+  if (opts || (!pivot && !std::getenv("RSVD_PIVOT_ALWAYS"))) {
+    const CholOpts o = opts ? *opts : CholOpts{};
     const int64_t ub = big * 8 + 2 * 32 * kInvPitch * 8 + 64;
     RSVD_CUDA(cudaFuncSetAttribute(uchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(ub)));
     uchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, ub, st>>>(
-        G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau);
+        G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau, o);
     RSVD_LAUNCH("uchol_kernel");
     return;
   }

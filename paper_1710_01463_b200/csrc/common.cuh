@@ -78,6 +78,9 @@ struct GemmOpts {
   int64_t colmap_stride = 0;
   bool b_upper = false;
   bool c_upper = false;
+  // item_mask[b] == 0 skips item b entirely (C untouched): the masked passes
+  // of the ill-conditioned CholeskyQR fallback (engine.cu orth).
+  const int* item_mask = nullptr;
 };
 void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
               int64_t batch, double* partial, int64_t partial_capacity, const GemmOpts& opt,
@@ -86,6 +89,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
 // returns false (nothing launched) when the operands do not qualify.
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
+               const int* item_mask,
                bool b_upper, cudaStream_t st);
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
 
@@ -93,9 +97,21 @@ int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64
 // G is consumed (used as factorization storage); scratch holds
 // pchol_scratch_elems(ellp, batch) doubles.
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch);
+// Options of the unpivoted kernel (any CholOpts forces it):
+//   mask       item b runs only if mask[b] != 0;
+//   gate_rank  item b runs only if gate_rank[b] < ell; ill_out[b] records it;
+//   Gsrc       factor a copy of Gsrc[b] (G[b] is overwritten);
+//   shift_coef factor G + coef * tr(G) * I (shifted CholeskyQR).
+struct CholOpts {
+  const int* mask = nullptr;
+  const int* gate_rank = nullptr;
+  int* ill_out = nullptr;
+  const double* Gsrc = nullptr;
+  double shift_coef = 0.0;
+};
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
-                  cudaStream_t st);
+                  cudaStream_t st, const CholOpts* opts = nullptr);
 
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.
@@ -109,7 +125,8 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
 // aux.cu
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
                            const uint64_t* seeds_dev, uint64_t tag, int64_t batch,
-                           int64_t row_offset, int64_t rows_global, cudaStream_t st);
+                           int64_t row_offset, int64_t rows_global, cudaStream_t st,
+                           const int* mask = nullptr);
 
 // Sum all-reduce across the ranks of a row-sharded factorization (NCCL or an
 // in-process group); stream-ordered on `st`.
@@ -127,7 +144,12 @@ std::unique_ptr<Reducer> make_nccl_reducer(int nranks, int rank, const unsigned 
 void nccl_unique_id(unsigned char* out);
 void launch_transpose(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_t batch,
                       cudaStream_t st);
+// dst[b] = src[b] (rows x cols) for the items with mask[b] != 0.
+void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, int64_t cols,
+                        int64_t batch, cudaStream_t st);
 void launch_set_identity(MatRef out, int64_t n, int64_t batch, cudaStream_t st);
+void launch_set_identity_rect(MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                              cudaStream_t st);
 void launch_finalize_spectrum(const double* HJ, int64_t ellp, int64_t ell, int64_t k,
                               int64_t m, int64_t n, double* sigma_out, int* perm, int* rank,
                               double* discarded, int64_t batch, cudaStream_t st);

@@ -239,7 +239,8 @@ struct Shape {
 struct Buffers {
   uint64_t* seeds;
   double *X, *X2, *Y, *Y2;
-  double *G, *T, *Rf1, *Rf2, *Rt, *H, *Jm, *cscratch;
+  double *G, *G0, *T, *Rf1, *Rf2, *Rt, *H, *Jm, *cscratch;
+  int* ill;  // per item: the current orth took the ill-conditioned fallback
   double *Ut, *Jr, *Vb;
   double* sig;
   double* dw;
@@ -280,6 +281,8 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   B.Y = c.take<double>(b * s.m * lp);
   B.Y2 = c.take<double>(b * s.m * lp);
   B.G = c.take<double>(b * lp * lp);
+  B.G0 = c.take<double>(b * lp * lp);
+  B.ill = c.take<int>(b);
   B.T = c.take<double>(b * lp * lp);
   B.Rf1 = c.take<double>(b * lp * lp);
   B.Rf2 = c.take<double>(b * lp * lp);
@@ -331,12 +334,23 @@ bool full_orth() {
 // CholeskyQR of Y (rows x ellp per item): `passes` = 2 is CholeskyQR2 (the
 // result is orthonormal to working precision); 1 pass gives Q1 = (Y P) R11^-1,
 // an exact-span, well-conditioned basis (kappa(Q1)^2 - 1 = O(u kappa(Y)^2) with
-// kappa(Y) <= tau^-1/2 by the pivot floor), which is all an intermediate
-// power-iteration step consumes: the next product only sees span(Q).  The
-// result is left in *Yb (the two buffers are swapped when passes is odd).
-// When Rt is given (passes = 2), also Rt = Rf2 * Rf1 with Y_in ~= Y_out * Rt.
+// kappa(Y) <= tau^-1/2), which is all an intermediate power-iteration step
+// consumes: the next product only sees span(Q).  The result is left in *Yb
+// (the two buffers are swapped when passes is odd).  When Rt is given, also
+// Rt = R_last ... R_1 with Y_in ~= Y_out * Rt.
 // m_side: Y has the (possibly row-sharded) m rows of A; its Gram is then
 // all-reduced across ranks and the completion uses global row indices.
+//
+// Ill-conditioned fallback (the north star's "TSQR fallback for ill-conditioned
+// Y", as shifted CholeskyQR, Fukaya et al. 2020): an item whose first
+// factorization stops below full rank (kappa(Y) > tau^-1/2 ~ 3e6, or a rank-
+// deficient Y) is refactored from the saved Gram as G + sI,
+// s = 11 (rows l + l (l + 1)) u tr(G), unpivoted and without truncation, and
+// gets one extra CholeskyQR pass (masked to those items).  Directions down to
+// sigma ~ u ||Y|| keep their true components, as with the reference's
+// Householder QR (lapack.cpp:146-201), instead of a random completion -- the
+// sampled tail (discarded weight) of steep spectra depends on them.  Items
+// that never truncate pay only the no-op launches.
 void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, double* Rt,
           uint64_t tag, int passes, bool m_side, cudaStream_t st) {
   const int64_t lp = s.ellp, b = s.batch;
@@ -345,42 +359,90 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
-  if (full_orth()) passes = 2;
-  for (int pass = 0; pass < passes; ++pass) {
-    const MatRef& in = pass == 0 ? Y : Tm;
-    const MatRef& out = pass == 0 ? Tm : Y;
-    double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
-    int* rk = pass == 0 ? B.rank1 : B.rank2;
-    {
-      Scope sc(P, kStGram, st);
-      GemmOpts sym;
-      sym.c_upper = true;
-      dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
-      if (sharded) B.red->allreduce_sum(B.G, b * lp * lp, st);  // G = sum_p Y_p^T Y_p
-    }
-    {
-      Scope sc(P, kStChol, st);
-      // Pass 1 pivots (rank revealing, QRCP order for the Jacobi); pass 2 sees
-      // a Gram ~ I and keeps the order so Rt = R2 R1 stays graded.
-      // Only the first pass on B^T needs the pivot order (it grades Rt for
-      // the Jacobi); elsewhere the unpivoted blocked kernel with breakdown
-      // detection gives the same span (RSVD_PIVOT_ALL=1 pivots every pass 1).
-      const bool pivot = (pass == 0 && (Rt || pivot_all())) || pivot_pass2();
-      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
-    }
-    Scope sc(P, kStApply, st);
+  if (full_orth()) passes = std::max(passes, 2);
+  auto gram = [&](const MatRef& in, const int* mask) {
+    Scope sc(P, kStGram, st);
+    GemmOpts sym;
+    sym.c_upper = true;
+    sym.item_mask = mask;
+    dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
+    if (sharded) B.red->allreduce_sum(B.G, b * lp * lp, st);  // G = sum_p Y_p^T Y_p
+  };
+  auto apply = [&](const MatRef& in, const MatRef& out, const int* mask) {
     // out = (in P) R11^{-1}: pivot-gathered columns, upper-triangular right factor.
     GemmOpts tri;
     tri.colmapA = B.perm;
     tri.colmap_stride = lp;
     tri.b_upper = true;
+    tri.item_mask = mask;
     dgemm_ex(false, rows, lp, lp, in, T, out, b, B.partial, B.partial_cap, tri, st);
-    launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global, st);
+  };
+  for (int pass = 0; pass < passes; ++pass) {
+    const MatRef& in = pass == 0 ? Y : Tm;
+    const MatRef& out = pass == 0 ? Tm : Y;
+    double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
+    int* rk = pass == 0 ? B.rank1 : B.rank2;
+    gram(in, nullptr);
+    {
+      Scope sc(P, kStChol, st);
+      if (pass == 0)
+        RSVD_CUDA(cudaMemcpyAsync(B.G0, B.G, sizeof(double) * b * lp * lp,
+                                  cudaMemcpyDeviceToDevice, st));
+      // Pass 1 on B^T pivots (QRCP order grades Rt for the Jacobi); elsewhere
+      // the unpivoted blocked kernel with breakdown detection gives the same
+      // span (RSVD_PIVOT_ALL=1 pivots every pass 1).
+      const bool pivot = (pass == 0 && (Rt || pivot_all())) || pivot_pass2();
+      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
+      if (pass == 0) {  // shifted retry of the items that stopped short of full rank
+        CholOpts o;
+        o.gate_rank = rk;
+        o.ill_out = B.ill;
+        o.Gsrc = B.G0;
+        o.shift_coef = 11.0 *
+                       (static_cast<double>(rows_global) * s.ell +
+                        static_cast<double>(s.ell) * (s.ell + 1)) *
+                       1.1102230246251565e-16;
+        launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, false, b, st, &o);
+      }
+    }
+    {
+      Scope sc(P, kStApply, st);
+      apply(in, out, nullptr);
+      launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global,
+                            st);
+    }
+    if (pass == 0) {
+      // Extra CholeskyQR pass for the ill items: out -> in (free now) -> out.
+      gram(out, B.ill);
+      {
+        Scope sc(P, kStChol, st);
+        CholOpts o;
+        o.mask = B.ill;
+        launch_pchol(B.G, B.T, Rt ? B.Rf2 : nullptr, B.cscratch, B.rank2, B.perm, s.ell, lp,
+                     kPivotTau, false, b, st, &o);
+      }
+      Scope sc(P, kStApply, st);
+      apply(out, in, B.ill);
+      launch_complete_basis(in, rows, s.ell, B.rank2, B.seeds, tag + 0x40, b, row_off, rows_global,
+                            st, B.ill);
+      launch_masked_copy(B.ill, in, out, rows, lp, b, st);
+      if (Rt) {  // R1 <- R_extra R1 for the ill items (Rt is scratch until the end)
+        GemmOpts mk;
+        mk.item_mask = B.ill;
+        dgemm_ex(false, lp, lp, lp, MatRef{B.Rf2, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp},
+                 MatRef{Rt, lp, lp * lp}, b, B.partial, B.partial_cap, mk, st);
+        launch_masked_copy(B.ill, MatRef{Rt, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp}, lp, lp, b,
+                           st);
+      }
+    }
   }
   if (Rt) {
     Scope sc(P, kStApply, st);
-    dgemm(false, lp, lp, lp, MatRef{B.Rf2, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp},
-          MatRef{Rt, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+    if (passes >= 2)
+      dgemm(false, lp, lp, lp, MatRef{B.Rf2, lp, lp * lp}, MatRef{B.Rf1, lp, lp * lp},
+            MatRef{Rt, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+    else
+      launch_copy_matrix(MatRef{B.Rf1, lp, lp * lp}, lp, lp, MatRef{Rt, lp, lp * lp}, b, st);
   }
   if (passes % 2 == 1) std::swap(Yb, Tmp);
 }
@@ -422,8 +484,13 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
 
 // Projection + small SVD + lift (factorize.cpp:86-93).  Outputs go to
 // U (m x k), S (k per item, contiguous stride sS), Vt (k x n).
+// exact_h (tsvd, Q = I): the Jacobi input is recomputed as H = A Qb instead of
+// Rt^T.  A annihilates the part of Qb outside range(A^T), so sigma(H) carries
+// only the O(u) departure of Qb from orthonormality: absolute errors
+// O(u ||A||) like LAPACK's gesdd, where Rt = R2 R1 alone inherits the
+// O(u kappa) residual of the first CholeskyQR pass on ill-conditioned blocks.
 void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64_t sS, MatRef Vt,
-               cudaStream_t st) {
+               cudaStream_t st, bool exact_h = false) {
   const int64_t lp = s.ellp, b = s.batch, k = s.k;
   const MatRef X{B.X, s.n, s.n * lp}, Y{B.Y, s.m, s.m * lp};
   Prof* P = B.prof;
@@ -434,9 +501,15 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
   }
   orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, 2, false, st);
+  const MatRef Qb{B.X, s.n, s.n * lp};  // orth may have swapped B.X and B.X2
   {
     Scope sc(P, kStJacobi, st);
-    launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
+    if (exact_h) {
+      RSVD_CUDA(cudaMemsetAsync(B.H, 0, sizeof(double) * b * lp * lp, st));
+      dgemm(false, s.m, lp, s.n, A, Qb, MatRef{B.H, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+    } else {
+      launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
+    }
     launch_jacobi(B.H, B.Jm, s.ell, lp, kMaxSweeps, B.sweeps, B.jflags, b, st);
   }
   Scope sc(P, kStLift, st);
@@ -448,7 +521,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   // V = Qb J[:, perm[:r]], Vt = V^T.
   launch_gather_scale_columns(B.Jm, lp, lp * lp, B.permS, lp, nullptr, k, B.rankF, lp, k, B.Jr,
                               lp, lp * k, b, st);
-  dgemm(false, s.n, k, lp, X, MatRef{B.Jr, lp, lp * k}, MatRef{B.Vb, s.n, s.n * k}, b, B.partial,
+  dgemm(false, s.n, k, lp, Qb, MatRef{B.Jr, lp, lp * k}, MatRef{B.Vb, s.n, s.n * k}, b, B.partial,
         B.partial_cap, st);
   launch_transpose(MatRef{B.Vb, s.n, s.n * k}, s.n, k, Vt, b, st);
   launch_copy_matrix(MatRef{B.sig, k, k}, k, 1, MatRef{S, k, sS}, b, st);
@@ -747,6 +820,93 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
     out_rank[b] = h->pin.ints[b];
     dw[b] = h->pin.dbls[b];
     h->last_sweeps = std::max(h->last_sweeps, h->pin.ints[batch + b]);
+  }
+}
+
+// Deterministic truncated SVD, rlftn::tsvd (factorize.cpp:42-50): the full
+// thin SVD then truncation with the exact discarded weight.  With Q = I
+// (l = min(m, n)) the RSVD's SVD stage is exact: B^T = A_e^T is factored by
+// CholeskyQR2 with R and the l x l factor by one-sided Jacobi.  For m > n the
+// engine factors A^T and swaps the factors (A = V S U^T).
+constexpr int64_t kTsvdMaxDim = 576;  // one-sided Jacobi register budget (18 rows / lane)
+uint64_t mix64_host(uint64_t z);
+
+void tsvd_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n, int64_t lda,
+               int64_t strideA, int64_t chi, double* U, int64_t ldu, int64_t strideU, double* S,
+               int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt, int64_t* out_rank,
+               double* dw, int flags) {
+  check_flags(flags);
+  if (m <= 0 || n <= 0) throw InvalidArgument("tsvd: empty matrix");  // :44
+  if (chi < 1) throw InvalidArgument("tsvd: rank must be >= 1");      // :45
+  if (batch < 0) throw InvalidArgument("tsvd: batch must be >= 0");
+  if (batch == 0) return;
+  const int64_t p = std::min(m, n), k = std::min(chi, p);
+  if (p > kTsvdMaxDim)
+    throw InvalidArgument("tsvd: min(m, n) > 576 is not supported by the GPU path");
+  if (!A || !U || !S || !Vt || !out_rank || !dw) throw InvalidArgument("tsvd: null pointer argument");
+  if (lda < m || ldu < m || ldvt < k) throw InvalidArgument("tsvd: leading dimension too small");
+  const bool host = flags == RSVD_PTR_HOST;
+  const bool tr = m > n;
+  const int64_t me = tr ? n : m, ne = tr ? m : n;
+  RSVD_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  Shape s{me, ne, batch, k, me, round_up(me, 32), 0};
+  auto layout = [&](Carver& c, Buffers& B, double*& Ain, double*& Ae, double*& Ue, double*& Ve,
+                    double*& Uo, double*& So, double*& Vo) {
+    B = carve(c, s, false, true);
+    Ain = host ? c.take<double>(batch * m * n) : nullptr;
+    Ae = tr ? c.take<double>(batch * me * ne) : nullptr;
+    Ue = c.take<double>(batch * me * k);
+    Ve = c.take<double>(batch * k * ne);
+    Uo = c.take<double>(batch * m * k);
+    So = c.take<double>(batch * k);
+    Vo = c.take<double>(batch * k * n);
+  };
+  Buffers B;
+  double *Ain, *Ae, *Ue, *Ve, *Uo, *So, *Vo;
+  Carver meas{nullptr};
+  layout(meas, B, Ain, Ae, Ue, Ve, Uo, So, Vo);
+  char* const before = h->arena.base;
+  h->arena.reserve(meas.off + 256);
+  if (h->arena.base != before) h->drop_graphs();
+  Carver cv{h->arena.base};
+  layout(cv, B, Ain, Ae, Ue, Ve, Uo, So, Vo);
+  if (h->pin.reserve(batch)) h->drop_graphs();
+  for (int64_t b = 0; b < batch; ++b) h->pin.seeds[b] = mix64_host(0x7473766400ull + b);  // completion only
+  B.prof = &h->prof;
+  B.red = nullptr;
+  RSVD_CUDA(cudaMemcpyAsync(B.seeds, h->pin.seeds, sizeof(uint64_t) * batch, cudaMemcpyHostToDevice,
+                            st));
+  CMatRef Ad{A, lda, strideA};
+  if (host) {
+    copy_batch(Ain, m, m * n, A, lda, strideA, m, n, batch, cudaMemcpyHostToDevice, st);
+    Ad = CMatRef{Ain, m, m * n};
+  }
+  CMatRef Aeff = Ad;
+  if (tr) {
+    launch_transpose(Ad, m, n, MatRef{Ae, me, me * ne}, batch, st);
+    Aeff = CMatRef{Ae, me, me * ne};
+  }
+  launch_set_identity_rect(MatRef{B.Y, me, me * s.ellp}, me, s.ellp, batch, st);
+  svd_stage(s, B, Aeff, MatRef{Ue, me, me * k}, So, k, MatRef{Ve, k, k * ne}, st, true);
+  if (!tr) {
+    launch_copy_matrix(CMatRef{Ue, me, me * k}, m, k, MatRef{Uo, m, m * k}, batch, st);
+    launch_copy_matrix(CMatRef{Ve, k, k * ne}, k, n, MatRef{Vo, k, k * n}, batch, st);
+  } else {
+    launch_transpose(CMatRef{Ve, k, k * ne}, k, m, MatRef{Uo, m, m * k}, batch, st);  // U = V_e
+    launch_transpose(CMatRef{Ue, me, me * k}, n, k, MatRef{Vo, k, k * n}, batch, st);  // Vt = U_e^T
+  }
+  const cudaMemcpyKind out = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  copy_batch(U, ldu, strideU, Uo, m, m * k, m, k, batch, out, st);
+  copy_batch(Vt, ldvt, strideVt, Vo, k, k * n, k, n, batch, out, st);
+  copy_batch(S, k, strideS, So, k, k, k, 1, batch, out, st);
+  RSVD_CUDA(cudaMemcpyAsync(h->pin.ints, B.rankF, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls, B.dw, sizeof(double) * batch, cudaMemcpyDeviceToHost, st));
+  RSVD_CUDA(cudaStreamSynchronize(st));
+  if (h->prof.on) h->prof.collect();
+  for (int64_t b = 0; b < batch; ++b) {
+    out_rank[b] = h->pin.ints[b];
+    dw[b] = h->pin.dbls[b];
   }
 }
 
@@ -1054,6 +1214,26 @@ int rsvd_f64_rowsharded(rsvd_handle h, const double* A_local, int64_t m_local, i
     rsvd::rsvd_batched_impl(h, 1, A_local, m_local, n, lda, 0, rank, oversample, power, &seed,
                             U_local, ldu, 0, S, 0, Vt, ldvt, 0, out_rank, discarded_weight, flags,
                             m_global, row_offset, true);
+  });
+}
+
+int rsvd_tsvd_f64(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t chi,
+                  double* U, int64_t ldu, double* S, double* Vt, int64_t ldvt, int64_t* out_rank,
+                  double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::tsvd_impl(h, 1, A, m, n, lda, 0, chi, U, ldu, 0, S, 0, Vt, ldvt, 0, out_rank,
+                    discarded_weight, flags);
+  });
+}
+
+int rsvd_tsvd_f64_batched(rsvd_handle h, int64_t batch, const double* A, int64_t m, int64_t n,
+                          int64_t lda, int64_t strideA, int64_t chi, double* U, int64_t ldu,
+                          int64_t strideU, double* S, int64_t strideS, double* Vt, int64_t ldvt,
+                          int64_t strideVt, int64_t* out_rank, double* discarded_weight,
+                          int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::tsvd_impl(h, batch, A, m, n, lda, strideA, chi, U, ldu, strideU, S, strideS, Vt, ldvt,
+                    strideVt, out_rank, discarded_weight, flags);
   });
 }
 

@@ -77,6 +77,7 @@ struct GemmArgs {
   int64_t colmap_stride;
   int b_upper;
   int c_upper;
+  const int* item_mask;  // item_mask[b] == 0: skip item b
 };
 
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, int VEC>
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
   const int64_t item = bz / p.splits;
   const int split = static_cast<int>(bz % p.splits);
   if (p.c_upper && m0 >= n0 + BN) return;  // tile strictly below the diagonal
+  if (p.item_mask && !p.item_mask[item]) return;
   const int64_t k_begin = split * p.k_per_split;
   int64_t k_end = min(p.K, k_begin + p.k_per_split);
   if (p.b_upper) k_end = min(k_end, n0 + BN);  // rows >= n0+BN of an upper B are zero
@@ -250,13 +252,14 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
 // Fixed-order split reduction: C[item](i,j) = sum_s partial[s][item](i,j).
 __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int64_t M, int64_t N,
                                      int splits, int64_t batch, double* __restrict__ C,
-                                     int64_t ldc, int64_t strideC) {
+                                     int64_t ldc, int64_t strideC, const int* __restrict__ mask) {
   const int64_t per = M * N;
   const int64_t total = per * batch;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t item = e / per;
     const int64_t rem = e - item * per;
+    if (mask && !mask[item]) continue;
     const int64_t j = rem / M, i = rem - j * M;
     double s = 0.0;
     for (int sp = 0; sp < splits; ++sp) s += partial[(sp * batch + item) * per + rem];
@@ -266,11 +269,12 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int64_t
 
 // C(r, c) = C(c, r) for r > c (square items).
 __global__ void mirror_upper_kernel(double* __restrict__ C, int64_t n, int64_t ldc,
-                                    int64_t strideC, int64_t batch) {
+                                    int64_t strideC, int64_t batch, const int* __restrict__ mask) {
   const int64_t per = n * n;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < per * batch;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t item = e / per, rem = e - item * per;
+    if (mask && !mask[item]) continue;
     const int64_t c = rem / n, r = rem - c * n;
     if (r > c) C[item * strideC + r + c * ldc] = C[item * strideC + c + r * ldc];
   }
@@ -401,6 +405,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   a.colmap_stride = opt.colmap_stride;
   a.b_upper = opt.b_upper ? 1 : 0;
   a.c_upper = (opt.c_upper && M == N) ? 1 : 0;
+  a.item_mask = opt.item_mask;
   if (c.splits > 1) {
     a.C = partial, a.ldc = M, a.strideC = M * N;
   } else {
@@ -412,7 +417,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
   const bool tma_done = !a.colmapA && c.bm == 128 && c.bn == 96 &&
                         dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
-                                  c.kps, a.c_upper != 0, a.b_upper != 0, st);
+                                  c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st);
   if (tma_done) {
   } else if (trans_a) {
     if (vec2) dispatch<true, 2>(c, a, st);
@@ -426,13 +431,13 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
     const int threads = 256;
     const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, threads), 8 * kNumSMs));
     splitk_reduce_kernel<<<blocks, threads, 0, st>>>(partial, M, N, c.splits, batch, C.base, C.ld,
-                                                     C.stride);
+                                                     C.stride, opt.item_mask);
     RSVD_LAUNCH("splitk_reduce_kernel");
   }
   if (a.c_upper) {  // symmetric result: mirror the upper triangle
     const int64_t total = M * M * batch;
     const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
-    mirror_upper_kernel<<<blocks, 256, 0, st>>>(C.base, M, C.ld, C.stride, batch);
+    mirror_upper_kernel<<<blocks, 256, 0, st>>>(C.base, M, C.ld, C.stride, batch, opt.item_mask);
     RSVD_LAUNCH("mirror_upper_kernel");
   }
 }

@@ -84,6 +84,7 @@ struct TmaArgs {
   int splits;
   int64_t k_per_split;
   int c_upper, b_upper;
+  const int* item_mask;
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 2)
   const int64_t item = bz / p.splits;
   const int split = static_cast<int>(bz % p.splits);
   if (p.c_upper && m0 >= n0 + BN) return;
+  if (p.item_mask && !p.item_mask[item]) return;
   const int64_t k_begin = split * p.k_per_split;
   int64_t k_end = min(p.K, k_begin + p.k_per_split);
   if (p.b_upper) k_end = min(k_end, n0 + BN);
@@ -283,7 +285,7 @@ bool tma_gemm_enabled() {
 
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
-               bool b_upper, cudaStream_t st) {
+               const int* item_mask, bool b_upper, cudaStream_t st) {
   if (!tma_gemm_enabled()) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al16(A.base) || !al16(B.base)) return false;
@@ -315,7 +317,8 @@ bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef
     const cuuint32_t box[4] = {16, kTBK, kBM / 16, 1};
     if (!make_map(&ma, A.base, 4, dims, str, box)) return false;
   }
-  TmaArgs a{M, N, K, C, ldc, strideC, batch, splits, kps, c_upper ? 1 : 0, b_upper ? 1 : 0};
+  TmaArgs a{M, N, K, C, ldc, strideC, batch, splits, kps, c_upper ? 1 : 0, b_upper ? 1 : 0,
+            item_mask};
   const int stg = tma_stages();
   if (trans_a) {
     if (stg == 3) launch<3, true>(ma, mb, a, st);

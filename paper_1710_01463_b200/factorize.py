@@ -139,6 +139,47 @@ def rsvd(a, params: RsvdParams, handle: Optional[_lib.Handle] = None) -> Truncat
 _MASK = (1 << 64) - 1
 
 
+def tsvd(a, chi: int, handle: Optional[_lib.Handle] = None) -> TruncatedFactorization:
+    """rlftn::tsvd (factorize.cpp:42-50): exact thin SVD truncated to
+    r = min(chi, numerical rank), exact discarded weight.  GPU path for
+    min(m, n) <= 576."""
+    lib = _lib.load()
+    h = handle or _lib.default_handle()
+    r = ctypes.c_int64(0)
+    dw = ctypes.c_double(0.0)
+    if _is_torch_cuda(a):
+        import torch
+
+        a, lda = _colmajor_torch(a)
+        m, n = a.shape
+        k = max(min(int(chi), m, n), 1)
+        U = torch.empty((k, m), dtype=torch.float64, device=a.device).t()
+        S = torch.empty(k, dtype=torch.float64, device=a.device)
+        Vt = torch.empty((n, k), dtype=torch.float64, device=a.device).t()
+        with _lib.on_torch_stream(h):
+            rc = lib.rsvd_tsvd_f64(h.raw, a.data_ptr() if a.numel() else 0, m, n, lda, int(chi),
+                                   U.data_ptr(), max(m, 1), S.data_ptr(), Vt.data_ptr(), k,
+                                   ctypes.byref(r), ctypes.byref(dw), _lib.PTR_DEVICE)
+        _lib.raise_for(rc, h.raw)
+        rr = r.value
+        return TruncatedFactorization(U[:, :rr], S[:rr], Vt[:rr, :], dw.value, True)
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2:
+        raise InvalidArgument("tsvd: expected a 2-D array")
+    m, n = a.shape
+    k = max(min(int(chi), m, n), 1)
+    U = np.zeros((m, k), order="F")
+    S = np.zeros(k)
+    Vt = np.zeros((k, n), order="F")
+    rc = lib.rsvd_tsvd_f64(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1), int(chi),
+                           U.ctypes.data, max(m, 1), S.ctypes.data, Vt.ctypes.data, k,
+                           ctypes.byref(r), ctypes.byref(dw), _lib.PTR_HOST)
+    _lib.raise_for(rc, h.raw)
+    rr = r.value
+    return TruncatedFactorization(U[:, :rr].copy(order="F"), S[:rr].copy(),
+                                  Vt[:rr, :].copy(order="F"), dw.value, True)
+
+
 @dataclass
 class BatchedFactorization:
     """Result of rsvd_batched: stacked buffers plus per-item ranks."""
@@ -148,11 +189,75 @@ class BatchedFactorization:
     right_adj: Any  # batch x k x n
     ranks: List[int] = field(default_factory=list)
     discarded_weight: List[float] = field(default_factory=list)
+    discarded_exact: bool = False
 
     def item(self, b: int) -> TruncatedFactorization:
         r = self.ranks[b]
         return TruncatedFactorization(self.left[b][:, :r], self.sigma[b][:r],
-                                      self.right_adj[b][:r, :], self.discarded_weight[b], False)
+                                      self.right_adj[b][:r, :], self.discarded_weight[b],
+                                      self.discarded_exact)
+
+
+def _batched_buffers(a, k: int, who: str):
+    """Stage a (batch, m, n) input and allocate (batch, m, k) / (batch, k) /
+    (batch, k, n) outputs with column-major items.  Returns
+    (bsz, m, n, flags, ptrs, U, S, Vt, Ub, Vb, keepalive)."""
+    import torch
+
+    if a.dim() != 3 or a.dtype != torch.float64:
+        raise InvalidArgument(f"{who}: expected a (batch, m, n) float64 tensor")
+    bsz, m, n = a.shape
+    if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
+        a = a.transpose(1, 2).contiguous().transpose(1, 2)
+    dev = a.device if a.is_cuda else None
+    pin = (not a.is_cuda) and bool(a.is_pinned())
+    kw = dict(dtype=torch.float64, device=dev) if dev is not None else dict(
+        dtype=torch.float64, pin_memory=pin)
+    U = torch.empty((bsz, k, m), **kw).transpose(1, 2)
+    S = torch.empty((bsz, k), **kw)
+    Vt = torch.empty((bsz, n, k), **kw).transpose(1, 2)
+    flags = _lib.PTR_DEVICE if a.is_cuda else _lib.PTR_HOST
+    return bsz, m, n, flags, (a.data_ptr(), U.data_ptr(), S.data_ptr(), Vt.data_ptr()), U, S, Vt, a
+
+
+def tsvd_batched(a, chi: int, handle: Optional[_lib.Handle] = None) -> BatchedFactorization:
+    """Batched tsvd over (batch, m, n) items of one shape (the exact route of
+    block_factorize for equal-shape sectors, blocks.cpp:82)."""
+    lib = _lib.load()
+    h = handle or _lib.default_handle()
+    if hasattr(a, "data_ptr") and hasattr(a, "is_pinned"):
+        m_, n_ = int(a.shape[1]), int(a.shape[2])
+        k = max(min(int(chi), m_, n_), 1)
+        bsz, m, n, flags, ptrs, U, S, Vt, a = _batched_buffers(a, k, "tsvd_batched")
+        Ub = None
+    else:
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 3:
+            raise InvalidArgument("tsvd_batched: expected a (batch, m, n) array")
+        bsz, m, n = a.shape
+        k = max(min(int(chi), m, n), 1)
+        a = np.ascontiguousarray(np.transpose(a, (0, 2, 1)))
+        Ub = np.zeros((bsz, k, m))
+        S = np.zeros((bsz, k))
+        Vb = np.zeros((bsz, n, k))
+        flags = _lib.PTR_HOST
+        ptrs = (a.ctypes.data, Ub.ctypes.data, S.ctypes.data, Vb.ctypes.data)
+    ranks = (ctypes.c_int64 * max(bsz, 1))()
+    dws = (ctypes.c_double * max(bsz, 1))()
+    if flags == _lib.PTR_DEVICE:
+        with _lib.on_torch_stream(h):
+            rc = lib.rsvd_tsvd_f64_batched(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1],
+                                           m, m * k, ptrs[2], k, ptrs[3], k, k * n, ranks, dws,
+                                           flags)
+    else:
+        rc = lib.rsvd_tsvd_f64_batched(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1], m,
+                                       m * k, ptrs[2], k, ptrs[3], k, k * n, ranks, dws, flags)
+    _lib.raise_for(rc, h.raw)
+    if Ub is not None:
+        U = np.transpose(Ub, (0, 2, 1))
+        Vt = np.transpose(Vb, (0, 2, 1))
+    return BatchedFactorization(U, S, Vt, [int(ranks[i]) for i in range(bsz)],
+                                [float(dws[i]) for i in range(bsz)], True)
 
 
 def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
