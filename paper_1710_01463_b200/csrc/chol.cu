@@ -27,7 +27,10 @@
 //     (mma.sync m16n8k4 f64), so no row/column swap ever touches global memory;
 //   * R rows are written in original column order, which is Rfull directly;
 //   * R11^{-1} by a blocked DMMA inverse (blocked_upper_inverse below).
+#include <cooperative_groups.h>
+
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -40,7 +43,7 @@ constexpr int kCholWarps = kCholThreads / 32;
 constexpr int PB = 32;  // panel width (pivots per panel)
 
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
       "{%0,%1,%2,%3};\n"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -368,43 +371,55 @@ __global__ void __launch_bounds__(kCholThreads)
 // at or beyond `ell` arrive as identity columns.
 __device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld, int ell, int o,
                                  double thresh, double* Rd, double* Dt, int lane) {
+  // Cholesky of the 32 x 32 block (lane = column, a[i] = row i) and, in the
+  // same sweep, Z = R^{-T} by forward substitution (lane j holds column j of
+  // Z, i.e. row j of R^{-1}).  Row k of R is broadcast through shared memory
+  // (Rd, read as double2) for the rank-1 update, column k through Dt (which
+  // holds R^T until the end); pivots use a warp-uniform rsqrt.  ~11k cycles
+  // (tools/probe/diag_probe4.cu) against ~29k for shuffles + a separate
+  // backward substitution.
   int brk = 32;
+  double z[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const double akk = __shfl_sync(0xffffffffu, a[k], k);
     if (brk == 32 && o + k < ell && !(akk > thresh)) brk = k;
+    double rk, inv = 1.0;
     if (brk == 32) {
-      const double rkk = sqrt(akk);
-      const double rk = (lane == k) ? rkk : (lane > k ? a[k] / rkk : 0.0);
-      a[k] = rk;
-#pragma unroll
-      for (int i = k + 1; i < 32; ++i) {
-        const double rki = __shfl_sync(0xffffffffu, rk, i);
-        if (lane > k) a[i] -= rki * rk;
-      }
+      inv = rsqrt(akk);
+      rk = (lane == k) ? akk * inv : (lane > k ? a[k] * inv : 0.0);
     } else {
-      a[k] = (lane == k) ? 1.0 : 0.0;  // beyond the breakdown: keep R_JJ invertible
+      rk = (lane == k) ? 1.0 : 0.0;  // beyond the breakdown: keep R_JJ invertible
     }
+    a[k] = rk;
+    Rd[k * kInvPitch + lane] = rk;
+    Dt[lane * kInvPitch + k] = rk;
+    __syncwarp();
+    const double rkm = lane > k ? rk : 0.0;
+    const double2* row = reinterpret_cast<const double2*>(Rd + k * kInvPitch);
+#pragma unroll
+    for (int i2 = (k + 1) / 2; i2 < 16; ++i2) {
+      const double2 v = row[i2];
+      if (2 * i2 > k) a[2 * i2] = fma(-v.x, rkm, a[2 * i2]);
+      if (2 * i2 + 1 > k) a[2 * i2 + 1] = fma(-v.y, rkm, a[2 * i2 + 1]);
+    }
+    const double2* col = reinterpret_cast<const double2*>(Dt + k * kInvPitch);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i2 = 0; 2 * i2 < k; ++i2) {
+      const double2 v = col[i2];
+      s0 = fma(v.x, z[2 * i2], s0);
+      if (2 * i2 + 1 < k) s1 = fma(v.y, z[2 * i2 + 1], s1);
+    }
+    z[k] = ((lane == k ? 1.0 : 0.0) - (s0 + s1)) * inv;
   }
   const bool colok = o + lane < ell;
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const double v = (k <= lane) ? a[k] : 0.0;
-    Rd[k * kInvPitch + lane] = v;
-    if (colok && o + k < ell && k <= lane) W[(o + k) + static_cast<int64_t>(o + lane) * ld] = v;
-  }
+  for (int k = 0; k < 32; ++k)
+    if (colok && o + k < ell && k <= lane) W[(o + k) + static_cast<int64_t>(o + lane) * ld] = a[k];
   __syncwarp();
-  double x[32];
 #pragma unroll
-  for (int i = 31; i >= 0; --i) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = i + 1; k < 32; ++k) s = fma(Rd[i * kInvPitch + k], x[k], s);
-    const double rii = Rd[i * kInvPitch + i];
-    x[i] = (i == lane) ? 1.0 / rii : ((i < lane) ? -s / rii : 0.0);
-  }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) Dt[i * kInvPitch + lane] = x[i];
+  for (int k = 0; k < 32; ++k) Dt[lane * kInvPitch + k] = z[k];  // (R^{-1})[lane][k] = Z[k][lane]
   __syncwarp();
   return brk;
 }
@@ -631,6 +646,371 @@ __global__ void __launch_bounds__(kCholThreads)
   if (tid == 0) rank_out[b] = r;
 }
 
+
+// ---------------------------------------------------------------------------
+// Grid-parallel unpivoted Cholesky + inverse (gchol).  The single-CTA kernels
+// above keep one item's whole factorization on one SM, which is latency bound
+// (~0.7 ms for l = 288, one CTA per item, the trailing matrix in L2).  gchol is
+// one persistent cooperative grid over all SMs; per 32-column block J:
+//   A  one warp per item factors the updated diagonal block (factor_diag_block:
+//      R_JJ and D_J = R_JJ^{-1}, breakdown -> numerical rank);
+//   B  warp tasks over (item, 32-column chunk): the block row
+//      R_J,right = D_J^T G_J,right, and the block column of the inverse
+//      T_I,J = -(sum_{K=I..J-1} T_I,K R_K,J) D_J  (T = R^{-1} built as R is);
+//   C  warp tasks over (item, upper 32 x 32 tile): the rank-32 trailing update
+//      G_right -= R_J,right^T R_J,right,
+// all products on DMMA (mma.sync m16n8k4 f64), operands from L2, with grid-wide
+// barriers between the phases.  Same outputs and breakdown rule as uchol_kernel.
+__device__ unsigned long long g_gc_trace[128];  // RSVD_GCHOL_TRACE: phase timestamps
+__device__ __forceinline__ void gc_mark(int& n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n < 128) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gc_trace[n] = t;
+  }
+  ++n;
+}
+
+constexpr int kGcThreads = 256;  // 8 warps: <= 255 registers, so the diagonal factor stays in registers
+constexpr int kGcWarps = kGcThreads / 32;
+constexpr int kGcDiagWarps = 2;  // warps per CTA with diagonal-factor smem
+
+struct GcholArgs {
+  double* G;
+  double* T;
+  double* Rfull;
+  double* scratch;
+  int* rank;
+  int* perm;
+  int ell, ellp;
+  double tau;
+  int64_t batch;
+  CholOpts o;
+};
+
+// acc (32 x 32, fragment layout) += A (32 x 32) * B (32 x 32), operands read
+// through the accessors; loads of 4 k-steps are issued before their DMMAs so
+// each group costs one memory round trip.
+template <class FA, class FB>
+__device__ __forceinline__ void warp_mma32(double (&acc)[2][4][4], FA&& Aat, FB&& Bat, int g,
+                                           int t) {
+#pragma unroll
+  for (int k1 = 0; k1 < 32; k1 += 16) {
+    double av[4][2][2], bv[4][4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k1 + kk * 4 + t;
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2) {
+        av[kk][a2][0] = Aat(a2 * 16 + g, k);
+        av[kk][a2][1] = Aat(a2 * 16 + g + 8, k);
+      }
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bv[kk][n] = Bat(k, n * 8 + g);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        dmma_16x8x4(acc[0][n], av[kk][0][0], av[kk][0][1], bv[kk][n]);
+        dmma_16x8x4(acc[1][n], av[kk][1][0], av[kk][1][1], bv[kk][n]);
+      }
+  }
+}
+
+__device__ __forceinline__ void zero_acc(double (&acc)[2][4][4]) {
+#pragma unroll
+  for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[a2][n][q] = 0.0;
+}
+
+// Store the fragment: f(i, c, value) for the 32 x 32 tile.
+template <class F>
+__device__ __forceinline__ void store_acc(const double (&acc)[2][4][4], F&& f, int g, int t) {
+#pragma unroll
+  for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        f(a2 * 16 + g + ((q & 2) ? 8 : 0), n * 8 + 2 * t + (q & 1), acc[a2][n][q]);
+}
+
+__device__ __forceinline__ double* gc_item_scratch(const GcholArgs& a, int64_t b) {
+  return a.scratch + b * 2 * static_cast<int64_t>(a.ellp) * a.ellp;
+}
+
+// Phase A for one item by one warp: factor the (updated) diagonal block J,
+// publish D_J (scratch) and T_JJ, lower the rank on breakdown.
+__device__ void gc_factor_diag(const GcholArgs& a, int64_t b, int J, double* Rd, double* Dt,
+                               int lane) {
+  const int ell = a.ell, ld = a.ellp, o = J * 32;
+  const int64_t sq = static_cast<int64_t>(ld) * ld;
+  double* W = a.G + b * sq;
+  double* S = gc_item_scratch(a, b);
+  double av[32];
+  const bool colok = o + lane < ell;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    av[i] = (colok && o + i < ell) ? __ldcg(W + (o + i) + static_cast<int64_t>(o + lane) * ld)
+                                   : (i == lane ? 1.0 : 0.0);
+  const int brk = factor_diag_block(av, W, ld, ell, o, S[2 * sq - 1], Rd, Dt, lane);
+  int r = a.rank[b];
+  if (brk < 32 && o + brk < r) r = o + brk;
+  double* Tb = a.T + b * sq;
+#pragma unroll 4
+  for (int i = 0; i < 32; ++i) {
+    const double x = Dt[i * kInvPitch + lane];
+    S[i * 32 + lane] = x;  // D_J, row-major
+    if (o + i < ell && o + lane < ell)
+      Tb[(o + i) + static_cast<int64_t>(o + lane) * ld] = (o + lane < r && i <= lane) ? x : 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) a.rank[b] = r;
+}
+
+// Grid-parallel unpivoted Cholesky + inverse.  Per 32-column block J
+// (right-looking, D_J = R_JJ^{-1}):
+//   B  R_J,c = D_J^T G_J,c (c > J) and T_I,J = -Acc_I,J D_J (I < J);
+//   C  G_x,y -= R_J,x^T R_J,y (upper tiles), Acc_I,J' (+)= T_I,J R_J,J'
+//      (I <= J < J'): the inverse is built right-looking too, so no task
+//      carries a chain longer than one 32 x 32 x 32 product; the diagonal block
+//      J+1 is updated first and factored by the same warp (lookahead).
+// Two grid barriers per block; a launch whose items are all gated off exits
+// before the first barrier.
+__global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_any;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int ell = a.ell, ld = a.ellp;
+  const int64_t sq = static_cast<int64_t>(ld) * ld;
+  const int64_t batch = a.batch;
+  const int nb = (ell + 31) / 32;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGcWarps + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kGcWarps;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int nmark = 0;
+  gc_mark(nmark);
+  // scratch per item: [0, 1024) D_J; [sq, 2 sq) Acc (strictly upper blocks);
+  // [2 sq - 2] go flag, [2 sq - 1] pivot floor (a diagonal block of Acc).
+  auto go_of = [&](int64_t b) -> double* { return gc_item_scratch(a, b) + 2 * sq - 2; };
+  auto gate = [&](int64_t b) {
+    int go = 1;
+    if (a.o.gate_rank) go = a.o.gate_rank[b] < ell;
+    if (a.o.mask && !a.o.mask[b]) go = 0;
+    return go;
+  };
+  // Every CTA evaluates the same predicate: all exit together or none does.
+  if (tid == 0) s_any = 0;
+  __syncthreads();
+  for (int64_t b = tid; b < batch; b += blockDim.x)
+    if (gate(b)) s_any = 1;
+  __syncthreads();
+  if (!s_any) {
+    if (a.o.ill_out)
+      for (int64_t b = gtid; b < batch; b += gstride) a.o.ill_out[b] = 0;
+    return;
+  }
+  for (int64_t b = gtid; b < batch; b += gstride) {
+    const int go = gate(b);
+    if (a.o.ill_out) a.o.ill_out[b] = (a.o.gate_rank && a.o.gate_rank[b] < ell) ? 1 : 0;
+    go_of(b)[0] = go ? 1.0 : 0.0;
+  }
+  grid.sync();
+  gc_mark(nmark);
+  for (int64_t e = gtid; e < batch * sq; e += gstride) {
+    const int64_t b = e / sq;
+    if (go_of(b)[0] == 0.0) continue;
+    if (a.o.Gsrc) a.G[e] = a.o.Gsrc[e];
+    a.T[e] = 0.0;
+  }
+  grid.sync();
+  gc_mark(nmark);
+  for (int64_t b = gw; b < batch; b += nw) {  // shift, pivot floor, initial rank
+    if (go_of(b)[0] == 0.0) continue;
+    double* W = a.G + b * sq;
+    double tr = 0.0, mx = 0.0;
+    for (int i = lane; i < ell; i += 32) {
+      const double d = W[i + static_cast<int64_t>(i) * ld];
+      tr += d;
+      mx = fmax(mx, d);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      tr += __shfl_xor_sync(0xffffffffu, tr, off);
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if (a.o.shift_coef > 0.0) {
+      const double sh = a.o.shift_coef * tr;
+      for (int i = lane; i < ell; i += 32) W[i + static_cast<int64_t>(i) * ld] += sh;
+      mx += sh;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      go_of(b)[1] = a.tau * mx;
+      a.rank[b] = (mx > 0.0) ? ell : 0;
+    }
+  }
+  grid.sync();
+  gc_mark(nmark);
+
+  const bool diag_warp = warp < kGcDiagWarps;
+  double* Rd = sm + (diag_warp ? warp : 0) * 2 * 32 * kInvPitch;
+  double* Dt = Rd + 32 * kInvPitch;
+  // Items whose diagonal factorizations this warp owns.
+  const int64_t d0 = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(warp) * gridDim.x;
+  const int64_t dstep = static_cast<int64_t>(gridDim.x) * kGcDiagWarps;
+  if (diag_warp)
+    for (int64_t b = d0; b < batch; b += dstep)
+      if (go_of(b)[0] != 0.0 && a.rank[b] > 0) gc_factor_diag(a, b, 0, Rd, Dt, lane);
+  grid.sync();
+  gc_mark(nmark);
+
+  const int64_t pw = static_cast<int64_t>(blockIdx.x) * (kGcWarps - kGcDiagWarps) + (warp - kGcDiagWarps);
+  const int64_t npw = static_cast<int64_t>(gridDim.x) * (kGcWarps - kGcDiagWarps);
+  for (int J = 0; J < nb; ++J) {
+    const int o = J * 32;
+    const int nr = nb - J - 1;  // blocks right of J
+    // ---- Phase B ----------------------------------------------------------
+    {
+      const int per = nr + J;
+      for (int64_t task = gw; task < batch * per; task += nw) {
+        const int64_t b = task / per;
+        const int idx = static_cast<int>(task - b * per);
+        if (go_of(b)[0] == 0.0) continue;
+        const int r = a.rank[b];
+        if (r <= o) continue;
+        double* W = a.G + b * sq;
+        const double* D = gc_item_scratch(a, b);
+        double acc[2][4][4];
+        zero_acc(acc);
+        if (idx < nr) {
+          if (r < o + 32) continue;  // broke down inside block J
+          const int cs = o + 32 + idx * 32;
+          warp_mma32(acc, [&](int i, int k) { return D[k * 32 + i]; },
+                     [&](int k, int c) {
+                       return cs + c < ell ? __ldcg(W + (o + k) + static_cast<int64_t>(cs + c) * ld)
+                                           : 0.0;
+                     },
+                     g, t);
+          store_acc(acc, [&](int i, int c, double v) {
+            if (cs + c < ell) W[(o + i) + static_cast<int64_t>(cs + c) * ld] = v;
+          }, g, t);
+        } else {
+          const int I = idx - nr;
+          const double* Acc = gc_item_scratch(a, b) + sq;
+          warp_mma32(acc,
+                     [&](int i, int k) {
+                       return __ldcg(Acc + (32 * I + i) + static_cast<int64_t>(o + k) * ld);
+                     },
+                     [&](int k, int c) { return D[k * 32 + c]; }, g, t);
+          double* Tb = a.T + b * sq;
+          store_acc(acc, [&](int i, int c, double v) {
+            if (o + c < ell) Tb[(32 * I + i) + static_cast<int64_t>(o + c) * ld] = (o + c < r) ? -v : 0.0;
+          }, g, t);
+        }
+      }
+    }
+    grid.sync();
+  gc_mark(nmark);
+    if (nr == 0) break;
+    // ---- Phase C (+ lookahead factor of block J+1) -----------------------
+    if (diag_warp) {
+      for (int64_t b = d0; b < batch; b += dstep) {
+        if (go_of(b)[0] == 0.0 || a.rank[b] < o + 32) continue;
+        double* W = a.G + b * sq;
+        const int x0 = o + 32;
+        double acc[2][4][4];
+        zero_acc(acc);
+        warp_mma32(acc,
+                   [&](int i, int k) {
+                     return x0 + i < ell ? __ldcg(W + (o + k) + static_cast<int64_t>(x0 + i) * ld) : 0.0;
+                   },
+                   [&](int k, int c) {
+                     return x0 + c < ell ? __ldcg(W + (o + k) + static_cast<int64_t>(x0 + c) * ld) : 0.0;
+                   },
+                   g, t);
+        store_acc(acc, [&](int i, int c, double v) {
+          if (x0 + i < ell && x0 + c < ell) W[(x0 + i) + static_cast<int64_t>(x0 + c) * ld] -= v;
+        }, g, t);
+        __syncwarp();
+        gc_factor_diag(a, b, J + 1, Rd, Dt, lane);
+      }
+    } else {
+      // Tile tasks per item: nr (nr + 1) / 2 - 1 trailing tiles (tx <= ty,
+      // without (0, 0)) then (J + 1) * nr inverse-accumulation tiles.
+      const int ntr = nr * (nr + 1) / 2 - 1;
+      const int per = ntr + (J + 1) * nr;
+      for (int64_t task = pw; task < batch * per; task += npw) {
+        const int64_t b = task / per;
+        int idx = static_cast<int>(task - b * per);
+        if (go_of(b)[0] == 0.0 || a.rank[b] < o + 32) continue;
+        double* W = a.G + b * sq;
+        double acc[2][4][4];
+        zero_acc(acc);
+        if (idx < ntr) {
+          idx += 1;
+          int ty = 0;
+          while (idx > ty) idx -= ++ty;
+          const int x0 = o + 32 + 32 * idx, y0 = o + 32 + 32 * ty;
+          warp_mma32(acc,
+                     [&](int i, int k) {
+                       return x0 + i < ell ? __ldcg(W + (o + k) + static_cast<int64_t>(x0 + i) * ld) : 0.0;
+                     },
+                     [&](int k, int c) {
+                       return y0 + c < ell ? __ldcg(W + (o + k) + static_cast<int64_t>(y0 + c) * ld) : 0.0;
+                     },
+                     g, t);
+          store_acc(acc, [&](int i, int c, double v) {
+            if (x0 + i < ell && y0 + c < ell) W[(x0 + i) + static_cast<int64_t>(y0 + c) * ld] -= v;
+          }, g, t);
+        } else {
+          idx -= ntr;
+          const int I = idx / nr, Jp = J + 1 + idx % nr;  // Acc_I,J' (+)= T_I,J R_J,J'
+          const double* Tb = a.T + b * sq;
+          double* Acc = gc_item_scratch(a, b) + sq;
+          warp_mma32(acc,
+                     [&](int i, int k) {
+                       return __ldcg(Tb + (32 * I + i) + static_cast<int64_t>(o + k) * ld);
+                     },
+                     [&](int k, int c) {
+                       return 32 * Jp + c < ell
+                                  ? __ldcg(W + (o + k) + static_cast<int64_t>(32 * Jp + c) * ld)
+                                  : 0.0;
+                     },
+                     g, t);
+          const bool first = I == J;
+          store_acc(acc, [&](int i, int c, double v) {
+            double* p = Acc + (32 * I + i) + static_cast<int64_t>(32 * Jp + c) * ld;
+            *p = first ? v : *p + v;
+          }, g, t);
+        }
+      }
+    }
+    grid.sync();
+  gc_mark(nmark);
+  }
+  // Epilogue: Rfull (rows < r, upper), identity permutation.
+  for (int64_t e = gtid; e < batch * sq; e += gstride) {
+    const int64_t b = e / sq;
+    if (go_of(b)[0] == 0.0) continue;
+    const int64_t rem = e - b * sq;
+    const int c = static_cast<int>(rem / ld), i = static_cast<int>(rem - static_cast<int64_t>(c) * ld);
+    if (a.Rfull) {
+      const int r = a.rank[b];
+      a.Rfull[e] = (i < r && i <= c && c < ell) ? a.G[e] : 0.0;
+    }
+    if (a.perm && c == 0) a.perm[b * ld + i] = i;
+  }
+}
+
 }  // namespace
 
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ellp * batch; }
@@ -642,6 +1022,42 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
   const int64_t pitch = ellp + 20;
   const int64_t big = std::max<int64_t>(PB * pitch, kInvSmem);
+  // gchol for the plain factorizations; the gated / masked calls of the
+  // ill-conditioned fallback (usually no item active) use the one-CTA-per-item
+  // kernel: cooperative launches replayed from a CUDA graph cost ~1 ms each
+  // even when every CTA exits at once (C2: 44.6 -> 24.3 ms per step).
+  static const bool gchol_all = std::getenv("RSVD_GCHOL_ALL") != nullptr;
+  if (!pivot && (!opts || gchol_all) && !std::getenv("RSVD_UCHOL") &&
+      !std::getenv("RSVD_PIVOT_ALWAYS")) {
+    GcholArgs ga{G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp),
+                 tau, batch, opts ? *opts : CholOpts{}};
+    const int bytes = kGcDiagWarps * 2 * 32 * kInvPitch * 8;
+    static int grid = 0;
+    if (grid == 0) {
+      RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes));
+      int per_sm = 0, dev = 0, sms = 0;
+      RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel, kGcThreads,
+                                                              bytes));
+      RSVD_CUDA(cudaGetDevice(&dev));
+      RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      if (per_sm < 1) throw CudaError("gchol_kernel: does not fit on an SM");
+      grid = per_sm * sms;
+    }
+    void* args[] = {&ga};
+    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel), dim3(grid),
+                                          dim3(kGcThreads), args, bytes, st));
+    RSVD_LAUNCH("gchol_kernel");
+    if (std::getenv("RSVD_GCHOL_TRACE")) {
+      unsigned long long tr[128] = {};
+      RSVD_CUDA(cudaStreamSynchronize(st));
+      RSVD_CUDA(cudaMemcpyFromSymbol(tr, g_gc_trace, sizeof(tr)));
+      std::fprintf(stderr, "gchol ell=%lld batch=%lld:", (long long)ell, (long long)batch);
+      for (int i = 1; i < 128 && tr[i] > tr[0]; ++i) std::fprintf(stderr, " %.1f", (tr[i] - tr[i - 1]) * 1e-3);
+      std::fprintf(stderr, "\n");
+    }
+    return;
+  }
   if (opts || (!pivot && !std::getenv("RSVD_PIVOT_ALWAYS"))) {
     const CholOpts o = opts ? *opts : CholOpts{};
     const int64_t ub = big * 8 + 2 * 32 * kInvPitch * 8 + 64;

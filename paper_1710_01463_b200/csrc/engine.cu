@@ -388,10 +388,11 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       if (pass == 0)
         RSVD_CUDA(cudaMemcpyAsync(B.G0, B.G, sizeof(double) * b * lp * lp,
                                   cudaMemcpyDeviceToDevice, st));
-      // Pass 1 on B^T pivots (QRCP order grades Rt for the Jacobi); elsewhere
-      // the unpivoted blocked kernel with breakdown detection gives the same
-      // span (RSVD_PIVOT_ALL=1 pivots every pass 1).
-      const bool pivot = (pass == 0 && (Rt || pivot_all())) || pivot_pass2();
+      // Unpivoted everywhere (grid-parallel gchol; breakdown -> numerical
+      // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
+      // Jacobi) measured no fewer sweeps: RSVD_BT_PIVOT=1 / RSVD_PIVOT_ALL=1.
+      static const bool bt_pivot = std::getenv("RSVD_BT_PIVOT") != nullptr;
+      const bool pivot = (pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2();
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
       if (pass == 0) {  // shifted retry of the items that stopped short of full rank
         CholOpts o;

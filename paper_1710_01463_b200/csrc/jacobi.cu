@@ -752,6 +752,12 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
   const char* env = std::getenv("RSVD_JACOBI_W");
   const int wforce = env ? std::atoi(env) : 0;
   if (!std::getenv("RSVD_JACOBI_OLD") && !std::getenv("RSVD_JACOBI_PAIRV")) {
+    // R = rows per lane: the smallest instantiation covering l (the column
+    // registers, smem pitch and dot products all scale with R).
+    if (ell <= 32 * 3 && !std::getenv("RSVD_JACOBI_R9"))
+      return launch_cyc_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_R9"))
+      return launch_cyc_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 9 && std::getenv("RSVD_JACOBI_MINB1"))
       return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 9) return launch_cyc_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);

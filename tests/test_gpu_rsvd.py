@@ -220,3 +220,79 @@ def test_host_pipelined_batch_equals_device(cuda, oracle_mod, monkeypatch):
         assert r == fd.ranks[b]
         assert rel_sigma_err(fh.sigma[b][:r].numpy(), fd.sigma[b][:r].cpu().numpy()) < 1e-13
         assert subspace_distance(fh.left[b][:, :r].numpy(), fd.left[b][:, :r].cpu().numpy()) < 1e-10
+
+
+def _steep_or_mild(oracle_mod, b, m, n):
+    """Even items: 2^-k spectrum (kappa(Y) >> tau^-1/2: the shifted-CholeskyQR
+    fallback runs); odd items: mild 0.97^k (plain CholeskyQR2)."""
+    sig = spectrum_family(0, min(m, n)) if b % 2 == 0 else 0.97 ** np.arange(min(m, n))
+    return matrix_with_spectrum(oracle_mod, 4100 + b, m, n, sig)
+
+
+def test_steep_spectrum_sampled_tail_matches_oracle(cuda, oracle_mod):
+    """Sampled values far below sqrt(tau) sigma_0 (the pivot floor) must carry
+    their true components like the reference's Householder bases: sigma and the
+    discarded weight of a 2^-k spectrum against the oracle."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = matrix_with_spectrum(oracle_mod, 41, 200, 150, spectrum_family(0, 150))
+    for k, ell, q in [(15, 40, 3), (10, 30, 0), (25, 50, 1)]:
+        f = rsvd(a, RsvdParams(k, ell, q, 4040 + q))
+        ref = oracle_mod.rsvd(a, k, ell, q, 4040 + q)
+        assert f.rank() == len(ref[1])
+        # kept values above ~1e-6 sigma_0 are resolvable to 1e-10 by any
+        # FP64 method; below that compare absolutely (u ||A|| scale)
+        big = ref[1] > 1e-6 * ref[1][0]
+        assert rel_sigma_err(f.sigma[big], ref[1][big]) < SIG_TOL
+        assert np.max(np.abs(f.sigma - ref[1])) < 1e-14 * ref[1][0]
+        assert f.discarded_weight == pytest.approx(ref[3], rel=1e-8, abs=1e-28)
+        assert isometry_err(f.left) < ISO_TOL and isometry_err(f.right_adj.T) < ISO_TOL
+
+
+def test_mixed_batch_fallback_masks(cuda, oracle_mod):
+    """A batch mixing ill-conditioned and mild items: the masked fallback passes
+    must touch only the ill items (every item against the oracle)."""
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, rsvd_batched
+
+    m, n, bsz = 256, 192, 6
+    mats = [_steep_or_mild(oracle_mod, b, m, n) for b in range(bsz)]
+    seeds = [300 + b for b in range(bsz)]
+    A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
+    bf = rsvd_batched(A, RsvdParams(20, 48, 2, 0), seeds)
+    for b in range(bsz):
+        ref = oracle_mod.rsvd(mats[b], 20, 48, 2, seeds[b])
+        fb = bf.item(b)
+        S = fb.sigma.cpu().numpy()
+        assert fb.rank() == len(ref[1]), b
+        big = ref[1] > 1e-6 * ref[1][0]
+        assert rel_sigma_err(S[big], ref[1][big]) < SIG_TOL, b
+        assert fb.discarded_weight == pytest.approx(ref[3], rel=1e-8, abs=1e-28), b
+        assert isometry_err(fb.left.cpu().numpy()) < ISO_TOL, b
+
+
+def test_rank_deficient_items_in_batch(cuda, oracle_mod):
+    """Exact-rank items (Y rank deficient: the fallback plus basis completion)
+    next to full-rank ones; the zero matrix too."""
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd_batched
+
+    m, n = 96, 80
+    mats = [matrix_with_spectrum(oracle_mod, 70, m, n, [3.0, 2.0, 1.0]),
+            matrix_with_spectrum(oracle_mod, 71, m, n, 0.9 ** np.arange(n)),
+            np.zeros((m, n)),
+            matrix_with_spectrum(oracle_mod, 72, m, n, [5.0] * 7)]
+    seeds = [5, 6, 7, 8]
+    A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
+    bf = rsvd_batched(A, RsvdParams(10, 20, 2, 0), seeds)
+    for b, a in enumerate(mats):
+        ref = oracle_mod.rsvd(a, 10, 20, 2, seeds[b])
+        fb = bf.item(b)
+        fb.left, fb.sigma, fb.right_adj = (x.cpu().numpy() for x in (fb.left, fb.sigma,
+                                                                    fb.right_adj))
+        assert fb.rank() == len(ref[1]), b
+        if fb.rank():
+            assert rel_sigma_err(fb.sigma, ref[1]) < SIG_TOL, b
+            assert isometry_err(fb.left) < ISO_TOL, b
+        if b != 1:
+            assert reconstruction_error(a, fb) <= 1e-10 * max(np.linalg.norm(a), 1.0), b
