@@ -18,6 +18,7 @@
 // whose pivot falls below tau * max pivot (rank deficiency) are replaced by
 // a deterministic Gaussian completion that the second pass orthonormalises,
 // so the result always has l orthonormal columns (lapack.hpp:18-20).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -194,13 +195,15 @@ struct rsvd_context {
   std::unique_ptr<rsvd::Reducer> red;  // row-sharded calls (NCCL or in-process group)
   // Host-pointer pipelining: copy-in / copy-out streams and per-slot events.
   cudaStream_t s_in = nullptr, s_out = nullptr, s_c2 = nullptr;
-  cudaEvent_t ev_slot_in[2] = {}, ev_slot_comp[2] = {}, ev_slot_out[2] = {};
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t ev_slot_in[kMaxChunks] = {}, ev_slot_comp[kMaxChunks] = {},
+              ev_slot_out[kMaxChunks] = {};
   void ensure_pipeline() {
     if (s_in) return;
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_c2, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMaxChunks; ++i) {
       RSVD_CUDA(cudaEventCreateWithFlags(&ev_slot_in[i], cudaEventDisableTiming));
       RSVD_CUDA(cudaEventCreateWithFlags(&ev_slot_comp[i], cudaEventDisableTiming));
       RSVD_CUDA(cudaEventCreateWithFlags(&ev_slot_out[i], cudaEventDisableTiming));
@@ -211,7 +214,7 @@ struct rsvd_context {
     cudaStreamDestroy(s_in);
     cudaStreamDestroy(s_out);
     cudaStreamDestroy(s_c2);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMaxChunks; ++i) {
       cudaEventDestroy(ev_slot_in[i]);
       cudaEventDestroy(ev_slot_comp[i]);
       cudaEventDestroy(ev_slot_out[i]);
@@ -581,98 +584,143 @@ void copy_batch(void* dst, int64_t dld, int64_t dstride, const void* src, int64_
             sld, rows, cols, kind, st);
 }
 
-// Core batched rsvd on device or host pointers.
-// Number of chunks for the host-pointer path: enough A bytes to be worth
-// overlapping the PCIe copies with compute, and big enough chunks to keep
-// the GEMMs full (>= 64 MB of A per chunk).
+// Number of chunks for the host-pointer path (overlap of the PCIe copies
+// with compute); RSVD_HOST_CHUNKS overrides.
 int64_t host_chunks(int64_t batch, int64_t m, int64_t n) {
-  if (const char* e = std::getenv("RSVD_HOST_CHUNKS")) return std::max<int64_t>(1, std::atoi(e));
-  // Two chunks on two compute streams measured best on C4 (141 ms vs 171 ms
-  // serial; 4 chunks 146 ms): more chunks repeat the latency-bound stages.
+  if (const char* e = std::getenv("RSVD_HOST_CHUNKS"))
+    return std::min<int64_t>(rsvd_context::kMaxChunks, std::max<int64_t>(1, std::atoi(e)));
+  // Each chunk has its own staging, so the H2D stream never waits for a slot;
+  // chunks of >= 512 MB keep the GEMMs full (C4: 4 chunks of 8 items).
   const int64_t per = m * n * 8;
   if (batch < 2 || per * batch < (int64_t(256) << 20)) return 1;
-  return 2;
+  const int64_t by_size = std::max<int64_t>(1, per * batch / (int64_t(512) << 20));
+  return std::max<int64_t>(2, std::min<int64_t>({by_size, batch, 4}));
 }
 
-// Host-pointer batched rsvd with copies overlapped: chunk c's H2D (stream
-// s_in) and chunk c-1's D2H (stream s_out) run under chunk c's... compute on
-// the handle stream; two device slots for A and the factors.
+// Host-pointer batched rsvd with the PCIe transfers overlapped: chunk c's H2D
+// (stream s_in) runs while earlier chunks compute; chunks alternate between
+// two compute streams, so one chunk's latency-bound stages (Cholesky, Jacobi)
+// overlap the next chunk's GEMMs; factors return on s_out.  Every chunk has
+// its own device staging and workspace (no slot reuse, no copy-engine stalls).
 void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, const double* A,
                          int64_t lda, int64_t strideA, double* U, int64_t ldu, int64_t strideU,
                          double* S, int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt) {
   const int64_t batch = full.batch, m = full.m, n = full.n, k = full.k;
-  const int64_t cb = ceil_div(batch, nchunks);
+  // Equal chunk sizes (a shorter last chunk measured no better on C4: the
+  // GPU, not the tail, is the limit).  RSVD_HOST_SPLIT="a,b,c" overrides.
+  std::vector<int64_t> sizes;
+  if (const char* e = std::getenv("RSVD_HOST_SPLIT")) {
+    int64_t tot = 0;
+    for (const char* p = e; *p && tot < batch;) {
+      const int64_t v = std::max<int64_t>(1, std::atoll(p));
+      sizes.push_back(std::min(v, batch - tot));
+      tot += sizes.back();
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    if (tot < batch) sizes.push_back(batch - tot);
+  } else {
+    const int64_t cb = ceil_div(batch, nchunks);
+    for (int64_t tot = 0; tot < batch; tot += cb) sizes.push_back(std::min(cb, batch - tot));
+  }
+  nchunks = static_cast<int64_t>(std::min<size_t>(sizes.size(), rsvd_context::kMaxChunks));
+  std::vector<int64_t> off(nchunks + 1, 0);
+  for (int64_t c = 0; c < nchunks; ++c) off[c + 1] = off[c] + sizes[c];
+  const int64_t cb = *std::max_element(sizes.begin(), sizes.begin() + nchunks);
   h->ensure_pipeline();
   cudaStream_t st = h->stream;
   Shape sc = full;
   sc.batch = cb;
-  // Two workspaces and two compute streams: consecutive chunks run
-  // concurrently, so one chunk's latency-bound stages (Cholesky, Jacobi)
-  // overlap the other chunk's GEMMs as well as the PCIe copies.
-  auto layout = [&](Carver& c, Buffers* B, double** Ah, double** Uh, double** Sh, double** Vh) {
-    for (int sl = 0; sl < 2; ++sl) {
-      B[sl] = carve(c, sc, false, true);
-      Ah[sl] = c.take<double>(cb * m * n);
-      Uh[sl] = c.take<double>(cb * m * k);
-      Sh[sl] = c.take<double>(cb * k);
-      Vh[sl] = c.take<double>(cb * k * n);
+  std::vector<Buffers> B(nchunks);
+  std::vector<double*> Ah(nchunks), Uh(nchunks), Sh(nchunks), Vh(nchunks);
+  auto layout = [&](Carver& c) {
+    for (int64_t q = 0; q < nchunks; ++q) {
+      B[q] = carve(c, sc, false, true);
+      Ah[q] = c.take<double>(cb * m * n);
+      Uh[q] = c.take<double>(cb * m * k);
+      Sh[q] = c.take<double>(cb * k);
+      Vh[q] = c.take<double>(cb * k * n);
     }
   };
-  Buffers B[2];
-  double *Ah[2], *Uh[2], *Sh[2], *Vh[2];
   Carver meas{nullptr};
-  layout(meas, B, Ah, Uh, Sh, Vh);
+  layout(meas);
   char* const before = h->arena.base;
   h->arena.reserve(meas.off + 256);
   if (h->arena.base != before) h->drop_graphs();
   Carver cv{h->arena.base};
-  layout(cv, B, Ah, Uh, Sh, Vh);
+  layout(cv);
   cudaStream_t cs[2] = {st, h->s_c2};
   // Order the side streams after whatever the caller queued on its stream.
   RSVD_CUDA(cudaEventRecord(h->ev_in, st));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c2, h->ev_in, 0));
+  // RSVD_PIPE_TRACE: event timeline of the chunks (ms from the call start).
+  static const bool trace = std::getenv("RSVD_PIPE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t q) {
+    if (!trace) return;
+    cudaEvent_t e;
+    RSVD_CUDA(cudaEventCreate(&e));
+    RSVD_CUDA(cudaEventRecord(e, q));
+    tev.push_back(e);
+  };
+  mark(st);
+  // All H2D copies first (one stream, back to back), then the compute chain.
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int sl = static_cast<int>(c & 1);
-    const int64_t b0 = c * cb, nb = std::min(cb, batch - b0);
-    if (nb <= 0) break;
-    cudaStream_t q = cs[sl];
-    if (c >= 2) RSVD_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_slot_out[sl], 0));
-    copy_batch(Ah[sl], m, m * n, A + b0 * strideA, lda, strideA, m, n, nb, cudaMemcpyHostToDevice,
+    const int64_t b0 = off[c], nb = sizes[c];
+    copy_batch(Ah[c], m, m * n, A + b0 * strideA, lda, strideA, m, n, nb, cudaMemcpyHostToDevice,
                h->s_in);
-    RSVD_CUDA(cudaEventRecord(h->ev_slot_in[sl], h->s_in));
-    RSVD_CUDA(cudaStreamWaitEvent(q, h->ev_slot_in[sl], 0));
+    RSVD_CUDA(cudaEventRecord(h->ev_slot_in[c], h->s_in));
+    mark(h->s_in);
+  }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t b0 = off[c], nb = sizes[c];
+    cudaStream_t q = cs[c & 1];
+    RSVD_CUDA(cudaStreamWaitEvent(q, h->ev_slot_in[c], 0));
+    mark(q);
     Shape s = sc;
     s.batch = nb;
-    Buffers Bq = B[sl];
-    Bq.prof = (sl == 0) ? &h->prof : nullptr;
+    Buffers Bq = B[c];
+    Bq.prof = (c == 0) ? &h->prof : nullptr;
     Bq.red = nullptr;
     RSVD_CUDA(cudaMemcpyAsync(Bq.seeds, h->pin.seeds + b0, sizeof(uint64_t) * nb,
                               cudaMemcpyHostToDevice, q));
-    const CMatRef Ad{Ah[sl], m, m * n};
+    const CMatRef Ad{Ah[c], m, m * n};
     range_finder(s, Bq, Ad, q);
-    svd_stage(s, Bq, Ad, MatRef{Uh[sl], m, m * k}, Sh[sl], k, MatRef{Vh[sl], k, k * n}, q);
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + b0, B[sl].rankF, sizeof(int) * nb,
+    svd_stage(s, Bq, Ad, MatRef{Uh[c], m, m * k}, Sh[c], k, MatRef{Vh[c], k, k * n}, q);
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + b0, B[c].rankF, sizeof(int) * nb,
                               cudaMemcpyDeviceToHost, q));
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch + b0, B[sl].sweeps, sizeof(int) * nb,
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch + b0, B[c].sweeps, sizeof(int) * nb,
                               cudaMemcpyDeviceToHost, q));
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls + b0, B[sl].dw, sizeof(double) * nb,
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls + b0, B[c].dw, sizeof(double) * nb,
                               cudaMemcpyDeviceToHost, q));
-    RSVD_CUDA(cudaEventRecord(h->ev_slot_comp[sl], q));
-    RSVD_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_slot_comp[sl], 0));
-    copy_batch(U + b0 * strideU, ldu, strideU, Uh[sl], m, m * k, m, k, nb, cudaMemcpyDeviceToHost,
+    mark(q);
+    RSVD_CUDA(cudaEventRecord(h->ev_slot_comp[c], q));
+    RSVD_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_slot_comp[c], 0));
+    copy_batch(U + b0 * strideU, ldu, strideU, Uh[c], m, m * k, m, k, nb, cudaMemcpyDeviceToHost,
                h->s_out);
-    copy_batch(Vt + b0 * strideVt, ldvt, strideVt, Vh[sl], k, k * n, k, n, nb,
+    copy_batch(Vt + b0 * strideVt, ldvt, strideVt, Vh[c], k, k * n, k, n, nb,
                cudaMemcpyDeviceToHost, h->s_out);
-    copy_batch(S + b0 * strideS, k, strideS, Sh[sl], k, k, k, 1, nb, cudaMemcpyDeviceToHost,
+    copy_batch(S + b0 * strideS, k, strideS, Sh[c], k, k, k, 1, nb, cudaMemcpyDeviceToHost,
                h->s_out);
-    RSVD_CUDA(cudaEventRecord(h->ev_slot_out[sl], h->s_out));
+    mark(h->s_out);
   }
   RSVD_CUDA(cudaStreamSynchronize(h->s_out));
   RSVD_CUDA(cudaStreamSynchronize(st));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c2));
   RSVD_CUDA(cudaStreamSynchronize(h->s_in));
+  if (trace && !tev.empty()) {
+    // h2d ends per chunk, then per chunk: compute start, compute end, d2h end
+    std::fprintf(stderr, "pipe:");
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, " %.1f", ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
 }
 
 void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n,

@@ -15,6 +15,7 @@
 // fit, otherwise in global memory (L2-resident).
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <cfloat>
@@ -521,6 +522,8 @@ void launch_pairv_t(double* H, double* J, int64_t ell, int64_t ellp, int max_swe
 // product through the update; norms are tracked through the exact 2 x 2
 // rotation; rotations accumulate into V and J_pair <- J_pair V runs once per
 // task on DMMA straight from global memory.
+__device__ long long g_jc_trace[64];  // RSVD_JACOBI_TRACE
+
 template <int R, int MINB>
 __global__ void __launch_bounds__(512, MINB)
     jacobi_cyc_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
@@ -539,7 +542,7 @@ __global__ void __launch_bounds__(512, MINB)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
 
   const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -572,6 +575,8 @@ __global__ void __launch_bounds__(512, MINB)
           bp = min(p, q), bq = max(p, q);
         }
         if (bp * W >= ell) continue;  // both blocks are padding
+        if (sweep == 0 && blockIdx.x == 0 && task == blockIdx.x && tid == 0 && phase < 4)
+          g_jc_trace[phase * 8 + 5] = clock64();
         double* Hg = H + item * sq;
         double* Jg = J + item * sq;
         auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
@@ -586,6 +591,8 @@ __global__ void __launch_bounds__(512, MINB)
         }
         if (tid == 0) s_rot = 0;
         __syncthreads();
+        const bool trace = sweep == 0 && blockIdx.x == 0 && task == blockIdx.x && tid == 0 && phase < 4;
+        if (trace) g_jc_trace[phase * 8 + 0] = clock64();
         for (int c = warp; c < NC; c += W) {
           double a = 0.0;
 #pragma unroll
@@ -613,19 +620,22 @@ __global__ void __launch_bounds__(512, MINB)
           double* hi = Hs + i * pitch;
           double* hj = Hs + jx * pitch;
           double xi[R], xj[R];
-          double ga = 0.0;
+          double ga0 = 0.0, ga1 = 0.0;
 #pragma unroll
           for (int u = 0; u < R; ++u) {
             xi[u] = hi[lane + 32 * u];
             xj[u] = hj[lane + 32 * u];
-            ga = fma(xi[u], xj[u], ga);
+            if (u & 1) ga1 = fma(xi[u], xj[u], ga1);
+            else ga0 = fma(xi[u], xj[u], ga0);
           }
-          ga = warp_sum(ga);
+          const double ga = warp_sum(ga0 + ga1);
           const double al = nrm[i], be = nrm[jx];
-          if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          // Rutishauser's rotation with two divisions, one sqrt, one rsqrt;
+          // the test |g| > tol sqrt(al be) squared (no square roots).
+          if (al > 0.0 && be > 0.0 && ga * ga > tol2 * al * be) {
             const double zeta = (be - al) / (2.0 * ga);
-            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + tt * tt);
+            const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double c = rsqrt(fma(tt, tt, 1.0));
             const double sn = c * tt;
 #pragma unroll
             for (int u = 0; u < R; ++u) {
@@ -648,6 +658,7 @@ __global__ void __launch_bounds__(512, MINB)
           }
           __syncthreads();
         }
+        if (trace) g_jc_trace[phase * 8 + 1] = clock64();
         if (rotated && lane == 0) atomicOr(&s_rot, 1);
         for (int e = tid; e < NC * pitch; e += blockDim.x) {
           const int c = e / pitch, r = e - c * pitch;
@@ -655,6 +666,7 @@ __global__ void __launch_bounds__(512, MINB)
           if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
         }
         __syncthreads();
+        if (trace) g_jc_trace[phase * 8 + 2] = clock64();
         if (s_rot) {  // J_pair <- J_pair V (warp per 16-row slab, DMMA)
           const int slabs = (ell + 15) / 16;
           for (int sl = warp; sl < slabs; sl += W) {
@@ -697,9 +709,11 @@ __global__ void __launch_bounds__(512, MINB)
           }
         }
         __syncthreads();
+        if (trace) g_jc_trace[phase * 8 + 3] = clock64();
         if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
       }
       grid.sync();
+      if (sweep == 0 && blockIdx.x == 0 && tid == 0 && phase < 4) g_jc_trace[phase * 8 + 4] = clock64();
     }
     int all = 1;
     for (int64_t i = 0; i < batch; ++i) {
@@ -741,6 +755,16 @@ void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
   RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512),
                                         args, bytes, st));
   RSVD_LAUNCH("jacobi_cyc_kernel");
+  if (std::getenv("RSVD_JACOBI_TRACE")) {
+    long long tr[64] = {};
+    RSVD_CUDA(cudaStreamSynchronize(st));
+    RSVD_CUDA(cudaMemcpyFromSymbol(tr, g_jc_trace, sizeof(tr)));
+    std::fprintf(stderr, "jacobi_cyc R=%d ell=%lld batch=%lld grid=%d\n", R, (long long)ell, (long long)batch, grid);
+    for (int ph = 0; ph < 4; ++ph)
+      std::fprintf(stderr, "  phase %d: load %lld steps %lld store %lld jupd %lld sync+idle %lld cycles\n", ph,
+                   tr[ph * 8 + 0] - tr[ph * 8 + 5], tr[ph * 8 + 1] - tr[ph * 8 + 0], tr[ph * 8 + 2] - tr[ph * 8 + 1],
+                   tr[ph * 8 + 3] - tr[ph * 8 + 2], tr[ph * 8 + 4] - tr[ph * 8 + 3]);
+  }
 }
 
 }  // namespace
@@ -758,6 +782,13 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
       return launch_cyc_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_R9"))
       return launch_cyc_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    // Few tasks (one or two items): one CTA per SM is enough, and the
+    // 128-register instantiations do not spill.
+    int nbt = static_cast<int>((ell + 15) / 16);
+    nbt += nbt & 1;
+    const bool few = batch * (nbt / 2) <= kNumSMs;
+    if (few && ell <= 32 * 5) return launch_cyc_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    if (few && ell <= 32 * 9) return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 9 && std::getenv("RSVD_JACOBI_MINB1"))
       return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 9) return launch_cyc_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);

@@ -261,12 +261,17 @@ def tsvd_batched(a, chi: int, handle: Optional[_lib.Handle] = None) -> BatchedFa
 
 
 def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
-                 handle: Optional[_lib.Handle] = None) -> BatchedFactorization:
+                 handle: Optional[_lib.Handle] = None, out: Optional[BatchedFactorization] = None
+                 ) -> BatchedFactorization:
     """Batched rsvd: ``a`` is (batch, m, n) with column-major items (a CUDA
     tensor whose items have strides (1, m), or a numpy array of shape
-    (batch, m, n)); item b uses ``seeds[b]``."""
+    (batch, m, n)); item b uses ``seeds[b]``.  ``out`` (torch inputs only):
+    a previous result of the same shapes and device whose buffers are reused,
+    e.g. pinned host factors in a loop (no per-call pinned allocation)."""
     lib = _lib.load()
     h = handle or _lib.default_handle()
+    if out is not None and hasattr(a, "data_ptr"):
+        return _rsvd_batched_into(lib, h, a, params, seeds, out)
     if _is_torch_cuda(a):
         import torch
 
@@ -328,6 +333,42 @@ def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
     if flags == _lib.PTR_HOST and Ub is not None:
         U = np.transpose(Ub, (0, 2, 1))
         Vt = np.transpose(Vb, (0, 2, 1))
+    return BatchedFactorization(U, S, Vt, [int(ranks[i]) for i in range(bsz)],
+                                [float(dws[i]) for i in range(bsz)])
+
+
+def _rsvd_batched_into(lib, h, a, params, seeds, out):
+    import torch
+
+    if a.dim() != 3 or a.dtype != torch.float64:
+        raise InvalidArgument("rsvd_batched: expected a (batch, m, n) float64 tensor")
+    bsz, m, n = a.shape
+    if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
+        a = a.transpose(1, 2).contiguous().transpose(1, 2)
+    k = max(int(params.rank), 1)
+    U, S, Vt = out.left, out.sigma, out.right_adj
+    ok = (tuple(U.shape) == (bsz, m, k) and U.stride() == (m * k, 1, m) and
+          tuple(S.shape) == (bsz, k) and S.is_contiguous() and
+          tuple(Vt.shape) == (bsz, k, n) and Vt.stride() == (k * n, 1, k) and
+          all(x.device == a.device and x.dtype == torch.float64 for x in (U, S, Vt)))
+    if not ok:
+        raise InvalidArgument("rsvd_batched: out= buffers do not match the input shapes")
+    if len(seeds) != bsz:
+        raise InvalidArgument("rsvd_batched: need one seed per item")
+    seeds_arr = (ctypes.c_uint64 * max(bsz, 1))(*[int(s) & _MASK for s in seeds])
+    ranks = (ctypes.c_int64 * max(bsz, 1))()
+    dws = (ctypes.c_double * max(bsz, 1))()
+    flags = _lib.PTR_DEVICE if a.is_cuda else _lib.PTR_HOST
+    if flags == _lib.PTR_DEVICE:
+        _torch_stream_guard(h)
+    try:
+        rc = lib.rsvd_f64_batched(h.raw, bsz, a.data_ptr(), m, n, m, m * n, params.rank,
+                                  params.oversample, params.power, seeds_arr, U.data_ptr(), m,
+                                  m * k, S.data_ptr(), k, Vt.data_ptr(), k, k * n, ranks, dws, flags)
+    finally:
+        if flags == _lib.PTR_DEVICE:
+            lib.rsvd_set_stream(h.raw, None)
+    _lib.raise_for(rc, h.raw)
     return BatchedFactorization(U, S, Vt, [int(ranks[i]) for i in range(bsz)],
                                 [float(dws[i]) for i in range(bsz)])
 

@@ -296,3 +296,27 @@ def test_rank_deficient_items_in_batch(cuda, oracle_mod):
             assert isometry_err(fb.left) < ISO_TOL, b
         if b != 1:
             assert reconstruction_error(a, fb) <= 1e-10 * max(np.linalg.norm(a), 1.0), b
+
+
+def test_batched_out_buffers_reused(cuda, oracle_mod):
+    """rsvd_batched(..., out=prev) writes into the previous result's buffers
+    (pinned host factors reused in a loop) with identical values."""
+    import torch
+    from paper_1710_01463_b200 import InvalidArgument, RsvdParams, rsvd_batched
+
+    m, n, bsz = 96, 80, 4
+    mats = [matrix_with_spectrum(oracle_mod, 600 + b, m, n, 0.9 ** np.arange(n)) for b in range(bsz)]
+    seeds = [11 + b for b in range(bsz)]
+    host = torch.from_numpy(np.stack([x.T for x in mats])).transpose(1, 2).pin_memory()
+    p = RsvdParams(10, 20, 2, 0)
+    first = rsvd_batched(host, p, seeds)
+    ptr = first.left.data_ptr()
+    again = rsvd_batched(host, p, seeds, out=first)
+    assert again.left.data_ptr() == ptr
+    ref = rsvd_batched(host, p, seeds)
+    assert torch.equal(again.sigma, ref.sigma) and torch.equal(again.left, ref.left)
+    dev = rsvd_batched(host.to(cuda), p, seeds)
+    dev2 = rsvd_batched(host.to(cuda), p, seeds, out=dev)
+    assert torch.equal(dev2.sigma.cpu(), ref.sigma)
+    with pytest.raises(InvalidArgument, match="out= buffers"):
+        rsvd_batched(host[:2], p, seeds[:2], out=first)
