@@ -13,7 +13,9 @@ UNIT = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0
         "second": 1e3, "s": 1e3}
 
 
-def launches(path):
+def launches(path, which="engine"):
+    """which="engine": only the engine's kernels (rsvd:: namespace) -- the
+    bench command also runs torch kernels that build the synthetic inputs."""
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, data = rows[hi], rows[hi + 1:]
@@ -22,7 +24,10 @@ def launches(path):
     for r in data:
         if len(r) <= vi:
             continue
+        if which == "engine" and "rsvd::" not in r[ki] and "unnamed>::" not in r[ki]:
+            continue
         name = r[ki].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        name = name.replace("rsvd::<unnamed>::", "")
         ms = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
@@ -67,4 +72,4 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report}[sys.argv[1]](*sys.argv[2:])
