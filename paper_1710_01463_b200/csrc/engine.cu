@@ -371,10 +371,12 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
     if (sharded) B.red->allreduce_sum(B.G, b * lp * lp, st);  // G = sum_p Y_p^T Y_p
   };
-  auto apply = [&](const MatRef& in, const MatRef& out, const int* mask) {
-    // out = (in P) R11^{-1}: pivot-gathered columns, upper-triangular right factor.
+  auto apply = [&](const MatRef& in, const MatRef& out, const int* mask, bool pivoted) {
+    // out = (in P) R11^{-1}: pivot-gathered columns (only when this pass
+    // pivoted; without the column map the TMA GEMM takes it), upper-triangular
+    // right factor.
     GemmOpts tri;
-    tri.colmapA = B.perm;
+    tri.colmapA = pivoted ? B.perm : nullptr;
     tri.colmap_stride = lp;
     tri.b_upper = true;
     tri.item_mask = mask;
@@ -385,6 +387,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     const MatRef& out = pass == 0 ? Tm : Y;
     double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
     int* rk = pass == 0 ? B.rank1 : B.rank2;
+    bool pivot = false;
     gram(in, nullptr);
     {
       Scope sc(P, kStChol, st);
@@ -395,7 +398,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
       // Jacobi) measured no fewer sweeps: RSVD_BT_PIVOT=1 / RSVD_PIVOT_ALL=1.
       static const bool bt_pivot = std::getenv("RSVD_BT_PIVOT") != nullptr;
-      const bool pivot = (pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2();
+      pivot = (pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2();
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
       if (pass == 0) {  // shifted retry of the items that stopped short of full rank
         CholOpts o;
@@ -411,7 +414,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     }
     {
       Scope sc(P, kStApply, st);
-      apply(in, out, nullptr);
+      apply(in, out, nullptr, pivot);
       launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global,
                             st);
     }
@@ -426,7 +429,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
                      kPivotTau, false, b, st, &o);
       }
       Scope sc(P, kStApply, st);
-      apply(out, in, B.ill);
+      apply(out, in, B.ill, false);
       launch_complete_basis(in, rows, s.ell, B.rank2, B.seeds, tag + 0x40, b, row_off, rows_global,
                             st, B.ill);
       launch_masked_copy(B.ill, in, out, rows, lp, b, st);
