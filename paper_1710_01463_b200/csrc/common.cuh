@@ -90,7 +90,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
                const int* item_mask,
-               bool b_upper, cudaStream_t st);
+               bool b_upper, cudaStream_t st, int tile = 0);
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch);
 
 // chol.cu — pivoted / plain Cholesky of SPD Grams (ell x ell, ld ell).

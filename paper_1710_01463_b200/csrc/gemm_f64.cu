@@ -373,9 +373,18 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 }  // namespace
 
-int64_t dgemm_partial_elems(bool, int64_t M, int64_t N, int64_t K, int64_t batch) {
+int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch) {
   const Choice c = choose(M, N, K, batch);
-  return c.splits > 1 ? static_cast<int64_t>(c.splits) * batch * M * N : 0;
+  int64_t splits = c.splits;
+  if (trans_a && M == N && M % 96 == 0) {  // the 96 x 96 Gram tiling of dgemm_ex
+    const int64_t t = M / 96, tiles = t * (t + 1) / 2 * batch;
+    int64_t sp = 1;
+    if (tiles < 2 * kNumSMs) sp = std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / 256));
+    sp = std::max<int64_t>(1, std::min<int64_t>(sp, 64));
+    sp = ceil_div(K, round_up(ceil_div(K, sp), kBK));
+    splits = std::max(splits, sp);
+  }
+  return splits > 1 ? splits * batch * M * N : 0;
 }
 
 void dgemm(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, MatRef C,
@@ -388,6 +397,20 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
               cudaStream_t st) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   Choice c = choose(M, N, K, batch);
+  // Symmetric Gram of a 96-multiple width: 96 x 96 TMA tiles (the 128 x 96
+  // tile leaves a partial row tile and computes ~40% more than the upper half).
+  const bool sq96 = opt.c_upper && trans_a && M == N && M % 96 == 0 && !opt.colmapA &&
+                    !std::getenv("RSVD_NO_GRAM96");
+  if (sq96) {
+    const int64_t t = M / 96;
+    const int64_t tiles = t * (t + 1) / 2 * batch;
+    int64_t splits = 1;
+    if (tiles < 2 * kNumSMs) splits = std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / 256));
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
+    int64_t kps = round_up(ceil_div(K, splits), kBK);
+    splits = ceil_div(K, kps);
+    c.bm = 96, c.bn = 96, c.splits = static_cast<int>(splits), c.kps = kps;
+  }
   if (K <= 0) c.splits = 1, c.kps = kBK;
   const int64_t need = c.splits > 1 ? static_cast<int64_t>(c.splits) * batch * M * N : 0;
   if (need > partial_capacity) {
@@ -415,9 +438,11 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool vec2 = aligned16(A.base) && aligned16(B.base) && (A.ld % 2 == 0) &&
                     (B.ld % 2 == 0) && (A.stride % 2 == 0) && (B.stride % 2 == 0) &&
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
-  const bool tma_done = !a.colmapA && c.bm == 128 && c.bn == 96 &&
+  const bool tma_done = !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
                         dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
-                                  c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st);
+                                  c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st,
+                                  sq96 ? 1 : 0);
+  if (sq96 && !tma_done) throw CudaError("dgemm: 96x96 Gram tile needs the TMA path");
   if (tma_done) {
   } else if (trans_a) {
     if (vec2) dispatch<true, 2>(c, a, st);

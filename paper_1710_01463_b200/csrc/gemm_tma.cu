@@ -260,19 +260,19 @@ int tma_stages() {
   return s;
 }
 
-template <int STAGES, bool TRANS_A>
+template <int STAGES, bool TRANS_A, int BM = kBM, int BN = kBN, int WM = kWM, int WN = kWN>
 void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& a, cudaStream_t st) {
-  auto kern = dgemm_tma_kernel<kBM, kBN, kWM, kWN, STAGES, TRANS_A>;
-  const size_t bytes = static_cast<size_t>(STAGES) * (kBM + kBN) * kTBK * 8 + 1024;
+  auto kern = dgemm_tma_kernel<BM, BN, WM, WN, STAGES, TRANS_A>;
+  const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * kTBK * 8 + 1024;
   static bool attr = false;
   if (!attr) {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(bytes)));
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(a.N, kBN)), static_cast<unsigned>(ceil_div(a.M, kBM)),
+  dim3 grid(static_cast<unsigned>(ceil_div(a.N, BN)), static_cast<unsigned>(ceil_div(a.M, BM)),
             static_cast<unsigned>(a.batch * a.splits));
-  kern<<<grid, kWM * kWN * 32, bytes, st>>>(ma, mb, a);
+  kern<<<grid, WM * WN * 32, bytes, st>>>(ma, mb, a);
   RSVD_LAUNCH("dgemm_tma_kernel");
 }
 
@@ -285,7 +285,10 @@ bool tma_gemm_enabled() {
 
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
-               const int* item_mask, bool b_upper, cudaStream_t st) {
+               const int* item_mask, bool b_upper, cudaStream_t st, int tile) {
+  // tile 0: 128 x 96 (8 warps as 4 x 2); tile 1: 96 x 96 (2 x 4 warps) for the
+  // symmetric Gram of a 96-multiple l_p (no partial 128-row tiles).
+  const int bm = tile == 1 ? 96 : kBM, bn = tile == 1 ? 96 : kBN;
   if (!tma_gemm_enabled()) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al16(A.base) || !al16(B.base)) return false;
@@ -300,26 +303,31 @@ bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N),
                                 static_cast<cuuint64_t>(batch)};
     const cuuint64_t str[2] = {static_cast<cuuint64_t>(B.ld) * 8, static_cast<cuuint64_t>(sB) * 8};
-    const cuuint32_t box[3] = {kTBK, kBN, 1};
+    const cuuint32_t box[3] = {kTBK, static_cast<cuuint32_t>(bn), 1};
     if (!make_map(&mb, B.base, 3, dims, str, box)) return false;
   }
   if (trans_a) {
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M),
                                 static_cast<cuuint64_t>(batch)};
     const cuuint64_t str[2] = {static_cast<cuuint64_t>(A.ld) * 8, static_cast<cuuint64_t>(sA) * 8};
-    const cuuint32_t box[3] = {kTBK, kBM, 1};
+    const cuuint32_t box[3] = {kTBK, static_cast<cuuint32_t>(bm), 1};
     if (!make_map(&ma, A.base, 3, dims, str, box)) return false;
   } else {
     const cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 16),
                                 static_cast<cuuint64_t>(batch)};
     const cuuint64_t str[3] = {static_cast<cuuint64_t>(A.ld) * 8, 128,
                                static_cast<cuuint64_t>(sA) * 8};
-    const cuuint32_t box[4] = {16, kTBK, kBM / 16, 1};
+    const cuuint32_t box[4] = {16, kTBK, static_cast<cuuint32_t>(bm / 16), 1};
     if (!make_map(&ma, A.base, 4, dims, str, box)) return false;
   }
   TmaArgs a{M, N, K, C, ldc, strideC, batch, splits, kps, c_upper ? 1 : 0, b_upper ? 1 : 0,
             item_mask};
   const int stg = tma_stages();
+  if (tile == 1) {
+    if (trans_a) launch<3, true, 96, 96, 2, 4>(ma, mb, a, st);
+    else launch<3, false, 96, 96, 2, 4>(ma, mb, a, st);
+    return true;
+  }
   if (trans_a) {
     if (stg == 3) launch<3, true>(ma, mb, a, st);
     else launch<4, true>(ma, mb, a, st);
