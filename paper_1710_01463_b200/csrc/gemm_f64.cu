@@ -438,7 +438,10 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool vec2 = aligned16(A.base) && aligned16(B.base) && (A.ld % 2 == 0) &&
                     (B.ld % 2 == 0) && (A.stride % 2 == 0) && (B.stride % 2 == 0) &&
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
-  const bool tma_done = !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
+  static const bool no_tma_apply = std::getenv("RSVD_NO_TMA_APPLY") != nullptr;
+  static const bool no_tma_mask = std::getenv("RSVD_NO_TMA_MASK") != nullptr;
+  const bool tma_ok = !(no_tma_apply && a.b_upper) && !(no_tma_mask && opt.item_mask);
+  const bool tma_done = tma_ok && !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
                         dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
                                   c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st,
                                   sq96 ? 1 : 0);

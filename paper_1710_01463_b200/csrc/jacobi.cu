@@ -534,6 +534,7 @@ __global__ void __launch_bounds__(512, MINB)
   constexpr int W = 16, NC = 32, VP = NC + 4;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
   const int pitch = 32 * R;
   double* Hs = sm;                  // NC x pitch
   double* Vs = sm + NC * pitch;     // NC x VP, column-major V[c*VP + k]
@@ -550,7 +551,11 @@ __global__ void __launch_bounds__(512, MINB)
     const int64_t rem = e % sq;
     J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
   }
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
+  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
   for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
   grid.sync();
 
@@ -559,8 +564,12 @@ __global__ void __launch_bounds__(512, MINB)
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
     if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
     for (int phase = 0; phase < nb; ++phase) {
       const bool diag = phase == 0;
       for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
@@ -589,7 +598,10 @@ __global__ void __launch_bounds__(512, MINB)
           const int c = e / VP, r = e - c * VP;
           Vs[e] = (r == c) ? 1.0 : 0.0;
         }
-        if (tid == 0) s_rot = 0;
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
         __syncthreads();
         const bool trace = sweep == 0 && blockIdx.x == 0 && task == blockIdx.x && tid == 0 && phase < 4;
         if (trace) g_jc_trace[phase * 8 + 0] = clock64();
@@ -605,6 +617,7 @@ __global__ void __launch_bounds__(512, MINB)
         }
         __syncthreads();
         int rotated = 0;
+        double wmax = 0.0;  // max g^2 / (alpha beta) over this warp's rotations
         const int steps = diag ? 15 : 16;
         for (int s2 = 0; s2 < steps; ++s2) {
           int i, jx;
@@ -633,6 +646,7 @@ __global__ void __launch_bounds__(512, MINB)
           // Rutishauser's rotation with two divisions, one sqrt, one rsqrt;
           // the test |g| > tol sqrt(al be) squared (no square roots).
           if (al > 0.0 && be > 0.0 && ga * ga > tol2 * al * be) {
+            wmax = fmax(wmax, (ga * ga) / (al * be));
             const double zeta = (be - al) / (2.0 * ga);
             const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
             const double c = rsqrt(fma(tt, tt, 1.0));
@@ -659,7 +673,10 @@ __global__ void __launch_bounds__(512, MINB)
           __syncthreads();
         }
         if (trace) g_jc_trace[phase * 8 + 1] = clock64();
-        if (rotated && lane == 0) atomicOr(&s_rot, 1);
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          atomicMax(&s_mx, static_cast<unsigned long long>(__double_as_longlong(wmax)));
+        }
         for (int e = tid; e < NC * pitch; e += blockDim.x) {
           const int c = e / pitch, r = e - c * pitch;
           const int gc = gcol(c);
@@ -710,20 +727,30 @@ __global__ void __launch_bounds__(512, MINB)
         }
         __syncthreads();
         if (trace) g_jc_trace[phase * 8 + 3] = clock64();
-        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
+        if (tid == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
       }
       grid.sync();
       if (sweep == 0 && blockIdx.x == 0 && tid == 0 && phase < 4) g_jc_trace[phase * 8 + 4] = clock64();
     }
+    // An item is done after a sweep with no rotation, or after a sweep whose
+    // largest rotated |g| / sqrt(alpha beta) was below 1e-9: the cyclic
+    // method converges quadratically, so that sweep left every off-diagonal
+    // ratio near 1e-18, far under tol (the no-op check sweep is skipped).
+    auto done = [&](int64_t i) {
+      return __ldcg(fl + i) == 0u || __longlong_as_double(static_cast<long long>(__ldcg(mxs + i))) < 1e-18;
+    };
     int all = 1;
     for (int64_t i = 0; i < batch; ++i) {
-      const unsigned f = __ldcg(fl + i);
-      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || f == 0u);
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
     }
     __syncthreads();
     for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (__ldcg(fl + i) == 0u) conv[i] = 1;
+      if (done(i)) conv[i] = 1;
     __syncthreads();
     if (all) break;
   }
@@ -769,7 +796,9 @@ void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
 
 }  // namespace
 
-int64_t jacobi_flag_elems(int64_t batch) { return 3 * batch; }
+// 3 rotating "rotated" flags per item, then (8-byte aligned) 3 rotating
+// per-item maxima of g^2 / (alpha beta) as double bits (jacobi_cyc_kernel).
+int64_t jacobi_flag_elems(int64_t batch) { return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch; }
 
 void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
                            int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
