@@ -66,20 +66,28 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("RSVD_BENCH_NO_CLOCKS"):  # diagnosis only
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except (OSError, ValueError):
             self.proc = None
-        time.sleep(0.15)
+        time.sleep(0.5)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def mark(self):
+        """Start of the timed region: only later samples are summarised.
+        The sampler itself is started before the warm-up -- nvidia-smi's NVML
+        initialisation stalled the first timed steps by up to 100 ms."""
+        self.first = len(self.lines)
 
     def stop(self):
         if not self.proc:
@@ -91,7 +99,9 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        for ln in self.lines:
+        first = getattr(self, "first", 0)
+        lines = self.lines[first:] if len(self.lines) > first else self.lines
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -205,11 +215,12 @@ def run_rowsharded(args, rank, world, local_rank):
     params = RsvdParams(cfg.rank, cfg.ell, cfg.power, seed)
     h = Handle(local_rank)
     sharding.attach_nccl(h, world, rank)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     for _ in range(args.warmup):
         sharding.rsvd_rowsharded(a_loc, cfg.m, first, params, h)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
+    clocks.mark()
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.kernel_launches()
@@ -294,24 +305,42 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    # Factors are written into the same device buffers every step (out=): a
+    # fresh 0.5 GB allocation per step made the second timed step re-allocate
+    # and re-capture its CUDA graph (+3 .. +100 ms).
+    f = None
     for _ in range(args.warmup):
-        rsvd_batched(A, params, seeds, handle=h)
+        f = rsvd_batched(A, params, seeds, handle=h, out=f)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region --------------------------------
-    clocks = ClockSampler(local_rank)
-    clocks.start()
+    clocks.mark()
     barrier()
     torch.cuda.synchronize()
     launches0 = _lib.kernel_launches()
     stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    verbose = bool(os.environ.get("RSVD_BENCH_VERBOSE"))
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if verbose else []
+    host_t = []
     e0.record(stream)
-    for _ in range(args.steps):
-        f = rsvd_batched(A, params, seeds, handle=h)
+    for i in range(args.steps):
+        th = time.perf_counter()
+        f = rsvd_batched(A, params, seeds, handle=h, out=f)
+        if verbose:
+            step_ev[i].record(stream)
+            host_t.append(round((time.perf_counter() - th) * 1e3, 2))
     e1.record(stream)
     torch.cuda.synchronize()
+    if verbose:
+        prev, dev_t = e0, []
+        for ev in step_ev:
+            dev_t.append(round(prev.elapsed_time(ev), 2))
+            prev = ev
+        print("step device ms:", dev_t, "host ms:", host_t, file=sys.stderr)
     barrier()
     launches = _lib.kernel_launches() - launches0
     clk = clocks.stop()

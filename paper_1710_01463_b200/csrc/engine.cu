@@ -829,6 +829,9 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
                   (long long)ell, (long long)ldu, (long long)strideU, (long long)strideS,
                   (long long)ldvt * 1000003LL + strideVt, power, (void*)B.red,
                   (long long)s.m_global, (long long)s.row_off);
+    // Keys include the caller's buffers: callers that allocate fresh outputs
+    // every call (instead of reusing them) would grow the cache without bound.
+    if (h->graphs.size() >= 64 && h->graphs.find(keybuf) == h->graphs.end()) h->drop_graphs();
     GraphEntry& ge = h->graphs[std::string(keybuf)];
     if (!ge.exec && !ge.failed) {
       cudaGraph_t g = nullptr;

@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(512, MINB)
         }
         __syncthreads();
         int rotated = 0;
-        double wmax = 0.0;  // max g^2 / (alpha beta) over this warp's rotations
+        int big = 0;  // a rotation with g^2 >= 1e-18 alpha beta happened
         const int steps = diag ? 15 : 16;
         for (int s2 = 0; s2 < steps; ++s2) {
           int i, jx;
@@ -643,12 +643,21 @@ __global__ void __launch_bounds__(512, MINB)
           }
           const double ga = warp_sum(ga0 + ga1);
           const double al = nrm[i], be = nrm[jx];
-          // Rutishauser's rotation with two divisions, one sqrt, one rsqrt;
-          // the test |g| > tol sqrt(al be) squared (no square roots).
-          if (al > 0.0 && be > 0.0 && ga * ga > tol2 * al * be) {
-            wmax = fmax(wmax, (ga * ga) / (al * be));
-            const double zeta = (be - al) / (2.0 * ga);
-            const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          // Rutishauser's rotation; the test |g| > tol sqrt(al be) squared (no
+          // square roots).  t = sign(d) 2g / (|d| + sqrt(d^2 + 4 g^2)), d = be - al:
+          // one division (the zeta form needs two) unless d, g are extreme.
+          const double gg = ga * ga, ab = al * be;
+          if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
+            big |= gg >= 1e-18 * ab;
+            const double d = be - al, g2 = 2.0 * ga;
+            const double mag = fmax(fabs(d), fabs(g2));
+            double tt;
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
             const double c = rsqrt(fma(tt, tt, 1.0));
             const double sn = c * tt;
 #pragma unroll
@@ -675,7 +684,7 @@ __global__ void __launch_bounds__(512, MINB)
         if (trace) g_jc_trace[phase * 8 + 1] = clock64();
         if (rotated && lane == 0) {
           atomicOr(&s_rot, 1);
-          atomicMax(&s_mx, static_cast<unsigned long long>(__double_as_longlong(wmax)));
+          if (big) atomicMax(&s_mx, 1ull);
         }
         for (int e = tid; e < NC * pitch; e += blockDim.x) {
           const int c = e / pitch, r = e - c * pitch;
@@ -740,7 +749,7 @@ __global__ void __launch_bounds__(512, MINB)
     // method converges quadratically, so that sweep left every off-diagonal
     // ratio near 1e-18, far under tol (the no-op check sweep is skipped).
     auto done = [&](int64_t i) {
-      return __ldcg(fl + i) == 0u || __longlong_as_double(static_cast<long long>(__ldcg(mxs + i))) < 1e-18;
+      return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull;
     };
     int all = 1;
     for (int64_t i = 0; i < batch; ++i) {
@@ -797,7 +806,7 @@ void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
 }  // namespace
 
 // 3 rotating "rotated" flags per item, then (8-byte aligned) 3 rotating
-// per-item maxima of g^2 / (alpha beta) as double bits (jacobi_cyc_kernel).
+// per-item "a rotation with g^2 >= 1e-18 alpha beta" flags (jacobi_cyc_kernel).
 int64_t jacobi_flag_elems(int64_t batch) { return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch; }
 
 void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
