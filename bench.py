@@ -147,6 +147,32 @@ def cpu_oracle_rsvd(A_items, cfg, seeds, threads):
     return times
 
 
+def cpu_modes(A_items, cfg, seeds, threads, budget_s):
+    """the reference protocol (1 BLAS thread) and all host cores,
+    for both methods -- rsvd and full-SVD truncation (tsvd = dgesdd +
+    truncate) -- on the first matrix of the sample; each mode is skipped once
+    the accumulated CPU time passes `budget_s`."""
+    from oracle import oracle
+
+    a, s = A_items[0], seeds[0]
+    out, spent = {}, 0.0
+    for name, fn, th in (("rsvd_1thread", lambda: oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), 1),
+                         ("rsvd_all_cores", lambda: oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), threads),
+                         ("tsvd_all_cores", lambda: oracle.tsvd(a, cfg.rank), threads),
+                         ("tsvd_1thread", lambda: oracle.tsvd(a, cfg.rank), 1)):
+        if spent > budget_s:
+            out[name] = None
+            continue
+        oracle.set_threads(th)
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        spent += dt
+        out[name] = {"value": 1.0 / dt, "unit": "truncations/s", "cores": th}
+    oracle.set_threads(threads)
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -405,6 +431,9 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"{len(times)} of the {B} {cfg.m}x{cfg.n} matrices, oracle rsvd "
                          "(restated reference: cblas_dgemm + dgeqrf/dorgqr + dgesdd, "
                          "OpenBLAS 0.3.31), all host threads"}
+        cpu["modes"] = cpu_modes(mats, cfg, seeds, threads, args.cpu_modes_budget)
+        cpu["modes"]["sample"] = (f"item 0 ({cfg.m}x{cfg.n}); a mode is skipped (null) once "
+                                  f"{args.cpu_modes_budget:.0f} s of CPU time were spent")
 
     if rank == 0:
         falg = f_alg(cfg.m, cfg.n, cfg.rank, cfg.ell, cfg.power)
@@ -454,6 +483,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2)
     ap.add_argument("--ref-sample", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-modes-budget", type=float, default=45.0,
+                    help="seconds of CPU time for the 1-thread / tsvd baseline modes")
     ap.add_argument("--rowshard", action="store_true",
                     help="row-sharded single-matrix path (default for C3/C5 when N > 1)")
     args = ap.parse_args()
