@@ -803,6 +803,338 @@ void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-split block-cyclic Jacobi for few items (jacobi_clu_kernel).  Same sweep
+// order, rotations, norm tracking and convergence rules as jacobi_cyc_kernel,
+// but every (item, block pair) task is owned by a thread-block CLUSTER of S
+// CTAs, CTA q holding rows [q * 32 RL, (q + 1) * 32 RL) of the 32 columns and
+// of J: each column-pair dot product is a warp-local partial sum, published in
+// shared memory and reduced across the cluster through DSMEM in a fixed rank
+// order (so every CTA derives bit-identical rotations), one cluster barrier
+// per rotation step.  A single 4096^2 matrix (9 block pairs) then runs on 45
+// SMs instead of 9, each with 1/5 of the rows.
+template <int RL>
+__global__ void __launch_bounds__(512, 1)
+    jacobi_clu_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                      int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int W = 16, NC = 32, VP = NC + 4, PITCH = 32 * RL;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
+  __shared__ double pd[2][W];  // per-warp partial dots, double-buffered by step parity
+  __shared__ double pn[NC];    // per-column partial norms
+  double* Hs = sm;              // NC x PITCH (local rows)
+  double* Vs = sm + NC * PITCH;  // NC x VP
+  double* nrm = Vs + NC * VP;    // NC
+  int* conv = reinterpret_cast<int*>(nrm + NC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int S = static_cast<int>(cluster.num_blocks());
+  const int q = static_cast<int>(cluster.block_rank());
+  const int row0 = q * PITCH;  // first global row of this CTA
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
+  const int64_t nclu = gridDim.x / S;
+  const int64_t clu = blockIdx.x / S;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = clu; task < tasks; task += nclu) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = rr_player(k, phase - 1, nb), qq = rr_player(nb - 1 - k, phase - 1, nb);
+          bp = min(p, qq), bq = max(p, qq);
+        }
+        if (bp * W >= ell) continue;  // both blocks are padding (uniform in the cluster)
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        for (int e = tid; e < NC * PITCH; e += blockDim.x) {
+          const int c = e / PITCH, r = row0 + (e - c * PITCH);
+          const int gc = gcol(c);
+          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
+        }
+        for (int e = tid; e < NC * VP; e += blockDim.x) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
+        __syncthreads();
+        for (int c = warp; c < NC; c += W) {
+          double a = 0.0;
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            const double x = Hs[c * PITCH + lane + 32 * u];
+            a = fma(x, x, a);
+          }
+          a = warp_sum(a);
+          if (lane == 0) pn[c] = a;
+        }
+        cluster.sync();
+        for (int c = tid; c < NC; c += blockDim.x) {
+          double a = 0.0;
+          for (int r = 0; r < S; ++r) a += *cluster.map_shared_rank(&pn[c], r);
+          nrm[c] = a;
+        }
+        cluster.sync();  // pn reads done before the next task rewrites it; nrm visible
+        int rotated = 0, big = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int i, jx;
+          if (diag) {
+            const int blk = warp >> 3, pi = warp & 7;
+            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
+            i = blk * 16 + min(a0, b0);
+            jx = blk * 16 + max(a0, b0);
+          } else {
+            i = warp;
+            jx = 16 + ((warp + s2) & 15);
+          }
+          double* hi = Hs + i * PITCH;
+          double* hj = Hs + jx * PITCH;
+          double xi[RL], xj[RL];
+          double ga = 0.0;
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            xi[u] = hi[lane + 32 * u];
+            xj[u] = hj[lane + 32 * u];
+            ga = fma(xi[u], xj[u], ga);
+          }
+          ga = warp_sum(ga);
+          const int buf = s2 & 1;
+          if (lane == 0) pd[buf][warp] = ga;
+          cluster.sync();
+          ga = 0.0;
+          for (int r = 0; r < S; ++r) ga += *cluster.map_shared_rank(&pd[buf][warp], r);
+          const double al = nrm[i], be = nrm[jx];
+          const double gg = ga * ga, ab = al * be;
+          if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
+            big |= gg >= 1e-18 * ab;
+            const double d = be - al, g2 = 2.0 * ga;
+            const double mag = fmax(fabs(d), fabs(g2));
+            double tt;
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
+            const double c = rsqrt(fma(tt, tt, 1.0));
+            const double sn = c * tt;
+#pragma unroll
+            for (int u = 0; u < RL; ++u) {
+              hi[lane + 32 * u] = c * xi[u] - sn * xj[u];
+              hj[lane + 32 * u] = sn * xi[u] + c * xj[u];
+            }
+            {
+              double* vi = Vs + i * VP;
+              double* vj = Vs + jx * VP;
+              const double x = vi[lane], y = vj[lane];
+              vi[lane] = c * x - sn * y;
+              vj[lane] = sn * x + c * y;
+            }
+            __syncwarp();
+            if (lane == 0) {
+              nrm[i] = al - tt * ga;
+              nrm[jx] = be + tt * ga;
+            }
+            rotated = 1;
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          if (big) atomicMax(&s_mx, 1ull);
+        }
+        for (int e = tid; e < NC * PITCH; e += blockDim.x) {
+          const int c = e / PITCH, r = row0 + (e - c * PITCH);
+          const int gc = gcol(c);
+          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
+        }
+        __syncthreads();
+        if (s_rot) {  // local rows of J_pair <- J_pair V (warp per 16-row slab, DMMA)
+          const int slabs = PITCH / 16;
+          for (int sl = warp; sl < slabs; sl += W) {
+            const int r0 = row0 + sl * 16;
+            double acc[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              double afr[4][2];
+#pragma unroll
+              for (int kq = 0; kq < 4; ++kq) {
+                const int gc = gcol((h2 * 4 + kq) * 4 + t4);
+                const bool okc = gc < ell;
+                const int ra = r0 + g, rb = r0 + g + 8;
+                afr[kq][0] =
+                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
+                afr[kq][1] =
+                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
+              }
+#pragma unroll
+              for (int kq = 0; kq < 4; ++kq)
+#pragma unroll
+                for (int n = 0; n < NC / 8; ++n) {
+                  const double bv = Vs[(n * 8 + g) * VP + (h2 * 4 + kq) * 4 + t4];
+                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                const int c = n * 8 + 2 * t4 + (qq & 1);
+                const int gc = gcol(c);
+                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
+              }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && q == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
+      }
+      grid.sync();
+    }
+    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (done(i)) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int RL>
+bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                  unsigned* flags, int64_t batch, int S, cudaStream_t st) {
+  const size_t bytes = (static_cast<size_t>(32) * 32 * RL + 32 * 36 + 32) * sizeof(double) +
+                       batch * sizeof(int) + 16;
+  auto kern = jacobi_clu_kernel<RL>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(bytes)) != cudaSuccess ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(S);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cfg.gridDim = dim3(static_cast<unsigned>(S));
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(tasks, max_clusters));
+  cfg.gridDim = dim3(static_cast<unsigned>(ncl * S));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
+  if (cudaLaunchKernelEx(&cfg, kern, H, J, ell_i, ellp_i, nb, batch, max_sweeps, flags, sweeps) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  RSVD_LAUNCH("jacobi_clu_kernel");
+  return true;
+}
+
+// Cluster size and rows per lane for the row-split kernel (S <= 6 and the
+// clusters of all tasks co-resident), rounded so the S slices cover l.
+bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                unsigned* flags, int64_t batch, cudaStream_t st) {
+  if (std::getenv("RSVD_NO_JACOBI_CLUSTER")) return false;
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int R = static_cast<int>((ell + 31) / 32);
+  // Per step the cluster barrier competes with the per-CTA rotation work:
+  // 5-6 CTAs per task measured best (C3: S 3/5/9 -> 4.6/4.4/4.8 ms, C5:
+  // S 3/5/9 -> 11.1/9.7/18.7 ms -- at 9 the clusters no longer fit at once).
+  int smax = static_cast<int>(std::min<int64_t>(6, kNumSMs / std::max<int64_t>(tasks, 1)));
+  if (const char* e = std::getenv("RSVD_JACOBI_CLUSTER")) smax = std::atoi(e);
+  if (smax < 2) return false;
+  int rl = (R + smax - 1) / smax;
+  static const int kRL[] = {1, 2, 3, 4, 6};
+  int pick = 0;
+  while (pick < 4 && kRL[pick] < rl) ++pick;
+  if (kRL[pick] < rl) return false;
+  rl = kRL[pick];
+  const int S = (R + rl - 1) / rl;
+  if (S < 2) return false;
+  switch (rl) {
+    case 1: return launch_clu_t<1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    case 2: return launch_clu_t<2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    case 3: return launch_clu_t<3>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    case 4: return launch_clu_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    default: return launch_clu_t<6>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+  }
+}
+
 }  // namespace
 
 // 3 rotating "rotated" flags per item, then (8-byte aligned) 3 rotating
@@ -825,6 +1157,10 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
     int nbt = static_cast<int>((ell + 15) / 16);
     nbt += nbt & 1;
     const bool few = batch * (nbt / 2) <= kNumSMs;
+    // Fewer tasks than SMs / 2: split every task's rows over a cluster.
+    if (batch * (nbt / 2) * 2 <= kNumSMs &&
+        launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
+      return;
     if (few && ell <= 32 * 5) return launch_cyc_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (few && ell <= 32 * 9) return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 9 && std::getenv("RSVD_JACOBI_MINB1"))
@@ -853,6 +1189,13 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st) {
   const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
+  {
+    int nbt = static_cast<int>((ell + 15) / 16);
+    nbt += nbt & 1;
+    if (batch * (nbt / 2) * 2 <= kNumSMs &&
+        launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
+      return;
+  }
   if (bytes <= 220 * 1024) {
     // Whole problem fits one CTA's shared memory: one CTA per item.
     RSVD_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
