@@ -1157,8 +1157,10 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
     int nbt = static_cast<int>((ell + 15) / 16);
     nbt += nbt & 1;
     const bool few = batch * (nbt / 2) <= kNumSMs;
-    // Fewer tasks than SMs / 2: split every task's rows over a cluster.
-    if (batch * (nbt / 2) * 2 <= kNumSMs &&
+    // Fewer tasks than SMs / 4: split every task's rows over a cluster (with
+    // more tasks the clusters would occupy most SMs, which costs more than it
+    // saves when another stream's GEMMs run beside, e.g. the host pipeline).
+    if (batch * (nbt / 2) * 4 <= kNumSMs &&
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
     if (few && ell <= 32 * 5) return launch_cyc_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
@@ -1192,7 +1194,7 @@ void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_swee
   {
     int nbt = static_cast<int>((ell + 15) / 16);
     nbt += nbt & 1;
-    if (batch * (nbt / 2) * 2 <= kNumSMs &&
+    if (batch * (nbt / 2) * 4 <= kNumSMs &&
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
   }
