@@ -315,7 +315,9 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   const int64_t w64 = round_up(N, 64), w96 = round_up(N, 96);
   if (N <= 32) c.bn = 32;
   else if (N <= 64) c.bn = 64;
-  else c.bn = (w96 <= w64) ? 96 : 64;
+  // 96-wide tiles take the TMA kernel (~25% faster per flop): worth up to
+  // 12.5% padding (N = 256: lift 1.97 -> 1.70 ms on C4).
+  else c.bn = (8 * w96 <= 9 * w64) ? 96 : 64;
   c.bm = (M <= 64) ? 64 : 128;
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
   const int64_t target = 2 * kNumSMs;  // two resident CTAs per SM
