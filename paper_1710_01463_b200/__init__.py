@@ -2,8 +2,8 @@
 
 Drop-in for the factorization path of rlftn (arXiv 1710.01463's
 TEBD bond compression): ``rsvd``, ``randomized_range``,
-``reconstruction_error``, ``tsvd``, ``block_factorize`` and the seed/RNG
-contract, computed by hand-written
+``reconstruction_error``, ``tsvd``, ``block_factorize``, the TEBD bond update
+(``tebd.apply_gate`` / ``apply_gate_layer``) and the seed/RNG contract, computed by hand-written
 sm_100a CUDA kernels in ``librsvd_b200.so`` behind the C ABI of
 ``include/rsvd_c.h``.
 """
@@ -21,7 +21,8 @@ from .factorize import (
     tsvd_batched,
 )
 from .blocks import (BlockDiagMatrix, BlockFactorization, BlockMethod, RankPolicy,
-                     SectorRankRequest, block_factorize, sector_request)
+                     SectorRankRequest, block_factorize, block_factorize_many, sector_request)
+from . import models, tebd  # noqa: E402  (TEBD bond update: SURVEY 8f row 3)
 from .rng import CounterRng, derive_seed, mix64, seed_tag
 
 __all__ = [
@@ -29,5 +30,6 @@ __all__ = [
     "LibraryMissing", "NumericalError", "RsvdParams", "TruncatedFactorization", "derive_seed",
     "mix64", "randomized_range", "reconstruction_error", "rsvd", "rsvd_batched", "seed_tag",
     "tsvd", "tsvd_batched", "BlockDiagMatrix", "BlockFactorization", "BlockMethod", "RankPolicy",
-    "SectorRankRequest", "block_factorize", "sector_request",
+    "SectorRankRequest", "block_factorize", "block_factorize_many", "sector_request", "models",
+    "tebd",
 ]

@@ -120,64 +120,83 @@ def _stack(blocks: List[Any]):
     return np.stack([np.asarray(x, dtype=np.float64) for x in blocks])
 
 
-def block_factorize(a: BlockDiagMatrix, chi: int, request: SectorRankRequest,
-                    method: BlockMethod, handle: Optional[_lib.Handle] = None
-                    ) -> BlockFactorization:
-    """rlftn::block_factorize (blocks.cpp:38-118) on the GPU engine."""
+def _validate(a: BlockDiagMatrix) -> None:
     if len(a.blocks) != len(a.charges):
         raise InvalidArgument("block_factorize: charges/blocks size mismatch")
     if not a.blocks:
         raise InvalidArgument("block_factorize: no sectors")
     if len(set(a.charges)) != len(a.charges):
         raise InvalidArgument("block_factorize: duplicate sector charge")
-    req = replace(request, chi=chi)
-    dims = [min(_shape(b)) for b in a.blocks]
-    want = sector_request(req, dims)
 
-    nsec = len(a.blocks)
-    factors: List[Optional[TruncatedFactorization]] = [None] * nsec
-    exact = True
-    # Group sectors that share one engine call: (route, shape, parameters).
-    groups: Dict[tuple, List[int]] = {}
-    for s in range(nsec):
-        if want[s] == 0 or dims[s] == 0:
-            factors[s] = _empty_factor(a.blocks[s])
-            continue
-        m, n = _shape(a.blocks[s])
-        if method.kind == "rsvd" and dims[s] >= method.rsvd_min_dim:
-            ov = method.rsvd.oversample
-            ell = min(max(ov, want[s]), dims[s]) if ov > 0 else min(2 * want[s], dims[s])
-            key = ("rsvd", m, n, want[s], ell, method.rsvd.power)
-            exact = False
-        else:
-            key = ("tsvd", m, n, want[s])
-        groups.setdefault(key, []).append(s)
+
+def block_factorize_many(mats: Sequence[BlockDiagMatrix], chi: int, request: SectorRankRequest,
+                         method: BlockMethod, handle: Optional[_lib.Handle] = None
+                         ) -> List[BlockFactorization]:
+    """block_factorize of several block-diagonal matrices (e.g. the bonds of
+    one TEBD layer) with their sector blocks pooled: every group of equal
+    (route, shape, rank, sample width) blocks -- across matrices -- is one
+    engine call.  Per matrix the result equals block_factorize."""
+    for a in mats:
+        _validate(a)
+    req = replace(request, chi=chi)
+    plans = []  # per matrix: (dims, want)
+    factors: List[List[Optional[TruncatedFactorization]]] = []
+    exact = []
+    groups: Dict[tuple, List[Tuple[int, int]]] = {}
+    for mi, a in enumerate(mats):
+        dims = [min(_shape(b)) for b in a.blocks]
+        want = sector_request(req, dims)
+        plans.append((dims, want))
+        factors.append([None] * len(a.blocks))
+        exact.append(True)
+        for s in range(len(a.blocks)):
+            if want[s] == 0 or dims[s] == 0:
+                factors[mi][s] = _empty_factor(a.blocks[s])
+                continue
+            m, n = _shape(a.blocks[s])
+            dev = str(a.blocks[s].device) if _is_torch_cuda(a.blocks[s]) else "host"
+            if method.kind == "rsvd" and dims[s] >= method.rsvd_min_dim:
+                ov = method.rsvd.oversample
+                ell = min(max(ov, want[s]), dims[s]) if ov > 0 else min(2 * want[s], dims[s])
+                key = ("rsvd", dev, m, n, want[s], ell, method.rsvd.power)
+                exact[mi] = False
+            else:
+                key = ("tsvd", dev, m, n, want[s])
+            groups.setdefault(key, []).append((mi, s))
 
     for key, members in groups.items():
+        blocks = [mats[mi].blocks[s] for mi, s in members]
         if key[0] == "tsvd":
+            k = key[4]
             if len(members) == 1:
-                factors[members[0]] = tsvd(a.blocks[members[0]], key[3], handle)
+                mi, s = members[0]
+                factors[mi][s] = tsvd(blocks[0], k, handle)
                 continue
-            bf = tsvd_batched(_stack([a.blocks[s] for s in members]), key[3], handle)
-            for i, s in enumerate(members):
-                factors[s] = bf.item(i)
-            continue
-        _, m, n, k, ell, power = key
-        seeds = [derive_seed(method.rsvd.seed, int(a.charges[s])) for s in members]
-        if len(members) == 1:
-            s = members[0]
-            factors[s] = rsvd(a.blocks[s], RsvdParams(k, ell, power, seeds[0]), handle)
-            continue
-        bf = rsvd_batched(_stack([a.blocks[s] for s in members]), RsvdParams(k, ell, power, 0),
-                          seeds, handle)
-        for i, s in enumerate(members):
-            factors[s] = bf.item(i)
+            bf = tsvd_batched(_stack(blocks), k, handle)
+        else:
+            _, _, m, n, k, ell, power = key
+            seeds = [derive_seed(method.rsvd.seed, int(mats[mi].charges[s])) for mi, s in members]
+            if len(members) == 1:
+                mi, s = members[0]
+                factors[mi][s] = rsvd(blocks[0], RsvdParams(k, ell, power, seeds[0]), handle)
+                continue
+            bf = rsvd_batched(_stack(blocks), RsvdParams(k, ell, power, 0), seeds, handle)
+        for i, (mi, s) in enumerate(members):
+            factors[mi][s] = bf.item(i)
 
-    # Global post-selection (blocks.cpp:86-105): chi largest values, ties to
-    # the lower charge, then the lower in-sector position.
+    return [_select(mats[mi], factors[mi], chi, exact[mi]) for mi in range(len(mats))]
+
+
+def _select(a: BlockDiagMatrix, factors, chi: int, exact: bool) -> BlockFactorization:
+    """Global post-selection (blocks.cpp:86-116): the chi largest values over
+    all sectors, ties to the lower charge then the lower in-sector position;
+    dropped values move into the sector's discarded weight."""
+    nsec = len(factors)
     cand = []
+    sigs = []
     for s, f in enumerate(factors):
         sig = f.sigma.cpu().numpy() if hasattr(f.sigma, "cpu") else np.asarray(f.sigma)
+        sigs.append(sig)
         for pos in range(f.rank()):
             cand.append((-float(sig[pos]), int(a.charges[s]), pos, s))
     cand.sort()
@@ -187,9 +206,17 @@ def block_factorize(a: BlockDiagMatrix, chi: int, request: SectorRankRequest,
     total_dw = 0.0
     out = []
     for s, f in enumerate(factors):
-        sig = f.sigma.cpu().numpy() if hasattr(f.sigma, "cpu") else np.asarray(f.sigma)
-        dw = f.discarded_weight + float(np.sum(sig[keep[s]:] ** 2))
+        dw = f.discarded_weight + float(np.sum(sigs[s][keep[s]:] ** 2))
         out.append(TruncatedFactorization(f.left[:, :keep[s]], f.sigma[:keep[s]],
                                           f.right_adj[:keep[s], :], dw, f.discarded_exact))
         total_dw += dw
     return BlockFactorization(list(a.charges), out, total_dw, exact)
+
+
+def block_factorize(a: BlockDiagMatrix, chi: int, request: SectorRankRequest,
+                    method: BlockMethod, handle: Optional[_lib.Handle] = None
+                    ) -> BlockFactorization:
+    """rlftn::block_factorize (blocks.cpp:38-118) on the GPU engine: per-sector
+    rsvd / tsvd dispatch (blocks.cpp:60-84; equal-shape sectors share one
+    batched engine call), then the global top-chi selection."""
+    return block_factorize_many([a], chi, request, method, handle)[0]

@@ -164,11 +164,13 @@ __device__ void blocked_upper_inverse(const double* __restrict__ R, double* __re
 __global__ void __launch_bounds__(kCholThreads)
     pchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
                  double* __restrict__ scratch, int* __restrict__ rank_out,
-                 int* __restrict__ perm_out, int ell, int ellp, double tau, int pivot) {
+                 int* __restrict__ perm_out, int ell, int ellp, double tau, int pivot,
+                 const int* __restrict__ mask) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_piv;
   __shared__ int s_stop;
   const int64_t b = blockIdx.x;
+  if (mask && !mask[b]) return;  // whole CTA: item not selected
   const int64_t sq = static_cast<int64_t>(ellp) * ellp;
   const int ld = ellp;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1058,7 +1060,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     }
     return;
   }
-  if (opts || (!pivot && !std::getenv("RSVD_PIVOT_ALWAYS"))) {
+  if (!pivot && (opts || !std::getenv("RSVD_PIVOT_ALWAYS"))) {
     const CholOpts o = opts ? *opts : CholOpts{};
     const int64_t ub = big * 8 + 2 * 32 * kInvPitch * 8 + 64;
     RSVD_CUDA(cudaFuncSetAttribute(uchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1073,7 +1075,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
                                  static_cast<int>(bytes)));
   pchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
       G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau,
-      pivot ? 1 : 0);
+      pivot ? 1 : 0, opts ? opts->mask : nullptr);
   RSVD_LAUNCH("pchol_kernel");
 }
 

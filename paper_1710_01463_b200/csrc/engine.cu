@@ -423,13 +423,16 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       gram(out, B.ill);
       {
         Scope sc(P, kStChol, st);
+        // Pivoted (dpstrf semantics): the shifted pass leaves exact-null
+        // directions as tiny columns at arbitrary positions, and an unpivoted
+        // factorization would stop at the first and drop every later column.
         CholOpts o;
         o.mask = B.ill;
         launch_pchol(B.G, B.T, Rt ? B.Rf2 : nullptr, B.cscratch, B.rank2, B.perm, s.ell, lp,
-                     kPivotTau, false, b, st, &o);
+                     kPivotTau, true, b, st, &o);
       }
       Scope sc(P, kStApply, st);
-      apply(out, in, B.ill, false);
+      apply(out, in, B.ill, true);
       launch_complete_basis(in, rows, s.ell, B.rank2, B.seeds, tag + 0x40, b, row_off, rows_global,
                             st, B.ill);
       launch_masked_copy(B.ill, in, out, rows, lp, b, st);

@@ -1198,7 +1198,13 @@ void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_swee
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
   }
-  if (bytes <= 220 * 1024) {
+  // The whole-problem-in-shared-memory kernel tracks column norms across the
+  // whole run; on rank-deficient, widely graded inputs (TEBD sector blocks,
+  // tests/golden/theta_rankdef_24x21.npy) its small values drifted by ~1e-10
+  // absolute.  The block-cyclic kernels re-derive the norms from the columns
+  // at every task and are exact to rounding, so they serve every size
+  // (RSVD_JACOBI_SMEM=1 restores the old kernel).
+  if (bytes <= 220 * 1024 && std::getenv("RSVD_JACOBI_SMEM")) {
     // Whole problem fits one CTA's shared memory: one CTA per item.
     RSVD_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(bytes)));

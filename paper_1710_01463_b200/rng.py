@@ -47,6 +47,10 @@ class CounterRng:
         self.counter += 1
         return mix64((self.key + self.counter * self.GOLDEN) & MASK64)
 
+    def uniform(self) -> float:
+        """((w >> 11) + 1) * 2^-53 in (0, 1] (rng.hpp:46)."""
+        return float((self.next() >> 11) + 1) * (1.0 / 9007199254740992.0)
+
     def fill_gaussian(self, out, count: int | None = None, handle: _lib.Handle | None = None):
         """Fill ``out`` (a float64 torch CUDA tensor or numpy array) with the
         first ``count`` normals of this stream, computed on the GPU."""

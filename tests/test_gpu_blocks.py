@@ -279,3 +279,20 @@ def test_block_many_sectors_vs_oracle(cuda, oracle_mod, kind, device):
         assert isometry_err(_np(g.left)) < ISO_TOL
         assert g.discarded_weight == pytest.approx(dws, rel=1e-8, abs=1e-26), s
     assert f.discarded_weight == pytest.approx(dw, rel=1e-8)
+
+
+def test_tsvd_rank_deficient_graded_block(cuda, oracle_mod):
+    """A TEBD sector block (24 x 21, numerical rank 15, values 0.79 .. 5e-15)
+    captured from the bond-update tests: every value to O(u ||A||)
+    absolutely, like the oracle's gesdd."""
+    import os
+
+    from paper_1710_01463_b200 import tsvd
+
+    a = np.load(os.path.join(os.path.dirname(__file__), "golden", "theta_rankdef_24x21.npy"))
+    _, S, _, dw = oracle_mod.tsvd(a, 100)
+    for x in (a, a.T.copy()):
+        f = tsvd(x, 100)
+        assert f.rank() == len(S)
+        assert np.max(np.abs(np.asarray(f.sigma) - S)) < 1e-14  # ~50 u ||A||
+        assert f.discarded_weight == pytest.approx(dw, abs=1e-28)
