@@ -22,7 +22,7 @@ from .factorize import (
 )
 from .blocks import (BlockDiagMatrix, BlockFactorization, BlockMethod, RankPolicy,
                      SectorRankRequest, block_factorize, block_factorize_many, sector_request)
-from . import cli, matrix_io, models, tebd  # noqa: E402
+from . import matrix_io, models, tebd  # noqa: E402  (CLI: python -m paper_1710_01463_b200.cli)
 from .rng import CounterRng, derive_seed, mix64, seed_tag
 
 __all__ = [
@@ -31,5 +31,5 @@ __all__ = [
     "mix64", "randomized_range", "reconstruction_error", "rsvd", "rsvd_batched", "seed_tag",
     "tsvd", "tsvd_batched", "BlockDiagMatrix", "BlockFactorization", "BlockMethod", "RankPolicy",
     "SectorRankRequest", "block_factorize", "block_factorize_many", "sector_request", "models",
-    "tebd", "matrix_io", "cli",
+    "tebd", "matrix_io",
 ]
