@@ -768,6 +768,312 @@ __global__ void __launch_bounds__(512, MINB)
       if (!conv[i]) sweeps_out[i] = max_sweeps;
 }
 
+// 16-byte global -> shared async copy; bytes < 16 zero-fills the rest.
+__device__ __forceinline__ void cpa16(void* dst, const void* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Stage the 32 columns gcol(c) (rows [0, rows), zero past ell / for padding
+// columns) of a column-major ellp x ellp matrix into S (column pitch PITCH).
+template <int PITCH, class GC>
+__device__ __forceinline__ void stage_pair(double* S, const double* G, int ell, int ellp, int rows,
+                                           GC&& gcol, int tid, int nthreads) {
+  const int half_rows = rows / 2;
+  for (int e = tid; e < 32 * half_rows; e += nthreads) {
+    const int c = e / half_rows, r = 2 * (e - c * half_rows);
+    const int gc = gcol(c);
+    int bytes = 0;
+    const double* src = G;
+    if (gc < ell && r < ell) {
+      bytes = min(16, (ell - r) * 8);
+      src = G + r + static_cast<int64_t>(gc) * ellp;
+    }
+    cpa16(S + c * PITCH + r, src, bytes);
+  }
+  cpa_wait_all();
+}
+
+// Gram-accelerated block-cyclic Jacobi (jacobi_gram_kernel).  Same sweep
+// order, rotation formula, thresholds and convergence flags as
+// jacobi_cyc_kernel, but inside a task the 16 rotation steps act on the
+// 32 x 32 Gram matrix of the staged block pair instead of on its l-long
+// columns: G = X^T X by DMMA, then per step every warp rotates one column
+// pair of G (G <- G R, then R^T G; lane = row) and of V, and at the end X <- X V
+// (and J <- J V) by DMMA.  Each step touches 32-element rows instead of
+// 2 l-element columns.  G is formed from the freshly rotated columns at every
+// task, so the dot products that decide the rotations are the one-sided ones
+// up to the in-task updates, whose rounding is O(u |x_i| |x_k|) like a fresh
+// dot product; after the last productive sweep the convergence test runs on
+// fresh Grams.
+template <int R, int MINB>
+__global__ void __launch_bounds__(512, MINB)
+    jacobi_gram_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                       int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                       int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1;
+  constexpr int PITCH = 32 * R + 2;  // padded column pitch (Gram fragment loads)
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
+  double* Hs = sm;                 // NC x PITCH
+  double* Vs = sm + NC * PITCH;    // NC x VP, column-major V[c*VP + k]
+  double* Gs = Vs + NC * VP;       // NC x GP, G[row + col*GP]
+  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  const int rows = 32 * R;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
+          bp = min(p, q), bq = max(p, q);
+        }
+        if (bp * W >= ell) continue;
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        stage_pair<PITCH>(Hs, Hg, ell, ellp, rows, gcol, tid, blockDim.x);
+        for (int e = tid; e < NC * VP; e += blockDim.x) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
+        __syncthreads();
+        // G = X^T X: warps 0..7 own one 16 x 8 tile each (K = rows, DMMA).
+        if (warp < 8) {
+          const int tm = warp >> 2, tn = warp & 3;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          const double* a0p = Hs + (16 * tm + g) * PITCH;
+          const double* a1p = Hs + (16 * tm + g + 8) * PITCH;
+          const double* b0p = Hs + (8 * tn + g) * PITCH;
+#pragma unroll 8
+          for (int k0 = 0; k0 < rows; k0 += 4)
+            dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
+          Gs[r0 + c0 * GP] = acc[0];
+          Gs[r0 + (c0 + 1) * GP] = acc[1];
+          Gs[r0 + 8 + c0 * GP] = acc[2];
+          Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
+        }
+        __syncthreads();
+        int rotated = 0, big = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int i, jx;
+          if (diag) {
+            const int blk = warp >> 3, pi = warp & 7;
+            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
+            i = blk * 16 + min(a0, b0);
+            jx = blk * 16 + max(a0, b0);
+          } else {
+            i = warp;
+            jx = 16 + ((warp + s2) & 15);
+          }
+          const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
+          const double gg = ga * ga, ab = al * be;
+          const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
+          double c = 1.0, sn = 0.0, tt = 0.0;
+          if (rot) {
+            big |= gg >= 1e-18 * ab;
+            const double d = be - al, g2 = 2.0 * ga;
+            const double mag = fmax(fabs(d), fabs(g2));
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
+            c = rsqrt(fma(tt, tt, 1.0));
+            sn = c * tt;
+            rotated = 1;
+            // columns of G and V (lane = row)
+            const double gi = Gs[lane + i * GP], gj = Gs[lane + jx * GP];
+            Gs[lane + i * GP] = c * gi - sn * gj;
+            Gs[lane + jx * GP] = sn * gi + c * gj;
+            const double vi = Vs[i * VP + lane], vj = Vs[jx * VP + lane];
+            Vs[i * VP + lane] = c * vi - sn * vj;
+            Vs[jx * VP + lane] = sn * vi + c * vj;
+          }
+          __syncthreads();
+          if (rot) {  // rows of G, then the exact 2 x 2 block
+            const double gi = Gs[i + lane * GP], gj = Gs[jx + lane * GP];
+            Gs[i + lane * GP] = c * gi - sn * gj;
+            Gs[jx + lane * GP] = sn * gi + c * gj;
+            __syncwarp();
+            if (lane == 0) {
+              Gs[i + i * GP] = al - tt * ga;
+              Gs[jx + jx * GP] = be + tt * ga;
+              Gs[i + jx * GP] = 0.0;
+              Gs[jx + i * GP] = 0.0;
+            }
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          if (big) atomicMax(&s_mx, 1ull);
+        }
+        __syncthreads();
+        if (s_rot) {
+          // X <- X V and J <- J V, warp per 16-row slab (DMMA).
+          const int slabs = rows / 16;
+          for (int sl = warp; sl < slabs; sl += W) {
+            const int r0 = sl * 16;
+            double acc[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) {
+              const int kc = kq * 4 + t4;
+              const double a0 = Hs[kc * PITCH + r0 + g], a1 = Hs[kc * PITCH + r0 + g + 8];
+#pragma unroll
+              for (int n = 0; n < NC / 8; ++n)
+                dmma_16x8x4(acc[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                const int c = n * 8 + 2 * t4 + (qq & 1);
+                Hs[c * PITCH + r] = acc[n][qq];
+              }
+          }
+          __syncthreads();
+          for (int e = tid; e < NC * rows; e += blockDim.x) {
+            const int c = e / rows, r = e - c * rows;
+            const int gc = gcol(c);
+            if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[c * PITCH + r];
+          }
+          __syncthreads();  // H written back: Hs is free for the J pair
+          stage_pair<PITCH>(Hs, Jg, ell, ellp, rows, gcol, tid, blockDim.x);
+          __syncthreads();
+          for (int sl = warp; sl < slabs; sl += W) {
+            const int r0 = sl * 16;
+            double acc[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) {
+              const int kc = kq * 4 + t4;
+              const double a0 = Hs[kc * PITCH + r0 + g], a1 = Hs[kc * PITCH + r0 + g + 8];
+#pragma unroll
+              for (int n = 0; n < NC / 8; ++n)
+                dmma_16x8x4(acc[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
+            }
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                const int c = n * 8 + 2 * t4 + (qq & 1);
+                const int gc = gcol(c);
+                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
+              }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
+      }
+      grid.sync();
+    }
+    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (done(i)) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int R, int MINB>
+void launch_gram_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                   unsigned* flags, int64_t batch, cudaStream_t st) {
+  const size_t bytes = (static_cast<size_t>(32) * (32 * R + 2) + 32 * 36 + 32 * 33) * sizeof(double) +
+                       batch * sizeof(int) + 16;
+  auto kern = jacobi_gram_kernel<R, MINB>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
+  if (per_sm < 1) throw CudaError("jacobi_gram_kernel: does not fit on an SM");
+  int dev = 0, sms = 0;
+  RSVD_CUDA(cudaGetDevice(&dev));
+  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
+  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512),
+                                        args, bytes, st));
+  RSVD_LAUNCH("jacobi_gram_kernel");
+}
+
 template <int R, int MINB>
 void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                   unsigned* flags, int64_t batch, cudaStream_t st) {
@@ -1148,6 +1454,19 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
   if (!std::getenv("RSVD_JACOBI_OLD") && !std::getenv("RSVD_JACOBI_PAIRV")) {
     // R = rows per lane: the smallest instantiation covering l (the column
     // registers, smem pitch and dot products all scale with R).
+    if (!std::getenv("RSVD_JACOBI_NO_GRAM")) {
+      // Gram-accelerated task steps (jacobi_gram_kernel).
+      int nbg = static_cast<int>((ell + 15) / 16);
+      nbg += nbg & 1;
+      const bool many = batch * (nbg / 2) > kNumSMs;
+      if (ell <= 32 * 3) return launch_gram_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      if (ell <= 32 * 5) return launch_gram_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      if (ell <= 32 * 9 && many)
+        return launch_gram_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      if (ell <= 32 * 9) return launch_gram_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      if (ell <= 32 * 18)
+        return launch_gram_t<18, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    }
     if (ell <= 32 * 3 && !std::getenv("RSVD_JACOBI_R9"))
       return launch_cyc_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
     if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_R9"))
