@@ -1363,12 +1363,276 @@ __global__ void __launch_bounds__(512, 1)
       if (!conv[i]) sweeps_out[i] = max_sweeps;
 }
 
+// Cluster + Gram variant (jacobi_clug_kernel): the row-split cluster of
+// jacobi_clu_kernel, with each task's rotations done on the block pair's
+// 32 x 32 Gram: every CTA forms the Gram of its row slice on DMMA, the S
+// partials are summed through DSMEM in rank order (bit-identical G in every
+// CTA), the 16 steps run redundantly on G and V in each CTA, and each CTA
+// applies X <- X V, J <- J V to its rows.  Two cluster barriers per task
+// instead of one per rotation step.
+template <int RL>
+__global__ void __launch_bounds__(512, 1)
+    jacobi_clug_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                       int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                       int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, PITCH = 32 * RL + 2, ROWS = 32 * RL;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
+  double* Hs = sm;                 // NC x PITCH (local rows)
+  double* Vs = Hs + NC * PITCH;    // NC x VP
+  double* Gs = Vs + NC * VP;       // NC x GP: the summed Gram
+  double* Gp = Gs + NC * GP;       // NC x GP: this CTA's partial Gram (read remotely)
+  int* conv = reinterpret_cast<int*>(Gp + NC * GP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int S = static_cast<int>(cluster.num_blocks());
+  const int q = static_cast<int>(cluster.block_rank());
+  const int row0 = q * ROWS;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
+  const int64_t nclu = gridDim.x / S;
+  const int64_t clu = blockIdx.x / S;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  // local slice [row0, row0 + ROWS) of the ellp rows, clipped to ell
+  const int lrows = max(0, min(ROWS, ell - row0));
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = clu; task < tasks; task += nclu) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = rr_player(k, phase - 1, nb), qq = rr_player(nb - 1 - k, phase - 1, nb);
+          bp = min(p, qq), bq = max(p, qq);
+        }
+        if (bp * W >= ell) continue;
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        // local rows: global row = row0 + r; stage_pair works on rows [0, ROWS)
+        // of a shifted matrix view whose "ell" is the local row count.
+        const double* Hl = Hg + row0;
+        {
+          const int half_rows = ROWS / 2;
+          for (int e = tid; e < 32 * half_rows; e += blockDim.x) {
+            const int c = e / half_rows, r = 2 * (e - c * half_rows);
+            const int gc = gcol(c);
+            int bytes = 0;
+            const double* src = Hg;
+            if (gc < ell && r < lrows) {
+              bytes = min(16, (lrows - r) * 8);
+              src = Hl + r + static_cast<int64_t>(gc) * ellp;
+            }
+            cpa16(Hs + c * PITCH + r, src, bytes);
+          }
+          cpa_wait_all();
+        }
+        for (int e = tid; e < NC * VP; e += blockDim.x) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
+        __syncthreads();
+        if (warp < 8) {  // partial Gram of the local rows (DMMA)
+          const int tm = warp >> 2, tn = warp & 3;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          const double* a0p = Hs + (16 * tm + g) * PITCH;
+          const double* a1p = Hs + (16 * tm + g + 8) * PITCH;
+          const double* b0p = Hs + (8 * tn + g) * PITCH;
+#pragma unroll 8
+          for (int k0 = 0; k0 < ROWS; k0 += 4)
+            dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
+          Gp[r0 + c0 * GP] = acc[0];
+          Gp[r0 + (c0 + 1) * GP] = acc[1];
+          Gp[r0 + 8 + c0 * GP] = acc[2];
+          Gp[r0 + 8 + (c0 + 1) * GP] = acc[3];
+        }
+        cluster.sync();
+        for (int e = tid; e < NC * NC; e += blockDim.x) {
+          const int c = e / NC, r = e - c * NC;
+          double v = 0.0;
+          for (int rr = 0; rr < S; ++rr) v += *cluster.map_shared_rank(&Gp[r + c * GP], rr);
+          Gs[r + c * GP] = v;
+        }
+        cluster.sync();  // every CTA has read every partial
+        int rotated = 0, big = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int i, jx;
+          if (diag) {
+            const int blk = warp >> 3, pi = warp & 7;
+            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
+            i = blk * 16 + min(a0, b0);
+            jx = blk * 16 + max(a0, b0);
+          } else {
+            i = warp;
+            jx = 16 + ((warp + s2) & 15);
+          }
+          const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
+          const double gg = ga * ga, ab = al * be;
+          const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
+          double c = 1.0, sn = 0.0, tt = 0.0;
+          if (rot) {
+            big |= gg >= 1e-18 * ab;
+            const double d = be - al, g2 = 2.0 * ga;
+            const double mag = fmax(fabs(d), fabs(g2));
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
+            c = rsqrt(fma(tt, tt, 1.0));
+            sn = c * tt;
+            rotated = 1;
+            const double gi = Gs[lane + i * GP], gj = Gs[lane + jx * GP];
+            Gs[lane + i * GP] = c * gi - sn * gj;
+            Gs[lane + jx * GP] = sn * gi + c * gj;
+            const double vi = Vs[i * VP + lane], vj = Vs[jx * VP + lane];
+            Vs[i * VP + lane] = c * vi - sn * vj;
+            Vs[jx * VP + lane] = sn * vi + c * vj;
+          }
+          __syncthreads();
+          if (rot) {
+            const double gi = Gs[i + lane * GP], gj = Gs[jx + lane * GP];
+            Gs[i + lane * GP] = c * gi - sn * gj;
+            Gs[jx + lane * GP] = sn * gi + c * gj;
+            __syncwarp();
+            if (lane == 0) {
+              Gs[i + i * GP] = al - tt * ga;
+              Gs[jx + jx * GP] = be + tt * ga;
+              Gs[i + jx * GP] = 0.0;
+              Gs[jx + i * GP] = 0.0;
+            }
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          if (big) atomicMax(&s_mx, 1ull);
+        }
+        __syncthreads();
+        if (s_rot) {
+          constexpr int slabs = ROWS / 16;
+          for (int pass = 0; pass < 2; ++pass) {  // 0: X <- X V, 1: J <- J V
+            if (pass == 1) {
+              __syncthreads();
+              const int half_rows = ROWS / 2;
+              const double* Jl = Jg + row0;
+              for (int e = tid; e < 32 * half_rows; e += blockDim.x) {
+                const int c = e / half_rows, r = 2 * (e - c * half_rows);
+                const int gc = gcol(c);
+                int bytes = 0;
+                const double* src = Jg;
+                if (gc < ell && r < lrows) {
+                  bytes = min(16, (lrows - r) * 8);
+                  src = Jl + r + static_cast<int64_t>(gc) * ellp;
+                }
+                cpa16(Hs + c * PITCH + r, src, bytes);
+              }
+              cpa_wait_all();
+              __syncthreads();
+            }
+            double* dst = pass == 0 ? Hg : Jg;
+            for (int sl = warp; sl < slabs; sl += W) {
+              const int r0 = sl * 16;
+              double acc[NC / 8][4];
+#pragma unroll
+              for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll
+              for (int kq = 0; kq < 8; ++kq) {
+                const int kc = kq * 4 + t4;
+                const double a0 = Hs[kc * PITCH + r0 + g], a1 = Hs[kc * PITCH + r0 + g + 8];
+#pragma unroll
+                for (int n = 0; n < NC / 8; ++n)
+                  dmma_16x8x4(acc[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
+              }
+#pragma unroll
+              for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                  const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                  const int cc = n * 8 + 2 * t4 + (qq & 1);
+                  const int gc = gcol(cc);
+                  if (r < lrows && gc < ell) dst[row0 + r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
+                }
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && q == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
+      }
+      grid.sync();
+    }
+    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (done(i)) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
 template <int RL>
 bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                   unsigned* flags, int64_t batch, int S, cudaStream_t st) {
-  const size_t bytes = (static_cast<size_t>(32) * 32 * RL + 32 * 36 + 32) * sizeof(double) +
-                       batch * sizeof(int) + 16;
-  auto kern = jacobi_clu_kernel<RL>;
+  static const bool no_gram = std::getenv("RSVD_JACOBI_NO_GRAM") != nullptr;
+  const size_t bytes =
+      no_gram ? (static_cast<size_t>(32) * 32 * RL + 32 * 36 + 32) * sizeof(double) +
+                    batch * sizeof(int) + 16
+              : (static_cast<size_t>(32) * (32 * RL + 2) + 32 * 36 + 2 * 32 * 33) * sizeof(double) +
+                    batch * sizeof(int) + 16;
+  auto kern = no_gram ? jacobi_clu_kernel<RL> : jacobi_clug_kernel<RL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(bytes)) != cudaSuccess ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
