@@ -264,6 +264,54 @@ __global__ void masked_copy_kernel(const int* __restrict__ mask, const double* _
   }
 }
 
+// Exact power-of-two range scaling (extreme-magnitude inputs).  Per item:
+// the largest |x| over rows x cols; outside [2^-200, 2^200] the item gets the
+// factor c = 2^-e (max |x| c in [0.5, 1)), else c = 1.  Scaling by a power of
+// two is exact, so in-range inputs are untouched bit for bit.
+__global__ void choose_scale_kernel(const double* __restrict__ X, int64_t ld, int64_t stride,
+                                    int64_t rows, int64_t cols, double* __restrict__ scale) {
+  __shared__ double red[32];
+  const int64_t b = blockIdx.x;
+  const double* x = X + b * stride;
+  double mx = 0.0;
+  for (int64_t e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const int64_t c = e / rows, r = e - c * rows;
+    mx = fmax(mx, fabs(x[r + c * ld]));
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    double c = 1.0;
+    if (m > 0.0 && isfinite(m) && (m < 0x1p-200 || m > 0x1p200)) {
+      int e = 0;
+      frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+      c = ldexp(1.0, -e);
+    }
+    scale[b] = c;
+  }
+}
+
+// X[b] *= c[b] (pow2 == true) or X[b] *= 1 / c[b]^pw for the spectrum (sigma,
+// pw = 1) and the discarded weight (pw = 2); items with c == 1 are skipped.
+__global__ void apply_scale_kernel(double* __restrict__ X, int64_t ld, int64_t stride,
+                                   int64_t rows, int64_t cols, const double* __restrict__ scale,
+                                   int inverse_power) {
+  const int64_t b = blockIdx.y;
+  const double c = scale[b];
+  if (c == 1.0) return;
+  double f = c;
+  if (inverse_power == 1) f = 1.0 / c;
+  if (inverse_power == 2) f = 1.0 / (c * c);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cc = e / rows, r = e - cc * rows;
+    X[b * stride + r + cc * ld] *= f;
+  }
+}
+
 unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
   return static_cast<unsigned>(
       std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * kNumSMs)));
@@ -307,6 +355,23 @@ void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, 
   masked_copy_kernel<<<grid, 256, 0, st>>>(mask, src.base, src.ld, src.stride, dst.base, dst.ld,
                                            dst.stride, rows, cols);
   RSVD_LAUNCH("masked_copy_kernel");
+}
+
+void launch_choose_scale(CMatRef X, int64_t rows, int64_t cols, double* scale, int64_t batch,
+                         cudaStream_t st) {
+  if (batch <= 0) return;
+  choose_scale_kernel<<<static_cast<unsigned>(batch), 512, 0, st>>>(X.base, X.ld, X.stride, rows,
+                                                                     cols, scale);
+  RSVD_LAUNCH("choose_scale_kernel");
+}
+
+void launch_apply_scale(MatRef X, int64_t rows, int64_t cols, const double* scale,
+                        int inverse_power, int64_t batch, cudaStream_t st) {
+  if (batch <= 0 || rows <= 0 || cols <= 0) return;
+  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  apply_scale_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, scale,
+                                           inverse_power);
+  RSVD_LAUNCH("apply_scale_kernel");
 }
 
 void launch_set_identity(MatRef out, int64_t n, int64_t batch, cudaStream_t st) {

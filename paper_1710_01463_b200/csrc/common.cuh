@@ -144,6 +144,13 @@ std::unique_ptr<Reducer> make_nccl_reducer(int nranks, int rank, const unsigned 
 void nccl_unique_id(unsigned char* out);
 void launch_transpose(CMatRef in, int64_t rows, int64_t cols, MatRef out, int64_t batch,
                       cudaStream_t st);
+// Exact power-of-two range scaling of extreme-magnitude items (aux.cu):
+// scale[b] = 2^-e when max|X[b]| is outside [2^-200, 2^200], else 1;
+// apply: X[b] *= scale[b] (inverse_power 0), / scale[b] (1), / scale[b]^2 (2).
+void launch_choose_scale(CMatRef X, int64_t rows, int64_t cols, double* scale, int64_t batch,
+                         cudaStream_t st);
+void launch_apply_scale(MatRef X, int64_t rows, int64_t cols, const double* scale,
+                        int inverse_power, int64_t batch, cudaStream_t st);
 // dst[b] = src[b] (rows x cols) for the items with mask[b] != 0.
 void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, int64_t cols,
                         int64_t batch, cudaStream_t st);

@@ -247,6 +247,8 @@ struct Buffers {
   double *Ut, *Jr, *Vb;
   double* sig;
   double* dw;
+  double* scale;  // per item: exact power-of-two input scaling (1 = none)
+  bool scaled;    // scale[] chosen for this call
   int *rank1, *rank2, *rankF, *perm, *permS, *sweeps;
   unsigned* jflags;
   double* partial;
@@ -279,6 +281,7 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   Buffers B{};
   const int64_t b = s.batch, lp = s.ellp;
   B.seeds = c.take<uint64_t>(b);
+  B.scale = c.take<double>(b);
   B.X = c.take<double>(b * s.n * lp);
   B.X2 = c.take<double>(b * s.n * lp);
   B.Y = c.take<double>(b * s.m * lp);
@@ -465,17 +468,32 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
     Scope sc(P, kStOmega, st);
     launch_fill_gaussian(MatRef{B.X, s.n, s.n * lp}, s.n, lp, s.ell, B.seeds, b, st);
   }
+  // Extreme-magnitude items run on 2^-e A (exact): the scale is chosen from
+  // the first product Y = A Omega (|Y| tracks sigma_max(A)) and applied to
+  // every A-pass output; sigma and the discarded weight are scaled back at the
+  // end.  Row-sharded calls are not scaled (a per-rank max would disagree).
+  static const bool no_scale = std::getenv("RSVD_NO_SCALE") != nullptr;
+  const bool do_scale = !B.red && !no_scale;
   auto nn = [&] {
     Scope sc(P, kStApassNN, st);
     dgemm(false, s.m, lp, s.n, A, MatRef{B.X, s.n, s.n * lp}, MatRef{B.Y, s.m, s.m * lp}, b,
           B.partial, B.partial_cap, st);
+    if (do_scale) {
+      if (!B.scaled) {
+        launch_choose_scale(MatRef{B.Y, s.m, s.m * lp}, s.m, s.ell, B.scale, b, st);
+        B.scaled = true;
+      }
+      launch_apply_scale(MatRef{B.Y, s.m, s.m * lp}, s.m, lp, B.scale, 0, b, st);
+    }
   };
   auto tn = [&] {
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, MatRef{B.Y, s.m, s.m * lp}, MatRef{B.X, s.n, s.n * lp}, b,
           B.partial, B.partial_cap, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // Z = sum_p A_p^T Q_p
+    if (do_scale) launch_apply_scale(MatRef{B.X, s.n, s.n * lp}, s.n, lp, B.scale, 0, b, st);
   };
+  B.scaled = false;
   nn();
   uint64_t tag = kCompletionTag;
   // Only the last orthonormalisation feeds B = Q^T A and U = Q U~; the
@@ -509,6 +527,13 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
+    if (!B.red) {
+      if (!B.scaled) {  // tsvd (Q = I): choose the scale from B^T = A_e^T
+        launch_choose_scale(X, s.n, s.ell, B.scale, b, st);
+        B.scaled = true;
+      }
+      launch_apply_scale(X, s.n, lp, B.scale, 0, b, st);
+    }
   }
   orth(s, B, B.X, B.X2, s.n, B.Rt, kCompletionTag + 0x1000, 2, false, st);
   const MatRef Qb{B.X, s.n, s.n * lp};  // orth may have swapped B.X and B.X2
@@ -517,6 +542,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     if (exact_h) {
       RSVD_CUDA(cudaMemsetAsync(B.H, 0, sizeof(double) * b * lp * lp, st));
       dgemm(false, s.m, lp, s.n, A, Qb, MatRef{B.H, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+      if (!B.red) launch_apply_scale(MatRef{B.H, lp, lp * lp}, s.m, lp, B.scale, 0, b, st);
     } else {
       launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
     }
@@ -534,6 +560,10 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   dgemm(false, s.n, k, lp, Qb, MatRef{B.Jr, lp, lp * k}, MatRef{B.Vb, s.n, s.n * k}, b, B.partial,
         B.partial_cap, st);
   launch_transpose(MatRef{B.Vb, s.n, s.n * k}, s.n, k, Vt, b, st);
+  if (!B.red) {  // back to the caller's scale (exact powers of two)
+    launch_apply_scale(MatRef{B.sig, k, k}, k, 1, B.scale, 1, b, st);
+    launch_apply_scale(MatRef{B.dw, 1, 1}, 1, 1, B.scale, 2, b, st);
+  }
   launch_copy_matrix(MatRef{B.sig, k, k}, k, 1, MatRef{S, k, sS}, b, st);
 }
 
