@@ -268,13 +268,14 @@ __global__ void masked_copy_kernel(const int* __restrict__ mask, const double* _
 // the largest |x| over rows x cols; outside [2^-200, 2^200] the item gets the
 // factor c = 2^-e (max |x| c in [0.5, 1)), else c = 1.  Scaling by a power of
 // two is exact, so in-range inputs are untouched bit for bit.
-__global__ void choose_scale_kernel(const double* __restrict__ X, int64_t ld, int64_t stride,
-                                    int64_t rows, int64_t cols, double* __restrict__ scale) {
+__global__ void maxabs_kernel(const double* __restrict__ X, int64_t ld, int64_t stride,
+                              int64_t rows, int64_t cols, unsigned long long* __restrict__ bits) {
   __shared__ double red[32];
-  const int64_t b = blockIdx.x;
+  const int64_t b = blockIdx.y;
   const double* x = X + b * stride;
   double mx = 0.0;
-  for (int64_t e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = e / rows, r = e - c * rows;
     mx = fmax(mx, fabs(x[r + c * ld]));
   }
@@ -284,14 +285,23 @@ __global__ void choose_scale_kernel(const double* __restrict__ X, int64_t ld, in
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
-    double c = 1.0;
-    if (m > 0.0 && isfinite(m) && (m < 0x1p-200 || m > 0x1p200)) {
-      int e = 0;
-      frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
-      c = ldexp(1.0, -e);
-    }
-    scale[b] = c;
+    // non-negative doubles order like their bit patterns: an integer max is exact
+    atomicMax(bits + b, static_cast<unsigned long long>(__double_as_longlong(m)));
   }
+}
+
+__global__ void choose_scale_kernel(unsigned long long* __restrict__ bits,
+                                    double* __restrict__ scale, int64_t batch) {
+  const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const double m = __longlong_as_double(static_cast<long long>(bits[b]));
+  double c = 1.0;
+  if (m > 0.0 && isfinite(m) && (m < 0x1p-200 || m > 0x1p200)) {
+    int e = 0;
+    frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+    c = ldexp(1.0, -e);
+  }
+  scale[b] = c;
 }
 
 // X[b] *= c[b] (pow2 == true) or X[b] *= 1 / c[b]^pw for the spectrum (sigma,
@@ -360,8 +370,15 @@ void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, 
 void launch_choose_scale(CMatRef X, int64_t rows, int64_t cols, double* scale, int64_t batch,
                          cudaStream_t st) {
   if (batch <= 0) return;
-  choose_scale_kernel<<<static_cast<unsigned>(batch), 512, 0, st>>>(X.base, X.ld, X.stride, rows,
-                                                                     cols, scale);
+  // scale[] doubles as the max-bits accumulator (same 8 bytes per item).
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(scale);
+  RSVD_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * batch, st));
+  dim3 grid(grid1(rows * cols, 256, 4), static_cast<unsigned>(batch));
+  if (batch > 1) grid.x = std::max(1u, std::min(grid.x, static_cast<unsigned>(4 * kNumSMs / batch + 1)));
+  maxabs_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, bits);
+  RSVD_LAUNCH("maxabs_kernel");
+  choose_scale_kernel<<<static_cast<unsigned>(ceil_div(batch, 256)), 256, 0, st>>>(bits, scale,
+                                                                                   batch);
   RSVD_LAUNCH("choose_scale_kernel");
 }
 

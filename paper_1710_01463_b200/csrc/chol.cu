@@ -827,11 +827,17 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
   }
   grid.sync();
   gc_mark(nmark);
-  for (int64_t e = gtid; e < batch * sq; e += gstride) {
-    const int64_t b = e / sq;
+  // Per item (flag read once), 16-byte stores: sq is a multiple of 1024.
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     if (go_of(b)[0] == 0.0) continue;
-    if (a.o.Gsrc) a.G[e] = a.o.Gsrc[e];
-    a.T[e] = 0.0;
+    double2* t2 = reinterpret_cast<double2*>(a.T + b * sq);
+    const double2 z = make_double2(0.0, 0.0);
+    for (int64_t e = tid; e < sq / 2; e += blockDim.x) t2[e] = z;
+    if (a.o.Gsrc) {
+      const double2* s2 = reinterpret_cast<const double2*>(a.o.Gsrc + b * sq);
+      double2* g2 = reinterpret_cast<double2*>(a.G + b * sq);
+      for (int64_t e = tid; e < sq / 2; e += blockDim.x) g2[e] = s2[e];
+    }
   }
   grid.sync();
   gc_mark(nmark);
@@ -1000,16 +1006,17 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
   gc_mark(nmark);
   }
   // Epilogue: Rfull (rows < r, upper), identity permutation.
-  for (int64_t e = gtid; e < batch * sq; e += gstride) {
-    const int64_t b = e / sq;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     if (go_of(b)[0] == 0.0) continue;
-    const int64_t rem = e - b * sq;
-    const int c = static_cast<int>(rem / ld), i = static_cast<int>(rem - static_cast<int64_t>(c) * ld);
-    if (a.Rfull) {
-      const int r = a.rank[b];
-      a.Rfull[e] = (i < r && i <= c && c < ell) ? a.G[e] : 0.0;
-    }
-    if (a.perm && c == 0) a.perm[b * ld + i] = i;
+    if (a.perm)
+      for (int i = tid; i < ld; i += blockDim.x) a.perm[b * ld + i] = i;
+    if (!a.Rfull) continue;
+    const int r = a.rank[b];
+    for (int c = warp; c < ld; c += kGcWarps)
+      for (int i = lane; i < ld; i += 32) {
+        const int64_t e = b * sq + i + static_cast<int64_t>(c) * ld;
+        a.Rfull[e] = (i < r && i <= c && c < ell) ? a.G[e] : 0.0;
+      }
   }
 }
 

@@ -527,7 +527,8 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
-    if (!B.red) {
+    static const bool no_scale = std::getenv("RSVD_NO_SCALE") != nullptr;
+    if (!B.red && !no_scale) {
       if (!B.scaled) {  // tsvd (Q = I): choose the scale from B^T = A_e^T
         launch_choose_scale(X, s.n, s.ell, B.scale, b, st);
         B.scaled = true;
@@ -542,7 +543,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     if (exact_h) {
       RSVD_CUDA(cudaMemsetAsync(B.H, 0, sizeof(double) * b * lp * lp, st));
       dgemm(false, s.m, lp, s.n, A, Qb, MatRef{B.H, lp, lp * lp}, b, B.partial, B.partial_cap, st);
-      if (!B.red) launch_apply_scale(MatRef{B.H, lp, lp * lp}, s.m, lp, B.scale, 0, b, st);
+      if (!B.red && B.scaled) launch_apply_scale(MatRef{B.H, lp, lp * lp}, s.m, lp, B.scale, 0, b, st);
     } else {
       launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
     }
@@ -560,7 +561,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   dgemm(false, s.n, k, lp, Qb, MatRef{B.Jr, lp, lp * k}, MatRef{B.Vb, s.n, s.n * k}, b, B.partial,
         B.partial_cap, st);
   launch_transpose(MatRef{B.Vb, s.n, s.n * k}, s.n, k, Vt, b, st);
-  if (!B.red) {  // back to the caller's scale (exact powers of two)
+  if (!B.red && B.scaled) {  // back to the caller's scale (exact powers of two)
     launch_apply_scale(MatRef{B.sig, k, k}, k, 1, B.scale, 1, b, st);
     launch_apply_scale(MatRef{B.dw, 1, 1}, 1, 1, B.scale, 2, b, st);
   }
