@@ -148,6 +148,7 @@ struct Scope {
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   bool failed = false;
+  uint64_t launches = 0;  // engine kernels captured in the graph (added on every replay)
 };
 
 // Pinned host staging for the per-call scalars (seeds in; ranks, sweeps,
@@ -870,8 +871,12 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
     if (!ge.exec && !ge.failed) {
       cudaGraph_t g = nullptr;
       RSVD_CUDA(cudaStreamBeginCapture(h->own, cudaStreamCaptureModeThreadLocal));
+      const uint64_t l0 = g_kernel_launches.load();
       try {
         enqueue(h->own);
+        // Capture does not run the kernels: count them once per replay instead.
+        ge.launches = g_kernel_launches.load() - l0;
+        g_kernel_launches.fetch_sub(ge.launches);
       } catch (...) {
         cudaStreamEndCapture(h->own, &g);
         if (g) cudaGraphDestroy(g);
@@ -892,6 +897,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
       RSVD_CUDA(cudaEventRecord(h->ev_in, st));
       RSVD_CUDA(cudaStreamWaitEvent(h->own, h->ev_in, 0));
       RSVD_CUDA(cudaGraphLaunch(ge.exec, h->own));
+      g_kernel_launches.fetch_add(ge.launches);
       RSVD_CUDA(cudaEventRecord(h->ev_out, h->own));
       RSVD_CUDA(cudaStreamWaitEvent(st, h->ev_out, 0));
       RSVD_CUDA(cudaStreamSynchronize(h->own));
