@@ -55,6 +55,16 @@ def lib() -> ctypes.CDLL:
                                              ctypes.c_int, i64, ctypes.c_int, u64, i64, vp, vp, vp,
                                              vp, vp, ctypes.POINTER(dbl),
                                              ctypes.POINTER(ctypes.c_int)]
+        L.oracle_zfill_gaussian.argtypes = [u64, vp, i64]
+        L.oracle_zrsvd.argtypes = [vp, i64, i64, i64, i64, i64, ctypes.c_int, u64, vp, vp, vp, vp,
+                                   i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
+        L.oracle_ztsvd.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp, i64, ctypes.POINTER(i64),
+                                   ctypes.POINTER(dbl)]
+        L.oracle_zrandomized_range.argtypes = [vp, i64, i64, i64, i64, ctypes.c_int, u64, vp, vp]
+        L.oracle_zreconstruction_error.argtypes = [vp, i64, i64, i64, vp, vp, vp, i64, i64,
+                                                   ctypes.c_int, ctypes.POINTER(dbl)]
+        L.oracle_zorthonormal_columns.argtypes = [vp, i64, i64, vp]
+        L.oracle_zsingular_values.argtypes = [vp, i64, i64, vp]
         _lib = L
     return _lib
 
@@ -252,3 +262,110 @@ def reference_rng_kat(nwords: int = 64, nnormal: int = 257):
     out = subprocess.run([REF_KAT, str(nwords), str(nnormal)], check=True, capture_output=True,
                          text=True).stdout
     return json.loads(out)
+
+
+# ------------------------------------------------------------------ complex
+# The reference's std::complex<double> instantiation of the same path
+# (factorize.cpp:106-118; lapack.cpp:73-110, 154-177): zgemm, zgeqrf+zungqr,
+# zgesdd -> zgesvd, complex CounterRng fill (rng.hpp:66-71).
+
+
+def _z(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.complex128))
+
+
+def zfill_gaussian(seed: int, n: int) -> np.ndarray:
+    out = np.zeros(n, dtype=np.complex128)
+    lib().oracle_zfill_gaussian(seed & ((1 << 64) - 1), out.ctypes.data, n)
+    return out
+
+
+def zgaussian_matrix(seed: int, rows: int, cols: int) -> np.ndarray:
+    """Complex Omega exactly as randomized_range<complex> fills it (column-major)."""
+    return zfill_gaussian(seed, rows * cols).reshape(cols, rows).T.copy(order="F")
+
+
+def zrsvd(a, rank: int, oversample: int, power: int, seed: int, omega=None):
+    """rlftn::rsvd<complex<double>> -> (U m x r, S r, Vt r x n, discarded_weight)."""
+    a = _z(a)
+    m, n = a.shape
+    k = max(rank, 1)
+    U = np.zeros((m, k), dtype=np.complex128, order="F")
+    S = np.zeros(k)
+    Vt = np.zeros((k, n), dtype=np.complex128, order="F")
+    r = ctypes.c_int64(0)
+    dw = ctypes.c_double(0.0)
+    om = None if omega is None else _z(omega)
+    _check(lib().oracle_zrsvd(a.ctypes.data if a.size else None, m, n, max(m, 1), rank, oversample,
+                              power, seed & ((1 << 64) - 1),
+                              None if om is None else om.ctypes.data, U.ctypes.data, S.ctypes.data,
+                              Vt.ctypes.data, k, ctypes.byref(r), ctypes.byref(dw)))
+    rr = r.value
+    return U[:, :rr].copy(order="F"), S[:rr].copy(), Vt[:rr, :].copy(order="F"), dw.value
+
+
+def ztsvd(a, chi: int):
+    a = _z(a)
+    m, n = a.shape
+    kk = max(min(max(chi, 1), min(m, n)) if m and n else 1, 1)
+    U = np.zeros((m, kk), dtype=np.complex128, order="F")
+    S = np.zeros(kk)
+    Vt = np.zeros((kk, n), dtype=np.complex128, order="F")
+    r = ctypes.c_int64(0)
+    dw = ctypes.c_double(0.0)
+    _check(lib().oracle_ztsvd(a.ctypes.data if a.size else None, m, n, max(m, 1), chi,
+                              U.ctypes.data, S.ctypes.data, Vt.ctypes.data, kk, ctypes.byref(r),
+                              ctypes.byref(dw)))
+    rr = r.value
+    return U[:, :rr].copy(order="F"), S[:rr].copy(), Vt[:rr, :].copy(order="F"), dw.value
+
+
+def zrandomized_range(a, ell: int, power: int, seed: int, omega=None) -> np.ndarray:
+    a = _z(a)
+    m, n = a.shape
+    Q = np.zeros((m, max(ell, 1)), dtype=np.complex128, order="F")
+    om = None if omega is None else _z(omega)
+    _check(lib().oracle_zrandomized_range(a.ctypes.data if a.size else None, m, n, max(m, 1), ell,
+                                          power, seed & ((1 << 64) - 1),
+                                          None if om is None else om.ctypes.data, Q.ctypes.data))
+    return Q[:, :ell]
+
+
+def zreconstruction_error(a, U, S, Vt, spectral: bool = False) -> float:
+    a = _z(a)
+    m, n = a.shape
+    r = len(S)
+    U = _z(U) if r else np.zeros((m, 1), dtype=np.complex128, order="F")
+    Vt = _z(Vt) if r else np.zeros((1, n), dtype=np.complex128, order="F")
+    S = np.ascontiguousarray(S, dtype=np.float64) if r else np.zeros(1)
+    out = ctypes.c_double(0.0)
+    _check(lib().oracle_zreconstruction_error(a.ctypes.data, m, n, m, U.ctypes.data, S.ctypes.data,
+                                              Vt.ctypes.data, max(r, 1), r, int(spectral),
+                                              ctypes.byref(out)))
+    return out.value
+
+
+def zorthonormal_columns(a) -> np.ndarray:
+    a = _z(a)
+    m, n = a.shape
+    Q = np.zeros((m, min(m, n)), dtype=np.complex128, order="F")
+    _check(lib().oracle_zorthonormal_columns(a.ctypes.data, m, n, Q.ctypes.data))
+    return Q
+
+
+def zsingular_values(a) -> np.ndarray:
+    a = _z(a)
+    m, n = a.shape
+    s = np.zeros(min(m, n))
+    _check(lib().oracle_zsingular_values(a.ctypes.data, m, n, s.ctypes.data))
+    return s
+
+
+def zhaar(seed: int, rows: int, cols: int) -> np.ndarray:
+    """Haar-distributed complex isometry: Householder Q of a complex CounterRng
+    Gaussian, columns phase-fixed so that diag(R) = diag(Q^H G) is real > 0."""
+    g = zgaussian_matrix(seed, rows, cols)
+    q = zorthonormal_columns(g)
+    d = np.einsum("ij,ij->j", q.conj(), g)
+    ph = np.where(np.abs(d) > 0, d / np.where(np.abs(d) > 0, np.abs(d), 1.0), 1.0)
+    return np.asfortranarray(q * ph[None, :])

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "rlftn/rng.hpp"
 
@@ -32,6 +33,20 @@ int main(int argc, char** argv) {
       std::uint64_t bits;
       std::memcpy(&bits, &v, 8);
       std::printf("%s\"%016" PRIx64 "\"", i ? ", " : "", bits);
+    }
+    // Complex fill (rng.hpp:66-71): which Box-Muller value lands in re / im
+    // depends on the compiler's argument evaluation order, so it is dumped
+    // from the reference's own header as built here (g++).
+    rlftn::CounterRng c(seeds[s]);
+    std::vector<std::complex<double>> z(static_cast<std::size_t>(nnormal));
+    c.fill_gaussian(z.data(), z.size());
+    std::printf("], \"complex\": [");
+    for (int i = 0; i < nnormal; ++i) {
+      std::uint64_t br, bi;
+      const double re = z[static_cast<std::size_t>(i)].real(), im = z[static_cast<std::size_t>(i)].imag();
+      std::memcpy(&br, &re, 8);
+      std::memcpy(&bi, &im, 8);
+      std::printf("%s\"%016" PRIx64 "\", \"%016" PRIx64 "\"", i ? ", " : "", br, bi);
     }
     std::printf("]}%s\n", s + 1 < sizeof(seeds) / sizeof(seeds[0]) ? "," : "");
   }

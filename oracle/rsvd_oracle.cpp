@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdint>
 #include <cstring>
 #include <limits>
@@ -50,6 +51,23 @@ int BLASFN(LAPACKE_dgeqrf_work)(int layout, int m, int n, double* a, int lda, do
                                 double* work, int lwork);
 int BLASFN(LAPACKE_dorgqr_work)(int layout, int m, int n, int k, double* a, int lda,
                                 const double* tau, double* work, int lwork);
+// Complex instantiation (lapack.cpp:73-87, 100-110, 154-177; Eigen complex
+// operator* -> zgemm).  std::complex<double> is layout-compatible with
+// lapack_complex_double (lapack.cpp:4-6).
+enum { CblasConjTrans = 113 };
+void BLASFN(cblas_zgemm)(int layout, int ta, int tb, int m, int n, int k, const void* alpha,
+                         const void* a, int lda, const void* b, int ldb, const void* beta, void* c,
+                         int ldc);
+int BLASFN(LAPACKE_zgesdd_work)(int layout, char jobz, int m, int n, void* a, int lda, double* s,
+                                void* u, int ldu, void* vt, int ldvt, void* work, int lwork,
+                                double* rwork, int* iwork);
+int BLASFN(LAPACKE_zgesvd_work)(int layout, char jobu, char jobvt, int m, int n, void* a, int lda,
+                                double* s, void* u, int ldu, void* vt, int ldvt, void* work,
+                                int lwork, double* rwork);
+int BLASFN(LAPACKE_zgeqrf_work)(int layout, int m, int n, void* a, int lda, void* tau, void* work,
+                                int lwork);
+int BLASFN(LAPACKE_zungqr_work)(int layout, int m, int n, int k, void* a, int lda, const void* tau,
+                                void* work, int lwork);
 void BLASFN(openblas_set_num_threads)(int);
 int BLASFN(openblas_get_num_threads)(void);
 }
@@ -89,6 +107,19 @@ class CounterRng {
   }
   void fill_gaussian(double* dst, std::size_t n) {  // rng.hpp:62-64
     for (std::size_t i = 0; i < n; ++i) dst[i] = normal();
+  }
+  // rng.hpp:66-71: std::complex<double>(normal() * inv_sqrt2, normal() * inv_sqrt2).
+  // The two calls are unsequenced; g++ (the reference's Linux build) evaluates
+  // the imaginary argument first, so the Box-Muller cosine lands in im and the
+  // sine in re -- pinned by the reference-built KAT (tests/golden/rng_kat.json
+  // "complex").
+  void fill_gaussian(std::complex<double>* dst, std::size_t n) {
+    constexpr double inv_sqrt2 = 0.70710678118654752440;
+    for (std::size_t i = 0; i < n; ++i) {
+      const double first = normal();
+      const double second = normal();
+      dst[i] = std::complex<double>(second * inv_sqrt2, first * inv_sqrt2);
+    }
   }
 
  private:
@@ -449,6 +480,251 @@ BlockResult block_factorize(const std::vector<Mat>& blocks, const std::vector<st
   return out;
 }
 
+
+// ============================================================ complex ===
+// The reference instantiates the same path for std::complex<double>
+// (factorize.cpp:106-118; lapack.cpp:73-110, 154-177, 206-223).  Same
+// operation order; A^H where the real path has A^T (factorize.cpp:70, 86).
+namespace z {
+
+using C = std::complex<double>;
+
+struct Mat {
+  std::int64_t rows = 0, cols = 0;
+  std::vector<C> d;
+  Mat() = default;
+  Mat(std::int64_t r, std::int64_t c) : rows(r), cols(c), d(static_cast<std::size_t>(r * c), C(0)) {}
+  C* data() { return d.data(); }
+  const C* data() const { return d.data(); }
+  C& operator()(std::int64_t i, std::int64_t j) { return d[static_cast<std::size_t>(i + j * rows)]; }
+  C operator()(std::int64_t i, std::int64_t j) const { return d[static_cast<std::size_t>(i + j * rows)]; }
+  std::int64_t size() const { return rows * cols; }
+};
+
+struct Workspace {
+  std::vector<C> zwork;
+  std::vector<double> rwork;
+  std::vector<int> iwork;
+  C* zz(std::size_t n) {
+    if (zwork.size() < n) zwork.resize(n);
+    return zwork.data();
+  }
+  double* rr(std::size_t n) {
+    if (rwork.size() < n) rwork.resize(n);
+    return rwork.data();
+  }
+  int* ii(std::size_t n) {
+    if (iwork.size() < n) iwork.resize(n);
+    return iwork.data();
+  }
+};
+Workspace& ws() {
+  thread_local Workspace w;
+  return w;
+}
+
+// C = op(A) op(B), op in {N, H} (Eigen operator* / adjoint() -> zgemm).
+Mat gemm(const Mat& a, bool ha, const Mat& b, bool hb) {
+  const std::int64_t m = ha ? a.cols : a.rows;
+  const std::int64_t k = ha ? a.rows : a.cols;
+  const std::int64_t n = hb ? b.rows : b.cols;
+  Mat c(m, n);
+  if (m == 0 || n == 0 || k == 0) return c;
+  const C one(1.0), zero(0.0);
+  BLASFN(cblas_zgemm)(CblasColMajor, ha ? int(CblasConjTrans) : int(CblasNoTrans),
+                      hb ? int(CblasConjTrans) : int(CblasNoTrans), static_cast<int>(m), static_cast<int>(n),
+                      static_cast<int>(k), &one, a.data(),
+                      static_cast<int>(std::max<std::int64_t>(1, a.rows)), b.data(),
+                      static_cast<int>(std::max<std::int64_t>(1, b.rows)), &zero, c.data(),
+                      static_cast<int>(std::max<std::int64_t>(1, m)));
+  return c;
+}
+
+// lapack.cpp:73-87 (rwork sizing as there)
+int gesdd(char jobz, int m, int n, C* a, int lda, double* s, C* u, int ldu, C* vt, int ldvt) {
+  const auto k = static_cast<std::size_t>(std::min(m, n));
+  const auto mx = static_cast<std::size_t>(std::max(m, n));
+  const std::size_t lrwork =
+      jobz == 'N' ? 7 * k : std::max<std::size_t>(1, 5 * k * k + 7 * k) + 2 * k * mx;
+  C query = 0;
+  int info = BLASFN(LAPACKE_zgesdd_work)(kColMajor, jobz, m, n, a, lda, s, u, ldu, vt, ldvt, &query,
+                                         -1, ws().rr(lrwork), ws().ii(8 * k));
+  if (info != 0) return info;
+  const int lwork = static_cast<int>(query.real());
+  return BLASFN(LAPACKE_zgesdd_work)(kColMajor, jobz, m, n, a, lda, s, u, ldu, vt, ldvt,
+                                     ws().zz(static_cast<std::size_t>(lwork)), lwork,
+                                     ws().rr(lrwork), ws().ii(8 * k));
+}
+// lapack.cpp:100-110
+int gesvd(char jobu, char jobvt, int m, int n, C* a, int lda, double* s, C* u, int ldu, C* vt,
+          int ldvt) {
+  const auto k = static_cast<std::size_t>(std::min(m, n));
+  C query = 0;
+  int info = BLASFN(LAPACKE_zgesvd_work)(kColMajor, jobu, jobvt, m, n, a, lda, s, u, ldu, vt, ldvt,
+                                         &query, -1, ws().rr(5 * k));
+  if (info != 0) return info;
+  const int lwork = static_cast<int>(query.real());
+  return BLASFN(LAPACKE_zgesvd_work)(kColMajor, jobu, jobvt, m, n, a, lda, s, u, ldu, vt, ldvt,
+                                     ws().zz(static_cast<std::size_t>(lwork)), lwork,
+                                     ws().rr(5 * k));
+}
+
+// lapack.cpp:112-128
+void svd(const Mat& a, Mat& u, std::vector<double>& s, Mat& vt) {
+  const int m = static_cast<int>(a.rows), n = static_cast<int>(a.cols);
+  if (m == 0 || n == 0) throw std::invalid_argument("lapack::svd: empty matrix");
+  const int k = std::min(m, n);
+  u = Mat(m, k);
+  s.assign(static_cast<std::size_t>(k), 0.0);
+  vt = Mat(k, n);
+  Mat work = a;
+  int info = gesdd('S', m, n, work.data(), m, s.data(), u.data(), m, vt.data(), k);
+  if (info != 0) {
+    work = a;
+    info = gesvd('S', 'S', m, n, work.data(), m, s.data(), u.data(), m, vt.data(), k);
+    if (info != 0) fail("gesdd/gesvd", info);
+  }
+}
+
+// lapack.cpp:130-144
+std::vector<double> singular_values(const Mat& a) {
+  const int m = static_cast<int>(a.rows), n = static_cast<int>(a.cols);
+  if (m == 0 || n == 0) return {};
+  std::vector<double> s(static_cast<std::size_t>(std::min(m, n)));
+  Mat work = a;
+  int info = gesdd('N', m, n, work.data(), m, s.data(), nullptr, m, nullptr, 1);
+  if (info != 0) {
+    work = a;
+    info = gesvd('N', 'N', m, n, work.data(), m, s.data(), nullptr, m, nullptr, 1);
+    if (info != 0) fail("gesdd/gesvd", info);
+  }
+  return s;
+}
+
+// lapack.cpp:154-162, 171-177, 180-201, 216-219 (zgeqrf + zungqr)
+Mat orthonormal_columns(Mat a) {
+  const int m = static_cast<int>(a.rows), n = static_cast<int>(a.cols);
+  if (m == 0 || n == 0) throw std::invalid_argument("lapack::qr: empty matrix");
+  const int k = std::min(m, n);
+  std::vector<C> tau(static_cast<std::size_t>(k));
+  C query = 0;
+  int info = BLASFN(LAPACKE_zgeqrf_work)(kColMajor, m, n, a.data(), m, tau.data(), &query, -1);
+  if (info == 0) {
+    const int lwork = static_cast<int>(query.real());
+    info = BLASFN(LAPACKE_zgeqrf_work)(kColMajor, m, n, a.data(), m, tau.data(),
+                                       ws().zz(static_cast<std::size_t>(lwork)), lwork);
+  }
+  if (info != 0) fail("geqrf", info);
+  a.cols = k;
+  a.d.resize(static_cast<std::size_t>(m) * static_cast<std::size_t>(k));
+  info = BLASFN(LAPACKE_zungqr_work)(kColMajor, m, k, k, a.data(), m, tau.data(), &query, -1);
+  if (info == 0) {
+    const int lwork = static_cast<int>(query.real());
+    info = BLASFN(LAPACKE_zungqr_work)(kColMajor, m, k, k, a.data(), m, tau.data(),
+                                       ws().zz(static_cast<std::size_t>(lwork)), lwork);
+  }
+  if (info != 0) fail("orgqr", info);
+  return a;
+}
+
+struct Factorization {
+  Mat left;
+  std::vector<double> sigma;
+  Mat right_adj;
+  double discarded_weight = 0.0;
+  bool discarded_exact = true;
+};
+
+// factorize.cpp:26-38 (numerical_rank is scalar-independent, :17-24)
+Factorization truncate_full(const Mat& u, const std::vector<double>& s, const Mat& vt,
+                            std::int64_t chi, std::int64_t m, std::int64_t n) {
+  Factorization f;
+  const std::int64_t r = std::min(chi, numerical_rank(s, m, n));
+  for (std::size_t k = static_cast<std::size_t>(r); k < s.size(); ++k) f.discarded_weight += s[k] * s[k];
+  f.left = Mat(u.rows, r);
+  std::copy(u.d.begin(), u.d.begin() + static_cast<std::ptrdiff_t>(u.rows * r), f.left.d.begin());
+  f.sigma.assign(s.begin(), s.begin() + r);
+  f.right_adj = Mat(r, vt.cols);
+  for (std::int64_t j = 0; j < vt.cols; ++j)
+    for (std::int64_t i = 0; i < r; ++i) f.right_adj(i, j) = vt(i, j);
+  f.discarded_exact = true;
+  return f;
+}
+
+// factorize.cpp:42-50
+Factorization tsvd(const Mat& a, std::int64_t chi) {
+  if (a.rows == 0 || a.cols == 0) throw std::invalid_argument("tsvd: empty matrix");
+  if (chi < 1) throw std::invalid_argument("tsvd: rank must be >= 1");
+  Mat u, vt;
+  std::vector<double> s;
+  svd(a, u, s, vt);
+  return truncate_full(u, s, vt, chi, a.rows, a.cols);
+}
+
+// factorize.cpp:52-74 with Scalar = complex: Omega from the complex fill,
+// A^H on the power step.
+Mat randomized_range(const Mat& a, std::int64_t ell, int power, std::uint64_t seed,
+                     const C* omega = nullptr) {
+  const std::int64_t m = a.rows, n = a.cols;
+  if (m == 0 || n == 0) throw std::invalid_argument("randomized_range: empty matrix");
+  if (ell < 1 || ell > std::min(m, n))
+    throw std::invalid_argument("randomized_range: need 1 <= ell <= min(m, n)");
+  if (power < 0) throw std::invalid_argument("randomized_range: power must be >= 0");
+  Mat om(n, ell);
+  if (omega) {
+    std::copy(omega, omega + n * ell, om.d.begin());
+  } else {
+    CounterRng rng(seed);
+    rng.fill_gaussian(om.data(), static_cast<std::size_t>(om.size()));
+  }
+  Mat q = orthonormal_columns(gemm(a, false, om, false));
+  for (int t = 0; t < power; ++t) {
+    q = orthonormal_columns(gemm(a, true, q, false));
+    q = orthonormal_columns(gemm(a, false, q, false));
+  }
+  return q;
+}
+
+// factorize.cpp:76-95 (B = Q^H A)
+Factorization rsvd(const Mat& a, std::int64_t rank, std::int64_t oversample, int power,
+                   std::uint64_t seed, const C* omega = nullptr) {
+  const std::int64_t m = a.rows, n = a.cols;
+  if (m == 0 || n == 0) throw std::invalid_argument("rsvd: empty matrix");
+  if (rank < 1) throw std::invalid_argument("rsvd: rank must be >= 1");
+  std::int64_t ell = oversample;
+  if (ell == 0) ell = std::min(2 * rank, std::min(m, n));
+  if (ell < rank) throw std::invalid_argument("rsvd: oversample must be >= rank");
+  const Mat q = randomized_range(a, ell, power, seed, omega);
+  const Mat b = gemm(q, true, a, false);
+  Mat ub, vtb;
+  std::vector<double> sb;
+  svd(b, ub, sb, vtb);
+  Factorization f = truncate_full(ub, sb, vtb, rank, m, n);
+  f.left = gemm(q, false, f.left, false);
+  f.discarded_exact = false;
+  return f;
+}
+
+// factorize.cpp:97-104
+double reconstruction_error(const Mat& a, const Factorization& f, bool spectral) {
+  Mat us = f.left;
+  for (std::int64_t j = 0; j < us.cols; ++j)
+    for (std::int64_t i = 0; i < us.rows; ++i) us(i, j) *= f.sigma[static_cast<std::size_t>(j)];
+  Mat rec = gemm(us, false, f.right_adj, false);
+  if (rec.rows != a.rows || rec.cols != a.cols) rec = Mat(a.rows, a.cols);
+  Mat resid(a.rows, a.cols);
+  for (std::size_t i = 0; i < resid.d.size(); ++i) resid.d[i] = a.d[i] - rec.d[i];
+  if (!spectral) {
+    double s = 0.0;
+    for (const C& v : resid.d) s += std::norm(v);
+    return std::sqrt(s);
+  }
+  const std::vector<double> s = singular_values(resid);
+  return s.empty() ? 0.0 : s[0];
+}
+
+}  // namespace z
+
 }  // namespace oracle
 
 // ------------------------------------------------------------- C ABI ---
@@ -619,4 +895,81 @@ int oracle_block_factorize(std::int64_t ns, const std::int64_t* charges, const d
   });
 }
 
+}  // extern "C"
+
+// ---- complex instantiation (interleaved re/im, column-major) ----
+namespace {
+using ZC = std::complex<double>;
+oracle::z::Mat zwrap(const ZC* a, std::int64_t m, std::int64_t n, std::int64_t lda) {
+  oracle::z::Mat x(m, n);
+  for (std::int64_t j = 0; j < n; ++j) std::copy(a + j * lda, a + j * lda + m, x.data() + j * m);
+  return x;
+}
+void zemit(const oracle::z::Factorization& f, ZC* u, double* s, ZC* vt, std::int64_t ldvt,
+           std::int64_t* rank, double* dw) {
+  const std::int64_t r = static_cast<std::int64_t>(f.sigma.size());
+  *rank = r;
+  *dw = f.discarded_weight;
+  if (u) std::copy(f.left.d.begin(), f.left.d.end(), u);
+  if (s) std::copy(f.sigma.begin(), f.sigma.end(), s);
+  if (vt)
+    for (std::int64_t j = 0; j < f.right_adj.cols; ++j)
+      for (std::int64_t i = 0; i < r; ++i) vt[i + j * ldvt] = f.right_adj(i, j);
+}
+}  // namespace
+
+extern "C" {
+void oracle_zfill_gaussian(std::uint64_t seed, void* out, std::int64_t n) {
+  oracle::CounterRng rng(seed);
+  rng.fill_gaussian(static_cast<ZC*>(out), static_cast<std::size_t>(n));
+}
+int oracle_zrsvd(const void* a, std::int64_t m, std::int64_t n, std::int64_t lda, std::int64_t k,
+                 std::int64_t ell, int q, std::uint64_t seed, const void* omega, void* u, double* s,
+                 void* vt, std::int64_t ldvt, std::int64_t* rank, double* dw) {
+  return guarded([&] {
+    const auto am = zwrap(static_cast<const ZC*>(a), m, n, lda);
+    zemit(oracle::z::rsvd(am, k, ell, q, seed, static_cast<const ZC*>(omega)), static_cast<ZC*>(u),
+          s, static_cast<ZC*>(vt), ldvt, rank, dw);
+  });
+}
+int oracle_ztsvd(const void* a, std::int64_t m, std::int64_t n, std::int64_t lda, std::int64_t chi,
+                 void* u, double* s, void* vt, std::int64_t ldvt, std::int64_t* rank, double* dw) {
+  return guarded([&] {
+    const auto am = zwrap(static_cast<const ZC*>(a), m, n, lda);
+    zemit(oracle::z::tsvd(am, chi), static_cast<ZC*>(u), s, static_cast<ZC*>(vt), ldvt, rank, dw);
+  });
+}
+int oracle_zrandomized_range(const void* a, std::int64_t m, std::int64_t n, std::int64_t lda,
+                             std::int64_t ell, int q, std::uint64_t seed, const void* omega,
+                             void* qout) {
+  return guarded([&] {
+    const auto qm = oracle::z::randomized_range(zwrap(static_cast<const ZC*>(a), m, n, lda), ell, q,
+                                                seed, static_cast<const ZC*>(omega));
+    std::copy(qm.d.begin(), qm.d.end(), static_cast<ZC*>(qout));
+  });
+}
+int oracle_zreconstruction_error(const void* a, std::int64_t m, std::int64_t n, std::int64_t lda,
+                                 const void* u, const double* s, const void* vt, std::int64_t ldvt,
+                                 std::int64_t r, int spectral, double* out) {
+  return guarded([&] {
+    oracle::z::Factorization f;
+    f.left = zwrap(static_cast<const ZC*>(u), m, r, m);
+    f.sigma.assign(s, s + r);
+    f.right_adj = zwrap(static_cast<const ZC*>(vt), r, n, ldvt);
+    *out = oracle::z::reconstruction_error(zwrap(static_cast<const ZC*>(a), m, n, lda), f,
+                                           spectral != 0);
+  });
+}
+int oracle_zorthonormal_columns(const void* a, std::int64_t m, std::int64_t n, void* qout) {
+  return guarded([&] {
+    const auto qm = oracle::z::orthonormal_columns(zwrap(static_cast<const ZC*>(a), m, n, m));
+    std::copy(qm.d.begin(), qm.d.end(), static_cast<ZC*>(qout));
+  });
+}
+int oracle_zsingular_values(const void* a, std::int64_t m, std::int64_t n, double* s) {
+  return guarded([&] {
+    const auto v = oracle::z::singular_values(zwrap(static_cast<const ZC*>(a), m, n, m));
+    std::copy(v.begin(), v.end(), s);
+  });
+}
 }  // extern "C"

@@ -40,14 +40,25 @@ def subspace_distance(U, U_ref) -> float:
     U_ref = np.asarray(U_ref)
     if U.shape[1] == 0:
         return 0.0
-    d = U - U_ref @ (U_ref.T @ U)
+    d = U - U_ref @ (U_ref.conj().T @ U)
     return float(np.linalg.norm(d, 2))
 
 
 def isometry_err(U) -> float:
     U = np.asarray(U)
     r = U.shape[1]
-    return float(np.max(np.abs(U.T @ U - np.eye(r)))) if r else 0.0
+    return float(np.max(np.abs(U.conj().T @ U - np.eye(r)))) if r else 0.0
+
+
+def zmatrix_with_spectrum(oracle, seed: int, rows: int, cols: int, sigma) -> np.ndarray:
+    """Complex A = U diag(sigma) V^H with Haar complex isometries
+    (helpers.hpp:78-88 matrix_with_spectrum<Complex>, regenerated from the
+    complex CounterRng fill + the oracle's zgeqrf/zungqr)."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    r = len(sigma)
+    u = oracle.zhaar(oracle.derive_seed(seed, 1), rows, r)
+    v = oracle.zhaar(oracle.derive_seed(seed, 2), cols, r)
+    return np.asfortranarray((u * sigma[None, :]) @ v.conj().T)
 
 
 def ulp_distance(a: np.ndarray, b: np.ndarray) -> np.ndarray:
