@@ -143,6 +143,46 @@ int rsvd_reconstruction_error_f64(rsvd_handle handle, const double* A, int64_t m
                                   const double* Vt, int64_t ldvt, int64_t r, double* out,
                                   int flags);
 
+/* ---- Complex instantiation: Scalar = std::complex<double> ------------------
+ * The reference instantiates the same path for Complex (factorize.cpp:106-118:
+ * rsvd, tsvd, randomized_range, reconstruction_error over zgemm, zgeqrf+zungqr
+ * and zgesdd/zgesvd, lapack.cpp:73-110, 154-177), used by complex TEBD runs
+ * (mps.cpp:549-569, cli.cpp:164).  Matrices are std::complex<double> /
+ * complex128 column-major, passed as double* to the interleaved (re, im)
+ * storage; leading dimensions and strides count COMPLEX elements; S (singular
+ * values) and discarded_weight stay real.  Arguments, defaults, errors and
+ * messages are those of the double entry points above; Vt is V^H (right_adj).
+ * Omega is the reference's complex CounterRng fill (rng.hpp:66-71). */
+int rsvd_z128(rsvd_handle handle, const double* A, int64_t m, int64_t n, int64_t lda,
+              int64_t rank, int64_t oversample, int power, uint64_t seed, double* U, int64_t ldu,
+              double* S, double* Vt, int64_t ldvt, int64_t* out_rank, double* discarded_weight,
+              int flags);
+int rsvd_z128_batched(rsvd_handle handle, int64_t batch, const double* A, int64_t m, int64_t n,
+                      int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
+                      const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
+                      int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
+                      int64_t* out_rank, double* discarded_weight, int flags);
+/* rlftn::tsvd<Complex> (factorize.cpp:42-50); GPU path for min(m, n) <= 1024. */
+int rsvd_tsvd_z128(rsvd_handle handle, const double* A, int64_t m, int64_t n, int64_t lda,
+                   int64_t chi, double* U, int64_t ldu, double* S, double* Vt, int64_t ldvt,
+                   int64_t* out_rank, double* discarded_weight, int flags);
+int rsvd_tsvd_z128_batched(rsvd_handle handle, int64_t batch, const double* A, int64_t m,
+                           int64_t n, int64_t lda, int64_t strideA, int64_t chi, double* U,
+                           int64_t ldu, int64_t strideU, double* S, int64_t strideS, double* Vt,
+                           int64_t ldvt, int64_t strideVt, int64_t* out_rank,
+                           double* discarded_weight, int flags);
+int rsvd_randomized_range_z128(rsvd_handle handle, const double* A, int64_t m, int64_t n,
+                               int64_t lda, int64_t ell, int power, uint64_t seed, double* Q,
+                               int64_t ldq, int flags);
+int rsvd_reconstruction_error_z128(rsvd_handle handle, const double* A, int64_t m, int64_t n,
+                                   int64_t lda, const double* U, int64_t ldu, const double* S,
+                                   const double* Vt, int64_t ldvt, int64_t r, double* out,
+                                   int flags);
+/* CounterRng(seed).fill_gaussian(complex<double>*, count) (rng.hpp:66-71):
+ * out receives 2 * count doubles. */
+int rsvd_fill_gaussian_z128(rsvd_handle handle, uint64_t seed, double* out, int64_t count,
+                            int flags);
+
 /* Argument validation of rlftn::rsvd + randomized_range with the reference's
  * order and messages (factorize.cpp:79-83, 56-59); host-only, usable without a
  * GPU.  On success *ell_out is the resolved sample width. */

@@ -95,6 +95,14 @@ SIGNATURES = {
          ctypes.POINTER(ctypes.c_double), _c_int],
     ),
 }
+# Complex instantiation: same signatures as the double entry points.
+for _z, _d in (("rsvd_z128", "rsvd_f64"), ("rsvd_z128_batched", "rsvd_f64_batched"),
+               ("rsvd_tsvd_z128", "rsvd_tsvd_f64"),
+               ("rsvd_tsvd_z128_batched", "rsvd_tsvd_f64_batched"),
+               ("rsvd_randomized_range_z128", "rsvd_randomized_range_f64"),
+               ("rsvd_reconstruction_error_z128", "rsvd_reconstruction_error_f64"),
+               ("rsvd_fill_gaussian_z128", "rsvd_fill_gaussian_f64")):
+    SIGNATURES[_z] = SIGNATURES[_d]
 
 _lib = None
 _lock = threading.Lock()

@@ -176,4 +176,33 @@ void launch_scale_columns(MatRef X, int64_t rows, int64_t cols, const double* sc
 void launch_residual_sumsq(CMatRef A, CMatRef R, int64_t rows, int64_t cols, double* partial,
                            int64_t nparts, cudaStream_t st);
 
+// zkern.cu — complex instantiation (see the layout notes there).
+void launch_zfill_gaussian_p(MatRef out, int64_t rows, int64_t lp, int64_t ell,
+                             const uint64_t* seeds_dev, int64_t batch, cudaStream_t st);
+void launch_zfill_gaussian_flat(double* out, int64_t count, uint64_t seed, cudaStream_t st);
+void launch_zcombine_nn(CMatRef P, MatRef Y, int64_t m, int64_t lp, int64_t batch,
+                        cudaStream_t st);
+void launch_zpair(CMatRef Q, MatRef out, int64_t m, int64_t lp, int64_t batch, cudaStream_t st);
+void launch_zp2i(CMatRef X, MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                 cudaStream_t st);
+void launch_zi2p(CMatRef X, MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                 cudaStream_t st);
+void launch_zadjoint(CMatRef X, bool from_p, MatRef out, int64_t rows, int64_t cols,
+                     int64_t batch, cudaStream_t st);
+void launch_zidentity_p(MatRef X, int64_t rows, int64_t lp, int64_t ell, int64_t batch,
+                        cudaStream_t st);
+void launch_zchol(const double* Gt, double* Tt, double* Rt, double* W, double* Rc, double* Tc,
+                  int* rank, int* rank2, int* colmap, int* ill, const int* mask, int64_t ell,
+                  int64_t lp, double tau, double shift_coef, int mode, int64_t batch,
+                  cudaStream_t st);
+void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
+                    double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
+                    int64_t batch, cudaStream_t st);
+void launch_zfinalize(const double* W, int64_t lp, int64_t ell, int64_t k, int64_t m, int64_t n,
+                      double* sigma_out, int* perm, int* rank, double* dw, int64_t batch,
+                      cudaStream_t st);
+void launch_zlift_operand(const double* W, int64_t lp, const int* perm, const double* sigma,
+                          int64_t k, const int* rank, int64_t ell, bool half, MatRef M,
+                          int64_t batch, cudaStream_t st);
+
 }  // namespace rsvd

@@ -1111,6 +1111,8 @@ uint64_t mix64_host(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+#include "zpath.inc"
+
 }  // namespace
 }  // namespace rsvd
 
@@ -1375,6 +1377,86 @@ int rsvd_reconstruction_error_f64(rsvd_handle h, const double* A, int64_t m, int
                                   int flags) {
   return rsvd::guarded(h, [&] {
     rsvd::recon_impl(h, A, m, n, lda, U, ldu, S, Vt, ldvt, r, out, flags);
+  });
+}
+
+// ---- complex instantiation (rlftn::rsvd<std::complex<double>> etc.) ----
+
+int rsvd_fill_gaussian_z128(rsvd_handle h, uint64_t seed, double* out, int64_t count, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::check_flags(flags);
+    if (count < 0) throw rsvd::InvalidArgument("fill_gaussian: count must be >= 0");
+    if (count == 0) return;
+    if (!out) throw rsvd::InvalidArgument("fill_gaussian: null pointer argument");
+    RSVD_CUDA(cudaSetDevice(h->device));
+    double* dst = out;
+    if (flags == RSVD_PTR_HOST) {
+      h->arena.reserve(sizeof(double) * 2 * count + 256);
+      dst = reinterpret_cast<double*>(h->arena.base);
+    }
+    rsvd::launch_zfill_gaussian_flat(dst, count, seed, h->stream);
+    if (flags == RSVD_PTR_HOST)
+      RSVD_CUDA(cudaMemcpyAsync(out, dst, sizeof(double) * 2 * count, cudaMemcpyDeviceToHost,
+                                h->stream));
+    RSVD_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int rsvd_z128(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t rank,
+              int64_t oversample, int power, uint64_t seed, double* U, int64_t ldu, double* S,
+              double* Vt, int64_t ldvt, int64_t* out_rank, double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::zrsvd_batched_impl(h, 1, A, m, n, lda, 0, rank, oversample, power, &seed, U, ldu, 0, S,
+                             0, Vt, ldvt, 0, out_rank, discarded_weight, flags);
+  });
+}
+
+int rsvd_z128_batched(rsvd_handle h, int64_t batch, const double* A, int64_t m, int64_t n,
+                      int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
+                      const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
+                      int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
+                      int64_t* out_rank, double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::zrsvd_batched_impl(h, batch, A, m, n, lda, strideA, rank, oversample, power, seeds, U,
+                             ldu, strideU, S, strideS, Vt, ldvt, strideVt, out_rank,
+                             discarded_weight, flags);
+  });
+}
+
+int rsvd_tsvd_z128(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t chi,
+                   double* U, int64_t ldu, double* S, double* Vt, int64_t ldvt, int64_t* out_rank,
+                   double* discarded_weight, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::ztsvd_impl(h, 1, A, m, n, lda, 0, chi, U, ldu, 0, S, 0, Vt, ldvt, 0, out_rank,
+                     discarded_weight, flags);
+  });
+}
+
+int rsvd_tsvd_z128_batched(rsvd_handle h, int64_t batch, const double* A, int64_t m, int64_t n,
+                           int64_t lda, int64_t strideA, int64_t chi, double* U, int64_t ldu,
+                           int64_t strideU, double* S, int64_t strideS, double* Vt, int64_t ldvt,
+                           int64_t strideVt, int64_t* out_rank, double* discarded_weight,
+                           int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::ztsvd_impl(h, batch, A, m, n, lda, strideA, chi, U, ldu, strideU, S, strideS, Vt, ldvt,
+                     strideVt, out_rank, discarded_weight, flags);
+  });
+}
+
+int rsvd_randomized_range_z128(rsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                               int64_t ell, int power, uint64_t seed, double* Q, int64_t ldq,
+                               int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::zrange_impl(h, A, m, n, lda, ell, power, seed, Q, ldq, flags);
+  });
+}
+
+int rsvd_reconstruction_error_z128(rsvd_handle h, const double* A, int64_t m, int64_t n,
+                                   int64_t lda, const double* U, int64_t ldu, const double* S,
+                                   const double* Vt, int64_t ldvt, int64_t r, double* out,
+                                   int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::zrecon_impl(h, A, m, n, lda, U, ldu, S, Vt, ldvt, r, out, flags);
   });
 }
 

@@ -1,0 +1,761 @@
+// Complex (std::complex<double>) instantiation of the RSVD path: the device
+// kernels that are specific to complex arithmetic.  The reference instantiates
+// rsvd / tsvd / randomized_range for Complex (factorize.cpp:106-118) on top of
+// zgemm, zgeqrf+zungqr and zgesdd (lapack.cpp:73-110, 154-177).
+//
+// Layouts (see zpath.inc for the pipeline):
+//   I-layout  the caller's complex128 column-major matrix; viewed as a real
+//             (2 rows) x cols matrix with interleaved (re, im) rows ("A-hat").
+//   P-layout  a complex rows x l basis stored as a real rows x 2lp matrix:
+//             column 2j = Re x_j, column 2j+1 = Im x_j.  Every small complex
+//             product is then a real GEMM against a realified right factor
+//             M~ (M~[2a,2c] = Re M, M~[2a+1,2c] = -Im M, M~[2a,2c+1] = Im M,
+//             M~[2a+1,2c+1] = Re M), so (X M)_P = X_P M~, and the CholeskyQR
+//             Gram of X is read off the real Gram X_P^T X_P.
+//   PAIR      the real 2 rows x 2lp matrix [x^_j, (-i x_j)^] (interleaved):
+//             A-hat^T PAIR(Q) = (A^H Q)_P, the TN A-pass, lands in P-layout.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace rsvd {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform_from(uint64_t w) {
+  return static_cast<double>((w >> 11) + 1) * 0x1.0p-53;
+}
+
+unsigned grid_for(int64_t work, int threads, int cap_per_sm = 8) {
+  return static_cast<unsigned>(
+      std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * kNumSMs)));
+}
+
+// ---------------------------------------------------------------- Omega
+// Complex CounterRng fill (rng.hpp:66-71) of Omega (n x l) in column-major
+// linear order: entry t = i + j n takes Box-Muller pair t, i.e. words 2t+1
+// (radius) and 2t+2 (angle).  g++ evaluates the imaginary constructor
+// argument first, so re = (r sin) / sqrt 2 and im = (r cos) / sqrt 2 (pinned by
+// the reference-built KAT, tests/golden/rng_kat.json "complex").
+// Written to P-layout; columns j >= l are zero.
+__global__ void zfill_kernel(double* __restrict__ out, int64_t ld, int64_t stride, int64_t rows,
+                             int64_t lp, int64_t ell, const uint64_t* __restrict__ seeds,
+                             int64_t batch) {
+  const int64_t per = rows * lp;
+  const int64_t total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t j = x / rows, i = x - j * rows;
+    double re = 0.0, im = 0.0;
+    if (j < ell) {
+      const uint64_t t = static_cast<uint64_t>(i + j * rows);
+      const uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+      const double u1 = uniform_from(mix64(seeds[b] + (2 * t + 1) * kGolden));
+      const double u2 = uniform_from(mix64(seeds[b] + (2 * t + 2) * kGolden));
+      const double r = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincos((2.0 * 3.141592653589793) * u2, &sn, &cs);
+      constexpr double inv_sqrt2 = 0.70710678118654752440;
+      re = __dmul_rn(__dmul_rn(r, sn), inv_sqrt2);
+      im = __dmul_rn(__dmul_rn(r, cs), inv_sqrt2);
+    }
+    double* o = out + b * stride;
+    o[i + (2 * j) * ld] = re;
+    o[i + (2 * j + 1) * ld] = im;
+  }
+}
+
+__global__ void zfill_flat_kernel(double2* __restrict__ out, int64_t count, uint64_t seed) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+    const double u1 = uniform_from(mix64(seed + (2 * t + 1) * kGolden));
+    const double u2 = uniform_from(mix64(seed + (2 * t + 2) * kGolden));
+    const double r = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincos((2.0 * 3.141592653589793) * u2, &sn, &cs);
+    constexpr double inv_sqrt2 = 0.70710678118654752440;
+    out[t] = make_double2(__dmul_rn(__dmul_rn(r, sn), inv_sqrt2),
+                          __dmul_rn(__dmul_rn(r, cs), inv_sqrt2));
+  }
+}
+
+// -------------------------------------------------------- layout glue
+// NN A-pass combine: Pm = A-hat X_P (2m x 2lp; column 2j = (A Re x_j)^,
+// 2j+1 = (A Im x_j)^) -> Y = A x_j in P-layout:
+//   Re y = Re(P_2j) - Im(P_2j+1),  Im y = Im(P_2j) + Re(P_2j+1).
+__global__ void zcombine_nn_kernel(const double* __restrict__ P, int64_t ldp, int64_t sp,
+                                   double* __restrict__ Y, int64_t ldy, int64_t sy, int64_t m,
+                                   int64_t lp, int64_t batch) {
+  const int64_t per = m * lp, total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t j = x / m, i = x - j * m;
+    const double* pb = P + b * sp;
+    const double2 p0 = *reinterpret_cast<const double2*>(pb + 2 * i + (2 * j) * ldp);
+    const double2 p1 = *reinterpret_cast<const double2*>(pb + 2 * i + (2 * j + 1) * ldp);
+    double* yb = Y + b * sy;
+    yb[i + (2 * j) * ldy] = p0.x - p1.y;
+    yb[i + (2 * j + 1) * ldy] = p0.y + p1.x;
+  }
+}
+
+// PAIR(Q): P-layout Q (m x 2lp) -> real 2m x 2lp with column 2j = q^_j and
+// column 2j+1 = (-i q_j)^ = (Im q, -Re q) interleaved.
+__global__ void zpair_kernel(const double* __restrict__ Q, int64_t ldq, int64_t sq,
+                             double* __restrict__ out, int64_t ldo, int64_t so, int64_t m,
+                             int64_t lp, int64_t batch) {
+  const int64_t per = m * lp, total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t j = x / m, i = x - j * m;
+    const double re = Q[b * sq + i + (2 * j) * ldq], im = Q[b * sq + i + (2 * j + 1) * ldq];
+    double* ob = out + b * so;
+    *reinterpret_cast<double2*>(ob + 2 * i + (2 * j) * ldo) = make_double2(re, im);
+    *reinterpret_cast<double2*>(ob + 2 * i + (2 * j + 1) * ldo) = make_double2(im, -re);
+  }
+}
+
+// P-layout -> I-layout (rows x cols complex): out[i, c] = X[i, 2c] + i X[i, 2c+1].
+__global__ void zp2i_kernel(const double* __restrict__ X, int64_t ldx, int64_t sx,
+                            double* __restrict__ out, int64_t ldo, int64_t so, int64_t rows,
+                            int64_t cols, int64_t batch) {
+  const int64_t per = rows * cols, total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t c = x / rows, i = x - c * rows;
+    const double re = X[b * sx + i + (2 * c) * ldx], im = X[b * sx + i + (2 * c + 1) * ldx];
+    *reinterpret_cast<double2*>(out + b * so + 2 * i + c * ldo) = make_double2(re, im);
+  }
+}
+
+// I-layout -> P-layout (rows x cols complex).
+__global__ void zi2p_kernel(const double* __restrict__ X, int64_t ldx, int64_t sx,
+                            double* __restrict__ out, int64_t ldo, int64_t so, int64_t rows,
+                            int64_t cols, int64_t batch) {
+  const int64_t per = rows * cols, total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t c = x / rows, i = x - c * rows;
+    const double2 v = *reinterpret_cast<const double2*>(X + b * sx + 2 * i + c * ldx);
+    out[b * so + i + (2 * c) * ldo] = v.x;
+    out[b * so + i + (2 * c + 1) * ldo] = v.y;
+  }
+}
+
+// Conjugate transpose, P-layout in (rows x cols complex) -> I-layout out
+// (cols x rows complex): out[c, i] = conj(X[i, c]).  32 x 32 complex tiles.
+__global__ void zadj_p2i_kernel(const double* __restrict__ X, int64_t ldx, int64_t sx,
+                                double* __restrict__ out, int64_t ldo, int64_t so, int64_t rows,
+                                int64_t cols) {
+  __shared__ double2 tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const double* src = X + b * sx;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + y;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < rows && c < cols) v = make_double2(src[r + (2 * c) * ldx], -src[r + (2 * c + 1) * ldx]);
+    tile[y][threadIdx.x] = v;
+  }
+  __syncthreads();
+  double* dst = out + b * so;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + y;  // out(c, r) = conj(X(r, c))
+    if (c < cols && r < rows) *reinterpret_cast<double2*>(dst + 2 * c + r * ldo) = tile[threadIdx.x][y];
+  }
+}
+
+// Conjugate transpose in I-layout (rows x cols -> cols x rows).
+__global__ void zadj_i2i_kernel(const double* __restrict__ X, int64_t ldx, int64_t sx,
+                                double* __restrict__ out, int64_t ldo, int64_t so, int64_t rows,
+                                int64_t cols) {
+  __shared__ double2 tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const double* src = X + b * sx;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + y;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < rows && c < cols) {
+      v = *reinterpret_cast<const double2*>(src + 2 * r + c * ldx);
+      v.y = -v.y;
+    }
+    tile[y][threadIdx.x] = v;
+  }
+  __syncthreads();
+  double* dst = out + b * so;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + y;
+    if (c < cols && r < rows) *reinterpret_cast<double2*>(dst + 2 * c + r * ldo) = tile[threadIdx.x][y];
+  }
+}
+
+// Identity in P-layout (rows x l complex, l <= rows): X[i, 2i] = 1.
+__global__ void zidentity_p_kernel(double* __restrict__ X, int64_t ld, int64_t stride, int64_t rows,
+                                   int64_t lp, int64_t ell, int64_t batch) {
+  const int64_t per = rows * 2 * lp, total = per * batch;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w / per, x = w - b * per;
+    const int64_t c = x / rows, i = x - c * rows;
+    X[b * stride + i + c * ld] = (c % 2 == 0 && c / 2 == i && i < ell) ? 1.0 : 0.0;
+  }
+}
+
+// ------------------------------------------------------ complex Cholesky
+// Hermitian Gram G (l x l) = X^H X read off the realified real Gram
+// Gt = X_P^T X_P (2lp x 2lp):
+//   G_ac = Gt[2a,2c] + Gt[2a+1,2c+1] + i (Gt[2a,2c+1] - Gt[2a+1,2c]).
+// Factor G = R^H R (optionally with diagonal pivoting, dpstrf-style), stop at
+// the first pivot <= tau * max diag (numerical rank r), T = R11^-1; write the
+// realified T~ (with the pivot as a real column map) and R~ (columns scattered
+// back: Y_in = Q_out R~).  One CTA per item; the working copy lives in a
+// global scratch (L2 resident).
+//   mode 0: unpivoted; an item that breaks down is refactored as G + s tr(G) I
+//           (shifted CholeskyQR, never truncated) and flagged ill[b] = 1.
+//   mode 1: pivoted, items with mask[b] == 0 skipped.
+//   mode 2: unpivoted, plain (breakdown -> rank).
+struct ZCholArgs {
+  const double* Gt;  // 2lp x 2lp per item
+  double* Tt;        // 2lp x 2lp per item (realified T)
+  double* Rt;        // optional, 2lp x 2lp per item (realified R P^T)
+  double2* W;        // scratch lp x lp per item
+  double2* Rc;       // scratch lp x lp per item (R, pivoted order)
+  double2* Tc;       // scratch lp x lp per item (T)
+  int* rank;         // complex rank per item
+  int* rank2;        // 2 * rank (real column count of the P-layout basis)
+  int* colmap;       // 2lp per item (pivoted mode)
+  int* ill;          // mode 0 output
+  const int* mask;   // mode 1 input
+  int64_t ell, lp;
+  double tau, shift_coef;
+  int mode;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+
+__global__ void __launch_bounds__(512) zchol_kernel(ZCholArgs p) {
+  const int64_t b = blockIdx.x;
+  const int ell = static_cast<int>(p.ell);
+  const int64_t lp = p.lp, L = 2 * lp;
+  if (p.mode == 1 && !p.mask[b]) return;
+  __shared__ int s_piv[1024];
+  __shared__ double s_red[32];
+  __shared__ int s_redi[32];
+  __shared__ int s_rank, s_shift, s_pivot;
+  __shared__ double s_dmax;
+  const double* Gt = p.Gt + b * L * L;
+  double2* W = p.W + b * lp * lp;
+  double2* Rc = p.Rc + b * lp * lp;
+  double2* Tc = p.Tc + b * lp * lp;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const bool pivot = p.mode == 1;
+  if (tid == 0) s_shift = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    // Load G (full Hermitian) into W, optional shift.
+    for (int64_t e = tid; e < static_cast<int64_t>(ell) * ell; e += nt) {
+      const int a = static_cast<int>(e % ell), c = static_cast<int>(e / ell);
+      const double re = Gt[2 * a + (2 * c) * L] + Gt[2 * a + 1 + (2 * c + 1) * L];
+      const double im = Gt[2 * a + (2 * c + 1) * L] - Gt[2 * a + 1 + (2 * c) * L];
+      W[a + c * lp] = make_double2(re, a == c ? 0.0 : im);
+    }
+    for (int a = tid; a < ell; a += nt) s_piv[a] = a;
+    __syncthreads();
+    if (s_shift) {  // G + coef * tr(G) * I
+      if (warp == 0) {
+        double tr = 0.0;
+        for (int a = lane; a < ell; a += 32) tr += W[a + a * lp].x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        if (lane == 0) s_red[0] = tr;
+      }
+      __syncthreads();
+      const double sh = p.shift_coef * s_red[0];
+      for (int a = tid; a < ell; a += nt) W[a + a * lp].x += sh;
+      __syncthreads();
+    }
+    // max diagonal
+    {
+      double mx = 0.0;
+      for (int a = tid; a < ell; a += nt) mx = fmax(mx, W[a + a * lp].x);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) s_red[warp] = mx;
+      __syncthreads();
+      if (tid == 0) {
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v = fmax(v, s_red[w]);
+        s_dmax = v;
+        s_rank = ell;
+      }
+      __syncthreads();
+    }
+    const double floor_v = p.tau * s_dmax;
+    for (int j = 0; j < ell; ++j) {
+      if (pivot) {
+        double best = -1.0;
+        int bi = j;
+        for (int a = j + tid; a < ell; a += nt) {
+          const double d = W[s_piv[a] + s_piv[a] * lp].x;
+          if (d > best) best = d, bi = a;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
+        }
+        if (lane == 0) s_red[warp] = best, s_redi[warp] = bi;
+        __syncthreads();
+        if (tid == 0) {
+          double bv = s_red[0];
+          int bx = s_redi[0];
+          for (int w = 1; w < nw; ++w)
+            if (s_red[w] > bv || (s_red[w] == bv && s_redi[w] < bx)) bv = s_red[w], bx = s_redi[w];
+          const int t = s_piv[j];
+          s_piv[j] = s_piv[bx];
+          s_piv[bx] = t;
+        }
+        __syncthreads();
+      }
+      const int pj = s_piv[j];
+      const double d = W[pj + pj * lp].x;
+      if (!(d > floor_v) || !(d > 0.0)) {
+        if (tid == 0) s_rank = j;
+        __syncthreads();
+        break;
+      }
+      const double rjj = sqrt(d), inv = 1.0 / rjj;
+      // Row j of R (pivoted order): R[j, c] = W[pj, pc] / rjj, c > j.
+      for (int c = j + 1 + tid; c < ell; c += nt) {
+        const double2 w = W[pj + s_piv[c] * lp];
+        Rc[j + c * lp] = make_double2(w.x * inv, w.y * inv);
+      }
+      if (tid == 0) Rc[j + j * lp] = make_double2(rjj, 0.0);
+      __syncthreads();
+      // Trailing update W[pa, pc] -= conj(R[j, a]) R[j, c], a, c > j.
+      const int nr = ell - j - 1;
+      for (int64_t e = tid; e < static_cast<int64_t>(nr) * nr; e += nt) {
+        const int a = j + 1 + static_cast<int>(e % nr), c = j + 1 + static_cast<int>(e / nr);
+        const double2 ra = Rc[j + a * lp], rc = Rc[j + c * lp];
+        const double2 u = cconjmul(ra, rc);
+        double2& w = W[s_piv[a] + s_piv[c] * lp];
+        w.x -= u.x;
+        w.y -= u.y;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (p.mode == 0 && attempt == 0 && s_rank < ell) {
+      if (tid == 0) s_shift = 1;
+      __syncthreads();
+      continue;  // refactor the shifted Gram
+    }
+    break;
+  }
+  const int r = s_rank;
+  if (tid == 0) {
+    p.rank[b] = r;
+    if (p.rank2) p.rank2[b] = 2 * r;
+    if (p.ill) p.ill[b] = s_shift;
+  }
+  // T = R11^-1, rows bottom-up: T[a, c] = (delta_ac - sum_{a<k<=c} R[a,k] T[k,c]) / R[a,a].
+  for (int a = r - 1; a >= 0; --a) {
+    const double2 raa = Rc[a + a * lp];
+    const double iv = 1.0 / raa.x;
+    for (int c = a + tid; c < r; c += nt) {
+      double2 s = make_double2(c == a ? 1.0 : 0.0, 0.0);
+      for (int k = a + 1; k <= c; ++k) {
+        const double2 u = cmul(Rc[a + k * lp], Tc[k + c * lp]);
+        s.x -= u.x;
+        s.y -= u.y;
+      }
+      Tc[a + c * lp] = make_double2(s.x * iv, s.y * iv);
+    }
+    __syncthreads();
+  }
+  // Realified outputs.
+  double* Tt = p.Tt + b * L * L;
+  for (int64_t e = tid; e < L * L; e += nt) {
+    const int64_t R2 = e % L, C2 = e / L;
+    const int a = static_cast<int>(R2 >> 1), c = static_cast<int>(C2 >> 1);
+    double v = 0.0;
+    if (a < r && c < r && a <= c) {
+      const double2 t = Tc[a + c * lp];
+      const int ra = static_cast<int>(R2 & 1), rc = static_cast<int>(C2 & 1);
+      v = (ra == rc) ? t.x : (ra ? -t.y : t.y);
+    }
+    Tt[e] = v;
+  }
+  if (p.Rt) {
+    double* Rt = p.Rt + b * L * L;
+    for (int64_t e = tid; e < L * L; e += nt) Rt[e] = 0.0;
+    __syncthreads();
+    // R P^T: column c of R (pivoted order) goes to column piv[c].
+    for (int64_t e = tid; e < static_cast<int64_t>(r) * ell; e += nt) {
+      const int a = static_cast<int>(e % r), c = static_cast<int>(e / r);
+      if (a > c) continue;
+      const double2 v = Rc[a + c * lp];
+      const int64_t oc = s_piv[c];
+      Rt[2 * a + (2 * oc) * L] = v.x;
+      Rt[2 * a + 1 + (2 * oc + 1) * L] = v.x;
+      Rt[2 * a + (2 * oc + 1) * L] = v.y;
+      Rt[2 * a + 1 + (2 * oc) * L] = -v.y;
+    }
+  }
+  if (p.colmap) {
+    int* cm = p.colmap + b * L;
+    for (int64_t e = tid; e < L; e += nt) {
+      const int c = static_cast<int>(e >> 1);
+      cm[e] = c < ell ? 2 * s_piv[c] + static_cast<int>(e & 1) : static_cast<int>(e);
+    }
+  }
+}
+
+// ------------------------------------------------------ complex Jacobi
+// One-sided (Hestenes) Jacobi on the complex l x l factor H (factorize.cpp:88
+// -> lapack::svd of B, here of Rt^H): columns p, q with alpha = |h_p|^2,
+// beta = |h_q|^2, gamma = h_p^H h_q = |gamma| e: the real rotation of
+// (h_p, conj(e) h_q) (zeta = (beta - alpha) / 2|gamma|, t = sign(zeta) /
+// (|zeta| + sqrt(1 + zeta^2))) gives h_p' = c h_p - s conj(e) h_q,
+// h_q' = s e h_p + c h_q; J accumulates the same unitary 2 x 2.  Rotation test
+// |gamma| > sqrt(l) eps sqrt(alpha beta) (dgesvj's); round-robin ordering,
+// every pair once per sweep; stops after a sweep with no rotation or whose
+// largest rotated ratio was below 1e-9 (quadratic convergence).
+// One CTA per item; H and J stay in global scratch (L2).
+//   src_mode 0: H = Rt^H from the realified R~t (2lp x 2lp);
+//   src_mode 1: H from a P-layout l x 2lp matrix (tsvd: H = A_e Qb).
+__global__ void __launch_bounds__(1024) zjacobi_kernel(const double* __restrict__ src,
+                                                       int64_t src_ld, int64_t src_stride,
+                                                       int src_mode, double2* __restrict__ H,
+                                                       double2* __restrict__ J, int64_t ell_,
+                                                       int64_t lp, int max_sweeps,
+                                                       int* __restrict__ sweeps_out) {
+  const int64_t b = blockIdx.x;
+  const int ell = static_cast<int>(ell_);
+  double2* Hb = H + b * lp * lp;
+  double2* Jb = J + b * lp * lp;
+  const double* S = src + b * src_stride;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int64_t e = tid; e < lp * lp; e += nt) {
+    const int a = static_cast<int>(e % lp), c = static_cast<int>(e / lp);
+    double2 h = make_double2(0.0, 0.0);
+    if (a < ell && c < ell) {
+      if (src_mode == 0)  // H[a, c] = conj(Rt[c, a]) = Rt~[2c, 2a] + i Rt~[2c+1, 2a]
+        h = make_double2(S[2 * c + (2 * a) * src_ld], S[2 * c + 1 + (2 * a) * src_ld]);
+      else
+        h = make_double2(S[a + (2 * c) * src_ld], S[a + (2 * c + 1) * src_ld]);
+    }
+    Hb[e] = h;
+    Jb[e] = make_double2(a == c ? 1.0 : 0.0, 0.0);
+  }
+  __shared__ unsigned long long s_max;  // largest rotated ratio of the sweep (bits of a double >= 0)
+  __shared__ int s_rot;
+  __syncthreads();
+  const int le = ell + (ell & 1);
+  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < max_sweeps && ell > 1; ++sweep) {
+    if (tid == 0) s_max = 0ull, s_rot = 0;
+    __syncthreads();
+    for (int step = 0; step < le - 1; ++step) {
+      for (int k = warp; k < le / 2; k += nw) {
+        const int pp = k == 0 ? 0 : ((k - 1 + step) % (le - 1)) + 1;
+        const int qq = ((le - 2 - k + step) % (le - 1)) + 1;
+        if (pp >= ell || qq >= ell) continue;
+        const int pc = min(pp, qq), qc = max(pp, qq);
+        double2* hp = Hb + pc * lp;
+        double2* hq = Hb + qc * lp;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = lane; i < ell; i += 32) {
+          const double2 x = hp[i], y = hq[i];
+          al = fma(x.x, x.x, fma(x.y, x.y, al));
+          be = fma(y.x, y.x, fma(y.y, y.y, be));
+          gr = fma(x.x, y.x, fma(x.y, y.y, gr));   // Re conj(x) y
+          gi = fma(x.x, y.y, fma(-x.y, y.x, gi));  // Im conj(x) y
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          gr += __shfl_xor_sync(0xffffffffu, gr, o);
+          gi += __shfl_xor_sync(0xffffffffu, gi, o);
+        }
+        const double g = hypot(gr, gi);
+        const double nrm = sqrt(al) * sqrt(be);
+        if (!(g > tol * nrm) || g == 0.0) continue;
+        if (lane == 0) {
+          atomicMax(&s_max, static_cast<unsigned long long>(__double_as_longlong(g / nrm)));
+          s_rot = 1;
+        }
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const double er = gr / g, ei = gi / g;  // e = gamma / |gamma|
+        // h_p' = c h_p - s conj(e) h_q ; h_q' = s e h_p + c h_q
+        auto rot = [&](double2* xp, double2* xq, int n) {
+          for (int i = lane; i < n; i += 32) {
+            const double2 x = xp[i], y = xq[i];
+            const double2 ey = make_double2(er * y.x + ei * y.y, er * y.y - ei * y.x);  // conj(e) y
+            const double2 ex = make_double2(er * x.x - ei * x.y, er * x.y + ei * x.x);  // e x
+            xp[i] = make_double2(c * x.x - s * ey.x, c * x.y - s * ey.y);
+            xq[i] = make_double2(s * ex.x + c * y.x, s * ex.y + c * y.y);
+          }
+        };
+        rot(hp, hq, ell);
+        rot(Jb + pc * lp, Jb + qc * lp, ell);
+      }
+      __syncthreads();
+    }
+    const bool any = s_rot != 0;
+    const double mx = __longlong_as_double(static_cast<long long>(s_max));
+    __syncthreads();
+    if (!any) {
+      ++sweep;
+      break;
+    }
+    if (mx < 1e-9) {
+      ++sweep;
+      break;
+    }
+  }
+  if (tid == 0 && sweeps_out) sweeps_out[b] = sweep;
+}
+
+// sigma_c = ||W e_c|| (complex columns), descending with ties by index,
+// numerical rank cut (factorize.cpp:17-24) r = min(k, rank), discarded weight
+// over the sampled tail (factorize.cpp:30-31).
+__global__ void zfinalize_kernel(const double2* __restrict__ W, int64_t lp, int ell, int64_t k,
+                                 int64_t m, int64_t n, double* __restrict__ sigma_out,
+                                 int* __restrict__ perm, int* __restrict__ rank_out,
+                                 double* __restrict__ dw_out) {
+  extern __shared__ double s_sig[];
+  int* s_pos = reinterpret_cast<int*>(s_sig + lp);
+  const int64_t b = blockIdx.x;
+  const double2* Wb = W + b * lp * lp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < ell; c += nw) {
+    double s = 0.0;
+    for (int r = lane; r < ell; r += 32) {
+      const double2 x = Wb[r + c * lp];
+      s = fma(x.x, x.x, fma(x.y, x.y, s));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) s_sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ell; c += blockDim.x) {
+    const double v = s_sig[c];
+    int pos = 0;
+    for (int d = 0; d < ell; ++d) {
+      const double w = s_sig[d];
+      pos += (w > v) || (w == v && d < c);
+    }
+    s_pos[c] = pos;
+    perm[b * lp + pos] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double smax = 0.0;
+    for (int c = 0; c < ell; ++c)
+      if (s_pos[c] == 0) smax = s_sig[c];
+    int nr = 0;
+    if (smax > 0.0) {
+      const double cut = static_cast<double>(m > n ? m : n) * DBL_EPSILON * smax;
+      for (int c = 0; c < ell; ++c) nr += s_sig[c] > cut;
+    }
+    const int r = static_cast<int>(nr < k ? nr : k);
+    rank_out[b] = r;
+    double dw = 0.0;
+    for (int pos = r; pos < ell; ++pos)
+      for (int c = 0; c < ell; ++c)
+        if (s_pos[c] == pos) {
+          dw += s_sig[c] * s_sig[c];
+          break;
+        }
+    dw_out[b] = dw;
+  }
+  __syncthreads();
+  const int r = rank_out[b];
+  for (int c = threadIdx.x; c < ell; c += blockDim.x) {
+    const int pos = s_pos[c];
+    if (pos < k) sigma_out[b * k + pos] = pos < r ? s_sig[c] : 0.0;
+  }
+  for (int pos = ell + threadIdx.x; pos < k; pos += blockDim.x) sigma_out[b * k + pos] = 0.0;
+}
+
+// Right factors of the lift, from the complex l x l W (or J) with the sorted
+// column order perm and 1/sigma (sigma may be null):
+//   half == 1: M (2lp x k) with M[2a, c] = Re w, M[2a+1, c] = -Im w, so that
+//              PAIR(Q) M = (Q w)^ lands in I-layout;
+//   half == 0: realified M~ (2lp x 2k) for a P-layout product.
+// Columns c >= rank[b] are zero.
+__global__ void zlift_operand_kernel(const double2* __restrict__ W, int64_t lp, const int* __restrict__ perm,
+                                     const double* __restrict__ sigma, int64_t k,
+                                     const int* __restrict__ rank, int ell, int half,
+                                     double* __restrict__ M, int64_t ldm, int64_t sm) {
+  const int64_t b = blockIdx.y;
+  const int r = rank[b];
+  const int64_t L = 2 * lp;
+  const int64_t cols = half ? k : 2 * k;
+  const int64_t total = L * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t R2 = e % L, C = e / L;
+    const int a = static_cast<int>(R2 >> 1), ra = static_cast<int>(R2 & 1);
+    const int c = static_cast<int>(half ? C : C >> 1), rc = static_cast<int>(half ? 0 : C & 1);
+    double v = 0.0;
+    if (c < r && a < ell) {
+      double2 w = W[b * lp * lp + a + static_cast<int64_t>(perm[b * lp + c]) * lp];
+      if (sigma) {
+        const double is = 1.0 / sigma[b * k + c];
+        w.x *= is;
+        w.y *= is;
+      }
+      v = (ra == rc) ? w.x : (ra ? -w.y : w.y);
+    }
+    M[b * sm + R2 + C * ldm] = v;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+void launch_zfill_gaussian_p(MatRef out, int64_t rows, int64_t lp, int64_t ell,
+                             const uint64_t* seeds_dev, int64_t batch, cudaStream_t st) {
+  if (rows <= 0 || lp <= 0 || batch <= 0) return;
+  zfill_kernel<<<grid_for(rows * lp * batch, 256), 256, 0, st>>>(out.base, out.ld, out.stride, rows,
+                                                                  lp, ell, seeds_dev, batch);
+  RSVD_LAUNCH("zfill_kernel");
+}
+
+void launch_zfill_gaussian_flat(double* out, int64_t count, uint64_t seed, cudaStream_t st) {
+  if (count <= 0) return;
+  zfill_flat_kernel<<<grid_for(count, 256, 16), 256, 0, st>>>(reinterpret_cast<double2*>(out),
+                                                              count, seed);
+  RSVD_LAUNCH("zfill_flat_kernel");
+}
+
+void launch_zcombine_nn(CMatRef P, MatRef Y, int64_t m, int64_t lp, int64_t batch,
+                        cudaStream_t st) {
+  if (m <= 0 || batch <= 0) return;
+  zcombine_nn_kernel<<<grid_for(m * lp * batch, 256), 256, 0, st>>>(P.base, P.ld, P.stride, Y.base,
+                                                                     Y.ld, Y.stride, m, lp, batch);
+  RSVD_LAUNCH("zcombine_nn_kernel");
+}
+
+void launch_zpair(CMatRef Q, MatRef out, int64_t m, int64_t lp, int64_t batch, cudaStream_t st) {
+  if (m <= 0 || batch <= 0) return;
+  zpair_kernel<<<grid_for(m * lp * batch, 256), 256, 0, st>>>(Q.base, Q.ld, Q.stride, out.base,
+                                                               out.ld, out.stride, m, lp, batch);
+  RSVD_LAUNCH("zpair_kernel");
+}
+
+void launch_zp2i(CMatRef X, MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                 cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return;
+  zp2i_kernel<<<grid_for(rows * cols * batch, 256), 256, 0, st>>>(X.base, X.ld, X.stride, out.base,
+                                                                   out.ld, out.stride, rows, cols,
+                                                                   batch);
+  RSVD_LAUNCH("zp2i_kernel");
+}
+
+void launch_zi2p(CMatRef X, MatRef out, int64_t rows, int64_t cols, int64_t batch,
+                 cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return;
+  zi2p_kernel<<<grid_for(rows * cols * batch, 256), 256, 0, st>>>(X.base, X.ld, X.stride, out.base,
+                                                                   out.ld, out.stride, rows, cols,
+                                                                   batch);
+  RSVD_LAUNCH("zi2p_kernel");
+}
+
+void launch_zadjoint(CMatRef X, bool from_p, MatRef out, int64_t rows, int64_t cols,
+                     int64_t batch, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(cols, 32)),
+            static_cast<unsigned>(batch));
+  if (from_p)
+    zadj_p2i_kernel<<<grid, dim3(32, 8), 0, st>>>(X.base, X.ld, X.stride, out.base, out.ld,
+                                                  out.stride, rows, cols);
+  else
+    zadj_i2i_kernel<<<grid, dim3(32, 8), 0, st>>>(X.base, X.ld, X.stride, out.base, out.ld,
+                                                  out.stride, rows, cols);
+  RSVD_LAUNCH("zadj_kernel");
+}
+
+void launch_zidentity_p(MatRef X, int64_t rows, int64_t lp, int64_t ell, int64_t batch,
+                        cudaStream_t st) {
+  if (rows <= 0 || batch <= 0) return;
+  zidentity_p_kernel<<<grid_for(rows * 2 * lp * batch, 256), 256, 0, st>>>(X.base, X.ld, X.stride,
+                                                                            rows, lp, ell, batch);
+  RSVD_LAUNCH("zidentity_p_kernel");
+}
+
+void launch_zchol(const double* Gt, double* Tt, double* Rt, double* W, double* Rc, double* Tc,
+                  int* rank, int* rank2, int* colmap, int* ill, const int* mask, int64_t ell,
+                  int64_t lp, double tau, double shift_coef, int mode, int64_t batch,
+                  cudaStream_t st) {
+  if (batch <= 0) return;
+  if (ell > 1024) throw std::invalid_argument("complex Cholesky: l > 1024 is not supported");
+  ZCholArgs a;
+  a.Gt = Gt, a.Tt = Tt, a.Rt = Rt;
+  a.W = reinterpret_cast<double2*>(W);
+  a.Rc = reinterpret_cast<double2*>(Rc);
+  a.Tc = reinterpret_cast<double2*>(Tc);
+  a.rank = rank, a.rank2 = rank2, a.colmap = colmap, a.ill = ill, a.mask = mask;
+  a.ell = ell, a.lp = lp, a.tau = tau, a.shift_coef = shift_coef, a.mode = mode;
+  zchol_kernel<<<static_cast<unsigned>(batch), 512, 0, st>>>(a);
+  RSVD_LAUNCH("zchol_kernel");
+}
+
+void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
+                    double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
+                    int64_t batch, cudaStream_t st) {
+  if (batch <= 0) return;
+  zjacobi_kernel<<<static_cast<unsigned>(batch), 1024, 0, st>>>(
+      src, src_ld, src_stride, src_mode, reinterpret_cast<double2*>(H),
+      reinterpret_cast<double2*>(J), ell, lp, max_sweeps, sweeps);
+  RSVD_LAUNCH("zjacobi_kernel");
+}
+
+void launch_zfinalize(const double* W, int64_t lp, int64_t ell, int64_t k, int64_t m, int64_t n,
+                      double* sigma_out, int* perm, int* rank, double* dw, int64_t batch,
+                      cudaStream_t st) {
+  if (batch <= 0) return;
+  const size_t smem = lp * (sizeof(double) + sizeof(int));
+  zfinalize_kernel<<<static_cast<unsigned>(batch), 512, smem, st>>>(
+      reinterpret_cast<const double2*>(W), lp, static_cast<int>(ell), k, m, n, sigma_out, perm,
+      rank, dw);
+  RSVD_LAUNCH("zfinalize_kernel");
+}
+
+void launch_zlift_operand(const double* W, int64_t lp, const int* perm, const double* sigma,
+                          int64_t k, const int* rank, int64_t ell, bool half, MatRef M,
+                          int64_t batch, cudaStream_t st) {
+  if (batch <= 0 || k <= 0) return;
+  const int64_t total = 2 * lp * (half ? k : 2 * k);
+  dim3 grid(grid_for(total, 256, 2), static_cast<unsigned>(batch));
+  zlift_operand_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(W), lp, perm, sigma, k,
+                                             rank, static_cast<int>(ell), half ? 1 : 0, M.base,
+                                             M.ld, M.stride);
+  RSVD_LAUNCH("zlift_operand_kernel");
+}
+
+}  // namespace rsvd

@@ -63,11 +63,29 @@ def _is_torch_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and hasattr(a, "data_ptr") and bool(a.is_cuda)
 
 
+def _is_complex(a) -> bool:
+    """Complex instantiation (factorize.cpp:106-118): complex128 numpy arrays or
+    torch tensors go to the *_z128 entry points."""
+    if hasattr(a, "is_complex") and hasattr(a, "data_ptr"):
+        return bool(a.is_complex())
+    return bool(np.iscomplexobj(a))
+
+
+def _np_dtype(cplx: bool):
+    return np.complex128 if cplx else np.float64
+
+
+def _torch_dtype(cplx: bool):
+    import torch
+
+    return torch.complex128 if cplx else torch.float64
+
+
 def _colmajor_torch(a):
     import torch
 
-    if a.dtype != torch.float64:
-        raise InvalidArgument("rsvd: expected a float64 tensor")
+    if a.dtype not in (torch.float64, torch.complex128):
+        raise InvalidArgument("rsvd: expected a float64 or complex128 tensor")
     if a.dim() != 2:
         raise InvalidArgument("rsvd: expected a 2-D tensor")
     m, n = a.shape
@@ -92,11 +110,14 @@ def _resolve_ell(m: int, n: int, p: RsvdParams) -> int:
 
 
 def rsvd(a, params: RsvdParams, handle: Optional[_lib.Handle] = None) -> TruncatedFactorization:
-    """rlftn::rsvd (factorize.cpp:76-95) on the GPU."""
+    """rlftn::rsvd (factorize.cpp:76-95) on the GPU; complex128 input runs the
+    complex instantiation (rsvd<std::complex<double>>)."""
     lib = _lib.load()
     h = handle or _lib.default_handle()
     out_rank = ctypes.c_int64(0)
     dw = ctypes.c_double(0.0)
+    cplx = _is_complex(a)
+    fn = lib.rsvd_z128 if cplx else lib.rsvd_f64
     if _is_torch_cuda(a):
         import torch
 
@@ -104,12 +125,12 @@ def rsvd(a, params: RsvdParams, handle: Optional[_lib.Handle] = None) -> Truncat
         m, n = a.shape
         k = max(int(params.rank), 0)
         kk = max(k, 1)
-        U = torch.empty((kk, m), dtype=torch.float64, device=a.device).t()  # m x k col-major
+        U = torch.empty((kk, m), dtype=a.dtype, device=a.device).t()  # m x k col-major
         S = torch.empty(kk, dtype=torch.float64, device=a.device)
-        Vt = torch.empty((n, kk), dtype=torch.float64, device=a.device).t()  # k x n col-major
+        Vt = torch.empty((n, kk), dtype=a.dtype, device=a.device).t()  # k x n col-major
         _torch_stream_guard(h)
         try:
-            rc = lib.rsvd_f64(h.raw, a.data_ptr() if a.numel() else 0, m, n, lda, params.rank,
+            rc = fn(h.raw, a.data_ptr() if a.numel() else 0, m, n, lda, params.rank,
                               params.oversample, params.power, params.seed & _MASK, U.data_ptr(),
                               max(m, 1), S.data_ptr(), Vt.data_ptr(), kk, ctypes.byref(out_rank),
                               ctypes.byref(dw), _lib.PTR_DEVICE)
@@ -118,15 +139,16 @@ def rsvd(a, params: RsvdParams, handle: Optional[_lib.Handle] = None) -> Truncat
         _lib.raise_for(rc, h.raw)
         r = out_rank.value
         return TruncatedFactorization(U[:, :r], S[:r], Vt[:r, :], dw.value, False)
-    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    dt = _np_dtype(cplx)
+    a = np.asfortranarray(np.asarray(a, dtype=dt))
     if a.ndim != 2:
         raise InvalidArgument("rsvd: expected a 2-D array")
     m, n = a.shape
     kk = max(int(params.rank), 1)
-    U = np.zeros((m, kk), order="F")
+    U = np.zeros((m, kk), dtype=dt, order="F")
     S = np.zeros(kk)
-    Vt = np.zeros((kk, n), order="F")
-    rc = lib.rsvd_f64(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1), params.rank,
+    Vt = np.zeros((kk, n), dtype=dt, order="F")
+    rc = fn(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1), params.rank,
                       params.oversample, params.power, params.seed & _MASK, U.ctypes.data,
                       max(m, 1), S.ctypes.data, Vt.ctypes.data, kk, ctypes.byref(out_rank),
                       ctypes.byref(dw), _lib.PTR_HOST)
@@ -147,31 +169,34 @@ def tsvd(a, chi: int, handle: Optional[_lib.Handle] = None) -> TruncatedFactoriz
     h = handle or _lib.default_handle()
     r = ctypes.c_int64(0)
     dw = ctypes.c_double(0.0)
+    cplx = _is_complex(a)
+    fn = lib.rsvd_tsvd_z128 if cplx else lib.rsvd_tsvd_f64
     if _is_torch_cuda(a):
         import torch
 
         a, lda = _colmajor_torch(a)
         m, n = a.shape
         k = max(min(int(chi), m, n), 1)
-        U = torch.empty((k, m), dtype=torch.float64, device=a.device).t()
+        U = torch.empty((k, m), dtype=a.dtype, device=a.device).t()
         S = torch.empty(k, dtype=torch.float64, device=a.device)
-        Vt = torch.empty((n, k), dtype=torch.float64, device=a.device).t()
+        Vt = torch.empty((n, k), dtype=a.dtype, device=a.device).t()
         with _lib.on_torch_stream(h):
-            rc = lib.rsvd_tsvd_f64(h.raw, a.data_ptr() if a.numel() else 0, m, n, lda, int(chi),
+            rc = fn(h.raw, a.data_ptr() if a.numel() else 0, m, n, lda, int(chi),
                                    U.data_ptr(), max(m, 1), S.data_ptr(), Vt.data_ptr(), k,
                                    ctypes.byref(r), ctypes.byref(dw), _lib.PTR_DEVICE)
         _lib.raise_for(rc, h.raw)
         rr = r.value
         return TruncatedFactorization(U[:, :rr], S[:rr], Vt[:rr, :], dw.value, True)
-    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    dt = _np_dtype(cplx)
+    a = np.asfortranarray(np.asarray(a, dtype=dt))
     if a.ndim != 2:
         raise InvalidArgument("tsvd: expected a 2-D array")
     m, n = a.shape
     k = max(min(int(chi), m, n), 1)
-    U = np.zeros((m, k), order="F")
+    U = np.zeros((m, k), dtype=dt, order="F")
     S = np.zeros(k)
-    Vt = np.zeros((k, n), order="F")
-    rc = lib.rsvd_tsvd_f64(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1), int(chi),
+    Vt = np.zeros((k, n), dtype=dt, order="F")
+    rc = fn(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1), int(chi),
                            U.ctypes.data, max(m, 1), S.ctypes.data, Vt.ctypes.data, k,
                            ctypes.byref(r), ctypes.byref(dw), _lib.PTR_HOST)
     _lib.raise_for(rc, h.raw)
@@ -204,18 +229,17 @@ def _batched_buffers(a, k: int, who: str):
     (bsz, m, n, flags, ptrs, U, S, Vt, Ub, Vb, keepalive)."""
     import torch
 
-    if a.dim() != 3 or a.dtype != torch.float64:
-        raise InvalidArgument(f"{who}: expected a (batch, m, n) float64 tensor")
+    if a.dim() != 3 or a.dtype not in (torch.float64, torch.complex128):
+        raise InvalidArgument(f"{who}: expected a (batch, m, n) float64 or complex128 tensor")
     bsz, m, n = a.shape
     if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
         a = a.transpose(1, 2).contiguous().transpose(1, 2)
     dev = a.device if a.is_cuda else None
     pin = (not a.is_cuda) and bool(a.is_pinned())
-    kw = dict(dtype=torch.float64, device=dev) if dev is not None else dict(
-        dtype=torch.float64, pin_memory=pin)
-    U = torch.empty((bsz, k, m), **kw).transpose(1, 2)
-    S = torch.empty((bsz, k), **kw)
-    Vt = torch.empty((bsz, n, k), **kw).transpose(1, 2)
+    kw = dict(device=dev) if dev is not None else dict(pin_memory=pin)
+    U = torch.empty((bsz, k, m), dtype=a.dtype, **kw).transpose(1, 2)
+    S = torch.empty((bsz, k), dtype=torch.float64, **kw)
+    Vt = torch.empty((bsz, n, k), dtype=a.dtype, **kw).transpose(1, 2)
     flags = _lib.PTR_DEVICE if a.is_cuda else _lib.PTR_HOST
     return bsz, m, n, flags, (a.data_ptr(), U.data_ptr(), S.data_ptr(), Vt.data_ptr()), U, S, Vt, a
 
@@ -225,32 +249,34 @@ def tsvd_batched(a, chi: int, handle: Optional[_lib.Handle] = None) -> BatchedFa
     block_factorize for equal-shape sectors, blocks.cpp:82)."""
     lib = _lib.load()
     h = handle or _lib.default_handle()
+    cplx = _is_complex(a)
+    fn = lib.rsvd_tsvd_z128_batched if cplx else lib.rsvd_tsvd_f64_batched
     if hasattr(a, "data_ptr") and hasattr(a, "is_pinned"):
         m_, n_ = int(a.shape[1]), int(a.shape[2])
         k = max(min(int(chi), m_, n_), 1)
         bsz, m, n, flags, ptrs, U, S, Vt, a = _batched_buffers(a, k, "tsvd_batched")
         Ub = None
     else:
-        a = np.asarray(a, dtype=np.float64)
+        dt = _np_dtype(cplx)
+        a = np.asarray(a, dtype=dt)
         if a.ndim != 3:
             raise InvalidArgument("tsvd_batched: expected a (batch, m, n) array")
         bsz, m, n = a.shape
         k = max(min(int(chi), m, n), 1)
         a = np.ascontiguousarray(np.transpose(a, (0, 2, 1)))
-        Ub = np.zeros((bsz, k, m))
+        Ub = np.zeros((bsz, k, m), dtype=dt)
         S = np.zeros((bsz, k))
-        Vb = np.zeros((bsz, n, k))
+        Vb = np.zeros((bsz, n, k), dtype=dt)
         flags = _lib.PTR_HOST
         ptrs = (a.ctypes.data, Ub.ctypes.data, S.ctypes.data, Vb.ctypes.data)
     ranks = (ctypes.c_int64 * max(bsz, 1))()
     dws = (ctypes.c_double * max(bsz, 1))()
     if flags == _lib.PTR_DEVICE:
         with _lib.on_torch_stream(h):
-            rc = lib.rsvd_tsvd_f64_batched(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1],
-                                           m, m * k, ptrs[2], k, ptrs[3], k, k * n, ranks, dws,
-                                           flags)
+            rc = fn(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1],
+                    m, m * k, ptrs[2], k, ptrs[3], k, k * n, ranks, dws, flags)
     else:
-        rc = lib.rsvd_tsvd_f64_batched(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1], m,
+        rc = fn(h.raw, bsz, ptrs[0], m, n, m, m * n, int(chi), ptrs[1], m,
                                        m * k, ptrs[2], k, ptrs[3], k, k * n, ranks, dws, flags)
     _lib.raise_for(rc, h.raw)
     if Ub is not None:
@@ -272,18 +298,20 @@ def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
     h = handle or _lib.default_handle()
     if out is not None and hasattr(a, "data_ptr"):
         return _rsvd_batched_into(lib, h, a, params, seeds, out)
+    cplx = _is_complex(a)
+    fn = lib.rsvd_z128_batched if cplx else lib.rsvd_f64_batched
     if _is_torch_cuda(a):
         import torch
 
-        if a.dim() != 3 or a.dtype != torch.float64:
+        if a.dim() != 3 or a.dtype not in (torch.float64, torch.complex128):
             raise InvalidArgument("rsvd_batched: expected a (batch, m, n) float64 tensor")
         bsz, m, n = a.shape
         if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
             a = a.transpose(1, 2).contiguous().transpose(1, 2)
         k = max(int(params.rank), 1)
-        U = torch.empty((bsz, k, m), dtype=torch.float64, device=a.device).transpose(1, 2)
+        U = torch.empty((bsz, k, m), dtype=a.dtype, device=a.device).transpose(1, 2)
         S = torch.empty((bsz, k), dtype=torch.float64, device=a.device)
-        Vt = torch.empty((bsz, n, k), dtype=torch.float64, device=a.device).transpose(1, 2)
+        Vt = torch.empty((bsz, n, k), dtype=a.dtype, device=a.device).transpose(1, 2)
         flags = _lib.PTR_DEVICE
         ptrs = (a.data_ptr(), U.data_ptr(), S.data_ptr(), Vt.data_ptr())
         _torch_stream_guard(h)
@@ -292,29 +320,30 @@ def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
         # engine copies in and out inside the call (the end-to-end path).
         import torch
 
-        if a.dim() != 3 or a.dtype != torch.float64:
+        if a.dim() != 3 or a.dtype not in (torch.float64, torch.complex128):
             raise InvalidArgument("rsvd_batched: expected a (batch, m, n) float64 tensor")
         bsz, m, n = a.shape
         if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
             a = a.transpose(1, 2).contiguous().transpose(1, 2)
         k = max(int(params.rank), 1)
         pin = bool(a.is_pinned())
-        U = torch.empty((bsz, k, m), dtype=torch.float64, pin_memory=pin).transpose(1, 2)
+        U = torch.empty((bsz, k, m), dtype=a.dtype, pin_memory=pin).transpose(1, 2)
         S = torch.empty((bsz, k), dtype=torch.float64, pin_memory=pin)
-        Vt = torch.empty((bsz, n, k), dtype=torch.float64, pin_memory=pin).transpose(1, 2)
+        Vt = torch.empty((bsz, n, k), dtype=a.dtype, pin_memory=pin).transpose(1, 2)
         flags = _lib.PTR_HOST
         ptrs = (a.data_ptr(), U.data_ptr(), S.data_ptr(), Vt.data_ptr())
         Ub = Vb = None
     else:
-        a = np.asarray(a, dtype=np.float64)
+        dt = _np_dtype(cplx)
+        a = np.asarray(a, dtype=dt)
         if a.ndim != 3:
             raise InvalidArgument("rsvd_batched: expected a (batch, m, n) array")
         bsz, m, n = a.shape
         a = np.ascontiguousarray(np.transpose(a, (0, 2, 1)))  # items column-major
         k = max(int(params.rank), 1)
-        Ub = np.zeros((bsz, k, m))
+        Ub = np.zeros((bsz, k, m), dtype=dt)
         S = np.zeros((bsz, k))
-        Vb = np.zeros((bsz, n, k))
+        Vb = np.zeros((bsz, n, k), dtype=dt)
         flags = _lib.PTR_HOST
         ptrs = (a.ctypes.data, Ub.ctypes.data, S.ctypes.data, Vb.ctypes.data)
     if len(seeds) != bsz:
@@ -323,9 +352,9 @@ def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
     ranks = (ctypes.c_int64 * max(bsz, 1))()
     dws = (ctypes.c_double * max(bsz, 1))()
     try:
-        rc = lib.rsvd_f64_batched(h.raw, bsz, ptrs[0], m, n, m, m * n, params.rank,
-                                  params.oversample, params.power, seeds_arr, ptrs[1], m, m * k,
-                                  ptrs[2], k, ptrs[3], k, k * n, ranks, dws, flags)
+        rc = fn(h.raw, bsz, ptrs[0], m, n, m, m * n, params.rank,
+                params.oversample, params.power, seeds_arr, ptrs[1], m, m * k,
+                ptrs[2], k, ptrs[3], k, k * n, ranks, dws, flags)
     finally:
         if flags == _lib.PTR_DEVICE:
             lib.rsvd_set_stream(h.raw, None)
@@ -340,17 +369,19 @@ def rsvd_batched(a, params: RsvdParams, seeds: Sequence[int],
 def _rsvd_batched_into(lib, h, a, params, seeds, out):
     import torch
 
-    if a.dim() != 3 or a.dtype != torch.float64:
+    if a.dim() != 3 or a.dtype not in (torch.float64, torch.complex128):
         raise InvalidArgument("rsvd_batched: expected a (batch, m, n) float64 tensor")
     bsz, m, n = a.shape
     if not (a.stride(1) == 1 and a.stride(2) == m and a.stride(0) == m * n):
         a = a.transpose(1, 2).contiguous().transpose(1, 2)
     k = max(int(params.rank), 1)
     U, S, Vt = out.left, out.sigma, out.right_adj
+    fn = lib.rsvd_z128_batched if a.is_complex() else lib.rsvd_f64_batched
     ok = (tuple(U.shape) == (bsz, m, k) and U.stride() == (m * k, 1, m) and
           tuple(S.shape) == (bsz, k) and S.is_contiguous() and
           tuple(Vt.shape) == (bsz, k, n) and Vt.stride() == (k * n, 1, k) and
-          all(x.device == a.device and x.dtype == torch.float64 for x in (U, S, Vt)))
+          all(x.device == a.device for x in (U, S, Vt)) and U.dtype == a.dtype and
+          Vt.dtype == a.dtype and S.dtype == torch.float64)
     if not ok:
         raise InvalidArgument("rsvd_batched: out= buffers do not match the input shapes")
     if len(seeds) != bsz:
@@ -362,7 +393,7 @@ def _rsvd_batched_into(lib, h, a, params, seeds, out):
     if flags == _lib.PTR_DEVICE:
         _torch_stream_guard(h)
     try:
-        rc = lib.rsvd_f64_batched(h.raw, bsz, a.data_ptr(), m, n, m, m * n, params.rank,
+        rc = fn(h.raw, bsz, a.data_ptr(), m, n, m, m * n, params.rank,
                                   params.oversample, params.power, seeds_arr, U.data_ptr(), m,
                                   m * k, S.data_ptr(), k, Vt.data_ptr(), k, k * n, ranks, dws, flags)
     finally:
@@ -378,25 +409,28 @@ def randomized_range(a, ell: int, power: int, seed: int,
     """rlftn::randomized_range (factorize.cpp:52-74): Q (m x ell)."""
     lib = _lib.load()
     h = handle or _lib.default_handle()
+    cplx = _is_complex(a)
+    fn = lib.rsvd_randomized_range_z128 if cplx else lib.rsvd_randomized_range_f64
     if _is_torch_cuda(a):
         import torch
 
         a, lda = _colmajor_torch(a)
         m, n = a.shape
-        Q = torch.empty((max(ell, 1), m), dtype=torch.float64, device=a.device).t()
+        Q = torch.empty((max(ell, 1), m), dtype=a.dtype, device=a.device).t()
         _torch_stream_guard(h)
         try:
-            rc = lib.rsvd_randomized_range_f64(h.raw, a.data_ptr() if a.numel() else 0, m, n,
+            rc = fn(h.raw, a.data_ptr() if a.numel() else 0, m, n,
                                                lda, ell, power, seed & _MASK, Q.data_ptr(),
                                                max(m, 1), _lib.PTR_DEVICE)
         finally:
             lib.rsvd_set_stream(h.raw, None)
         _lib.raise_for(rc, h.raw)
         return Q[:, :ell]
-    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    dt = _np_dtype(cplx)
+    a = np.asfortranarray(np.asarray(a, dtype=dt))
     m, n = a.shape
-    Q = np.zeros((m, max(ell, 1)), order="F")
-    rc = lib.rsvd_randomized_range_f64(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1),
+    Q = np.zeros((m, max(ell, 1)), dtype=dt, order="F")
+    rc = fn(h.raw, a.ctypes.data if a.size else 0, m, n, max(m, 1),
                                        ell, power, seed & _MASK, Q.ctypes.data, max(m, 1),
                                        _lib.PTR_HOST)
     _lib.raise_for(rc, h.raw)
@@ -416,30 +450,33 @@ def reconstruction_error(a, f: TruncatedFactorization, norm: ErrorNorm = ErrorNo
     h = handle or _lib.default_handle()
     out = ctypes.c_double(0.0)
     r = f.rank()
+    cplx = _is_complex(a)
+    fn = lib.rsvd_reconstruction_error_z128 if cplx else lib.rsvd_reconstruction_error_f64
     if _is_torch_cuda(a):
         import torch
 
         a, lda = _colmajor_torch(a)
         m, n = a.shape
-        U = f.left.t().contiguous().t() if r else torch.zeros((m, 1), dtype=torch.float64,
-                                                              device=a.device)
-        Vt = f.right_adj.t().contiguous().t() if r else torch.zeros((1, n), dtype=torch.float64,
-                                                                    device=a.device)
+        U = f.left.to(a.dtype).t().contiguous().t() if r else torch.zeros(
+            (m, 1), dtype=a.dtype, device=a.device)
+        Vt = f.right_adj.to(a.dtype).t().contiguous().t() if r else torch.zeros(
+            (1, n), dtype=a.dtype, device=a.device)
         S = f.sigma.contiguous() if r else torch.zeros(1, dtype=torch.float64, device=a.device)
         _torch_stream_guard(h)
         try:
-            rc = lib.rsvd_reconstruction_error_f64(h.raw, a.data_ptr(), m, n, lda, U.data_ptr(),
+            rc = fn(h.raw, a.data_ptr(), m, n, lda, U.data_ptr(),
                                                    m, S.data_ptr(), Vt.data_ptr(), max(r, 1), r,
                                                    ctypes.byref(out), _lib.PTR_DEVICE)
         finally:
             lib.rsvd_set_stream(h.raw, None)
     else:
-        a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        dt = _np_dtype(cplx)
+        a = np.asfortranarray(np.asarray(a, dtype=dt))
         m, n = a.shape
-        U = np.asfortranarray(f.left if r else np.zeros((m, 1)))
-        Vt = np.asfortranarray(f.right_adj if r else np.zeros((1, n)))
+        U = np.asfortranarray(np.asarray(f.left, dtype=dt) if r else np.zeros((m, 1), dtype=dt))
+        Vt = np.asfortranarray(np.asarray(f.right_adj, dtype=dt) if r else np.zeros((1, n), dtype=dt))
         S = np.ascontiguousarray(f.sigma if r else np.zeros(1))
-        rc = lib.rsvd_reconstruction_error_f64(h.raw, a.ctypes.data, m, n, m, U.ctypes.data, m,
+        rc = fn(h.raw, a.ctypes.data, m, n, m, U.ctypes.data, m,
                                                S.ctypes.data, Vt.ctypes.data, max(r, 1), r,
                                                ctypes.byref(out), _lib.PTR_HOST)
     _lib.raise_for(rc, h.raw)
@@ -450,16 +487,17 @@ def _spectral_error(a, f: TruncatedFactorization, handle) -> float:
     import torch
 
     dev = a.device if _is_torch_cuda(a) else torch.device("cuda", (handle.device if handle else 0))
-    A = a if _is_torch_cuda(a) else torch.from_numpy(np.asarray(a, dtype=np.float64)).to(dev)
+    A = a if _is_torch_cuda(a) else torch.from_numpy(
+        np.asarray(a, dtype=_np_dtype(_is_complex(a)))).to(dev)
     m, n = A.shape
     R = A.clone()
     if f.rank():
         U = torch.as_tensor(np.asarray(f.left) if not hasattr(f.left, "to") else f.left,
-                            dtype=torch.float64).to(dev)
+                            dtype=A.dtype).to(dev)
         S = torch.as_tensor(np.asarray(f.sigma) if not hasattr(f.sigma, "to") else f.sigma,
                             dtype=torch.float64).to(dev)
         Vt = torch.as_tensor(np.asarray(f.right_adj) if not hasattr(f.right_adj, "to")
-                             else f.right_adj, dtype=torch.float64).to(dev)
+                             else f.right_adj, dtype=A.dtype).to(dev)
         R = R - (U * S[None, :]) @ Vt
     if float(torch.linalg.norm(R)) == 0.0:
         return 0.0

@@ -53,7 +53,10 @@ class CounterRng:
 
     def fill_gaussian(self, out, count: int | None = None, handle: _lib.Handle | None = None):
         """Fill ``out`` (a float64 torch CUDA tensor or numpy array) with the
-        first ``count`` normals of this stream, computed on the GPU."""
+        first ``count`` normals of this stream, computed on the GPU.  A
+        complex128 ``out`` takes the complex fill (rng.hpp:66-71): entry t =
+        (normal 2t+1, normal 2t) / sqrt 2 as the reference's g++ build orders
+        the two unsequenced calls."""
         h = handle or _lib.default_handle()
         lib = _lib.load()
         try:
@@ -63,17 +66,21 @@ class CounterRng:
             is_torch = False
         if is_torch:
             n = out.numel() if count is None else count
-            if out.dtype.itemsize != 8 or not out.is_contiguous():
+            cplx = bool(out.is_complex())
+            if out.dtype.itemsize != (16 if cplx else 8) or not out.is_contiguous():
                 raise _lib.InvalidArgument("fill_gaussian: need a contiguous float64 tensor")
-            import torch
+            fn = lib.rsvd_fill_gaussian_z128 if cplx else lib.rsvd_fill_gaussian_f64
             lib.rsvd_set_stream(h.raw, ctypes.c_void_p(_lib.torch_stream_ptr()))
-            rc = lib.rsvd_fill_gaussian_f64(h.raw, self.key, out.data_ptr(), n, _lib.PTR_DEVICE)
+            rc = fn(h.raw, self.key, out.data_ptr(), n, _lib.PTR_DEVICE)
             lib.rsvd_set_stream(h.raw, None)
         else:
             import numpy as np
-            if out.dtype != np.float64 or not out.flags.c_contiguous and not out.flags.f_contiguous:
+            cplx = out.dtype == np.complex128
+            if (out.dtype != np.float64 and not cplx) or (
+                    not out.flags.c_contiguous and not out.flags.f_contiguous):
                 raise _lib.InvalidArgument("fill_gaussian: need a contiguous float64 array")
             n = out.size if count is None else count
-            rc = lib.rsvd_fill_gaussian_f64(h.raw, self.key, out.ctypes.data, n, _lib.PTR_HOST)
+            fn = lib.rsvd_fill_gaussian_z128 if cplx else lib.rsvd_fill_gaussian_f64
+            rc = fn(h.raw, self.key, out.ctypes.data, n, _lib.PTR_HOST)
         _lib.raise_for(rc, h.raw)
         return out

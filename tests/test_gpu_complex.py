@@ -1,0 +1,230 @@
+"""GPU parity of the complex instantiation (rsvd / tsvd / randomized_range /
+reconstruction_error for std::complex<double>, factorize.cpp:106-118) against
+the complex oracle (zgemm, zgeqrf+zungqr, zgesdd restated).
+
+Same tolerances as the real path (north_star): singular values 1e-10
+relative, reconstruction error 1e-10 relative, subspace distance <= 1e-8 on a
+gapped prefix, factor isometry 1e-12 (test_factorize.cpp:73-83)."""
+import numpy as np
+import pytest
+
+from tests.helpers import (isometry_err, rel_sigma_err, spectrum_family, subspace_distance,
+                           ulp_distance, zmatrix_with_spectrum)
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-10
+REC_TOL = 1e-10
+SUB_TOL = 1e-8
+ISO_TOL = 1e-12
+
+
+def _gapped_prefix(S, k, rel_gap=1e-3):
+    for j in range(min(k, len(S) - 1), 0, -1):
+        if (S[j - 1] - S[j]) > rel_gap * S[0]:
+            return j
+    return 0
+
+
+def check_against(a, f, ref, label="", dw_rel=1e-9):
+    from paper_1710_01463_b200 import reconstruction_error
+
+    U, S, Vt, dw = ref
+    assert f.rank() == len(S), (label, f.rank(), len(S))
+    assert rel_sigma_err(f.sigma, S) < SIG_TOL, (label, rel_sigma_err(f.sigma, S))
+    left = np.asarray(f.left)
+    right = np.asarray(f.right_adj)
+    assert left.dtype == np.complex128 and right.dtype == np.complex128
+    assert isometry_err(left) < ISO_TOL, (label, isometry_err(left))
+    assert isometry_err(right.conj().T) < ISO_TOL, label
+    e_gpu = reconstruction_error(a, f)
+    e_ref = float(np.linalg.norm(a - (U * S[None, :]) @ Vt))
+    if e_ref > 1e-12 * np.linalg.norm(a):
+        assert abs(e_gpu - e_ref) / e_ref < REC_TOL, (label, e_gpu, e_ref)
+    else:
+        assert e_gpu <= 1e-10 * np.linalg.norm(a), label
+    j = _gapped_prefix(S, f.rank())
+    if j:
+        assert subspace_distance(left[:, :j], U[:, :j]) < SUB_TOL, label
+        assert subspace_distance(right[:j].conj().T, Vt[:j].conj().T) < SUB_TOL, label
+    assert f.discarded_weight == pytest.approx(dw, rel=dw_rel, abs=1e-28), label
+
+
+CASES = [
+    # (rows, cols, spectrum, rank, ell, q, seed)
+    (50, 30, ("fam", 0, 30), 10, 20, 4, 123),
+    (36, 24, ("fam", 2, 24), 8, 16, 4, 99),
+    (30, 70, ("fam", 2, 30), 8, 16, 2, 7),
+    (37, 53, ("fam", 1, 37), 5, 13, 1, 2024),
+    (64, 64, ("fam", 2, 64), 12, 20, 0, 5),
+    (200, 160, ("exp", 32.0, 160), 32, 42, 2, 31337),
+    (300, 256, ("exp", 64.0, 256), 64, 138, 2, 77),
+]
+
+
+def _spectrum(spec):
+    if spec[0] == "fam":
+        return spectrum_family(spec[1], spec[2])
+    return np.exp(-np.arange(spec[2]) / spec[1])
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}k{c[3]}l{c[4]}q{c[5]}" for c in CASES])
+def test_complex_rsvd_matches_oracle(cuda, oracle_mod, case):
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    rows, cols, spec, k, ell, q, seed = case
+    a = zmatrix_with_spectrum(oracle_mod, seed + 1, rows, cols, _spectrum(spec))
+    f = rsvd(a, RsvdParams(k, ell, q, seed))
+    ref = oracle_mod.zrsvd(a, k, ell, q, seed)
+    check_against(a, f, ref, str(case))
+
+
+def test_complex_omega_matches_reference_stream(cuda, oracle_mod):
+    import torch
+    from paper_1710_01463_b200.rng import CounterRng
+
+    for seed in (0, 42, 0xDEADBEEFCAFEF00D):
+        want = oracle_mod.zfill_gaussian(seed, 4099)
+        got = torch.empty(4099, dtype=torch.complex128, device=cuda)
+        CounterRng(seed).fill_gaussian(got)
+        g = got.cpu().numpy()
+        d = ulp_distance(np.concatenate([g.real, g.imag]), np.concatenate([want.real, want.imag]))
+        assert d.max() <= 4
+        assert (d == 0).mean() > 0.5
+        host = np.empty(33, dtype=np.complex128)
+        CounterRng(seed).fill_gaussian(host)
+        assert np.array_equal(host, g[:33])
+
+
+@pytest.mark.parametrize("r", [3, 7])
+def test_complex_exact_rank_reconstructs(cuda, oracle_mod, r):
+    # test_factorize.cpp:105-120 (complex half): rank-deficient sample Y.
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
+
+    sigma = [5.0 / (1.0 + j) for j in range(r)]
+    a = zmatrix_with_spectrum(oracle_mod, 17 + r, 60, 40, sigma)
+    f = rsvd(a, RsvdParams(10, 20, 4, 5))
+    assert reconstruction_error(a, f) <= 1e-10 * np.linalg.norm(a)
+    assert f.rank() <= 10
+    assert isometry_err(np.asarray(f.left)) < ISO_TOL
+    ref = oracle_mod.zrsvd(a, 10, 20, 4, 5)
+    assert f.rank() == len(ref[1])
+    assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
+
+
+def test_complex_tsvd_and_rsvd_agree(cuda, oracle_mod):
+    # test_factorize.cpp:122-131
+    from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
+
+    sigma = spectrum_family(2, 24)
+    a = zmatrix_with_spectrum(oracle_mod, 29, 36, 24, sigma)
+    ft = tsvd(a, 8)
+    fr = rsvd(a, RsvdParams(8, 16, 4, 99))
+    assert np.all(np.abs(ft.sigma - sigma[:8]) <= 1e-11 * sigma[:8])
+    assert np.all(np.abs(fr.sigma - ft.sigma) / ft.sigma < 1e-9)
+    assert ft.discarded_exact and not fr.discarded_exact
+    assert 0 < fr.discarded_weight <= ft.discarded_weight * (1 + 1e-8)
+
+
+@pytest.mark.parametrize("shape", [(40, 25), (25, 40), (64, 64), (130, 97)])
+def test_complex_tsvd_matches_oracle(cuda, oracle_mod, shape):
+    from paper_1710_01463_b200 import tsvd
+
+    m, n = shape
+    p = min(m, n)
+    sigma = np.exp(-np.arange(p) / 6.0)
+    a = zmatrix_with_spectrum(oracle_mod, 3 * m + n, m, n, sigma)
+    for chi in (1, 7, p):
+        f = tsvd(a, chi)
+        ref = oracle_mod.ztsvd(a, chi)
+        check_against(a, f, ref, f"{shape} chi={chi}", dw_rel=1e-8)
+        assert f.discarded_exact
+
+
+def test_complex_steep_spectrum_sampled_tail(cuda, oracle_mod):
+    # 2^-k spectrum: Y is numerically rank deficient after the power steps
+    # (the shifted CholeskyQR fallback keeps the tiny directions' components).
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = zmatrix_with_spectrum(oracle_mod, 91, 80, 60, spectrum_family(0, 60))
+    f = rsvd(a, RsvdParams(10, 30, 4, 11))
+    ref = oracle_mod.zrsvd(a, 10, 30, 4, 11)
+    assert f.rank() == len(ref[1])
+    assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
+    assert f.discarded_weight == pytest.approx(ref[3], rel=1e-8)
+
+
+def test_complex_batched_matches_single_calls(cuda, oracle_mod):
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, rsvd, rsvd_batched
+
+    mats = [zmatrix_with_spectrum(oracle_mod, 500 + i, 96, 80, np.exp(-np.arange(80) / (8.0 + i)))
+            for i in range(5)]
+    seeds = [1000 + 7 * i for i in range(5)]
+    p = RsvdParams(12, 24, 2, 0)
+    stack = np.stack(mats)
+    fb = rsvd_batched(stack, p, seeds)
+    ad = torch.from_numpy(stack).to(cuda).transpose(1, 2).contiguous().transpose(1, 2)
+    fd = rsvd_batched(ad, p, seeds)
+    for i, a in enumerate(mats):
+        fi = rsvd(a, RsvdParams(12, 24, 2, seeds[i]))
+        bi = fb.item(i)
+        assert rel_sigma_err(np.asarray(bi.sigma), np.asarray(fi.sigma)) < 1e-12
+        di = fd.item(i)
+        # host- and device-pointer batches run the same kernels: bitwise equal
+        assert np.array_equal(di.sigma.cpu().numpy(), np.asarray(bi.sigma))
+        assert np.array_equal(di.right_adj.cpu().numpy(), np.asarray(bi.right_adj))
+        check_against(a, bi, oracle_mod.zrsvd(a, 12, 24, 2, seeds[i]), f"batch item {i}")
+        ref = oracle_mod.zrsvd(a, 12, 24, 2, seeds[i])
+        check_against(a, fi, ref, f"item {i}")
+
+
+def test_complex_device_tensor_and_determinism(cuda, oracle_mod):
+    import torch
+    from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
+
+    a = zmatrix_with_spectrum(oracle_mod, 8, 120, 100, np.exp(-np.arange(100) / 10.0))
+    ad = torch.from_numpy(a).to(cuda).t().contiguous().t()
+    f1 = rsvd(ad, RsvdParams(16, 30, 2, 3))
+    f2 = rsvd(ad, RsvdParams(16, 30, 2, 3))
+    assert torch.equal(f1.left, f2.left) and torch.equal(f1.sigma, f2.sigma)
+    fh = rsvd(a, RsvdParams(16, 30, 2, 3))
+    assert np.array_equal(fh.left, f1.left.cpu().numpy())
+    e_dev = reconstruction_error(ad, f1)
+    e_ora = oracle_mod.zreconstruction_error(a, fh.left, fh.sigma, fh.right_adj)
+    assert abs(e_dev - e_ora) / e_ora < REC_TOL
+
+
+def test_complex_randomized_range_spans_oracle_range(cuda, oracle_mod):
+    from paper_1710_01463_b200 import randomized_range
+
+    a = zmatrix_with_spectrum(oracle_mod, 44, 90, 70, np.exp(-np.arange(70) / 5.0))
+    Q = np.asarray(randomized_range(a, 20, 2, 9))
+    Qr = oracle_mod.zrandomized_range(a, 20, 2, 9)
+    assert Q.dtype == np.complex128
+    assert isometry_err(Q) < ISO_TOL
+    # exp(-k/5) spectrum: the leading 12 directions are captured to ~1e-12
+    assert subspace_distance(Qr[:, :12], Q) < SUB_TOL
+
+
+def test_complex_invalid_arguments(cuda):
+    from paper_1710_01463_b200 import InvalidArgument, RsvdParams, rsvd, tsvd
+
+    a = np.ones((6, 4), dtype=np.complex128)
+    with pytest.raises(InvalidArgument, match="rank must be >= 1"):
+        rsvd(a, RsvdParams(0, 0, 1, 0))
+    with pytest.raises(InvalidArgument, match="oversample must be >= rank"):
+        rsvd(a, RsvdParams(2, 1, 1, 0))
+    with pytest.raises(InvalidArgument, match="need 1 <= ell"):
+        rsvd(a, RsvdParams(2, 5, 1, 0))
+    with pytest.raises(InvalidArgument, match="tsvd: rank must be >= 1"):
+        tsvd(a, 0)
+
+
+def test_complex_zero_matrix(cuda):
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    a = np.zeros((20, 16), dtype=np.complex128)
+    f = rsvd(a, RsvdParams(4, 8, 2, 1))
+    assert f.rank() == 0
+    assert f.discarded_weight == 0.0
