@@ -97,8 +97,10 @@ def _shape(b) -> Tuple[int, int]:
 
 def _sqnorm(b) -> float:
     if _is_torch_cuda(b):
-        return float((b * b).sum().item())
-    return float(np.sum(np.asarray(b, dtype=np.float64) ** 2))
+        return float((b.abs() ** 2).sum().item()) if b.is_complex() else float((b * b).sum().item())
+    x = np.asarray(b)
+    return float(np.sum(np.abs(x) ** 2)) if np.iscomplexobj(x) else float(
+        np.sum(np.asarray(x, dtype=np.float64) ** 2))
 
 
 def _empty_factor(b) -> TruncatedFactorization:
@@ -106,10 +108,12 @@ def _empty_factor(b) -> TruncatedFactorization:
     if _is_torch_cuda(b):
         import torch
 
-        z = lambda *s: torch.zeros(s, dtype=torch.float64, device=b.device)  # noqa: E731
-        return TruncatedFactorization(z(m, 0), z(0), z(0, n), _sqnorm(b), True)
-    return TruncatedFactorization(np.zeros((m, 0)), np.zeros(0), np.zeros((0, n)), _sqnorm(b),
-                                  True)
+        z = lambda *s: torch.zeros(s, dtype=b.dtype, device=b.device)  # noqa: E731
+        return TruncatedFactorization(z(m, 0), torch.zeros(0, dtype=torch.float64, device=b.device),
+                                      z(0, n), _sqnorm(b), True)
+    dt = np.complex128 if np.iscomplexobj(b) else np.float64
+    return TruncatedFactorization(np.zeros((m, 0), dtype=dt), np.zeros(0), np.zeros((0, n), dtype=dt),
+                                  _sqnorm(b), True)
 
 
 def _stack(blocks: List[Any]):
@@ -117,7 +121,8 @@ def _stack(blocks: List[Any]):
         import torch
 
         return torch.stack([x.t() for x in blocks]).transpose(1, 2)  # column-major items
-    return np.stack([np.asarray(x, dtype=np.float64) for x in blocks])
+    dt = np.complex128 if any(np.iscomplexobj(x) for x in blocks) else np.float64
+    return np.stack([np.asarray(x, dtype=dt) for x in blocks])
 
 
 def _validate(a: BlockDiagMatrix) -> None:

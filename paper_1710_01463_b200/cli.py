@@ -10,8 +10,9 @@ three-line stdout summary; rank clipped to min(m, n); the rsvd seed is
 derive_seed(S, rsvd_stream) (cli.cpp:197); output directory precedence
 RLFTN_OUT, then --out, then "factors".  Exit codes: 0 ok, 1 runtime error
 ("error: ..." or, with --error-json, a JSON object), 2 usage error.
-Real FP64 matrices only: complex input exits 1 (the complex instantiation is
-not built on the GPU).
+Real and complex matrices (the reference's std::visit over AnyMatrix,
+cli.cpp:185-240): a complex file runs the complex instantiation and writes
+complex factors, "complex": true in summary.json.
 """
 from __future__ import annotations
 
@@ -57,9 +58,7 @@ def cmd_factorize(o) -> int:
     if o.method not in ("tsvd", "rsvd"):
         raise UsageError("--method must be tsvd or rsvd")
     a = load_matrix(o.inp)
-    if np.iscomplexobj(a):
-        raise RuntimeError("complex matrices are not supported by the B200 engine "
-                           "(real FP64 path only)")
+    cplx = bool(np.iscomplexobj(a))
     out_dir = _resolve_out(o.out, o.out is not None, "factors")
     os.makedirs(out_dir, exist_ok=True)
     m, n = a.shape
@@ -75,7 +74,7 @@ def cmd_factorize(o) -> int:
         fh.write(",".join(fmt(x) for x in sig) + "\n")
     save_matrix_binary(os.path.join(out_dir, "left.bin"), np.asarray(f.left))
     save_matrix_binary(os.path.join(out_dir, "right.bin"), np.asarray(f.right_adj))
-    j = {"rows": m, "cols": n, "complex": False, "requested_rank": o.rank, "rank": f.rank(),
+    j = {"rows": m, "cols": n, "complex": cplx, "requested_rank": o.rank, "rank": f.rank(),
          "method": o.method, "discarded_weight": f.discarded_weight,
          "discarded_exact": f.discarded_exact, "frobenius_error": fro,
          "files": {"spectrum": "spectrum.csv", "left": "left.bin", "right": "right.bin"}}

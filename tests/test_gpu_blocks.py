@@ -296,3 +296,29 @@ def test_tsvd_rank_deficient_graded_block(cuda, oracle_mod):
         assert f.rank() == len(S)
         assert np.max(np.abs(np.asarray(f.sigma) - S)) < 1e-14  # ~50 u ||A||
         assert f.discarded_weight == pytest.approx(dw, abs=1e-28)
+
+
+@pytest.mark.parametrize("kind", ["tsvd", "rsvd"])
+def test_block_factorize_complex_vs_oracle(cuda, oracle_mod, kind):
+    """block_factorize<Complex> (blocks.cpp:122): complex sectors through the
+    complex engine, global selection over the merged spectra as for real."""
+    from paper_1710_01463_b200 import BlockDiagMatrix, BlockMethod, block_factorize
+    from tests.helpers import zmatrix_with_spectrum
+
+    blocks = [zmatrix_with_spectrum(oracle_mod, 70 + i, 48 + 8 * i, 40, np.exp(-np.arange(40) / (5.0 + i)))
+              for i in range(3)]
+    a = BlockDiagMatrix([0, 1, 2], blocks)
+    meth = BlockMethod.randomized(4, 77) if kind == "rsvd" else BlockMethod.deterministic()
+    f = block_factorize(a, 24, _req(), meth)
+    assert f.total_rank() == 24
+    merged = np.sort(np.concatenate([np.asarray(x.sigma) for x in f.factors]))[::-1]
+    want = np.sort(np.concatenate([np.exp(-np.arange(40) / (5.0 + i)) for i in range(3)]))[::-1][:24]
+    np.testing.assert_allclose(merged, want, rtol=1e-9)
+    for x, b in zip(f.factors, blocks):
+        assert np.asarray(x.left).dtype == np.complex128
+        r = x.rank()
+        if r:
+            rec = (np.asarray(x.left) * np.asarray(x.sigma)[None, :]) @ np.asarray(x.right_adj)
+            tail = np.linalg.norm(b - rec) ** 2
+            assert tail == pytest.approx(np.linalg.norm(b) ** 2 - np.sum(np.asarray(x.sigma) ** 2),
+                                         rel=1e-8, abs=1e-20)

@@ -66,3 +66,26 @@ def test_factorize_matches_oracle_and_env_out(cuda, tmp_path, oracle_mod):
     np.testing.assert_array_equal(got, ref.sigma)
     _, S, _, _ = oracle_mod.rsvd(a, 7, 14, 2, derive_seed(9, 2))
     np.testing.assert_allclose(got, S, rtol=1e-10)
+
+
+def test_factorize_complex_file(cuda, tmp_path, oracle_mod):
+    """Complex input runs the complex instantiation (cli.cpp:185-240 visits
+    MatrixC): complex factors in left.bin / right.bin, "complex": true."""
+    from tests.helpers import zmatrix_with_spectrum
+
+    a = zmatrix_with_spectrum(oracle_mod, 4, 40, 30, np.exp(-np.arange(30) / 4.0))
+    io.save_matrix_binary(str(tmp_path / "z.bin"), a)
+    for method in ("tsvd", "rsvd"):
+        out = tmp_path / method
+        r = _cli("factorize", "--in", str(tmp_path / "z.bin"), "--rank", "6", "--method", method,
+                 "--oversample", "12", "--power", "2", "--out", str(out))
+        assert r.returncode == 0, r.stderr
+        j = json.loads((out / "summary.json").read_text())
+        assert j["complex"] is True and j["rank"] == 6
+        left = io.load_matrix(str(out / "left.bin"))
+        right = io.load_matrix(str(out / "right.bin"))
+        assert left.dtype == np.complex128 and left.shape == (40, 6) and right.shape == (6, 30)
+        got = np.array([float(x) for x in (out / "spectrum.csv").read_text().split(",")])
+        np.testing.assert_allclose(got, np.exp(-np.arange(6) / 4.0), rtol=1e-10)
+        rec = left @ np.diag(got) @ right
+        assert np.linalg.norm(a - rec) == pytest.approx(j["frobenius_error"], rel=1e-8)
