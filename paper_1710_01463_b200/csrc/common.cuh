@@ -191,10 +191,7 @@ void launch_zadjoint(CMatRef X, bool from_p, MatRef out, int64_t rows, int64_t c
                      int64_t batch, cudaStream_t st);
 void launch_zidentity_p(MatRef X, int64_t rows, int64_t lp, int64_t ell, int64_t batch,
                         cudaStream_t st);
-void launch_zchol(const double* Gt, double* Tt, double* Rt, double* W, double* Rc, double* Tc,
-                  int* rank, int* rank2, int* colmap, int* ill, const int* mask, int64_t ell,
-                  int64_t lp, double tau, double shift_coef, int mode, int64_t batch,
-                  cudaStream_t st);
+void launch_hermitize(double* G, int64_t lp, const int* mask, int64_t batch, cudaStream_t st);
 void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                     double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
                     int64_t batch, cudaStream_t st);

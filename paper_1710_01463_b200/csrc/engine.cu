@@ -358,8 +358,12 @@ bool full_orth() {
 // Householder QR (lapack.cpp:146-201), instead of a random completion -- the
 // sampled tail (discarded weight) of steep spectra depends on them.  Items
 // that never truncate pay only the no-op launches.
+// cplx: Y is a complex basis in P-layout (zkern.cu; s.ell / s.ellp are the
+// realified 2l / 2lp) and every Gram is replaced by the realified complex Gram
+// before the Cholesky (launch_hermitize): the same passes then compute the
+// complex CholeskyQR.
 void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, double* Rt,
-          uint64_t tag, int passes, bool m_side, cudaStream_t st) {
+          uint64_t tag, int passes, bool m_side, cudaStream_t st, bool cplx = false) {
   const int64_t lp = s.ellp, b = s.batch;
   const bool sharded = m_side && B.red;
   const int64_t row_off = m_side ? s.row_off : 0, rows_global = m_side ? s.mg() : rows;
@@ -374,6 +378,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     sym.item_mask = mask;
     dgemm_ex(true, lp, lp, rows, in, in, G, b, B.partial, B.partial_cap, sym, st);
     if (sharded) B.red->allreduce_sum(B.G, b * lp * lp, st);  // G = sum_p Y_p^T Y_p
+    if (cplx) launch_hermitize(B.G, lp / 2, mask, b, st);
   };
   auto apply = [&](const MatRef& in, const MatRef& out, const int* mask, bool pivoted) {
     // out = (in P) R11^{-1}: pivot-gathered columns (only when this pass

@@ -16,6 +16,8 @@
 //             A-hat^T PAIR(Q) = (A^H Q)_P, the TN A-pass, lands in P-layout.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace rsvd {
@@ -212,219 +214,29 @@ __global__ void zidentity_p_kernel(double* __restrict__ X, int64_t ld, int64_t s
   }
 }
 
-// ------------------------------------------------------ complex Cholesky
-// Hermitian Gram G (l x l) = X^H X read off the realified real Gram
-// Gt = X_P^T X_P (2lp x 2lp):
-//   G_ac = Gt[2a,2c] + Gt[2a+1,2c+1] + i (Gt[2a,2c+1] - Gt[2a+1,2c]).
-// Factor G = R^H R (optionally with diagonal pivoting, dpstrf-style), stop at
-// the first pivot <= tau * max diag (numerical rank r), T = R11^-1; write the
-// realified T~ (with the pivot as a real column map) and R~ (columns scattered
-// back: Y_in = Q_out R~).  One CTA per item; the working copy lives in a
-// global scratch (L2 resident).
-//   mode 0: unpivoted; an item that breaks down is refactored as G + s tr(G) I
-//           (shifted CholeskyQR, never truncated) and flagged ill[b] = 1.
-//   mode 1: pivoted, items with mask[b] == 0 skipped.
-//   mode 2: unpivoted, plain (breakdown -> rank).
-struct ZCholArgs {
-  const double* Gt;  // 2lp x 2lp per item
-  double* Tt;        // 2lp x 2lp per item (realified T)
-  double* Rt;        // optional, 2lp x 2lp per item (realified R P^T)
-  double2* W;        // scratch lp x lp per item
-  double2* Rc;       // scratch lp x lp per item (R, pivoted order)
-  double2* Tc;       // scratch lp x lp per item (T)
-  int* rank;         // complex rank per item
-  int* rank2;        // 2 * rank (real column count of the P-layout basis)
-  int* colmap;       // 2lp per item (pivoted mode)
-  int* ill;          // mode 0 output
-  const int* mask;   // mode 1 input
-  int64_t ell, lp;
-  double tau, shift_coef;
-  int mode;
-};
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {  // conj(a) * b
-  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
-}
-
-__global__ void __launch_bounds__(512) zchol_kernel(ZCholArgs p) {
-  const int64_t b = blockIdx.x;
-  const int ell = static_cast<int>(p.ell);
-  const int64_t lp = p.lp, L = 2 * lp;
-  if (p.mode == 1 && !p.mask[b]) return;
-  __shared__ int s_piv[1024];
-  __shared__ double s_red[32];
-  __shared__ int s_redi[32];
-  __shared__ int s_rank, s_shift, s_pivot;
-  __shared__ double s_dmax;
-  const double* Gt = p.Gt + b * L * L;
-  double2* W = p.W + b * lp * lp;
-  double2* Rc = p.Rc + b * lp * lp;
-  double2* Tc = p.Tc + b * lp * lp;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  const bool pivot = p.mode == 1;
-  if (tid == 0) s_shift = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    // Load G (full Hermitian) into W, optional shift.
-    for (int64_t e = tid; e < static_cast<int64_t>(ell) * ell; e += nt) {
-      const int a = static_cast<int>(e % ell), c = static_cast<int>(e / ell);
-      const double re = Gt[2 * a + (2 * c) * L] + Gt[2 * a + 1 + (2 * c + 1) * L];
-      const double im = Gt[2 * a + (2 * c + 1) * L] - Gt[2 * a + 1 + (2 * c) * L];
-      W[a + c * lp] = make_double2(re, a == c ? 0.0 : im);
-    }
-    for (int a = tid; a < ell; a += nt) s_piv[a] = a;
-    __syncthreads();
-    if (s_shift) {  // G + coef * tr(G) * I
-      if (warp == 0) {
-        double tr = 0.0;
-        for (int a = lane; a < ell; a += 32) tr += W[a + a * lp].x;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
-        if (lane == 0) s_red[0] = tr;
-      }
-      __syncthreads();
-      const double sh = p.shift_coef * s_red[0];
-      for (int a = tid; a < ell; a += nt) W[a + a * lp].x += sh;
-      __syncthreads();
-    }
-    // max diagonal
-    {
-      double mx = 0.0;
-      for (int a = tid; a < ell; a += nt) mx = fmax(mx, W[a + a * lp].x);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) s_red[warp] = mx;
-      __syncthreads();
-      if (tid == 0) {
-        double v = 0.0;
-        for (int w = 0; w < nw; ++w) v = fmax(v, s_red[w]);
-        s_dmax = v;
-        s_rank = ell;
-      }
-      __syncthreads();
-    }
-    const double floor_v = p.tau * s_dmax;
-    for (int j = 0; j < ell; ++j) {
-      if (pivot) {
-        double best = -1.0;
-        int bi = j;
-        for (int a = j + tid; a < ell; a += nt) {
-          const double d = W[s_piv[a] + s_piv[a] * lp].x;
-          if (d > best) best = d, bi = a;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
-        }
-        if (lane == 0) s_red[warp] = best, s_redi[warp] = bi;
-        __syncthreads();
-        if (tid == 0) {
-          double bv = s_red[0];
-          int bx = s_redi[0];
-          for (int w = 1; w < nw; ++w)
-            if (s_red[w] > bv || (s_red[w] == bv && s_redi[w] < bx)) bv = s_red[w], bx = s_redi[w];
-          const int t = s_piv[j];
-          s_piv[j] = s_piv[bx];
-          s_piv[bx] = t;
-        }
-        __syncthreads();
-      }
-      const int pj = s_piv[j];
-      const double d = W[pj + pj * lp].x;
-      if (!(d > floor_v) || !(d > 0.0)) {
-        if (tid == 0) s_rank = j;
-        __syncthreads();
-        break;
-      }
-      const double rjj = sqrt(d), inv = 1.0 / rjj;
-      // Row j of R (pivoted order): R[j, c] = W[pj, pc] / rjj, c > j.
-      for (int c = j + 1 + tid; c < ell; c += nt) {
-        const double2 w = W[pj + s_piv[c] * lp];
-        Rc[j + c * lp] = make_double2(w.x * inv, w.y * inv);
-      }
-      if (tid == 0) Rc[j + j * lp] = make_double2(rjj, 0.0);
-      __syncthreads();
-      // Trailing update W[pa, pc] -= conj(R[j, a]) R[j, c], a, c > j.
-      const int nr = ell - j - 1;
-      for (int64_t e = tid; e < static_cast<int64_t>(nr) * nr; e += nt) {
-        const int a = j + 1 + static_cast<int>(e % nr), c = j + 1 + static_cast<int>(e / nr);
-        const double2 ra = Rc[j + a * lp], rc = Rc[j + c * lp];
-        const double2 u = cconjmul(ra, rc);
-        double2& w = W[s_piv[a] + s_piv[c] * lp];
-        w.x -= u.x;
-        w.y -= u.y;
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    if (p.mode == 0 && attempt == 0 && s_rank < ell) {
-      if (tid == 0) s_shift = 1;
-      __syncthreads();
-      continue;  // refactor the shifted Gram
-    }
-    break;
-  }
-  const int r = s_rank;
-  if (tid == 0) {
-    p.rank[b] = r;
-    if (p.rank2) p.rank2[b] = 2 * r;
-    if (p.ill) p.ill[b] = s_shift;
-  }
-  // T = R11^-1, rows bottom-up: T[a, c] = (delta_ac - sum_{a<k<=c} R[a,k] T[k,c]) / R[a,a].
-  for (int a = r - 1; a >= 0; --a) {
-    const double2 raa = Rc[a + a * lp];
-    const double iv = 1.0 / raa.x;
-    for (int c = a + tid; c < r; c += nt) {
-      double2 s = make_double2(c == a ? 1.0 : 0.0, 0.0);
-      for (int k = a + 1; k <= c; ++k) {
-        const double2 u = cmul(Rc[a + k * lp], Tc[k + c * lp]);
-        s.x -= u.x;
-        s.y -= u.y;
-      }
-      Tc[a + c * lp] = make_double2(s.x * iv, s.y * iv);
-    }
-    __syncthreads();
-  }
-  // Realified outputs.
-  double* Tt = p.Tt + b * L * L;
-  for (int64_t e = tid; e < L * L; e += nt) {
-    const int64_t R2 = e % L, C2 = e / L;
-    const int a = static_cast<int>(R2 >> 1), c = static_cast<int>(C2 >> 1);
-    double v = 0.0;
-    if (a < r && c < r && a <= c) {
-      const double2 t = Tc[a + c * lp];
-      const int ra = static_cast<int>(R2 & 1), rc = static_cast<int>(C2 & 1);
-      v = (ra == rc) ? t.x : (ra ? -t.y : t.y);
-    }
-    Tt[e] = v;
-  }
-  if (p.Rt) {
-    double* Rt = p.Rt + b * L * L;
-    for (int64_t e = tid; e < L * L; e += nt) Rt[e] = 0.0;
-    __syncthreads();
-    // R P^T: column c of R (pivoted order) goes to column piv[c].
-    for (int64_t e = tid; e < static_cast<int64_t>(r) * ell; e += nt) {
-      const int a = static_cast<int>(e % r), c = static_cast<int>(e / r);
-      if (a > c) continue;
-      const double2 v = Rc[a + c * lp];
-      const int64_t oc = s_piv[c];
-      Rt[2 * a + (2 * oc) * L] = v.x;
-      Rt[2 * a + 1 + (2 * oc + 1) * L] = v.x;
-      Rt[2 * a + (2 * oc + 1) * L] = v.y;
-      Rt[2 * a + 1 + (2 * oc) * L] = -v.y;
-    }
-  }
-  if (p.colmap) {
-    int* cm = p.colmap + b * L;
-    for (int64_t e = tid; e < L; e += nt) {
-      const int c = static_cast<int>(e >> 1);
-      cm[e] = c < ell ? 2 * s_piv[c] + static_cast<int>(e & 1) : static_cast<int>(e);
-    }
+// Realified Hermitian Gram, in place.  In: Gt = X_P^T X_P (2lp x 2lp real,
+// symmetric).  Out: the realification of G = X^H X in the M~ convention,
+//   G_ac = Gt[2a,2c] + Gt[2a+1,2c+1] + i (Gt[2a,2c+1] - Gt[2a+1,2c]),
+// whose real Cholesky factor is exactly the realified complex factor R~
+// (realification is a *-homomorphism and R~ is upper triangular with
+// diagonal blocks r I), so the real CholeskyQR machinery orthonormalises the
+// complex basis X_P (engine.cu orth(..., cplx = true)).
+__global__ void hermitize_kernel(double* __restrict__ G, int64_t lp, const int* __restrict__ mask) {
+  const int64_t b = blockIdx.y;
+  if (mask && !mask[b]) return;
+  const int64_t L = 2 * lp;
+  double* g = G + b * L * L;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < lp * lp;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = e % lp, c = e / lp;
+    double* p0 = g + 2 * a + (2 * c) * L;  // column 2c, rows 2a, 2a+1
+    double* p1 = g + 2 * a + (2 * c + 1) * L;
+    const double2 c0 = *reinterpret_cast<const double2*>(p0);
+    const double2 c1 = *reinterpret_cast<const double2*>(p1);
+    const double gr = c0.x + c1.y;
+    const double gi = a == c ? 0.0 : c1.x - c0.y;
+    *reinterpret_cast<double2*>(p0) = make_double2(gr, -gi);
+    *reinterpret_cast<double2*>(p1) = make_double2(gi, gr);
   }
 }
 
@@ -438,44 +250,60 @@ __global__ void __launch_bounds__(512) zchol_kernel(ZCholArgs p) {
 // |gamma| > sqrt(l) eps sqrt(alpha beta) (dgesvj's); round-robin ordering,
 // every pair once per sweep; stops after a sweep with no rotation or whose
 // largest rotated ratio was below 1e-9 (quadratic convergence).
-// One CTA per item; H and J stay in global scratch (L2).
+// Each item is owned by a thread-block cluster of S CTAs (S = 1 for large
+// batches): the l/2 disjoint pairs of a round-robin step are spread over the
+// S x 16 warps, one cluster barrier per step; H and J live in global scratch
+// (L2), read with ld.global.cg so no CTA sees a stale L1 line.  RPL > 0 keeps
+// each warp's two columns in registers (RPL complex rows per lane) between
+// the dot products and the rotation; RPL = 0 streams them twice.
 //   src_mode 0: H = Rt^H from the realified R~t (2lp x 2lp);
 //   src_mode 1: H from a P-layout l x 2lp matrix (tsvd: H = A_e Qb).
-__global__ void __launch_bounds__(1024) zjacobi_kernel(const double* __restrict__ src,
-                                                       int64_t src_ld, int64_t src_stride,
-                                                       int src_mode, double2* __restrict__ H,
-                                                       double2* __restrict__ J, int64_t ell_,
-                                                       int64_t lp, int max_sweeps,
-                                                       int* __restrict__ sweeps_out) {
-  const int64_t b = blockIdx.x;
-  const int ell = static_cast<int>(ell_);
+__device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
+
+template <int RPL>
+__global__ void __launch_bounds__(512) zjacobi_kernel(const double* __restrict__ src,
+                                                      int64_t src_ld, int64_t src_stride,
+                                                      int src_mode, double2* __restrict__ H,
+                                                      double2* __restrict__ J, int ell,
+                                                      int64_t lp, int max_sweeps,
+                                                      int* __restrict__ sweeps_out, int S) {
+  namespace cg = cooperative_groups;
+  const int crank = S > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const int64_t b = blockIdx.x / S;
   double2* Hb = H + b * lp * lp;
   double2* Jb = J + b * lp * lp;
-  const double* S = src + b * src_stride;
+  const double* Sb = src + b * src_stride;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  for (int64_t e = tid; e < lp * lp; e += nt) {
+  auto sync_all = [&] {
+    if (S > 1)
+      cg::this_cluster().sync();
+    else
+      __syncthreads();
+  };
+  for (int64_t e = static_cast<int64_t>(crank) * nt + tid; e < lp * lp;
+       e += static_cast<int64_t>(S) * nt) {
     const int a = static_cast<int>(e % lp), c = static_cast<int>(e / lp);
     double2 h = make_double2(0.0, 0.0);
     if (a < ell && c < ell) {
       if (src_mode == 0)  // H[a, c] = conj(Rt[c, a]) = Rt~[2c, 2a] + i Rt~[2c+1, 2a]
-        h = make_double2(S[2 * c + (2 * a) * src_ld], S[2 * c + 1 + (2 * a) * src_ld]);
+        h = make_double2(Sb[2 * c + (2 * a) * src_ld], Sb[2 * c + 1 + (2 * a) * src_ld]);
       else
-        h = make_double2(S[a + (2 * c) * src_ld], S[a + (2 * c + 1) * src_ld]);
+        h = make_double2(Sb[a + (2 * c) * src_ld], Sb[a + (2 * c + 1) * src_ld]);
     }
     Hb[e] = h;
     Jb[e] = make_double2(a == c ? 1.0 : 0.0, 0.0);
   }
   __shared__ unsigned long long s_max;  // largest rotated ratio of the sweep (bits of a double >= 0)
   __shared__ int s_rot;
-  __syncthreads();
   const int le = ell + (ell & 1);
   const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
+  const int gw = crank * nw + warp, tw = S * nw;
   int sweep = 0;
+  if (tid == 0) s_max = 0ull, s_rot = 0;
+  sync_all();
   for (; sweep < max_sweeps && ell > 1; ++sweep) {
-    if (tid == 0) s_max = 0ull, s_rot = 0;
-    __syncthreads();
     for (int step = 0; step < le - 1; ++step) {
-      for (int k = warp; k < le / 2; k += nw) {
+      for (int k = gw; k < le / 2; k += tw) {
         const int pp = k == 0 ? 0 : ((k - 1 + step) % (le - 1)) + 1;
         const int qq = ((le - 2 - k + step) % (le - 1)) + 1;
         if (pp >= ell || qq >= ell) continue;
@@ -483,12 +311,30 @@ __global__ void __launch_bounds__(1024) zjacobi_kernel(const double* __restrict_
         double2* hp = Hb + pc * lp;
         double2* hq = Hb + qc * lp;
         double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-        for (int i = lane; i < ell; i += 32) {
-          const double2 x = hp[i], y = hq[i];
-          al = fma(x.x, x.x, fma(x.y, x.y, al));
-          be = fma(y.x, y.x, fma(y.y, y.y, be));
-          gr = fma(x.x, y.x, fma(x.y, y.y, gr));   // Re conj(x) y
-          gi = fma(x.x, y.y, fma(-x.y, y.x, gi));  // Im conj(x) y
+        double2 xr[RPL > 0 ? RPL : 1], yr[RPL > 0 ? RPL : 1];
+        if (RPL > 0) {
+#pragma unroll
+          for (int r = 0; r < (RPL > 0 ? RPL : 1); ++r) {
+            const int i = lane + 32 * r;
+            xr[r] = i < ell ? ldcg2(hp + i) : make_double2(0.0, 0.0);
+            yr[r] = i < ell ? ldcg2(hq + i) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int r = 0; r < (RPL > 0 ? RPL : 1); ++r) {
+            const double2 x = xr[r], y = yr[r];
+            al = fma(x.x, x.x, fma(x.y, x.y, al));
+            be = fma(y.x, y.x, fma(y.y, y.y, be));
+            gr = fma(x.x, y.x, fma(x.y, y.y, gr));
+            gi = fma(x.x, y.y, fma(-x.y, y.x, gi));
+          }
+        } else {
+          for (int i = lane; i < ell; i += 32) {
+            const double2 x = ldcg2(hp + i), y = ldcg2(hq + i);
+            al = fma(x.x, x.x, fma(x.y, x.y, al));
+            be = fma(y.x, y.x, fma(y.y, y.y, be));
+            gr = fma(x.x, y.x, fma(x.y, y.y, gr));
+            gi = fma(x.x, y.y, fma(-x.y, y.x, gi));
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -506,36 +352,67 @@ __global__ void __launch_bounds__(1024) zjacobi_kernel(const double* __restrict_
         }
         const double zeta = (be - al) / (2.0 * g);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
         const double er = gr / g, ei = gi / g;  // e = gamma / |gamma|
         // h_p' = c h_p - s conj(e) h_q ; h_q' = s e h_p + c h_q
-        auto rot = [&](double2* xp, double2* xq, int n) {
-          for (int i = lane; i < n; i += 32) {
-            const double2 x = xp[i], y = xq[i];
-            const double2 ey = make_double2(er * y.x + ei * y.y, er * y.y - ei * y.x);  // conj(e) y
-            const double2 ex = make_double2(er * x.x - ei * x.y, er * x.y + ei * x.x);  // e x
-            xp[i] = make_double2(c * x.x - s * ey.x, c * x.y - s * ey.y);
-            xq[i] = make_double2(s * ex.x + c * y.x, s * ex.y + c * y.y);
-          }
+        auto rot = [&](double2 x, double2 y, double2& xo, double2& yo) {
+          const double2 ey = make_double2(er * y.x + ei * y.y, er * y.y - ei * y.x);  // conj(e) y
+          const double2 ex = make_double2(er * x.x - ei * x.y, er * x.y + ei * x.x);  // e x
+          xo = make_double2(c * x.x - sn * ey.x, c * x.y - sn * ey.y);
+          yo = make_double2(sn * ex.x + c * y.x, sn * ex.y + c * y.y);
         };
-        rot(hp, hq, ell);
-        rot(Jb + pc * lp, Jb + qc * lp, ell);
+        if (RPL > 0) {
+#pragma unroll
+          for (int r = 0; r < (RPL > 0 ? RPL : 1); ++r) {
+            const int i = lane + 32 * r;
+            if (i < ell) {
+              double2 xo, yo;
+              rot(xr[r], yr[r], xo, yo);
+              hp[i] = xo;
+              hq[i] = yo;
+            }
+          }
+        } else {
+          for (int i = lane; i < ell; i += 32) {
+            double2 xo, yo;
+            rot(ldcg2(hp + i), ldcg2(hq + i), xo, yo);
+            hp[i] = xo;
+            hq[i] = yo;
+          }
+        }
+        double2* jp = Jb + pc * lp;
+        double2* jq = Jb + qc * lp;
+        for (int i = lane; i < ell; i += 32) {
+          double2 xo, yo;
+          rot(ldcg2(jp + i), ldcg2(jq + i), xo, yo);
+          jp[i] = xo;
+          jq[i] = yo;
+        }
       }
-      __syncthreads();
+      sync_all();
     }
-    const bool any = s_rot != 0;
-    const double mx = __longlong_as_double(static_cast<long long>(s_max));
-    __syncthreads();
-    if (!any) {
-      ++sweep;
-      break;
+    // Cluster-wide decision: every CTA reads every CTA's flags (identical result).
+    bool any = false;
+    double mx = 0.0;
+    if (S > 1) {
+      cg::cluster_group cl = cg::this_cluster();
+      for (int r = 0; r < S; ++r) {
+        any = any || (*cl.map_shared_rank(&s_rot, r) != 0);
+        mx = fmax(mx, __longlong_as_double(static_cast<long long>(*cl.map_shared_rank(&s_max, r))));
+      }
+    } else {
+      any = s_rot != 0;
+      mx = __longlong_as_double(static_cast<long long>(s_max));
     }
-    if (mx < 1e-9) {
+    sync_all();
+    if (tid == 0) s_max = 0ull, s_rot = 0;
+    sync_all();
+    if (!any || mx < 1e-9) {
       ++sweep;
       break;
     }
   }
-  if (tid == 0 && sweeps_out) sweeps_out[b] = sweep;
+  if (crank == 0 && tid == 0 && sweeps_out) sweeps_out[b] = sweep;
 }
 
 // sigma_c = ||W e_c|| (complex columns), descending with ties by index,
@@ -708,31 +585,58 @@ void launch_zidentity_p(MatRef X, int64_t rows, int64_t lp, int64_t ell, int64_t
   RSVD_LAUNCH("zidentity_p_kernel");
 }
 
-void launch_zchol(const double* Gt, double* Tt, double* Rt, double* W, double* Rc, double* Tc,
-                  int* rank, int* rank2, int* colmap, int* ill, const int* mask, int64_t ell,
-                  int64_t lp, double tau, double shift_coef, int mode, int64_t batch,
-                  cudaStream_t st) {
-  if (batch <= 0) return;
-  if (ell > 1024) throw std::invalid_argument("complex Cholesky: l > 1024 is not supported");
-  ZCholArgs a;
-  a.Gt = Gt, a.Tt = Tt, a.Rt = Rt;
-  a.W = reinterpret_cast<double2*>(W);
-  a.Rc = reinterpret_cast<double2*>(Rc);
-  a.Tc = reinterpret_cast<double2*>(Tc);
-  a.rank = rank, a.rank2 = rank2, a.colmap = colmap, a.ill = ill, a.mask = mask;
-  a.ell = ell, a.lp = lp, a.tau = tau, a.shift_coef = shift_coef, a.mode = mode;
-  zchol_kernel<<<static_cast<unsigned>(batch), 512, 0, st>>>(a);
-  RSVD_LAUNCH("zchol_kernel");
+void launch_hermitize(double* G, int64_t lp, const int* mask, int64_t batch, cudaStream_t st) {
+  if (batch <= 0 || lp <= 0) return;
+  dim3 grid(grid_for(lp * lp, 256, 2), static_cast<unsigned>(batch));
+  hermitize_kernel<<<grid, 256, 0, st>>>(G, lp, mask);
+  RSVD_LAUNCH("hermitize_kernel");
+}
+
+template <int RPL>
+void launch_zjacobi_t(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
+                      double* H, double* J, int ell, int64_t lp, int max_sweeps, int* sweeps,
+                      int64_t batch, int S, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(S);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(512);
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * S));
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = S > 1 ? 1 : 0;
+  RSVD_CUDA(cudaLaunchKernelEx(&cfg, zjacobi_kernel<RPL>, src, src_ld, src_stride, src_mode,
+                               reinterpret_cast<double2*>(H), reinterpret_cast<double2*>(J), ell,
+                               lp, max_sweeps, sweeps, S));
+  RSVD_LAUNCH("zjacobi_kernel");
 }
 
 void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                     double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
                     int64_t batch, cudaStream_t st) {
   if (batch <= 0) return;
-  zjacobi_kernel<<<static_cast<unsigned>(batch), 1024, 0, st>>>(
-      src, src_ld, src_stride, src_mode, reinterpret_cast<double2*>(H),
-      reinterpret_cast<double2*>(J), ell, lp, max_sweeps, sweeps);
-  RSVD_LAUNCH("zjacobi_kernel");
+  // Cluster size: fill the SMs (S CTAs per item, at most 8, portable) but
+  // never more warps than the l/2 pairs of a step.
+  const int64_t pairs = (ell + 1) / 2;
+  int S = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, kNumSMs / batch)));
+  S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, ceil_div(pairs, 16))));
+  if (const char* e = std::getenv("RSVD_ZJACOBI_CLUSTER")) S = std::max(1, std::min(8, std::atoi(e)));
+  const int e = static_cast<int>(ell);
+  const int rpl = static_cast<int>(ceil_div(ell, 32));
+  if (rpl <= 1)
+    launch_zjacobi_t<1>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
+  else if (rpl <= 2)
+    launch_zjacobi_t<2>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
+  else if (rpl <= 3)
+    launch_zjacobi_t<3>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
+  else if (rpl <= 5)
+    launch_zjacobi_t<5>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
+  else if (rpl <= 9)
+    launch_zjacobi_t<9>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
+  else
+    launch_zjacobi_t<0>(src, src_ld, src_stride, src_mode, H, J, e, lp, max_sweeps, sweeps, batch, S, st);
 }
 
 void launch_zfinalize(const double* W, int64_t lp, int64_t ell, int64_t k, int64_t m, int64_t n,
