@@ -2,8 +2,10 @@
 // the C ABI of include/rsvd_c.h.
 //
 // Mirrors proj/include/rlftn/factorize.hpp: RsvdParams (hpp:40-45),
-// TruncatedFactorization (hpp:15-31), rsvd (hpp:62-63), randomized_range
-// (hpp:56-57), reconstruction_error (hpp:68-70), and rng.hpp's mix64 /
+// TruncatedFactorization<Scalar> (hpp:15-31), rsvd (hpp:62-63), tsvd
+// (hpp:49-50), randomized_range (hpp:56-57), reconstruction_error
+// (hpp:68-70), each for Scalar = double and std::complex<double> as the
+// reference instantiates them (factorize.cpp:106-118), and rng.hpp's mix64 /
 // derive_seed / seed_tag.  Errors are rethrown as the reference's exception
 // types with the reference's messages (std::invalid_argument for argument
 // errors, std::runtime_error otherwise).  The matrix type is an owning
@@ -12,9 +14,11 @@
 // a.cols().
 #pragma once
 
+#include <complex>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "rsvd_c.h"
@@ -22,19 +26,24 @@
 namespace rlftn_b200 {
 
 using Index = std::int64_t;
+using Complex = std::complex<double>;
 
-struct MatrixR {
+template <class Scalar>
+struct Matrix {
   Index r = 0, c = 0;
-  std::vector<double> v;
-  MatrixR() = default;
-  MatrixR(Index rows, Index cols) : r(rows), c(cols), v(static_cast<size_t>(rows * cols), 0.0) {}
+  std::vector<Scalar> v;
+  using value_type = Scalar;
+  Matrix() = default;
+  Matrix(Index rows, Index cols) : r(rows), c(cols), v(static_cast<size_t>(rows * cols), Scalar(0)) {}
   Index rows() const { return r; }
   Index cols() const { return c; }
-  double* data() { return v.data(); }
-  const double* data() const { return v.data(); }
-  double& operator()(Index i, Index j) { return v[static_cast<size_t>(i + j * r)]; }
-  double operator()(Index i, Index j) const { return v[static_cast<size_t>(i + j * r)]; }
+  Scalar* data() { return v.data(); }
+  const Scalar* data() const { return v.data(); }
+  Scalar& operator()(Index i, Index j) { return v[static_cast<size_t>(i + j * r)]; }
+  Scalar operator()(Index i, Index j) const { return v[static_cast<size_t>(i + j * r)]; }
 };
+using MatrixR = Matrix<double>;
+using MatrixC = Matrix<Complex>;
 
 struct RsvdParams {
   Index rank = 0;
@@ -43,10 +52,11 @@ struct RsvdParams {
   std::uint64_t seed = 0;
 };
 
+template <class Scalar>
 struct TruncatedFactorization {
-  MatrixR left;                // m x r
+  Matrix<Scalar> left;         // m x r
   std::vector<double> sigma;   // r
-  MatrixR right_adj;           // r x n
+  Matrix<Scalar> right_adj;    // r x n
   double discarded_weight = 0.0;
   bool discarded_exact = true;
   Index rank() const { return static_cast<Index>(sigma.size()); }
@@ -96,50 +106,96 @@ inline Engine& default_engine() {
   return e;
 }
 
-// rlftn::rsvd<double> (factorize.cpp:76-95) on the GPU.
-inline TruncatedFactorization rsvd(const MatrixR& a, const RsvdParams& p,
-                                   Engine& e = default_engine()) {
+namespace detail {
+template <class Scalar>
+const double* dp(const Scalar* p) {
+  return reinterpret_cast<const double*>(p);
+}
+template <class Scalar>
+double* dp(Scalar* p) {
+  return reinterpret_cast<double*>(p);
+}
+template <class Scalar>
+constexpr bool is_complex() {
+  return std::is_same_v<Scalar, Complex>;
+}
+// Copy the leading r columns / rows of the engine's k-wide outputs.
+template <class Scalar>
+TruncatedFactorization<Scalar> trim(const Matrix<Scalar>& u, const std::vector<double>& s,
+                                    const Matrix<Scalar>& vt, Index r, double dw, bool exact) {
+  TruncatedFactorization<Scalar> f;
+  f.left = Matrix<Scalar>(u.rows(), r);
+  for (Index j = 0; j < r; ++j)
+    for (Index i = 0; i < u.rows(); ++i) f.left(i, j) = u(i, j);
+  f.sigma.assign(s.begin(), s.begin() + r);
+  f.right_adj = Matrix<Scalar>(r, vt.cols());
+  for (Index j = 0; j < vt.cols(); ++j)
+    for (Index i = 0; i < r; ++i) f.right_adj(i, j) = vt(i, j);
+  f.discarded_weight = dw;
+  f.discarded_exact = exact;
+  return f;
+}
+}  // namespace detail
+
+// rlftn::rsvd<Scalar> (factorize.cpp:76-95) on the GPU.
+template <class Scalar>
+TruncatedFactorization<Scalar> rsvd(const Matrix<Scalar>& a, const RsvdParams& p,
+                                    Engine& e = default_engine()) {
+  static_assert(std::is_same_v<Scalar, double> || detail::is_complex<Scalar>());
   const Index m = a.rows(), n = a.cols();
   const Index k = p.rank > 0 ? p.rank : 1;
-  MatrixR u(m, k), vt(k, n);
+  Matrix<Scalar> u(m, k), vt(k, n);
   std::vector<double> s(static_cast<size_t>(k));
   std::int64_t r = 0;
   double dw = 0.0;
-  e.check(rsvd_f64(e.raw(), a.data(), m, n, m > 0 ? m : 1, p.rank, p.oversample, p.power, p.seed,
-                   u.data(), m > 0 ? m : 1, s.data(), vt.data(), k, &r, &dw, RSVD_PTR_HOST));
-  TruncatedFactorization f;
-  f.left = MatrixR(m, r);
-  for (Index j = 0; j < r; ++j)
-    for (Index i = 0; i < m; ++i) f.left(i, j) = u(i, j);
-  f.sigma.assign(s.begin(), s.begin() + r);
-  f.right_adj = MatrixR(r, n);
-  for (Index j = 0; j < n; ++j)
-    for (Index i = 0; i < r; ++i) f.right_adj(i, j) = vt(i, j);
-  f.discarded_weight = dw;
-  f.discarded_exact = false;
-  return f;
+  auto fn = detail::is_complex<Scalar>() ? rsvd_z128 : rsvd_f64;
+  e.check(fn(e.raw(), detail::dp(a.data()), m, n, m > 0 ? m : 1, p.rank, p.oversample, p.power,
+             p.seed, detail::dp(u.data()), m > 0 ? m : 1, s.data(), detail::dp(vt.data()), k, &r,
+             &dw, RSVD_PTR_HOST));
+  return detail::trim(u, s, vt, r, dw, false);
 }
 
-// rlftn::randomized_range<double> (factorize.cpp:52-74).
-inline MatrixR randomized_range(const MatrixR& a, Index ell, int power, std::uint64_t seed,
+// rlftn::tsvd<Scalar> (factorize.cpp:42-50): full thin SVD truncated to chi.
+template <class Scalar>
+TruncatedFactorization<Scalar> tsvd(const Matrix<Scalar>& a, Index chi,
+                                    Engine& e = default_engine()) {
+  static_assert(std::is_same_v<Scalar, double> || detail::is_complex<Scalar>());
+  const Index m = a.rows(), n = a.cols();
+  Index k = chi < (m < n ? m : n) ? chi : (m < n ? m : n);
+  if (k < 1) k = 1;
+  Matrix<Scalar> u(m, k), vt(k, n);
+  std::vector<double> s(static_cast<size_t>(k));
+  std::int64_t r = 0;
+  double dw = 0.0;
+  auto fn = detail::is_complex<Scalar>() ? rsvd_tsvd_z128 : rsvd_tsvd_f64;
+  e.check(fn(e.raw(), detail::dp(a.data()), m, n, m > 0 ? m : 1, chi, detail::dp(u.data()),
+             m > 0 ? m : 1, s.data(), detail::dp(vt.data()), k, &r, &dw, RSVD_PTR_HOST));
+  return detail::trim(u, s, vt, r, dw, true);
+}
+
+// rlftn::randomized_range<Scalar> (factorize.cpp:52-74).
+template <class Scalar>
+Matrix<Scalar> randomized_range(const Matrix<Scalar>& a, Index ell, int power, std::uint64_t seed,
                                 Engine& e = default_engine()) {
-  MatrixR q(a.rows(), ell > 0 ? ell : 0);
-  e.check(rsvd_randomized_range_f64(e.raw(), a.data(), a.rows(), a.cols(),
-                                    a.rows() > 0 ? a.rows() : 1, ell, power, seed, q.data(),
-                                    a.rows() > 0 ? a.rows() : 1, RSVD_PTR_HOST));
+  Matrix<Scalar> q(a.rows(), ell > 0 ? ell : 0);
+  auto fn = detail::is_complex<Scalar>() ? rsvd_randomized_range_z128 : rsvd_randomized_range_f64;
+  e.check(fn(e.raw(), detail::dp(a.data()), a.rows(), a.cols(), a.rows() > 0 ? a.rows() : 1, ell,
+             power, seed, detail::dp(q.data()), a.rows() > 0 ? a.rows() : 1, RSVD_PTR_HOST));
   return q;
 }
 
 // rlftn::reconstruction_error(a, f, ErrorNorm::frobenius) (factorize.cpp:97-104).
-inline double reconstruction_error(const MatrixR& a, const TruncatedFactorization& f,
-                                   Engine& e = default_engine()) {
+template <class Scalar>
+double reconstruction_error(const Matrix<Scalar>& a, const TruncatedFactorization<Scalar>& f,
+                            Engine& e = default_engine()) {
   double out = 0.0;
   const Index r = f.rank();
-  e.check(rsvd_reconstruction_error_f64(e.raw(), a.data(), a.rows(), a.cols(), a.rows(),
-                                        r ? f.left.data() : nullptr, a.rows(),
-                                        r ? f.sigma.data() : nullptr,
-                                        r ? f.right_adj.data() : nullptr, r > 0 ? r : 1, r,
-                                        &out, RSVD_PTR_HOST));
+  auto fn = detail::is_complex<Scalar>() ? rsvd_reconstruction_error_z128
+                                         : rsvd_reconstruction_error_f64;
+  e.check(fn(e.raw(), detail::dp(a.data()), a.rows(), a.cols(), a.rows(),
+             r ? detail::dp(f.left.data()) : nullptr, a.rows(), r ? f.sigma.data() : nullptr,
+             r ? detail::dp(f.right_adj.data()) : nullptr, r > 0 ? r : 1, r, &out,
+             RSVD_PTR_HOST));
   return out;
 }
 

@@ -31,6 +31,35 @@ int main() {
   } catch (const std::invalid_argument& e) {
     if (std::string(e.what()) != "rsvd: oversample must be >= rank") { std::printf("FAIL msg %s\n", e.what()); return 1; }
   }
-  std::printf("shim ok: sigma0=%.3f rank=%lld err^2=%.6e\n", f.sigma[0], (long long)f.rank(), err * err);
+  // tsvd keeps the leading values exactly (test_factorize.cpp:33-55).
+  MatrixR d(3, 3);
+  d(0, 0) = 3.0, d(1, 1) = 2.0, d(2, 2) = 1.0;
+  const auto t = tsvd(d, 2);
+  if (t.rank() != 2 || std::abs(t.sigma[0] - 3.0) > 1e-14 || std::abs(t.sigma[1] - 2.0) > 1e-14 ||
+      std::abs(t.discarded_weight - 1.0) > 1e-14 || !t.discarded_exact) {
+    std::printf("FAIL tsvd\n");
+    return 1;
+  }
+  // Complex instantiation (factorize.cpp:106-118): a phase-twisted diagonal.
+  MatrixC z(24, 20);
+  for (Index i = 0; i < 20; ++i)
+    z(i, i) = std::polar(std::pow(0.5, static_cast<double>(i)), 0.3 * static_cast<double>(i));
+  const auto fz = rsvd(z, RsvdParams{6, 12, 2, 3});
+  const auto tz = tsvd(z, 6);
+  for (Index k = 0; k < 6; ++k) {
+    const double want = std::pow(0.5, static_cast<double>(k));
+    if (std::abs(fz.sigma[k] - want) > 1e-12 * want || std::abs(tz.sigma[k] - want) > 1e-12 * want) {
+      std::printf("FAIL complex sigma %lld\n", (long long)k);
+      return 1;
+    }
+  }
+  double ztail = 0.0;
+  for (Index k = 6; k < 20; ++k) ztail += std::pow(0.25, static_cast<double>(k));
+  const double zerr = reconstruction_error(z, tz);
+  if (std::abs(zerr * zerr - ztail) > 1e-10 * ztail) { std::printf("FAIL complex err\n"); return 1; }
+  const auto q = randomized_range(z, 8, 1, 5);
+  if (q.rows() != 24 || q.cols() != 8) { std::printf("FAIL range shape\n"); return 1; }
+  std::printf("shim ok: sigma0=%.3f rank=%lld err^2=%.6e complex err^2=%.6e\n", f.sigma[0],
+              (long long)f.rank(), err * err, zerr * zerr);
   return 0;
 }
