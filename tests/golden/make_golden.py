@@ -7,6 +7,8 @@
                     /root/reference/proj/include/rlftn/rng.hpp).
   rsvd_small.npz  : small rsvd/tsvd known-answer cases computed by the oracle
                     restatement (oracle/liboracle.so) on CounterRng inputs.
+  zrsvd_small.npz : the same cases for the complex instantiation
+                    (rsvd/tsvd<std::complex<double>>, complex CounterRng inputs).
 """
 import json
 import os
@@ -64,6 +66,24 @@ def build_case(i, rows, cols, spec):
     return matrix_with_spectrum(seed, rows, cols, s)
 
 
+def zbuild_case(i, rows, cols, spec):
+    """Complex counterpart of build_case: Haar complex isometries (complex
+    CounterRng fill + zgeqrf/zungqr, phase-fixed) or a complex Gaussian."""
+    seed = oracle.derive_seed(0x2601DE5, i)
+    if spec is None:
+        return oracle.zgaussian_matrix(seed, rows, cols)
+    if spec[0] == "fam":
+        s = spectrum_family(spec[1], spec[2])
+    elif spec[0] == "exp":
+        s = np.exp(-np.arange(spec[2]) / spec[1])
+    else:
+        s = np.asarray(spec[1])
+    r = len(s)
+    u = oracle.zhaar(oracle.derive_seed(seed, 1), rows, r)
+    v = oracle.zhaar(oracle.derive_seed(seed, 2), cols, r)
+    return np.asfortranarray((u * s[None, :]) @ v.conj().T)
+
+
 def main():
     oracle.build()
     kat = oracle.reference_rng_kat(64, 257)
@@ -88,6 +108,22 @@ def main():
         out[f"{name}/omega"] = oracle.gaussian_matrix(seed, cols, ell)
     np.savez_compressed(os.path.join(HERE, "rsvd_small.npz"), **out)
     print("wrote", len(CASES), "cases")
+    zout = {}
+    for i, (name, rows, cols, spec, k, ell, q, seed) in enumerate(CASES):
+        a = zbuild_case(i, rows, cols, spec)
+        U, S, Vt, dw = oracle.zrsvd(a, k, ell, q, seed)
+        Ut, St, Vtt, dwt = oracle.ztsvd(a, k)
+        zout[f"{name}/a"] = a
+        zout[f"{name}/params"] = np.array([k, ell, q, seed], dtype=np.uint64)
+        zout[f"{name}/U"] = U
+        zout[f"{name}/S"] = S
+        zout[f"{name}/Vt"] = Vt
+        zout[f"{name}/dw"] = np.array([dw])
+        zout[f"{name}/S_tsvd"] = St
+        zout[f"{name}/dw_tsvd"] = np.array([dwt])
+        zout[f"{name}/omega"] = oracle.zgaussian_matrix(seed, cols, ell)
+    np.savez_compressed(os.path.join(HERE, "zrsvd_small.npz"), **zout)
+    print("wrote", len(CASES), "complex cases")
 
 
 if __name__ == "__main__":

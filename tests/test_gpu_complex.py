@@ -236,3 +236,22 @@ def test_complex_zero_matrix(cuda):
     f = rsvd(a, RsvdParams(4, 8, 2, 1))
     assert f.rank() == 0
     assert f.discarded_weight == 0.0
+
+
+def test_complex_golden_fixture(cuda):
+    """The committed complex fixture (tests/golden/zrsvd_small.npz): GPU rsvd
+    and tsvd against the oracle's outputs stored there."""
+    import os
+
+    from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "zrsvd_small.npz"))
+    for name in sorted({k.split("/")[0] for k in g.files}):
+        a = g[f"{name}/a"]
+        k, ell, q, seed = (int(x) for x in g[f"{name}/params"])
+        f = rsvd(a, RsvdParams(k, ell, q, seed))
+        ref = (g[f"{name}/U"], g[f"{name}/S"], g[f"{name}/Vt"], float(g[f"{name}/dw"][0]))
+        check_against(a, f, ref, name, dw_rel=1e-8)
+        ft = tsvd(a, k)
+        St = g[f"{name}/S_tsvd"]
+        assert np.max(np.abs(np.asarray(ft.sigma) - St)) <= 1e-13 * St[0], name

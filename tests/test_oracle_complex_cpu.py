@@ -73,3 +73,20 @@ def test_complex_invalid_arguments(oracle_mod):
         oracle_mod.zrsvd(a, 2, 1, 1, 0)
     with pytest.raises(oracle_mod.OracleInvalid, match="need 1 <= ell"):
         oracle_mod.zrsvd(a, 2, 4, 1, 0)
+
+
+def test_complex_oracle_reproduces_committed_golden(oracle_mod):
+    """tests/golden/zrsvd_small.npz (made by tests/golden/make_golden.py) is
+    reproduced by the oracle here: the fixture and the restatement agree."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "zrsvd_small.npz"))
+    names = sorted({k.split("/")[0] for k in g.files})
+    assert len(names) == 9
+    for name in names:
+        a = g[f"{name}/a"]
+        k, ell, q, seed = (int(x) for x in g[f"{name}/params"])
+        assert np.array_equal(oracle_mod.zgaussian_matrix(seed, a.shape[1], ell), g[f"{name}/omega"])
+        U, S, Vt, dw = oracle_mod.zrsvd(a, k, ell, q, seed)
+        np.testing.assert_allclose(S, g[f"{name}/S"], rtol=1e-12)
+        assert dw == pytest.approx(float(g[f"{name}/dw"][0]), rel=1e-9, abs=1e-30)
+        St = oracle_mod.ztsvd(a, k)[1]
+        np.testing.assert_allclose(St, g[f"{name}/S_tsvd"], rtol=1e-12, atol=1e-15)
