@@ -104,10 +104,12 @@ class SymmetricMPS:
 
 
 def random_product_state(site: SiteStructure, length: int, seed: int,
-                         device="cuda") -> SymmetricMPS:
+                         device="cuda", dtype=None) -> SymmetricMPS:
     """mps.cpp:62-108: uniform basis states from
     CounterRng(derive_seed(seed, initial_state)), the last site closing the
-    total parity to even."""
+    total parity to even.  ``dtype`` torch.complex128 gives the
+    SymmetricMPS<Complex> instantiation (mps.cpp:551-555): complex Gammas (the
+    bond updates then run the complex factorization), real lambdas."""
     torch = _torch()
     if length < 2:
         raise InvalidArgument("random_product_state: need at least two sites")
@@ -132,6 +134,7 @@ def random_product_state(site: SiteStructure, length: int, seed: int,
     for j in range(length):
         cum[j + 1] = cum[j] ^ site.charges[basis[j]]
     f64 = dict(dtype=torch.float64, device=device)
+    gdt = dict(dtype=dtype or torch.float64, device=device)
     lambdas = []
     for b in range(length + 1):
         pair = [torch.zeros(0, **f64), torch.zeros(0, **f64)]
@@ -145,7 +148,7 @@ def random_product_state(site: SiteStructure, length: int, seed: int,
             for a in (0, 1):
                 rows = 1 if a == cum[j] else 0
                 cols = 1 if (a ^ site.charges[m]) == cum[j + 1] else 0
-                pair.append(torch.zeros(rows, cols, **f64))
+                pair.append(torch.zeros(rows, cols, **gdt))
             site_t.append(pair)
         site_t[basis[j]][cum[j]][0, 0] = 1.0
         gammas.append(site_t)
@@ -175,7 +178,8 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
     lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
     g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
     dev = lam_l[0].device
-    f64 = dict(dtype=torch.float64, device=dev)
+    # theta carries the Gammas' scalar type (real or complex MPS); gates are real.
+    f64 = dict(dtype=g1[0][0].dtype, device=dev)
     nl = [lam_l[0].numel(), lam_l[1].numel()]
     nm = [lam_m[0].numel(), lam_m[1].numel()]
     nr = [lam_r[0].numel(), lam_r[1].numel()]
@@ -278,7 +282,8 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
                 thetap[sp] = r @ y
         plan.lifted = True
     plan.thetap = thetap
-    plan.total_sq = float(sum((tp * tp).sum() for tp in thetap))
+    plan.total_sq = float(sum((tp.abs() ** 2).sum() if tp.is_complex() else (tp * tp).sum()
+                              for tp in thetap))
     if not (plan.total_sq > 0.0):
         raise RuntimeError("apply_gate: evolved wavefunction vanished")
     return plan

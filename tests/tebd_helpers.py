@@ -18,11 +18,12 @@ def mps_to_dense(gammas, lambdas, charges):
     n = len(gammas)
     lam = [[_np(x) for x in pair] for pair in lambdas]
     dims = [(len(l[0]), len(l[1])) for l in lam]
+    cplx = any(np.iscomplexobj(_np(x)) for site in gammas for pair in site for x in pair)
 
     def full_gamma(j, m):
         r0, r1 = dims[j]
         c0, c1 = dims[j + 1]
-        g = np.zeros((r0 + r1, c0 + c1))
+        g = np.zeros((r0 + r1, c0 + c1), dtype=np.complex128 if cplx else np.float64)
         for a in (0, 1):
             b = _np(gammas[j][m][a])
             ro = 0 if a == 0 else r0

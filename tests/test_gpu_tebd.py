@@ -91,6 +91,43 @@ def test_matches_dense_evolution(cuda, model, seed):  # test_mps.cpp:42-79, 128-
     psi.validate()
 
 
+@pytest.mark.parametrize("model,seed,form", [(M.ChainModel(4, 0.5, 1.0), 11, "block"),
+                                             (M.CylinderModel(3, 2, 3.0), 21, "block"),
+                                             (M.ChainModel(4, 0.5, 1.0), 7, "product")])
+def test_complex_mps_matches_dense_evolution(cuda, model, seed, form):
+    """check_against_dense_evolution<Complex> (test_mps.cpp:128-137): a
+    SymmetricMPS<Complex> evolved by the same real gates; every bond update runs
+    the complex factorization (complex Gammas, arbitrary singular-vector
+    phases), the state must track the dense evolution."""
+    import torch
+
+    from paper_1710_01463_b200 import BlockMethod, tebd
+
+    st = M.parity_structure(model)
+    n = model.length
+    psi = tebd.random_product_state(st, n, seed, device=cuda, dtype=torch.complex128)
+    ref = mps_to_dense(*psi.to_numpy(), st.charges)
+    assert np.iscomplexobj(ref)
+    bonds = M.bond_hamiltonians(model)
+    gf = M.GateForm.block if form == "block" else M.GateForm.product
+    dts = [0.2, 0.35, 0.1]
+    gi = 0
+    for ps in range(3):
+        for b in range(ps % 2, n - 1, 2):
+            gate = M.build_gate(bonds[b], st.charges, dts[gi % 3], gf)
+            gi += 1
+            meth = BlockMethod.deterministic() if gi % 2 else BlockMethod.randomized(4, 99)
+            tebd.apply_gate(psi, b, gate, 256, meth, _req(256))
+            ref = apply_two_site(ref, gate.block, b, n, st.dim)
+            ref /= np.linalg.norm(ref)
+            got = mps_to_dense(*psi.to_numpy(), st.charges)
+            assert abs(np.vdot(ref, got)) / np.linalg.norm(got) == pytest.approx(1.0, abs=1e-10)
+    assert psi.gammas[0][0][0].dtype == torch.complex128
+    psi.validate()
+    tebd.canonicalize(psi)
+    assert tebd.lambda_norm_error(psi) < 1e-12
+
+
 def test_block_and_product_forms_agree(cuda):  # test_mps.cpp:139-161
     from paper_1710_01463_b200 import BlockMethod, tebd
 
