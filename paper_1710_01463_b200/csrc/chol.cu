@@ -240,6 +240,29 @@ __global__ void __launch_bounds__(kCholThreads)
         if (!pivot) {  // plain Cholesky: keep the order, still test the pivot floor
           ix = j;
           v = d[j] - work[j];
+        } else if (pivot == 2) {
+          // Pair pivoting (realified complex Gram, columns 2a / 2a+1 = Re / Im
+          // of complex column a): even positions take the best even original
+          // column, odd positions its partner, so P is the realification of a
+          // complex permutation and R stays the realified complex factor.
+          int want = -1;
+          if (j & 1) want = pos2orig[j - 1] ^ 1;
+          v = -DBL_MAX;
+          ix = 0x7fffffff;
+          for (int x = j + lane; x < ell; x += 32) {
+            const int o = pos2orig[x];
+            const bool ok = (j & 1) ? (o == want) : ((o & 1) == 0);
+            if (!ok) continue;
+            const double dv = d[x] - work[x];
+            if (dv > v || (dv == v && x < ix)) v = dv, ix = x;
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, ix, off);
+            if (ov > v || (ov == v && oi < ix)) v = ov, ix = oi;
+          }
+          if (ix == 0x7fffffff) ix = j, v = -DBL_MAX;  // no candidate: stop
         }
         const bool stop = !(v > thresh);
         if (!stop && ix != j) {  // logical swap of positions j and ix
@@ -272,6 +295,12 @@ __global__ void __launch_bounds__(kCholThreads)
       if (s_stop) {
         jdone = jj;
         r = j;
+        if (pivot == 2 && (j & 1)) {  // drop the unpaired half: rank stays even
+          jdone = jj - 1;
+          r = j - 1;
+          for (int e = tid; e < ellp; e += blockDim.x) Rorig[(j - 1) + static_cast<int64_t>(e) * ld] = 0.0;
+          __syncthreads();
+        }
         break;
       }
       const double rjj = sqrt(s_piv);
@@ -1082,7 +1111,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
                                  static_cast<int>(bytes)));
   pchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
       G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau,
-      pivot ? 1 : 0, opts ? opts->mask : nullptr);
+      pivot ? (opts && opts->pairs ? 2 : 1) : 0, opts ? opts->mask : nullptr);
   RSVD_LAUNCH("pchol_kernel");
 }
 

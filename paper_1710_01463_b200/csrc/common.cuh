@@ -108,6 +108,7 @@ struct CholOpts {
   int* ill_out = nullptr;
   const double* Gsrc = nullptr;
   double shift_coef = 0.0;
+  bool pairs = false;  // pivoted kernel: pivot complex columns (2a, 2a+1) together
 };
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,

@@ -407,7 +407,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
       // Jacobi) measured no fewer sweeps: RSVD_BT_PIVOT=1 / RSVD_PIVOT_ALL=1.
       static const bool bt_pivot = std::getenv("RSVD_BT_PIVOT") != nullptr;
-      pivot = (pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2();
+      pivot = ((pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2()) && !cplx;
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
       if (pass == 0) {  // shifted retry of the items that stopped short of full rank
         CholOpts o;
@@ -437,6 +437,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
         // factorization would stop at the first and drop every later column.
         CholOpts o;
         o.mask = B.ill;
+        o.pairs = cplx;
         launch_pchol(B.G, B.T, Rt ? B.Rf2 : nullptr, B.cscratch, B.rank2, B.perm, s.ell, lp,
                      kPivotTau, true, b, st, &o);
       }
