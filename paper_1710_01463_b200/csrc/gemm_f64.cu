@@ -401,8 +401,12 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   Choice c = choose(M, N, K, batch);
   // Symmetric Gram of a 96-multiple width: 96 x 96 TMA tiles (the 128 x 96
   // tile leaves a partial row tile and computes ~40% more than the upper half).
+  // (Only when the TMA path can take the operands: an odd row count, e.g. a
+  // tsvd of a 37 x 53 block, has an odd leading dimension.)
+  const bool tma_operands = aligned16(A.base) && aligned16(B.base) && A.ld % 2 == 0 &&
+                            B.ld % 2 == 0 && (batch == 1 || (A.stride % 2 == 0 && B.stride % 2 == 0));
   const bool sq96 = opt.c_upper && trans_a && M == N && M % 96 == 0 && !opt.colmapA &&
-                    !std::getenv("RSVD_NO_GRAM96");
+                    tma_operands && !std::getenv("RSVD_NO_GRAM96");
   if (sq96) {
     const int64_t t = M / 96;
     const int64_t tiles = t * (t + 1) / 2 * batch;
