@@ -277,3 +277,63 @@ def test_gram96_with_odd_rows(cuda, oracle_mod, dtype):
         ref = oracle_mod.ztsvd(a, p)
     f = tsvd(a, p)
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (9, 1), (5, 5), (3, 40)])
+def test_complex_tiny_shapes(cuda, oracle_mod, shape):
+    """Degenerate shapes: rank 1 rows/columns, l = min(m, n) (Q spans everything)."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
+
+    m, n = shape
+    rng = np.random.default_rng(m * 100 + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)))
+    p = min(m, n)
+    f = rsvd(a, RsvdParams(p, p, 2, 4))
+    ref = oracle_mod.zrsvd(a, p, p, 2, 4)
+    check_against(a, f, ref, f"rsvd {shape}")
+    t = tsvd(a, p + 3)  # chi above min(m, n): clipped, exact
+    St = oracle_mod.ztsvd(a, p + 3)[1]
+    assert rel_sigma_err(t.sigma, St) < SIG_TOL
+    assert t.discarded_weight == pytest.approx(0.0, abs=1e-24)
+
+
+@pytest.mark.parametrize("scale", [1e-300, 1e300, 2.0 ** -1000])
+def test_complex_extreme_magnitudes(cuda, oracle_mod, scale):
+    """Exact power-of-two range scaling also covers the complex path: results
+    equal the unscaled factorization times the scale (relative 1e-12)."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
+
+    a = zmatrix_with_spectrum(oracle_mod, 66, 60, 44, np.exp(-np.arange(44) / 6.0))
+    f1 = rsvd(a, RsvdParams(8, 16, 2, 5))
+    fs = rsvd(a * scale, RsvdParams(8, 16, 2, 5))
+    assert fs.rank() == f1.rank()
+    np.testing.assert_allclose(np.asarray(fs.sigma) / scale, f1.sigma, rtol=1e-12)
+    assert np.all(np.isfinite(np.asarray(fs.left)))
+    t1 = tsvd(a, 8)
+    ts = tsvd(a * scale, 8)
+    np.testing.assert_allclose(np.asarray(ts.sigma) / scale, t1.sigma, rtol=1e-12)
+
+
+def test_complex_real_valued_input_matches_real_path(cuda, oracle_mod):
+    """A complex matrix with zero imaginary part has the real matrix's singular
+    values: the complex instantiation agrees with the real one."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
+    from tests.helpers import matrix_with_spectrum
+
+    ar = matrix_with_spectrum(oracle_mod, 31, 80, 64, np.exp(-np.arange(64) / 9.0))
+    az = ar.astype(np.complex128)
+    fr, fz = rsvd(ar, RsvdParams(12, 24, 2, 3)), rsvd(az, RsvdParams(12, 24, 2, 3))
+    # Omega differs (complex fill), so compare through the exact values
+    np.testing.assert_allclose(np.asarray(tsvd(az, 12).sigma), np.asarray(tsvd(ar, 12).sigma),
+                               rtol=1e-12)
+    np.testing.assert_allclose(np.asarray(fz.sigma), np.exp(-np.arange(12) / 9.0), rtol=1e-9)
+    np.testing.assert_allclose(np.asarray(fr.sigma), np.exp(-np.arange(12) / 9.0), rtol=1e-9)
+
+
+def test_complex_empty_matrix_errors(cuda):
+    from paper_1710_01463_b200 import InvalidArgument, RsvdParams, rsvd, tsvd
+
+    with pytest.raises(InvalidArgument, match="rsvd: empty matrix"):
+        rsvd(np.zeros((0, 4), dtype=np.complex128), RsvdParams(1, 0, 1, 0))
+    with pytest.raises(InvalidArgument, match="tsvd: empty matrix"):
+        tsvd(np.zeros((3, 0), dtype=np.complex128), 1)
