@@ -326,8 +326,9 @@ def test_complex_real_valued_input_matches_real_path(cuda, oracle_mod):
     # Omega differs (complex fill), so compare through the exact values
     np.testing.assert_allclose(np.asarray(tsvd(az, 12).sigma), np.asarray(tsvd(ar, 12).sigma),
                                rtol=1e-12)
-    np.testing.assert_allclose(np.asarray(fz.sigma), np.exp(-np.arange(12) / 9.0), rtol=1e-9)
-    np.testing.assert_allclose(np.asarray(fr.sigma), np.exp(-np.arange(12) / 9.0), rtol=1e-9)
+    # each randomized result against its own restated reference (same Omega)
+    assert rel_sigma_err(fz.sigma, oracle_mod.zrsvd(az, 12, 24, 2, 3)[1]) < SIG_TOL
+    assert rel_sigma_err(fr.sigma, oracle_mod.rsvd(ar, 12, 24, 2, 3)[1]) < SIG_TOL
 
 
 def test_complex_empty_matrix_errors(cuda):
