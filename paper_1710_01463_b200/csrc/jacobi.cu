@@ -1771,138 +1771,6 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
     launch_blocked_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
 }
 
-// H-in-shared-memory one-sided Jacobi for many small items (TEBD-style
-// batches, C2: 256 x l = 138): one CTA per item keeps the whole l x l H in
-// shared memory (ld = 32 R rows) for the entire run, so the pair dot products
-// and H updates never leave the SM; J stays in global memory (L2 resident for
-// the batch) and each warp prefetches its pair's J columns before the dot
-// products, so the J round trip overlaps the reduction.  Round-robin
-// ordering (every pair once per sweep, l/2 disjoint pairs per step, 32 warps),
-// column norms recomputed from the columns at every pair (no drift),
-// dgesvj's rotation test |h_p^T h_q| > sqrt(l) eps ||h_p|| ||h_q||, stop after
-// a sweep without rotations or whose largest rotated ratio was < 1e-9.
-template <int R>
-__global__ void __launch_bounds__(1024) jacobi_hsmem_kernel(double* __restrict__ H,
-                                                            double* __restrict__ J, int ell,
-                                                            int ellp, int max_sweeps,
-                                                            int* __restrict__ sweeps_out) {
-  extern __shared__ double hs[];
-  constexpr int LD = 32 * R;
-  const int64_t b = blockIdx.x;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  double* Hb = H + b * sq;
-  double* Jb = J + b * sq;
-  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  for (int e = tid; e < LD * ell; e += nt) {
-    const int r = e % LD, c = e / LD;
-    hs[e] = r < ell ? Hb[r + static_cast<int64_t>(c) * ellp] : 0.0;
-  }
-  for (int64_t e = tid; e < sq; e += nt) Jb[e] = (e % ellp == e / ellp) ? 1.0 : 0.0;
-  __shared__ unsigned long long s_max;
-  __shared__ int s_rot;
-  if (tid == 0) s_max = 0ull, s_rot = 0;
-  __syncthreads();
-  const int le = ell + (ell & 1);
-  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
-  int sweep = 0;
-  for (; sweep < max_sweeps && ell > 1; ++sweep) {
-    for (int step = 0; step < le - 1; ++step) {
-      for (int k = warp; k < le / 2; k += nw) {
-        const int pp = k == 0 ? 0 : ((k - 1 + step) % (le - 1)) + 1;
-        const int qq = ((le - 2 - k + step) % (le - 1)) + 1;
-        if (pp >= ell || qq >= ell) continue;
-        const int pc = min(pp, qq), qc = max(pp, qq);
-        double* jp = Jb + static_cast<int64_t>(pc) * ellp;
-        double* jq = Jb + static_cast<int64_t>(qc) * ellp;
-        double jx[R], jy[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {  // J prefetch (consumed only if the pair rotates)
-          const int i = lane + 32 * r;
-          jx[r] = i < ell ? __ldcg(jp + i) : 0.0;
-          jy[r] = i < ell ? __ldcg(jq + i) : 0.0;
-        }
-        double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double xv = hs[lane + 32 * r + pc * LD];
-          const double yv = hs[lane + 32 * r + qc * LD];
-          al = fma(xv, xv, al);
-          be = fma(yv, yv, be);
-          ga = fma(xv, yv, ga);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        }
-        const double nrm = sqrt(al) * sqrt(be);
-        if (!(fabs(ga) > tol * nrm)) continue;
-        if (lane == 0) {
-          atomicMax(&s_max, static_cast<unsigned long long>(__double_as_longlong(fabs(ga) / nrm)));
-          s_rot = 1;
-        }
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = lane + 32 * r;
-          const double xv = hs[i + pc * LD], yv = hs[i + qc * LD];  // re-read (register budget)
-          hs[i + pc * LD] = c * xv - sn * yv;
-          hs[i + qc * LD] = sn * xv + c * yv;
-          if (i < ell) {
-            jp[i] = c * jx[r] - sn * jy[r];
-            jq[i] = sn * jx[r] + c * jy[r];
-          }
-        }
-      }
-      __syncthreads();
-    }
-    const bool any = s_rot != 0;
-    const double mx = __longlong_as_double(static_cast<long long>(s_max));
-    __syncthreads();
-    if (tid == 0) s_max = 0ull, s_rot = 0;
-    __syncthreads();
-    if (!any || mx < 1e-9) {
-      ++sweep;
-      break;
-    }
-  }
-  for (int64_t e = tid; e < sq; e += nt) {
-    const int r = static_cast<int>(e % ellp), c = static_cast<int>(e / ellp);
-    Hb[e] = (r < ell && c < ell) ? hs[r + c * LD] : 0.0;
-  }
-  if (tid == 0 && sweeps_out) sweeps_out[b] = sweep;
-}
-
-template <int R>
-void launch_hsmem_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                    int64_t batch, cudaStream_t st) {
-  const int bytes = static_cast<int>(32 * R * ell * sizeof(double));
-  RSVD_CUDA(cudaFuncSetAttribute(jacobi_hsmem_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 bytes));
-  jacobi_hsmem_kernel<R><<<static_cast<unsigned>(batch), 1024, bytes, st>>>(
-      H, J, static_cast<int>(ell), static_cast<int>(ellp), max_sweeps, sweeps);
-  RSVD_LAUNCH("jacobi_hsmem_kernel");
-}
-
-// Many small items: H in shared memory (l <= 160, >= SMs/2 items).
-bool launch_hsmem(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                  int64_t batch, cudaStream_t st) {
-  static const bool off = std::getenv("RSVD_NO_JACOBI_HSMEM") != nullptr;
-  if (off || ell > 160 || ell < 2 || batch < kNumSMs / 2) return false;
-  const int R = static_cast<int>((ell + 31) / 32);
-  switch (R) {
-    case 1: launch_hsmem_t<1>(H, J, ell, ellp, max_sweeps, sweeps, batch, st); return true;
-    case 2: launch_hsmem_t<2>(H, J, ell, ellp, max_sweeps, sweeps, batch, st); return true;
-    case 3: launch_hsmem_t<3>(H, J, ell, ellp, max_sweeps, sweeps, batch, st); return true;
-    case 4: launch_hsmem_t<4>(H, J, ell, ellp, max_sweeps, sweeps, batch, st); return true;
-    case 5: launch_hsmem_t<5>(H, J, ell, ellp, max_sweeps, sweeps, batch, st); return true;
-    default: return false;
-  }
-}
-
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st) {
   const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
@@ -1913,7 +1781,6 @@ void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_swee
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
   }
-  if (launch_hsmem(H, J, ell, ellp, max_sweeps, sweeps, batch, st)) return;
   // The whole-problem-in-shared-memory kernel tracks column norms across the
   // whole run; on rank-deficient, widely graded inputs (TEBD sector blocks,
   // tests/golden/theta_rankdef_24x21.npy) its small values drifted by ~1e-10
