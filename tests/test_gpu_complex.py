@@ -338,3 +338,26 @@ def test_complex_empty_matrix_errors(cuda):
         rsvd(np.zeros((0, 4), dtype=np.complex128), RsvdParams(1, 0, 1, 0))
     with pytest.raises(InvalidArgument, match="tsvd: empty matrix"):
         tsvd(np.zeros((3, 0), dtype=np.complex128), 1)
+
+
+@pytest.mark.parametrize("case", [(700, 400, 200, 330, 1), (520, 480, 300, 480, 0)],
+                         ids=["rsvd-l330", "rsvd-l480-q0"])
+def test_complex_wide_sample_streaming_jacobi(cuda, oracle_mod, case):
+    """l > 288: the complex Jacobi streams its columns (no register-resident
+    variant) and the realified Cholesky runs on 2l > 576 columns."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+
+    m, n, k, ell, q = case
+    a = zmatrix_with_spectrum(oracle_mod, m + n, m, n, np.exp(-np.arange(min(m, n)) / 90.0))
+    f = rsvd(a, RsvdParams(k, ell, q, 21))
+    ref = oracle_mod.zrsvd(a, k, ell, q, 21)
+    check_against(a, f, ref, str(case), dw_rel=1e-8)
+
+
+def test_complex_tsvd_streaming_jacobi(cuda, oracle_mod):
+    from paper_1710_01463_b200 import tsvd
+
+    a = zmatrix_with_spectrum(oracle_mod, 5, 330, 300, np.exp(-np.arange(300) / 80.0))
+    f = tsvd(a, 300)
+    ref = oracle_mod.ztsvd(a, 300)
+    check_against(a, f, ref, "tsvd 330x300", dw_rel=1e-8)
