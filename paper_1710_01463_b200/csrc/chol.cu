@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kCholThreads)
     pchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
                  double* __restrict__ scratch, int* __restrict__ rank_out,
                  int* __restrict__ perm_out, int ell, int ellp, double tau, int pivot,
-                 const int* __restrict__ mask) {
+                 const int* __restrict__ mask, int rp_global) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_piv;
   __shared__ int s_stop;
@@ -179,8 +179,12 @@ __global__ void __launch_bounds__(kCholThreads)
   // multiple of 8), which makes the DMMA fragment loads conflict free, and
   // >= ellp + 16 so 16-wide tiles never read past zeroed storage.
   const int rp_pitch = ellp + 20;
-  const int64_t big = max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
-  double* Rp = sm;                                 // PB x rp_pitch (panel rows of R)
+  // Large l (realified complex Grams): the panel does not fit next to the
+  // inverse workspace; it then lives in the scratch tail (rp_global).
+  const int64_t big = rp_global ? static_cast<int64_t>(kInvSmem)
+                                : max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
+  double* Rp = rp_global ? scratch + 2 * sq * static_cast<int64_t>(gridDim.x) + b * PB * rp_pitch
+                         : sm;                     // PB x rp_pitch (panel rows of R)
   double* d = sm + big;                            // panel-start Schur diagonal (by position)
   double* work = d + ellp;                         // in-panel sum of R[k][x]^2
   double* diag = work + ellp;                      // diagonal of R11 (by position)
@@ -468,7 +472,8 @@ __device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld
 __global__ void __launch_bounds__(kCholThreads)
     uchol_kernel(double* __restrict__ G, double* __restrict__ T, double* __restrict__ Rfull,
                  double* __restrict__ scratch, int* __restrict__ rank_out,
-                 int* __restrict__ perm_out, int ell, int ellp, double tau, const CholOpts o) {
+                 int* __restrict__ perm_out, int ell, int ellp, double tau, const CholOpts o,
+                 int rp_global) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_thresh;
   __shared__ int s_r;
@@ -479,8 +484,10 @@ __global__ void __launch_bounds__(kCholThreads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int rp_pitch = ellp + 20;
-  const int64_t big = max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
-  double* Rp = sm;                  // 32 x rp_pitch: row block J of R, columns >= o + 32
+  const int64_t big = rp_global ? static_cast<int64_t>(kInvSmem)
+                                : max(static_cast<int64_t>(PB) * rp_pitch, static_cast<int64_t>(kInvSmem));
+  double* Rp = rp_global ? scratch + 2 * sq * static_cast<int64_t>(gridDim.x) + b * PB * rp_pitch
+                         : sm;      // 32 x rp_pitch: row block J of R, columns >= o + 32
   double* Rd = sm + big;            // R_JJ,        Rd[i * 36 + c]
   double* Dt = Rd + 32 * kInvPitch;  // R_JJ^{-1},  Dt[i * 36 + c]
   double* W = G + b * sq;
@@ -1051,7 +1058,18 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
 
 }  // namespace
 
-int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) { return 2 * ellp * ellp * batch; }
+// Per item 2 l_p^2 (trailing buffers / inverse), plus a tail of PB x (l_p + 20)
+// per item for the single-CTA kernels' panel when it does not fit in shared
+// memory next to the inverse workspace (l_p > ~840).
+constexpr int64_t kSmemCap = 227 * 1024;
+bool panel_in_global(int64_t ellp) {
+  const int64_t big = std::max<int64_t>(PB * (ellp + 20), kInvSmem);
+  return big * 8 + 3 * ellp * 8 + 2 * ellp * 4 + 64 > kSmemCap ||
+         big * 8 + 2 * 32 * kInvPitch * 8 + 64 > kSmemCap;
+}
+int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) {
+  return 2 * ellp * ellp * batch + (panel_in_global(ellp) ? batch * PB * (ellp + 20) : 0);
+}
 
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
@@ -1059,7 +1077,8 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   if (batch <= 0) return;
   if (ellp % 32 != 0) throw CudaError("launch_pchol: ellp must be a multiple of 32");
   const int64_t pitch = ellp + 20;
-  const int64_t big = std::max<int64_t>(PB * pitch, kInvSmem);
+  const int rpg = panel_in_global(ellp) ? 1 : 0;
+  const int64_t big = rpg ? static_cast<int64_t>(kInvSmem) : std::max<int64_t>(PB * pitch, kInvSmem);
   // gchol for the plain factorizations; the gated / masked calls of the
   // ill-conditioned fallback (usually no item active) use the one-CTA-per-item
   // kernel: cooperative launches replayed from a CUDA graph cost ~1 ms each
@@ -1102,7 +1121,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     RSVD_CUDA(cudaFuncSetAttribute(uchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(ub)));
     uchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, ub, st>>>(
-        G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau, o);
+        G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau, o, rpg);
     RSVD_LAUNCH("uchol_kernel");
     return;
   }
@@ -1111,7 +1130,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
                                  static_cast<int>(bytes)));
   pchol_kernel<<<static_cast<unsigned>(batch), kCholThreads, bytes, st>>>(
       G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau,
-      pivot ? (opts && opts->pairs ? 2 : 1) : 0, opts ? opts->mask : nullptr);
+      pivot ? (opts && opts->pairs ? 2 : 1) : 0, opts ? opts->mask : nullptr, rpg);
   RSVD_LAUNCH("pchol_kernel");
 }
 

@@ -1104,6 +1104,7 @@ int guarded(rsvd_context* h, F&& f) {
     return RSVD_ERR_NUMERICAL;
   } catch (const CudaError& e) {
     h->err = e.what();
+    cudaGetLastError();  // a failed launch / attribute call must not poison the next call
     return RSVD_ERR_CUDA;
   } catch (const std::exception& e) {
     h->err = e.what();
