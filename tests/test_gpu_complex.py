@@ -361,3 +361,25 @@ def test_complex_tsvd_streaming_jacobi(cuda, oracle_mod):
     f = tsvd(a, 300)
     ref = oracle_mod.ztsvd(a, 300)
     check_against(a, f, ref, "tsvd 330x300", dw_rel=1e-8)
+
+
+@pytest.mark.parametrize("kind,ell", [("real", 900), ("complex", 512), ("complex", 1024)])
+def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell):
+    """Sample widths whose (realified) Cholesky panel does not fit in shared
+    memory (l_p > ~840): the panel moves to global scratch; the reference's
+    default l = 2k makes such widths ordinary (k = 256 complex -> 2l = 1024)."""
+    from paper_1710_01463_b200 import RsvdParams, rsvd
+    from tests.helpers import matrix_with_spectrum
+
+    m, n = 1200, 1100
+    sig = np.exp(-np.arange(n) / 200.0)
+    if kind == "real":
+        a = matrix_with_spectrum(oracle_mod, 77, m, n, sig)
+        ref = oracle_mod.rsvd(a, ell // 2, ell, 1, 3)
+    else:
+        a = zmatrix_with_spectrum(oracle_mod, 77, m, n, sig)
+        ref = oracle_mod.zrsvd(a, ell // 2, ell, 1, 3)
+    f = rsvd(a, RsvdParams(ell // 2, ell, 1, 3))
+    assert f.rank() == len(ref[1])
+    assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
+    assert isometry_err(np.asarray(f.left)) < ISO_TOL
