@@ -117,7 +117,7 @@ int rsvd_f64_rowsharded(rsvd_handle handle, const double* A_local, int64_t m_loc
 /* rlftn::tsvd<double>(a, chi) (factorize.hpp:49-50, factorize.cpp:42-50): full
  * thin SVD then truncation to r = min(chi, numerical rank) with the EXACT
  * discarded weight (discarded_exact = true).  U: m x min(chi, min(m,n)),
- * S, Vt: min(chi, min(m,n)) x n.  GPU path for min(m, n) <= 576 (the TEBD
+ * S, Vt: min(chi, min(m,n)) x n.  GPU path for min(m, n) <= 1600 (the TEBD
  * sector blocks below rsvd_min_dim and the block_factorize exact route,
  * blocks.cpp:82); larger -> RSVD_ERR_INVALID. */
 int rsvd_tsvd_f64(rsvd_handle handle, const double* A, int64_t m, int64_t n, int64_t lda,
@@ -162,7 +162,7 @@ int rsvd_z128_batched(rsvd_handle handle, int64_t batch, const double* A, int64_
                       const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
                       int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt,
                       int64_t* out_rank, double* discarded_weight, int flags);
-/* rlftn::tsvd<Complex> (factorize.cpp:42-50); GPU path for min(m, n) <= 1024. */
+/* rlftn::tsvd<Complex> (factorize.cpp:42-50); GPU path for min(m, n) <= 1600. */
 int rsvd_tsvd_z128(rsvd_handle handle, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t chi, double* U, int64_t ldu, double* S, double* Vt, int64_t ldvt,
                    int64_t* out_rank, double* discarded_weight, int flags);

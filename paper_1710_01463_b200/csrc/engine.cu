@@ -33,6 +33,9 @@ namespace rsvd {
 namespace {
 
 constexpr double kPivotTau = 1e-13;   // relative pivot floor of the CholeskyQR Gram
+// Widest l x l factor the one-sided Jacobi kernels take (the pair-staged
+// kernel keeps 16 columns of l rows in shared memory beyond l = 576).
+constexpr int64_t kTsvdMaxDim = 1600;
 constexpr int kMaxSweeps = 40;        // one-sided Jacobi sweep cap
 constexpr uint64_t kCompletionTag = 0x436f6d706c657465ull;  // "Complete"
 
@@ -786,6 +789,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   if (!A || !U || !S || !Vt || !seeds || !out_rank || !dw)
     throw InvalidArgument("rsvd: null pointer argument");
   if (lda < m || ldu < m || ldvt < rank) throw InvalidArgument("rsvd: leading dimension too small");
+  if (ell > kTsvdMaxDim) throw InvalidArgument("rsvd: l > 1600 is not supported by the GPU path");
   const bool host = flags == RSVD_PTR_HOST;
   RSVD_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
@@ -929,7 +933,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
 // (l = min(m, n)) the RSVD's SVD stage is exact: B^T = A_e^T is factored by
 // CholeskyQR2 with R and the l x l factor by one-sided Jacobi.  For m > n the
 // engine factors A^T and swaps the factors (A = V S U^T).
-constexpr int64_t kTsvdMaxDim = 576;  // one-sided Jacobi register budget (18 rows / lane)
+
 uint64_t mix64_host(uint64_t z);
 
 void tsvd_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n, int64_t lda,
@@ -943,7 +947,7 @@ void tsvd_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64
   if (batch == 0) return;
   const int64_t p = std::min(m, n), k = std::min(chi, p);
   if (p > kTsvdMaxDim)
-    throw InvalidArgument("tsvd: min(m, n) > 576 is not supported by the GPU path");
+    throw InvalidArgument("tsvd: min(m, n) > 1600 is not supported by the GPU path");
   if (!A || !U || !S || !Vt || !out_rank || !dw) throw InvalidArgument("tsvd: null pointer argument");
   if (lda < m || ldu < m || ldvt < k) throw InvalidArgument("tsvd: leading dimension too small");
   const bool host = flags == RSVD_PTR_HOST;

@@ -383,3 +383,23 @@ def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell):
     assert f.rank() == len(ref[1])
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
     assert isometry_err(np.asarray(f.left)) < ISO_TOL
+
+
+@pytest.mark.parametrize("kind,m,n", [("real", 1024, 1024), ("real", 900, 1300),
+                                      ("complex", 700, 650)])
+def test_large_tsvd(cuda, oracle_mod, kind, m, n):
+    """Full-SVD truncation beyond the register-resident Jacobi (min(m, n) up
+    to 1600 on the GPU): C1's 1024^2 matrix is the BASELINE's tsvd comparator."""
+    from paper_1710_01463_b200 import tsvd
+    from tests.helpers import matrix_with_spectrum
+
+    p = min(m, n)
+    sig = np.exp(-np.arange(p) / 32.0)
+    if kind == "real":
+        a = matrix_with_spectrum(oracle_mod, 3, m, n, sig)
+        ref = oracle_mod.tsvd(a, 64)
+    else:
+        a = zmatrix_with_spectrum(oracle_mod, 3, m, n, sig)
+        ref = oracle_mod.ztsvd(a, 64)
+    f = tsvd(a, 64)
+    check_against(a, f, ref, f"{kind} tsvd {m}x{n}", dw_rel=1e-8)
