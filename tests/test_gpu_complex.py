@@ -34,7 +34,7 @@ def check_against(a, f, ref, label="", dw_rel=1e-9):
     assert rel_sigma_err(f.sigma, S) < SIG_TOL, (label, rel_sigma_err(f.sigma, S))
     left = np.asarray(f.left)
     right = np.asarray(f.right_adj)
-    assert left.dtype == np.complex128 and right.dtype == np.complex128
+    assert left.dtype == np.asarray(a).dtype and right.dtype == np.asarray(a).dtype
     assert isometry_err(left) < ISO_TOL, (label, isometry_err(left))
     assert isometry_err(right.conj().T) < ISO_TOL, label
     e_gpu = reconstruction_error(a, f)
