@@ -383,6 +383,23 @@ def run_ours(args, rank, world, local_rank):
     prof = _lib.profile_read(h)
     _lib.profile_enable(h, False)
     sweeps = _lib.last_jacobi_sweeps(h)
+    # GPU full-SVD truncation (tsvd, factorize.cpp:42-50) of the same batch, the
+    # comparator BASELINE.json names for C1; GPU path for min(m, n) <= 1600.
+    gpu_tsvd = None
+    if min(cfg.m, cfg.n) <= 1600:
+        from paper_1710_01463_b200 import tsvd_batched
+
+        ft = tsvd_batched(A, cfg.rank, handle=h)
+        torch.cuda.synchronize()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(stream)
+        ft = tsvd_batched(A, cfg.rank, handle=h)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        tms = max_over_ranks(t0e.elapsed_time(t1e))
+        gpu_tsvd = {"value": B * world / (tms / 1000.0), "unit": "truncations/s", "ms_per_step": tms,
+                    "note": "tsvd_batched (one-sided Jacobi on the full min(m,n) factor), 1 step"}
+        del ft
     ap_ms = prof["apass_nn"][0] + prof["apass_tn"][0]
     ap_calls = prof["apass_nn"][1] + prof["apass_tn"][1]
     ap_flops_per_launch = 2.0 * cfg.m * cfg.n * cfg.ell * B  # algorithmic: one pass over A per item
@@ -464,6 +481,8 @@ def run_ours(args, rank, world, local_rank):
                          "jacobi_sweeps": sweeps, "ranks_ok": ranks_ok},
             "clocks": clk,
         }
+        if gpu_tsvd is not None:
+            line["gpu_tsvd"] = gpu_tsvd
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))
