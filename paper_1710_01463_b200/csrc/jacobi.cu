@@ -1689,9 +1689,9 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
   if (const char* e = std::getenv("RSVD_JACOBI_CLUSTER")) smax = std::atoi(e);
   if (smax < 2) return false;
   int rl = (R + smax - 1) / smax;
-  static const int kRL[] = {1, 2, 3, 4, 6};
+  static const int kRL[] = {1, 2, 3, 4, 6, 8, 12};  // 8, 12: wide factors (tsvd up to l = 1600)
   int pick = 0;
-  while (pick < 4 && kRL[pick] < rl) ++pick;
+  while (pick < 6 && kRL[pick] < rl) ++pick;
   if (kRL[pick] < rl) return false;
   rl = kRL[pick];
   const int S = (R + rl - 1) / rl;
@@ -1701,7 +1701,9 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
     case 2: return launch_clu_t<2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
     case 3: return launch_clu_t<3>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
     case 4: return launch_clu_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
-    default: return launch_clu_t<6>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    case 6: return launch_clu_t<6>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    case 8: return launch_clu_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
+    default: return launch_clu_t<12>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, S, st);
   }
 }
 
