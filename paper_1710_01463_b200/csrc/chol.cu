@@ -1101,8 +1101,17 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
       if (per_sm < 1) throw CudaError("gchol_kernel: does not fit on an SM");
       grid = per_sm * sms;
     }
+    // Size the persistent grid to the work: the widest step has one warp task
+    // per (item, upper 32 x 32 tile); a full-GPU grid for a small batch (a
+    // chunk of the host pipeline) only spins in grid barriers while occupying
+    // the SMs the other chunk's GEMMs could use.  RSVD_GCHOL_GRID overrides.
+    const int64_t nbk = ceil_div(ellp, 32);
+    const int64_t want = ceil_div(batch * nbk * (nbk + 1) / 2, kGcWarps);
+    int g = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(want, 32)));
+    static const int genv = std::getenv("RSVD_GCHOL_GRID") ? std::atoi(std::getenv("RSVD_GCHOL_GRID")) : 0;
+    if (genv > 0) g = std::min(grid, genv);
     void* args[] = {&ga};
-    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel), dim3(grid),
+    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel), dim3(g),
                                           dim3(kGcThreads), args, bytes, st));
     RSVD_LAUNCH("gchol_kernel");
     if (std::getenv("RSVD_GCHOL_TRACE")) {

@@ -44,3 +44,5 @@ for spec in sys.argv[1:]:
     out = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True,
                          text=True)
     print(out.stdout.strip() or out.stderr[-500:], flush=True)
+    if env.get("RSVD_PIPE_TRACE"):
+        print("\n".join(out.stderr.strip().splitlines()[-3:]), flush=True)
