@@ -813,31 +813,13 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
       return;
     }
   }
-  // Device-pointer batches of big items run as two half-batches on two
-  // streams (one captured graph with a fork/join): while one half sits in a
-  // latency-bound stage (Cholesky grid barriers, Jacobi) whose persistent grid
-  // covers only part of the SMs, the other half's GEMMs fill the rest.
-  static const bool no_split = std::getenv("RSVD_NO_SPLIT2") != nullptr;
-  const bool split = !no_split && !host && !sharded && !h->prof.on && batch >= 8 &&
-                     m * n >= (int64_t(1) << 22);
-  const int64_t h0 = split ? (batch + 1) / 2 : batch;
-  Shape s0 = s, s1 = s;
-  s0.batch = h0;
-  s1.batch = batch - h0;
-  Buffers B1{};
-  auto layout = [&](Carver& c) {
-    Buffers b0 = carve(c, split ? s0 : s, host, true);
-    if (split) B1 = carve(c, s1, false, true);
-    return b0;
-  };
   Carver meas{nullptr};
-  layout(meas);
+  carve(meas, s, host, true);
   char* const arena_before = h->arena.base;
   h->arena.reserve(meas.off + 256);
   if (h->arena.base != arena_before) h->drop_graphs();
   Carver cv{h->arena.base};
-  Buffers B = layout(cv);
-  if (split) h->ensure_pipeline();
+  Buffers B = carve(cv, s, host, true);
 
   if (h->pin.reserve(batch)) h->drop_graphs();
   std::memcpy(h->pin.seeds, seeds, sizeof(uint64_t) * batch);
@@ -854,34 +836,17 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   }
   B.prof = &h->prof;
   B.red = sharded ? h->red.get() : nullptr;
-  B1.prof = nullptr;
-  B1.red = nullptr;
-  // One (half-)batch: pinned seeds in, pipeline, small results out.
-  auto run_part = [&](const Shape& sp, const Buffers& Bp, int64_t b0, cudaStream_t q) {
-    const int64_t nb = sp.batch;
-    RSVD_CUDA(cudaMemcpyAsync(Bp.seeds, h->pin.seeds + b0, sizeof(uint64_t) * nb,
-                              cudaMemcpyHostToDevice, q));
-    Buffers Bq = Bp;  // range_finder swaps ping-pong buffers in its copy
-    const CMatRef Ap{Ad.base + b0 * Ad.stride, Ad.ld, Ad.stride};
-    range_finder(sp, Bq, Ap, q);
-    svd_stage(sp, Bq, Ap, MatRef{Ud.base + b0 * Ud.stride, Ud.ld, Ud.stride}, Sd + b0 * sS, sS,
-              MatRef{Vtd.base + b0 * Vtd.stride, Vtd.ld, Vtd.stride}, q);
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + b0, Bp.rankF, sizeof(int) * nb, cudaMemcpyDeviceToHost, q));
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch + b0, Bp.sweeps, sizeof(int) * nb,
-                              cudaMemcpyDeviceToHost, q));
-    RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls + b0, Bp.dw, sizeof(double) * nb, cudaMemcpyDeviceToHost, q));
-  };
+  // The device part of the call: pinned seeds in, pipeline, small results out.
   auto enqueue = [&](cudaStream_t q) {
-    if (!split) {
-      run_part(s, B, 0, q);
-      return;
-    }
-    RSVD_CUDA(cudaEventRecord(h->ev_slot_in[0], q));  // fork
-    RSVD_CUDA(cudaStreamWaitEvent(h->s_c2, h->ev_slot_in[0], 0));
-    run_part(s0, B, 0, q);
-    run_part(s1, B1, h0, h->s_c2);
-    RSVD_CUDA(cudaEventRecord(h->ev_slot_comp[0], h->s_c2));  // join
-    RSVD_CUDA(cudaStreamWaitEvent(q, h->ev_slot_comp[0], 0));
+    RSVD_CUDA(cudaMemcpyAsync(B.seeds, h->pin.seeds, sizeof(uint64_t) * batch,
+                              cudaMemcpyHostToDevice, q));
+    Buffers Bq = B;  // range_finder swaps ping-pong buffers in its copy
+    range_finder(s, Bq, Ad, q);
+    svd_stage(s, Bq, Ad, Ud, Sd, sS, Vtd, q);
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints, B.rankF, sizeof(int) * batch, cudaMemcpyDeviceToHost, q));
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch, B.sweeps, sizeof(int) * batch,
+                              cudaMemcpyDeviceToHost, q));
+    RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls, B.dw, sizeof(double) * batch, cudaMemcpyDeviceToHost, q));
   };
 
   if (host) {
