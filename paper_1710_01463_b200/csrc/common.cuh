@@ -193,9 +193,11 @@ void launch_zadjoint(CMatRef X, bool from_p, MatRef out, int64_t rows, int64_t c
 void launch_zidentity_p(MatRef X, int64_t rows, int64_t lp, int64_t ell, int64_t batch,
                         cudaStream_t st);
 void launch_hermitize(double* G, int64_t lp, const int* mask, int64_t batch, cudaStream_t st);
+// flags (jacobi_flag_elems(batch), optional): enables the block-cyclic
+// Gram-accelerated kernel for batches with many tasks.
 void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                     double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
-                    int64_t batch, cudaStream_t st);
+                    int64_t batch, cudaStream_t st, unsigned* flags = nullptr);
 void launch_zfinalize(const double* W, int64_t lp, int64_t ell, int64_t k, int64_t m, int64_t n,
                       double* sigma_out, int* perm, int* rank, double* dw, int64_t batch,
                       cudaStream_t st);

@@ -592,6 +592,359 @@ void launch_hermitize(double* G, int64_t lp, const int* mask, int64_t batch, cud
   RSVD_LAUNCH("hermitize_kernel");
 }
 
+
+// ------------------------------------------- complex Gram-accelerated Jacobi
+// Block-cyclic complex one-sided Jacobi for many items (the complex analogue
+// of jacobi.cu's jacobi_gram_kernel): columns in blocks of 16; a sweep is a
+// diagonal phase (every block rotates its 120 intra pairs) plus nb - 1
+// round-robin block-pair phases (256 inter pairs each), so every pair is
+// rotated once per sweep.  Per task (item, block pair) the 32 complex columns
+// are staged in shared memory in P-layout (64 real columns), the complex Gram
+// G = X^H X is formed on DMMA (Re: Re^T Re + Im^T Im, Im: Re^T Im - Im^T Re),
+// the 15-16 rotation steps run on G and on the accumulated unitary V (a warp
+// per pair, same complex rotation as zjacobi_kernel, exact 2 x 2 block), and
+// X <- X V, J <- J V run on DMMA as the real products X_P V~ with the
+// realified V.  Same rotation test and sweep stop rule as the scalar kernel;
+// one cooperative grid, a grid barrier per phase.
+__device__ __forceinline__ void zdmma(double (&c)[4], double a0, double a1, double b0) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+__device__ __forceinline__ int zrr(int slot, int s, int nn) {
+  return slot == 0 ? 0 : 1 + (slot - 1 + s) % (nn - 1);
+}
+
+template <int R>
+__global__ void __launch_bounds__(512, 1)
+    zjacobi_gram_kernel(const double* __restrict__ src, int64_t src_ld, int64_t src_stride,
+                        int src_mode, double2* __restrict__ H, double2* __restrict__ J, int ell,
+                        int lp, int nb, int64_t batch, int max_sweeps,
+                        unsigned* __restrict__ flags, int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int W = 16, NC = 32, RC = 64, GP = NC + 1;
+  constexpr int PITCH = 32 * R + 2;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
+  double* Xs = sm;                                          // RC x PITCH (P-layout)
+  double2* Vs = reinterpret_cast<double2*>(Xs + RC * PITCH);  // V[k + c * GP]
+  double2* Gs = Vs + NC * GP;                               // G[row + col * GP]
+  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t sq = static_cast<int64_t>(lp) * lp;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
+  const int rows = 32 * R;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t b = e / sq, rem = e - b * sq;
+    const int a = static_cast<int>(rem % lp), c = static_cast<int>(rem / lp);
+    const double* S = src + b * src_stride;
+    double2 h = make_double2(0.0, 0.0);
+    if (a < ell && c < ell) {
+      if (src_mode == 0)
+        h = make_double2(S[2 * c + (2 * a) * src_ld], S[2 * c + 1 + (2 * a) * src_ld]);
+      else
+        h = make_double2(S[a + (2 * c) * src_ld], S[a + (2 * c + 1) * src_ld]);
+    }
+    H[e] = h;
+    J[e] = make_double2(a == c ? 1.0 : 0.0, 0.0);
+  }
+  unsigned long long* mxr =
+      reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = zrr(k, phase - 1, nb), q = zrr(nb - 1 - k, phase - 1, nb);
+          bp = min(p, q), bq = max(p, q);
+        }
+        if (bp * W >= ell) continue;
+        double2* Hg = H + item * sq;
+        double2* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        auto stage = [&](const double2* M) {  // I-layout global -> P-layout smem
+          for (int e = tid; e < NC * rows; e += blockDim.x) {
+            const int c = e / rows, r = e - c * rows;
+            const int gc = gcol(c);
+            double2 v = make_double2(0.0, 0.0);
+            if (gc < ell && r < ell) v = __ldcg(M + r + static_cast<int64_t>(gc) * lp);
+            Xs[(2 * c) * PITCH + r] = v.x;
+            Xs[(2 * c + 1) * PITCH + r] = v.y;
+          }
+        };
+        stage(Hg);
+        for (int e = tid; e < NC * GP; e += blockDim.x) {
+          const int c = e / GP, r = e - c * GP;
+          Vs[e] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+        }
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
+        __syncthreads();
+        // G = X^H X on DMMA: warps 0-7 the real part, 8-15 the imaginary part,
+        // one 16 x 8 tile each (K runs over the rows twice).
+        {
+          const int part = warp >> 3, tw = warp & 7;
+          const int tm = tw >> 2, tn = tw & 3;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          const int a_0 = 16 * tm + g, a_1 = a_0 + 8, b_0 = 8 * tn + g;
+          // pass 1: Re(a)^T Re(b) (real part) / Re(a)^T Im(b) (imaginary part)
+          {
+            const double* ap0 = Xs + (2 * a_0) * PITCH;
+            const double* ap1 = Xs + (2 * a_1) * PITCH;
+            const double* bp0 = Xs + (2 * b_0 + part) * PITCH;
+#pragma unroll 4
+            for (int k0 = 0; k0 < rows; k0 += 4) zdmma(acc, ap0[k0 + t4], ap1[k0 + t4], bp0[k0 + t4]);
+          }
+          // pass 2: Im(a)^T Im(b) (real part) / -Im(a)^T Re(b) (imaginary part)
+          {
+            const double* ap0 = Xs + (2 * a_0 + 1) * PITCH;
+            const double* ap1 = Xs + (2 * a_1 + 1) * PITCH;
+            const double* bp0 = Xs + (2 * b_0 + 1 - part) * PITCH;
+            const double sg = part ? -1.0 : 1.0;
+#pragma unroll 4
+            for (int k0 = 0; k0 < rows; k0 += 4)
+              zdmma(acc, ap0[k0 + t4], ap1[k0 + t4], sg * bp0[k0 + t4]);
+          }
+          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
+          double* gd = reinterpret_cast<double*>(Gs);
+          gd[2 * (r0 + c0 * GP) + part] = acc[0];
+          gd[2 * (r0 + (c0 + 1) * GP) + part] = acc[1];
+          gd[2 * (r0 + 8 + c0 * GP) + part] = acc[2];
+          gd[2 * (r0 + 8 + (c0 + 1) * GP) + part] = acc[3];
+        }
+        __syncthreads();
+        int rotated = 0, big = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int i, jx;
+          if (diag) {
+            const int blk = warp >> 3, pi = warp & 7;
+            const int a0 = zrr(pi, s2, 16), b0 = zrr(15 - pi, s2, 16);
+            i = blk * 16 + min(a0, b0);
+            jx = blk * 16 + max(a0, b0);
+          } else {
+            i = warp;
+            jx = 16 + ((warp + s2) & 15);
+          }
+          const double al = Gs[i + i * GP].x, be = Gs[jx + jx * GP].x;
+          const double2 ga = Gs[i + jx * GP];
+          const double gg = ga.x * ga.x + ga.y * ga.y, ab = al * be;
+          const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
+          double c = 1.0, sn = 0.0, tt = 0.0, gm = 0.0, er = 1.0, ei = 0.0;
+          if (rot) {
+            big |= gg >= 1e-18 * ab;
+            gm = sqrt(gg);
+            er = ga.x / gm, ei = ga.y / gm;
+            const double d = be - al, g2 = 2.0 * gm;
+            const double mag = fmax(fabs(d), g2);
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
+            c = rsqrt(fma(tt, tt, 1.0));
+            sn = c * tt;
+            rotated = 1;
+            // columns of G and V (lane = row): x' = c x - s conj(e) y, y' = s e x + c y
+            auto colrot = [&](double2* M, int ld) {
+              const double2 x = M[lane + i * ld], y = M[lane + jx * ld];
+              const double2 ey = make_double2(er * y.x + ei * y.y, er * y.y - ei * y.x);
+              const double2 ex = make_double2(er * x.x - ei * x.y, er * x.y + ei * x.x);
+              M[lane + i * ld] = make_double2(c * x.x - sn * ey.x, c * x.y - sn * ey.y);
+              M[lane + jx * ld] = make_double2(sn * ex.x + c * y.x, sn * ex.y + c * y.y);
+            };
+            colrot(Gs, GP);
+            colrot(Vs, GP);
+          }
+          __syncthreads();
+          if (rot) {  // rows (lane = column): row_i' = c row_i - s e row_j, row_j' = s conj(e) row_i + c row_j
+            const double2 x = Gs[i + lane * GP], y = Gs[jx + lane * GP];
+            const double2 ey = make_double2(er * y.x - ei * y.y, er * y.y + ei * y.x);  // e y
+            const double2 ex = make_double2(er * x.x + ei * x.y, er * x.y - ei * x.x);  // conj(e) x
+            Gs[i + lane * GP] = make_double2(c * x.x - sn * ey.x, c * x.y - sn * ey.y);
+            Gs[jx + lane * GP] = make_double2(sn * ex.x + c * y.x, sn * ex.y + c * y.y);
+            __syncwarp();
+            if (lane == 0) {
+              Gs[i + i * GP] = make_double2(al - tt * gm, 0.0);
+              Gs[jx + jx * GP] = make_double2(be + tt * gm, 0.0);
+              Gs[i + jx * GP] = make_double2(0.0, 0.0);
+              Gs[jx + i * GP] = make_double2(0.0, 0.0);
+            }
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          if (big) atomicMax(&s_mx, 1ull);
+        }
+        __syncthreads();
+        if (s_rot) {
+          // X_P <- X_P V~ (64 x 64 realified V), warp per 16-row slab, in place.
+          auto apply_v = [&](double2* Mg) {
+            const int slabs = rows / 16;
+            for (int sl = warp; sl < slabs; sl += W) {
+              const int r0 = sl * 16;
+              double acc[RC / 8][4];
+#pragma unroll
+              for (int n = 0; n < RC / 8; ++n)
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+#pragma unroll 4
+              for (int kq = 0; kq < RC / 4; ++kq) {
+                const int kc = kq * 4 + t4;  // real row of V~
+                const double a0 = Xs[kc * PITCH + r0 + g], a1 = Xs[kc * PITCH + r0 + g + 8];
+                const int ka = kc >> 1, kr = kc & 1;
+#pragma unroll
+                for (int n = 0; n < RC / 8; ++n) {
+                  const int cc = n * 8 + g, ca = cc >> 1, cr = cc & 1;
+                  const double2 v = Vs[ka + ca * GP];
+                  // V~[2a+ra][2c+rc]: (0,0),(1,1) Re; (0,1) Im; (1,0) -Im
+                  const double b0 = (kr == cr) ? v.x : (kr ? -v.y : v.y);
+                  zdmma(acc[n], a0, a1, b0);
+                }
+              }
+              __syncwarp();
+              if (Mg == nullptr) {
+#pragma unroll
+                for (int n = 0; n < RC / 8; ++n)
+#pragma unroll
+                  for (int qq = 0; qq < 4; ++qq) {
+                    const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                    const int cc = n * 8 + 2 * t4 + (qq & 1);
+                    Xs[cc * PITCH + r] = acc[n][qq];
+                  }
+              } else {
+                // straight to global I-layout: (Re, Im) pairs are (qq, qq + 1)
+#pragma unroll
+                for (int n = 0; n < RC / 8; ++n)
+#pragma unroll
+                  for (int h2 = 0; h2 < 2; ++h2) {
+                    const int r = r0 + g + h2 * 8;
+                    const int ccx = (n * 8 + 2 * t4) >> 1;  // complex column in the pair
+                    const int gc = gcol(ccx);
+                    if (r < ell && gc < ell)
+                      Mg[r + static_cast<int64_t>(gc) * lp] =
+                          make_double2(acc[n][2 * h2], acc[n][2 * h2 + 1]);
+                  }
+              }
+            }
+          };
+          apply_v(nullptr);
+          __syncthreads();
+          for (int e = tid; e < NC * rows; e += blockDim.x) {
+            const int cc = e / rows, r = e - cc * rows;
+            const int gc = gcol(cc);
+            if (gc < ell && r < ell)
+              Hg[r + static_cast<int64_t>(gc) * lp] =
+                  make_double2(Xs[(2 * cc) * PITCH + r], Xs[(2 * cc + 1) * PITCH + r]);
+          }
+          __syncthreads();  // H written back: Xs is free for the J pair
+          stage(Jg);
+          __syncthreads();
+          apply_v(Jg);
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
+      }
+      grid.sync();
+    }
+    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (done(i)) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int R>
+bool launch_zgram_t(const double* src, int64_t src_ld, int64_t src_stride, int src_mode, double* H,
+                    double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
+                    unsigned* flags, int64_t batch, cudaStream_t st) {
+  const size_t bytes = static_cast<size_t>(64) * (32 * R + 2) * sizeof(double) +
+                       2 * 32 * 33 * sizeof(double2) + batch * sizeof(int) + 16;
+  if (bytes > 227 * 1024) return false;
+  auto kern = zjacobi_gram_kernel<R>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
+  if (per_sm < 1) return false;
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * kNumSMs)));
+  int ell_i = static_cast<int>(ell), lp_i = static_cast<int>(lp);
+  double2* Hc = reinterpret_cast<double2*>(H);
+  double2* Jc = reinterpret_cast<double2*>(J);
+  void* args[] = {const_cast<double**>(&src), &src_ld, &src_stride, &src_mode, &Hc, &Jc, &ell_i,
+                  &lp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512), args,
+                                        bytes, st));
+  RSVD_LAUNCH("zjacobi_gram_kernel");
+  return true;
+}
+
+bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
+                         double* H, double* J, int64_t ell, int64_t lp, int max_sweeps,
+                         int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
+  static const bool off = std::getenv("RSVD_NO_ZGRAM") != nullptr;
+  if (off || !flags || ell < 2) return false;
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  if (batch * (nb / 2) * 4 <= kNumSMs) return false;  // few tasks: the cluster kernel
+  const int R = static_cast<int>((ell + 31) / 32);
+  if (R <= 3) return launch_zgram_t<3>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
+  if (R <= 5) return launch_zgram_t<5>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
+  if (R <= 9) return launch_zgram_t<9>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
+  return false;
+}
+
 template <int RPL>
 void launch_zjacobi_t(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                       double* H, double* J, int ell, int64_t lp, int max_sweeps, int* sweeps,
@@ -615,8 +968,11 @@ void launch_zjacobi_t(const double* src, int64_t src_ld, int64_t src_stride, int
 
 void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                     double* H, double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
-                    int64_t batch, cudaStream_t st) {
+                    int64_t batch, cudaStream_t st, unsigned* flags) {
   if (batch <= 0) return;
+  if (launch_zjacobi_gram(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps,
+                          flags, batch, st))
+    return;
   // Cluster size: fill the SMs (S CTAs per item, at most 8, portable) but
   // never more warps than the l/2 pairs of a step.
   const int64_t pairs = (ell + 1) / 2;
