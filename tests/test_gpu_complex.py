@@ -403,3 +403,27 @@ def test_large_tsvd(cuda, oracle_mod, kind, m, n):
         ref = oracle_mod.ztsvd(a, 64)
     f = tsvd(a, 64)
     check_against(a, f, ref, f"{kind} tsvd {m}x{n}", dw_rel=1e-8)
+
+
+@pytest.mark.parametrize("case", [(40, 96, 80, 12, 24), (20, 200, 180, 64, 138), (8, 300, 280, 128, 276)],
+                         ids=["R3", "R5", "R9"])
+def test_complex_batched_block_jacobi(cuda, oracle_mod, case):
+    """Batches with more than SMs/4 block-pair tasks take the complex
+    Gram-accelerated block-cyclic Jacobi (one instantiation per rows-per-lane
+    class); every item against the complex oracle."""
+    import torch
+
+    from paper_1710_01463_b200 import RsvdParams, rsvd_batched
+
+    batch, m, n, k, ell = case
+    mats = [zmatrix_with_spectrum(oracle_mod, 900 + 7 * i + m, m, n,
+                                  np.exp(-np.arange(n) / (n / 6.0 + i))) for i in range(batch)]
+    seeds = [31 + 5 * i for i in range(batch)]
+    ad = torch.from_numpy(np.stack(mats)).to(cuda).transpose(1, 2).contiguous().transpose(1, 2)
+    f = rsvd_batched(ad, RsvdParams(k, ell, 2, 0), seeds)
+    for i in range(0, batch, max(1, batch // 6)):
+        fi = f.item(i)
+        fi.left, fi.sigma, fi.right_adj = (fi.left.cpu().numpy(), fi.sigma.cpu().numpy(),
+                                           fi.right_adj.cpu().numpy())
+        check_against(mats[i], fi, oracle_mod.zrsvd(mats[i], k, ell, 2, seeds[i]), f"item {i}",
+                      dw_rel=1e-8)
