@@ -937,7 +937,8 @@ bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, 
   if (off || !flags || ell < 2) return false;
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
-  if (batch * (nb / 2) * 4 <= kNumSMs) return false;  // few tasks: the cluster kernel
+  static const bool few_scalar = std::getenv("RSVD_ZJACOBI_FEW_SCALAR") != nullptr;
+  if (few_scalar && batch * (nb / 2) * 4 <= kNumSMs) return false;  // few tasks: the cluster kernel
   const int R = static_cast<int>((ell + 31) / 32);
   if (R <= 3) return launch_zgram_t<3>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
   if (R <= 5) return launch_zgram_t<5>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
