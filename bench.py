@@ -205,7 +205,7 @@ def run_reference(args, rank, world):
         "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE.json C4 recipe, seeded CounterRng)",
+        "data": f"synthetic (BASELINE.json {cfg.name} recipe, seeded CounterRng)",
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": cfg.batch,
                    "rank_k": cfg.rank, "ell": cfg.ell, "power_q": cfg.power,
                    "step": f"{sample} truncation(s) of the workload (bounded CPU sample)"},
