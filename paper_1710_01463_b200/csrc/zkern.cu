@@ -616,7 +616,12 @@ __device__ __forceinline__ int zrr(int slot, int s, int nn) {
   return slot == 0 ? 0 : 1 + (slot - 1 + s) % (nn - 1);
 }
 
-template <int R>
+// CLU: few tasks (single matrices) -- each task is owned by a thread-block
+// cluster of S CTAs that split its rows (32 R per CTA): every CTA forms the
+// partial Gram of its row slice, the S partials are summed through DSMEM in
+// rank order (bit-identical G in every CTA), the rotations run redundantly and
+// each CTA applies V~ to its own rows of H and J (jacobi.cu's clug scheme).
+template <int R, bool CLU>
 __global__ void __launch_bounds__(512, 1)
     zjacobi_gram_kernel(const double* __restrict__ src, int64_t src_ld, int64_t src_stride,
                         int src_mode, double2* __restrict__ H, double2* __restrict__ J, int ell,
@@ -632,12 +637,18 @@ __global__ void __launch_bounds__(512, 1)
   double* Xs = sm;                                          // RC x PITCH (P-layout)
   double2* Vs = reinterpret_cast<double2*>(Xs + RC * PITCH);  // V[k + c * GP]
   double2* Gs = Vs + NC * GP;                               // G[row + col * GP]
-  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
+  double2* Gp = Gs + NC * GP;                               // CLU: this CTA's partial Gram
+  int* conv = reinterpret_cast<int*>(Gp + (CLU ? NC * GP : 0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t sq = static_cast<int64_t>(lp) * lp;
   const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
   const int rows = 32 * R;
+  const int S = CLU ? static_cast<int>(cg::this_cluster().num_blocks()) : 1;
+  const int crank = CLU ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const int row0 = crank * rows;                         // this CTA's slice of the rows
+  const int lrows = max(0, min(rows, ell - row0));
+  const int64_t nclu = gridDim.x / S, clu = blockIdx.x / S;
 
   const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -677,7 +688,7 @@ __global__ void __launch_bounds__(512, 1)
       }
     for (int phase = 0; phase < nb; ++phase) {
       const bool diag = phase == 0;
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+      for (int64_t task = clu; task < tasks; task += nclu) {
         const int64_t item = task / half;
         if (conv[item]) continue;
         const int k = static_cast<int>(task % half);
@@ -697,7 +708,7 @@ __global__ void __launch_bounds__(512, 1)
             const int c = e / rows, r = e - c * rows;
             const int gc = gcol(c);
             double2 v = make_double2(0.0, 0.0);
-            if (gc < ell && r < ell) v = __ldcg(M + r + static_cast<int64_t>(gc) * lp);
+            if (gc < ell && r < lrows) v = __ldcg(M + row0 + r + static_cast<int64_t>(gc) * lp);
             Xs[(2 * c) * PITCH + r] = v.x;
             Xs[(2 * c + 1) * PITCH + r] = v.y;
           }
@@ -738,13 +749,29 @@ __global__ void __launch_bounds__(512, 1)
               zdmma(acc, ap0[k0 + t4], ap1[k0 + t4], sg * bp0[k0 + t4]);
           }
           const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
-          double* gd = reinterpret_cast<double*>(Gs);
+          double* gd = reinterpret_cast<double*>(CLU ? Gp : Gs);
           gd[2 * (r0 + c0 * GP) + part] = acc[0];
           gd[2 * (r0 + (c0 + 1) * GP) + part] = acc[1];
           gd[2 * (r0 + 8 + c0 * GP) + part] = acc[2];
           gd[2 * (r0 + 8 + (c0 + 1) * GP) + part] = acc[3];
         }
-        __syncthreads();
+        if (CLU) {  // G = sum of the S partials, in rank order
+          cg::cluster_group cl = cg::this_cluster();
+          cl.sync();
+          for (int e = tid; e < NC * NC; e += blockDim.x) {
+            const int c = e / NC, r = e - c * NC;
+            double2 v = make_double2(0.0, 0.0);
+            for (int rr = 0; rr < S; ++rr) {
+              const double2 w = *cl.map_shared_rank(&Gp[r + c * GP], rr);
+              v.x += w.x;
+              v.y += w.y;
+            }
+            Gs[r + c * GP] = v;
+          }
+          cl.sync();  // every CTA has read every partial
+        } else {
+          __syncthreads();
+        }
         int rotated = 0, big = 0;
         const int steps = diag ? 15 : 16;
         for (int s2 = 0; s2 < steps; ++s2) {
@@ -855,8 +882,8 @@ __global__ void __launch_bounds__(512, 1)
                     const int r = r0 + g + h2 * 8;
                     const int ccx = (n * 8 + 2 * t4) >> 1;  // complex column in the pair
                     const int gc = gcol(ccx);
-                    if (r < ell && gc < ell)
-                      Mg[r + static_cast<int64_t>(gc) * lp] =
+                    if (r < lrows && gc < ell)
+                      Mg[row0 + r + static_cast<int64_t>(gc) * lp] =
                           make_double2(acc[n][2 * h2], acc[n][2 * h2 + 1]);
                   }
               }
@@ -867,8 +894,8 @@ __global__ void __launch_bounds__(512, 1)
           for (int e = tid; e < NC * rows; e += blockDim.x) {
             const int cc = e / rows, r = e - cc * rows;
             const int gc = gcol(cc);
-            if (gc < ell && r < ell)
-              Hg[r + static_cast<int64_t>(gc) * lp] =
+            if (gc < ell && r < lrows)
+              Hg[row0 + r + static_cast<int64_t>(gc) * lp] =
                   make_double2(Xs[(2 * cc) * PITCH + r], Xs[(2 * cc + 1) * PITCH + r]);
           }
           __syncthreads();  // H written back: Xs is free for the J pair
@@ -902,30 +929,53 @@ __global__ void __launch_bounds__(512, 1)
       if (!conv[i]) sweeps_out[i] = max_sweeps;
 }
 
-template <int R>
+template <int R, bool CLU>
 bool launch_zgram_t(const double* src, int64_t src_ld, int64_t src_stride, int src_mode, double* H,
                     double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
-                    unsigned* flags, int64_t batch, cudaStream_t st) {
+                    unsigned* flags, int64_t batch, int S, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(64) * (32 * R + 2) * sizeof(double) +
-                       2 * 32 * 33 * sizeof(double2) + batch * sizeof(int) + 16;
+                       (CLU ? 3 : 2) * 32 * 33 * sizeof(double2) + batch * sizeof(int) + 16;
   if (bytes > 227 * 1024) return false;
-  auto kern = zjacobi_gram_kernel<R>;
+  auto kern = zjacobi_gram_kernel<R, CLU>;
   RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));
-  int per_sm = 0;
-  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
-  if (per_sm < 1) return false;
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
   const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * kNumSMs)));
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = static_cast<unsigned>(CLU ? S : 1);
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = CLU ? 2 : 1;
+  int64_t grid = 0;
+  if (CLU) {
+    cfg.gridDim = dim3(static_cast<unsigned>(S));
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    grid = std::max<int64_t>(1, std::min<int64_t>(tasks, max_clusters)) * S;
+  } else {
+    int per_sm = 0;
+    RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
+    if (per_sm < 1) return false;
+    grid = std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * kNumSMs));
+  }
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
   int ell_i = static_cast<int>(ell), lp_i = static_cast<int>(lp);
   double2* Hc = reinterpret_cast<double2*>(H);
   double2* Jc = reinterpret_cast<double2*>(J);
-  void* args[] = {const_cast<double**>(&src), &src_ld, &src_stride, &src_mode, &Hc, &Jc, &ell_i,
-                  &lp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512), args,
-                                        bytes, st));
+  RSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, src, src_ld, src_stride, src_mode, Hc, Jc, ell_i, lp_i,
+                               nb, batch, max_sweeps, flags, sweeps));
   RSVD_LAUNCH("zjacobi_gram_kernel");
   return true;
 }
@@ -937,12 +987,29 @@ bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, 
   if (off || !flags || ell < 2) return false;
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
-  static const bool few_scalar = std::getenv("RSVD_ZJACOBI_FEW_SCALAR") != nullptr;
-  if (few_scalar && batch * (nb / 2) * 4 <= kNumSMs) return false;  // few tasks: the cluster kernel
+  const int64_t tasks = batch * (nb / 2);
   const int R = static_cast<int>((ell + 31) / 32);
-  if (R <= 3) return launch_zgram_t<3>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
-  if (R <= 5) return launch_zgram_t<5>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
-  if (R <= 9) return launch_zgram_t<9>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, st);
+  static const bool no_clu = std::getenv("RSVD_NO_ZGRAM_CLUSTER") != nullptr;
+  if (!no_clu && tasks * 4 <= kNumSMs && R >= 2) {
+    // Few tasks: split each task's rows over a cluster of S <= 6 CTAs.
+    const int smax = static_cast<int>(std::min<int64_t>(6, kNumSMs / std::max<int64_t>(tasks, 1)));
+    if (smax >= 2) {
+      int rl = (R + smax - 1) / smax;
+      rl = rl <= 1 ? 1 : (rl <= 2 ? 2 : (rl <= 3 ? 3 : 5));
+      const int S = (R + rl - 1) / rl;
+      bool ok = false;
+      if (S >= 2) {
+        if (rl == 1) ok = launch_zgram_t<1, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else if (rl == 2) ok = launch_zgram_t<2, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else if (rl == 3) ok = launch_zgram_t<3, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else ok = launch_zgram_t<5, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+      }
+      if (ok) return true;
+    }
+  }
+  if (R <= 3) return launch_zgram_t<3, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 5) return launch_zgram_t<5, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 9) return launch_zgram_t<9, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
   return false;
 }
 
