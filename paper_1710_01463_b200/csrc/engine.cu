@@ -770,6 +770,55 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   }
 }
 
+// Replay a captured CUDA graph of `enqueue` (one host launch per call), keyed
+// by everything the captured pointers and shapes depend on; captured on the
+// handle's own stream and ordered after / before the caller's stream with
+// events.  Falls back to a direct enqueue when capture fails.
+template <class F>
+void run_graph(rsvd_context* h, const std::string& key, cudaStream_t st, F&& enqueue) {
+    // Keys include the caller's buffers: callers that allocate fresh outputs
+    // every call (instead of reusing them) would grow the cache without bound.
+    if (h->graphs.size() >= 64 && h->graphs.find(key) == h->graphs.end()) h->drop_graphs();
+    GraphEntry& ge = h->graphs[key];
+    if (!ge.exec && !ge.failed) {
+      cudaGraph_t g = nullptr;
+      RSVD_CUDA(cudaStreamBeginCapture(h->own, cudaStreamCaptureModeThreadLocal));
+      const uint64_t l0 = g_kernel_launches.load();
+      try {
+        enqueue(h->own);
+        // Capture does not run the kernels: count them once per replay instead.
+        ge.launches = g_kernel_launches.load() - l0;
+        g_kernel_launches.fetch_sub(ge.launches);
+      } catch (...) {
+        cudaStreamEndCapture(h->own, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        ge.failed = true;
+      }
+      if (!ge.failed) {
+        const cudaError_t e = cudaStreamEndCapture(h->own, &g);
+        if (e != cudaSuccess || !g || cudaGraphInstantiate(&ge.exec, g, 0) != cudaSuccess) {
+          ge.failed = true;
+          ge.exec = nullptr;
+          cudaGetLastError();
+        }
+        if (g) cudaGraphDestroy(g);
+      }
+    }
+    if (ge.exec) {
+      RSVD_CUDA(cudaEventRecord(h->ev_in, st));
+      RSVD_CUDA(cudaStreamWaitEvent(h->own, h->ev_in, 0));
+      RSVD_CUDA(cudaGraphLaunch(ge.exec, h->own));
+      g_kernel_launches.fetch_add(ge.launches);
+      RSVD_CUDA(cudaEventRecord(h->ev_out, h->own));
+      RSVD_CUDA(cudaStreamWaitEvent(st, h->ev_out, 0));
+      RSVD_CUDA(cudaStreamSynchronize(h->own));
+    } else {
+      enqueue(st);
+      RSVD_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
 void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n,
                        int64_t lda, int64_t strideA, int64_t rank, int64_t oversample, int power,
                        const uint64_t* seeds, double* U, int64_t ldu, int64_t strideU, double* S,
@@ -874,47 +923,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
                   (long long)ell, (long long)ldu, (long long)strideU, (long long)strideS,
                   (long long)ldvt * 1000003LL + strideVt, power, (void*)B.red,
                   (long long)s.m_global, (long long)s.row_off);
-    // Keys include the caller's buffers: callers that allocate fresh outputs
-    // every call (instead of reusing them) would grow the cache without bound.
-    if (h->graphs.size() >= 64 && h->graphs.find(keybuf) == h->graphs.end()) h->drop_graphs();
-    GraphEntry& ge = h->graphs[std::string(keybuf)];
-    if (!ge.exec && !ge.failed) {
-      cudaGraph_t g = nullptr;
-      RSVD_CUDA(cudaStreamBeginCapture(h->own, cudaStreamCaptureModeThreadLocal));
-      const uint64_t l0 = g_kernel_launches.load();
-      try {
-        enqueue(h->own);
-        // Capture does not run the kernels: count them once per replay instead.
-        ge.launches = g_kernel_launches.load() - l0;
-        g_kernel_launches.fetch_sub(ge.launches);
-      } catch (...) {
-        cudaStreamEndCapture(h->own, &g);
-        if (g) cudaGraphDestroy(g);
-        cudaGetLastError();
-        ge.failed = true;
-      }
-      if (!ge.failed) {
-        const cudaError_t e = cudaStreamEndCapture(h->own, &g);
-        if (e != cudaSuccess || !g || cudaGraphInstantiate(&ge.exec, g, 0) != cudaSuccess) {
-          ge.failed = true;
-          ge.exec = nullptr;
-          cudaGetLastError();
-        }
-        if (g) cudaGraphDestroy(g);
-      }
-    }
-    if (ge.exec) {
-      RSVD_CUDA(cudaEventRecord(h->ev_in, st));
-      RSVD_CUDA(cudaStreamWaitEvent(h->own, h->ev_in, 0));
-      RSVD_CUDA(cudaGraphLaunch(ge.exec, h->own));
-      g_kernel_launches.fetch_add(ge.launches);
-      RSVD_CUDA(cudaEventRecord(h->ev_out, h->own));
-      RSVD_CUDA(cudaStreamWaitEvent(st, h->ev_out, 0));
-      RSVD_CUDA(cudaStreamSynchronize(h->own));
-    } else {
-      enqueue(st);
-      RSVD_CUDA(cudaStreamSynchronize(st));
-    }
+    run_graph(h, std::string(keybuf), st, enqueue);
   } else {
     enqueue(st);
     RSVD_CUDA(cudaStreamSynchronize(st));
