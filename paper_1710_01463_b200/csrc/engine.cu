@@ -152,6 +152,7 @@ struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   bool failed = false;
   uint64_t launches = 0;  // engine kernels captured in the graph (added on every replay)
+  int seen = 0;           // calls with this key so far
 };
 
 // Pinned host staging for the per-call scalars (seeds in; ranks, sweeps,
@@ -780,6 +781,13 @@ void run_graph(rsvd_context* h, const std::string& key, cudaStream_t st, F&& enq
     // every call (instead of reusing them) would grow the cache without bound.
     if (h->graphs.size() >= 64 && h->graphs.find(key) == h->graphs.end()) h->drop_graphs();
     GraphEntry& ge = h->graphs[key];
+    // Capture on the second call with the same key: a caller that passes fresh
+    // output buffers every call (a new key each time) never pays a capture.
+    if (ge.seen++ == 0) {
+      enqueue(st);
+      RSVD_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
     if (!ge.exec && !ge.failed) {
       cudaGraph_t g = nullptr;
       RSVD_CUDA(cudaStreamBeginCapture(h->own, cudaStreamCaptureModeThreadLocal));
