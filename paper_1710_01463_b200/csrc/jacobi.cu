@@ -25,6 +25,20 @@
 namespace rsvd {
 namespace {
 
+// Sweep stop rule: an item is done after a sweep whose largest rotated
+// g^2 / (alpha beta) stayed below this (default (1e-9)^2; RSVD_JACOBI_STOP_RATIO
+// overrides the ratio for experiments).
+__constant__ double c_stop_ratio2 = 1e-18;
+void set_stop_ratio_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (const char* e = std::getenv("RSVD_JACOBI_STOP_RATIO")) {
+    const double r = std::atof(e);
+    const double r2 = r * r;
+    cudaMemcpyToSymbol(c_stop_ratio2, &r2, sizeof(double));
+  }
+}
 constexpr int kJacThreads = 1024;
 constexpr int kJacWarps = kJacThreads / 32;
 
@@ -648,7 +662,7 @@ __global__ void __launch_bounds__(512, MINB)
           // one division (the zeta form needs two) unless d, g are extreme.
           const double gg = ga * ga, ab = al * be;
           if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
-            big |= gg >= 1e-18 * ab;
+            big |= gg >= c_stop_ratio2 * ab;
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             double tt;
@@ -920,7 +934,7 @@ __global__ void __launch_bounds__(512, MINB)
           const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
           double c = 1.0, sn = 0.0, tt = 0.0;
           if (rot) {
-            big |= gg >= 1e-18 * ab;
+            big |= gg >= c_stop_ratio2 * ab;
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             if (mag > 1e-140 && mag < 1e140) {
@@ -1253,7 +1267,7 @@ __global__ void __launch_bounds__(512, 1)
           const double al = nrm[i], be = nrm[jx];
           const double gg = ga * ga, ab = al * be;
           if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
-            big |= gg >= 1e-18 * ab;
+            big |= gg >= c_stop_ratio2 * ab;
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             double tt;
@@ -1509,7 +1523,7 @@ __global__ void __launch_bounds__(512, 1)
           const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
           double c = 1.0, sn = 0.0, tt = 0.0;
           if (rot) {
-            big |= gg >= 1e-18 * ab;
+            big |= gg >= c_stop_ratio2 * ab;
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             if (mag > 1e-140 && mag < 1e140) {
@@ -1775,6 +1789,7 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
 
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st) {
+  set_stop_ratio_once();
   const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
   {
     int nbt = static_cast<int>((ell + 15) / 16);
