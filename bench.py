@@ -147,6 +147,27 @@ def cpu_oracle_rsvd(A_items, cfg, seeds, threads):
     return times
 
 
+L2_BYTES = 126 * 1024 * 1024  # B200 L2
+
+
+def l2_flush_buffer(input_bytes, dev):
+    """A 256 MB device buffer to overwrite before every timed step when the
+    per-rank inputs are under twice the L2 (C1 8 MB, C2/C3 134 MB), else None
+    (C4 4.3 GB, C5 537 MB: the inputs themselves stream through L2)."""
+    import torch
+
+    if input_bytes >= 2 * L2_BYTES:
+        return None
+    return torch.empty(2 * L2_BYTES // 8, dtype=torch.float64, device=dev)
+
+
+def l2_note(input_bytes):
+    if input_bytes >= 2 * L2_BYTES:
+        return "inputs larger than L2 (%.2f GB per rank, > 2 x 126 MB)" % (input_bytes / 1e9)
+    return ("L2 flushed before every timed step (252 MB write outside the timed span; "
+            "inputs %.1f MB per rank)" % (input_bytes / 1e6))
+
+
 def cpu_modes(A_items, cfg, seeds, threads, budget_s):
     """the reference protocol (1 BLAS thread) and all host cores,
     for both methods -- rsvd and full-SVD truncation (tsvd = dgesdd +
@@ -250,17 +271,22 @@ def run_rowsharded(args, rank, world, local_rank):
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.kernel_launches()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    flush = l2_flush_buffer(count * cfg.n * 8, dev)
+    pairs = []
     for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record()
         f = sharding.rsvd_rowsharded(a_loc, cfg.m, first, params, h)
-    e1.record()
+        ee.record()
+        pairs.append((es, ee))
     torch.cuda.synchronize()
+    step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     dist.barrier()
     launches = _lib.kernel_launches() - launches0
     clk = clocks.stop()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = args.steps / (ms / 1000.0)
@@ -288,7 +314,7 @@ def run_rowsharded(args, rank, world, local_rank):
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "rank_k": cfg.rank,
                        "ell": cfg.ell, "power_q": cfg.power,
                        "parallelism": f"row shard x{world} (NCCL all-reduce of Grams / A^T Q panels)",
-                       "rows_per_rank": count},
+                       "rows_per_rank": count, "l2": l2_note(count * cfg.n * 8)},
             "e2e": {"value": e2e_value, "unit": "truncations/s",
                     "h2d_bytes_per_step": count * cfg.n * 8,
                     "d2h_bytes_per_step": (count * k + k + k * cfg.n) * 8},
@@ -352,15 +378,30 @@ def run_ours(args, rank, world, local_rank):
     verbose = bool(os.environ.get("RSVD_BENCH_VERBOSE"))
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if verbose else []
     host_t = []
-    e0.record(stream)
-    for i in range(args.steps):
-        th = time.perf_counter()
-        f = rsvd_batched(A, params, seeds, handle=h, out=f)
-        if verbose:
-            step_ev[i].record(stream)
-            host_t.append(round((time.perf_counter() - th) * 1e3, 2))
-    e1.record(stream)
-    torch.cuda.synchronize()
+    flush = l2_flush_buffer(B * cfg.m * cfg.n * 8, dev)
+    if flush is None:
+        e0.record(stream)
+        for i in range(args.steps):
+            th = time.perf_counter()
+            f = rsvd_batched(A, params, seeds, handle=h, out=f)
+            if verbose:
+                step_ev[i].record(stream)
+                host_t.append(round((time.perf_counter() - th) * 1e3, 2))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        step_ms = e0.elapsed_time(e1)
+    else:
+        # Inputs fit the 126 MB L2: flush it before every step, time the steps only.
+        pairs = []
+        for i in range(args.steps):
+            flush.zero_()
+            es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            f = rsvd_batched(A, params, seeds, handle=h, out=f)
+            ee.record(stream)
+            pairs.append((es, ee))
+        torch.cuda.synchronize()
+        step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     if verbose:
         prev, dev_t = e0, []
         for ev in step_ev:
@@ -370,7 +411,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = _lib.kernel_launches() - launches0
     clk = clocks.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms = max_over_ranks(step_ms)
     value = B * world * args.steps / (ms / 1000.0)
     ranks_ok = all(r == cfg.rank for r in f.ranks)
 
@@ -468,7 +509,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": B,
                        "global_batch": B * world, "rank_k": cfg.rank, "ell": cfg.ell,
                        "power_q": cfg.power, "parallelism": f"batch split dp{world}",
-                       "l2": "inputs larger than L2 (%.1f GB per rank)" % (B * cfg.m * cfg.n * 8 / 1e9)},
+                       "l2": l2_note(B * cfg.m * cfg.n * 8)},
             "e2e": {"value": e2e_value, "unit": "truncations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "host_memory": "pinned" if e2e_pinned else "pageable"},
             "gpu_launches": launches,
