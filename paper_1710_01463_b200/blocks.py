@@ -169,6 +169,13 @@ def block_factorize_many(mats: Sequence[BlockDiagMatrix], chi: int, request: Sec
                 key = ("tsvd", dev, m, n, want[s])
             groups.setdefault(key, []).append((mi, s))
 
+    # Host copies of the singular values (the selection runs on the host): one
+    # transfer per engine call instead of one per sector.
+    host_sig: Dict[Tuple[int, int], np.ndarray] = {}
+    for mi, a in enumerate(mats):
+        for s, f in enumerate(factors[mi]):
+            if f is not None:
+                host_sig[(mi, s)] = np.zeros(0)
     for key, members in groups.items():
         blocks = [mats[mi].blocks[s] for mi, s in members]
         if key[0] == "tsvd":
@@ -176,6 +183,7 @@ def block_factorize_many(mats: Sequence[BlockDiagMatrix], chi: int, request: Sec
             if len(members) == 1:
                 mi, s = members[0]
                 factors[mi][s] = tsvd(blocks[0], k, handle)
+                host_sig[(mi, s)] = _host(factors[mi][s].sigma)
                 continue
             bf = tsvd_batched(_stack(blocks), k, handle)
         else:
@@ -184,23 +192,34 @@ def block_factorize_many(mats: Sequence[BlockDiagMatrix], chi: int, request: Sec
             if len(members) == 1:
                 mi, s = members[0]
                 factors[mi][s] = rsvd(blocks[0], RsvdParams(k, ell, power, seeds[0]), handle)
+                host_sig[(mi, s)] = _host(factors[mi][s].sigma)
                 continue
             bf = rsvd_batched(_stack(blocks), RsvdParams(k, ell, power, 0), seeds, handle)
+        sig_all = _host(bf.sigma)
         for i, (mi, s) in enumerate(members):
             factors[mi][s] = bf.item(i)
+            host_sig[(mi, s)] = sig_all[i][:bf.ranks[i]]
 
-    return [_select(mats[mi], factors[mi], chi, exact[mi]) for mi in range(len(mats))]
+    return [_select(mats[mi], factors[mi], chi, exact[mi],
+                    [host_sig[(mi, s)] for s in range(len(factors[mi]))])
+            for mi in range(len(mats))]
 
 
-def _select(a: BlockDiagMatrix, factors, chi: int, exact: bool) -> BlockFactorization:
+def _host(x) -> np.ndarray:
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def _select(a: BlockDiagMatrix, factors, chi: int, exact: bool,
+            host_sigs=None) -> BlockFactorization:
     """Global post-selection (blocks.cpp:86-116): the chi largest values over
     all sectors, ties to the lower charge then the lower in-sector position;
-    dropped values move into the sector's discarded weight."""
+    dropped values move into the sector's discarded weight.  Each kept factor
+    carries `sigma_host`, a host copy of its values."""
     nsec = len(factors)
     cand = []
     sigs = []
     for s, f in enumerate(factors):
-        sig = f.sigma.cpu().numpy() if hasattr(f.sigma, "cpu") else np.asarray(f.sigma)
+        sig = host_sigs[s] if host_sigs is not None else _host(f.sigma)
         sigs.append(sig)
         for pos in range(f.rank()):
             cand.append((-float(sig[pos]), int(a.charges[s]), pos, s))
@@ -212,8 +231,10 @@ def _select(a: BlockDiagMatrix, factors, chi: int, exact: bool) -> BlockFactoriz
     out = []
     for s, f in enumerate(factors):
         dw = f.discarded_weight + float(np.sum(sigs[s][keep[s]:] ** 2))
-        out.append(TruncatedFactorization(f.left[:, :keep[s]], f.sigma[:keep[s]],
-                                          f.right_adj[:keep[s], :], dw, f.discarded_exact))
+        tf = TruncatedFactorization(f.left[:, :keep[s]], f.sigma[:keep[s]],
+                                    f.right_adj[:keep[s], :], dw, f.discarded_exact)
+        tf.sigma_host = sigs[s][:keep[s]]
+        out.append(tf)
         total_dw += dw
     return BlockFactorization(list(a.charges), out, total_dw, exact)
 

@@ -214,12 +214,19 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
         for m1 in range(d):
             for m2 in range(d):
                 pairs[p[m1] ^ p[m2]].append((m1, m2))
-        gblock = torch.as_tensor(gate.block, **f64)
-        gt = []
-        for q in (0, 1):
-            idx = torch.tensor([m1 * d + m2 for (m1, m2) in pairs[q]], device=dev, dtype=torch.long)
-            # theta' columns = theta columns * gt, gt(i, j) = gate(pair_j, pair_i)
-            gt.append(gblock[idx][:, idx].t().contiguous() if len(pairs[q]) else None)
+        # theta' columns = theta columns * gt, gt(i, j) = gate(pair_j, pair_i);
+        # built once per (gate, scalar type, device) and cached on the gate.
+        cache = gate.__dict__.setdefault("_device_blocks", {})
+        ckey = (f64["dtype"], str(dev), tuple(p))
+        gt = cache.get(ckey)
+        if gt is None:
+            gblock = torch.as_tensor(gate.block, **f64)
+            gt = []
+            for q in (0, 1):
+                idx = torch.tensor([m1 * d + m2 for (m1, m2) in pairs[q]], device=dev,
+                                   dtype=torch.long)
+                gt.append(gblock[idx][:, idx].t().contiguous() if len(pairs[q]) else None)
+            cache[ckey] = gt
         thetap = [torch.zeros(rows[sp], cols[sp], **f64) for sp in (0, 1)]
         for a in (0, 1):
             for c in (0, 1):
@@ -282,24 +289,38 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
                 thetap[sp] = r @ y
         plan.lifted = True
     plan.thetap = thetap
-    plan.total_sq = float(sum((tp.abs() ** 2).sum() if tp.is_complex() else (tp * tp).sum()
-                              for tp in thetap))
-    if not (plan.total_sq > 0.0):
-        raise RuntimeError("apply_gate: evolved wavefunction vanished")
+    # kept on the device: the callers read all bonds' norms in one transfer
+    plan.total_sq_t = sum((tp.abs() ** 2).sum() if tp.is_complex() else (tp * tp).sum()
+                          for tp in thetap)
     return plan
+
+
+def _read_norms(plans) -> None:
+    """One device -> host transfer for every plan's ||theta'||^2 (mps.cpp:268)."""
+    torch = _torch()
+    vals = torch.stack([torch.as_tensor(p.total_sq_t, dtype=torch.float64,
+                                        device=p.thetap[0].device).reshape(())
+                        for p in plans]).cpu().tolist()
+    for p, v in zip(plans, vals):
+        p.total_sq = float(v)
+        if not (p.total_sq > 0.0):
+            raise RuntimeError("apply_gate: evolved wavefunction vanished")
 
 
 def _finish(psi: SymmetricMPS, plan: _BondPlan, f, seconds: float) -> GateStats:
     """mps.cpp:276-321: trim, renormalise, lift, gauge update."""
     torch = _torch()
     factors = f.factors
-    sig = [x.sigma for x in factors]
-    kept_sq = float(sum((s * s).sum() for s in sig))
+    # host copies of the kept values (blocks._select), no per-sector transfer
+    sh = [getattr(x, "sigma_host", None) for x in factors]
+    sh = [v if v is not None else (x.sigma.cpu().numpy() if hasattr(x.sigma, "cpu")
+                                   else np.asarray(x.sigma)) for v, x in zip(sh, factors)]
+    kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
     if kept_sq > 0.0:
         cut = LAMBDA_TRIM * np.sqrt(kept_sq)
         trimmed = False
-        for fac in factors:
-            sv = fac.sigma.cpu().numpy() if hasattr(fac.sigma, "cpu") else np.asarray(fac.sigma)
+        for i, fac in enumerate(factors):
+            sv = sh[i]
             r = len(sv)
             while r > 0 and sv[r - 1] < cut:
                 r -= 1
@@ -308,9 +329,11 @@ def _finish(psi: SymmetricMPS, plan: _BondPlan, f, seconds: float) -> GateStats:
             fac.left = fac.left[:, :r]
             fac.sigma = fac.sigma[:r]
             fac.right_adj = fac.right_adj[:r, :]
+            sh[i] = sv[:r]
+            fac.sigma_host = sh[i]
             trimmed = True
         if trimmed:
-            kept_sq = float(sum((x.sigma * x.sigma).sum() for x in factors))
+            kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
     if not (kept_sq > 0.0):
         raise RuntimeError("apply_gate: truncation removed the whole state")
     if plan.lifted:
@@ -348,6 +371,7 @@ def apply_gate(psi: SymmetricMPS, bond: int, gate: TwoSiteGate, chi: int, method
         raise InvalidArgument("apply_gate: chi must be >= 1")
     request = request or SectorRankRequest()
     plan = _assemble(psi, bond, gate)
+    _read_norms([plan])
     torch = _torch()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -375,6 +399,7 @@ def apply_gate_layer(psi: SymmetricMPS, bonds: Sequence[int], gates: Sequence[Tw
         used.add(b)
     request = request or SectorRankRequest()
     plans = [_assemble(psi, b, g) for b, g in zip(bonds, gates)]
+    _read_norms(plans)
     torch = _torch()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
