@@ -235,18 +235,17 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
                 blk = nl[a] * nr[c]
                 if blk == 0 or npair == 0:
                     continue
-                tin = torch.empty(blk, npair, **f64)
-                for i, (m1, m2) in enumerate(pairs[q]):
-                    s = a ^ p[m1]
-                    sub = theta[s][row_off[s][m1]:row_off[s][m1] + nl[a],
-                                   col_off[s][m2]:col_off[s][m2] + nr[c]]
-                    tin[:, i] = sub.t().reshape(-1)  # column-major vec, as Eigen::Map
-                tout = tin @ gt[q]
+                # the (m1, m2) blocks of this (a, c) stacked, mixed by the gate in
+                # one product: block'_j = sum_i gt(i, j) block_i
+                tin = torch.stack([
+                    theta[a ^ p[m1]][row_off[a ^ p[m1]][m1]:row_off[a ^ p[m1]][m1] + nl[a],
+                                     col_off[a ^ p[m1]][m2]:col_off[a ^ p[m1]][m2] + nr[c]]
+                    for (m1, m2) in pairs[q]])
+                tout = (gt[q].t() @ tin.reshape(npair, blk)).reshape(npair, nl[a], nr[c])
                 for i, (m1, m2) in enumerate(pairs[q]):
                     sp = a ^ p[m1]
                     thetap[sp][row_off[sp][m1]:row_off[sp][m1] + nl[a],
-                               col_off[sp][m2]:col_off[sp][m2] + nr[c]] = \
-                        tout[:, i].reshape(nr[c], nl[a]).t()
+                               col_off[sp][m2]:col_off[sp][m2] + nr[c]] = tout[i]
     else:
         if not gate.terms:
             raise InvalidArgument("apply_gate: product-form gate has no terms")
