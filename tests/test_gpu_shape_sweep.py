@@ -55,7 +55,10 @@ def test_sweep_rsvd_against_oracle(cuda, oracle_mod, case):
         e_gpu = np.linalg.norm(mats[b] - rec)
         e_ref = np.linalg.norm(mats[b] - (U * S[None, :]) @ Vt)
         scale = np.linalg.norm(mats[b])
-        assert abs(e_gpu - e_ref) <= 1e-10 * max(e_ref, 1e-6 * scale), (case, b, e_gpu, e_ref)
+        if e_ref > 1e-12 * scale:  # a real truncation error: 1e-10 relative (north_star)
+            assert abs(e_gpu - e_ref) <= 1e-10 * e_ref, (case, b, e_gpu, e_ref)
+        else:  # exact reconstruction: roundoff on both sides (test_factorize.cpp:105-120 bound)
+            assert e_gpu <= 1e-10 * scale, (case, b, e_gpu, e_ref)
         assert fb.discarded_weight == pytest.approx(dw, rel=1e-8, abs=1e-24 * scale ** 2), (case, b)
 
 
@@ -73,5 +76,8 @@ def test_sweep_tsvd_against_oracle(cuda, oracle_mod, case):
         f = tsvd(a, chi)
         _, S, _, dw = (oracle_mod.ztsvd if cplx else oracle_mod.tsvd)(a, chi)
         assert f.rank() == len(S)
-        assert rel_sigma_err(f.sigma, S) < 1e-10, (case, chi)
-        assert f.discarded_weight == pytest.approx(dw, rel=1e-9, abs=1e-26)
+        # 0.8^k runs down to ~1e-25: like gesdd the small values are accurate to
+        # O(u ||A||) absolute; 1e-10 relative where that is meaningful.
+        sv = np.asarray(f.sigma)
+        assert np.all(np.abs(sv - S) <= 1e-10 * S + 1e-12 * S[0]), (case, chi)
+        assert f.discarded_weight == pytest.approx(dw, rel=1e-9, abs=1e-22 * S[0] ** 2)
