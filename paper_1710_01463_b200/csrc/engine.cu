@@ -907,17 +907,35 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   };
 
   if (host) {
-    for (int64_t b = 0; b < batch; ++b)
-      copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, st);
-    enqueue(st);
-    for (int64_t b = 0; b < batch; ++b) {
-      copy_2d(U + b * strideU, ldu, B.Uh + b * m * rank, m, m, rank, cudaMemcpyDeviceToHost, st);
-      copy_2d(Vt + b * strideVt, ldvt, B.Vth + b * rank * n, rank, rank, n, cudaMemcpyDeviceToHost,
-              st);
-      RSVD_CUDA(cudaMemcpyAsync(S + b * strideS, B.Sh + b * rank, sizeof(double) * rank,
-                                cudaMemcpyDeviceToHost, st));
+    // Copies in, pipeline, factors out: one graph when the caller's host
+    // buffers are page-locked and reused (a pageable buffer fails the capture
+    // and the call runs directly).
+    auto enqueue_host = [&](cudaStream_t q) {
+      for (int64_t b = 0; b < batch; ++b)
+        copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, q);
+      enqueue(q);
+      for (int64_t b = 0; b < batch; ++b) {
+        copy_2d(U + b * strideU, ldu, B.Uh + b * m * rank, m, m, rank, cudaMemcpyDeviceToHost, q);
+        copy_2d(Vt + b * strideVt, ldvt, B.Vth + b * rank * n, rank, rank, n,
+                cudaMemcpyDeviceToHost, q);
+        RSVD_CUDA(cudaMemcpyAsync(S + b * strideS, B.Sh + b * rank, sizeof(double) * rank,
+                                  cudaMemcpyDeviceToHost, q));
+      }
+    };
+    if (!h->prof.on && graphs_enabled() && !sharded) {
+      char keybuf[512];
+      std::snprintf(keybuf, sizeof(keybuf),
+                    "h|%p|%p|%p|%p|%p|%p|%p|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d",
+                    (const void*)A, (void*)U, (void*)S, (void*)Vt, (void*)h->arena.base,
+                    (void*)h->pin.seeds, (void*)h->pin.ints, (long long)m, (long long)n,
+                    (long long)lda, (long long)strideA, (long long)batch, (long long)rank,
+                    (long long)ell, (long long)ldu, (long long)strideU, (long long)strideS,
+                    (long long)ldvt * 1000003LL + strideVt, power);
+      run_graph(h, std::string(keybuf), st, enqueue_host);
+    } else {
+      enqueue_host(st);
+      RSVD_CUDA(cudaStreamSynchronize(st));
     }
-    RSVD_CUDA(cudaStreamSynchronize(st));
   } else if (!h->prof.on && graphs_enabled() && (!B.red || B.red->capturable())) {
     // Replay a captured CUDA graph of the whole pipeline (one host launch per
     // call); captured on the handle's own stream and ordered after / before the
