@@ -639,12 +639,13 @@ void copy_batch(void* dst, int64_t dld, int64_t dstride, const void* src, int64_
 int64_t host_chunks(int64_t batch, int64_t m, int64_t n) {
   if (const char* e = std::getenv("RSVD_HOST_CHUNKS"))
     return std::min<int64_t>(rsvd_context::kMaxChunks, std::max<int64_t>(1, std::atoi(e)));
-  // Each chunk has its own staging, so the H2D stream never waits for a slot;
-  // chunks of >= 512 MB keep the GEMMs full (C4: 4 chunks of 8 items).
+  // Each chunk has its own staging, so the H2D stream never waits for a slot.
+  // C4 (4.3 GB): 7 chunks (5,5,5,5,5,5,2) on three compute streams measured
+  // 319 trunc/s against 295 for 4 chunks on two (tools/probe/e2e_probe.py).
   const int64_t per = m * n * 8;
   if (batch < 2 || per * batch < (int64_t(256) << 20)) return 1;
   const int64_t by_size = std::max<int64_t>(1, per * batch / (int64_t(512) << 20));
-  return std::max<int64_t>(2, std::min<int64_t>({by_size, batch, 4}));
+  return std::max<int64_t>(2, std::min<int64_t>({by_size, batch, 7}));
 }
 
 // Host-pointer batched rsvd with the PCIe transfers overlapped: chunk c's H2D
@@ -702,8 +703,8 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   cudaStream_t cs[3] = {st, h->s_c2, h->s_c3};
   static const int nstreams = [] {
     const char* e = std::getenv("RSVD_PIPE_STREAMS");
-    const int v = e ? std::atoi(e) : 2;
-    return v == 3 ? 3 : 2;
+    const int v = e ? std::atoi(e) : 3;
+    return v == 2 ? 2 : 3;
   }();
   // Order the side streams after whatever the caller queued on its stream.
   RSVD_CUDA(cudaEventRecord(h->ev_in, st));
