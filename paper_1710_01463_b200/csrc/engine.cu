@@ -921,16 +921,13 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
     // buffers are page-locked and reused (a pageable buffer fails the capture
     // and the call runs directly).
     auto enqueue_host = [&](cudaStream_t q) {
-      for (int64_t b = 0; b < batch; ++b)
-        copy_2d(B.Ah + b * m * n, m, A + b * strideA, lda, m, n, cudaMemcpyHostToDevice, q);
+      // one linear copy per operand when the items are packed (copy_batch)
+      copy_batch(B.Ah, m, m * n, A, lda, strideA, m, n, batch, cudaMemcpyHostToDevice, q);
       enqueue(q);
-      for (int64_t b = 0; b < batch; ++b) {
-        copy_2d(U + b * strideU, ldu, B.Uh + b * m * rank, m, m, rank, cudaMemcpyDeviceToHost, q);
-        copy_2d(Vt + b * strideVt, ldvt, B.Vth + b * rank * n, rank, rank, n,
-                cudaMemcpyDeviceToHost, q);
-        RSVD_CUDA(cudaMemcpyAsync(S + b * strideS, B.Sh + b * rank, sizeof(double) * rank,
-                                  cudaMemcpyDeviceToHost, q));
-      }
+      copy_batch(U, ldu, strideU, B.Uh, m, m * rank, m, rank, batch, cudaMemcpyDeviceToHost, q);
+      copy_batch(Vt, ldvt, strideVt, B.Vth, rank, rank * n, rank, n, batch, cudaMemcpyDeviceToHost,
+                 q);
+      copy_batch(S, rank, strideS, B.Sh, rank, rank, rank, 1, batch, cudaMemcpyDeviceToHost, q);
     };
     if (!h->prof.on && graphs_enabled() && !sharded) {
       char keybuf[512];
