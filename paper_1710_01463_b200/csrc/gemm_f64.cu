@@ -375,16 +375,39 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 }  // namespace
 
+// Split-K count of the symmetric 96 x 96 Gram tiling: the upper tiles times
+// the splits should fill whole waves of the 2 x SMs resident CTAs (C4: 192
+// tiles -> 3 splits = 1.95 waves instead of 2 splits = 1.3 waves), each split
+// keeping >= 256 of K.
+int64_t sq96_splits(int64_t M, int64_t K, int64_t batch) {
+  static const bool old = std::getenv("RSVD_GRAM_SPLIT_OLD") != nullptr;
+  const int64_t t = M / 96, tiles = t * (t + 1) / 2 * batch;
+  const int64_t slots = 2 * kNumSMs;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / 256));
+  if (old) {
+    int64_t sp = 1;
+    if (tiles < slots) sp = std::min<int64_t>(ceil_div(slots, tiles), smax);
+    return std::max<int64_t>(1, std::min<int64_t>(sp, 64));
+  }
+  if (tiles >= 4 * slots) return 1;
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t ctas = tiles * sp;
+    const double eff = static_cast<double>(ctas) / static_cast<double>(ceil_div(ctas, slots) * slots);
+    // prefer fuller waves; among (nearly) equal, fewer splits (less partial traffic)
+    if (eff > best_eff + 0.02) best_eff = eff, best = sp;
+    if (ctas >= 3 * slots) break;
+  }
+  return best;
+}
+
 int64_t dgemm_partial_elems(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t batch) {
   const Choice c = choose(M, N, K, batch);
   int64_t splits = c.splits;
   if (trans_a && M == N && M % 96 == 0) {  // the 96 x 96 Gram tiling of dgemm_ex
-    const int64_t t = M / 96, tiles = t * (t + 1) / 2 * batch;
-    int64_t sp = 1;
-    if (tiles < 2 * kNumSMs) sp = std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / 256));
-    sp = std::max<int64_t>(1, std::min<int64_t>(sp, 64));
-    sp = ceil_div(K, round_up(ceil_div(K, sp), kBK));
-    splits = std::max(splits, sp);
+    const int64_t sp = sq96_splits(M, K, batch);
+    splits = std::max(splits, ceil_div(K, round_up(ceil_div(K, sp), kBK)));
   }
   return splits > 1 ? splits * batch * M * N : 0;
 }
@@ -408,11 +431,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool sq96 = opt.c_upper && trans_a && M == N && M % 96 == 0 && !opt.colmapA &&
                     tma_operands && !std::getenv("RSVD_NO_GRAM96");
   if (sq96) {
-    const int64_t t = M / 96;
-    const int64_t tiles = t * (t + 1) / 2 * batch;
-    int64_t splits = 1;
-    if (tiles < 2 * kNumSMs) splits = std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / 256));
-    splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
+    int64_t splits = sq96_splits(M, K, batch);
     int64_t kps = round_up(ceil_div(K, splits), kBK);
     splits = ceil_div(K, kps);
     c.bm = 96, c.bn = 96, c.splits = static_cast<int>(splits), c.kps = kps;
