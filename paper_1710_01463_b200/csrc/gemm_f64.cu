@@ -396,7 +396,7 @@ int64_t sq96_splits(int64_t M, int64_t K, int64_t batch) {
     const int64_t ctas = tiles * sp;
     const double eff = static_cast<double>(ctas) / static_cast<double>(ceil_div(ctas, slots) * slots);
     // prefer fuller waves; among (nearly) equal, fewer splits (less partial traffic)
-    if (eff > best_eff + 0.02) best_eff = eff, best = sp;
+    if (eff > best_eff * 1.02) best_eff = eff, best = sp;
     if (ctas >= 3 * slots) break;
   }
   return best;
