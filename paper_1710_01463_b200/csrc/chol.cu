@@ -819,9 +819,21 @@ __device__ void gc_factor_diag(const GcholArgs& a, int64_t b, int J, double* Rd,
 //      J+1 is updated first and factored by the same warp (lookahead).
 // Two grid barriers per block; a launch whose items are all gated off exits
 // before the first barrier.
+// CLU: the whole (small) grid is one thread-block cluster and the grid
+// barriers become cluster barriers (hardware, ~1 us cheaper each); used for
+// single matrices / small batches whose widest step fits 16 CTAs.  Cross-CTA
+// data is read with ld.global.cg in both modes.
+template <bool CLU>
 __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a) {
   namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+  struct Sync {
+    __device__ void sync() {
+      if constexpr (CLU)
+        cg::this_cluster().sync();
+      else
+        cg::this_grid().sync();
+    }
+  } grid;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_any;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1091,10 +1103,10 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     const int bytes = kGcDiagWarps * 2 * 32 * kInvPitch * 8;
     static int grid = 0;
     if (grid == 0) {
-      RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bytes));
       int per_sm = 0, dev = 0, sms = 0;
-      RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel, kGcThreads,
+      RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel<false>, kGcThreads,
                                                               bytes));
       RSVD_CUDA(cudaGetDevice(&dev));
       RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1110,8 +1122,55 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     int g = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(want, 32)));
     static const int genv = std::getenv("RSVD_GCHOL_GRID") ? std::atoi(std::getenv("RSVD_GCHOL_GRID")) : 0;
     if (genv > 0) g = std::min(grid, genv);
+    // Small work: one cluster of 8-16 CTAs with cluster barriers.
+    static const bool no_clu = std::getenv("RSVD_NO_GCHOL_CLUSTER") != nullptr;
+    static int clu_ok = -1;  // 16-CTA (non-portable) clusters available
+    if (!no_clu && want <= 16 && genv == 0) {
+      if (clu_ok < 0) {
+        clu_ok = 0;
+        if (cudaFuncSetAttribute(gchol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 bytes) == cudaSuccess &&
+            cudaFuncSetAttribute(gchol_kernel<true>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+          cudaLaunchConfig_t probe{};
+          cudaLaunchAttribute pa[1];
+          pa[0].id = cudaLaunchAttributeClusterDimension;
+          pa[0].val.clusterDim.x = 16;
+          pa[0].val.clusterDim.y = 1;
+          pa[0].val.clusterDim.z = 1;
+          probe.gridDim = dim3(16);
+          probe.blockDim = dim3(kGcThreads);
+          probe.dynamicSmemBytes = bytes;
+          probe.attrs = pa;
+          probe.numAttrs = 1;
+          int ncl = 0;
+          if (cudaOccupancyMaxActiveClusters(&ncl, gchol_kernel<true>, &probe) == cudaSuccess &&
+              ncl >= 1)
+            clu_ok = 1;
+        }
+        cudaGetLastError();
+      }
+      if (clu_ok == 1) {
+        const int S = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(16, want)));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(S);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(static_cast<unsigned>(S));
+        cfg.blockDim = dim3(kGcThreads);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        RSVD_CUDA(cudaLaunchKernelEx(&cfg, gchol_kernel<true>, ga));
+        RSVD_LAUNCH("gchol_kernel");
+        return;
+      }
+    }
     void* args[] = {&ga};
-    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel), dim3(g),
+    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel<false>), dim3(g),
                                           dim3(kGcThreads), args, bytes, st));
     RSVD_LAUNCH("gchol_kernel");
     if (std::getenv("RSVD_GCHOL_TRACE")) {
