@@ -199,7 +199,7 @@ struct rsvd_context {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::unique_ptr<rsvd::Reducer> red;  // row-sharded calls (NCCL or in-process group)
   // Host-pointer pipelining: copy-in / copy-out streams and per-slot events.
-  cudaStream_t s_in = nullptr, s_out = nullptr, s_c2 = nullptr, s_c3 = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_c2 = nullptr, s_c3 = nullptr, s_c4 = nullptr;
   static constexpr int kMaxChunks = 16;
   cudaEvent_t ev_slot_in[kMaxChunks] = {}, ev_slot_comp[kMaxChunks] = {},
               ev_slot_out[kMaxChunks] = {};
@@ -209,6 +209,7 @@ struct rsvd_context {
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_c2, cudaStreamNonBlocking));
     RSVD_CUDA(cudaStreamCreateWithFlags(&s_c3, cudaStreamNonBlocking));
+    RSVD_CUDA(cudaStreamCreateWithFlags(&s_c4, cudaStreamNonBlocking));
     for (int i = 0; i < kMaxChunks; ++i) {
       RSVD_CUDA(cudaEventCreateWithFlags(&ev_slot_in[i], cudaEventDisableTiming));
       RSVD_CUDA(cudaEventCreateWithFlags(&ev_slot_comp[i], cudaEventDisableTiming));
@@ -221,6 +222,7 @@ struct rsvd_context {
     cudaStreamDestroy(s_out);
     cudaStreamDestroy(s_c2);
     cudaStreamDestroy(s_c3);
+    cudaStreamDestroy(s_c4);
     for (int i = 0; i < kMaxChunks; ++i) {
       cudaEventDestroy(ev_slot_in[i]);
       cudaEventDestroy(ev_slot_comp[i]);
@@ -700,11 +702,11 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   if (h->arena.base != before) h->drop_graphs();
   Carver cv{h->arena.base};
   layout(cv);
-  cudaStream_t cs[3] = {st, h->s_c2, h->s_c3};
+  cudaStream_t cs[4] = {st, h->s_c2, h->s_c3, h->s_c4};
   static const int nstreams = [] {
     const char* e = std::getenv("RSVD_PIPE_STREAMS");
     const int v = e ? std::atoi(e) : 3;
-    return v == 2 ? 2 : 3;
+    return v < 2 ? 2 : (v > 4 ? 4 : v);
   }();
   // Order the side streams after whatever the caller queued on its stream.
   RSVD_CUDA(cudaEventRecord(h->ev_in, st));
@@ -712,6 +714,7 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   RSVD_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c2, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c3, h->ev_in, 0));
+  RSVD_CUDA(cudaStreamWaitEvent(h->s_c4, h->ev_in, 0));
   // RSVD_PIPE_TRACE: event timeline of the chunks (ms from the call start).
   static const bool trace = std::getenv("RSVD_PIPE_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
@@ -767,6 +770,7 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   RSVD_CUDA(cudaStreamSynchronize(st));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c2));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c3));
+  RSVD_CUDA(cudaStreamSynchronize(h->s_c4));
   RSVD_CUDA(cudaStreamSynchronize(h->s_in));
   if (trace && !tev.empty()) {
     // h2d ends per chunk, then per chunk: compute start, compute end, d2h end
