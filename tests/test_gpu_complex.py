@@ -460,3 +460,33 @@ def test_pinned_host_calls_replay_graph(cuda, oracle_mod, dtype):
     out = rsvd_batched(a_host, p, seeds, out=out)
     ref2 = rsvd_batched(a_host.to(cuda), p, seeds)
     assert torch.equal(out.sigma, ref2.sigma.cpu())
+
+
+@pytest.mark.parametrize("dtype", ["float64", "complex128"])
+def test_layouts_and_pointer_kinds_agree(cuda, oracle_mod, dtype):
+    """Row-major and column-major inputs, numpy and CUDA tensors, single and
+    batched entry points all give the same factorization (layout conversion
+    is part of the public API, factorize.py)."""
+    import torch
+
+    from paper_1710_01463_b200 import RsvdParams, rsvd, rsvd_batched, tsvd, tsvd_batched
+    from tests.helpers import matrix_with_spectrum
+
+    cplx = dtype == "complex128"
+    mk = zmatrix_with_spectrum if cplx else matrix_with_spectrum
+    a = mk(oracle_mod, 123, 70, 50, np.exp(-np.arange(50) / 7.0))
+    p = RsvdParams(8, 16, 2, 11)
+    base = rsvd(np.asfortranarray(a), p)
+    variants = [np.ascontiguousarray(a),                                   # numpy row-major
+                torch.from_numpy(np.ascontiguousarray(a)).to(cuda),       # torch row-major
+                torch.from_numpy(np.ascontiguousarray(a)).to(cuda).t().contiguous().t()]  # col-major
+    for v in variants:
+        f = rsvd(v, p)
+        s = f.sigma.cpu().numpy() if hasattr(f.sigma, "cpu") else np.asarray(f.sigma)
+        np.testing.assert_array_equal(s, base.sigma)
+    fb = rsvd_batched(np.stack([a, a]), p, [11, 11])
+    np.testing.assert_allclose(np.asarray(fb.item(1).sigma), base.sigma, rtol=1e-13)
+    t = tsvd(a, 8)
+    tb = tsvd_batched(np.stack([a, a]), 8)
+    np.testing.assert_allclose(np.asarray(tb.item(0).sigma), np.asarray(t.sigma), rtol=1e-13)
+    assert isometry_err(np.asarray(fb.item(0).left)) < ISO_TOL
