@@ -1740,8 +1740,11 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
       nbg += nbg & 1;
       const bool many = batch * (nbg / 2) > kNumSMs;
       if (ell <= 32 * 3) return launch_gram_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 5) return launch_gram_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 9 && many)
+      if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_GRAM_MINB1"))
+        return launch_gram_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      if (ell <= 32 * 5) return launch_gram_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+      static const bool minb1 = std::getenv("RSVD_JACOBI_GRAM_MINB1") != nullptr;
+      if (ell <= 32 * 9 && many && !minb1)
         return launch_gram_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
       if (ell <= 32 * 9) return launch_gram_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
       if (ell <= 32 * 18)
