@@ -621,8 +621,8 @@ __device__ __forceinline__ int zrr(int slot, int s, int nn) {
 // partial Gram of its row slice, the S partials are summed through DSMEM in
 // rank order (bit-identical G in every CTA), the rotations run redundantly and
 // each CTA applies V~ to its own rows of H and J (jacobi.cu's clug scheme).
-template <int R, bool CLU>
-__global__ void __launch_bounds__(512, 1)
+template <int R, bool CLU, int MINB>
+__global__ void __launch_bounds__(512, MINB)
     zjacobi_gram_kernel(const double* __restrict__ src, int64_t src_ld, int64_t src_stride,
                         int src_mode, double2* __restrict__ H, double2* __restrict__ J, int ell,
                         int lp, int nb, int64_t batch, int max_sweeps,
@@ -630,7 +630,10 @@ __global__ void __launch_bounds__(512, 1)
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   constexpr int W = 16, NC = 32, RC = 64, GP = NC + 1;
-  constexpr int PITCH = 32 * R + 2;
+  // Rows staged per CTA: the 32 R slice of a cluster, else l rounded up to
+  // 16 (C2-shaped l = 138 -> 144: 108 KB of staging, two CTAs per SM).
+  const int rows = CLU ? 32 * R : min(32 * R, (ell + 15) & ~15);
+  const int PITCH = rows + 2;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_rot;
   __shared__ unsigned long long s_mx;
@@ -643,7 +646,6 @@ __global__ void __launch_bounds__(512, 1)
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t sq = static_cast<int64_t>(lp) * lp;
   const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
-  const int rows = 32 * R;
   const int S = CLU ? static_cast<int>(cg::this_cluster().num_blocks()) : 1;
   const int crank = CLU ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   const int row0 = crank * rows;                         // this CTA's slice of the rows
@@ -839,48 +841,41 @@ __global__ void __launch_bounds__(512, 1)
         }
         __syncthreads();
         if (s_rot) {
-          // X_P <- X_P V~ (64 x 64 realified V), warp per 16-row slab, in place.
+          // (X V)_P = X_P V~ (64 x 64 realified V), warp per 16-row slab, in two
+          // halves of 32 output columns (register budget), written straight to
+          // the global I-layout matrix; Xs (the staged pair) is only read.
           auto apply_v = [&](double2* Mg) {
             const int slabs = rows / 16;
             for (int sl = warp; sl < slabs; sl += W) {
               const int r0 = sl * 16;
-              double acc[RC / 8][4];
+#pragma unroll 1
+              for (int hf = 0; hf < 2; ++hf) {
+                double acc[4][4];
 #pragma unroll
-              for (int n = 0; n < RC / 8; ++n)
+                for (int n = 0; n < 4; ++n)
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
+                  for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
 #pragma unroll 4
-              for (int kq = 0; kq < RC / 4; ++kq) {
-                const int kc = kq * 4 + t4;  // real row of V~
-                const double a0 = Xs[kc * PITCH + r0 + g], a1 = Xs[kc * PITCH + r0 + g + 8];
-                const int ka = kc >> 1, kr = kc & 1;
+                for (int kq = 0; kq < RC / 4; ++kq) {
+                  const int kc = kq * 4 + t4;  // real row of V~
+                  const double a0 = Xs[kc * PITCH + r0 + g], a1 = Xs[kc * PITCH + r0 + g + 8];
+                  const int ka = kc >> 1, kr = kc & 1;
 #pragma unroll
-                for (int n = 0; n < RC / 8; ++n) {
-                  const int cc = n * 8 + g, ca = cc >> 1, cr = cc & 1;
-                  const double2 v = Vs[ka + ca * GP];
-                  // V~[2a+ra][2c+rc]: (0,0),(1,1) Re; (0,1) Im; (1,0) -Im
-                  const double b0 = (kr == cr) ? v.x : (kr ? -v.y : v.y);
-                  zdmma(acc[n], a0, a1, b0);
-                }
-              }
-              __syncwarp();
-              if (Mg == nullptr) {
-#pragma unroll
-                for (int n = 0; n < RC / 8; ++n)
-#pragma unroll
-                  for (int qq = 0; qq < 4; ++qq) {
-                    const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                    const int cc = n * 8 + 2 * t4 + (qq & 1);
-                    Xs[cc * PITCH + r] = acc[n][qq];
+                  for (int n = 0; n < 4; ++n) {
+                    const int cc = 32 * hf + n * 8 + g, ca = cc >> 1, cr = cc & 1;
+                    const double2 v = Vs[ka + ca * GP];
+                    // V~[2a+ra][2c+rc]: (0,0),(1,1) Re; (0,1) Im; (1,0) -Im
+                    const double b0 = (kr == cr) ? v.x : (kr ? -v.y : v.y);
+                    zdmma(acc[n], a0, a1, b0);
                   }
-              } else {
-                // straight to global I-layout: (Re, Im) pairs are (qq, qq + 1)
+                }
+                // (Re, Im) of one complex column are the (qq, qq + 1) pairs
 #pragma unroll
-                for (int n = 0; n < RC / 8; ++n)
+                for (int n = 0; n < 4; ++n)
 #pragma unroll
                   for (int h2 = 0; h2 < 2; ++h2) {
                     const int r = r0 + g + h2 * 8;
-                    const int ccx = (n * 8 + 2 * t4) >> 1;  // complex column in the pair
+                    const int ccx = (32 * hf + n * 8 + 2 * t4) >> 1;  // complex column in the pair
                     const int gc = gcol(ccx);
                     if (r < lrows && gc < ell)
                       Mg[row0 + r + static_cast<int64_t>(gc) * lp] =
@@ -889,16 +884,8 @@ __global__ void __launch_bounds__(512, 1)
               }
             }
           };
-          apply_v(nullptr);
-          __syncthreads();
-          for (int e = tid; e < NC * rows; e += blockDim.x) {
-            const int cc = e / rows, r = e - cc * rows;
-            const int gc = gcol(cc);
-            if (gc < ell && r < lrows)
-              Hg[row0 + r + static_cast<int64_t>(gc) * lp] =
-                  make_double2(Xs[(2 * cc) * PITCH + r], Xs[(2 * cc + 1) * PITCH + r]);
-          }
-          __syncthreads();  // H written back: Xs is free for the J pair
+          apply_v(Hg);
+          __syncthreads();  // H written: Xs is free for the J pair
           stage(Jg);
           __syncthreads();
           apply_v(Jg);
@@ -929,14 +916,15 @@ __global__ void __launch_bounds__(512, 1)
       if (!conv[i]) sweeps_out[i] = max_sweeps;
 }
 
-template <int R, bool CLU>
+template <int R, bool CLU, int MINB>
 bool launch_zgram_t(const double* src, int64_t src_ld, int64_t src_stride, int src_mode, double* H,
                     double* J, int64_t ell, int64_t lp, int max_sweeps, int* sweeps,
                     unsigned* flags, int64_t batch, int S, cudaStream_t st) {
-  const size_t bytes = static_cast<size_t>(64) * (32 * R + 2) * sizeof(double) +
+  const int rows = CLU ? 32 * R : static_cast<int>(std::min<int64_t>(32 * R, (ell + 15) & ~int64_t(15)));
+  const size_t bytes = static_cast<size_t>(64) * (rows + 2) * sizeof(double) +
                        (CLU ? 3 : 2) * 32 * 33 * sizeof(double2) + batch * sizeof(int) + 16;
   if (bytes > 227 * 1024) return false;
-  auto kern = zjacobi_gram_kernel<R, CLU>;
+  auto kern = zjacobi_gram_kernel<R, CLU, MINB>;
   RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));
   int nb = static_cast<int>((ell + 15) / 16);
@@ -999,17 +987,17 @@ bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, 
       const int S = (R + rl - 1) / rl;
       bool ok = false;
       if (S >= 2) {
-        if (rl == 1) ok = launch_zgram_t<1, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
-        else if (rl == 2) ok = launch_zgram_t<2, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
-        else if (rl == 3) ok = launch_zgram_t<3, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
-        else ok = launch_zgram_t<5, true>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        if (rl == 1) ok = launch_zgram_t<1, true, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else if (rl == 2) ok = launch_zgram_t<2, true, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else if (rl == 3) ok = launch_zgram_t<3, true, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
+        else ok = launch_zgram_t<5, true, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, S, st);
       }
       if (ok) return true;
     }
   }
-  if (R <= 3) return launch_zgram_t<3, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
-  if (R <= 5) return launch_zgram_t<5, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
-  if (R <= 9) return launch_zgram_t<9, false>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 3) return launch_zgram_t<3, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 5) return launch_zgram_t<5, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 9) return launch_zgram_t<9, false, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
   return false;
 }
 
