@@ -848,11 +848,14 @@ __global__ void __launch_bounds__(512, MINB)
             const int slabs = rows / 16;
             for (int sl = warp; sl < slabs; sl += W) {
               const int r0 = sl * 16;
+              // two CTAs per SM (MINB 2): two passes of 32 columns in 64
+              // registers; one CTA per SM: one pass of 64 columns
+              constexpr int NH = MINB == 1 ? 1 : 2, NT = 8 / NH;
 #pragma unroll 1
-              for (int hf = 0; hf < 2; ++hf) {
-                double acc[4][4];
+              for (int hf = 0; hf < NH; ++hf) {
+                double acc[NT][4];
 #pragma unroll
-                for (int n = 0; n < 4; ++n)
+                for (int n = 0; n < NT; ++n)
 #pragma unroll
                   for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
 #pragma unroll 4
@@ -861,8 +864,8 @@ __global__ void __launch_bounds__(512, MINB)
                   const double a0 = Xs[kc * PITCH + r0 + g], a1 = Xs[kc * PITCH + r0 + g + 8];
                   const int ka = kc >> 1, kr = kc & 1;
 #pragma unroll
-                  for (int n = 0; n < 4; ++n) {
-                    const int cc = 32 * hf + n * 8 + g, ca = cc >> 1, cr = cc & 1;
+                  for (int n = 0; n < NT; ++n) {
+                    const int cc = 8 * NT * hf + n * 8 + g, ca = cc >> 1, cr = cc & 1;
                     const double2 v = Vs[ka + ca * GP];
                     // V~[2a+ra][2c+rc]: (0,0),(1,1) Re; (0,1) Im; (1,0) -Im
                     const double b0 = (kr == cr) ? v.x : (kr ? -v.y : v.y);
@@ -871,11 +874,11 @@ __global__ void __launch_bounds__(512, MINB)
                 }
                 // (Re, Im) of one complex column are the (qq, qq + 1) pairs
 #pragma unroll
-                for (int n = 0; n < 4; ++n)
+                for (int n = 0; n < NT; ++n)
 #pragma unroll
                   for (int h2 = 0; h2 < 2; ++h2) {
                     const int r = r0 + g + h2 * 8;
-                    const int ccx = (32 * hf + n * 8 + 2 * t4) >> 1;  // complex column in the pair
+                    const int ccx = (8 * NT * hf + n * 8 + 2 * t4) >> 1;  // complex column in the pair
                     const int gc = gcol(ccx);
                     if (r < lrows && gc < ell)
                       Mg[row0 + r + static_cast<int64_t>(gc) * lp] =
