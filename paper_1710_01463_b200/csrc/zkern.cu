@@ -872,6 +872,18 @@ __global__ void __launch_bounds__(512, MINB)
                     zdmma(acc[n], a0, a1, b0);
                   }
                 }
+                if (Mg == nullptr) {  // in place (one pass only: all of X_P was read)
+                  __syncwarp();
+#pragma unroll
+                  for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                      const int r = r0 + g + ((qq & 2) ? 8 : 0);
+                      const int cc = 8 * NT * hf + n * 8 + 2 * t4 + (qq & 1);
+                      Xs[cc * PITCH + r] = acc[n][qq];
+                    }
+                  continue;
+                }
                 // (Re, Im) of one complex column are the (qq, qq + 1) pairs
 #pragma unroll
                 for (int n = 0; n < NT; ++n)
@@ -887,7 +899,21 @@ __global__ void __launch_bounds__(512, MINB)
               }
             }
           };
-          apply_v(Hg);
+          if constexpr (MINB == 1) {
+            // one pass: update the staged pair in place, then write H back
+            // with coalesced column stores
+            apply_v(nullptr);
+            __syncthreads();
+            for (int e = tid; e < NC * rows; e += blockDim.x) {
+              const int cc = e / rows, r = e - cc * rows;
+              const int gc = gcol(cc);
+              if (gc < ell && r < lrows)
+                Hg[row0 + r + static_cast<int64_t>(gc) * lp] =
+                    make_double2(Xs[(2 * cc) * PITCH + r], Xs[(2 * cc + 1) * PITCH + r]);
+            }
+          } else {
+            apply_v(Hg);
+          }
           __syncthreads();  // H written: Xs is free for the J pair
           stage(Jg);
           __syncthreads();
