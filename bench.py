@@ -5,8 +5,11 @@ Default workload: config C4 of BASELINE.json — a batch of 32 independent
 4096 x 4096 FP64 bond matrices (chi=256, d=16), A = U diag(sigma) V^T with
 Haar factors and sigma_i = exp(-0.02 i)(1 + 0.1 g_i), truncated to k=256 with
 p=20 (l = 276) and q=2.  It is "4096^2, k=256", fits one GPU and shards by
-item: under torchrun every rank factorizes its own 32 matrices (items
-rank*32 .. rank*32+31), no collective on the data path -> scaling "weak".
+item: at N GPUs the 32 matrices are split contiguously across the ranks (32/N
+each, sharding.batch_partition), no collective on the data path -> scaling
+"strong" (BASELINE: "batched across 8 GPUs"; `--weak` gives every rank its
+own full batch instead).  `--gpus N` without torchrun re-launches itself
+under torch.distributed.run with N ranks (127.0.0.1).
 
   value  : truncations/s over all ranks, inputs resident in HBM, device time
            (CUDA events on the launching stream, max over ranks).
@@ -14,12 +17,15 @@ rank*32 .. rank*32+31), no collective on the data path -> scaling "weak".
            (H2D of A and D2H of U, S, Vt inside every timed step).
   roofline: the dominant kernel (the DMMA A-pass GEMM) against the measured
            FP64 tensor peak.
-  cpu_baseline: the CPU oracle (restated reference rsvd, OpenBLAS/LAPACK) on
-           the host cores, rank 0 at N=1, on a bounded sample.
+  cpu_baseline: the reference's own rsvd (proj/src/factorize.cpp + lapack.cpp
+           compiled unmodified into oracle/_ref/librlftn_ref.so, OpenBLAS
+           LAPACK) on the host cores, rank 0 at N=1, on a bounded sample.
 
-`--impl reference` times the reference's CPU implementation of the path
-(the oracle port; the reference itself needs Eigen and cannot be built here)
-on the same config with all host threads.
+`--impl reference` times that same reference build on the same config with
+all host threads.  Its process never touches CUDA or librsvd_b200.so: the
+sample input is synthesised on the host (CounterRng Gaussians from the
+reference's own generator, torch CPU QR), and the run checks its own
+/proc/self/maps before printing.
 """
 import argparse
 import json
@@ -133,16 +139,27 @@ def make_inputs(cfg, items, first_item, device):
     return synth.make_batch(cfg, device=device, batch=items, first_item=first_item)
 
 
-def cpu_oracle_rsvd(A_items, cfg, seeds, threads):
-    """Time the oracle rsvd on host copies of the given items; returns
-    (seconds per truncation list)."""
-    from oracle import oracle
+def cpu_checker():
+    """The reference build (oracle/_ref/librlftn_ref.so) when present -- kind
+    "reference" -- else the restatement port (bitwise equal to it,
+    tests/test_ref_pin_cpu.py) -- kind "port"."""
+    from oracle import oracle, ref
 
-    oracle.set_threads(threads)
+    if ref.available():
+        return ref, "reference", ("reference rsvd: proj/src/factorize.cpp + lapack.cpp compiled "
+                                  "unmodified (oracle/_ref), OpenBLAS 0.3.31 LAPACK")
+    return oracle, "port", "oracle rsvd (restated reference, OpenBLAS 0.3.31 LAPACK)"
+
+
+def cpu_ref_rsvd(A_items, cfg, seeds, threads):
+    """Time the reference rsvd on host copies of the given items; returns
+    (seconds per truncation list)."""
+    mod, _, _ = cpu_checker()
+    mod.set_threads(threads)
     times = []
     for a, s in zip(A_items, seeds):
         t0 = time.perf_counter()
-        oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s)
+        mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, s)
         times.append(time.perf_counter() - t0)
     return times
 
@@ -173,69 +190,127 @@ def cpu_modes(A_items, cfg, seeds, threads, budget_s):
     for both methods -- rsvd and full-SVD truncation (tsvd = dgesdd +
     truncate) -- on the first matrix of the sample; each mode is skipped once
     the accumulated CPU time passes `budget_s`."""
-    from oracle import oracle
-
+    mod, _, _ = cpu_checker()
     a, s = A_items[0], seeds[0]
     out, spent = {}, 0.0
-    for name, fn, th in (("rsvd_1thread", lambda: oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), 1),
-                         ("rsvd_all_cores", lambda: oracle.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), threads),
-                         ("tsvd_all_cores", lambda: oracle.tsvd(a, cfg.rank), threads),
-                         ("tsvd_1thread", lambda: oracle.tsvd(a, cfg.rank), 1)):
+    for name, fn, th in (("rsvd_1thread", lambda: mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), 1),
+                         ("rsvd_all_cores", lambda: mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, s), threads),
+                         ("tsvd_all_cores", lambda: mod.tsvd(a, cfg.rank), threads),
+                         ("tsvd_1thread", lambda: mod.tsvd(a, cfg.rank), 1)):
         if spent > budget_s:
             out[name] = None
             continue
-        oracle.set_threads(th)
+        mod.set_threads(th)
         t0 = time.perf_counter()
         fn()
         dt = time.perf_counter() - t0
         spent += dt
         out[name] = {"value": 1.0 / dt, "unit": "truncations/s", "cores": th}
-    oracle.set_threads(threads)
+    mod.set_threads(threads)
     return out
 
 
+METRIC = "FP64 RSVD truncations/sec (4096^2, k=256)"
+DATA = "synthetic (BASELINE.json config recipe, seeded CounterRng, Haar factors)"
+
+
+def batch_config(cfg, world, count_per_rank, global_batch, weak):
+    """The `config` object of a batch-split line -- shared verbatim by the GPU
+    arm and the reference arm (same workload, same N)."""
+    return {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": count_per_rank,
+            "global_batch": global_batch, "rank_k": cfg.rank, "ell": cfg.ell,
+            "power_q": cfg.power,
+            "parallelism": (f"batch replicated dp{world} (weak)" if weak
+                            else f"batch split dp{world}"),
+            "l2": l2_note(count_per_rank * cfg.m * cfg.n * 8)}
+
+
+def rowshard_config(cfg, world, rows_per_rank):
+    return {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "rank_k": cfg.rank,
+            "ell": cfg.ell, "power_q": cfg.power,
+            "parallelism": f"row shard x{world} (NCCL all-reduce of Grams / A^T Q panels)",
+            "rows_per_rank": rows_per_rank, "l2": l2_note(rows_per_rank * cfg.n * 8)}
+
+
+def rowsharded(args, world, cfg):
+    return args.rowshard or (world > 1 and cfg.batch == 1)
+
+
+def loaded_shared_objects():
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")
+                           or ".so." in ln})
+    except OSError:
+        return []
+
+
 def run_reference(args, rank, world):
+    """The reference's own rsvd (oracle/_ref: proj/src/factorize.cpp + lapack.cpp
+    compiled unmodified) on the host cores, on the GPU arm's config.  Rank 0
+    alone runs under torchrun; CUDA and librsvd_b200.so are never touched."""
     if rank != 0:
         return 0
     import numpy as np
     import torch
 
-    from paper_1710_01463_b200 import synth
+    from paper_1710_01463_b200 import sharding, synth
 
+    mod, kind, what = cpu_checker()
     cfg = synth.CONFIGS[args.config]
     threads = host_threads()
     sample = max(1, args.ref_sample)
-    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
-    gauss = None
-    if dev == "cpu":
-        from oracle import oracle
-        gauss = lambda seed, count: torch.from_numpy(oracle.fill_gaussian(seed, count))  # noqa
-    A = synth.make_batch(cfg, device=dev, batch=sample, gauss=gauss)
-    mats = [np.asfortranarray(A[i].cpu().numpy()) for i in range(sample)]
-    del A
-    seeds = synth.omega_seeds(cfg, batch=sample)
+    # the GPU arm's workload description at this N (verbatim)
+    if rowsharded(args, world, cfg):
+        config = rowshard_config(cfg, world, sharding.row_partition(cfg.m, world, 0)[1])
+        units = 1
+    else:
+        glob = cfg.batch if args.batch is None else args.batch
+        per = glob if args.weak else sharding.batch_partition(glob, world, 0)[1]
+        config = batch_config(cfg, world, per, glob * world if args.weak else glob, args.weak)
+        units = config["global_batch"]
+    # host-side synthesis of the sample: the reference's own CounterRng
+    # Gaussians (the same streams the GPU arm draws on the device) + torch CPU QR
+    gauss = lambda seed, count: torch.from_numpy(mod.fill_gaussian(seed, count))  # noqa: E731
+    mats = [np.asfortranarray(synth.make_matrix(cfg, i, "cpu", gauss).numpy())
+            for i in range(min(sample, cfg.batch))]
+    seeds = synth.omega_seeds(cfg, batch=len(mats))
     for _ in range(args.warmup):
-        cpu_oracle_rsvd(mats[:1], cfg, seeds[:1], threads)
+        cpu_ref_rsvd(mats[:1], cfg, seeds[:1], threads)
     t = 0.0
     for _ in range(args.steps):
-        t += sum(cpu_oracle_rsvd(mats, cfg, seeds, threads))
-    value = args.steps * sample / t
+        t += sum(cpu_ref_rsvd(mats, cfg, seeds, threads))
+    value = args.steps * len(mats) / t
+    one = None
+    if args.ref_one_thread:
+        one = 1.0 / sum(cpu_ref_rsvd(mats[:1], cfg, seeds[:1], 1))
+        mod.set_threads(threads)
+    sos = loaded_shared_objects()
+    bad = [p for p in sos if "librsvd_b200" in p]
+    if bad or torch.cuda.is_initialized():
+        raise SystemExit(f"reference arm touched the GPU path: {bad}")
     line = {
         "impl": "reference",
-        "metric": "FP64 RSVD truncations/sec (4096^2, k=256)",
+        "metric": METRIC,
         "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (BASELINE.json {cfg.name} recipe, seeded CounterRng)",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": cfg.batch,
-                   "rank_k": cfg.rank, "ell": cfg.ell, "power_q": cfg.power,
-                   "step": f"{sample} truncation(s) of the workload (bounded CPU sample)"},
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": config,
+        "reference_sample": {
+            "step": f"{len(mats)} of the {units} truncation(s) of the workload per step "
+                    "(bounded CPU sample; value = truncations per second of CPU time)",
+            "input": "host-synthesised (reference CounterRng Gaussians, torch CPU QR)"},
         "cpu_baseline": {"value": value, "unit": "truncations/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{sample} of the {cfg.batch} {cfg.m}x{cfg.n} matrices per step, "
-                                   "oracle rsvd (restated reference, OpenBLAS 0.3.31 LAPACK)"},
+                         "kind": kind, "sample": f"{len(mats)} {cfg.m}x{cfg.n} matrix per step, "
+                                                 + what + ", all host threads",
+                         "rsvd_1thread": (None if one is None else
+                                          {"value": one, "unit": "truncations/s", "cores": 1,
+                                           "note": "reference protocol: BLAS pinned to one "
+                                                   "thread (lapack.cpp:225, main.cpp:7)"})},
         "e2e": {"value": value, "unit": "truncations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "loaded_native": [p for p in sos if "/oracle/" in p],
     }
     print(json.dumps(line))
     return 0
@@ -306,15 +381,12 @@ def run_rowsharded(args, rank, world, local_rank):
         falg = f_alg(cfg.m, cfg.n, cfg.rank, cfg.ell, cfg.power)
         k = cfg.rank
         print(json.dumps({
-            "metric": "FP64 RSVD truncations/sec (4096^2, k=256)",
+            "metric": METRIC,
             "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE.json config recipe, seeded CounterRng, Haar factors)",
-            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "rank_k": cfg.rank,
-                       "ell": cfg.ell, "power_q": cfg.power,
-                       "parallelism": f"row shard x{world} (NCCL all-reduce of Grams / A^T Q panels)",
-                       "rows_per_rank": count, "l2": l2_note(count * cfg.n * 8)},
+            "data": DATA,
+            "config": rowshard_config(cfg, world, sharding.row_partition(cfg.m, world, 0)[1]),
             "e2e": {"value": e2e_value, "unit": "truncations/s",
                     "h2d_bytes_per_step": count * cfg.n * 8,
                     "d2h_bytes_per_step": (count * k + k + k * cfg.n) * 8},
@@ -331,15 +403,21 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_1710_01463_b200 import Handle, RsvdParams, _lib, rsvd_batched, synth
+    from paper_1710_01463_b200 import Handle, RsvdParams, _lib, rsvd_batched, sharding, synth
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
-    B = cfg.batch if args.batch is None else args.batch
-    first = rank * B
+    glob = cfg.batch if args.batch is None else args.batch
+    if args.weak:  # every rank its own full batch (opt-in)
+        B, first, total = glob, rank * glob, glob * world
+    else:          # BASELINE: the batch is split across the GPUs (strong)
+        first, B = sharding.batch_partition(glob, world, rank)
+        total = glob
+    if B < 1:
+        raise SystemExit(f"rank {rank}: no items ({glob} over {world} ranks)")
     A = make_inputs(cfg, B, first, dev)
     seeds = synth.omega_seeds(cfg, batch=B, first_item=first)
     params = RsvdParams(cfg.rank, cfg.ell, cfg.power, 0)
@@ -412,7 +490,7 @@ def run_ours(args, rank, world, local_rank):
     launches = _lib.kernel_launches() - launches0
     clk = clocks.stop()
     ms = max_over_ranks(step_ms)
-    value = B * world * args.steps / (ms / 1000.0)
+    value = total * args.steps / (ms / 1000.0)
     ranks_ok = all(r == cfg.rank for r in f.ranks)
 
     # ---- per-stage profile pass (events around each stage) ------------
@@ -438,7 +516,7 @@ def run_ours(args, rank, world, local_rank):
         t1e.record(stream)
         torch.cuda.synchronize()
         tms = max_over_ranks(t0e.elapsed_time(t1e))
-        gpu_tsvd = {"value": B * world / (tms / 1000.0), "unit": "truncations/s", "ms_per_step": tms,
+        gpu_tsvd = {"value": total / (tms / 1000.0), "unit": "truncations/s", "ms_per_step": tms,
                     "note": "tsvd_batched (one-sided Jacobi on the full min(m,n) factor), 1 step"}
         del ft
     ap_ms = prof["apass_nn"][0] + prof["apass_tn"][0]
@@ -477,7 +555,7 @@ def run_ours(args, rank, world, local_rank):
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     if os.environ.get("RSVD_BENCH_VERBOSE"):
         print("e2e per call ms:", per_call, file=sys.stderr)
-    e2e_value = B * world * args.steps / t_e2e
+    e2e_value = total * args.steps / t_e2e
     k = max(cfg.rank, 1)
     h2d = B * cfg.m * cfg.n * 8 + B * 8
     d2h = B * (cfg.m * k + k + k * cfg.n) * 8 + B * 16
@@ -488,12 +566,12 @@ def run_ours(args, rank, world, local_rank):
         threads = host_threads()
         n_cpu = max(1, args.cpu_sample)
         mats = [np.asfortranarray(A_host[i].numpy()) for i in range(min(n_cpu, B))]
-        times = cpu_oracle_rsvd(mats, cfg, seeds[:len(mats)], threads)
+        times = cpu_ref_rsvd(mats, cfg, seeds[:len(mats)], threads)
+        _, kind, what = cpu_checker()
         cpu = {"value": len(times) / sum(times), "unit": "truncations/s", "cores": threads,
-               "kind": "port",
-               "sample": f"{len(times)} of the {B} {cfg.m}x{cfg.n} matrices, oracle rsvd "
-                         "(restated reference: cblas_dgemm + dgeqrf/dorgqr + dgesdd, "
-                         "OpenBLAS 0.3.31), all host threads"}
+               "kind": kind,
+               "sample": f"{len(times)} of the {B} {cfg.m}x{cfg.n} matrices, {what}, "
+                         "all host threads"}
         cpu["modes"] = cpu_modes(mats, cfg, seeds, threads, args.cpu_modes_budget)
         cpu["modes"]["sample"] = (f"item 0 ({cfg.m}x{cfg.n}); a mode is skipped (null) once "
                                   f"{args.cpu_modes_budget:.0f} s of CPU time were spent")
@@ -501,15 +579,12 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         falg = f_alg(cfg.m, cfg.n, cfg.rank, cfg.ell, cfg.power)
         line = {
-            "metric": "FP64 RSVD truncations/sec (4096^2, k=256)",
+            "metric": METRIC,
             "value": value, "unit": "truncations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE.json config recipe, seeded CounterRng, Haar factors)",
-            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "batch_per_rank": B,
-                       "global_batch": B * world, "rank_k": cfg.rank, "ell": cfg.ell,
-                       "power_q": cfg.power, "parallelism": f"batch split dp{world}",
-                       "l2": l2_note(B * cfg.m * cfg.n * 8)},
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": DATA,
+            "config": batch_config(cfg, world, B, total, args.weak),
             "e2e": {"value": e2e_value, "unit": "truncations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "host_memory": "pinned" if e2e_pinned else "pageable"},
             "gpu_launches": launches,
@@ -521,7 +596,7 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_flops_per_launch": ap_flops_per_launch,
                          "peak_source": FP64_PEAK_SOURCE,
                          "apass_share_of_step": ap_ms / prof_steps / step_ms_prof},
-            "pipeline": {"tflops_alg": falg * B * world * args.steps / (ms / 1000) / 1e12 / world,
+            "pipeline": {"tflops_alg": falg * total * args.steps / (ms / 1000) / 1e12 / world,
                          "frac_fp64_peak": falg * B * args.steps / (ms / 1000) / 1e12 / FP64_PEAK_TFLOPS,
                          "stage_ms_per_step": {k2: v[0] / prof_steps for k2, v in prof.items()},
                          "jacobi_sweeps": sweeps, "ranks_ok": ranks_ok},
@@ -537,6 +612,27 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
+def spawn(args) -> int:
+    """`--gpus N` outside torchrun: re-launch this script as N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1, as the driver does."""
+    import socket
+
+    if args.impl != "reference":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) visible", file=sys.stderr)
+            return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -544,15 +640,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--batch", type=int, default=None, help="override items per rank")
+    ap.add_argument("--batch", type=int, default=None, help="override the global batch")
+    ap.add_argument("--weak", action="store_true",
+                    help="every rank factorizes its own full batch (weak scaling)")
     ap.add_argument("--cpu-sample", type=int, default=2)
     ap.add_argument("--ref-sample", type=int, default=1)
+    ap.add_argument("--ref-one-thread", action=argparse.BooleanOptionalAction, default=True,
+                    help="reference arm: also time one truncation with 1 BLAS thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-modes-budget", type=float, default=45.0,
                     help="seconds of CPU time for the 1-thread / tsvd baseline modes")
     ap.add_argument("--rowshard", action="store_true",
                     help="row-sharded single-matrix path (default for C3/C5 when N > 1)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":
+            return run_reference(args, 0, args.gpus)
+        return spawn(args)
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
@@ -560,7 +664,7 @@ def main():
         return run_reference(args, rank, world)
     from paper_1710_01463_b200 import synth
 
-    if args.rowshard or (world > 1 and synth.CONFIGS[args.config].batch == 1):
+    if rowsharded(args, world, synth.CONFIGS[args.config]):
         return run_rowsharded(args, rank, world, local_rank)
     return run_ours(args, rank, world, local_rank)
 

@@ -324,7 +324,7 @@ __global__ void apply_scale_kernel(double* __restrict__ X, int64_t ld, int64_t s
 
 unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
   return static_cast<unsigned>(
-      std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * kNumSMs)));
+      std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * num_sms())));
 }
 
 }  // namespace
@@ -374,7 +374,7 @@ void launch_choose_scale(CMatRef X, int64_t rows, int64_t cols, double* scale, i
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(scale);
   RSVD_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * batch, st));
   dim3 grid(grid1(rows * cols, 256, 4), static_cast<unsigned>(batch));
-  if (batch > 1) grid.x = std::max(1u, std::min(grid.x, static_cast<unsigned>(4 * kNumSMs / batch + 1)));
+  if (batch > 1) grid.x = std::max(1u, std::min(grid.x, static_cast<unsigned>(4 * num_sms() / batch + 1)));
   maxabs_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, bits);
   RSVD_LAUNCH("maxabs_kernel");
   choose_scale_kernel<<<static_cast<unsigned>(ceil_div(batch, 256)), 256, 0, st>>>(bits, scale,

@@ -1101,17 +1101,18 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     GcholArgs ga{G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp),
                  tau, batch, opts ? *opts : CholOpts{}};
     const int bytes = kGcDiagWarps * 2 * 32 * kInvPitch * 8;
-    static int grid = 0;
+    // per device: the smem opt-in is per context, the co-resident grid per SKU
+    static std::atomic<int> grid_dev[kMaxDevices];
+    int grid = grid_dev[current_device()].load(std::memory_order_acquire);
     if (grid == 0) {
       RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bytes));
-      int per_sm = 0, dev = 0, sms = 0;
+      int per_sm = 0;
       RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel<false>, kGcThreads,
                                                               bytes));
-      RSVD_CUDA(cudaGetDevice(&dev));
-      RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       if (per_sm < 1) throw CudaError("gchol_kernel: does not fit on an SM");
-      grid = per_sm * sms;
+      grid = per_sm * num_sms();
+      grid_dev[current_device()].store(grid, std::memory_order_release);
     }
     // Size the persistent grid to the work: the widest step has one warp task
     // per (item, upper 32 x 32 tile); a full-GPU grid for a small batch (a
@@ -1124,8 +1125,10 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     if (genv > 0) g = std::min(grid, genv);
     // Small work: one cluster of 8-16 CTAs with cluster barriers.
     static const bool no_clu = std::getenv("RSVD_NO_GCHOL_CLUSTER") != nullptr;
-    static int clu_ok = -1;  // 16-CTA (non-portable) clusters available
+    // 16-CTA (non-portable) clusters available on this device: 0 unknown, 1 no, 2 yes
+    static std::atomic<int> clu_dev[kMaxDevices];
     if (!no_clu && want <= 16 && genv == 0) {
+      int clu_ok = clu_dev[current_device()].load(std::memory_order_acquire) - 1;
       if (clu_ok < 0) {
         clu_ok = 0;
         if (cudaFuncSetAttribute(gchol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1149,6 +1152,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
             clu_ok = 1;
         }
         cudaGetLastError();
+        clu_dev[current_device()].store(clu_ok + 1, std::memory_order_release);
       }
       if (clu_ok == 1) {
         const int S = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(16, want)));

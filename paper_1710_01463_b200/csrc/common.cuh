@@ -53,7 +53,37 @@ extern std::atomic<uint64_t> g_kernel_launches;
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
-constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+// Per-device facts, cached per device ordinal (thread-safe: the in-process
+// rank threads of sharding.GroupReducer and multi-device callers share them).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & (kMaxDevices - 1);
+}
+// SM count of the current device (148 on a full B200; fewer under MIG / MPS
+// limits), used for grid sizing and co-residency of cooperative launches.
+inline int num_sms() {
+  static std::atomic<int> cache[kMaxDevices];
+  const int d = current_device();
+  int v = cache[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+// Function attributes (e.g. the dynamic shared-memory opt-in) are per device
+// context: `mask` (one per kernel instantiation) records the devices on which
+// `apply` already ran.  apply() is idempotent, so a race only repeats it.
+template <class F>
+inline void once_per_device(std::atomic<uint64_t>& mask, F&& apply) {
+  const uint64_t bit = 1ull << current_device();
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  apply();
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 // ---------------------------------------------------------------- kernels
 // Launch wrappers (defined in the .cu files).  All are batched and

@@ -1101,7 +1101,7 @@ void recon_impl(rsvd_context* h, const double* A, int64_t m, int64_t n, int64_t 
   RSVD_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
   const int64_t rr = std::max<int64_t>(r, 1);
-  const int64_t nparts = 4 * kNumSMs;
+  const int64_t nparts = 4 * num_sms();
   Carver meas{nullptr};
   auto layout = [&](Carver& c, double*& Ad, double*& Us, double*& Vd, double*& Sd, double*& R,
                     double*& part, double*& pg) {

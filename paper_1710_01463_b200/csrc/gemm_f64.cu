@@ -285,12 +285,11 @@ template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRA
 void launch_cfg(const GemmArgs& a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC>;
   auto kern = dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, VEC, MINB>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  once_per_device(attr_set, [&] {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(Cfg::kSmemBytes)));
-    attr_set = true;
-  }
+  });
   dim3 grid(static_cast<unsigned>(ceil_div(a.N, BN)), static_cast<unsigned>(ceil_div(a.M, BM)),
             static_cast<unsigned>(a.batch * a.splits));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(a);
@@ -320,7 +319,7 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   else c.bn = (8 * w96 <= 9 * w64) ? 96 : 64;
   c.bm = (M <= 64) ? 64 : 128;
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
-  const int64_t target = 2 * kNumSMs;  // two resident CTAs per SM
+  const int64_t target = 2 * num_sms();  // two resident CTAs per SM
   int64_t splits = 1;
   if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / 256));
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
@@ -382,7 +381,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 int64_t sq96_splits(int64_t M, int64_t K, int64_t batch) {
   static const bool old = std::getenv("RSVD_GRAM_SPLIT_OLD") != nullptr;
   const int64_t t = M / 96, tiles = t * (t + 1) / 2 * batch;
-  const int64_t slots = 2 * kNumSMs;
+  const int64_t slots = 2 * num_sms();
   const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / 256));
   if (old) {
     int64_t sp = 1;
@@ -482,14 +481,14 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   if (c.splits > 1) {
     const int64_t total = M * N * batch;
     const int threads = 256;
-    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, threads), 8 * kNumSMs));
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, threads), 8 * num_sms()));
     splitk_reduce_kernel<<<blocks, threads, 0, st>>>(partial, M, N, c.splits, batch, C.base, C.ld,
                                                      C.stride, opt.item_mask);
     RSVD_LAUNCH("splitk_reduce_kernel");
   }
   if (a.c_upper) {  // symmetric result: mirror the upper triangle
     const int64_t total = M * M * batch;
-    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * num_sms()));
     mirror_upper_kernel<<<blocks, 256, 0, st>>>(C.base, M, C.ld, C.stride, batch, opt.item_mask);
     RSVD_LAUNCH("mirror_upper_kernel");
   }

@@ -264,12 +264,11 @@ template <int STAGES, bool TRANS_A, int BM = kBM, int BN = kBN, int WM = kWM, in
 void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& a, cudaStream_t st) {
   auto kern = dgemm_tma_kernel<BM, BN, WM, WN, STAGES, TRANS_A>;
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * kTBK * 8 + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(bytes)));
-    attr = true;
-  }
+  });
   dim3 grid(static_cast<unsigned>(ceil_div(a.N, BN)), static_cast<unsigned>(ceil_div(a.M, BM)),
             static_cast<unsigned>(a.batch * a.splits));
   kern<<<grid, WM * WN * 32, bytes, st>>>(ma, mb, a);

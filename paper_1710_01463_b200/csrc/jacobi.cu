@@ -1699,7 +1699,7 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
   // Per step the cluster barrier competes with the per-CTA rotation work:
   // 5-6 CTAs per task measured best (C3: S 3/5/9 -> 4.6/4.4/4.8 ms, C5:
   // S 3/5/9 -> 11.1/9.7/18.7 ms -- at 9 the clusters no longer fit at once).
-  int smax = static_cast<int>(std::min<int64_t>(6, kNumSMs / std::max<int64_t>(tasks, 1)));
+  int smax = static_cast<int>(std::min<int64_t>(6, num_sms() / std::max<int64_t>(tasks, 1)));
   if (const char* e = std::getenv("RSVD_JACOBI_CLUSTER")) smax = std::atoi(e);
   if (smax < 2) return false;
   int rl = (R + smax - 1) / smax;
@@ -1738,7 +1738,7 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
       // Gram-accelerated task steps (jacobi_gram_kernel).
       int nbg = static_cast<int>((ell + 15) / 16);
       nbg += nbg & 1;
-      const bool many = batch * (nbg / 2) > kNumSMs;
+      const bool many = batch * (nbg / 2) > num_sms();
       if (ell <= 32 * 3) return launch_gram_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
       if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_GRAM_MINB1"))
         return launch_gram_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
@@ -1758,11 +1758,11 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
     // 128-register instantiations do not spill.
     int nbt = static_cast<int>((ell + 15) / 16);
     nbt += nbt & 1;
-    const bool few = batch * (nbt / 2) <= kNumSMs;
+    const bool few = batch * (nbt / 2) <= num_sms();
     // Fewer tasks than SMs / 4: split every task's rows over a cluster (with
     // more tasks the clusters would occupy most SMs, which costs more than it
     // saves when another stream's GEMMs run beside, e.g. the host pipeline).
-    if (batch * (nbt / 2) * 4 <= kNumSMs &&
+    if (batch * (nbt / 2) * 4 <= num_sms() &&
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
     if (few && ell <= 32 * 5) return launch_cyc_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
@@ -1797,7 +1797,7 @@ void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_swee
   {
     int nbt = static_cast<int>((ell + 15) / 16);
     nbt += nbt & 1;
-    if (batch * (nbt / 2) * 4 <= kNumSMs &&
+    if (batch * (nbt / 2) * 4 <= num_sms() &&
         launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
       return;
   }

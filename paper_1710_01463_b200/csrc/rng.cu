@@ -87,7 +87,7 @@ void launch_fill_gaussian(MatRef out, int64_t rows, int64_t cols, int64_t valid_
   if (rows <= 0 || cols <= 0 || batch <= 0) return;
   const int64_t work = ((rows * valid_cols + 1) / 2 + rows * (cols - valid_cols)) * batch;
   const int threads = 256;
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(work, threads), 16 * kNumSMs));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(work, threads), 16 * num_sms()));
   fill_gaussian_kernel<<<blocks, threads, 0, st>>>(out.base, out.ld, out.stride, rows, cols,
                                                    valid_cols, seeds_dev, batch);
   RSVD_LAUNCH("fill_gaussian_kernel");
@@ -97,7 +97,7 @@ void launch_fill_gaussian_flat(double* out, int64_t count, uint64_t seed, cudaSt
   if (count <= 0) return;
   const int threads = 256;
   const int blocks =
-      static_cast<int>(std::min<int64_t>(ceil_div((count + 1) / 2, threads), 16 * kNumSMs));
+      static_cast<int>(std::min<int64_t>(ceil_div((count + 1) / 2, threads), 16 * num_sms()));
   fill_flat_kernel<<<blocks, threads, 0, st>>>(out, count, seed);
   RSVD_LAUNCH("fill_flat_kernel");
 }

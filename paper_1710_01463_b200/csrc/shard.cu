@@ -141,7 +141,7 @@ struct GroupReducer final : Reducer {
       }
       SlotPtrs sp{};
       for (int r = 0; r < g->n; ++r) sp.p[r] = g->slots[r];
-      const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(count, 256), 8 * kNumSMs));
+      const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()));
       group_sum_kernel<<<std::max(blocks, 1), 256, 0, st>>>(sp, g->n, count, g->sum);
       RSVD_LAUNCH("group_sum_kernel");
       RSVD_CUDA(cudaStreamSynchronize(st));

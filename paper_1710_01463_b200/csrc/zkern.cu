@@ -34,7 +34,7 @@ __device__ __forceinline__ double uniform_from(uint64_t w) {
 
 unsigned grid_for(int64_t work, int threads, int cap_per_sm = 8) {
   return static_cast<unsigned>(
-      std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * kNumSMs)));
+      std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * num_sms())));
 }
 
 // ---------------------------------------------------------------- Omega
@@ -985,7 +985,7 @@ bool launch_zgram_t(const double* src, int64_t src_ld, int64_t src_stride, int s
     int per_sm = 0;
     RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
     if (per_sm < 1) return false;
-    grid = std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * kNumSMs));
+    grid = std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * num_sms()));
   }
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   int ell_i = static_cast<int>(ell), lp_i = static_cast<int>(lp);
@@ -1007,9 +1007,9 @@ bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, 
   const int64_t tasks = batch * (nb / 2);
   const int R = static_cast<int>((ell + 31) / 32);
   static const bool no_clu = std::getenv("RSVD_NO_ZGRAM_CLUSTER") != nullptr;
-  if (!no_clu && tasks * 4 <= kNumSMs && R >= 2) {
+  if (!no_clu && tasks * 4 <= num_sms() && R >= 2) {
     // Few tasks: split each task's rows over a cluster of S <= 6 CTAs.
-    const int smax = static_cast<int>(std::min<int64_t>(6, kNumSMs / std::max<int64_t>(tasks, 1)));
+    const int smax = static_cast<int>(std::min<int64_t>(6, num_sms() / std::max<int64_t>(tasks, 1)));
     if (smax >= 2) {
       int rl = (R + smax - 1) / smax;
       rl = rl <= 1 ? 1 : (rl <= 2 ? 2 : (rl <= 3 ? 3 : 5));
@@ -1061,7 +1061,7 @@ void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int s
   // Cluster size: fill the SMs (S CTAs per item, at most 8, portable) but
   // never more warps than the l/2 pairs of a step.
   const int64_t pairs = (ell + 1) / 2;
-  int S = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, kNumSMs / batch)));
+  int S = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, num_sms() / batch)));
   S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, ceil_div(pairs, 16))));
   if (const char* e = std::getenv("RSVD_ZJACOBI_CLUSTER")) S = std::max(1, std::min(8, std::atoi(e)));
   const int e = static_cast<int>(ell);

@@ -36,3 +36,21 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="session")
+def ref_mod():
+    """The reference's own factorize.cpp / lapack.cpp / blocks.cpp, compiled
+    unmodified into oracle/_ref/librlftn_ref.so (oracle/Makefile `ref`).  The
+    parity anchor: missing it is a failure, not a skip."""
+    from oracle import ref
+
+    if not ref.available():
+        from oracle import oracle
+
+        oracle.build()
+    if not ref.available():
+        pytest.fail("oracle/_ref/librlftn_ref.so is missing: run `make -C oracle ref` "
+                    "where /root/reference exists (build() does)")
+    ref.set_threads(min(os.cpu_count() or 1, 16))
+    return ref

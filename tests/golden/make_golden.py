@@ -5,8 +5,10 @@
                     six seeds, produced by the REFERENCE's own rng.hpp
                     (oracle/_ref/rng_kat, compiled from
                     /root/reference/proj/include/rlftn/rng.hpp).
-  rsvd_small.npz  : small rsvd/tsvd known-answer cases computed by the oracle
-                    restatement (oracle/liboracle.so) on CounterRng inputs.
+  rsvd_small.npz  : small rsvd/tsvd known-answer cases computed by the
+                    REFERENCE's own factorize.cpp/lapack.cpp compiled unmodified
+                    (oracle/_ref/librlftn_ref.so, 1 BLAS thread as lapack.cpp:225)
+                    on CounterRng inputs; the restatement must agree bitwise.
   zrsvd_small.npz : the same cases for the complex instantiation
                     (rsvd/tsvd<std::complex<double>>, complex CounterRng inputs).
 """
@@ -21,6 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
 from oracle import oracle  # noqa: E402
+from oracle import ref  # noqa: E402
 
 
 def spectrum_family(family, n):
@@ -84,6 +87,10 @@ def zbuild_case(i, rows, cols, spec):
     return np.asfortranarray((u * s[None, :]) @ v.conj().T)
 
 
+def _same(x, y, name):
+    assert all(np.array_equal(p, q) for p, q in zip(x[:3], y[:3])) and x[3] == y[3], name
+
+
 def main():
     oracle.build()
     kat = oracle.reference_rng_kat(64, 257)
@@ -92,11 +99,13 @@ def main():
     with open(os.path.join(HERE, "rng_kat.json"), "w") as f:
         json.dump(kat, f, indent=1)
     oracle.set_threads(1)
+    ref.set_threads(1)
     out = {}
     for i, (name, rows, cols, spec, k, ell, q, seed) in enumerate(CASES):
         a = build_case(i, rows, cols, spec)
-        U, S, Vt, dw = oracle.rsvd(a, k, ell, q, seed)
-        Ut, St, Vtt, dwt = oracle.tsvd(a, k)
+        U, S, Vt, dw = ref.rsvd(a, k, ell, q, seed)
+        Ut, St, Vtt, dwt = ref.tsvd(a, k)
+        _same(oracle.rsvd(a, k, ell, q, seed), (U, S, Vt, dw), name)
         out[f"{name}/a"] = a
         out[f"{name}/params"] = np.array([k, ell, q, seed], dtype=np.uint64)
         out[f"{name}/U"] = U
@@ -111,8 +120,9 @@ def main():
     zout = {}
     for i, (name, rows, cols, spec, k, ell, q, seed) in enumerate(CASES):
         a = zbuild_case(i, rows, cols, spec)
-        U, S, Vt, dw = oracle.zrsvd(a, k, ell, q, seed)
-        Ut, St, Vtt, dwt = oracle.ztsvd(a, k)
+        U, S, Vt, dw = ref.rsvd(a, k, ell, q, seed)
+        Ut, St, Vtt, dwt = ref.tsvd(a, k)
+        _same(oracle.zrsvd(a, k, ell, q, seed), (U, S, Vt, dw), name)
         zout[f"{name}/a"] = a
         zout[f"{name}/params"] = np.array([k, ell, q, seed], dtype=np.uint64)
         zout[f"{name}/U"] = U

@@ -52,12 +52,12 @@ def test_tsvd_geometric_spectrum(cuda, oracle_mod):  # test_factorize.cpp:57-71
 @pytest.mark.parametrize("m,n,chi", [(40, 25, 8), (25, 40, 8), (64, 64, 64), (200, 96, 30),
                                      (96, 300, 50), (17, 5, 9), (1, 7, 3), (7, 1, 3),
                                      (576, 600, 100)])
-def test_tsvd_vs_oracle(cuda, oracle_mod, m, n, chi):
+def test_tsvd_vs_oracle(cuda, oracle_mod, m, n, chi, ref_mod):
     from paper_1710_01463_b200 import tsvd
 
     a = oracle_mod.gaussian_matrix(1000 + m + 7 * n, m, n)
     f = tsvd(a, chi)
-    U, S, Vt, dw = oracle_mod.tsvd(a, chi)
+    U, S, Vt, dw = ref_mod.tsvd(a, chi)
     assert f.rank() == len(S)
     assert rel_sigma_err(f.sigma, S) < SIG_TOL
     assert isometry_err(f.left) < ISO_TOL and isometry_err(f.right_adj.T) < ISO_TOL
@@ -90,7 +90,7 @@ def test_tsvd_invalid(cuda):  # factorize.cpp:44-45
         tsvd(np.eye(4), 0)
 
 
-def test_tsvd_batched_and_device(cuda, oracle_mod):
+def test_tsvd_batched_and_device(cuda, oracle_mod, ref_mod):
     import torch
 
     from paper_1710_01463_b200 import tsvd, tsvd_batched
@@ -100,7 +100,7 @@ def test_tsvd_batched_and_device(cuda, oracle_mod):
     at = torch.from_numpy(np.stack(items)).to(cuda)
     bd = tsvd_batched(at, 12)
     for b, a in enumerate(items):
-        U, S, Vt, dw = oracle_mod.tsvd(a, 12)
+        U, S, Vt, dw = ref_mod.tsvd(a, 12)
         fb = bf.item(b)
         assert fb.discarded_exact
         assert rel_sigma_err(fb.sigma, S) < SIG_TOL
@@ -243,7 +243,7 @@ def test_block_rank_zero_sector(cuda):  # test_blocks.cpp:260-279
 
 @pytest.mark.parametrize("kind", ["tsvd", "rsvd"])
 @pytest.mark.parametrize("device", [False, True])
-def test_block_many_sectors_vs_oracle(cuda, oracle_mod, kind, device):
+def test_block_many_sectors_vs_oracle(cuda, oracle_mod, kind, device, ref_mod):
     """A TEBD-like bond: 7 sectors, three sharing one shape (one batched engine
     call), ragged others, a sector below rsvd_min_dim, one zero-width sector;
     per-sector results against the oracle's block_factorize."""
@@ -266,7 +266,7 @@ def test_block_many_sectors_vs_oracle(cuda, oracle_mod, kind, device):
     if device:
         ins[-1] = np.zeros((0, 12))  # empty sector stays on the host path
     f = block_factorize(BlockDiagMatrix(charges, ins), chi, _req(), meth)
-    ref, dw, exact = oracle_mod.block_factorize(blocks, charges, chi, kind=kind, power=3,
+    ref, dw, exact = ref_mod.block_factorize(blocks, charges, chi, kind=kind, power=3,
                                                 seed=4242)
     assert f.discarded_exact == exact
     assert f.total_rank() == sum(len(x[1]) for x in ref)
@@ -281,7 +281,7 @@ def test_block_many_sectors_vs_oracle(cuda, oracle_mod, kind, device):
     assert f.discarded_weight == pytest.approx(dw, rel=1e-8)
 
 
-def test_tsvd_rank_deficient_graded_block(cuda, oracle_mod):
+def test_tsvd_rank_deficient_graded_block(cuda, oracle_mod, ref_mod):
     """A TEBD sector block (24 x 21, numerical rank 15, values 0.79 .. 5e-15)
     captured from the bond-update tests: every value to O(u ||A||)
     absolutely, like the oracle's gesdd."""
@@ -290,7 +290,7 @@ def test_tsvd_rank_deficient_graded_block(cuda, oracle_mod):
     from paper_1710_01463_b200 import tsvd
 
     a = np.load(os.path.join(os.path.dirname(__file__), "golden", "theta_rankdef_24x21.npy"))
-    _, S, _, dw = oracle_mod.tsvd(a, 100)
+    _, S, _, dw = ref_mod.tsvd(a, 100)
     for x in (a, a.T.copy()):
         f = tsvd(x, 100)
         assert f.rank() == len(S)

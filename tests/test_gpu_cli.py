@@ -50,7 +50,7 @@ def test_factorize_randomized_reproducible(cuda, tmp_path):  # test_cli.cpp:98-1
     assert v1 == pytest.approx(3.0, rel=1e-12) and v2 == pytest.approx(2.0, rel=1e-12)
 
 
-def test_factorize_matches_oracle_and_env_out(cuda, tmp_path, oracle_mod):
+def test_factorize_matches_oracle_and_env_out(cuda, tmp_path, oracle_mod, ref_mod):
     """A CSV input through the CLI equals the library call; RLFTN_OUT wins."""
     from paper_1710_01463_b200 import RsvdParams, derive_seed, rsvd
 
@@ -64,11 +64,11 @@ def test_factorize_matches_oracle_and_env_out(cuda, tmp_path, oracle_mod):
     got = np.array([float(x) for x in (env_out / "spectrum.csv").read_text().split(",")])
     ref = rsvd(a, RsvdParams(7, 14, 2, derive_seed(9, 2)))
     np.testing.assert_array_equal(got, ref.sigma)
-    _, S, _, _ = oracle_mod.rsvd(a, 7, 14, 2, derive_seed(9, 2))
+    _, S, _, _ = ref_mod.rsvd(a, 7, 14, 2, derive_seed(9, 2))
     np.testing.assert_allclose(got, S, rtol=1e-10)
 
 
-def test_factorize_complex_file(cuda, tmp_path, oracle_mod):
+def test_factorize_complex_file(cuda, tmp_path, oracle_mod, ref_mod):
     """Complex input runs the complex instantiation (cli.cpp:185-240 visits
     MatrixC): complex factors in left.bin / right.bin, "complex": true."""
     from tests.helpers import zmatrix_with_spectrum
@@ -91,7 +91,7 @@ def test_factorize_complex_file(cuda, tmp_path, oracle_mod):
         else:  # a randomized approximation: compare with the restated reference
             from paper_1710_01463_b200 import derive_seed
 
-            _, S, _, _ = oracle_mod.zrsvd(a, 6, 12, 2, derive_seed(1, 2))
+            _, S, _, _ = ref_mod.rsvd(a, 6, 12, 2, derive_seed(1, 2))
             np.testing.assert_allclose(got, S, rtol=1e-10)
         rec = left @ np.diag(got) @ right
         assert np.linalg.norm(a - rec) == pytest.approx(j["frobenius_error"], rel=1e-8)

@@ -69,13 +69,13 @@ def _spectrum(spec):
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}k{c[3]}l{c[4]}q{c[5]}" for c in CASES])
-def test_complex_rsvd_matches_oracle(cuda, oracle_mod, case):
+def test_complex_rsvd_matches_oracle(cuda, oracle_mod, case, ref_mod):
     from paper_1710_01463_b200 import RsvdParams, rsvd
 
     rows, cols, spec, k, ell, q, seed = case
     a = zmatrix_with_spectrum(oracle_mod, seed + 1, rows, cols, _spectrum(spec))
     f = rsvd(a, RsvdParams(k, ell, q, seed))
-    ref = oracle_mod.zrsvd(a, k, ell, q, seed)
+    ref = ref_mod.rsvd(a, k, ell, q, seed)
     check_against(a, f, ref, str(case))
 
 
@@ -97,7 +97,7 @@ def test_complex_omega_matches_reference_stream(cuda, oracle_mod):
 
 
 @pytest.mark.parametrize("r", [3, 7])
-def test_complex_exact_rank_reconstructs(cuda, oracle_mod, r):
+def test_complex_exact_rank_reconstructs(cuda, oracle_mod, r, ref_mod):
     # test_factorize.cpp:105-120 (complex half): rank-deficient sample Y.
     from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
 
@@ -107,7 +107,7 @@ def test_complex_exact_rank_reconstructs(cuda, oracle_mod, r):
     assert reconstruction_error(a, f) <= 1e-10 * np.linalg.norm(a)
     assert f.rank() <= 10
     assert isometry_err(np.asarray(f.left)) < ISO_TOL
-    ref = oracle_mod.zrsvd(a, 10, 20, 4, 5)
+    ref = ref_mod.rsvd(a, 10, 20, 4, 5)
     assert f.rank() == len(ref[1])
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
 
@@ -127,7 +127,7 @@ def test_complex_tsvd_and_rsvd_agree(cuda, oracle_mod):
 
 
 @pytest.mark.parametrize("shape", [(40, 25), (25, 40), (64, 64), (130, 97)])
-def test_complex_tsvd_matches_oracle(cuda, oracle_mod, shape):
+def test_complex_tsvd_matches_oracle(cuda, oracle_mod, shape, ref_mod):
     from paper_1710_01463_b200 import tsvd
 
     m, n = shape
@@ -136,7 +136,7 @@ def test_complex_tsvd_matches_oracle(cuda, oracle_mod, shape):
     a = zmatrix_with_spectrum(oracle_mod, 3 * m + n, m, n, sigma)
     for chi in (1, 7, p):
         f = tsvd(a, chi)
-        ref = oracle_mod.ztsvd(a, chi)
+        ref = ref_mod.tsvd(a, chi)
         check_against(a, f, ref, f"{shape} chi={chi}", dw_rel=1e-8)
         assert f.discarded_exact
     # Graded to 1e-7: like gesdd, the tiny values are accurate to O(u ||A||)
@@ -144,25 +144,25 @@ def test_complex_tsvd_matches_oracle(cuda, oracle_mod, shape):
     steep = np.exp(-np.arange(p) / 6.0)
     a = zmatrix_with_spectrum(oracle_mod, 5 * m + n, m, n, steep)
     f = tsvd(a, p)
-    _, S, _, _ = oracle_mod.ztsvd(a, p)
+    _, S, _, _ = ref_mod.tsvd(a, p)
     assert np.max(np.abs(np.asarray(f.sigma) - S)) < 1e-13
     assert np.max(np.abs(np.asarray(f.sigma) - steep) / steep) < 1e-7
 
 
-def test_complex_steep_spectrum_sampled_tail(cuda, oracle_mod):
+def test_complex_steep_spectrum_sampled_tail(cuda, oracle_mod, ref_mod):
     # 2^-k spectrum: Y is numerically rank deficient after the power steps
     # (the shifted CholeskyQR fallback keeps the tiny directions' components).
     from paper_1710_01463_b200 import RsvdParams, rsvd
 
     a = zmatrix_with_spectrum(oracle_mod, 91, 80, 60, spectrum_family(0, 60))
     f = rsvd(a, RsvdParams(10, 30, 4, 11))
-    ref = oracle_mod.zrsvd(a, 10, 30, 4, 11)
+    ref = ref_mod.rsvd(a, 10, 30, 4, 11)
     assert f.rank() == len(ref[1])
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
     assert f.discarded_weight == pytest.approx(ref[3], rel=1e-8)
 
 
-def test_complex_batched_matches_single_calls(cuda, oracle_mod):
+def test_complex_batched_matches_single_calls(cuda, oracle_mod, ref_mod):
     import torch
     from paper_1710_01463_b200 import RsvdParams, rsvd, rsvd_batched
 
@@ -182,12 +182,12 @@ def test_complex_batched_matches_single_calls(cuda, oracle_mod):
         # host- and device-pointer batches run the same kernels: bitwise equal
         assert np.array_equal(di.sigma.cpu().numpy(), np.asarray(bi.sigma))
         assert np.array_equal(di.right_adj.cpu().numpy(), np.asarray(bi.right_adj))
-        check_against(a, bi, oracle_mod.zrsvd(a, 12, 24, 2, seeds[i]), f"batch item {i}")
-        ref = oracle_mod.zrsvd(a, 12, 24, 2, seeds[i])
+        check_against(a, bi, ref_mod.rsvd(a, 12, 24, 2, seeds[i]), f"batch item {i}")
+        ref = ref_mod.rsvd(a, 12, 24, 2, seeds[i])
         check_against(a, fi, ref, f"item {i}")
 
 
-def test_complex_device_tensor_and_determinism(cuda, oracle_mod):
+def test_complex_device_tensor_and_determinism(cuda, oracle_mod, ref_mod):
     import torch
     from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
 
@@ -199,16 +199,16 @@ def test_complex_device_tensor_and_determinism(cuda, oracle_mod):
     fh = rsvd(a, RsvdParams(16, 30, 2, 3))
     assert np.array_equal(fh.left, f1.left.cpu().numpy())
     e_dev = reconstruction_error(ad, f1)
-    e_ora = oracle_mod.zreconstruction_error(a, fh.left, fh.sigma, fh.right_adj)
+    e_ora = ref_mod.reconstruction_error(a, fh.left, fh.sigma, fh.right_adj)
     assert abs(e_dev - e_ora) / e_ora < REC_TOL
 
 
-def test_complex_randomized_range_spans_oracle_range(cuda, oracle_mod):
+def test_complex_randomized_range_spans_oracle_range(cuda, oracle_mod, ref_mod):
     from paper_1710_01463_b200 import randomized_range
 
     a = zmatrix_with_spectrum(oracle_mod, 44, 90, 70, np.exp(-np.arange(70) / 5.0))
     Q = np.asarray(randomized_range(a, 20, 2, 9))
-    Qr = oracle_mod.zrandomized_range(a, 20, 2, 9)
+    Qr = ref_mod.randomized_range(a, 20, 2, 9)
     assert Q.dtype == np.complex128
     assert isometry_err(Q) < ISO_TOL
     # exp(-k/5) spectrum: the leading 12 directions are captured to ~1e-12
@@ -258,7 +258,7 @@ def test_complex_golden_fixture(cuda):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.complex128])
-def test_gram96_with_odd_rows(cuda, oracle_mod, dtype):
+def test_gram96_with_odd_rows(cuda, oracle_mod, dtype, ref_mod):
     """Regression: a 96-multiple (realified) sample width with an odd row
     count (odd leading dimension) cannot take the TMA Gram tile; the Gram must
     fall back to the cp.async tiles instead of failing."""
@@ -271,16 +271,16 @@ def test_gram96_with_odd_rows(cuda, oracle_mod, dtype):
         from tests.helpers import matrix_with_spectrum
 
         a = matrix_with_spectrum(oracle_mod, 12, m, n, sigma)
-        ref = oracle_mod.tsvd(a, p)
+        ref = ref_mod.tsvd(a, p)
     else:
         a = zmatrix_with_spectrum(oracle_mod, 12, m, n, sigma)
-        ref = oracle_mod.ztsvd(a, p)
+        ref = ref_mod.tsvd(a, p)
     f = tsvd(a, p)
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (1, 7), (9, 1), (5, 5), (3, 40)])
-def test_complex_tiny_shapes(cuda, oracle_mod, shape):
+def test_complex_tiny_shapes(cuda, oracle_mod, shape, ref_mod):
     """Degenerate shapes: rank 1 rows/columns, l = min(m, n) (Q spans everything)."""
     from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
 
@@ -289,10 +289,10 @@ def test_complex_tiny_shapes(cuda, oracle_mod, shape):
     a = np.asfortranarray(rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)))
     p = min(m, n)
     f = rsvd(a, RsvdParams(p, p, 2, 4))
-    ref = oracle_mod.zrsvd(a, p, p, 2, 4)
+    ref = ref_mod.rsvd(a, p, p, 2, 4)
     check_against(a, f, ref, f"rsvd {shape}")
     t = tsvd(a, p + 3)  # chi above min(m, n): clipped, exact
-    St = oracle_mod.ztsvd(a, p + 3)[1]
+    St = ref_mod.tsvd(a, p + 3)[1]
     assert rel_sigma_err(t.sigma, St) < SIG_TOL
     assert t.discarded_weight == pytest.approx(0.0, abs=1e-24)
 
@@ -314,7 +314,7 @@ def test_complex_extreme_magnitudes(cuda, oracle_mod, scale):
     np.testing.assert_allclose(np.asarray(ts.sigma) / scale, t1.sigma, rtol=1e-12)
 
 
-def test_complex_real_valued_input_matches_real_path(cuda, oracle_mod):
+def test_complex_real_valued_input_matches_real_path(cuda, oracle_mod, ref_mod):
     """A complex matrix with zero imaginary part has the real matrix's singular
     values: the complex instantiation agrees with the real one."""
     from paper_1710_01463_b200 import RsvdParams, rsvd, tsvd
@@ -327,8 +327,8 @@ def test_complex_real_valued_input_matches_real_path(cuda, oracle_mod):
     np.testing.assert_allclose(np.asarray(tsvd(az, 12).sigma), np.asarray(tsvd(ar, 12).sigma),
                                rtol=1e-12)
     # each randomized result against its own restated reference (same Omega)
-    assert rel_sigma_err(fz.sigma, oracle_mod.zrsvd(az, 12, 24, 2, 3)[1]) < SIG_TOL
-    assert rel_sigma_err(fr.sigma, oracle_mod.rsvd(ar, 12, 24, 2, 3)[1]) < SIG_TOL
+    assert rel_sigma_err(fz.sigma, ref_mod.rsvd(az, 12, 24, 2, 3)[1]) < SIG_TOL
+    assert rel_sigma_err(fr.sigma, ref_mod.rsvd(ar, 12, 24, 2, 3)[1]) < SIG_TOL
 
 
 def test_complex_empty_matrix_errors(cuda):
@@ -342,7 +342,7 @@ def test_complex_empty_matrix_errors(cuda):
 
 @pytest.mark.parametrize("case", [(700, 400, 200, 330, 1), (520, 480, 300, 480, 0)],
                          ids=["rsvd-l330", "rsvd-l480-q0"])
-def test_complex_wide_sample_streaming_jacobi(cuda, oracle_mod, case):
+def test_complex_wide_sample_streaming_jacobi(cuda, oracle_mod, case, ref_mod):
     """l > 288: the complex Jacobi streams its columns (no register-resident
     variant) and the realified Cholesky runs on 2l > 576 columns."""
     from paper_1710_01463_b200 import RsvdParams, rsvd
@@ -350,21 +350,21 @@ def test_complex_wide_sample_streaming_jacobi(cuda, oracle_mod, case):
     m, n, k, ell, q = case
     a = zmatrix_with_spectrum(oracle_mod, m + n, m, n, np.exp(-np.arange(min(m, n)) / 90.0))
     f = rsvd(a, RsvdParams(k, ell, q, 21))
-    ref = oracle_mod.zrsvd(a, k, ell, q, 21)
+    ref = ref_mod.rsvd(a, k, ell, q, 21)
     check_against(a, f, ref, str(case), dw_rel=1e-8)
 
 
-def test_complex_tsvd_streaming_jacobi(cuda, oracle_mod):
+def test_complex_tsvd_streaming_jacobi(cuda, oracle_mod, ref_mod):
     from paper_1710_01463_b200 import tsvd
 
     a = zmatrix_with_spectrum(oracle_mod, 5, 330, 300, np.exp(-np.arange(300) / 80.0))
     f = tsvd(a, 300)
-    ref = oracle_mod.ztsvd(a, 300)
+    ref = ref_mod.tsvd(a, 300)
     check_against(a, f, ref, "tsvd 330x300", dw_rel=1e-8)
 
 
 @pytest.mark.parametrize("kind,ell", [("real", 900), ("complex", 512), ("complex", 1024)])
-def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell):
+def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell, ref_mod):
     """Sample widths whose (realified) Cholesky panel does not fit in shared
     memory (l_p > ~840): the panel moves to global scratch; the reference's
     default l = 2k makes such widths ordinary (k = 256 complex -> 2l = 1024)."""
@@ -375,10 +375,10 @@ def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell):
     sig = np.exp(-np.arange(n) / 200.0)
     if kind == "real":
         a = matrix_with_spectrum(oracle_mod, 77, m, n, sig)
-        ref = oracle_mod.rsvd(a, ell // 2, ell, 1, 3)
+        ref = ref_mod.rsvd(a, ell // 2, ell, 1, 3)
     else:
         a = zmatrix_with_spectrum(oracle_mod, 77, m, n, sig)
-        ref = oracle_mod.zrsvd(a, ell // 2, ell, 1, 3)
+        ref = ref_mod.rsvd(a, ell // 2, ell, 1, 3)
     f = rsvd(a, RsvdParams(ell // 2, ell, 1, 3))
     assert f.rank() == len(ref[1])
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
@@ -387,7 +387,7 @@ def test_wide_samples_beyond_shared_memory_panels(cuda, oracle_mod, kind, ell):
 
 @pytest.mark.parametrize("kind,m,n", [("real", 1024, 1024), ("real", 900, 1300),
                                       ("complex", 700, 650)])
-def test_large_tsvd(cuda, oracle_mod, kind, m, n):
+def test_large_tsvd(cuda, oracle_mod, kind, m, n, ref_mod):
     """Full-SVD truncation beyond the register-resident Jacobi (min(m, n) up
     to 1600 on the GPU): C1's 1024^2 matrix is the BASELINE's tsvd comparator."""
     from paper_1710_01463_b200 import tsvd
@@ -397,17 +397,17 @@ def test_large_tsvd(cuda, oracle_mod, kind, m, n):
     sig = np.exp(-np.arange(p) / 32.0)
     if kind == "real":
         a = matrix_with_spectrum(oracle_mod, 3, m, n, sig)
-        ref = oracle_mod.tsvd(a, 64)
+        ref = ref_mod.tsvd(a, 64)
     else:
         a = zmatrix_with_spectrum(oracle_mod, 3, m, n, sig)
-        ref = oracle_mod.ztsvd(a, 64)
+        ref = ref_mod.tsvd(a, 64)
     f = tsvd(a, 64)
     check_against(a, f, ref, f"{kind} tsvd {m}x{n}", dw_rel=1e-8)
 
 
 @pytest.mark.parametrize("case", [(40, 96, 80, 12, 24), (20, 200, 180, 64, 138), (8, 300, 280, 128, 276)],
                          ids=["R3", "R5", "R9"])
-def test_complex_batched_block_jacobi(cuda, oracle_mod, case):
+def test_complex_batched_block_jacobi(cuda, oracle_mod, case, ref_mod):
     """Batches with more than SMs/4 block-pair tasks take the complex
     Gram-accelerated block-cyclic Jacobi (one instantiation per rows-per-lane
     class); every item against the complex oracle."""
@@ -425,7 +425,7 @@ def test_complex_batched_block_jacobi(cuda, oracle_mod, case):
         fi = f.item(i)
         fi.left, fi.sigma, fi.right_adj = (fi.left.cpu().numpy(), fi.sigma.cpu().numpy(),
                                            fi.right_adj.cpu().numpy())
-        check_against(mats[i], fi, oracle_mod.zrsvd(mats[i], k, ell, 2, seeds[i]), f"item {i}",
+        check_against(mats[i], fi, ref_mod.rsvd(mats[i], k, ell, 2, seeds[i]), f"item {i}",
                       dw_rel=1e-8)
 
 

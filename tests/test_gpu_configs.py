@@ -1,9 +1,10 @@
 """Parity on BASELINE.json's five full-size configurations.
 
 The same A bytes (generated on the GPU by paper_1710_01463_b200.synth, copied
-to the host) go to the engine and to the CPU oracle (restated reference rsvd,
-OpenBLAS LAPACK, all host threads); the oracle draws its own Omega from the
-same CounterRng seed.  Batched configs check a sample of items against the
+to the host) go to the engine and to the REFERENCE's own rsvd
+(proj/src/factorize.cpp + lapack.cpp compiled unmodified into
+oracle/_ref/librlftn_ref.so, OpenBLAS LAPACK, all host threads), which draws
+its own Omega from the same CounterRng seed.  Batched configs check a sample of items against the
 oracle and the whole batch through size-independent properties (isometry,
 ordering, Eckart-Young, determinism)."""
 import numpy as np
@@ -42,7 +43,7 @@ def compare(a, U, S, Vt, dw, ref, label):
     return {"sig": rel_sigma_err(S, Sr), "rec": abs(e - er) / er, "j": j}
 
 
-def run_config(name, cuda, oracle_mod, items):
+def run_config(name, cuda, ref_mod, items):
     import torch
 
     from paper_1710_01463_b200 import RsvdParams, rsvd_batched, synth
@@ -56,7 +57,7 @@ def run_config(name, cuda, oracle_mod, items):
     out = {}
     for b in items:
         a = np.asfortranarray(A[b].cpu().numpy())
-        ref = oracle_mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, seeds[b])
+        ref = ref_mod.rsvd(a, cfg.rank, cfg.ell, cfg.power, seeds[b])
         r = f.ranks[b]
         U = f.left[b][:, :r].cpu().numpy()
         S = f.sigma[b][:r].cpu().numpy()
@@ -65,14 +66,14 @@ def run_config(name, cuda, oracle_mod, items):
     return A, f, out
 
 
-def test_c1(cuda, oracle_mod):
-    run_config("C1", cuda, oracle_mod, [0])
+def test_c1(cuda, ref_mod):
+    run_config("C1", cuda, ref_mod, [0])
 
 
-def test_c2_batch(cuda, oracle_mod):
+def test_c2_batch(cuda, ref_mod):
     import torch
 
-    A, f, _ = run_config("C2", cuda, oracle_mod, [0, 97, 255])
+    A, f, _ = run_config("C2", cuda, ref_mod, [0, 97, 255])
     # whole batch: isometry and ordering of every item
     for b in range(A.shape[0]):
         r = f.ranks[b]
@@ -84,16 +85,16 @@ def test_c2_batch(cuda, oracle_mod):
 
 
 @pytest.mark.parametrize("name", ["C3", "C3q3"])
-def test_c3(cuda, oracle_mod, name):
-    run_config(name, cuda, oracle_mod, [0])
+def test_c3(cuda, ref_mod, name):
+    run_config(name, cuda, ref_mod, [0])
 
 
-def test_c4_batch(cuda, oracle_mod):
+def test_c4_batch(cuda, ref_mod):
     import torch
 
     from paper_1710_01463_b200 import RsvdParams, rsvd_batched, synth
 
-    A, f, _ = run_config("C4", cuda, oracle_mod, [0, 31])
+    A, f, _ = run_config("C4", cuda, ref_mod, [0, 31])
     cfg = synth.CONFIGS["C4"]
     # determinism of the whole batch: bitwise equal on a second call
     f2 = rsvd_batched(A, RsvdParams(cfg.rank, cfg.ell, cfg.power, 0), synth.omega_seeds(cfg))
@@ -111,5 +112,5 @@ def test_c4_batch(cuda, oracle_mod):
 
 
 @pytest.mark.slow
-def test_c5(cuda, oracle_mod):
-    run_config("C5", cuda, oracle_mod, [0])
+def test_c5(cuda, ref_mod):
+    run_config("C5", cuda, ref_mod, [0])

@@ -67,12 +67,12 @@ def test_spectral_reconstruction_error(cuda, oracle_mod):  # test_factorize.cpp:
                                          (50, 30, 12, 30, 2), (5000, 30, 8, 20, 2),
                                          (30, 5000, 8, 20, 2), (257, 129, 17, 37, 1),
                                          (1, 300, 1, 1, 2), (300, 1, 1, 1, 2)])
-def test_boundary_shapes_vs_oracle(cuda, oracle_mod, m, n, k, ell, q):
+def test_boundary_shapes_vs_oracle(cuda, oracle_mod, m, n, k, ell, q, ref_mod):
     from paper_1710_01463_b200 import RsvdParams, rsvd
 
     a = matrix_with_spectrum(oracle_mod, 7 + m + n, m, n, 0.8 ** np.arange(min(m, n)))
     f = rsvd(a, RsvdParams(k, ell, q, 99))
-    U, S, Vt, dw = oracle_mod.rsvd(a, k, ell, q, 99)
+    U, S, Vt, dw = ref_mod.rsvd(a, k, ell, q, 99)
     assert f.rank() == len(S)
     big = S > 1e-6 * S[0]
     assert rel_sigma_err(f.sigma[big], S[big]) < 1e-10
@@ -80,7 +80,7 @@ def test_boundary_shapes_vs_oracle(cuda, oracle_mod, m, n, k, ell, q):
     assert f.discarded_weight == pytest.approx(dw, rel=1e-8, abs=1e-28)
 
 
-def test_strided_device_buffers_through_the_c_abi(cuda, oracle_mod):
+def test_strided_device_buffers_through_the_c_abi(cuda, oracle_mod, ref_mod):
     """lda > m, ldu > m, ldvt > k and item strides with padding, device pointers."""
     import torch
 
@@ -108,7 +108,7 @@ def test_strided_device_buffers_through_the_c_abi(cuda, oracle_mod):
                                   ranks, dws, _lib.PTR_DEVICE)
     _lib.raise_for(rc, h.raw)
     for b, a in enumerate(mats):
-        Uo, So, Vto, dwo = oracle_mod.rsvd(a, k, ell, 2, 500 + b)
+        Uo, So, Vto, dwo = ref_mod.rsvd(a, k, ell, 2, 500 + b)
         s = S[b * ss:b * ss + k].cpu().numpy()
         assert ranks[b] == len(So) and rel_sigma_err(s, So) < 1e-10
         u = U[b * su:b * su + ldu * k].view(k, ldu)[:, :m].t().cpu().numpy()
@@ -117,7 +117,7 @@ def test_strided_device_buffers_through_the_c_abi(cuda, oracle_mod):
     h.close()
 
 
-def test_many_tiny_matrices(cuda, oracle_mod):
+def test_many_tiny_matrices(cuda, oracle_mod, ref_mod):
     import torch
 
     from paper_1710_01463_b200 import RsvdParams, rsvd_batched
@@ -129,7 +129,7 @@ def test_many_tiny_matrices(cuda, oracle_mod):
     seeds = list(range(bsz))
     bf = rsvd_batched(A, RsvdParams(2, 4, 1, 0), seeds)
     for b in range(0, bsz, 149):
-        _, S, _, _ = oracle_mod.rsvd(mats[b], 2, 4, 1, b)
+        _, S, _, _ = ref_mod.rsvd(mats[b], 2, 4, 1, b)
         assert rel_sigma_err(bf.sigma[b][:len(S)].cpu().numpy(), S) < 1e-10
 
 

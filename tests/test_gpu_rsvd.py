@@ -78,12 +78,12 @@ def test_device_pointers_match_host_pointers(cuda, golden_small):
     assert np.array_equal(fh.right_adj, fd.right_adj.cpu().numpy())
 
 
-def test_rsvd_matches_tsvd_fast_decay(cuda, oracle_mod):  # test_factorize.cpp:85-103
+def test_rsvd_matches_tsvd_fast_decay(cuda, oracle_mod, ref_mod):  # test_factorize.cpp:85-103
     from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
 
     sigma = spectrum_family(0, 30)
     a = matrix_with_spectrum(oracle_mod, 3, 50, 30, sigma)
-    Ut, St, Vtt, dwt = oracle_mod.tsvd(a, 10)
+    Ut, St, Vtt, dwt = ref_mod.tsvd(a, 10)
     f = rsvd(a, RsvdParams(10, 20, 4, 123))
     assert f.rank() == 10 and not f.discarded_exact
     assert rel_sigma_err(f.sigma, St) < 1e-10
@@ -93,7 +93,7 @@ def test_rsvd_matches_tsvd_fast_decay(cuda, oracle_mod):  # test_factorize.cpp:8
 
 
 @pytest.mark.parametrize("r", [3, 7])
-def test_exact_rank_reconstructs(cuda, oracle_mod, r):  # test_factorize.cpp:105-120
+def test_exact_rank_reconstructs(cuda, oracle_mod, r, ref_mod):  # test_factorize.cpp:105-120
     from paper_1710_01463_b200 import RsvdParams, reconstruction_error, rsvd
 
     sigma = [5.0 / (1.0 + k) for k in range(r)]
@@ -101,7 +101,7 @@ def test_exact_rank_reconstructs(cuda, oracle_mod, r):  # test_factorize.cpp:105
     f = rsvd(a, RsvdParams(10, 20, 4, 5))
     assert reconstruction_error(a, f) <= 1e-10 * np.linalg.norm(a)
     assert f.rank() <= 10
-    ref = oracle_mod.rsvd(a, 10, 20, 4, 5)
+    ref = ref_mod.rsvd(a, 10, 20, 4, 5)
     assert f.rank() == len(ref[1])
     assert rel_sigma_err(f.sigma, ref[1]) < SIG_TOL
 
@@ -169,18 +169,18 @@ def test_power_iterations_monotone(cuda, oracle_mod):  # test_factorize.cpp:209-
     assert np.all(mean[1:] <= mean[:-1] * (1 + 1e-12))
 
 
-def test_same_omega_as_oracle(cuda, oracle_mod):
+def test_same_omega_as_oracle(cuda, oracle_mod, ref_mod):
     """Feeding the oracle the reference Omega vs its own gives the same
     answer to within the Omega ulp noise: parity is not an artefact of Omega."""
     from paper_1710_01463_b200 import RsvdParams, rsvd
 
     a = matrix_with_spectrum(oracle_mod, 77, 300, 250, np.exp(-np.arange(250) / 20.0))
     f = rsvd(a, RsvdParams(40, 50, 2, 4242))
-    ref = oracle_mod.rsvd(a, 40, 50, 2, 4242)
+    ref = ref_mod.rsvd(a, 40, 50, 2, 4242)
     check_against(a, f, ref, "omega")
 
 
-def test_batched_matches_single(cuda, oracle_mod):
+def test_batched_matches_single(cuda, oracle_mod, ref_mod):
     import torch
     from paper_1710_01463_b200 import RsvdParams, rsvd, rsvd_batched
 
@@ -191,7 +191,7 @@ def test_batched_matches_single(cuda, oracle_mod):
     A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
     bf = rsvd_batched(A, RsvdParams(20, 30, 2, 0), seeds)
     for b in range(bsz):
-        ref = oracle_mod.rsvd(mats[b], 20, 30, 2, seeds[b])
+        ref = ref_mod.rsvd(mats[b], 20, 30, 2, seeds[b])
         fb = bf.item(b)
         fb.left, fb.sigma, fb.right_adj = (x.cpu().numpy() for x in (fb.left, fb.sigma,
                                                                     fb.right_adj))
@@ -229,7 +229,7 @@ def _steep_or_mild(oracle_mod, b, m, n):
     return matrix_with_spectrum(oracle_mod, 4100 + b, m, n, sig)
 
 
-def test_steep_spectrum_sampled_tail_matches_oracle(cuda, oracle_mod):
+def test_steep_spectrum_sampled_tail_matches_oracle(cuda, oracle_mod, ref_mod):
     """Sampled values far below sqrt(tau) sigma_0 (the pivot floor) must carry
     their true components like the reference's Householder bases: sigma and the
     discarded weight of a 2^-k spectrum against the oracle."""
@@ -238,7 +238,7 @@ def test_steep_spectrum_sampled_tail_matches_oracle(cuda, oracle_mod):
     a = matrix_with_spectrum(oracle_mod, 41, 200, 150, spectrum_family(0, 150))
     for k, ell, q in [(15, 40, 3), (10, 30, 0), (25, 50, 1)]:
         f = rsvd(a, RsvdParams(k, ell, q, 4040 + q))
-        ref = oracle_mod.rsvd(a, k, ell, q, 4040 + q)
+        ref = ref_mod.rsvd(a, k, ell, q, 4040 + q)
         assert f.rank() == len(ref[1])
         # kept values above ~1e-6 sigma_0 are resolvable to 1e-10 by any
         # FP64 method; below that compare absolutely (u ||A|| scale)
@@ -249,7 +249,7 @@ def test_steep_spectrum_sampled_tail_matches_oracle(cuda, oracle_mod):
         assert isometry_err(f.left) < ISO_TOL and isometry_err(f.right_adj.T) < ISO_TOL
 
 
-def test_mixed_batch_fallback_masks(cuda, oracle_mod):
+def test_mixed_batch_fallback_masks(cuda, oracle_mod, ref_mod):
     """A batch mixing ill-conditioned and mild items: the masked fallback passes
     must touch only the ill items (every item against the oracle)."""
     import torch
@@ -261,7 +261,7 @@ def test_mixed_batch_fallback_masks(cuda, oracle_mod):
     A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
     bf = rsvd_batched(A, RsvdParams(20, 48, 2, 0), seeds)
     for b in range(bsz):
-        ref = oracle_mod.rsvd(mats[b], 20, 48, 2, seeds[b])
+        ref = ref_mod.rsvd(mats[b], 20, 48, 2, seeds[b])
         fb = bf.item(b)
         S = fb.sigma.cpu().numpy()
         assert fb.rank() == len(ref[1]), b
@@ -271,7 +271,7 @@ def test_mixed_batch_fallback_masks(cuda, oracle_mod):
         assert isometry_err(fb.left.cpu().numpy()) < ISO_TOL, b
 
 
-def test_rank_deficient_items_in_batch(cuda, oracle_mod):
+def test_rank_deficient_items_in_batch(cuda, oracle_mod, ref_mod):
     """Exact-rank items (Y rank deficient: the fallback plus basis completion)
     next to full-rank ones; the zero matrix too."""
     import torch
@@ -286,7 +286,7 @@ def test_rank_deficient_items_in_batch(cuda, oracle_mod):
     A = torch.from_numpy(np.stack([x.T for x in mats])).to(cuda).transpose(1, 2)
     bf = rsvd_batched(A, RsvdParams(10, 20, 2, 0), seeds)
     for b, a in enumerate(mats):
-        ref = oracle_mod.rsvd(a, 10, 20, 2, seeds[b])
+        ref = ref_mod.rsvd(a, 10, 20, 2, seeds[b])
         fb = bf.item(b)
         fb.left, fb.sigma, fb.right_adj = (x.cpu().numpy() for x in (fb.left, fb.sigma,
                                                                     fb.right_adj))
