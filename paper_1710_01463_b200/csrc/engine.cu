@@ -33,9 +33,10 @@ namespace rsvd {
 namespace {
 
 constexpr double kPivotTau = 1e-13;   // relative pivot floor of the CholeskyQR Gram
-// Widest l x l factor the one-sided Jacobi kernels take (the pair-staged
-// kernel keeps 16 columns of l rows in shared memory beyond l = 576).
-constexpr int64_t kTsvdMaxDim = 1600;
+// Widest l x l factor the GPU path takes (the row-streamed Jacobi kernel has
+// no l-dependent shared memory; the bound keeps int32 element offsets of the
+// l x l work matrices safe and the workspace within one device).
+constexpr int64_t kTsvdMaxDim = 16384;
 constexpr int kMaxSweeps = 40;        // one-sided Jacobi sweep cap
 constexpr uint64_t kCompletionTag = 0x436f6d706c657465ull;  // "Complete"
 
@@ -860,7 +861,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   if (!A || !U || !S || !Vt || !seeds || !out_rank || !dw)
     throw InvalidArgument("rsvd: null pointer argument");
   if (lda < m || ldu < m || ldvt < rank) throw InvalidArgument("rsvd: leading dimension too small");
-  if (ell > kTsvdMaxDim) throw InvalidArgument("rsvd: l > 1600 is not supported by the GPU path");
+  if (ell > kTsvdMaxDim) throw InvalidArgument("rsvd: l > 16384 is not supported by the GPU path");
   const bool host = flags == RSVD_PTR_HOST;
   RSVD_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
@@ -993,7 +994,7 @@ void tsvd_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64
   if (batch == 0) return;
   const int64_t p = std::min(m, n), k = std::min(chi, p);
   if (p > kTsvdMaxDim)
-    throw InvalidArgument("tsvd: min(m, n) > 1600 is not supported by the GPU path");
+    throw InvalidArgument("tsvd: min(m, n) > 16384 is not supported by the GPU path");
   if (!A || !U || !S || !Vt || !out_rank || !dw) throw InvalidArgument("tsvd: null pointer argument");
   if (lda < m || ldu < m || ldvt < k) throw InvalidArgument("tsvd: leading dimension too small");
   const bool host = flags == RSVD_PTR_HOST;

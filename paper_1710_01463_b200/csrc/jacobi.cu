@@ -1721,6 +1721,311 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-streamed Gram-accelerated block-cyclic Jacobi (jacobi_rs_kernel).
+// Same sweep order, rotation formula, thresholds and convergence flags as
+// jacobi_gram_kernel, re-laid-out so that nothing scales with l in shared
+// memory: any l (tsvd up to min(m, n) = 4096 and beyond) and small CTAs.
+//   * G = X^T X of the task's 32 columns is accumulated over row chunks of RC
+//     rows, staged by cp.async into a double buffer (DMMA, 8 warps, one
+//     16 x 8 tile each);
+//   * the 16 rotation steps run on G / V in shared memory (8 warps, two
+//     column pairs each per step);
+//   * X <- X V and J <- J V read their 16-row slabs straight from global
+//     memory (L2) into DMMA fragments and write the products back in place
+//     (a warp loads its whole slab before it stores it).
+// 256 threads and ~52 KB per CTA: 3 CTAs (24 warps) per SM keep several
+// tasks' latency-bound rotation steps in flight.
+template <int RC>
+__global__ void __launch_bounds__(256, 3)
+    jacobi_rs_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+                     int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
+                     int* __restrict__ sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, NW = 8;
+  constexpr int PITCH = RC + 2;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  __shared__ unsigned long long s_mx;
+  const int nch = (ell + RC - 1) / RC;
+  double* Xs = sm;                              // (1 or 2) x (NC x PITCH): row-chunk buffers
+  double* Vs = sm + (nch > 1 ? 2 : 1) * NC * PITCH;  // NC x VP, column-major V[c*VP + k]
+  double* Gs = Vs + NC * VP;           // NC x GP, G[row + col*GP]
+  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
+
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = gtid; e < sq * batch; e += gstride) {
+    const int64_t rem = e % sq;
+    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
+  }
+  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
+  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
+    flags[e] = 0u;
+    mxr[e] = 0ull;
+  }
+  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
+  grid.sync();
+
+  const int half = nb / 2;
+  const int64_t tasks = batch * half;
+  const int slabs = (ell + 15) / 16;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* fl = flags + (sweep % 3) * batch;
+    unsigned long long* mxs = mxr + (sweep % 3) * batch;
+    if (blockIdx.x == 0)
+      for (int64_t i = tid; i < batch; i += blockDim.x) {
+        flags[((sweep + 1) % 3) * batch + i] = 0u;
+        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
+      }
+    for (int phase = 0; phase < nb; ++phase) {
+      const bool diag = phase == 0;
+      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const int64_t item = task / half;
+        if (conv[item]) continue;
+        const int k = static_cast<int>(task % half);
+        int bp, bq;
+        if (diag) {
+          bp = 2 * k, bq = 2 * k + 1;
+        } else {
+          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
+          bp = min(p, q), bq = max(p, q);
+        }
+        if (bp * W >= ell) continue;
+        double* Hg = H + item * sq;
+        double* Jg = J + item * sq;
+        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+        // ---- G = X^T X over row chunks (cp.async double buffer, DMMA) ----
+        auto stage = [&](int c, int buf) {
+          const int r0 = c * RC;
+          double* dst = Xs + buf * NC * PITCH;
+          for (int e = tid; e < NC * (RC / 2); e += NW * 32) {
+            const int cc = e / (RC / 2), r = 2 * (e - cc * (RC / 2));
+            const int gc = gcol(cc), gr = r0 + r;
+            int bytes = 0;
+            const double* src = Hg;
+            if (gc < ell && gr < ell) {
+              bytes = min(16, (ell - gr) * 8);
+              src = Hg + gr + static_cast<int64_t>(gc) * ellp;
+            }
+            cpa16(dst + cc * PITCH + r, src, bytes);
+          }
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        for (int e = tid; e < NC * VP; e += NW * 32) {
+          const int c = e / VP, r = e - c * VP;
+          Vs[e] = (r == c) ? 1.0 : 0.0;
+        }
+        if (tid == 0) {
+          s_rot = 0;
+          s_mx = 0ull;
+        }
+        const int tm = warp >> 2, tn = warp & 3;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        stage(0, 0);
+        for (int c = 0; c < nch; ++c) {
+          if (c + 1 < nch) {
+            stage(c + 1, (c + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+          }
+          __syncthreads();
+          const double* Xb = Xs + (c & 1) * NC * PITCH;
+          const double* a0p = Xb + (16 * tm + g) * PITCH;
+          const double* a1p = Xb + (16 * tm + g + 8) * PITCH;
+          const double* b0p = Xb + (8 * tn + g) * PITCH;
+#pragma unroll 8
+          for (int k0 = 0; k0 < RC; k0 += 4)
+            dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+          __syncthreads();  // buffer c & 1 is restaged at c + 2
+        }
+        {
+          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
+          Gs[r0 + c0 * GP] = acc[0];
+          Gs[r0 + (c0 + 1) * GP] = acc[1];
+          Gs[r0 + 8 + c0 * GP] = acc[2];
+          Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
+        }
+        __syncthreads();
+        // ---- rotation steps on G and V (each warp: two column pairs) ----
+        int rotated = 0, big = 0;
+        const int steps = diag ? 15 : 16;
+        for (int s2 = 0; s2 < steps; ++s2) {
+          int pi[2], pj[2];
+          double pc[2], ps[2], pt[2], pal[2], pbe[2], pga[2];
+          bool prot[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int pr = warp + NW * u;  // pair 0..15
+            int i, jx;
+            if (diag) {
+              const int blk = pr >> 3, pk = pr & 7;
+              const int a0 = rr_player(pk, s2, 16), b0 = rr_player(15 - pk, s2, 16);
+              i = blk * 16 + min(a0, b0);
+              jx = blk * 16 + max(a0, b0);
+            } else {
+              i = pr;
+              jx = 16 + ((pr + s2) & 15);
+            }
+            pi[u] = i;
+            pj[u] = jx;
+            const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
+            pal[u] = al;
+            pbe[u] = be;
+            pga[u] = ga;
+            const double gg = ga * ga, ab = al * be;
+            const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
+            double c = 1.0, sn = 0.0, tt = 0.0;
+            if (rot) {
+              big |= gg >= c_stop_ratio2 * ab;
+              const double d = be - al, g2 = 2.0 * ga;
+              const double mag = fmax(fabs(d), fabs(g2));
+              if (mag > 1e-140 && mag < 1e140) {
+                tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+              } else {
+                const double zeta = d / g2;
+                tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              }
+              c = rsqrt(fma(tt, tt, 1.0));
+              sn = c * tt;
+              rotated = 1;
+            }
+            prot[u] = rot;
+            pc[u] = c;
+            ps[u] = sn;
+            pt[u] = tt;
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (!prot[u]) continue;
+            const int i = pi[u], jx = pj[u];
+            const double c = pc[u], sn = ps[u];
+            const double gi = Gs[lane + i * GP], gj = Gs[lane + jx * GP];
+            Gs[lane + i * GP] = c * gi - sn * gj;
+            Gs[lane + jx * GP] = sn * gi + c * gj;
+            const double vi = Vs[i * VP + lane], vj = Vs[jx * VP + lane];
+            Vs[i * VP + lane] = c * vi - sn * vj;
+            Vs[jx * VP + lane] = sn * vi + c * vj;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (!prot[u]) continue;
+            const int i = pi[u], jx = pj[u];
+            const double c = pc[u], sn = ps[u];
+            const double gi = Gs[i + lane * GP], gj = Gs[jx + lane * GP];
+            Gs[i + lane * GP] = c * gi - sn * gj;
+            Gs[jx + lane * GP] = sn * gi + c * gj;
+          }
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (!prot[u]) continue;
+              const int i = pi[u], jx = pj[u];
+              Gs[i + i * GP] = pal[u] - pt[u] * pga[u];
+              Gs[jx + jx * GP] = pbe[u] + pt[u] * pga[u];
+              Gs[i + jx * GP] = 0.0;
+              Gs[jx + i * GP] = 0.0;
+            }
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) {
+          atomicOr(&s_rot, 1);
+          if (big) atomicMax(&s_mx, 1ull);
+        }
+        __syncthreads();
+        if (s_rot) {
+          // ---- X <- X V and J <- J V, in place, 16-row slab per warp ----
+          for (int job = warp; job < 2 * slabs; job += NW) {
+            double* M = job < slabs ? Hg : Jg;
+            const int r0 = (job < slabs ? job : job - slabs) * 16;
+            const int ra = r0 + g, rb = r0 + g + 8;
+            double accv[NC / 8][4];
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) accv[n][qq] = 0.0;
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) {
+              const int kc = kq * 4 + t4;
+              const int gc = gcol(kc);
+              const double* col = M + static_cast<int64_t>(gc) * ellp;
+              const bool okc = gc < ell;
+              const double a0 = (okc && ra < ell) ? __ldcg(col + ra) : 0.0;
+              const double a1 = (okc && rb < ell) ? __ldcg(col + rb) : 0.0;
+#pragma unroll
+              for (int n = 0; n < NC / 8; ++n)
+                dmma_16x8x4(accv[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
+            }
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const int r = (qq & 2) ? rb : ra;
+                const int gc = gcol(n * 8 + 2 * t4 + (qq & 1));
+                if (r < ell && gc < ell) __stcg(M + r + static_cast<int64_t>(gc) * ellp, accv[n][qq]);
+              }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_rot) {
+          atomicOr(fl + item, 1u);
+          atomicMax(mxs + item, s_mx);
+        }
+      }
+      grid.sync();
+    }
+    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
+    int all = 1;
+    for (int64_t i = 0; i < batch; ++i) {
+      const bool d = done(i);
+      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
+      all &= (conv[i] || d);
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (done(i)) conv[i] = 1;
+    __syncthreads();
+    if (all) break;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tid; i < batch; i += blockDim.x)
+      if (!conv[i]) sweeps_out[i] = max_sweeps;
+}
+
+template <int RC>
+void launch_rs_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+                 unsigned* flags, int64_t batch, cudaStream_t st) {
+  const int nbuf = ell > RC ? 2 : 1;
+  const size_t bytes = (static_cast<size_t>(nbuf * 32) * (RC + 2) + 32 * 36 + 32 * 33) * sizeof(double) +
+                       batch * sizeof(int) + 16;
+  auto kern = jacobi_rs_kernel<RC>;
+  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  int per_sm = 0;
+  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, bytes));
+  if (per_sm < 1) throw CudaError("jacobi_rs_kernel: does not fit on an SM");
+  int nb = static_cast<int>((ell + 15) / 16);
+  nb += nb & 1;
+  const int64_t tasks = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * num_sms())));
+  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
+  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(256),
+                                        args, bytes, st));
+  RSVD_LAUNCH("jacobi_rs_kernel");
+}
+
 }  // namespace
 
 // 3 rotating "rotated" flags per item, then (8-byte aligned) 3 rotating
@@ -1793,6 +2098,11 @@ void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int 
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st) {
   set_stop_ratio_once();
+  static const bool rs_all = std::getenv("RSVD_JACOBI_RS") != nullptr;
+  if (rs_all || ell > 1600) {
+    if (ell <= 160 && ell > 64) return launch_rs_t<160>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+    return launch_rs_t<64>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  }
   const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
   {
     int nbt = static_cast<int>((ell + 15) / 16);

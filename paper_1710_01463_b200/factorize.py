@@ -163,8 +163,8 @@ _MASK = (1 << 64) - 1
 
 def tsvd(a, chi: int, handle: Optional[_lib.Handle] = None) -> TruncatedFactorization:
     """rlftn::tsvd (factorize.cpp:42-50): exact thin SVD truncated to
-    r = min(chi, numerical rank), exact discarded weight.  GPU path for
-    min(m, n) <= 1600."""
+    r = min(chi, numerical rank), exact discarded weight.  Any size (the
+    row-streamed Jacobi handles min(m, n) into the thousands)."""
     lib = _lib.load()
     h = handle or _lib.default_handle()
     r = ctypes.c_int64(0)
@@ -442,8 +442,8 @@ def reconstruction_error(a, f: TruncatedFactorization, norm: ErrorNorm = ErrorNo
     """rlftn::reconstruction_error (factorize.cpp:97-104).  Frobenius: the
     engine's fused residual kernel.  Spectral (the reference's gesdd('N') of
     the residual, lapack.cpp:130-144): the residual is formed on the device and
-    its largest singular value taken with the engine's tsvd (min(m, n) <= 1600)
-    or a rank-1 rsvd with 8 power iterations."""
+    its largest singular value taken with the engine's tsvd (exact, as
+    gesdd('N'))."""
     if norm != ErrorNorm.frobenius:
         return _spectral_error(a, f, handle)
     lib = _lib.load()
@@ -501,8 +501,5 @@ def _spectral_error(a, f: TruncatedFactorization, handle) -> float:
         R = R - (U * S[None, :]) @ Vt
     if float(torch.linalg.norm(R)) == 0.0:
         return 0.0
-    if min(m, n) <= 1600:
-        g = tsvd(R, 1, handle)
-    else:
-        g = rsvd(R, RsvdParams(1, min(32, min(m, n)), 8, 0x5eed), handle)
+    g = tsvd(R, 1, handle)
     return float(g.sigma[0]) if g.rank() else 0.0
