@@ -150,8 +150,6 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 int64_t jacobi_flag_elems(int64_t batch);
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st);
-void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
-                           int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st);
 
 // aux.cu
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,

@@ -8,11 +8,21 @@
 // columns, give sigma_i = ||W e_i|| (computed from the vectors themselves,
 // hence relatively accurate), U~ = W Sigma^{-1} and V~ = Qb J.
 //
-// Parallel cyclic ordering (round-robin tournament): each of the l-1 steps of
-// a sweep rotates l/2 disjoint column pairs, one warp per pair; a sweep with
-// no rotation above tol = sqrt(l) * eps (dgesvj's convergence test) ends the
-// iteration.  One CTA per batch item; H and J live in shared memory when both
-// fit, otherwise in global memory (L2-resident).
+// Block-cyclic ordering: columns in blocks of 16, one sweep = a diagonal
+// phase (each block pair (2k, 2k+1) rotates its intra pairs) plus nb - 1
+// round-robin block-pair phases (every inter-block pair once).  A task =
+// (item, block pair): G = X^T X of its 32 columns on DMMA, 15-16 rotation
+// steps on G and a 32 x 32 V (dgesvj's threshold |g| <= sqrt(l) eps
+// sqrt(alpha beta), exact 2 x 2 updates), then X <- X V and J <- J V on DMMA.
+// An item stops after a sweep whose largest rotated ratio was below 1e-9
+// (quadratic convergence leaves ~1e-18 behind).
+//
+// Two kernels:
+//   * jacobi_df_kernel  -- many tasks (batches: C2, C4, TEBD layers) and any
+//     l: dataflow over (sweep, phase, item, pair) with per-item dependencies,
+//     no grid barrier, no l-dependent shared memory;
+//   * jacobi_clug_kernel -- few tasks (single matrices: C1, C3, C5): every
+//     task is owned by a thread-block cluster whose CTAs split its rows.
 #include <cooperative_groups.h>
 
 #include <cstdio>
@@ -26,283 +36,14 @@ namespace rsvd {
 namespace {
 
 // Sweep stop rule: an item is done after a sweep whose largest rotated
-// g^2 / (alpha beta) stayed below this (default (1e-9)^2; RSVD_JACOBI_STOP_RATIO
-// overrides the ratio for experiments).
+// g^2 / (alpha beta) stayed below (1e-9)^2.
 __constant__ double c_stop_ratio2 = 1e-18;
-void set_stop_ratio_once() {
-  static bool done = false;
-  if (done) return;
-  done = true;
-  if (const char* e = std::getenv("RSVD_JACOBI_STOP_RATIO")) {
-    const double r = std::atof(e);
-    const double r2 = r * r;
-    cudaMemcpyToSymbol(c_stop_ratio2, &r2, sizeof(double));
-  }
-}
-constexpr int kJacThreads = 1024;
-constexpr int kJacWarps = kJacThreads / 32;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  return v;
-}
 
 // Round-robin pairing for `nn` (even) players at step s: slot 0 fixed, the
 // others rotate.  Pair k couples slot k with slot nn-1-k.
 __device__ __forceinline__ int rr_player(int slot, int s, int nn) {
   if (slot == 0) return 0;
   return 1 + (slot - 1 + s) % (nn - 1);
-}
-
-template <bool IN_SMEM>
-__global__ void __launch_bounds__(kJacThreads)
-    jacobi_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp,
-                  int max_sweeps, int* __restrict__ sweeps_out) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  const int64_t b = blockIdx.x;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  double* Hg = H + b * sq;
-  double* Jg = J + b * sq;
-  double* Hs = IN_SMEM ? sm : Hg;
-  double* Js = IN_SMEM ? sm + sq : Jg;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (IN_SMEM) {
-    for (int64_t e = tid; e < sq; e += blockDim.x) Hs[e] = Hg[e];
-  }
-  for (int64_t e = tid; e < sq; e += blockDim.x) {
-    const int64_t j = e / ellp, i = e - j * ellp;
-    Js[e] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-
-  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
-  const int nn = ell + (ell & 1);
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    __syncthreads();
-    int rotated = 0;
-    for (int s = 0; s < nn - 1; ++s) {
-      for (int k = warp; k < nn / 2; k += kJacWarps) {
-        const int p = rr_player(k, s, nn), q = rr_player(nn - 1 - k, s, nn);
-        const int i = min(p, q), j = max(p, q);
-        if (j >= ell) continue;  // dummy player for odd l
-        double* hi = Hs + static_cast<int64_t>(i) * ellp;
-        double* hj = Hs + static_cast<int64_t>(j) * ellp;
-        double a = 0.0, bb = 0.0, g = 0.0;
-        for (int r = lane; r < ell; r += 32) {
-          const double x = hi[r], y = hj[r];
-          a = fma(x, x, a);
-          bb = fma(y, y, bb);
-          g = fma(x, y, g);
-        }
-        a = warp_sum(a);
-        bb = warp_sum(bb);
-        g = warp_sum(g);
-        if (!(a > 0.0) || !(bb > 0.0)) continue;
-        if (!(fabs(g) > tol * sqrt(a) * sqrt(bb))) continue;
-        const double zeta = (bb - a) / (2.0 * g);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + tt * tt);
-        const double sn = c * tt;
-        for (int r = lane; r < ell; r += 32) {
-          const double x = hi[r], y = hj[r];
-          hi[r] = c * x - sn * y;
-          hj[r] = sn * x + c * y;
-        }
-        double* ji = Js + static_cast<int64_t>(i) * ellp;
-        double* jj = Js + static_cast<int64_t>(j) * ellp;
-        for (int r = lane; r < ell; r += 32) {
-          const double x = ji[r], y = jj[r];
-          ji[r] = c * x - sn * y;
-          jj[r] = sn * x + c * y;
-        }
-        rotated = 1;
-      }
-      __syncthreads();
-    }
-    if (rotated && lane == 0) atomicOr(&s_rot, 1);
-    __syncthreads();
-    const int any = s_rot;
-    __syncthreads();
-    if (!any) break;
-  }
-  if (IN_SMEM) {
-    for (int64_t e = tid; e < sq; e += blockDim.x) {
-      Hg[e] = Hs[e];
-      Jg[e] = Js[e];
-    }
-  }
-  if (tid == 0 && sweeps_out) sweeps_out[b] = sweep + 1;
-}
-
-// ---------------------------------------------------------------------------
-// Block-pair one-sided Jacobi for l too large for one CTA's shared memory.
-//
-// Columns are grouped into nb blocks of W (nb even, trailing blocks may be
-// partly or wholly beyond l).  One outer step pairs the blocks round-robin;
-// each pair (2W columns of H and J, rows < l) is staged in shared memory by
-// one CTA, which runs `inner` cyclic sweeps over the 2W local columns (one
-// warp per column pair, W warps) and writes them back.  Every column pair
-// meets in each outer sweep, so the outer sweep is a superset of a scalar
-// cyclic sweep.  A persistent cooperative grid walks the (item, pair) tasks of
-// a step, grid-syncs, and items whose whole sweep rotated nothing (same
-// sqrt(l) eps test as above) drop out.
-template <int W>
-__global__ void __launch_bounds__(W * 32)
-    jacobi_blocked_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp,
-                          int nb, int64_t batch, int max_sweeps, int inner,
-                          unsigned* __restrict__ flags, int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  constexpr int NC = 2 * W;
-  const int pitch = ell + (ell & 1);
-  double* Hs = sm;                  // NC x pitch
-  double* Js = sm + NC * pitch;     // NC x pitch
-  int* conv = reinterpret_cast<int*>(Js + NC * pitch);  // per-item converged (batch ints)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
-
-  // J = I, flags cleared.
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = gtid; e < sq * batch; e += gstride) {
-    const int64_t rem = e % sq;
-    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
-  }
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
-    for (int s = 0; s < nb - 1; ++s) {
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        const int p = rr_player(k, s, nb), q = rr_player(nb - 1 - k, s, nb);
-        const int bp = min(p, q), bq = max(p, q);
-        if (bp * W >= ell) continue;  // both blocks are padding
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        // stage: local column c < W from block bp, c >= W from block bq
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = (c < W ? bp * W + c : bq * W + (c - W));
-          const bool ok = gc < ell && r < ell;
-          Hs[e] = ok ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
-          Js[e] = ok ? __ldcg(Jg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
-        }
-        if (tid == 0) s_rot = 0;
-        __syncthreads();
-        int rotated = 0;
-        for (int it = 0; it < inner; ++it) {
-          for (int s2 = 0; s2 < NC - 1; ++s2) {
-            const int a = rr_player(warp, s2, NC), bb2 = rr_player(NC - 1 - warp, s2, NC);
-            const int i = min(a, bb2), jx = max(a, bb2);
-            double* hi = Hs + i * pitch;
-            double* hj = Hs + jx * pitch;
-            double al = 0.0, be = 0.0, ga = 0.0;
-            for (int r = lane; r < ell; r += 32) {
-              const double x = hi[r], y = hj[r];
-              al = fma(x, x, al);
-              be = fma(y, y, be);
-              ga = fma(x, y, ga);
-            }
-            al = warp_sum(al);
-            be = warp_sum(be);
-            ga = warp_sum(ga);
-            if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-              const double zeta = (be - al) / (2.0 * ga);
-              const double tt =
-                  (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              const double c = 1.0 / sqrt(1.0 + tt * tt);
-              const double sn = c * tt;
-              for (int r = lane; r < ell; r += 32) {
-                const double x = hi[r], y = hj[r];
-                hi[r] = c * x - sn * y;
-                hj[r] = sn * x + c * y;
-              }
-              double* ji = Js + i * pitch;
-              double* jj = Js + jx * pitch;
-              for (int r = lane; r < ell; r += 32) {
-                const double x = ji[r], y = jj[r];
-                ji[r] = c * x - sn * y;
-                jj[r] = sn * x + c * y;
-              }
-              rotated = 1;
-            }
-            __syncthreads();
-          }
-        }
-        if (rotated && lane == 0) atomicOr(&s_rot, 1);
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = (c < W ? bp * W + c : bq * W + (c - W));
-          if (gc < ell && r < ell) {
-            Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
-            Jg[r + static_cast<int64_t>(gc) * ellp] = Js[e];
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
-      }
-      grid.sync();
-    }
-    // Items whose sweep rotated nothing are converged (same view in every CTA).
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const unsigned f = __ldcg(fl + i);
-      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || f == 0u);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (__ldcg(fl + i) == 0u) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
-}
-
-template <int W>
-void launch_blocked_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
-                      int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
-  const int pitch = static_cast<int>(ell + (ell & 1));
-  const size_t bytes = 2 * (2 * W) * pitch * sizeof(double) + batch * sizeof(int) + 16;
-  auto kern = jacobi_blocked_kernel<W>;
-  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
-  int per_sm = 0;
-  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, bytes));
-  if (per_sm < 1) throw CudaError("jacobi_blocked_kernel: does not fit on an SM");
-  int dev = 0, sms = 0;
-  RSVD_CUDA(cudaGetDevice(&dev));
-  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int nb = static_cast<int>((ell + W - 1) / W);
-  nb += nb & 1;
-  const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
-  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp), inner = 1;
-  if (const char* e = std::getenv("RSVD_JACOBI_INNER")) inner = std::max(1, std::atoi(e));
-  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &inner, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(W * 32),
-                                        args, bytes, st));
-  RSVD_LAUNCH("jacobi_blocked_kernel");
 }
 
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
@@ -313,473 +54,10 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Block-pair one-sided Jacobi, second generation.  Same schedule as
-// jacobi_blocked_kernel, but per task only the 2W columns of H are staged in
-// shared memory; the inner sweep's rotations are accumulated into a small
-// 2W x 2W orthogonal V (shared memory) and J's block-pair columns are
-// updated once per task, J_pair <- J_pair V, with DMMA straight from/to
-// global memory.  Column norms are computed once at staging and tracked
-// through each exact 2 x 2 rotation (alpha' = alpha - t gamma,
-// beta' = beta + t gamma), so an inner step needs one dot product.  The
-// smaller footprint (H pair + V) fits two CTAs per SM.
-template <int W>
-__global__ void __launch_bounds__(W * 32, 2)
-    jacobi_pairv_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
-                        int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
-                        int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  constexpr int NC = 2 * W;
-  constexpr int VP = NC + 4;  // V pitch (column-major V[c*VP + k]), 4 mod 16 words
-  const int pitch = ell + (ell & 1);
-  double* Hs = sm;                          // NC x pitch
-  double* Vs = sm + NC * pitch;             // NC x VP
-  double* nrm = Vs + NC * VP;               // NC column norms^2
-  int* conv = reinterpret_cast<int*>(nrm + NC);  // batch ints
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol = sqrt(static_cast<double>(ell)) * DBL_EPSILON;
-
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = gtid; e < sq * batch; e += gstride) {
-    const int64_t rem = e % sq;
-    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
-  }
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) flags[e] = 0u;
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) flags[((sweep + 1) % 3) * batch + i] = 0u;
-    for (int s = 0; s < nb - 1; ++s) {
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        const int p = rr_player(k, s, nb), q = rr_player(nb - 1 - k, s, nb);
-        const int bp = min(p, q), bq = max(p, q);
-        if (bp * W >= ell) continue;  // both blocks are padding
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = gcol(c);
-          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
-        }
-        for (int e = tid; e < NC * VP; e += blockDim.x) {
-          const int c = e / VP, r = e - c * VP;
-          Vs[e] = (r == c) ? 1.0 : 0.0;
-        }
-        if (tid == 0) s_rot = 0;
-        __syncthreads();
-        for (int c = warp; c < NC; c += W) {
-          double a = 0.0;
-          for (int r = lane; r < ell; r += 32) a = fma(Hs[c * pitch + r], Hs[c * pitch + r], a);
-          a = warp_sum(a);
-          if (lane == 0) nrm[c] = a;
-        }
-        __syncthreads();
-        int rotated = 0;
-        for (int s2 = 0; s2 < NC - 1; ++s2) {
-          const int a0 = rr_player(warp, s2, NC), b0 = rr_player(NC - 1 - warp, s2, NC);
-          const int i = min(a0, b0), jx = max(a0, b0);
-          double* hi = Hs + i * pitch;
-          double* hj = Hs + jx * pitch;
-          double ga = 0.0;
-          for (int r = lane; r < ell; r += 32) ga = fma(hi[r], hj[r], ga);
-          ga = warp_sum(ga);
-          const double al = nrm[i], be = nrm[jx];
-          if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-            const double zeta = (be - al) / (2.0 * ga);
-            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + tt * tt);
-            const double sn = c * tt;
-            for (int r = lane; r < ell; r += 32) {
-              const double x = hi[r], y = hj[r];
-              hi[r] = c * x - sn * y;
-              hj[r] = sn * x + c * y;
-            }
-            if (lane < NC) {
-              double* vi = Vs + i * VP;
-              double* vj = Vs + jx * VP;
-              const double x = vi[lane], y = vj[lane];
-              vi[lane] = c * x - sn * y;
-              vj[lane] = sn * x + c * y;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              nrm[i] = al - tt * ga;
-              nrm[jx] = be + tt * ga;
-            }
-            rotated = 1;
-          }
-          __syncthreads();
-        }
-        if (rotated && lane == 0) atomicOr(&s_rot, 1);
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = gcol(c);
-          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
-        }
-        // J_pair <- J_pair V: warp per 16-row slab, A fragments straight from global.
-        __syncthreads();
-        if (s_rot) {
-          const int slabs = (ell + 15) / 16;
-          for (int sl = warp; sl < slabs; sl += W) {
-            const int r0 = sl * 16;
-            double acc[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
-            constexpr int KH = NC / 8;  // k-steps per half
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              double afr[KH][2];
-#pragma unroll
-              for (int kq = 0; kq < KH; ++kq) {
-                const int gc = gcol((h2 * KH + kq) * 4 + t4);
-                const bool okc = gc < ell;
-                const int ra = r0 + g, rb = r0 + g + 8;
-                afr[kq][0] =
-                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
-                afr[kq][1] =
-                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
-              }
-#pragma unroll
-              for (int kq = 0; kq < KH; ++kq)
-#pragma unroll
-                for (int n = 0; n < NC / 8; ++n) {
-                  const double bv = Vs[(n * 8 + g) * VP + (h2 * KH + kq) * 4 + t4];
-                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
-                }
-            }
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                const int c = n * 8 + 2 * t4 + (qq & 1);
-                const int gc = gcol(c);
-                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
-              }
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && s_rot) atomicOr(fl + item, 1u);
-      }
-      grid.sync();
-    }
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const unsigned f = __ldcg(fl + i);
-      if (tid == 0 && !conv[i] && f == 0u && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || f == 0u);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (__ldcg(fl + i) == 0u) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
-}
-
-template <int W>
-void launch_pairv_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                    unsigned* flags, int64_t batch, cudaStream_t st) {
-  constexpr int NC = 2 * W;
-  const int pitch = static_cast<int>(ell + (ell & 1));
-  const size_t bytes =
-      (static_cast<size_t>(NC) * pitch + NC * (NC + 4) + NC) * sizeof(double) +
-      batch * sizeof(int) + 16;
-  auto kern = jacobi_pairv_kernel<W>;
-  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
-  int per_sm = 0;
-  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, bytes));
-  if (per_sm < 1) throw CudaError("jacobi_pairv_kernel: does not fit on an SM");
-  int dev = 0, sms = 0;
-  RSVD_CUDA(cudaGetDevice(&dev));
-  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int nb = static_cast<int>((ell + W - 1) / W);
-  nb += nb & 1;
-  const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
-  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
-  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(W * 32),
-                                        args, bytes, st));
-  RSVD_LAUNCH("jacobi_pairv_kernel");
-}
-
-// Block-cyclic one-sided Jacobi (third generation).  Columns in blocks of 16;
-// one outer sweep = one "diagonal" phase (every block rotates its own 120
-// intra-block pairs, 15 steps of 8 disjoint pairs per block) + nb-1 phases in
-// which round-robin block pairs (p, q) rotate their 256 inter-block pairs
-// (16 steps, warp w pairs column p_w with q_{(w+t) mod 16}).  Every column pair
-// is rotated exactly once per sweep — a cyclic-by-blocks sweep — instead of
-// re-rotating intra-block pairs in every phase.  Within a step a warp keeps its
-// two columns in registers (R = ceil(l/32) rows per lane) from the dot
-// product through the update; norms are tracked through the exact 2 x 2
-// rotation; rotations accumulate into V and J_pair <- J_pair V runs once per
-// task on DMMA straight from global memory.
-__device__ long long g_jc_trace[64];  // RSVD_JACOBI_TRACE
-
-template <int R, int MINB>
-__global__ void __launch_bounds__(512, MINB)
-    jacobi_cyc_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
-                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
-                      int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  constexpr int W = 16, NC = 32, VP = NC + 4;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  __shared__ unsigned long long s_mx;
-  const int pitch = 32 * R;
-  double* Hs = sm;                  // NC x pitch
-  double* Vs = sm + NC * pitch;     // NC x VP, column-major V[c*VP + k]
-  double* nrm = Vs + NC * VP;       // NC
-  int* conv = reinterpret_cast<int*>(nrm + NC);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
-
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = gtid; e < sq * batch; e += gstride) {
-    const int64_t rem = e % sq;
-    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
-  }
-  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
-    flags[e] = 0u;
-    mxr[e] = 0ull;
-  }
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    unsigned long long* mxs = mxr + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) {
-        flags[((sweep + 1) % 3) * batch + i] = 0u;
-        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
-      }
-    for (int phase = 0; phase < nb; ++phase) {
-      const bool diag = phase == 0;
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        int bp, bq;
-        if (diag) {
-          bp = 2 * k, bq = 2 * k + 1;
-        } else {
-          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
-          bp = min(p, q), bq = max(p, q);
-        }
-        if (bp * W >= ell) continue;  // both blocks are padding
-        if (sweep == 0 && blockIdx.x == 0 && task == blockIdx.x && tid == 0 && phase < 4)
-          g_jc_trace[phase * 8 + 5] = clock64();
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = gcol(c);
-          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
-        }
-        for (int e = tid; e < NC * VP; e += blockDim.x) {
-          const int c = e / VP, r = e - c * VP;
-          Vs[e] = (r == c) ? 1.0 : 0.0;
-        }
-        if (tid == 0) {
-          s_rot = 0;
-          s_mx = 0ull;
-        }
-        __syncthreads();
-        const bool trace = sweep == 0 && blockIdx.x == 0 && task == blockIdx.x && tid == 0 && phase < 4;
-        if (trace) g_jc_trace[phase * 8 + 0] = clock64();
-        for (int c = warp; c < NC; c += W) {
-          double a = 0.0;
-#pragma unroll
-          for (int u = 0; u < R; ++u) {
-            const double x = Hs[c * pitch + lane + 32 * u];
-            a = fma(x, x, a);
-          }
-          a = warp_sum(a);
-          if (lane == 0) nrm[c] = a;
-        }
-        __syncthreads();
-        int rotated = 0;
-        int big = 0;  // a rotation with g^2 >= 1e-18 alpha beta happened
-        const int steps = diag ? 15 : 16;
-        for (int s2 = 0; s2 < steps; ++s2) {
-          int i, jx;
-          if (diag) {
-            const int blk = warp >> 3, pi = warp & 7;
-            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
-            i = blk * 16 + min(a0, b0);
-            jx = blk * 16 + max(a0, b0);
-          } else {
-            i = warp;
-            jx = 16 + ((warp + s2) & 15);
-          }
-          double* hi = Hs + i * pitch;
-          double* hj = Hs + jx * pitch;
-          double xi[R], xj[R];
-          double ga0 = 0.0, ga1 = 0.0;
-#pragma unroll
-          for (int u = 0; u < R; ++u) {
-            xi[u] = hi[lane + 32 * u];
-            xj[u] = hj[lane + 32 * u];
-            if (u & 1) ga1 = fma(xi[u], xj[u], ga1);
-            else ga0 = fma(xi[u], xj[u], ga0);
-          }
-          const double ga = warp_sum(ga0 + ga1);
-          const double al = nrm[i], be = nrm[jx];
-          // Rutishauser's rotation; the test |g| > tol sqrt(al be) squared (no
-          // square roots).  t = sign(d) 2g / (|d| + sqrt(d^2 + 4 g^2)), d = be - al:
-          // one division (the zeta form needs two) unless d, g are extreme.
-          const double gg = ga * ga, ab = al * be;
-          if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
-            big |= gg >= c_stop_ratio2 * ab;
-            const double d = be - al, g2 = 2.0 * ga;
-            const double mag = fmax(fabs(d), fabs(g2));
-            double tt;
-            if (mag > 1e-140 && mag < 1e140) {
-              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-            } else {
-              const double zeta = d / g2;
-              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            }
-            const double c = rsqrt(fma(tt, tt, 1.0));
-            const double sn = c * tt;
-#pragma unroll
-            for (int u = 0; u < R; ++u) {
-              hi[lane + 32 * u] = c * xi[u] - sn * xj[u];
-              hj[lane + 32 * u] = sn * xi[u] + c * xj[u];
-            }
-            {
-              double* vi = Vs + i * VP;
-              double* vj = Vs + jx * VP;
-              const double x = vi[lane], y = vj[lane];
-              vi[lane] = c * x - sn * y;
-              vj[lane] = sn * x + c * y;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              nrm[i] = al - tt * ga;
-              nrm[jx] = be + tt * ga;
-            }
-            rotated = 1;
-          }
-          __syncthreads();
-        }
-        if (trace) g_jc_trace[phase * 8 + 1] = clock64();
-        if (rotated && lane == 0) {
-          atomicOr(&s_rot, 1);
-          if (big) atomicMax(&s_mx, 1ull);
-        }
-        for (int e = tid; e < NC * pitch; e += blockDim.x) {
-          const int c = e / pitch, r = e - c * pitch;
-          const int gc = gcol(c);
-          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
-        }
-        __syncthreads();
-        if (trace) g_jc_trace[phase * 8 + 2] = clock64();
-        if (s_rot) {  // J_pair <- J_pair V (warp per 16-row slab, DMMA)
-          const int slabs = (ell + 15) / 16;
-          for (int sl = warp; sl < slabs; sl += W) {
-            const int r0 = sl * 16;
-            double acc[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              double afr[4][2];
-#pragma unroll
-              for (int kq = 0; kq < 4; ++kq) {
-                const int gc = gcol((h2 * 4 + kq) * 4 + t4);
-                const bool okc = gc < ell;
-                const int ra = r0 + g, rb = r0 + g + 8;
-                afr[kq][0] =
-                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
-                afr[kq][1] =
-                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
-              }
-#pragma unroll
-              for (int kq = 0; kq < 4; ++kq)
-#pragma unroll
-                for (int n = 0; n < NC / 8; ++n) {
-                  const double bv = Vs[(n * 8 + g) * VP + (h2 * 4 + kq) * 4 + t4];
-                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
-                }
-            }
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                const int c = n * 8 + 2 * t4 + (qq & 1);
-                const int gc = gcol(c);
-                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
-              }
-          }
-        }
-        __syncthreads();
-        if (trace) g_jc_trace[phase * 8 + 3] = clock64();
-        if (tid == 0 && s_rot) {
-          atomicOr(fl + item, 1u);
-          atomicMax(mxs + item, s_mx);
-        }
-      }
-      grid.sync();
-      if (sweep == 0 && blockIdx.x == 0 && tid == 0 && phase < 4) g_jc_trace[phase * 8 + 4] = clock64();
-    }
-    // An item is done after a sweep with no rotation, or after a sweep whose
-    // largest rotated |g| / sqrt(alpha beta) was below 1e-9: the cyclic
-    // method converges quadratically, so that sweep left every off-diagonal
-    // ratio near 1e-18, far under tol (the no-op check sweep is skipped).
-    auto done = [&](int64_t i) {
-      return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull;
-    };
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const bool d = done(i);
-      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || d);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (done(i)) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // 16-byte global -> shared async copy; bytes < 16 zero-fills the rest.
@@ -813,573 +91,10 @@ __device__ __forceinline__ void stage_pair(double* S, const double* G, int ell, 
   cpa_wait_all();
 }
 
-// Gram-accelerated block-cyclic Jacobi (jacobi_gram_kernel).  Same sweep
-// order, rotation formula, thresholds and convergence flags as
-// jacobi_cyc_kernel, but inside a task the 16 rotation steps act on the
-// 32 x 32 Gram matrix of the staged block pair instead of on its l-long
-// columns: G = X^T X by DMMA, then per step every warp rotates one column
-// pair of G (G <- G R, then R^T G; lane = row) and of V, and at the end X <- X V
-// (and J <- J V) by DMMA.  Each step touches 32-element rows instead of
-// 2 l-element columns.  G is formed from the freshly rotated columns at every
-// task, so the dot products that decide the rotations are the one-sided ones
-// up to the in-task updates, whose rounding is O(u |x_i| |x_k|) like a fresh
-// dot product; after the last productive sweep the convergence test runs on
-// fresh Grams.
-template <int R, int MINB>
-__global__ void __launch_bounds__(512, MINB)
-    jacobi_gram_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
-                       int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
-                       int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1;
-  constexpr int PITCH = 32 * R + 2;  // padded column pitch (Gram fragment loads)
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  __shared__ unsigned long long s_mx;
-  double* Hs = sm;                 // NC x PITCH
-  double* Vs = sm + NC * PITCH;    // NC x VP, column-major V[c*VP + k]
-  double* Gs = Vs + NC * VP;       // NC x GP, G[row + col*GP]
-  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
-
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = gtid; e < sq * batch; e += gstride) {
-    const int64_t rem = e % sq;
-    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
-  }
-  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
-    flags[e] = 0u;
-    mxr[e] = 0ull;
-  }
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  const int rows = 32 * R;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    unsigned long long* mxs = mxr + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) {
-        flags[((sweep + 1) % 3) * batch + i] = 0u;
-        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
-      }
-    for (int phase = 0; phase < nb; ++phase) {
-      const bool diag = phase == 0;
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        int bp, bq;
-        if (diag) {
-          bp = 2 * k, bq = 2 * k + 1;
-        } else {
-          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
-          bp = min(p, q), bq = max(p, q);
-        }
-        if (bp * W >= ell) continue;
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
-        stage_pair<PITCH>(Hs, Hg, ell, ellp, rows, gcol, tid, blockDim.x);
-        for (int e = tid; e < NC * VP; e += blockDim.x) {
-          const int c = e / VP, r = e - c * VP;
-          Vs[e] = (r == c) ? 1.0 : 0.0;
-        }
-        if (tid == 0) {
-          s_rot = 0;
-          s_mx = 0ull;
-        }
-        __syncthreads();
-        // G = X^T X: warps 0..7 own one 16 x 8 tile each (K = rows, DMMA).
-        if (warp < 8) {
-          const int tm = warp >> 2, tn = warp & 3;
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          const double* a0p = Hs + (16 * tm + g) * PITCH;
-          const double* a1p = Hs + (16 * tm + g + 8) * PITCH;
-          const double* b0p = Hs + (8 * tn + g) * PITCH;
-#pragma unroll 8
-          for (int k0 = 0; k0 < rows; k0 += 4)
-            dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
-          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
-          Gs[r0 + c0 * GP] = acc[0];
-          Gs[r0 + (c0 + 1) * GP] = acc[1];
-          Gs[r0 + 8 + c0 * GP] = acc[2];
-          Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
-        }
-        __syncthreads();
-        int rotated = 0, big = 0;
-        const int steps = diag ? 15 : 16;
-        for (int s2 = 0; s2 < steps; ++s2) {
-          int i, jx;
-          if (diag) {
-            const int blk = warp >> 3, pi = warp & 7;
-            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
-            i = blk * 16 + min(a0, b0);
-            jx = blk * 16 + max(a0, b0);
-          } else {
-            i = warp;
-            jx = 16 + ((warp + s2) & 15);
-          }
-          const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
-          const double gg = ga * ga, ab = al * be;
-          const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
-          double c = 1.0, sn = 0.0, tt = 0.0;
-          if (rot) {
-            big |= gg >= c_stop_ratio2 * ab;
-            const double d = be - al, g2 = 2.0 * ga;
-            const double mag = fmax(fabs(d), fabs(g2));
-            if (mag > 1e-140 && mag < 1e140) {
-              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-            } else {
-              const double zeta = d / g2;
-              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            }
-            c = rsqrt(fma(tt, tt, 1.0));
-            sn = c * tt;
-            rotated = 1;
-            // columns of G and V (lane = row)
-            const double gi = Gs[lane + i * GP], gj = Gs[lane + jx * GP];
-            Gs[lane + i * GP] = c * gi - sn * gj;
-            Gs[lane + jx * GP] = sn * gi + c * gj;
-            const double vi = Vs[i * VP + lane], vj = Vs[jx * VP + lane];
-            Vs[i * VP + lane] = c * vi - sn * vj;
-            Vs[jx * VP + lane] = sn * vi + c * vj;
-          }
-          __syncthreads();
-          if (rot) {  // rows of G, then the exact 2 x 2 block
-            const double gi = Gs[i + lane * GP], gj = Gs[jx + lane * GP];
-            Gs[i + lane * GP] = c * gi - sn * gj;
-            Gs[jx + lane * GP] = sn * gi + c * gj;
-            __syncwarp();
-            if (lane == 0) {
-              Gs[i + i * GP] = al - tt * ga;
-              Gs[jx + jx * GP] = be + tt * ga;
-              Gs[i + jx * GP] = 0.0;
-              Gs[jx + i * GP] = 0.0;
-            }
-          }
-          __syncthreads();
-        }
-        if (rotated && lane == 0) {
-          atomicOr(&s_rot, 1);
-          if (big) atomicMax(&s_mx, 1ull);
-        }
-        __syncthreads();
-        if (s_rot) {
-          // X <- X V and J <- J V, warp per 16-row slab (DMMA).
-          const int slabs = rows / 16;
-          for (int sl = warp; sl < slabs; sl += W) {
-            const int r0 = sl * 16;
-            double acc[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
-#pragma unroll
-            for (int kq = 0; kq < 8; ++kq) {
-              const int kc = kq * 4 + t4;
-              const double a0 = Hs[kc * PITCH + r0 + g], a1 = Hs[kc * PITCH + r0 + g + 8];
-#pragma unroll
-              for (int n = 0; n < NC / 8; ++n)
-                dmma_16x8x4(acc[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                const int c = n * 8 + 2 * t4 + (qq & 1);
-                Hs[c * PITCH + r] = acc[n][qq];
-              }
-          }
-          __syncthreads();
-          for (int e = tid; e < NC * rows; e += blockDim.x) {
-            const int c = e / rows, r = e - c * rows;
-            const int gc = gcol(c);
-            if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[c * PITCH + r];
-          }
-          __syncthreads();  // H written back: Hs is free for the J pair
-          stage_pair<PITCH>(Hs, Jg, ell, ellp, rows, gcol, tid, blockDim.x);
-          __syncthreads();
-          for (int sl = warp; sl < slabs; sl += W) {
-            const int r0 = sl * 16;
-            double acc[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
-#pragma unroll
-            for (int kq = 0; kq < 8; ++kq) {
-              const int kc = kq * 4 + t4;
-              const double a0 = Hs[kc * PITCH + r0 + g], a1 = Hs[kc * PITCH + r0 + g + 8];
-#pragma unroll
-              for (int n = 0; n < NC / 8; ++n)
-                dmma_16x8x4(acc[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
-            }
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                const int c = n * 8 + 2 * t4 + (qq & 1);
-                const int gc = gcol(c);
-                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
-              }
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && s_rot) {
-          atomicOr(fl + item, 1u);
-          atomicMax(mxs + item, s_mx);
-        }
-      }
-      grid.sync();
-    }
-    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const bool d = done(i);
-      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || d);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (done(i)) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
-}
-
-template <int R, int MINB>
-void launch_gram_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                   unsigned* flags, int64_t batch, cudaStream_t st) {
-  const size_t bytes = (static_cast<size_t>(32) * (32 * R + 2) + 32 * 36 + 32 * 33) * sizeof(double) +
-                       batch * sizeof(int) + 16;
-  auto kern = jacobi_gram_kernel<R, MINB>;
-  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
-  int per_sm = 0;
-  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
-  if (per_sm < 1) throw CudaError("jacobi_gram_kernel: does not fit on an SM");
-  int dev = 0, sms = 0;
-  RSVD_CUDA(cudaGetDevice(&dev));
-  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int nb = static_cast<int>((ell + 15) / 16);
-  nb += nb & 1;
-  const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
-  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
-  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512),
-                                        args, bytes, st));
-  RSVD_LAUNCH("jacobi_gram_kernel");
-}
-
-template <int R, int MINB>
-void launch_cyc_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
-                  unsigned* flags, int64_t batch, cudaStream_t st) {
-  const size_t bytes = (static_cast<size_t>(32) * 32 * R + 32 * 36 + 32) * sizeof(double) +
-                       batch * sizeof(int) + 16;
-  auto kern = jacobi_cyc_kernel<R, MINB>;
-  RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
-  int per_sm = 0;
-  RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, bytes));
-  if (per_sm < 1) throw CudaError("jacobi_cyc_kernel: does not fit on an SM");
-  int dev = 0, sms = 0;
-  RSVD_CUDA(cudaGetDevice(&dev));
-  RSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int nb = static_cast<int>((ell + 15) / 16);
-  nb += nb & 1;
-  const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * sms)));
-  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
-  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(512),
-                                        args, bytes, st));
-  RSVD_LAUNCH("jacobi_cyc_kernel");
-  if (std::getenv("RSVD_JACOBI_TRACE")) {
-    long long tr[64] = {};
-    RSVD_CUDA(cudaStreamSynchronize(st));
-    RSVD_CUDA(cudaMemcpyFromSymbol(tr, g_jc_trace, sizeof(tr)));
-    std::fprintf(stderr, "jacobi_cyc R=%d ell=%lld batch=%lld grid=%d\n", R, (long long)ell, (long long)batch, grid);
-    for (int ph = 0; ph < 4; ++ph)
-      std::fprintf(stderr, "  phase %d: load %lld steps %lld store %lld jupd %lld sync+idle %lld cycles\n", ph,
-                   tr[ph * 8 + 0] - tr[ph * 8 + 5], tr[ph * 8 + 1] - tr[ph * 8 + 0], tr[ph * 8 + 2] - tr[ph * 8 + 1],
-                   tr[ph * 8 + 3] - tr[ph * 8 + 2], tr[ph * 8 + 4] - tr[ph * 8 + 3]);
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// Row-split block-cyclic Jacobi for few items (jacobi_clu_kernel).  Same sweep
-// order, rotations, norm tracking and convergence rules as jacobi_cyc_kernel,
-// but every (item, block pair) task is owned by a thread-block CLUSTER of S
-// CTAs, CTA q holding rows [q * 32 RL, (q + 1) * 32 RL) of the 32 columns and
-// of J: each column-pair dot product is a warp-local partial sum, published in
-// shared memory and reduced across the cluster through DSMEM in a fixed rank
-// order (so every CTA derives bit-identical rotations), one cluster barrier
-// per rotation step.  A single 4096^2 matrix (9 block pairs) then runs on 45
-// SMs instead of 9, each with 1/5 of the rows.
-template <int RL>
-__global__ void __launch_bounds__(512, 1)
-    jacobi_clu_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
-                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
-                      int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  cg::cluster_group cluster = cg::this_cluster();
-  constexpr int W = 16, NC = 32, VP = NC + 4, PITCH = 32 * RL;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_rot;
-  __shared__ unsigned long long s_mx;
-  __shared__ double pd[2][W];  // per-warp partial dots, double-buffered by step parity
-  __shared__ double pn[NC];    // per-column partial norms
-  double* Hs = sm;              // NC x PITCH (local rows)
-  double* Vs = sm + NC * PITCH;  // NC x VP
-  double* nrm = Vs + NC * VP;    // NC
-  int* conv = reinterpret_cast<int*>(nrm + NC);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int S = static_cast<int>(cluster.num_blocks());
-  const int q = static_cast<int>(cluster.block_rank());
-  const int row0 = q * PITCH;  // first global row of this CTA
-  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
-  const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
-  const int64_t nclu = gridDim.x / S;
-  const int64_t clu = blockIdx.x / S;
-
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = gtid; e < sq * batch; e += gstride) {
-    const int64_t rem = e % sq;
-    J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
-  }
-  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
-    flags[e] = 0u;
-    mxr[e] = 0ull;
-  }
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    unsigned long long* mxs = mxr + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) {
-        flags[((sweep + 1) % 3) * batch + i] = 0u;
-        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
-      }
-    for (int phase = 0; phase < nb; ++phase) {
-      const bool diag = phase == 0;
-      for (int64_t task = clu; task < tasks; task += nclu) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        int bp, bq;
-        if (diag) {
-          bp = 2 * k, bq = 2 * k + 1;
-        } else {
-          const int p = rr_player(k, phase - 1, nb), qq = rr_player(nb - 1 - k, phase - 1, nb);
-          bp = min(p, qq), bq = max(p, qq);
-        }
-        if (bp * W >= ell) continue;  // both blocks are padding (uniform in the cluster)
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
-        for (int e = tid; e < NC * PITCH; e += blockDim.x) {
-          const int c = e / PITCH, r = row0 + (e - c * PITCH);
-          const int gc = gcol(c);
-          Hs[e] = (gc < ell && r < ell) ? __ldcg(Hg + r + static_cast<int64_t>(gc) * ellp) : 0.0;
-        }
-        for (int e = tid; e < NC * VP; e += blockDim.x) {
-          const int c = e / VP, r = e - c * VP;
-          Vs[e] = (r == c) ? 1.0 : 0.0;
-        }
-        if (tid == 0) {
-          s_rot = 0;
-          s_mx = 0ull;
-        }
-        __syncthreads();
-        for (int c = warp; c < NC; c += W) {
-          double a = 0.0;
-#pragma unroll
-          for (int u = 0; u < RL; ++u) {
-            const double x = Hs[c * PITCH + lane + 32 * u];
-            a = fma(x, x, a);
-          }
-          a = warp_sum(a);
-          if (lane == 0) pn[c] = a;
-        }
-        cluster.sync();
-        for (int c = tid; c < NC; c += blockDim.x) {
-          double a = 0.0;
-          for (int r = 0; r < S; ++r) a += *cluster.map_shared_rank(&pn[c], r);
-          nrm[c] = a;
-        }
-        cluster.sync();  // pn reads done before the next task rewrites it; nrm visible
-        int rotated = 0, big = 0;
-        const int steps = diag ? 15 : 16;
-        for (int s2 = 0; s2 < steps; ++s2) {
-          int i, jx;
-          if (diag) {
-            const int blk = warp >> 3, pi = warp & 7;
-            const int a0 = rr_player(pi, s2, 16), b0 = rr_player(15 - pi, s2, 16);
-            i = blk * 16 + min(a0, b0);
-            jx = blk * 16 + max(a0, b0);
-          } else {
-            i = warp;
-            jx = 16 + ((warp + s2) & 15);
-          }
-          double* hi = Hs + i * PITCH;
-          double* hj = Hs + jx * PITCH;
-          double xi[RL], xj[RL];
-          double ga = 0.0;
-#pragma unroll
-          for (int u = 0; u < RL; ++u) {
-            xi[u] = hi[lane + 32 * u];
-            xj[u] = hj[lane + 32 * u];
-            ga = fma(xi[u], xj[u], ga);
-          }
-          ga = warp_sum(ga);
-          const int buf = s2 & 1;
-          if (lane == 0) pd[buf][warp] = ga;
-          cluster.sync();
-          ga = 0.0;
-          for (int r = 0; r < S; ++r) ga += *cluster.map_shared_rank(&pd[buf][warp], r);
-          const double al = nrm[i], be = nrm[jx];
-          const double gg = ga * ga, ab = al * be;
-          if (al > 0.0 && be > 0.0 && gg > tol2 * ab) {
-            big |= gg >= c_stop_ratio2 * ab;
-            const double d = be - al, g2 = 2.0 * ga;
-            const double mag = fmax(fabs(d), fabs(g2));
-            double tt;
-            if (mag > 1e-140 && mag < 1e140) {
-              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-            } else {
-              const double zeta = d / g2;
-              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            }
-            const double c = rsqrt(fma(tt, tt, 1.0));
-            const double sn = c * tt;
-#pragma unroll
-            for (int u = 0; u < RL; ++u) {
-              hi[lane + 32 * u] = c * xi[u] - sn * xj[u];
-              hj[lane + 32 * u] = sn * xi[u] + c * xj[u];
-            }
-            {
-              double* vi = Vs + i * VP;
-              double* vj = Vs + jx * VP;
-              const double x = vi[lane], y = vj[lane];
-              vi[lane] = c * x - sn * y;
-              vj[lane] = sn * x + c * y;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              nrm[i] = al - tt * ga;
-              nrm[jx] = be + tt * ga;
-            }
-            rotated = 1;
-          }
-          __syncthreads();
-        }
-        if (rotated && lane == 0) {
-          atomicOr(&s_rot, 1);
-          if (big) atomicMax(&s_mx, 1ull);
-        }
-        for (int e = tid; e < NC * PITCH; e += blockDim.x) {
-          const int c = e / PITCH, r = row0 + (e - c * PITCH);
-          const int gc = gcol(c);
-          if (gc < ell && r < ell) Hg[r + static_cast<int64_t>(gc) * ellp] = Hs[e];
-        }
-        __syncthreads();
-        if (s_rot) {  // local rows of J_pair <- J_pair V (warp per 16-row slab, DMMA)
-          const int slabs = PITCH / 16;
-          for (int sl = warp; sl < slabs; sl += W) {
-            const int r0 = row0 + sl * 16;
-            double acc[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) acc[n][qq] = 0.0;
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              double afr[4][2];
-#pragma unroll
-              for (int kq = 0; kq < 4; ++kq) {
-                const int gc = gcol((h2 * 4 + kq) * 4 + t4);
-                const bool okc = gc < ell;
-                const int ra = r0 + g, rb = r0 + g + 8;
-                afr[kq][0] =
-                    (okc && ra < ell) ? __ldcg(Jg + ra + static_cast<int64_t>(gc) * ellp) : 0.0;
-                afr[kq][1] =
-                    (okc && rb < ell) ? __ldcg(Jg + rb + static_cast<int64_t>(gc) * ellp) : 0.0;
-              }
-#pragma unroll
-              for (int kq = 0; kq < 4; ++kq)
-#pragma unroll
-                for (int n = 0; n < NC / 8; ++n) {
-                  const double bv = Vs[(n * 8 + g) * VP + (h2 * 4 + kq) * 4 + t4];
-                  dmma_16x8x4(acc[n], afr[kq][0], afr[kq][1], bv);
-                }
-            }
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = r0 + g + ((qq & 2) ? 8 : 0);
-                const int c = n * 8 + 2 * t4 + (qq & 1);
-                const int gc = gcol(c);
-                if (r < ell && gc < ell) Jg[r + static_cast<int64_t>(gc) * ellp] = acc[n][qq];
-              }
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && q == 0 && s_rot) {
-          atomicOr(fl + item, 1u);
-          atomicMax(mxs + item, s_mx);
-        }
-      }
-      grid.sync();
-    }
-    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const bool d = done(i);
-      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || d);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (done(i)) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
-}
-
-// Cluster + Gram variant (jacobi_clug_kernel): the row-split cluster of
-// jacobi_clu_kernel, with each task's rotations done on the block pair's
-// 32 x 32 Gram: every CTA forms the Gram of its row slice on DMMA, the S
+// Row-split cluster variant (jacobi_clug_kernel) for few tasks: every
+// (item, block pair) task is owned by a thread-block CLUSTER of S CTAs, CTA q
+// holding a slice of the rows of the 32 columns and of J; each task's
+// rotations are done on the block pair's 32 x 32 Gram: every CTA forms the Gram of its row slice on DMMA, the S
 // partials are summed through DSMEM in rank order (bit-identical G in every
 // CTA), the 16 steps run redundantly on G and V in each CTA, and each CTA
 // applies X <- X V, J <- J V to its rows.  Two cluster barriers per task
@@ -1640,13 +355,9 @@ __global__ void __launch_bounds__(512, 1)
 template <int RL>
 bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                   unsigned* flags, int64_t batch, int S, cudaStream_t st) {
-  static const bool no_gram = std::getenv("RSVD_JACOBI_NO_GRAM") != nullptr;
-  const size_t bytes =
-      no_gram ? (static_cast<size_t>(32) * 32 * RL + 32 * 36 + 32) * sizeof(double) +
-                    batch * sizeof(int) + 16
-              : (static_cast<size_t>(32) * (32 * RL + 2) + 32 * 36 + 2 * 32 * 33) * sizeof(double) +
-                    batch * sizeof(int) + 16;
-  auto kern = no_gram ? jacobi_clu_kernel<RL> : jacobi_clug_kernel<RL>;
+  const size_t bytes = (static_cast<size_t>(32) * (32 * RL + 2) + 32 * 36 + 2 * 32 * 33) * sizeof(double) +
+                       batch * sizeof(int) + 16;
+  auto kern = jacobi_clug_kernel<RL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(bytes)) != cudaSuccess ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -1683,7 +394,7 @@ bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
     cudaGetLastError();
     return false;
   }
-  RSVD_LAUNCH("jacobi_clu_kernel");
+  RSVD_LAUNCH("jacobi_clug_kernel");
   return true;
 }
 
@@ -1691,7 +402,6 @@ bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweep
 // clusters of all tasks co-resident), rounded so the S slices cover l.
 bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                 unsigned* flags, int64_t batch, cudaStream_t st) {
-  if (std::getenv("RSVD_NO_JACOBI_CLUSTER")) return false;
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
   const int64_t tasks = batch * (nb / 2);
@@ -1700,7 +410,6 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
   // 5-6 CTAs per task measured best (C3: S 3/5/9 -> 4.6/4.4/4.8 ms, C5:
   // S 3/5/9 -> 11.1/9.7/18.7 ms -- at 9 the clusters no longer fit at once).
   int smax = static_cast<int>(std::min<int64_t>(6, num_sms() / std::max<int64_t>(tasks, 1)));
-  if (const char* e = std::getenv("RSVD_JACOBI_CLUSTER")) smax = std::atoi(e);
   if (smax < 2) return false;
   int rl = (R + smax - 1) / smax;
   static const int kRL[] = {1, 2, 3, 4, 6, 8, 12};  // 8, 12: wide factors (tsvd up to l = 1600)
@@ -1723,410 +432,385 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
 
 
 // ---------------------------------------------------------------------------
-// Row-streamed Gram-accelerated block-cyclic Jacobi (jacobi_rs_kernel).
-// Same sweep order, rotation formula, thresholds and convergence flags as
-// jacobi_gram_kernel, re-laid-out so that nothing scales with l in shared
-// memory: any l (tsvd up to min(m, n) = 4096 and beyond) and small CTAs.
-//   * G = X^T X of the task's 32 columns is accumulated over row chunks of RC
-//     rows, staged by cp.async into a double buffer (DMMA, 8 warps, one
-//     16 x 8 tile each);
-//   * the 16 rotation steps run on G / V in shared memory (8 warps, two
-//     column pairs each per step);
-//   * X <- X V and J <- J V read their 16-row slabs straight from global
-//     memory (L2) into DMMA fragments and write the products back in place
-//     (a warp loads its whole slab before it stores it).
-// 256 threads and ~52 KB per CTA: 3 CTAs (24 warps) per SM keep several
-// tasks' latency-bound rotation steps in flight.
-template <int RC>
-__global__ void __launch_bounds__(256, 3)
-    jacobi_rs_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
+// Dataflow row-streamed Gram-accelerated block-cyclic Jacobi (jacobi_df_kernel).
+// Same sweep order, rotation formula, thresholds and convergence rule as
+// jacobi_gram_kernel, but
+//   * no grid-wide barrier: tasks (sweep, phase, item, block pair) are pulled
+//     in that order from one atomic counter by a persistent grid, and a task
+//     waits only for its OWN item's previous phase (a per-item completion
+//     counter, release/acquire) -- items, and the pairs of a phase, never wait
+//     for each other, so uneven task times and converged items cost nothing;
+//   * the convergence decision for sweep s of an item is taken by its phase-0
+//     tasks of sweep s + 1 from that sweep's final flags;
+//   * nothing scales with l in shared memory: G = X^T X of the task's 32
+//     columns is accumulated over RC-row chunks staged by cp.async (double
+//     buffer), the 16 rotation steps run on G / V in shared memory (8 warps,
+//     two column pairs each per step), and X <- X V, J <- J V read their
+//     16-row slabs from global memory (L2) into DMMA fragments and write the
+//     products back in place -- any l (tsvd of 4096^2 and beyond).
+// Dependencies point only to earlier tasks, which were pulled by running
+// CTAs, so the launch needs no co-residency guarantee (plain launch, graph
+// friendly).  Workspace (jacobi_flag_elems): per item 3 rotating "rotated"
+// flags, 3 rotating "big rotation" flags, a completion counter and a
+// converged flag; then the task counter and the converged-item count.
+template <int RC, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    jacobi_df_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
                      int* __restrict__ sweeps_out) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, NW = 8;
   constexpr int PITCH = RC + 2;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_rot;
   __shared__ unsigned long long s_mx;
+  __shared__ long long s_task;
+  __shared__ int s_work;
   const int nch = (ell + RC - 1) / RC;
-  double* Xs = sm;                              // (1 or 2) x (NC x PITCH): row-chunk buffers
+  double* Xs = sm;                                   // (1 or 2) x (NC x PITCH) row chunks
   double* Vs = sm + (nch > 1 ? 2 : 1) * NC * PITCH;  // NC x VP, column-major V[c*VP + k]
-  double* Gs = Vs + NC * VP;           // NC x GP, G[row + col*GP]
-  int* conv = reinterpret_cast<int*>(Gs + NC * GP);
+  double* Gs = Vs + NC * VP;                         // NC x GP, G[row + col*GP]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t sq = static_cast<int64_t>(ellp) * ellp;
   const double tol2 = static_cast<double>(ell) * DBL_EPSILON * DBL_EPSILON;
 
-  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid;
+  const int64_t fpad = (3 * batch + 1) & ~int64_t(1);
+  unsigned* fl3 = flags;
+  unsigned long long* mx3 = reinterpret_cast<unsigned long long*>(flags + fpad);
+  unsigned* cnt = flags + fpad + 6 * batch;
+  unsigned* convg = cnt + batch;
+  unsigned long long* next = reinterpret_cast<unsigned long long*>(convg + batch);
+  unsigned* nconv = reinterpret_cast<unsigned*>(next + 1);
+
+  const int half = nb / 2;
+  const int64_t per_phase = batch * half;
+  const int64_t total = static_cast<int64_t>(max_sweeps) * nb * per_phase;
+  const int slabs = (ell + 15) / 16;
+  for (;;) {
+    if (tid == 0) {
+      long long t = -1;
+      if (*reinterpret_cast<volatile unsigned*>(nconv) < batch) {
+        t = static_cast<long long>(atomicAdd(next, 1ull));
+        if (t >= total) t = -1;
+      }
+      s_task = t;
+    }
+    __syncthreads();
+    const long long t = s_task;
+    if (t < 0) break;
+    const int sweep = static_cast<int>(t / (nb * per_phase));
+    const int64_t rem = t - static_cast<int64_t>(sweep) * nb * per_phase;
+    const int phase = static_cast<int>(rem / per_phase);
+    const int64_t r2 = rem - phase * per_phase;
+    const int64_t item = r2 / half;
+    const int k = static_cast<int>(r2 - item * half);
+    const bool diag = phase == 0;
+    int bp, bq;
+    if (diag) {
+      bp = 2 * k, bq = 2 * k + 1;
+    } else {
+      const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
+      bp = min(p, q), bq = max(p, q);
+    }
+    if (tid == 0) {
+      // 1: do the task; 0: count it without work; -1: item converged, skip
+      int work = 1;
+      const unsigned need = static_cast<unsigned>((static_cast<int64_t>(sweep) * nb + phase) * half);
+      volatile unsigned* vc = convg + item;
+      unsigned c;
+      while ((c = ld_acquire(cnt + item)) < need && *vc == 0u) __nanosleep(100);
+      if (*vc != 0u) {
+        work = -1;
+      } else if (diag && sweep > 0) {
+        const int slot = (sweep - 1) % 3;
+        if (__ldcg(fl3 + slot * batch + item) == 0u || __ldcg(mx3 + slot * batch + item) == 0ull) {
+          work = -1;
+          // every phase-0 task of this sweep reaches the same verdict; the
+          // first one to flag the item records it
+          if (atomicCAS(convg + item, 0u, 1u) == 0u) {
+            sweeps_out[item] = sweep;
+            atomicAdd(nconv, 1u);
+          }
+        }
+      }
+      if (work == 1 && diag && k == 0) {  // this sweep's successor slot starts clean
+        const int slot = (sweep + 1) % 3;
+        fl3[slot * batch + item] = 0u;
+        mx3[slot * batch + item] = 0ull;
+      }
+      if (work == 1 && bp * W >= ell) work = 0;
+      s_work = work;
+      s_rot = 0;
+      s_mx = 0ull;
+    }
+    __syncthreads();
+    const int work = s_work;
+    if (work == 1) {
+      double* Hg = H + item * sq;
+      double* Jg = J + item * sq;
+      auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
+      auto stage = [&](int c, int buf) {
+        const int r0 = c * RC;
+        double* dst = Xs + buf * NC * PITCH;
+        for (int e = tid; e < NC * (RC / 2); e += NW * 32) {
+          const int cc = e / (RC / 2), r = 2 * (e - cc * (RC / 2));
+          const int gc = gcol(cc), gr = r0 + r;
+          int bytes = 0;
+          const double* src = Hg;
+          if (gc < ell && gr < ell) {
+            bytes = min(16, (ell - gr) * 8);
+            src = Hg + gr + static_cast<int64_t>(gc) * ellp;
+          }
+          cpa16(dst + cc * PITCH + r, src, bytes);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      for (int e = tid; e < NC * VP; e += NW * 32) {
+        const int c = e / VP, r = e - c * VP;
+        Vs[e] = (r == c) ? 1.0 : 0.0;
+      }
+      // ---- G = X^T X over row chunks (cp.async double buffer, DMMA) ----
+      const int tm = warp >> 2, tn = warp & 3;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      stage(0, 0);
+      for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) {
+          stage(c + 1, (c + 1) & 1);
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const double* Xb = Xs + (c & 1) * NC * PITCH;
+        const double* a0p = Xb + (16 * tm + g) * PITCH;
+        const double* a1p = Xb + (16 * tm + g + 8) * PITCH;
+        const double* b0p = Xb + (8 * tn + g) * PITCH;
+#pragma unroll 8
+        for (int k0 = 0; k0 < RC; k0 += 4)
+          dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+        __syncthreads();  // buffer c & 1 is restaged at c + 2
+      }
+      {
+        const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
+        Gs[r0 + c0 * GP] = acc[0];
+        Gs[r0 + (c0 + 1) * GP] = acc[1];
+        Gs[r0 + 8 + c0 * GP] = acc[2];
+        Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
+      }
+      __syncthreads();
+      // ---- rotation steps on G and V ----
+      // A step's 16 disjoint pairs act on G as G <- R^T G R with R a
+      // permuted direct sum of 2 x 2 rotations, so every 2 x 2 block
+      // (pair p rows, pair q cols) transforms independently:
+      // G_pq <- R_p^T G_pq R_q.  Phase A: thread p < 16 derives pair p's
+      // rotation from the current G; phase B: one thread per upper block
+      // (p <= q, mirrored) and two V rows per thread apply them.
+      double* Rc = Gs + NC * GP;  // c, s, t per pair; flag per pair after
+      int* Rf = reinterpret_cast<int*>(Rc + 3 * 16);
+      int rotated = 0, big = 0;
+      const int steps = diag ? 15 : 16;
+      auto pair_of = [&](int pr, int s2, int& i, int& jx) {
+        if (diag) {
+          const int blk = pr >> 3, pk = pr & 7;
+          const int a0 = rr_player(pk, s2, 16), b0 = rr_player(15 - pk, s2, 16);
+          i = blk * 16 + min(a0, b0);
+          jx = blk * 16 + max(a0, b0);
+        } else {
+          i = pr;
+          jx = 16 + ((pr + s2) & 15);
+        }
+      };
+      const int bpp = tid >> 4, bqq = tid & 15;  // phase-B block of this thread
+      const int vp = tid >> 4, vr = (tid & 15) * 2;  // phase-B V rows of this thread
+      for (int s2 = 0; s2 < steps; ++s2) {
+        if (tid < 16) {
+          int i, jx;
+          pair_of(tid, s2, i, jx);
+          const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
+          const double gg = ga * ga, ab = al * be;
+          const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
+          double c = 1.0, sn = 0.0, tt = 0.0;
+          if (rot) {
+            big |= gg >= c_stop_ratio2 * ab;
+            const double d = be - al, g2 = 2.0 * ga;
+            const double mag = fmax(fabs(d), fabs(g2));
+            if (mag > 1e-140 && mag < 1e140) {
+              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            } else {
+              const double zeta = d / g2;
+              tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            }
+            c = rsqrt(fma(tt, tt, 1.0));
+            sn = c * tt;
+            rotated = 1;
+          }
+          Rc[tid] = c;
+          Rc[16 + tid] = sn;
+          Rc[32 + tid] = tt;
+          Rf[tid] = rot;
+        }
+        __syncthreads();
+        if (bpp <= bqq) {
+          int ip, jp, iq, jq;
+          pair_of(bpp, s2, ip, jp);
+          pair_of(bqq, s2, iq, jq);
+          if (bpp == bqq) {
+            if (Rf[bpp]) {
+              const double ga = Gs[ip + jp * GP], tt = Rc[32 + bpp];
+              Gs[ip + ip * GP] -= tt * ga;
+              Gs[jp + jp * GP] += tt * ga;
+              Gs[ip + jp * GP] = 0.0;
+              Gs[jp + ip * GP] = 0.0;
+            }
+          } else if (Rf[bpp] | Rf[bqq]) {
+            const double cp = Rc[bpp], sp = Rc[16 + bpp], cq = Rc[bqq], sq2 = Rc[16 + bqq];
+            const double a = Gs[ip + iq * GP], b = Gs[ip + jq * GP];
+            const double c0 = Gs[jp + iq * GP], d = Gs[jp + jq * GP];
+            // right: columns (iq, jq) by R_q; left: rows (ip, jp) by R_p
+            const double a1 = cq * a - sq2 * b, b1 = sq2 * a + cq * b;
+            const double c1 = cq * c0 - sq2 * d, d1 = sq2 * c0 + cq * d;
+            const double a2 = cp * a1 - sp * c1, c2 = sp * a1 + cp * c1;
+            const double b2 = cp * b1 - sp * d1, d2 = sp * b1 + cp * d1;
+            Gs[ip + iq * GP] = a2;
+            Gs[ip + jq * GP] = b2;
+            Gs[jp + iq * GP] = c2;
+            Gs[jp + jq * GP] = d2;
+            Gs[iq + ip * GP] = a2;
+            Gs[jq + ip * GP] = b2;
+            Gs[iq + jp * GP] = c2;
+            Gs[jq + jp * GP] = d2;
+          }
+        }
+        if (Rf[vp]) {
+          int i, jx;
+          pair_of(vp, s2, i, jx);
+          const double c = Rc[vp], sn = Rc[16 + vp];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double vi = Vs[i * VP + vr + u], vj = Vs[jx * VP + vr + u];
+            Vs[i * VP + vr + u] = c * vi - sn * vj;
+            Vs[jx * VP + vr + u] = sn * vi + c * vj;
+          }
+        }
+        __syncthreads();
+      }
+      if (rotated) {
+        atomicOr(&s_rot, 1);
+        if (big) atomicMax(&s_mx, 1ull);
+      }
+      __syncthreads();
+      if (s_rot) {
+        // ---- X <- X V and J <- J V, in place, 16-row slab per warp ----
+        for (int job = warp; job < 2 * slabs; job += NW) {
+          double* M = job < slabs ? Hg : Jg;
+          const int r0 = (job < slabs ? job : job - slabs) * 16;
+          const int ra = r0 + g, rb = r0 + g + 8;
+          double accv[NC / 8][4];
+#pragma unroll
+          for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) accv[n][qq] = 0.0;
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) {
+            const int kc = kq * 4 + t4;
+            const int gc = gcol(kc);
+            const double* col = M + static_cast<int64_t>(gc) * ellp;
+            const bool okc = gc < ell;
+            const double a0 = (okc && ra < ell) ? __ldcg(col + ra) : 0.0;
+            const double a1 = (okc && rb < ell) ? __ldcg(col + rb) : 0.0;
+#pragma unroll
+            for (int n = 0; n < NC / 8; ++n)
+              dmma_16x8x4(accv[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
+          }
+#pragma unroll
+          for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const int r = (qq & 2) ? rb : ra;
+              const int gc = gcol(n * 8 + 2 * t4 + (qq & 1));
+              if (r < ell && gc < ell) __stcg(M + r + static_cast<int64_t>(gc) * ellp, accv[n][qq]);
+            }
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && s_rot) {
+        const int slot = sweep % 3;
+        atomicOr(fl3 + slot * batch + item, 1u);
+        atomicMax(mx3 + slot * batch + item, s_mx);
+      }
+    }
+    if (tid == 0 && work >= 0) {
+      __threadfence();
+      atomicAdd(cnt + item, 1u);
+    }
+  }
+}
+
+// J = I per item, sweeps = max_sweeps (overwritten on convergence), flags,
+// counters and the task queue zeroed.
+__global__ void jacobi_df_init_kernel(double* __restrict__ J, int ellp, int64_t batch,
+                                      int max_sweeps, unsigned* __restrict__ flags,
+                                      int64_t nflags, int* __restrict__ sweeps_out) {
+  const int64_t sq = static_cast<int64_t>(ellp) * ellp;
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t e = gtid; e < sq * batch; e += gstride) {
     const int64_t rem = e % sq;
     J[e] = (rem % ellp == rem / ellp) ? 1.0 : 0.0;
   }
-  unsigned long long* mxr = reinterpret_cast<unsigned long long*>(flags + ((3 * batch + 1) & ~int64_t(1)));
-  for (int64_t e = gtid; e < 3 * batch; e += gstride) {
-    flags[e] = 0u;
-    mxr[e] = 0ull;
-  }
-  for (int64_t i = tid; i < batch; i += blockDim.x) conv[i] = 0;
-  grid.sync();
-
-  const int half = nb / 2;
-  const int64_t tasks = batch * half;
-  const int slabs = (ell + 15) / 16;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned* fl = flags + (sweep % 3) * batch;
-    unsigned long long* mxs = mxr + (sweep % 3) * batch;
-    if (blockIdx.x == 0)
-      for (int64_t i = tid; i < batch; i += blockDim.x) {
-        flags[((sweep + 1) % 3) * batch + i] = 0u;
-        mxr[((sweep + 1) % 3) * batch + i] = 0ull;
-      }
-    for (int phase = 0; phase < nb; ++phase) {
-      const bool diag = phase == 0;
-      for (int64_t task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const int64_t item = task / half;
-        if (conv[item]) continue;
-        const int k = static_cast<int>(task % half);
-        int bp, bq;
-        if (diag) {
-          bp = 2 * k, bq = 2 * k + 1;
-        } else {
-          const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
-          bp = min(p, q), bq = max(p, q);
-        }
-        if (bp * W >= ell) continue;
-        double* Hg = H + item * sq;
-        double* Jg = J + item * sq;
-        auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
-        // ---- G = X^T X over row chunks (cp.async double buffer, DMMA) ----
-        auto stage = [&](int c, int buf) {
-          const int r0 = c * RC;
-          double* dst = Xs + buf * NC * PITCH;
-          for (int e = tid; e < NC * (RC / 2); e += NW * 32) {
-            const int cc = e / (RC / 2), r = 2 * (e - cc * (RC / 2));
-            const int gc = gcol(cc), gr = r0 + r;
-            int bytes = 0;
-            const double* src = Hg;
-            if (gc < ell && gr < ell) {
-              bytes = min(16, (ell - gr) * 8);
-              src = Hg + gr + static_cast<int64_t>(gc) * ellp;
-            }
-            cpa16(dst + cc * PITCH + r, src, bytes);
-          }
-          asm volatile("cp.async.commit_group;\n" ::: "memory");
-        };
-        for (int e = tid; e < NC * VP; e += NW * 32) {
-          const int c = e / VP, r = e - c * VP;
-          Vs[e] = (r == c) ? 1.0 : 0.0;
-        }
-        if (tid == 0) {
-          s_rot = 0;
-          s_mx = 0ull;
-        }
-        const int tm = warp >> 2, tn = warp & 3;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        stage(0, 0);
-        for (int c = 0; c < nch; ++c) {
-          if (c + 1 < nch) {
-            stage(c + 1, (c + 1) & 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-          } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-          }
-          __syncthreads();
-          const double* Xb = Xs + (c & 1) * NC * PITCH;
-          const double* a0p = Xb + (16 * tm + g) * PITCH;
-          const double* a1p = Xb + (16 * tm + g + 8) * PITCH;
-          const double* b0p = Xb + (8 * tn + g) * PITCH;
-#pragma unroll 8
-          for (int k0 = 0; k0 < RC; k0 += 4)
-            dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
-          __syncthreads();  // buffer c & 1 is restaged at c + 2
-        }
-        {
-          const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
-          Gs[r0 + c0 * GP] = acc[0];
-          Gs[r0 + (c0 + 1) * GP] = acc[1];
-          Gs[r0 + 8 + c0 * GP] = acc[2];
-          Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
-        }
-        __syncthreads();
-        // ---- rotation steps on G and V (each warp: two column pairs) ----
-        int rotated = 0, big = 0;
-        const int steps = diag ? 15 : 16;
-        for (int s2 = 0; s2 < steps; ++s2) {
-          int pi[2], pj[2];
-          double pc[2], ps[2], pt[2], pal[2], pbe[2], pga[2];
-          bool prot[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int pr = warp + NW * u;  // pair 0..15
-            int i, jx;
-            if (diag) {
-              const int blk = pr >> 3, pk = pr & 7;
-              const int a0 = rr_player(pk, s2, 16), b0 = rr_player(15 - pk, s2, 16);
-              i = blk * 16 + min(a0, b0);
-              jx = blk * 16 + max(a0, b0);
-            } else {
-              i = pr;
-              jx = 16 + ((pr + s2) & 15);
-            }
-            pi[u] = i;
-            pj[u] = jx;
-            const double al = Gs[i + i * GP], be = Gs[jx + jx * GP], ga = Gs[i + jx * GP];
-            pal[u] = al;
-            pbe[u] = be;
-            pga[u] = ga;
-            const double gg = ga * ga, ab = al * be;
-            const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
-            double c = 1.0, sn = 0.0, tt = 0.0;
-            if (rot) {
-              big |= gg >= c_stop_ratio2 * ab;
-              const double d = be - al, g2 = 2.0 * ga;
-              const double mag = fmax(fabs(d), fabs(g2));
-              if (mag > 1e-140 && mag < 1e140) {
-                tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-              } else {
-                const double zeta = d / g2;
-                tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-              }
-              c = rsqrt(fma(tt, tt, 1.0));
-              sn = c * tt;
-              rotated = 1;
-            }
-            prot[u] = rot;
-            pc[u] = c;
-            ps[u] = sn;
-            pt[u] = tt;
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (!prot[u]) continue;
-            const int i = pi[u], jx = pj[u];
-            const double c = pc[u], sn = ps[u];
-            const double gi = Gs[lane + i * GP], gj = Gs[lane + jx * GP];
-            Gs[lane + i * GP] = c * gi - sn * gj;
-            Gs[lane + jx * GP] = sn * gi + c * gj;
-            const double vi = Vs[i * VP + lane], vj = Vs[jx * VP + lane];
-            Vs[i * VP + lane] = c * vi - sn * vj;
-            Vs[jx * VP + lane] = sn * vi + c * vj;
-          }
-          __syncthreads();
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (!prot[u]) continue;
-            const int i = pi[u], jx = pj[u];
-            const double c = pc[u], sn = ps[u];
-            const double gi = Gs[i + lane * GP], gj = Gs[jx + lane * GP];
-            Gs[i + lane * GP] = c * gi - sn * gj;
-            Gs[jx + lane * GP] = sn * gi + c * gj;
-          }
-          __syncwarp();
-          if (lane == 0) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (!prot[u]) continue;
-              const int i = pi[u], jx = pj[u];
-              Gs[i + i * GP] = pal[u] - pt[u] * pga[u];
-              Gs[jx + jx * GP] = pbe[u] + pt[u] * pga[u];
-              Gs[i + jx * GP] = 0.0;
-              Gs[jx + i * GP] = 0.0;
-            }
-          }
-          __syncthreads();
-        }
-        if (rotated && lane == 0) {
-          atomicOr(&s_rot, 1);
-          if (big) atomicMax(&s_mx, 1ull);
-        }
-        __syncthreads();
-        if (s_rot) {
-          // ---- X <- X V and J <- J V, in place, 16-row slab per warp ----
-          for (int job = warp; job < 2 * slabs; job += NW) {
-            double* M = job < slabs ? Hg : Jg;
-            const int r0 = (job < slabs ? job : job - slabs) * 16;
-            const int ra = r0 + g, rb = r0 + g + 8;
-            double accv[NC / 8][4];
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) accv[n][qq] = 0.0;
-#pragma unroll
-            for (int kq = 0; kq < 8; ++kq) {
-              const int kc = kq * 4 + t4;
-              const int gc = gcol(kc);
-              const double* col = M + static_cast<int64_t>(gc) * ellp;
-              const bool okc = gc < ell;
-              const double a0 = (okc && ra < ell) ? __ldcg(col + ra) : 0.0;
-              const double a1 = (okc && rb < ell) ? __ldcg(col + rb) : 0.0;
-#pragma unroll
-              for (int n = 0; n < NC / 8; ++n)
-                dmma_16x8x4(accv[n], a0, a1, Vs[(n * 8 + g) * VP + kc]);
-            }
-#pragma unroll
-            for (int n = 0; n < NC / 8; ++n)
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const int r = (qq & 2) ? rb : ra;
-                const int gc = gcol(n * 8 + 2 * t4 + (qq & 1));
-                if (r < ell && gc < ell) __stcg(M + r + static_cast<int64_t>(gc) * ellp, accv[n][qq]);
-              }
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && s_rot) {
-          atomicOr(fl + item, 1u);
-          atomicMax(mxs + item, s_mx);
-        }
-      }
-      grid.sync();
-    }
-    auto done = [&](int64_t i) { return __ldcg(fl + i) == 0u || __ldcg(mxs + i) == 0ull; };
-    int all = 1;
-    for (int64_t i = 0; i < batch; ++i) {
-      const bool d = done(i);
-      if (tid == 0 && !conv[i] && d && blockIdx.x == 0) sweeps_out[i] = sweep + 1;
-      all &= (conv[i] || d);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (done(i)) conv[i] = 1;
-    __syncthreads();
-    if (all) break;
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = tid; i < batch; i += blockDim.x)
-      if (!conv[i]) sweeps_out[i] = max_sweeps;
+  for (int64_t e = gtid; e < nflags; e += gstride) flags[e] = 0u;
+  for (int64_t e = gtid; e < batch; e += gstride) sweeps_out[e] = max_sweeps;
 }
 
-template <int RC>
-void launch_rs_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
+template <int RC, int MINB>
+void launch_df_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                  unsigned* flags, int64_t batch, cudaStream_t st) {
   const int nbuf = ell > RC ? 2 : 1;
-  const size_t bytes = (static_cast<size_t>(nbuf * 32) * (RC + 2) + 32 * 36 + 32 * 33) * sizeof(double) +
-                       batch * sizeof(int) + 16;
-  auto kern = jacobi_rs_kernel<RC>;
+  const size_t bytes = (static_cast<size_t>(nbuf * 32) * (RC + 2) + 32 * 36 + 32 * 33 + 3 * 16 + 8) *
+                       sizeof(double);
+  auto kern = jacobi_df_kernel<RC, MINB>;
   RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));
   int per_sm = 0;
   RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, bytes));
-  if (per_sm < 1) throw CudaError("jacobi_rs_kernel: does not fit on an SM");
+  if (per_sm < 1) throw CudaError("jacobi_df_kernel: does not fit on an SM");
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
-  const int64_t tasks = batch * (nb / 2);
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tasks, per_sm * num_sms())));
-  int ell_i = static_cast<int>(ell), ellp_i = static_cast<int>(ellp);
-  void* args[] = {&H, &J, &ell_i, &ellp_i, &nb, &batch, &max_sweeps, &flags, &sweeps};
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(256),
-                                        args, bytes, st));
-  RSVD_LAUNCH("jacobi_rs_kernel");
+  const int64_t per_phase = batch * (nb / 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(per_phase, per_sm * num_sms())));
+  const int64_t nflags = jacobi_flag_elems(batch);
+  const int64_t init_work = std::max<int64_t>(ellp * ellp * batch, nflags);
+  jacobi_df_init_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(init_work, 256), 8 * num_sms())),
+                          256, 0, st>>>(J, static_cast<int>(ellp), batch, max_sweeps, flags, nflags,
+                                        sweeps);
+  RSVD_LAUNCH("jacobi_df_init_kernel");
+  kern<<<grid, 256, bytes, st>>>(H, J, static_cast<int>(ell), static_cast<int>(ellp), nb, batch,
+                                 max_sweeps, flags, sweeps);
+  RSVD_LAUNCH("jacobi_df_kernel");
 }
 
 }  // namespace
 
-// 3 rotating "rotated" flags per item, then (8-byte aligned) 3 rotating
-// per-item "a rotation with g^2 >= 1e-18 alpha beta" flags (jacobi_cyc_kernel).
-int64_t jacobi_flag_elems(int64_t batch) { return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch; }
+// Per item: 3 rotating "rotated" flags, then (8-byte aligned) 3 rotating
+// "a rotation with g^2 >= 1e-18 alpha beta" flags.
 
-void launch_jacobi_blocked(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
-                           int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
-  const char* env = std::getenv("RSVD_JACOBI_W");
-  const int wforce = env ? std::atoi(env) : 0;
-  if (!std::getenv("RSVD_JACOBI_OLD") && !std::getenv("RSVD_JACOBI_PAIRV")) {
-    // R = rows per lane: the smallest instantiation covering l (the column
-    // registers, smem pitch and dot products all scale with R).
-    if (!std::getenv("RSVD_JACOBI_NO_GRAM")) {
-      // Gram-accelerated task steps (jacobi_gram_kernel).
-      int nbg = static_cast<int>((ell + 15) / 16);
-      nbg += nbg & 1;
-      const bool many = batch * (nbg / 2) > num_sms();
-      if (ell <= 32 * 3) return launch_gram_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_GRAM_MINB1"))
-        return launch_gram_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 5) return launch_gram_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      static const bool minb1 = std::getenv("RSVD_JACOBI_GRAM_MINB1") != nullptr;
-      if (ell <= 32 * 9 && many && !minb1)
-        return launch_gram_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 9) return launch_gram_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-      if (ell <= 32 * 18)
-        return launch_gram_t<18, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    }
-    if (ell <= 32 * 3 && !std::getenv("RSVD_JACOBI_R9"))
-      return launch_cyc_t<3, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    if (ell <= 32 * 5 && !std::getenv("RSVD_JACOBI_R9"))
-      return launch_cyc_t<5, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    // Few tasks (one or two items): one CTA per SM is enough, and the
-    // 128-register instantiations do not spill.
-    int nbt = static_cast<int>((ell + 15) / 16);
-    nbt += nbt & 1;
-    const bool few = batch * (nbt / 2) <= num_sms();
-    // Fewer tasks than SMs / 4: split every task's rows over a cluster (with
-    // more tasks the clusters would occupy most SMs, which costs more than it
-    // saves when another stream's GEMMs run beside, e.g. the host pipeline).
-    if (batch * (nbt / 2) * 4 <= num_sms() &&
-        launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
-      return;
-    if (few && ell <= 32 * 5) return launch_cyc_t<5, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    if (few && ell <= 32 * 9) return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    if (ell <= 32 * 9 && std::getenv("RSVD_JACOBI_MINB1"))
-      return launch_cyc_t<9, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    if (ell <= 32 * 9) return launch_cyc_t<9, 2>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    if (ell <= 32 * 18)
-      return launch_cyc_t<18, 1>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  }
-  if (!std::getenv("RSVD_JACOBI_OLD")) {
-    if (wforce != 8 && 32 * ell * 8 <= 100 * 1024)
-      return launch_pairv_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    return launch_pairv_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  }
-  if (wforce == 8 && 4 * 8 * ell * 8 <= 200 * 1024)
-    launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  else if (wforce == 4)
-    launch_blocked_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  else if (4 * 16 * ell * 8 <= 200 * 1024)
-    launch_blocked_t<16>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  else if (4 * 8 * ell * 8 <= 200 * 1024)
-    launch_blocked_t<8>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  else
-    launch_blocked_t<4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+int64_t jacobi_flag_elems(int64_t batch) {
+  // + per-item completion counter and converged flag, task counter (8 B) and
+  // converged-item count for jacobi_df_kernel
+  return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch + 2 * batch + 4;
 }
 
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st) {
-  set_stop_ratio_once();
-  static const bool rs_all = std::getenv("RSVD_JACOBI_RS") != nullptr;
-  if (rs_all || ell > 1600) {
-    if (ell <= 160 && ell > 64) return launch_rs_t<160>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-    return launch_rs_t<64>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
-  }
-  const int64_t bytes = 2 * ellp * ellp * static_cast<int64_t>(sizeof(double));
-  {
-    int nbt = static_cast<int>((ell + 15) / 16);
-    nbt += nbt & 1;
-    if (batch * (nbt / 2) * 4 <= num_sms() &&
-        launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
-      return;
-  }
-  // The whole-problem-in-shared-memory kernel tracks column norms across the
-  // whole run; on rank-deficient, widely graded inputs (TEBD sector blocks,
-  // tests/golden/theta_rankdef_24x21.npy) its small values drifted by ~1e-10
-  // absolute.  The block-cyclic kernels re-derive the norms from the columns
-  // at every task and are exact to rounding, so they serve every size
-  // (RSVD_JACOBI_SMEM=1 restores the old kernel).
-  if (bytes <= 220 * 1024 && std::getenv("RSVD_JACOBI_SMEM")) {
-    // Whole problem fits one CTA's shared memory: one CTA per item.
-    RSVD_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(bytes)));
-    jacobi_kernel<true><<<static_cast<unsigned>(batch), kJacThreads, bytes, st>>>(
-        H, J, static_cast<int>(ell), static_cast<int>(ellp), max_sweeps, sweeps);
-    RSVD_LAUNCH("jacobi_kernel");
+  int nbt = static_cast<int>((ell + 15) / 16);
+  nbt += nbt & 1;
+  // Fewer tasks than SMs / 4 (single matrices): split every task's rows over
+  // a cluster; with more tasks the dataflow kernel keeps all SMs busy.
+  if (batch * (nbt / 2) * 4 <= num_sms() &&
+      launch_clu(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st))
     return;
-  }
-  launch_jacobi_blocked(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  if (ell <= 144 && ell > 64) return launch_df_t<144, 4>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
+  launch_df_t<64, 3>(H, J, ell, ellp, max_sweeps, sweeps, flags, batch, st);
 }
 
 }  // namespace rsvd
