@@ -202,6 +202,63 @@ int rsvd_profile_read(rsvd_handle handle, double* ms, int64_t* calls, int n);
 const char* rsvd_profile_stage_name(int i);
 int rsvd_last_jacobi_sweeps(rsvd_handle handle);
 
+/* ---- TEBD two-site bond update (rlftn::apply_gate, mps.cpp:111-323) ----
+ * Table-driven device operations that let a caller assemble theta', measure
+ * it and apply the gauge update for a whole layer of disjoint bonds
+ * (mps.cpp:448-457) in a few launches.  The tables are HOST arrays (copied
+ * by the call); every pointer inside them is DEVICE memory.  Element (i, j)
+ * of an operand lives at base[i * rs + j * cs] (strides in elements; a
+ * complex element is two interleaved doubles).  `complex_` selects double2
+ * elements (the SymmetricMPS<Complex> instantiation, mps.cpp:551-555).
+ * Stream-ordered on the handle's stream; nothing is synchronized. */
+typedef struct {
+  const void* src;
+  int64_t rs, cs;
+  const double* row_scale; /* optional, NULL = 1: src row i scaled by row_scale[i] */
+  const double* col_scale; /* optional, NULL = 1 */
+  double coef_re, coef_im; /* coefficient (coef_im ignored for real data) */
+} rsvd_block_term;
+
+typedef struct {
+  void* dst;
+  int64_t rs, cs;
+  int64_t rows, cols;
+  int64_t term_begin, term_count; /* terms[term_begin .. +term_count) */
+} rsvd_block_job;
+
+typedef struct {
+  const void* A; int64_t a_rs, a_cs; /* M x K */
+  const void* B; int64_t b_rs, b_cs; /* K x N */
+  void* C; int64_t c_rs, c_cs;       /* M x N */
+  int64_t M, N, K;
+} rsvd_gemm_job;
+
+/* dst(i, j) = sum_t coef_t * row_scale_t[i] * col_scale_t[j] * src_t(i, j) for
+ * every job (zero when term_count = 0): the lambda-weighted site blocks
+ * (mps.cpp:130-137), gate mixing of the (m1, m2) blocks (mps.cpp:205-222),
+ * the product form's Kronecker sums x / y (mps.cpp:223-255) and the gauge
+ * update (mps.cpp:307-316).  Jobs must not write overlapping elements. */
+int rsvd_combine_blocks(rsvd_handle handle, int complex_, int64_t njobs,
+                        const rsvd_block_job* jobs, int64_t nterms, const rsvd_block_term* terms);
+/* C = A B for every job (independent shapes): theta_mu = Astack Bstack
+ * (mps.cpp:164-204), the product form's core r * y (mps.cpp:265) and the
+ * lift qfac * left (mps.cpp:301-303). */
+int rsvd_grouped_gemm(rsvd_handle handle, int complex_, int64_t njobs, const rsvd_gemm_job* jobs);
+/* out[s] (device) = sum of |x|^2 over blocks[slot_begin[s] .. slot_begin[s+1])
+ * in table order, bitwise reproducible: ||theta'||^2 per bond (mps.cpp:268).
+ * Only dst/rs/cs/rows/cols of the blocks are read. */
+int rsvd_block_sqnorms(rsvd_handle handle, int complex_, int64_t nslots, const int64_t* slot_begin,
+                       const rsvd_block_job* blocks, double* out);
+/* Thin QR, A = Q R for a batch of m x n (m >= n >= 1) matrices: the
+ * product-form factor lapack::qr(x, q, r) (mps.cpp:265 -> lapack.cpp:180-201),
+ * computed by the engine's CholeskyQR2 (shifted / completed when A is
+ * ill-conditioned or rank-deficient, so Q always has n orthonormal columns
+ * and A = Q R to working precision).  R is n x n: upper triangular when A
+ * has full numerical rank, a column-permuted triangle otherwise. */
+int rsvd_qr_f64(rsvd_handle handle, int64_t batch, const double* A, int64_t m, int64_t n,
+                int64_t lda, int64_t strideA, double* Q, int64_t ldq, int64_t strideQ, double* R,
+                int64_t ldr, int64_t strideR, int flags);
+
 /* Testing hook (not part of the reference surface): the engine's batched FP64
  * GEMM, C = op(A) B, on device pointers; trans_a selects A^T (A stored K x M). */
 int rsvd_testing_dgemm(rsvd_handle handle, int trans_a, int64_t M, int64_t N, int64_t K,

@@ -10,6 +10,8 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librsvd_b200.so")
 
@@ -89,6 +91,14 @@ SIGNATURES = {
         [_c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
          _c_i64, _c_i64, _c_i64],
     ),
+    "rsvd_combine_blocks": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_i64, _c_vp]),
+    "rsvd_grouped_gemm": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp]),
+    "rsvd_block_sqnorms": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_dp]),
+    "rsvd_qr_f64": (
+        _c_int,
+        [_c_vp, _c_i64, _c_dp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
+         _c_i64, _c_i64, _c_int],
+    ),
     "rsvd_reconstruction_error_f64": (
         _c_int,
         [_c_vp, _c_dp, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_dp, _c_dp, _c_i64, _c_i64,
@@ -103,6 +113,17 @@ for _z, _d in (("rsvd_z128", "rsvd_f64"), ("rsvd_z128_batched", "rsvd_f64_batche
                ("rsvd_reconstruction_error_z128", "rsvd_reconstruction_error_f64"),
                ("rsvd_fill_gaussian_z128", "rsvd_fill_gaussian_f64")):
     SIGNATURES[_z] = SIGNATURES[_d]
+
+# Table rows of rsvd_combine_blocks / rsvd_grouped_gemm / rsvd_block_sqnorms
+# (include/rsvd_c.h): all fields 8 bytes wide, so the packed numpy layout is
+# the C struct layout.
+BLOCK_TERM = np.dtype([("src", "u8"), ("rs", "i8"), ("cs", "i8"), ("row_scale", "u8"),
+                       ("col_scale", "u8"), ("coef_re", "f8"), ("coef_im", "f8")])
+BLOCK_JOB = np.dtype([("dst", "u8"), ("rs", "i8"), ("cs", "i8"), ("rows", "i8"), ("cols", "i8"),
+                      ("term_begin", "i8"), ("term_count", "i8")])
+GEMM_JOB = np.dtype([("A", "u8"), ("a_rs", "i8"), ("a_cs", "i8"), ("B", "u8"), ("b_rs", "i8"),
+                     ("b_cs", "i8"), ("C", "u8"), ("c_rs", "i8"), ("c_cs", "i8"), ("M", "i8"),
+                     ("N", "i8"), ("K", "i8")])
 
 _lib = None
 _lock = threading.Lock()

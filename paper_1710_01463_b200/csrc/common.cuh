@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/rsvd_c.h"
+
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -150,6 +152,15 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 int64_t jacobi_flag_elems(int64_t batch);
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st);
+
+// tebd.cu -- table-driven TEBD bond-update kernels (tables in device memory).
+void launch_combine_blocks(bool cplx, const rsvd_block_job* jobs_dev, const rsvd_block_term* terms_dev,
+                           const int64_t* start_dev, int64_t njobs, int64_t total, cudaStream_t st);
+void launch_grouped_gemm(bool cplx, const rsvd_gemm_job* jobs_dev, const int4* tiles_dev,
+                         int64_t ntiles, cudaStream_t st);
+int64_t grouped_gemm_tile(int64_t extent);  // tiles along one extent
+void launch_block_sqnorms(bool cplx, const rsvd_block_job* blocks_dev, const int64_t* begin_dev,
+                          int64_t nslots, double* out_dev, cudaStream_t st);
 
 // aux.cu
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,

@@ -196,6 +196,7 @@ struct rsvd_context {
   rsvd::Arena arena;
   rsvd::Prof prof;
   rsvd::Pinned pin;
+  rsvd::Arena tab;  // device copies of the TEBD job tables (rsvd_combine_blocks & co.)
   std::unordered_map<std::string, rsvd::GraphEntry> graphs;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::unique_ptr<rsvd::Reducer> red;  // row-sharded calls (NCCL or in-process group)
@@ -1169,6 +1170,74 @@ uint64_t mix64_host(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Thin QR through the engine's CholeskyQR2 (orth with R accumulation): the
+// product-form factor lapack::qr (mps.cpp:265 -> lapack.cpp:180-201).
+void qr_impl(rsvd_context* h, int64_t batch, const double* A, int64_t m, int64_t n, int64_t lda,
+             int64_t strideA, double* Q, int64_t ldq, int64_t strideQ, double* R, int64_t ldr,
+             int64_t strideR, int flags) {
+  check_flags(flags);
+  if (batch < 0) throw InvalidArgument("qr: batch must be >= 0");
+  if (batch == 0) return;
+  if (m <= 0 || n <= 0) throw InvalidArgument("lapack::qr: empty matrix");  // lapack.cpp:184
+  if (m < n) throw InvalidArgument("qr: need m >= n (thin QR of a tall matrix)");
+  if (!A || !Q || !R) throw InvalidArgument("qr: null pointer argument");
+  if (lda < m || ldq < m || ldr < n) throw InvalidArgument("qr: leading dimension too small");
+  if (n > kTsvdMaxDim) throw InvalidArgument("qr: n > 16384 is not supported by the GPU path");
+  const bool host = flags == RSVD_PTR_HOST;
+  RSVD_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  Shape s{m, 1, batch, 1, n, round_up(n, 32), 0};
+  Carver meas{nullptr};
+  carve(meas, s, false, true);
+  h->arena.reserve(meas.off + 256);
+  Carver cv{h->arena.base};
+  Buffers B = carve(cv, s, false, true);
+  B.prof = &h->prof;
+  B.red = nullptr;
+  if (h->pin.reserve(batch)) h->drop_graphs();
+  for (int64_t b = 0; b < batch; ++b) h->pin.seeds[b] = mix64_host(0x7172000000ull + b);  // completion
+  RSVD_CUDA(cudaMemcpyAsync(B.seeds, h->pin.seeds, sizeof(uint64_t) * batch, cudaMemcpyHostToDevice,
+                            st));
+  const int64_t lp = s.ellp;
+  const cudaMemcpyKind in = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind out = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  copy_batch(B.Y, m, m * lp, A, lda, strideA, m, n, batch, in, st);
+  if (lp > n)
+    RSVD_CUDA(cudaMemset2DAsync(B.Y + m * n, sizeof(double) * m * lp, 0, sizeof(double) * m * (lp - n),
+                                batch, st));
+  double *Yb = B.Y, *Tmp = B.Y2;
+  orth(s, B, Yb, Tmp, m, B.Rt, kCompletionTag + 0x2000, 2, true, st);
+  copy_batch(Q, ldq, strideQ, Yb, m, m * lp, m, n, batch, out, st);
+  copy_batch(R, ldr, strideR, B.Rt, lp, lp * lp, n, n, batch, out, st);
+  if (host) RSVD_CUDA(cudaStreamSynchronize(st));
+}
+
+// Copy host job tables into the handle's table arena (stream-ordered).
+template <class... P>
+void upload_tables(rsvd_context* h, cudaStream_t st, P&... parts) {
+  size_t total = 0;
+  auto sz = [&](auto& p) { total = (total + 255) & ~size_t(255); total += p.bytes; };
+  (sz(parts), ...);
+  if (total > h->tab.cap) {
+    RSVD_CUDA(cudaStreamSynchronize(st));
+    h->tab.reserve(std::max<size_t>(total, 1 << 16));
+  }
+  size_t off = 0;
+  auto put = [&](auto& p) {
+    off = (off + 255) & ~size_t(255);
+    p.dev = h->tab.base + off;
+    if (p.bytes) RSVD_CUDA(cudaMemcpyAsync(p.dev, p.host, p.bytes, cudaMemcpyHostToDevice, st));
+    off += p.bytes;
+  };
+  (put(parts), ...);
+}
+
+struct TablePart {
+  const void* host;
+  size_t bytes;
+  char* dev = nullptr;
+};
+
 #include "zpath.inc"
 
 }  // namespace
@@ -1246,6 +1315,7 @@ int rsvd_destroy(rsvd_handle h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   h->arena.release();
+  h->tab.release();
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
   return RSVD_OK;
@@ -1266,6 +1336,7 @@ int rsvd_trim(rsvd_handle h) {
     RSVD_CUDA(cudaStreamSynchronize(h->stream));
     h->drop_graphs();
     h->arena.release();
+    h->tab.release();
   });
 }
 
@@ -1515,6 +1586,86 @@ int rsvd_reconstruction_error_z128(rsvd_handle h, const double* A, int64_t m, in
                                    int flags) {
   return rsvd::guarded(h, [&] {
     rsvd::zrecon_impl(h, A, m, n, lda, U, ldu, S, Vt, ldvt, r, out, flags);
+  });
+}
+
+int rsvd_qr_f64(rsvd_handle h, int64_t batch, const double* A, int64_t m, int64_t n, int64_t lda,
+                int64_t strideA, double* Q, int64_t ldq, int64_t strideQ, double* R, int64_t ldr,
+                int64_t strideR, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::qr_impl(h, batch, A, m, n, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, flags);
+  });
+}
+
+int rsvd_combine_blocks(rsvd_handle h, int complex_, int64_t njobs, const rsvd_block_job* jobs,
+                        int64_t nterms, const rsvd_block_term* terms) {
+  return rsvd::guarded(h, [&] {
+    if (njobs < 0 || nterms < 0) throw rsvd::InvalidArgument("combine_blocks: negative table size");
+    if (njobs == 0) return;
+    if (!jobs || (nterms > 0 && !terms)) throw rsvd::InvalidArgument("combine_blocks: null table");
+    std::vector<int64_t> start(static_cast<size_t>(njobs) + 1, 0);
+    for (int64_t j = 0; j < njobs; ++j) {
+      const rsvd_block_job& jb = jobs[j];
+      if (jb.rows < 0 || jb.cols < 0 || jb.term_begin < 0 || jb.term_count < 0 ||
+          jb.term_begin + jb.term_count > nterms || (jb.rows * jb.cols > 0 && !jb.dst))
+        throw rsvd::InvalidArgument("combine_blocks: malformed job");
+      start[j + 1] = start[j] + jb.rows * jb.cols;
+    }
+    RSVD_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = h->stream;
+    rsvd::TablePart pj{jobs, sizeof(rsvd_block_job) * njobs}, pt{terms, sizeof(rsvd_block_term) * nterms},
+        ps{start.data(), sizeof(int64_t) * (njobs + 1)};
+    rsvd::upload_tables(h, st, pj, pt, ps);
+    rsvd::launch_combine_blocks(complex_ != 0, reinterpret_cast<const rsvd_block_job*>(pj.dev),
+                                reinterpret_cast<const rsvd_block_term*>(pt.dev),
+                                reinterpret_cast<const int64_t*>(ps.dev), njobs, start[njobs], st);
+  });
+}
+
+int rsvd_grouped_gemm(rsvd_handle h, int complex_, int64_t njobs, const rsvd_gemm_job* jobs) {
+  return rsvd::guarded(h, [&] {
+    if (njobs < 0) throw rsvd::InvalidArgument("grouped_gemm: negative table size");
+    if (njobs == 0) return;
+    if (!jobs) throw rsvd::InvalidArgument("grouped_gemm: null table");
+    std::vector<int4> tiles;
+    for (int64_t j = 0; j < njobs; ++j) {
+      const rsvd_gemm_job& jb = jobs[j];
+      if (jb.M < 0 || jb.N < 0 || jb.K < 0) throw rsvd::InvalidArgument("grouped_gemm: negative size");
+      if (jb.M == 0 || jb.N == 0) continue;
+      if (!jb.C || (jb.K > 0 && (!jb.A || !jb.B))) throw rsvd::InvalidArgument("grouped_gemm: null operand");
+      const int64_t tm = rsvd::grouped_gemm_tile(jb.M), tn = rsvd::grouped_gemm_tile(jb.N);
+      for (int64_t a = 0; a < tm; ++a)
+        for (int64_t b = 0; b < tn; ++b)
+          tiles.push_back(make_int4(static_cast<int>(j), static_cast<int>(a), static_cast<int>(b), 0));
+    }
+    if (tiles.empty()) return;
+    RSVD_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = h->stream;
+    rsvd::TablePart pj{jobs, sizeof(rsvd_gemm_job) * njobs}, pt{tiles.data(), sizeof(int4) * tiles.size()};
+    rsvd::upload_tables(h, st, pj, pt);
+    rsvd::launch_grouped_gemm(complex_ != 0, reinterpret_cast<const rsvd_gemm_job*>(pj.dev),
+                              reinterpret_cast<const int4*>(pt.dev), static_cast<int64_t>(tiles.size()), st);
+  });
+}
+
+int rsvd_block_sqnorms(rsvd_handle h, int complex_, int64_t nslots, const int64_t* slot_begin,
+                       const rsvd_block_job* blocks, double* out) {
+  return rsvd::guarded(h, [&] {
+    if (nslots < 0) throw rsvd::InvalidArgument("block_sqnorms: negative slot count");
+    if (nslots == 0) return;
+    if (!slot_begin || !out) throw rsvd::InvalidArgument("block_sqnorms: null argument");
+    const int64_t nb = slot_begin[nslots];
+    if (slot_begin[0] != 0 || nb < 0 || (nb > 0 && !blocks))
+      throw rsvd::InvalidArgument("block_sqnorms: malformed slot table");
+    for (int64_t s2 = 0; s2 < nslots; ++s2)
+      if (slot_begin[s2 + 1] < slot_begin[s2]) throw rsvd::InvalidArgument("block_sqnorms: malformed slot table");
+    RSVD_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = h->stream;
+    rsvd::TablePart pb{blocks, sizeof(rsvd_block_job) * nb},
+        ps{slot_begin, sizeof(int64_t) * (nslots + 1)};
+    rsvd::upload_tables(h, st, pb, ps);
+    rsvd::launch_block_sqnorms(complex_ != 0, reinterpret_cast<const rsvd_block_job*>(pb.dev),
+                               reinterpret_cast<const int64_t*>(ps.dev), nslots, out, st);
   });
 }
 

@@ -19,9 +19,13 @@ mps.cpp:448-457) with ONE batched factorization: the sector blocks of all
 bonds are grouped by shape into shared engine calls (blocks.block_factorize_many),
 which is where the GPU wins over the reference's bond-by-bond loop.
 
-The GEMMs of the assembly are plain cuBLAS calls through torch (library GEMMs
-on chi-sized blocks) and the product-form QR is cuSOLVER's; the factorization
-is the engine's.
+Every arithmetic step runs on the engine's own kernels through the C ABI:
+the lambda weighting, stacking, gate mixing, Kronecker sums, theta norms and
+gauge update are table-driven launches covering the whole layer
+(rsvd_combine_blocks / rsvd_block_sqnorms), the theta products, the
+product-form core R y and the lift Q U are one grouped GEMM launch each
+(rsvd_grouped_gemm), and the product-form QR is the engine's CholeskyQR2
+(rsvd_qr_f64, batched per shape).  torch only allocates device memory.
 """
 from __future__ import annotations
 
@@ -31,6 +35,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+from . import _lib
 from ._lib import InvalidArgument
 from .blocks import (BlockDiagMatrix, BlockMethod, SectorRankRequest, block_factorize,
                      block_factorize_many)
@@ -165,9 +170,79 @@ class _BondPlan:
     gauge update (sector offsets, the assembled theta', QR factors)."""
 
 
-def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
-    """mps.cpp:111-266: the two-site matrix theta' as a 2-sector block matrix."""
+def _colmajor(rows: int, cols: int, like):
+    """Uninitialised device matrix in column-major storage (the engine's
+    layout; the table kernels write it row-fastest, i.e. coalesced)."""
     torch = _torch()
+    return torch.empty((cols, rows), dtype=like.dtype, device=like.device).t()
+
+
+class _Tables:
+    """Host job tables of one launch of the engine's table-driven bond-update
+    kernels (rsvd_combine_blocks / rsvd_grouped_gemm / rsvd_block_sqnorms)."""
+
+    def __init__(self):
+        self.jobs, self.terms, self.gemms = [], [], []
+        self.keep = []  # tensors whose storage the tables point to
+
+    @staticmethod
+    def _view(t):
+        return t.data_ptr(), t.stride(0), t.stride(1)
+
+    def combine(self, dst, terms):
+        """dst = sum_t coef * diag(row_scale) src diag(col_scale); terms =
+        [(src, row_scale or None, col_scale or None, coef)]."""
+        rows, cols = dst.shape
+        if rows == 0 or cols == 0:
+            return
+        begin = len(self.terms)
+        for src, rsc, csc, coef in terms:
+            if coef == 0:
+                continue
+            sp, srs, scs = self._view(src)
+            c = complex(coef)
+            self.terms.append((sp, srs, scs, rsc.data_ptr() if rsc is not None else 0,
+                               csc.data_ptr() if csc is not None else 0, c.real, c.imag))
+            self.keep.append(src)
+        dp, drs, dcs = self._view(dst)
+        self.jobs.append((dp, drs, dcs, rows, cols, begin, len(self.terms) - begin))
+        self.keep.append(dst)
+
+    def gemm(self, c, a, b):
+        if c.shape[0] == 0 or c.shape[1] == 0:
+            return
+        if a.shape[1] == 0:
+            self.combine(c, [])
+            return
+        ap, ars, acs = self._view(a)
+        bp, brs, bcs = self._view(b)
+        cp, crs, ccs = self._view(c)
+        self.gemms.append((ap, ars, acs, bp, brs, bcs, cp, crs, ccs, c.shape[0], c.shape[1],
+                           a.shape[1]))
+        self.keep += [a, b, c]
+
+    def run_combine(self, h, cplx: bool):
+        lib = _lib.load()
+        if not self.jobs:
+            return
+        jobs = np.array(self.jobs, dtype=_lib.BLOCK_JOB)
+        terms = np.array(self.terms, dtype=_lib.BLOCK_TERM) if self.terms else \
+            np.zeros(1, dtype=_lib.BLOCK_TERM)
+        _lib.raise_for(lib.rsvd_combine_blocks(h.raw, int(cplx), len(jobs), jobs.ctypes.data,
+                                               len(self.terms), terms.ctypes.data), h.raw)
+        self.jobs, self.terms = [], []
+
+    def run_gemm(self, h, cplx: bool):
+        lib = _lib.load()
+        if not self.gemms:
+            return
+        g = np.array(self.gemms, dtype=_lib.GEMM_JOB)
+        _lib.raise_for(lib.rsvd_grouped_gemm(h.raw, int(cplx), len(g), g.ctypes.data), h.raw)
+        self.gemms = []
+
+
+def _bond_sizes(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
+    """Validation and sector bookkeeping of apply_gate (mps.cpp:114-156)."""
     n_sites = psi.length()
     if bond < 0 or bond + 1 >= n_sites:
         raise InvalidArgument("apply_gate: bond out of range")
@@ -175,17 +250,12 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
     p = psi.site.charges
     if gate.block is None or gate.block.shape != (d * d, d * d):
         raise InvalidArgument("apply_gate: gate does not match the physical dimension")
+    if gate.form != GateForm.block and not gate.terms:
+        raise InvalidArgument("apply_gate: product-form gate has no terms")
     lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
-    g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
-    dev = lam_l[0].device
-    # theta carries the Gammas' scalar type (real or complex MPS); gates are real.
-    f64 = dict(dtype=g1[0][0].dtype, device=dev)
     nl = [lam_l[0].numel(), lam_l[1].numel()]
     nm = [lam_m[0].numel(), lam_m[1].numel()]
     nr = [lam_r[0].numel(), lam_r[1].numel()]
-    alm = [[lam_l[a][:, None] * g1[m][a] * lam_m[a ^ p[m]][None, :] for a in (0, 1)]
-           for m in range(d)]
-    br = [[g2[m][a] * lam_r[a ^ p[m]][None, :] for a in (0, 1)] for m in range(d)]
     row_off = [[0] * d, [0] * d]
     col_off = [[0] * d, [0] * d]
     rows, cols = [0, 0], [0, 0]
@@ -196,197 +266,264 @@ def _assemble(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
             col_off[s][m] = cols[s]
             cols[s] += nr[s ^ p[m]]
     plan = _BondPlan()
-    plan.bond, plan.nl, plan.nm, plan.nr = bond, nl, nm, nr
+    plan.bond, plan.gate, plan.nl, plan.nm, plan.nr = bond, gate, nl, nm, nr
     plan.row_off, plan.col_off, plan.rows, plan.cols = row_off, col_off, rows, cols
-    plan.lifted = False
     plan.qfac = [None, None]
-    thetap = [None, None]
-    if gate.form == GateForm.block:
-        theta = []
-        for s in (0, 1):
-            if nm[s] == 0:
-                theta.append(torch.zeros(rows[s], cols[s], **f64))
-                continue
-            astack = torch.cat([alm[m][s ^ p[m]] for m in range(d)], dim=0)
-            bstack = torch.cat([br[m][s] for m in range(d)], dim=1)
-            theta.append(astack @ bstack)
-        pairs = [[], []]
-        for m1 in range(d):
-            for m2 in range(d):
-                pairs[p[m1] ^ p[m2]].append((m1, m2))
-        # theta' columns = theta columns * gt, gt(i, j) = gate(pair_j, pair_i);
-        # built once per (gate, scalar type, device) and cached on the gate.
-        cache = gate.__dict__.setdefault("_device_blocks", {})
-        ckey = (f64["dtype"], str(dev), tuple(p))
-        gt = cache.get(ckey)
-        if gt is None:
-            gblock = torch.as_tensor(gate.block, **f64)
-            gt = []
-            for q in (0, 1):
-                idx = torch.tensor([m1 * d + m2 for (m1, m2) in pairs[q]], device=dev,
-                                   dtype=torch.long)
-                gt.append(gblock[idx][:, idx].t().contiguous() if len(pairs[q]) else None)
-            cache[ckey] = gt
-        thetap = [torch.zeros(rows[sp], cols[sp], **f64) for sp in (0, 1)]
-        for a in (0, 1):
-            for c in (0, 1):
-                q = a ^ c
-                npair = len(pairs[q])
-                blk = nl[a] * nr[c]
-                if blk == 0 or npair == 0:
-                    continue
-                # the (m1, m2) blocks of this (a, c) stacked, mixed by the gate in
-                # one product: block'_j = sum_i gt(i, j) block_i
-                tin = torch.stack([
-                    theta[a ^ p[m1]][row_off[a ^ p[m1]][m1]:row_off[a ^ p[m1]][m1] + nl[a],
-                                     col_off[a ^ p[m1]][m2]:col_off[a ^ p[m1]][m2] + nr[c]]
-                    for (m1, m2) in pairs[q]])
-                tout = (gt[q].t() @ tin.reshape(npair, blk)).reshape(npair, nl[a], nr[c])
-                for i, (m1, m2) in enumerate(pairs[q]):
-                    sp = a ^ p[m1]
-                    thetap[sp][row_off[sp][m1]:row_off[sp][m1] + nl[a],
-                               col_off[sp][m2]:col_off[sp][m2] + nr[c]] = tout[i]
-    else:
-        if not gate.terms:
-            raise InvalidArgument("apply_gate: product-form gate has no terms")
-        nk = len(gate.terms)
-        for sp in (0, 1):
-            koff = []
-            fused = 0
-            for t in gate.terms:
-                koff.append(fused)
-                fused += nm[sp ^ t.charge]
-            x = torch.zeros(rows[sp], fused, **f64)
-            y = torch.zeros(fused, cols[sp], **f64)
-            for k in range(nk):
-                t = gate.terms[k]
-                w = nm[sp ^ t.charge]
-                if w == 0:
-                    continue
-                for m1p in range(d):
-                    a = sp ^ p[m1p]
-                    if nl[a] == 0:
-                        continue
-                    xb = x[row_off[sp][m1p]:row_off[sp][m1p] + nl[a], koff[k]:koff[k] + w]
-                    for m1 in range(d):
-                        if t.left[m1p, m1] != 0.0:
-                            xb += float(t.left[m1p, m1]) * alm[m1][a]
-                for m2p in range(d):
-                    c = sp ^ p[m2p]
-                    if nr[c] == 0:
-                        continue
-                    yb = y[koff[k]:koff[k] + w, col_off[sp][m2p]:col_off[sp][m2p] + nr[c]]
-                    for m2 in range(d):
-                        if t.right[m2p, m2] != 0.0:
-                            yb += float(t.right[m2p, m2]) * br[m2][sp ^ t.charge]
-            if rows[sp] == 0 or fused == 0:
-                plan.qfac[sp] = torch.zeros(rows[sp], 0, **f64)
-                thetap[sp] = torch.zeros(0, cols[sp], **f64)
-            else:
-                qf, r = torch.linalg.qr(x, mode="reduced")
-                plan.qfac[sp] = qf
-                thetap[sp] = r @ y
-        plan.lifted = True
-    plan.thetap = thetap
-    # kept on the device: the callers read all bonds' norms in one transfer
-    plan.total_sq_t = sum((tp.abs() ** 2).sum() if tp.is_complex() else (tp * tp).sum()
-                          for tp in thetap)
+    plan.thetap = [None, None]
     return plan
 
 
-def _read_norms(plans) -> None:
-    """One device -> host transfer for every plan's ||theta'||^2 (mps.cpp:268)."""
+def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
+    """mps.cpp:111-268 for every bond of `plans`: theta' of each bond as a
+    2-sector block matrix, in four engine launches for the whole layer --
+    (1) the lambda-weighted site blocks written into the stacked operands
+    (block form) or the Kronecker sums x, y (product form); (2) the grouped
+    products theta_mu = Astack_mu Bstack_mu; (3) the gate mixing of the
+    (m1, m2) blocks into theta'; (4) ||theta'||^2 per bond -- plus, for the
+    product form, one batched CholeskyQR2 per shape (x = Q R) and the grouped
+    core products R y.  No library GEMM or factorization is called."""
     torch = _torch()
-    vals = torch.stack([torch.as_tensor(p.total_sq_t, dtype=torch.float64,
-                                        device=p.thetap[0].device).reshape(())
-                        for p in plans]).cpu().tolist()
-    for p, v in zip(plans, vals):
-        p.total_sq = float(v)
-        if not (p.total_sq > 0.0):
+    h = handle or _lib.default_handle()
+    d = psi.site.dim
+    p = psi.site.charges
+    ref = psi.gammas[0][0][0]
+    cplx = ref.is_complex()
+    dev = ref.device
+    st1, st2, st3 = _Tables(), _Tables(), _Tables()
+    qr_groups = {}  # (rows, fused) -> [(plan, sp, x, y)]
+    lifted_y = []   # (plan, sp, x, y) multiplied directly (no QR)
+    for pl in plans:
+        bond = pl.bond
+        lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
+        g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
+        nl, nm, nr, rows, cols = pl.nl, pl.nm, pl.nr, pl.rows, pl.cols
+        gate = pl.gate
+        if gate.form == GateForm.block:
+            pl.lifted = False
+            theta = [None, None]
+            for mu in (0, 1):
+                if nm[mu] == 0:
+                    continue
+                A = _colmajor(rows[mu], nm[mu], ref)
+                B = _colmajor(nm[mu], cols[mu], ref)
+                for m in range(d):
+                    a = mu ^ p[m]
+                    st1.combine(A[pl.row_off[mu][m]:pl.row_off[mu][m] + nl[a]],
+                                [(g1[m][a], lam_l[a], lam_m[mu], 1.0)])
+                    c = mu ^ p[m]
+                    st1.combine(B[:, pl.col_off[mu][m]:pl.col_off[mu][m] + nr[c]],
+                                [(g2[m][mu], None, lam_r[c], 1.0)])
+                theta[mu] = _colmajor(rows[mu], cols[mu], ref)
+                st2.gemm(theta[mu], A, B)
+            gb = gate.block
+            thetap = [_colmajor(rows[sp], cols[sp], ref) for sp in (0, 1)]
+            for sp in (0, 1):
+                for m1 in range(d):
+                    a = sp ^ p[m1]
+                    for m2 in range(d):
+                        c = sp ^ p[m2]
+                        q = p[m1] ^ p[m2]
+                        out = thetap[sp][pl.row_off[sp][m1]:pl.row_off[sp][m1] + nl[a],
+                                         pl.col_off[sp][m2]:pl.col_off[sp][m2] + nr[c]]
+                        terms = []
+                        for i1 in range(d):
+                            for i2 in range(d):
+                                if p[i1] ^ p[i2] != q:
+                                    continue
+                                coef = float(gb[m1 * d + m2, i1 * d + i2])
+                                mu = a ^ p[i1]
+                                if coef == 0.0 or theta[mu] is None:
+                                    continue
+                                src = theta[mu][pl.row_off[mu][i1]:pl.row_off[mu][i1] + nl[a],
+                                                pl.col_off[mu][i2]:pl.col_off[mu][i2] + nr[c]]
+                                terms.append((src, None, None, coef))
+                        st3.combine(out, terms)
+            pl.thetap = thetap
+        else:
+            pl.lifted = True
+            for sp in (0, 1):
+                koff, fused = [], 0
+                for t in gate.terms:
+                    koff.append(fused)
+                    fused += nm[sp ^ t.charge]
+                x = _colmajor(rows[sp], fused, ref)
+                y = _colmajor(fused, cols[sp], ref)
+                for k, t in enumerate(gate.terms):
+                    mu = sp ^ t.charge
+                    w = nm[mu]
+                    if w == 0:
+                        continue
+                    for m1p in range(d):
+                        a = sp ^ p[m1p]
+                        st1.combine(x[pl.row_off[sp][m1p]:pl.row_off[sp][m1p] + nl[a],
+                                      koff[k]:koff[k] + w],
+                                    [(g1[m1][a], lam_l[a], lam_m[mu], float(t.left[m1p, m1]))
+                                     for m1 in range(d) if t.left[m1p, m1] != 0.0])
+                    for m2p in range(d):
+                        c = sp ^ p[m2p]
+                        st1.combine(y[koff[k]:koff[k] + w,
+                                      pl.col_off[sp][m2p]:pl.col_off[sp][m2p] + nr[c]],
+                                    [(g2[m2][mu], None, lam_r[c], float(t.right[m2p, m2]))
+                                     for m2 in range(d) if t.right[m2p, m2] != 0.0])
+                if rows[sp] == 0 or fused == 0:  # mps.cpp:256-258
+                    pl.qfac[sp] = torch.zeros(rows[sp], 0, dtype=ref.dtype, device=dev)
+                    pl.thetap[sp] = torch.zeros(0, cols[sp], dtype=ref.dtype, device=dev)
+                    continue
+                if not cplx and rows[sp] > fused:
+                    qr_groups.setdefault((rows[sp], fused), []).append((pl, sp, x, y))
+                else:
+                    # no reduction possible (or complex state): theta' = x y with
+                    # qfac = I -- the same factorization, exactly, as Q (R y)
+                    pl.qfac[sp] = None
+                    pl.thetap[sp] = _colmajor(rows[sp], cols[sp], ref)
+                    lifted_y.append((pl, sp, x, y))
+    # (1) weighted site blocks / Kronecker sums
+    with _lib.on_torch_stream(h):
+        st1.run_combine(h, cplx)
+        # product form: batched CholeskyQR2 per (rows, fused) shape, then R y
+        for (m, n), members in qr_groups.items():
+            nb = len(members)
+            X = torch.empty((nb, n, m), dtype=ref.dtype, device=dev)
+            Xv = X.transpose(1, 2)
+            for i, (_, _, x, _) in enumerate(members):
+                Xv[i].copy_(x)
+            Qb = torch.empty((nb, n, m), dtype=ref.dtype, device=dev).transpose(1, 2)
+            Rb = torch.empty((nb, n, n), dtype=ref.dtype, device=dev).transpose(1, 2)
+            lib = _lib.load()
+            _lib.raise_for(lib.rsvd_qr_f64(h.raw, nb, Xv.data_ptr(), m, n, m, m * n,
+                                           Qb.data_ptr(), m, m * n, Rb.data_ptr(), n, n * n,
+                                           _lib.PTR_DEVICE), h.raw)
+            for i, (pl, sp, _, y) in enumerate(members):
+                pl.qfac[sp] = Qb[i]
+                pl.thetap[sp] = _colmajor(n, pl.cols[sp], ref)
+                st2.gemm(pl.thetap[sp], Rb[i], y)
+        for pl, sp, x, y in lifted_y:
+            st2.gemm(pl.thetap[sp], x, y)
+        # (2) theta_mu = Astack Bstack, R y, x y
+        st2.run_gemm(h, cplx)
+        # (3) gate mixing
+        st3.run_combine(h, cplx)
+        # (4) ||theta'||^2 per bond, one device -> host transfer for the layer
+        blocks, begin = [], [0]
+        for pl in plans:
+            for tp in pl.thetap:
+                if tp is not None and tp.numel():
+                    dp_, rs_, cs_ = _Tables._view(tp)
+                    blocks.append((dp_, rs_, cs_, tp.shape[0], tp.shape[1], 0, 0))
+            begin.append(len(blocks))
+        out = torch.empty(len(plans), dtype=torch.float64, device=dev)
+        bt = np.array(blocks if blocks else [(0, 0, 0, 0, 0, 0, 0)], dtype=_lib.BLOCK_JOB)
+        bg = np.array(begin, dtype=np.int64)
+        lib = _lib.load()
+        _lib.raise_for(lib.rsvd_block_sqnorms(h.raw, int(cplx), len(plans), bg.ctypes.data,
+                                              bt.ctypes.data, out.data_ptr()), h.raw)
+        vals = out.cpu().tolist()
+    # keep every table operand alive until the stream has consumed it
+    for pl, v in zip(plans, vals):
+        pl.total_sq = float(v)
+        pl._keep = (st1.keep, st2.keep, st3.keep)
+        if not (pl.total_sq > 0.0):
             raise RuntimeError("apply_gate: evolved wavefunction vanished")
 
 
-def _finish(psi: SymmetricMPS, plan: _BondPlan, f, seconds: float) -> GateStats:
-    """mps.cpp:276-321: trim, renormalise, lift, gauge update."""
+def _finish_layer(psi: SymmetricMPS, plans, fs, seconds, handle) -> List[GateStats]:
+    """mps.cpp:276-321 for every bond: trim, renormalise, lift (one grouped
+    product for the layer), gauge update (one table launch for the layer)."""
     torch = _torch()
-    factors = f.factors
-    # host copies of the kept values (blocks._select), no per-sector transfer
-    sh = [getattr(x, "sigma_host", None) for x in factors]
-    sh = [v if v is not None else (x.sigma.cpu().numpy() if hasattr(x.sigma, "cpu")
-                                   else np.asarray(x.sigma)) for v, x in zip(sh, factors)]
-    kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
-    if kept_sq > 0.0:
-        cut = LAMBDA_TRIM * np.sqrt(kept_sq)
-        trimmed = False
-        for i, fac in enumerate(factors):
-            sv = sh[i]
-            r = len(sv)
-            while r > 0 and sv[r - 1] < cut:
-                r -= 1
-            if r == len(sv):
-                continue
-            fac.left = fac.left[:, :r]
-            fac.sigma = fac.sigma[:r]
-            fac.right_adj = fac.right_adj[:r, :]
-            sh[i] = sv[:r]
-            fac.sigma_host = sh[i]
-            trimmed = True
-        if trimmed:
-            kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
-    if not (kept_sq > 0.0):
-        raise RuntimeError("apply_gate: truncation removed the whole state")
-    if plan.lifted:
-        for sp in (0, 1):
-            factors[sp].left = plan.qfac[sp] @ factors[sp].left
-    bond = plan.bond
+    h = handle or _lib.default_handle()
     d = psi.site.dim
     p = psi.site.charges
-    lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
-    inv_norm = 1.0 / np.sqrt(kept_sq)
-    for s in (0, 1):
-        lam_m[s] = factors[s].sigma * inv_norm
-    linv = [_floored_inverse(lam_l[0]), _floored_inverse(lam_l[1])]
-    rinv = [_floored_inverse(lam_r[0]), _floored_inverse(lam_r[1])]
-    g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
-    nl, nr = plan.nl, plan.nr
-    for m in range(d):
-        for a in (0, 1):
-            s = a ^ p[m]
-            lrows = factors[s].left[plan.row_off[s][m]:plan.row_off[s][m] + nl[a], :]
-            g1[m][a] = linv[a][:, None] * lrows
-            rcols = factors[a].right_adj[:, plan.col_off[a][m]:plan.col_off[a][m] + nr[a ^ p[m]]]
-            g2[m][a] = rcols * rinv[a ^ p[m]][None, :]
-    out = GateStats()
-    out.discarded_weight = max(0.0, 1.0 - kept_sq / plan.total_sq)
-    out.factorize_seconds = seconds
-    out.mid_rank = int(lam_m[0].numel() + lam_m[1].numel())
-    return out
+    lift, gauge = _Tables(), _Tables()
+    stats, cplx = [], False
+    for plan, f in zip(plans, fs):
+        factors = f.factors
+        sh = [getattr(x, "sigma_host", None) for x in factors]
+        sh = [v if v is not None else (x.sigma.cpu().numpy() if hasattr(x.sigma, "cpu")
+                                       else np.asarray(x.sigma)) for v, x in zip(sh, factors)]
+        kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
+        if kept_sq > 0.0:
+            cut = LAMBDA_TRIM * np.sqrt(kept_sq)
+            trimmed = False
+            for i, fac in enumerate(factors):
+                sv = sh[i]
+                r = len(sv)
+                while r > 0 and sv[r - 1] < cut:
+                    r -= 1
+                if r == len(sv):
+                    continue
+                fac.left = fac.left[:, :r]
+                fac.sigma = fac.sigma[:r]
+                fac.right_adj = fac.right_adj[:r, :]
+                sh[i] = sv[:r]
+                fac.sigma_host = sh[i]
+                trimmed = True
+            if trimmed:
+                kept_sq = float(sum(float(np.dot(v, v)) for v in sh))
+        if not (kept_sq > 0.0):
+            raise RuntimeError("apply_gate: truncation removed the whole state")
+        if plan.lifted:
+            for sp in (0, 1):
+                q = plan.qfac[sp]
+                if q is None:
+                    continue  # qfac = I: theta' was x y itself
+                left = factors[sp].left
+                lifted = _colmajor(q.shape[0], left.shape[1], left)
+                lift.gemm(lifted, q, left)
+                factors[sp].left = lifted
+        plan.kept_sq = kept_sq
+        cplx = cplx or factors[0].left.is_complex()
+    with _lib.on_torch_stream(h):
+        lift.run_gemm(h, cplx)
+    for plan, f in zip(plans, fs):
+        factors = f.factors
+        bond = plan.bond
+        lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
+        inv_norm = 1.0 / np.sqrt(plan.kept_sq)
+        for s in (0, 1):
+            lam_m[s] = factors[s].sigma * inv_norm
+        linv = [_floored_inverse(lam_l[0]), _floored_inverse(lam_l[1])]
+        rinv = [_floored_inverse(lam_r[0]), _floored_inverse(lam_r[1])]
+        g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
+        nl, nr = plan.nl, plan.nr
+        for m in range(d):
+            for a in (0, 1):
+                s = a ^ p[m]
+                left = factors[s].left
+                lrows = left[plan.row_off[s][m]:plan.row_off[s][m] + nl[a], :]
+                g1[m][a] = _colmajor(nl[a], left.shape[1], left)
+                gauge.combine(g1[m][a], [(lrows, linv[a], None, 1.0)])
+                ra = factors[a].right_adj
+                c = a ^ p[m]
+                rcols = ra[:, plan.col_off[a][m]:plan.col_off[a][m] + nr[c]]
+                g2[m][a] = _colmajor(ra.shape[0], nr[c], ra)
+                gauge.combine(g2[m][a], [(rcols, None, rinv[c], 1.0)])
+        out = GateStats()
+        out.discarded_weight = max(0.0, 1.0 - plan.kept_sq / plan.total_sq)
+        out.factorize_seconds = seconds / max(len(plans), 1)
+        out.mid_rank = int(lam_m[0].numel() + lam_m[1].numel())
+        stats.append(out)
+        plan._keep_gauge = (linv, rinv)
+    with _lib.on_torch_stream(h):
+        gauge.run_combine(h, cplx)
+    # the table operands (factors, inverse lambdas) must outlive the launch
+    torch.cuda.current_stream().synchronize()
+    return stats
 
 
 def apply_gate(psi: SymmetricMPS, bond: int, gate: TwoSiteGate, chi: int, method: BlockMethod,
                request: Optional[SectorRankRequest] = None, handle=None) -> GateStats:
     """rlftn::apply_gate (mps.cpp:111-323) on device-resident tensors."""
-    if chi < 1:
-        raise InvalidArgument("apply_gate: chi must be >= 1")
-    request = request or SectorRankRequest()
-    plan = _assemble(psi, bond, gate)
-    _read_norms([plan])
-    torch = _torch()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    f = block_factorize(BlockDiagMatrix([0, 1], plan.thetap), chi, request, method, handle)
-    torch.cuda.synchronize()
-    return _finish(psi, plan, f, time.perf_counter() - t0)
+    return apply_gate_layer(psi, [bond], [gate], chi, method, request, handle)[0]
 
 
 def apply_gate_layer(psi: SymmetricMPS, bonds: Sequence[int], gates: Sequence[TwoSiteGate],
                      chi: int, method: BlockMethod, request: Optional[SectorRankRequest] = None,
                      handle=None) -> List[GateStats]:
     """One TEBD layer: gates on disjoint bonds (mps.cpp:448-457), all theta'
-    assembled first, then ONE batched block factorization for all bonds
-    (equal-shape sector blocks of different bonds share engine calls), then
-    the per-bond gauge updates.  Same result as applying the gates one by
-    one."""
+    assembled first (engine table kernels, _assemble_layer), then ONE batched
+    block factorization for all bonds (equal-shape sector blocks of different
+    bonds share engine calls), then the per-bond trims and one gauge-update
+    launch.  Same result as applying the gates one by one."""
     if chi < 1:
         raise InvalidArgument("apply_gate: chi must be >= 1")
     if len(bonds) != len(gates):
@@ -397,8 +534,8 @@ def apply_gate_layer(psi: SymmetricMPS, bonds: Sequence[int], gates: Sequence[Tw
             raise InvalidArgument("apply_gate_layer: bonds must be disjoint")
         used.add(b)
     request = request or SectorRankRequest()
-    plans = [_assemble(psi, b, g) for b, g in zip(bonds, gates)]
-    _read_norms(plans)
+    plans = [_bond_sizes(psi, b, g) for b, g in zip(bonds, gates)]
+    _assemble_layer(psi, plans, handle)
     torch = _torch()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -406,7 +543,7 @@ def apply_gate_layer(psi: SymmetricMPS, bonds: Sequence[int], gates: Sequence[Tw
                               method, handle)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    return [_finish(psi, pl, f, dt / max(len(plans), 1)) for pl, f in zip(plans, fs)]
+    return _finish_layer(psi, plans, fs, dt, handle)
 
 
 def canonicalize(psi: SymmetricMPS, handle=None) -> None:
