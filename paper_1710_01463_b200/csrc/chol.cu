@@ -699,15 +699,6 @@ __global__ void __launch_bounds__(kCholThreads)
 //      G_right -= R_J,right^T R_J,right,
 // all products on DMMA (mma.sync m16n8k4 f64), operands from L2, with grid-wide
 // barriers between the phases.  Same outputs and breakdown rule as uchol_kernel.
-__device__ unsigned long long g_gc_trace[128];  // RSVD_GCHOL_TRACE: phase timestamps
-__device__ __forceinline__ void gc_mark(int& n) {
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n < 128) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_gc_trace[n] = t;
-  }
-  ++n;
-}
 
 constexpr int kGcThreads = 256;  // 8 warps: <= 255 registers, so the diagonal factor stays in registers
 constexpr int kGcWarps = kGcThreads / 32;
@@ -846,8 +837,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
   const int64_t nw = static_cast<int64_t>(gridDim.x) * kGcWarps;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  int nmark = 0;
-  gc_mark(nmark);
   // scratch per item: [0, 1024) D_J; [sq, 2 sq) Acc (strictly upper blocks);
   // [2 sq - 2] go flag, [2 sq - 1] pivot floor (a diagonal block of Acc).
   auto go_of = [&](int64_t b) -> double* { return gc_item_scratch(a, b) + 2 * sq - 2; };
@@ -874,7 +863,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
     go_of(b)[0] = go ? 1.0 : 0.0;
   }
   grid.sync();
-  gc_mark(nmark);
   // Per item (flag read once), 16-byte stores: sq is a multiple of 1024.
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     if (go_of(b)[0] == 0.0) continue;
@@ -888,7 +876,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
     }
   }
   grid.sync();
-  gc_mark(nmark);
   for (int64_t b = gw; b < batch; b += nw) {  // shift, pivot floor, initial rank
     if (go_of(b)[0] == 0.0) continue;
     double* W = a.G + b * sq;
@@ -915,7 +902,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
     }
   }
   grid.sync();
-  gc_mark(nmark);
 
   const bool diag_warp = warp < kGcDiagWarps;
   double* Rd = sm + (diag_warp ? warp : 0) * 2 * 32 * kInvPitch;
@@ -927,7 +913,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
     for (int64_t b = d0; b < batch; b += dstep)
       if (go_of(b)[0] != 0.0 && a.rank[b] > 0) gc_factor_diag(a, b, 0, Rd, Dt, lane);
   grid.sync();
-  gc_mark(nmark);
 
   const int64_t pw = static_cast<int64_t>(blockIdx.x) * (kGcWarps - kGcDiagWarps) + (warp - kGcDiagWarps);
   const int64_t npw = static_cast<int64_t>(gridDim.x) * (kGcWarps - kGcDiagWarps);
@@ -975,7 +960,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
       }
     }
     grid.sync();
-  gc_mark(nmark);
     if (nr == 0) break;
     // ---- Phase C (+ lookahead factor of block J+1) -----------------------
     if (diag_warp) {
@@ -1051,7 +1035,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
       }
     }
     grid.sync();
-  gc_mark(nmark);
   }
   // Epilogue: Rfull (rows < r, upper), identity permutation.
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
@@ -1095,9 +1078,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   // ill-conditioned fallback (usually no item active) use the one-CTA-per-item
   // kernel: cooperative launches replayed from a CUDA graph cost ~1 ms each
   // even when every CTA exits at once (C2: 44.6 -> 24.3 ms per step).
-  static const bool gchol_all = std::getenv("RSVD_GCHOL_ALL") != nullptr;
-  if (!pivot && (!opts || gchol_all) && !std::getenv("RSVD_UCHOL") &&
-      !std::getenv("RSVD_PIVOT_ALWAYS")) {
+  if (!pivot && !opts) {
     GcholArgs ga{G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp),
                  tau, batch, opts ? *opts : CholOpts{}};
     const int bytes = kGcDiagWarps * 2 * 32 * kInvPitch * 8;
@@ -1121,13 +1102,10 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     const int64_t nbk = ceil_div(ellp, 32);
     const int64_t want = ceil_div(batch * nbk * (nbk + 1) / 2, kGcWarps);
     int g = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(want, 32)));
-    static const int genv = std::getenv("RSVD_GCHOL_GRID") ? std::atoi(std::getenv("RSVD_GCHOL_GRID")) : 0;
-    if (genv > 0) g = std::min(grid, genv);
     // Small work: one cluster of 8-16 CTAs with cluster barriers.
-    static const bool no_clu = std::getenv("RSVD_NO_GCHOL_CLUSTER") != nullptr;
     // 16-CTA (non-portable) clusters available on this device: 0 unknown, 1 no, 2 yes
     static std::atomic<int> clu_dev[kMaxDevices];
-    if (!no_clu && want <= 16 && genv == 0) {
+    if (want <= 16) {
       int clu_ok = clu_dev[current_device()].load(std::memory_order_acquire) - 1;
       if (clu_ok < 0) {
         clu_ok = 0;
@@ -1177,17 +1155,9 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel<false>), dim3(g),
                                           dim3(kGcThreads), args, bytes, st));
     RSVD_LAUNCH("gchol_kernel");
-    if (std::getenv("RSVD_GCHOL_TRACE")) {
-      unsigned long long tr[128] = {};
-      RSVD_CUDA(cudaStreamSynchronize(st));
-      RSVD_CUDA(cudaMemcpyFromSymbol(tr, g_gc_trace, sizeof(tr)));
-      std::fprintf(stderr, "gchol ell=%lld batch=%lld:", (long long)ell, (long long)batch);
-      for (int i = 1; i < 128 && tr[i] > tr[0]; ++i) std::fprintf(stderr, " %.1f", (tr[i] - tr[i - 1]) * 1e-3);
-      std::fprintf(stderr, "\n");
-    }
     return;
   }
-  if (!pivot && (opts || !std::getenv("RSVD_PIVOT_ALWAYS"))) {
+  if (!pivot) {
     const CholOpts o = opts ? *opts : CholOpts{};
     const int64_t ub = big * 8 + 2 * 32 * kInvPitch * 8 + 64;
     RSVD_CUDA(cudaFuncSetAttribute(uchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

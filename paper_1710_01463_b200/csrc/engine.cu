@@ -334,20 +334,6 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   return B;
 }
 
-bool pivot_pass2() {
-  static const bool v = std::getenv("RSVD_PIVOT_PASS2") != nullptr;
-  return v;
-}
-bool pivot_all() {
-  static const bool v = std::getenv("RSVD_PIVOT_ALL") != nullptr;
-  return v;
-}
-
-bool full_orth() {
-  static const bool v = std::getenv("RSVD_FULL_ORTH") != nullptr;
-  return v;
-}
-
 // CholeskyQR of Y (rows x ellp per item): `passes` = 2 is CholeskyQR2 (the
 // result is orthonormal to working precision); 1 pass gives Q1 = (Y P) R11^-1,
 // an exact-span, well-conditioned basis (kappa(Q1)^2 - 1 = O(u kappa(Y)^2) with
@@ -380,7 +366,6 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
-  if (full_orth()) passes = std::max(passes, 2);
   auto gram = [&](const MatRef& in, const int* mask) {
     Scope sc(P, kStGram, st);
     GemmOpts sym;
@@ -415,9 +400,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
                                   cudaMemcpyDeviceToDevice, st));
       // Unpivoted everywhere (grid-parallel gchol; breakdown -> numerical
       // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
-      // Jacobi) measured no fewer sweeps: RSVD_BT_PIVOT=1 / RSVD_PIVOT_ALL=1.
-      static const bool bt_pivot = std::getenv("RSVD_BT_PIVOT") != nullptr;
-      pivot = ((pass == 0 && ((Rt && bt_pivot) || pivot_all())) || pivot_pass2()) && !cplx;
+      // Jacobi) measured no fewer sweeps (r01 and r02, C2 8 / C4 7 sweeps).
       launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
       if (pass == 0) {  // shifted retry of the items that stopped short of full rank
         CholOpts o;
@@ -489,8 +472,7 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
   // the first product Y = A Omega (|Y| tracks sigma_max(A)) and applied to
   // every A-pass output; sigma and the discarded weight are scaled back at the
   // end.  Row-sharded calls are not scaled (a per-rank max would disagree).
-  static const bool no_scale = std::getenv("RSVD_NO_SCALE") != nullptr;
-  const bool do_scale = !B.red && !no_scale;
+  const bool do_scale = !B.red;
   auto nn = [&] {
     Scope sc(P, kStApassNN, st);
     dgemm(false, s.m, lp, s.n, A, MatRef{B.X, s.n, s.n * lp}, MatRef{B.Y, s.m, s.m * lp}, b,
@@ -544,8 +526,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     Scope sc(P, kStApassTN, st);
     dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
-    static const bool no_scale = std::getenv("RSVD_NO_SCALE") != nullptr;
-    if (!B.red && !no_scale) {
+    if (!B.red) {
       if (!B.scaled) {  // tsvd (Q = I): choose the scale from B^T = A_e^T
         launch_choose_scale(X, s.n, s.ell, B.scale, b, st);
         B.scaled = true;
@@ -662,19 +643,9 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                          double* S, int64_t strideS, double* Vt, int64_t ldvt, int64_t strideVt) {
   const int64_t batch = full.batch, m = full.m, n = full.n, k = full.k;
   // Equal chunk sizes (a shorter last chunk measured no better on C4: the
-  // GPU, not the tail, is the limit).  RSVD_HOST_SPLIT="a,b,c" overrides.
+  // GPU, not the tail, is the limit).
   std::vector<int64_t> sizes;
-  if (const char* e = std::getenv("RSVD_HOST_SPLIT")) {
-    int64_t tot = 0;
-    for (const char* p = e; *p && tot < batch;) {
-      const int64_t v = std::max<int64_t>(1, std::atoll(p));
-      sizes.push_back(std::min(v, batch - tot));
-      tot += sizes.back();
-      while (*p && *p != ',') ++p;
-      if (*p == ',') ++p;
-    }
-    if (tot < batch) sizes.push_back(batch - tot);
-  } else {
+  {
     const int64_t cb = ceil_div(batch, nchunks);
     for (int64_t tot = 0; tot < batch; tot += cb) sizes.push_back(std::min(cb, batch - tot));
   }
@@ -705,11 +676,7 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   Carver cv{h->arena.base};
   layout(cv);
   cudaStream_t cs[4] = {st, h->s_c2, h->s_c3, h->s_c4};
-  static const int nstreams = [] {
-    const char* e = std::getenv("RSVD_PIPE_STREAMS");
-    const int v = e ? std::atoi(e) : 3;
-    return v < 2 ? 2 : (v > 4 ? 4 : v);
-  }();
+  constexpr int nstreams = 3;  // 3 compute streams measured best on C4 (2: 295, 3: 319 trunc/s)
   // Order the side streams after whatever the caller queued on its stream.
   RSVD_CUDA(cudaEventRecord(h->ev_in, st));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_in, 0));
@@ -717,30 +684,17 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c2, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c3, h->ev_in, 0));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_c4, h->ev_in, 0));
-  // RSVD_PIPE_TRACE: event timeline of the chunks (ms from the call start).
-  static const bool trace = std::getenv("RSVD_PIPE_TRACE") != nullptr;
-  std::vector<cudaEvent_t> tev;
-  auto mark = [&](cudaStream_t q) {
-    if (!trace) return;
-    cudaEvent_t e;
-    RSVD_CUDA(cudaEventCreate(&e));
-    RSVD_CUDA(cudaEventRecord(e, q));
-    tev.push_back(e);
-  };
-  mark(st);
   // All H2D copies first (one stream, back to back), then the compute chain.
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t b0 = off[c], nb = sizes[c];
     copy_batch(Ah[c], m, m * n, A + b0 * strideA, lda, strideA, m, n, nb, cudaMemcpyHostToDevice,
                h->s_in);
     RSVD_CUDA(cudaEventRecord(h->ev_slot_in[c], h->s_in));
-    mark(h->s_in);
   }
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t b0 = off[c], nb = sizes[c];
     cudaStream_t q = cs[c % nstreams];
     RSVD_CUDA(cudaStreamWaitEvent(q, h->ev_slot_in[c], 0));
-    mark(q);
     Shape s = sc;
     s.batch = nb;
     Buffers Bq = B[c];
@@ -757,7 +711,6 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                               cudaMemcpyDeviceToHost, q));
     RSVD_CUDA(cudaMemcpyAsync(h->pin.dbls + b0, B[c].dw, sizeof(double) * nb,
                               cudaMemcpyDeviceToHost, q));
-    mark(q);
     RSVD_CUDA(cudaEventRecord(h->ev_slot_comp[c], q));
     RSVD_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_slot_comp[c], 0));
     copy_batch(U + b0 * strideU, ldu, strideU, Uh[c], m, m * k, m, k, nb, cudaMemcpyDeviceToHost,
@@ -766,7 +719,6 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                cudaMemcpyDeviceToHost, h->s_out);
     copy_batch(S + b0 * strideS, k, strideS, Sh[c], k, k, k, 1, nb, cudaMemcpyDeviceToHost,
                h->s_out);
-    mark(h->s_out);
   }
   RSVD_CUDA(cudaStreamSynchronize(h->s_out));
   RSVD_CUDA(cudaStreamSynchronize(st));
@@ -774,17 +726,6 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   RSVD_CUDA(cudaStreamSynchronize(h->s_c3));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c4));
   RSVD_CUDA(cudaStreamSynchronize(h->s_in));
-  if (trace && !tev.empty()) {
-    // h2d ends per chunk, then per chunk: compute start, compute end, d2h end
-    std::fprintf(stderr, "pipe:");
-    for (size_t i = 1; i < tev.size(); ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, tev[0], tev[i]);
-      std::fprintf(stderr, " %.1f", ms);
-    }
-    std::fprintf(stderr, "\n");
-    for (auto e : tev) cudaEventDestroy(e);
-  }
 }
 
 // Replay a captured CUDA graph of `enqueue` (one host launch per call), keyed

@@ -323,7 +323,6 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   int64_t splits = 1;
   if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / 256));
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
-  if (const char* env = std::getenv("RSVD_MAX_SPLITS")) splits = std::min<int64_t>(splits, std::atoi(env));
   int64_t kps = round_up(ceil_div(K, splits), kBK);
   splits = ceil_div(K, kps);
   c.splits = static_cast<int>(std::max<int64_t>(1, splits));
@@ -331,31 +330,8 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   return c;
 }
 
-int tuning_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("RSVD_GEMM_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <bool TRANS_A, int VEC>
 void dispatch(const Choice& c, const GemmArgs& a, cudaStream_t st) {
-  // Tuning variants for the large aligned A-pass shapes (RSVD_GEMM_VARIANT).
-  if constexpr (VEC == 2) {
-    const int v = tuning_variant();
-    if (v != 0 && c.bm == 128 && c.bn == 96 && a.splits == 1) {
-      switch (v) {
-        case 1: return launch_cfg<128, 96, 16, 4, 2, 3, TRANS_A, VEC, 2>(a, st);
-        case 2: return launch_cfg<128, 96, 32, 4, 2, 2, TRANS_A, VEC, 1>(a, st);
-        case 3: return launch_cfg<128, 144, 16, 4, 3, 3, TRANS_A, VEC, 1>(a, st);
-        case 4: return launch_cfg<128, 96, 16, 4, 2, 4, TRANS_A, VEC, 1>(a, st);
-        case 5: return launch_cfg<64, 96, 16, 2, 2, 3, TRANS_A, VEC, 3>(a, st);
-        case 6: return launch_cfg<192, 96, 16, 6, 2, 3, TRANS_A, VEC, 1>(a, st);
-        default: break;
-      }
-    }
-  }
   if (c.bm == 128 && c.bn == 96)  // 128 registers: two CTAs per SM (profiles/r01_gemm_tune.txt)
     launch_cfg<128, 96, kBK, 4, 2, kStages, TRANS_A, VEC, 2>(a, st);
   else if (c.bm == 128 && c.bn == 64)
@@ -379,15 +355,9 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // tiles -> 3 splits = 1.95 waves instead of 2 splits = 1.3 waves), each split
 // keeping >= 256 of K.
 int64_t sq96_splits(int64_t M, int64_t K, int64_t batch) {
-  static const bool old = std::getenv("RSVD_GRAM_SPLIT_OLD") != nullptr;
   const int64_t t = M / 96, tiles = t * (t + 1) / 2 * batch;
   const int64_t slots = 2 * num_sms();
   const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / 256));
-  if (old) {
-    int64_t sp = 1;
-    if (tiles < slots) sp = std::min<int64_t>(ceil_div(slots, tiles), smax);
-    return std::max<int64_t>(1, std::min<int64_t>(sp, 64));
-  }
   if (tiles >= 4 * slots) return 1;
   int64_t best = 1;
   double best_eff = -1.0;
@@ -428,7 +398,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool tma_operands = aligned16(A.base) && aligned16(B.base) && A.ld % 2 == 0 &&
                             B.ld % 2 == 0 && (batch == 1 || (A.stride % 2 == 0 && B.stride % 2 == 0));
   const bool sq96 = opt.c_upper && trans_a && M == N && M % 96 == 0 && !opt.colmapA &&
-                    tma_operands && !std::getenv("RSVD_NO_GRAM96");
+                    tma_operands;
   if (sq96) {
     int64_t splits = sq96_splits(M, K, batch);
     int64_t kps = round_up(ceil_div(K, splits), kBK);
@@ -462,10 +432,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool vec2 = aligned16(A.base) && aligned16(B.base) && (A.ld % 2 == 0) &&
                     (B.ld % 2 == 0) && (A.stride % 2 == 0) && (B.stride % 2 == 0) &&
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
-  static const bool no_tma_apply = std::getenv("RSVD_NO_TMA_APPLY") != nullptr;
-  static const bool no_tma_mask = std::getenv("RSVD_NO_TMA_MASK") != nullptr;
-  const bool tma_ok = !(no_tma_apply && a.b_upper) && !(no_tma_mask && opt.item_mask);
-  const bool tma_done = tma_ok && !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
+  const bool tma_done = !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
                         dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
                                   c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st,
                                   sq96 ? 1 : 0);

@@ -18,7 +18,6 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -250,15 +249,8 @@ bool make_map(CUtensorMap* map, const double* base, int rank, const cuuint64_t* 
 
 constexpr int kBM = 128, kBN = 96, kWM = 4, kWN = 2;
 
-int tma_stages() {
-  static const int s = [] {
-    const char* e = std::getenv("RSVD_TMA_STAGES");
-    // 3 stages (86 KB) keep two CTAs per SM; measured faster than 4 (one CTA).
-    const int v = e ? std::atoi(e) : 3;
-    return (v == 3 || v == 4) ? v : 3;
-  }();
-  return s;
-}
+// 3 stages (86 KB) keep two CTAs per SM; measured faster than 4 (one CTA).
+constexpr int kTmaStages = 3;
 
 template <int STAGES, bool TRANS_A, int BM = kBM, int BN = kBN, int WM = kWM, int WN = kWN>
 void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& a, cudaStream_t st) {
@@ -277,18 +269,12 @@ void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& a, cuda
 
 }  // namespace
 
-bool tma_gemm_enabled() {
-  static const bool v = std::getenv("RSVD_NO_TMA") == nullptr;
-  return v;
-}
-
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
                const int* item_mask, bool b_upper, cudaStream_t st, int tile) {
   // tile 0: 128 x 96 (8 warps as 4 x 2); tile 1: 96 x 96 (2 x 4 warps) for the
   // symmetric Gram of a 96-multiple l_p (no partial 128-row tiles).
   const int bm = tile == 1 ? 96 : kBM, bn = tile == 1 ? 96 : kBN;
-  if (!tma_gemm_enabled()) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al16(A.base) || !al16(B.base)) return false;
   if (A.ld % 2 || B.ld % 2 || A.stride % 2 || B.stride % 2) return false;
@@ -321,19 +307,13 @@ bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef
   }
   TmaArgs a{M, N, K, C, ldc, strideC, batch, splits, kps, c_upper ? 1 : 0, b_upper ? 1 : 0,
             item_mask};
-  const int stg = tma_stages();
   if (tile == 1) {
     if (trans_a) launch<3, true, 96, 96, 2, 4>(ma, mb, a, st);
     else launch<3, false, 96, 96, 2, 4>(ma, mb, a, st);
     return true;
   }
-  if (trans_a) {
-    if (stg == 3) launch<3, true>(ma, mb, a, st);
-    else launch<4, true>(ma, mb, a, st);
-  } else {
-    if (stg == 3) launch<3, false>(ma, mb, a, st);
-    else launch<4, false>(ma, mb, a, st);
-  }
+  if (trans_a) launch<kTmaStages, true>(ma, mb, a, st);
+  else launch<kTmaStages, false>(ma, mb, a, st);
   return true;
 }
 

@@ -1000,14 +1000,12 @@ bool launch_zgram_t(const double* src, int64_t src_ld, int64_t src_stride, int s
 bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, int src_mode,
                          double* H, double* J, int64_t ell, int64_t lp, int max_sweeps,
                          int* sweeps, unsigned* flags, int64_t batch, cudaStream_t st) {
-  static const bool off = std::getenv("RSVD_NO_ZGRAM") != nullptr;
-  if (off || !flags || ell < 2) return false;
+  if (!flags || ell < 2) return false;
   int nb = static_cast<int>((ell + 15) / 16);
   nb += nb & 1;
   const int64_t tasks = batch * (nb / 2);
   const int R = static_cast<int>((ell + 31) / 32);
-  static const bool no_clu = std::getenv("RSVD_NO_ZGRAM_CLUSTER") != nullptr;
-  if (!no_clu && tasks * 4 <= num_sms() && R >= 2) {
+  if (tasks * 4 <= num_sms() && R >= 2) {
     // Few tasks: split each task's rows over a cluster of S <= 6 CTAs.
     const int smax = static_cast<int>(std::min<int64_t>(6, num_sms() / std::max<int64_t>(tasks, 1)));
     if (smax >= 2) {
@@ -1063,7 +1061,6 @@ void launch_zjacobi(const double* src, int64_t src_ld, int64_t src_stride, int s
   const int64_t pairs = (ell + 1) / 2;
   int S = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, num_sms() / batch)));
   S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, ceil_div(pairs, 16))));
-  if (const char* e = std::getenv("RSVD_ZJACOBI_CLUSTER")) S = std::max(1, std::min(8, std::atoi(e)));
   const int e = static_cast<int>(ell);
   const int rpl = static_cast<int>(ceil_div(ell, 32));
   if (rpl <= 1)

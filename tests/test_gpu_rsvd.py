@@ -320,3 +320,38 @@ def test_batched_out_buffers_reused(cuda, oracle_mod):
     assert torch.equal(dev2.sigma.cpu(), ref.sigma)
     with pytest.raises(InvalidArgument, match="out= buffers"):
         rsvd_batched(host[:2], p, seeds[:2], out=first)
+
+
+_NO_GRAPH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1710_01463_b200 import RsvdParams, rsvd_batched
+rng = np.random.default_rng(5)
+a = torch.from_numpy(rng.standard_normal((6, 96, 80))).to("cuda:0").transpose(1, 2)
+p = RsvdParams(10, 20, 2, 0)
+for _ in range(3):  # the graph path captures on the second call and replays on the third
+    f = rsvd_batched(a, p, list(range(6)))
+torch.cuda.synchronize()
+np.save({out!r}, np.concatenate([f.sigma.cpu().numpy().ravel(), f.left.cpu().numpy().ravel()]))
+"""
+
+
+def test_graph_replay_equals_direct_launches(cuda, tmp_path):
+    """RSVD_NO_GRAPH=1 (direct launches, no CUDA-graph capture) gives bitwise
+    the same factors as the captured-and-replayed path."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_graph in ("0", "1"):
+        out = str(tmp_path / f"f{env_graph}.npy")
+        env = dict(os.environ)
+        env.pop("RSVD_NO_GRAPH", None)
+        if env_graph == "1":
+            env["RSVD_NO_GRAPH"] = "1"
+        subprocess.run([sys.executable, "-c", _NO_GRAPH_SCRIPT.format(root=root, out=out)],
+                       check=True, env=env, timeout=300)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
