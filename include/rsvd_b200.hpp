@@ -14,6 +14,7 @@
 // a.cols().
 #pragma once
 
+#include <algorithm>
 #include <complex>
 #include <cstdint>
 #include <stdexcept>
@@ -196,6 +197,111 @@ double reconstruction_error(const Matrix<Scalar>& a, const TruncatedFactorizatio
              r ? detail::dp(f.left.data()) : nullptr, a.rows(), r ? f.sigma.data() : nullptr,
              r ? detail::dp(f.right_adj.data()) : nullptr, r > 0 ? r : 1, r, &out,
              RSVD_PTR_HOST));
+  return out;
+}
+
+// ---- blocks.hpp: block-diagonal (symmetry-sector) factorization ---------
+using SectorId = int;  // blocks.hpp:14
+
+// blocks.hpp:16-27
+template <class Scalar>
+struct BlockDiagMatrix {
+  std::vector<SectorId> charges;
+  std::vector<Matrix<Scalar>> blocks;
+  Index sector_count() const { return static_cast<Index>(blocks.size()); }
+};
+
+enum class RankPolicy { per_sector_estimate, maximal };  // blocks.hpp:29-32
+
+struct SectorRankRequest {  // blocks.hpp:36-41
+  RankPolicy policy = RankPolicy::per_sector_estimate;
+  Index chi = 0;
+  Index slack = -1;
+};
+
+struct BlockMethod {  // blocks.hpp:49-63
+  enum class Kind { tsvd, rsvd };
+  Kind kind = Kind::tsvd;
+  RsvdParams rsvd;
+  Index rsvd_min_dim = 32;
+  static BlockMethod deterministic() { return {}; }
+  static BlockMethod randomized(int power = 4, std::uint64_t seed = 0) {
+    BlockMethod m;
+    m.kind = Kind::rsvd;
+    m.rsvd.power = power;
+    m.rsvd.seed = seed;
+    return m;
+  }
+};
+
+template <class Scalar>
+struct BlockFactorization {  // blocks.hpp:68-81
+  std::vector<SectorId> charges;
+  std::vector<TruncatedFactorization<Scalar>> factors;
+  double discarded_weight = 0.0;
+  bool discarded_exact = true;
+  Index total_rank() const {
+    Index r = 0;
+    for (const auto& f : factors) r += f.rank();
+    return r;
+  }
+};
+
+// rlftn::block_factorize<double> (blocks.cpp:38-118) through
+// rsvd_block_factorize_f64: equal-shape sectors share one batched engine call,
+// then the reference's global top-chi selection and tie-breaks.
+inline BlockFactorization<double> block_factorize(const BlockDiagMatrix<double>& a, Index chi,
+                                                  const SectorRankRequest& request,
+                                                  const BlockMethod& method,
+                                                  Engine& e = default_engine()) {
+  if (a.blocks.size() != a.charges.size())  // blocks.cpp:42 (the ABI takes one count)
+    throw std::invalid_argument("block_factorize: charges/blocks size mismatch");
+  const Index ns = static_cast<Index>(a.blocks.size());
+  std::vector<std::int64_t> ch(a.charges.begin(), a.charges.end()), rows(ns), cols(ns), ld(ns),
+      ldu(ns), ldvt(ns), rank(ns);
+  std::vector<const double*> in(ns);
+  std::vector<Matrix<double>> u(ns), vt(ns);
+  std::vector<std::vector<double>> s(ns);
+  std::vector<double*> up(ns), sp(ns), vp(ns);
+  std::vector<double> sdw(ns);
+  for (Index i = 0; i < ns; ++i) {
+    const Matrix<double>& b = a.blocks[static_cast<size_t>(i)];
+    rows[i] = b.rows(), cols[i] = b.cols(), ld[i] = b.rows() > 0 ? b.rows() : 1;
+    in[i] = b.data();
+    const Index cap = std::max<Index>(1, std::min(std::min(b.rows(), b.cols()), chi));
+    u[i] = Matrix<double>(b.rows() > 0 ? b.rows() : 1, cap);
+    vt[i] = Matrix<double>(cap, b.cols() > 0 ? b.cols() : 1);
+    s[i].assign(static_cast<size_t>(cap), 0.0);
+    up[i] = u[i].data(), sp[i] = s[i].data(), vp[i] = vt[i].data();
+    ldu[i] = u[i].rows(), ldvt[i] = cap;
+  }
+  double tot = 0.0;
+  int exact = 1;
+  e.check(rsvd_block_factorize_f64(
+      e.raw(), ns, ch.data(), in.data(), rows.data(), cols.data(), ld.data(), chi,
+      request.policy == RankPolicy::maximal ? 1 : 0, request.slack,
+      method.kind == BlockMethod::Kind::rsvd ? 1 : 0, method.rsvd.oversample, method.rsvd.power,
+      method.rsvd.seed, method.rsvd_min_dim, up.data(), ldu.data(), sp.data(), vp.data(),
+      ldvt.data(), rank.data(), sdw.data(), &tot, &exact, RSVD_PTR_HOST));
+  BlockFactorization<double> out;
+  out.charges = a.charges;
+  out.discarded_weight = tot;
+  out.discarded_exact = exact != 0;
+  for (Index i = 0; i < ns; ++i) {
+    Matrix<double> left(rows[i], rank[i]), right(rank[i], cols[i]);
+    for (Index j = 0; j < rank[i]; ++j)
+      for (Index r = 0; r < rows[i]; ++r) left(r, j) = u[i](r, j);
+    for (Index j = 0; j < cols[i]; ++j)
+      for (Index r = 0; r < rank[i]; ++r) right(r, j) = vt[i](r, j);
+    TruncatedFactorization<double> f;
+    f.left = std::move(left);
+    f.sigma.assign(s[i].begin(), s[i].begin() + rank[i]);
+    f.right_adj = std::move(right);
+    f.discarded_weight = sdw[i];
+    f.discarded_exact = method.kind == BlockMethod::Kind::tsvd ||
+                        std::min(rows[i], cols[i]) < method.rsvd_min_dim;
+    out.factors.push_back(std::move(f));
+  }
   return out;
 }
 

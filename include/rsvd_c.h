@@ -202,6 +202,28 @@ int rsvd_profile_read(rsvd_handle handle, double* ms, int64_t* calls, int n);
 const char* rsvd_profile_stage_name(int i);
 int rsvd_last_jacobi_sweeps(rsvd_handle handle);
 
+/* rlftn::block_factorize<double>(a, chi, request, method) (blocks.cpp:38-118):
+ * truncated factorization of a block-diagonal matrix with one dense block per
+ * symmetry sector.  Sector s: charge charges[s] (unique), block rows[s] x
+ * cols[s] at blocks[s] (column-major, leading dimension ld[s]).
+ * Request (SectorRankRequest, blocks.hpp:31-35): policy 0 per_sector_estimate
+ * (slack < 0 -> default), 1 maximal.  Method (BlockMethod, blocks.hpp:49-63):
+ * kind 0 tsvd / 1 rsvd with oversample (l), power, seed (per-sector seeds
+ * derive_seed(seed, charge), blocks.cpp:78) and rsvd_min_dim.  Equal-shape
+ * sectors of a route are factorized by one batched engine call.
+ * Outputs per sector: out_rank[s] = kept rank after the global top-chi
+ * selection; U[s] (ldu[s] >= rows[s]) and Vt[s] (ldvt[s] >= its rank) need
+ * room for min(rows[s], cols[s], chi) columns / rows, S[s] for as many values;
+ * sector_dw[s] and *total_dw the discarded weights, *exact = discarded_exact.
+ * Errors: the reference's messages (blocks.cpp:42-46, 19-24). */
+int rsvd_block_factorize_f64(rsvd_handle handle, int64_t nsectors, const int64_t* charges,
+                             const double* const* blocks, const int64_t* rows, const int64_t* cols,
+                             const int64_t* ld, int64_t chi, int policy, int64_t slack, int kind,
+                             int64_t oversample, int power, uint64_t seed, int64_t rsvd_min_dim,
+                             double* const* U, const int64_t* ldu, double* const* S,
+                             double* const* Vt, const int64_t* ldvt, int64_t* out_rank,
+                             double* sector_dw, double* total_dw, int* exact, int flags);
+
 /* ---- TEBD two-site bond update (rlftn::apply_gate, mps.cpp:111-323) ----
  * Table-driven device operations that let a caller assemble theta', measure
  * it and apply the gauge update for a whole layer of disjoint bonds

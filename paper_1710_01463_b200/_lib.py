@@ -91,6 +91,12 @@ SIGNATURES = {
         [_c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
          _c_i64, _c_i64, _c_i64],
     ),
+    "rsvd_block_factorize_f64": (
+        _c_int,
+        [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_int, _c_i64, _c_int, _c_i64,
+         _c_int, _c_u64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_dp, _c_vp,
+         _c_int],
+    ),
     "rsvd_combine_blocks": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_i64, _c_vp]),
     "rsvd_grouped_gemm": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp]),
     "rsvd_block_sqnorms": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_dp]),

@@ -24,6 +24,8 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/rsvd_c.h"
@@ -197,6 +199,7 @@ struct rsvd_context {
   rsvd::Prof prof;
   rsvd::Pinned pin;
   rsvd::Arena tab;  // device copies of the TEBD job tables (rsvd_combine_blocks & co.)
+  rsvd::Arena blk;  // sector staging of rsvd_block_factorize_f64 (outside the engine arena)
   std::unordered_map<std::string, rsvd::GraphEntry> graphs;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::unique_ptr<rsvd::Reducer> red;  // row-sharded calls (NCCL or in-process group)
@@ -1180,6 +1183,7 @@ struct TablePart {
 };
 
 #include "zpath.inc"
+#include "blocks.inc"
 
 }  // namespace
 }  // namespace rsvd
@@ -1257,6 +1261,7 @@ int rsvd_destroy(rsvd_handle h) {
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   h->arena.release();
   h->tab.release();
+  h->blk.release();
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
   return RSVD_OK;
@@ -1278,6 +1283,7 @@ int rsvd_trim(rsvd_handle h) {
     h->drop_graphs();
     h->arena.release();
     h->tab.release();
+    h->blk.release();
   });
 }
 
@@ -1527,6 +1533,20 @@ int rsvd_reconstruction_error_z128(rsvd_handle h, const double* A, int64_t m, in
                                    int flags) {
   return rsvd::guarded(h, [&] {
     rsvd::zrecon_impl(h, A, m, n, lda, U, ldu, S, Vt, ldvt, r, out, flags);
+  });
+}
+
+int rsvd_block_factorize_f64(rsvd_handle h, int64_t nsectors, const int64_t* charges,
+                             const double* const* blocks, const int64_t* rows, const int64_t* cols,
+                             const int64_t* ld, int64_t chi, int policy, int64_t slack, int kind,
+                             int64_t oversample, int power, uint64_t seed, int64_t rsvd_min_dim,
+                             double* const* U, const int64_t* ldu, double* const* S,
+                             double* const* Vt, const int64_t* ldvt, int64_t* out_rank,
+                             double* sector_dw, double* total_dw, int* exact, int flags) {
+  return rsvd::guarded(h, [&] {
+    rsvd::block_factorize_impl(h, nsectors, charges, blocks, rows, cols, ld, chi, policy, slack,
+                               kind, oversample, power, seed, rsvd_min_dim, U, ldu, S, Vt, ldvt,
+                               out_rank, sector_dw, total_dw, exact, flags);
   });
 }
 

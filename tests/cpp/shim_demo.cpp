@@ -59,6 +59,46 @@ int main() {
   if (std::abs(zerr * zerr - ztail) > 1e-10 * ztail) { std::printf("FAIL complex err\n"); return 1; }
   const auto q = randomized_range(z, 8, 1, 5);
   if (q.rows() != 24 || q.cols() != 8) { std::printf("FAIL range shape\n"); return 1; }
+  // block_factorize (test_blocks.cpp:82-95, 114-140): global selection of the
+  // chi largest values across sectors, exact ties to the lower charge.
+  BlockDiagMatrix<double> bd;
+  bd.charges = {7, 3};
+  bd.blocks.resize(2, MatrixR(2, 2));
+  for (auto& b : bd.blocks) b(0, 0) = 2.0, b(1, 1) = 1.0;
+  SectorRankRequest req;
+  req.policy = RankPolicy::maximal;
+  const auto bf = block_factorize(bd, 3, req, BlockMethod::deterministic());
+  if (bf.factors[0].rank() != 1 || bf.factors[1].rank() != 2 ||
+      std::abs(bf.discarded_weight - 1.0) > 1e-14 || !bf.discarded_exact) {
+    std::printf("FAIL block_factorize ties\n");
+    return 1;
+  }
+  // randomized sectors of equal shape share one batched engine call
+  BlockDiagMatrix<double> big;
+  big.charges = {0, 1, 2};
+  for (int s = 0; s < 3; ++s) {
+    MatrixR b(48, 40);
+    for (Index i = 0; i < 40; ++i) b(i, i) = std::pow(0.7, static_cast<double>(i)) * (1.0 + s);
+    big.blocks.push_back(b);
+  }
+  const auto rb = block_factorize(big, 12, SectorRankRequest{}, BlockMethod::randomized(2, 9));
+  if (rb.total_rank() != 12 || rb.discarded_exact || std::abs(rb.factors[2].sigma[0] - 3.0) > 1e-12) {
+    std::printf("FAIL block_factorize rsvd (rank %lld)\n", (long long)rb.total_rank());
+    return 1;
+  }
+  try {
+    BlockDiagMatrix<double> dup;
+    dup.charges = {1, 1};
+    dup.blocks.resize(2, MatrixR(2, 2));
+    (void)block_factorize(dup, 2, SectorRankRequest{}, BlockMethod::deterministic());
+    std::printf("FAIL no throw (duplicate)\n");
+    return 1;
+  } catch (const std::invalid_argument& ex) {
+    if (std::string(ex.what()) != "block_factorize: duplicate sector charge") {
+      std::printf("FAIL msg %s\n", ex.what());
+      return 1;
+    }
+  }
   std::printf("shim ok: sigma0=%.3f rank=%lld err^2=%.6e complex err^2=%.6e\n", f.sigma[0],
               (long long)f.rank(), err * err, zerr * zerr);
   return 0;
