@@ -814,29 +814,54 @@ __device__ void gc_factor_diag(const GcholArgs& a, int64_t b, int J, double* Rd,
 // barriers become cluster barriers (hardware, ~1 us cheaper each); used for
 // single matrices / small batches whose widest step fits 16 CTAs.  Cross-CTA
 // data is read with ld.global.cg in both modes.
-template <bool CLU>
-__global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a) {
+// MODE 0: persistent cooperative grid over all items; MODE 1: the same as
+// one thread-block cluster; MODE 2: one independent CTA per item (blockIdx.x
+// = item, block barriers only, no co-residency needed) -- for small l_p,
+// where an item's whole factorization is a few dozen warp tasks and the
+// grid / cluster barriers would dominate.
+template <int MODE>
+__global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_in) {
   namespace cg = cooperative_groups;
   struct Sync {
     __device__ void sync() {
-      if constexpr (CLU)
+      if constexpr (MODE == 1)
         cg::this_cluster().sync();
+      else if constexpr (MODE == 2)
+        __syncthreads();
       else
         cg::this_grid().sync();
     }
   } grid;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_any;
+  GcholArgs a = a_in;
+  int cta = blockIdx.x, ncta = gridDim.x;
+  if constexpr (MODE == 2) {  // this CTA's item as a batch of one
+    const int64_t b0 = blockIdx.x, q = static_cast<int64_t>(a.ellp) * a.ellp;
+    a.G += b0 * q;
+    a.T += b0 * q;
+    if (a.Rfull) a.Rfull += b0 * q;
+    a.scratch += b0 * 2 * q;
+    a.rank += b0;
+    if (a.perm) a.perm += b0 * a.ellp;
+    if (a.o.gate_rank) a.o.gate_rank += b0;
+    if (a.o.mask) a.o.mask += b0;
+    if (a.o.ill_out) a.o.ill_out += b0;
+    if (a.o.Gsrc) a.o.Gsrc += b0 * q;
+    a.batch = 1;
+    cta = 0;
+    ncta = 1;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int ell = a.ell, ld = a.ellp;
   const int64_t sq = static_cast<int64_t>(ld) * ld;
   const int64_t batch = a.batch;
   const int nb = (ell + 31) / 32;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGcWarps + warp;
-  const int64_t nw = static_cast<int64_t>(gridDim.x) * kGcWarps;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gw = static_cast<int64_t>(cta) * kGcWarps + warp;
+  const int64_t nw = static_cast<int64_t>(ncta) * kGcWarps;
+  const int64_t gtid = static_cast<int64_t>(cta) * blockDim.x + tid;
+  const int64_t gstride = static_cast<int64_t>(ncta) * blockDim.x;
   // scratch per item: [0, 1024) D_J; [sq, 2 sq) Acc (strictly upper blocks);
   // [2 sq - 2] go flag, [2 sq - 1] pivot floor (a diagonal block of Acc).
   auto go_of = [&](int64_t b) -> double* { return gc_item_scratch(a, b) + 2 * sq - 2; };
@@ -864,7 +889,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
   }
   grid.sync();
   // Per item (flag read once), 16-byte stores: sq is a multiple of 1024.
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+  for (int64_t b = cta; b < batch; b += ncta) {
     if (go_of(b)[0] == 0.0) continue;
     double2* t2 = reinterpret_cast<double2*>(a.T + b * sq);
     const double2 z = make_double2(0.0, 0.0);
@@ -907,15 +932,15 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
   double* Rd = sm + (diag_warp ? warp : 0) * 2 * 32 * kInvPitch;
   double* Dt = Rd + 32 * kInvPitch;
   // Items whose diagonal factorizations this warp owns.
-  const int64_t d0 = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(warp) * gridDim.x;
-  const int64_t dstep = static_cast<int64_t>(gridDim.x) * kGcDiagWarps;
+  const int64_t d0 = static_cast<int64_t>(cta) + static_cast<int64_t>(warp) * ncta;
+  const int64_t dstep = static_cast<int64_t>(ncta) * kGcDiagWarps;
   if (diag_warp)
     for (int64_t b = d0; b < batch; b += dstep)
       if (go_of(b)[0] != 0.0 && a.rank[b] > 0) gc_factor_diag(a, b, 0, Rd, Dt, lane);
   grid.sync();
 
-  const int64_t pw = static_cast<int64_t>(blockIdx.x) * (kGcWarps - kGcDiagWarps) + (warp - kGcDiagWarps);
-  const int64_t npw = static_cast<int64_t>(gridDim.x) * (kGcWarps - kGcDiagWarps);
+  const int64_t pw = static_cast<int64_t>(cta) * (kGcWarps - kGcDiagWarps) + (warp - kGcDiagWarps);
+  const int64_t npw = static_cast<int64_t>(ncta) * (kGcWarps - kGcDiagWarps);
   for (int J = 0; J < nb; ++J) {
     const int o = J * 32;
     const int nr = nb - J - 1;  // blocks right of J
@@ -1037,7 +1062,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a)
     grid.sync();
   }
   // Epilogue: Rfull (rows < r, upper), identity permutation.
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+  for (int64_t b = cta; b < batch; b += ncta) {
     if (go_of(b)[0] == 0.0) continue;
     if (a.perm)
       for (int i = tid; i < ld; i += blockDim.x) a.perm[b * ld + i] = i;
@@ -1086,19 +1111,32 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
     static std::atomic<int> grid_dev[kMaxDevices];
     int grid = grid_dev[current_device()].load(std::memory_order_acquire);
     if (grid == 0) {
-      RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bytes));
       int per_sm = 0;
-      RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel<false>, kGcThreads,
+      RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gchol_kernel<0>, kGcThreads,
                                                               bytes));
       if (per_sm < 1) throw CudaError("gchol_kernel: does not fit on an SM");
       grid = per_sm * num_sms();
       grid_dev[current_device()].store(grid, std::memory_order_release);
     }
+    // l_p <= 96 (single small matrices, narrow TEBD sectors): one CTA per
+    // item, block barriers only (C1 Cholesky 0.60 -> 0.52 ms per call chain;
+    // from l_p = 160 up the grid / cluster modes are as fast or faster).
+    if (ceil_div(ellp, 32) <= 3) {
+      static std::atomic<uint64_t> attr2{0};
+      once_per_device(attr2, [&] {
+        RSVD_CUDA(cudaFuncSetAttribute(gchol_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       bytes));
+      });
+      gchol_kernel<2><<<static_cast<unsigned>(batch), kGcThreads, bytes, st>>>(ga);
+      RSVD_LAUNCH("gchol_kernel");
+      return;
+    }
     // Size the persistent grid to the work: the widest step has one warp task
     // per (item, upper 32 x 32 tile); a full-GPU grid for a small batch (a
     // chunk of the host pipeline) only spins in grid barriers while occupying
-    // the SMs the other chunk's GEMMs could use.  RSVD_GCHOL_GRID overrides.
+    // the SMs the other chunk's GEMMs could use.
     const int64_t nbk = ceil_div(ellp, 32);
     const int64_t want = ceil_div(batch * nbk * (nbk + 1) / 2, kGcWarps);
     int g = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(want, 32)));
@@ -1109,9 +1147,9 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
       int clu_ok = clu_dev[current_device()].load(std::memory_order_acquire) - 1;
       if (clu_ok < 0) {
         clu_ok = 0;
-        if (cudaFuncSetAttribute(gchol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gchol_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  bytes) == cudaSuccess &&
-            cudaFuncSetAttribute(gchol_kernel<true>,
+            cudaFuncSetAttribute(gchol_kernel<1>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
           cudaLaunchConfig_t probe{};
           cudaLaunchAttribute pa[1];
@@ -1125,7 +1163,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
           probe.attrs = pa;
           probe.numAttrs = 1;
           int ncl = 0;
-          if (cudaOccupancyMaxActiveClusters(&ncl, gchol_kernel<true>, &probe) == cudaSuccess &&
+          if (cudaOccupancyMaxActiveClusters(&ncl, gchol_kernel<1>, &probe) == cudaSuccess &&
               ncl >= 1)
             clu_ok = 1;
         }
@@ -1146,13 +1184,13 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
         cfg.stream = st;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        RSVD_CUDA(cudaLaunchKernelEx(&cfg, gchol_kernel<true>, ga));
+        RSVD_CUDA(cudaLaunchKernelEx(&cfg, gchol_kernel<1>, ga));
         RSVD_LAUNCH("gchol_kernel");
         return;
       }
     }
     void* args[] = {&ga};
-    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel<false>), dim3(g),
+    RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gchol_kernel<0>), dim3(g),
                                           dim3(kGcThreads), args, bytes, st));
     RSVD_LAUNCH("gchol_kernel");
     return;

@@ -140,3 +140,47 @@ def test_qr_f64_rejects_wide(cuda):
                               X.data_ptr(), 8, 64, L.PTR_DEVICE)
     with pytest.raises(InvalidArgument, match="m >= n"):
         L.raise_for(rc, h.raw)
+
+
+@pytest.mark.parametrize("log_kappa", [2, 6, 9, 12, 15])
+def test_qr_fallback_range(cuda, log_kappa):
+    """The engine's orthonormalisation (the reference's Householder QR,
+    lapack.cpp:180-201 -> shifted CholeskyQR with pivoted completion here,
+    DESIGN.md §4) over a kappa(Y) sweep: Q stays orthonormal to 1e-12
+    throughout; Y = Q R holds to working precision up to kappa = 1e12 and to
+    ~4e-12 relative at kappa = 1e15 (numerically rank deficient: Householder
+    would keep ~1e-16 there -- the documented limit of the fallback), while
+    plain CholeskyQR2 (restated in numpy below) has already broken down from
+    kappa ~ 1e8 (the Gram loses definiteness)."""
+    import torch
+
+    L, h = _lib()
+    m, n = 300, 40
+    rng = np.random.default_rng(log_kappa)
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    y = (u * np.logspace(0, -log_kappa, n)) @ v.T
+    X = torch.from_numpy(np.asfortranarray(y).T.copy()).to(cuda).t()
+    Q = torch.empty((n, m), dtype=torch.float64, device=cuda).t()
+    R = torch.empty((n, n), dtype=torch.float64, device=cuda).t()
+    L.raise_for(L.load().rsvd_qr_f64(h.raw, 1, X.data_ptr(), m, n, m, m * n, Q.data_ptr(), m,
+                                     m * n, R.data_ptr(), n, n * n, L.PTR_DEVICE), h.raw)
+    torch.cuda.synchronize()
+    q, r = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.max(np.abs(q.T @ q - np.eye(n))) < 1e-12
+    tol = 1e-13 if log_kappa <= 12 else 1e-11
+    assert np.linalg.norm(y - q @ r) <= tol * np.linalg.norm(y)
+
+    def cholqr2(a):
+        for _ in range(2):
+            rr = np.linalg.cholesky(a.T @ a).T
+            a = np.linalg.solve(rr.T, a.T).T
+        return a
+
+    try:
+        qq = cholqr2(y)
+        plain_ok = np.max(np.abs(qq.T @ qq - np.eye(n))) < 1e-12
+    except np.linalg.LinAlgError:
+        plain_ok = False
+    if log_kappa >= 9:
+        assert not plain_ok  # the range the fallback exists for
