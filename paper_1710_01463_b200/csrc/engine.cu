@@ -24,6 +24,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <initializer_list>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -731,6 +732,22 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   RSVD_CUDA(cudaStreamSynchronize(h->s_in));
 }
 
+// True when every host buffer is page-locked right now.  A captured host-copy
+// graph is keyed on raw addresses: a caller that frees a pinned buffer and
+// gets pageable memory back at the same address must not replay copies bound
+// to the old pinned allocation, so the check runs before every replay.
+bool all_pinned(std::initializer_list<const void*> ptrs) {
+  for (const void* p : ptrs) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
 // Replay a captured CUDA graph of `enqueue` (one host launch per call), keyed
 // by everything the captured pointers and shapes depend on; captured on the
 // handle's own stream and ordered after / before the caller's stream with
@@ -879,7 +896,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
                  q);
       copy_batch(S, rank, strideS, B.Sh, rank, rank, rank, 1, batch, cudaMemcpyDeviceToHost, q);
     };
-    if (!h->prof.on && graphs_enabled() && !sharded) {
+    if (!h->prof.on && graphs_enabled() && !sharded && all_pinned({A, U, S, Vt})) {
       char keybuf[512];
       std::snprintf(keybuf, sizeof(keybuf),
                     "h|%p|%p|%p|%p|%p|%p|%p|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d",

@@ -1022,8 +1022,19 @@ bool launch_zjacobi_gram(const double* src, int64_t src_ld, int64_t src_stride, 
       if (ok) return true;
     }
   }
-  if (R <= 3) return launch_zgram_t<3, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
-  if (R <= 5) return launch_zgram_t<5, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  // The 64-register (MINB = 2) instantiations only pay off when two CTAs
+  // really fit an SM's shared memory; otherwise they just spill.
+  auto two_fit = [&] {
+    const int64_t rows = std::min<int64_t>(32 * R, (ell + 15) & ~int64_t(15));
+    const int64_t bytes = 64 * (rows + 2) * 8 + 2 * 32 * 33 * 16 + batch * 4 + 16;
+    int per_sm_smem = 0;
+    cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, current_device());
+    return 2 * (bytes + 1024) <= per_sm_smem;
+  };
+  const bool minb2 = two_fit();
+  if (R <= 3 && minb2) return launch_zgram_t<3, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 5 && minb2) return launch_zgram_t<5, false, 2>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
+  if (R <= 5) return launch_zgram_t<5, false, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
   if (R <= 9) return launch_zgram_t<9, false, 1>(src, src_ld, src_stride, src_mode, H, J, ell, lp, max_sweeps, sweeps, flags, batch, 1, st);
   return false;
 }
