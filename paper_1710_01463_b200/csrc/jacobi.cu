@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(256, MINB)
                      int64_t batch, int max_sweeps, unsigned* __restrict__ flags,
                      int* __restrict__ sweeps_out) {
   constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, NW = 8;
-  constexpr int PITCH = RC + 2;
+  constexpr int PITCH = RC + 4;  // = 4 mod 16 doubles: conflict-free DMMA fragment loads
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_rot;
   __shared__ unsigned long long s_mx;
@@ -766,7 +766,7 @@ template <int RC, int MINB>
 void launch_df_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                  unsigned* flags, int64_t batch, cudaStream_t st) {
   const int nbuf = ell > RC ? 2 : 1;
-  const size_t bytes = (static_cast<size_t>(nbuf * 32) * (RC + 2) + 32 * 36 + 32 * 33 + 3 * 16 + 8) *
+  const size_t bytes = (static_cast<size_t>(nbuf * 32) * (RC + 4) + 32 * 36 + 32 * 33 + 3 * 16 + 8) *
                        sizeof(double);
   auto kern = jacobi_df_kernel<RC, MINB>;
   RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
