@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(512, 1)
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   cg::cluster_group cluster = cg::this_cluster();
-  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, PITCH = 32 * RL + 2, ROWS = 32 * RL;
+  constexpr int W = 16, NC = 32, VP = NC + 4, GP = NC + 1, PITCH = 32 * RL + 4, ROWS = 32 * RL;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_rot;
   __shared__ unsigned long long s_mx;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(512, 1)
 template <int RL>
 bool launch_clu_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                   unsigned* flags, int64_t batch, int S, cudaStream_t st) {
-  const size_t bytes = (static_cast<size_t>(32) * (32 * RL + 2) + 32 * 36 + 2 * 32 * 33) * sizeof(double) +
+  const size_t bytes = (static_cast<size_t>(32) * (32 * RL + 4) + 32 * 36 + 2 * 32 * 33) * sizeof(double) +
                        batch * sizeof(int) + 16;
   auto kern = jacobi_clug_kernel<RL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
