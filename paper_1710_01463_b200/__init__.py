@@ -22,7 +22,7 @@ from .factorize import (
 )
 from .blocks import (BlockDiagMatrix, BlockFactorization, BlockMethod, RankPolicy,
                      SectorRankRequest, block_factorize, block_factorize_many, sector_request)
-from . import matrix_io, models, tebd  # noqa: E402  (CLI: python -m paper_1710_01463_b200.cli)
+from . import gates, matrix_io, tebd  # noqa: E402  (CLI: python -m paper_1710_01463_b200.cli)
 from .rng import CounterRng, derive_seed, mix64, seed_tag
 
 __all__ = [
@@ -30,6 +30,6 @@ __all__ = [
     "LibraryMissing", "NumericalError", "RsvdParams", "TruncatedFactorization", "derive_seed",
     "mix64", "randomized_range", "reconstruction_error", "rsvd", "rsvd_batched", "seed_tag",
     "tsvd", "tsvd_batched", "BlockDiagMatrix", "BlockFactorization", "BlockMethod", "RankPolicy",
-    "SectorRankRequest", "block_factorize", "block_factorize_many", "sector_request", "models",
+    "SectorRankRequest", "block_factorize", "block_factorize_many", "sector_request", "gates",
     "tebd", "matrix_io",
 ]

@@ -39,8 +39,7 @@ from . import _lib
 from ._lib import InvalidArgument
 from .blocks import (BlockDiagMatrix, BlockMethod, SectorRankRequest, block_factorize,
                      block_factorize_many)
-from .models import GateForm, SiteStructure, TwoSiteGate
-from .rng import CounterRng, derive_seed, seed_tag
+from .gates import GateForm, SiteStructure, TwoSiteGate
 
 LAMBDA_FLOOR = 1e-12  # mps.cpp:22
 LAMBDA_TRIM = 1e-11   # mps.cpp:23
@@ -106,58 +105,6 @@ class SymmetricMPS:
         g = [[[x.cpu().numpy() for x in pair] for pair in site] for site in self.gammas]
         lam = [[x.cpu().numpy() for x in pair] for pair in self.lambdas]
         return g, lam
-
-
-def random_product_state(site: SiteStructure, length: int, seed: int,
-                         device="cuda", dtype=None) -> SymmetricMPS:
-    """mps.cpp:62-108: uniform basis states from
-    CounterRng(derive_seed(seed, initial_state)), the last site closing the
-    total parity to even.  ``dtype`` torch.complex128 gives the
-    SymmetricMPS<Complex> instantiation (mps.cpp:551-555): complex Gammas (the
-    bond updates then run the complex factorization), real lambdas."""
-    torch = _torch()
-    if length < 2:
-        raise InvalidArgument("random_product_state: need at least two sites")
-    d = site.dim
-    if d < 2 or len(site.charges) != d:
-        raise InvalidArgument("random_product_state: invalid site structure")
-    rng = CounterRng(derive_seed(seed, seed_tag.initial_state))
-
-    def draw(n):
-        return min(n - 1, int(rng.uniform() * float(n)))
-
-    basis = [0] * length
-    partial = 0
-    for j in range(length - 1):
-        basis[j] = draw(d)
-        partial ^= site.charges[basis[j]]
-    closing = [m for m in range(d) if site.charges[m] == partial]
-    if not closing:
-        raise InvalidArgument("random_product_state: parity not closable")
-    basis[length - 1] = closing[draw(len(closing))]
-    cum = [0] * (length + 1)
-    for j in range(length):
-        cum[j + 1] = cum[j] ^ site.charges[basis[j]]
-    f64 = dict(dtype=torch.float64, device=device)
-    gdt = dict(dtype=dtype or torch.float64, device=device)
-    lambdas = []
-    for b in range(length + 1):
-        pair = [torch.zeros(0, **f64), torch.zeros(0, **f64)]
-        pair[cum[b]] = torch.ones(1, **f64)
-        lambdas.append(pair)
-    gammas = []
-    for j in range(length):
-        site_t = []
-        for m in range(d):
-            pair = []
-            for a in (0, 1):
-                rows = 1 if a == cum[j] else 0
-                cols = 1 if (a ^ site.charges[m]) == cum[j + 1] else 0
-                pair.append(torch.zeros(rows, cols, **gdt))
-            site_t.append(pair)
-        site_t[basis[j]][cum[j]][0, 0] = 1.0
-        gammas.append(site_t)
-    return SymmetricMPS(site, gammas, lambdas)
 
 
 def _floored_inverse(lam):
@@ -544,29 +491,3 @@ def apply_gate_layer(psi: SymmetricMPS, bonds: Sequence[int], gates: Sequence[Tw
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     return _finish_layer(psi, plans, fs, dt, handle)
-
-
-def canonicalize(psi: SymmetricMPS, handle=None) -> None:
-    """rlftn::canonicalize (mps.cpp:326-350): identity gates right-to-left,
-    left-to-right, then one even-bond layer, exact factorization with the cap
-    d * max bond dimension (identity gates cannot raise a rank)."""
-    from .blocks import RankPolicy
-
-    psi.validate()
-    n = psi.length()
-    d = psi.site.dim
-    ident = TwoSiteGate(GateForm.block, 0.0, np.eye(d * d), [])
-    req = SectorRankRequest(RankPolicy.maximal, 0)
-    exact = BlockMethod.deterministic()
-    cap = d * psi.max_bond_dimension()
-    for b in range(n - 2, -1, -1):
-        apply_gate(psi, b, ident, cap, exact, req, handle)
-    for b in range(n - 1):
-        apply_gate(psi, b, ident, cap, exact, req, handle)
-    layer = list(range(0, n - 1, 2))
-    apply_gate_layer(psi, layer, [ident] * len(layer), cap, exact, req, handle)
-
-
-def lambda_norm_error(psi: SymmetricMPS) -> float:
-    """mps.cpp:352-358: max_b |sum lambda_b^2 - 1|."""
-    return max(abs(float((l[0] * l[0]).sum() + (l[1] * l[1]).sum()) - 1.0) for l in psi.lambdas)

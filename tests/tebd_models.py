@@ -1,4 +1,7 @@
-"""Model and gate construction for the TEBD bond update (host-side setup).
+"""TEST INFRASTRUCTURE: model and gate construction feeding the TEBD
+bond-update tests and tools/tebd_bench.py (model construction is out of the
+hot-path scope; the product keeps only the gate / site
+interface types, paper_1710_01463_b200/gates.py).
 
 Restates rlftn's models.hpp / models.cpp: spin operators (models.cpp:121-145),
 the Z2 parity structure (models.cpp:151-158), the two-site bond Hamiltonians of
@@ -16,7 +19,8 @@ from typing import List, Union
 
 import numpy as np
 
-from ._lib import InvalidArgument
+from paper_1710_01463_b200._lib import InvalidArgument
+from paper_1710_01463_b200.gates import GateForm, KronTerm, SiteStructure, TwoSiteGate  # noqa: F401
 
 
 @dataclass
@@ -64,13 +68,6 @@ class CylinderModel:
 
 Model = Union[ChainModel, CylinderModel]
 
-
-@dataclass
-class SiteStructure:
-    dim: int
-    charges: List[int]
-    dim_even: int = 0
-    dim_odd: int = 0
 
 
 def _pauli_x():
@@ -133,25 +130,7 @@ def bond_hamiltonians(model: Model) -> List[np.ndarray]:
     return out
 
 
-class GateForm(enum.Enum):
-    block = 0
-    product = 1
 
-
-@dataclass
-class KronTerm:
-    left: np.ndarray
-    right: np.ndarray
-    charge: int = 0
-    weight: float = 0.0
-
-
-@dataclass
-class TwoSiteGate:
-    form: GateForm = GateForm.block
-    dt: float = 0.0
-    block: np.ndarray = None
-    terms: List[KronTerm] = field(default_factory=list)
 
 
 def _commutes_with_parity(h, charges):

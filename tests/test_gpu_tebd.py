@@ -8,7 +8,8 @@ weights, the dense state."""
 import numpy as np
 import pytest
 
-from paper_1710_01463_b200 import models as M
+from tests import tebd_helpers as TH
+from tests import tebd_models as M
 
 from .tebd_helpers import apply_two_site, mps_to_dense, schmidt_values, sorted_lambdas
 
@@ -73,7 +74,7 @@ def test_matches_dense_evolution(cuda, model, seed):  # test_mps.cpp:42-79, 128-
 
     st = M.parity_structure(model)
     n = model.length
-    psi = tebd.random_product_state(st, n, seed, device=cuda)
+    psi = TH.random_product_state(st, n, seed, device=cuda)
     ref = mps_to_dense(*psi.to_numpy(), st.charges)
     bonds = M.bond_hamiltonians(model)
     dts = [0.2, 0.35, 0.1]
@@ -105,7 +106,7 @@ def test_complex_mps_matches_dense_evolution(cuda, model, seed, form):
 
     st = M.parity_structure(model)
     n = model.length
-    psi = tebd.random_product_state(st, n, seed, device=cuda, dtype=torch.complex128)
+    psi = TH.random_product_state(st, n, seed, device=cuda, dtype=torch.complex128)
     ref = mps_to_dense(*psi.to_numpy(), st.charges)
     assert np.iscomplexobj(ref)
     bonds = M.bond_hamiltonians(model)
@@ -124,8 +125,8 @@ def test_complex_mps_matches_dense_evolution(cuda, model, seed, form):
             assert abs(np.vdot(ref, got)) / np.linalg.norm(got) == pytest.approx(1.0, abs=1e-10)
     assert psi.gammas[0][0][0].dtype == torch.complex128
     psi.validate()
-    tebd.canonicalize(psi)
-    assert tebd.lambda_norm_error(psi) < 1e-12
+    TH.canonicalize(psi)
+    assert TH.lambda_norm_error(psi) < 1e-12
 
 
 def test_block_and_product_forms_agree(cuda):  # test_mps.cpp:139-161
@@ -134,8 +135,8 @@ def test_block_and_product_forms_agree(cuda):  # test_mps.cpp:139-161
     for m in (M.ChainModel(4, 1.0, 1.1), M.CylinderModel(3, 2, 2.9)):
         st = M.parity_structure(m)
         n = m.length
-        pb = tebd.random_product_state(st, n, 31, device=cuda)
-        pp = tebd.random_product_state(st, n, 31, device=cuda)
+        pb = TH.random_product_state(st, n, 31, device=cuda)
+        pp = TH.random_product_state(st, n, 31, device=cuda)
         bonds = M.bond_hamiltonians(m)
         for ps in range(2):
             for b in range(ps, n - 1, 2):
@@ -175,14 +176,14 @@ def test_lambdas_are_schmidt_values(cuda):  # test_mps.cpp:198-215 (GPU-evolved 
     for m in (M.ChainModel(5, 0.5, 0.9), M.CylinderModel(3, 2, 3.1)):
         st = M.parity_structure(m)
         n = m.length
-        psi = tebd.random_product_state(st, n, 23, device=cuda)
+        psi = TH.random_product_state(st, n, 23, device=cuda)
         bonds = M.bond_hamiltonians(m)
         for ps in range(3):
             for b in range(ps % 2, n - 1, 2):
                 tebd.apply_gate(psi, b, M.build_gate(bonds[b], st.charges, 0.35), 64,
                                 BlockMethod.deterministic(), _req(64))
-        tebd.canonicalize(psi)  # mps.cpp:326-350
-        assert tebd.lambda_norm_error(psi) < 1e-12
+        TH.canonicalize(psi)  # mps.cpp:326-350
+        assert TH.lambda_norm_error(psi) < 1e-12
         v = mps_to_dense(*psi.to_numpy(), st.charges)
         assert np.linalg.norm(v) == pytest.approx(1.0, abs=1e-10)
         for b in range(1, n):

@@ -4,7 +4,8 @@ against the oracle), layer validation."""
 import numpy as np
 import pytest
 
-from paper_1710_01463_b200 import models as M
+from tests import tebd_helpers as TH
+from tests import tebd_models as M
 from paper_1710_01463_b200._lib import InvalidArgument
 
 from .tebd_helpers import mps_to_dense
@@ -155,7 +156,7 @@ def test_random_product_state_matches_oracle(seed):  # test_mps.cpp:82-108
     from paper_1710_01463_b200 import tebd
 
     st = M.parity_structure(M.ChainModel(6, 1.0, 1.0))
-    psi = tebd.random_product_state(st, 6, seed, device="cpu")
+    psi = TH.random_product_state(st, 6, seed, device="cpu")
     psi.validate()
     assert psi.max_bond_dimension() == 1
     g, lam = psi.to_numpy()
@@ -176,11 +177,11 @@ def test_product_state_deterministic_in_seed():  # test_mps.cpp:96-108
     from paper_1710_01463_b200 import tebd
 
     st = M.parity_structure(M.CylinderModel(5, 2, 3.0))
-    a = mps_to_dense(*tebd.random_product_state(st, 5, 7, device="cpu").to_numpy(), st.charges)
-    b = mps_to_dense(*tebd.random_product_state(st, 5, 7, device="cpu").to_numpy(), st.charges)
+    a = mps_to_dense(*TH.random_product_state(st, 5, 7, device="cpu").to_numpy(), st.charges)
+    b = mps_to_dense(*TH.random_product_state(st, 5, 7, device="cpu").to_numpy(), st.charges)
     assert np.array_equal(a, b)
     assert any(not np.array_equal(
-        mps_to_dense(*tebd.random_product_state(st, 5, s, device="cpu").to_numpy(), st.charges), a)
+        mps_to_dense(*TH.random_product_state(st, 5, s, device="cpu").to_numpy(), st.charges), a)
         for s in range(8, 16))
 
 
@@ -190,11 +191,11 @@ def test_validate_rejects_corrupted_states():  # test_mps.cpp:475-492
     from paper_1710_01463_b200 import tebd
 
     st = M.parity_structure(M.ChainModel(4, 0.5, 1.0))
-    psi = tebd.random_product_state(st, 4, 3, device="cpu")
+    psi = TH.random_product_state(st, 4, 3, device="cpu")
     psi.gammas[1][0][0] = torch.zeros(3, 3, dtype=torch.float64)
     with pytest.raises(ValueError, match="fusion rule"):
         psi.validate()
-    psi = tebd.random_product_state(st, 4, 3, device="cpu")
+    psi = TH.random_product_state(st, 4, 3, device="cpu")
     psi.lambdas.pop()
     with pytest.raises(ValueError, match="one bond more"):
         psi.validate()

@@ -5,7 +5,7 @@ sys.argv = [sys.argv[0]] + sys.argv[1:]
 import torch
 from tools import tebd_bench as TB
 from paper_1710_01463_b200 import BlockMethod, RankPolicy, SectorRankRequest, tebd
-from paper_1710_01463_b200 import models as M
+from tests import tebd_models as M
 chi = int(os.environ.get("CHI", "32"))
 dev = torch.device("cuda:0")
 model = M.ChainModel(64, 0.5, 1.0)

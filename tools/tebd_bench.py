@@ -18,7 +18,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1710_01463_b200 import BlockMethod, RankPolicy, SectorRankRequest  # noqa: E402
-from paper_1710_01463_b200 import models as M  # noqa: E402
+from tests import tebd_helpers as TH
+from tests import tebd_models as M  # noqa: E402
 from paper_1710_01463_b200 import tebd  # noqa: E402
 
 
@@ -78,7 +79,7 @@ def main():
     if args.random_state:
         psi = random_mps(site, args.length, args.chi, dev)
     else:
-        psi = tebd.random_product_state(site, args.length, 1, device=dev)
+        psi = TH.random_product_state(site, args.length, 1, device=dev)
         # grow the entanglement (imaginary time saturates well below chi on
         # the critical chain; --random-state loads the full chi instead)
         for i in range(64):
