@@ -1076,6 +1076,303 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused CholeskyQR pass for small bases (fcqr_kernel), l_p <= 160: one CTA per
+// item does the whole pass -- Gram, Cholesky, inverse factors and Q = Y R^-1 --
+// with the Gram / R kept in shared memory as upper 32 x 32 blocks, so the
+// latency-bound small factorization never goes through L2 or a grid barrier
+// and the three launches (+ split-K reduce and mirror) of the unfused pass
+// become one.  Same outputs and breakdown rule as gchol_kernel:
+//   1. G = Y^T Y, upper blocks, Y streamed in CR-row chunks (cp.async double
+//      buffer, DMMA); the full symmetric G is also written to G0 (global) for
+//      the shifted-CholeskyQR retry of ill-conditioned items;
+//   2. per 32-column block J: one warp factors the diagonal block
+//      (factor_diag_block: R_JJ, D_J = R_JJ^-1, breakdown at pivot <= tau *
+//      max diag G -> rank r), R_J,c = D_J^T G_J,c, trailing update
+//      G_c,c' -= R_J,c^T R_J,c' (warp tasks, DMMA, shared memory);
+//   3. Rf = R (rows < r) when requested; W_IJ = R_IJ D_J in place of R_IJ;
+//   4. Q_J = Y_J D_J - sum_{I<J} Q_I W_IJ: each warp owns 16-row slabs and runs
+//      the block columns J in order (no CTA barrier; columns >= r are zero, the
+//      caller's completion fills them).
+// 16-byte global -> shared async copy; bytes < 16 zero-fills the rest.
+__device__ __forceinline__ void cpa16(void* dst, const void* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
+
+constexpr int kFqThreads = 256;  // 8 warps: <= 255 registers, the diagonal factor stays in registers
+constexpr int kFqWarps = kFqThreads / 32;
+constexpr int kFqBlk = 32 * kInvPitch;  // doubles per stored 32 x 32 block (pitch 36)
+
+struct FcqrArgs {
+  const double* Y;
+  int64_t ldy, sY;
+  double* Q;
+  int64_t ldq, sQ;
+  double* G0;  // full symmetric Gram (l_p x l_p, ld l_p) per item, or null
+  double* Rf;  // R (l_p x l_p, ld l_p, upper, zero below / beyond rank), or null
+  int* rank;
+  int rows, ell, ellp, cr;  // cr: staged rows per chunk (multiple of 16)
+  double tau;
+};
+
+__device__ __forceinline__ int fq_ub(int I, int J) { return J * (J + 1) / 2 + I; }  // I <= J
+
+__global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double s_red[kFqWarps];
+  __shared__ int s_rank;
+  __shared__ double s_thresh;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int ell = a.ell, ellp = a.ellp, rows = a.rows, CR = a.cr, CRP = a.cr + 4;
+  const int nbk = ellp / 32, nub = nbk * (nbk + 1) / 2;
+  double* Gb = sm;                   // upper blocks, element (i, j) at i + j * kInvPitch
+  double* U = sm + nub * kFqBlk;     // union: Y chunk buffers | D_J blocks + diag scratch
+  double* Dst = U;                   // D_J (row-major, pitch kInvPitch), J < nbk
+  double* Rd = U + nbk * kFqBlk;     // factor_diag_block scratch
+  double* Dt = Rd + kFqBlk;
+  const double* Y = a.Y + b * a.sY;
+  double* Q = a.Q + b * a.sQ;
+  auto blk = [&](int I, int J) { return Gb + fq_ub(I, J) * kFqBlk; };
+
+  // ---- 1. Gram (upper blocks) ------------------------------------------------
+  // 8 DMMA tiles (16 x 8) per warp per round; l_p > 128 takes two rounds over Y.
+  const int ntiles = 8 * nub;
+  // 16-byte copies need 16-byte aligned columns (even ld, aligned base);
+  // otherwise (odd row counts) 8-byte copies.
+  const bool vec16 = (a.ldy % 2 == 0) && (a.sY % 2 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.Y) & 15u) == 0);
+  auto stage = [&](int c, int buf) {
+    const int r0 = c * CR;
+    double* dst = U + buf * ellp * CRP;
+    if (vec16) {
+      const int per = CR / 2;
+      for (int e = tid; e < ellp * per; e += kFqThreads) {
+        const int col = e / per, r = 2 * (e - col * per);
+        const int gr = r0 + r;
+        int bytes = 0;
+        const double* src = Y;
+        if (col < ell && gr < rows) {
+          bytes = min(16, (rows - gr) * 8);
+          src = Y + gr + static_cast<int64_t>(col) * a.ldy;
+        }
+        cpa16(dst + r + col * CRP, src, bytes);
+      }
+    } else {
+      for (int e = tid; e < ellp * CR; e += kFqThreads) {
+        const int col = e / CR, r = e - col * CR;
+        const int gr = r0 + r;
+        const bool ok = col < ell && gr < rows;
+        const double* src = ok ? Y + gr + static_cast<int64_t>(col) * a.ldy : Y;
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + r + col * CRP));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                     "r"(ok ? 8 : 0)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int nch = (rows + CR - 1) / CR;
+  for (int t0 = 0; t0 < ntiles; t0 += 8 * kFqWarps) {
+    double acc[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+    int tI[8], tJ[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ub = (t0 + warp + kFqWarps * u) >> 3;
+      int J = 0;
+      while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+      tJ[u] = J;
+      tI[u] = ub - J * (J + 1) / 2;
+    }
+    stage(0, 0);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        stage(c + 1, (c + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncthreads();
+      const double* Yc = U + (c & 1) * ellp * CRP;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int tt = t0 + warp + kFqWarps * u;
+        if (tt < ntiles) {
+          const int tm = (tt >> 2) & 1, tn = tt & 3;
+          const double* ap0 = Yc + (32 * tI[u] + 16 * tm + g) * CRP + t;
+          const double* ap1 = ap0 + 8 * CRP;
+          const double* bp = Yc + (32 * tJ[u] + 8 * tn + g) * CRP + t;
+          for (int k0 = 0; k0 < CR; k0 += 4) dmma_16x8x4(acc[u], ap0[k0], ap1[k0], bp[k0]);
+        }
+      }
+      __syncthreads();  // buffer c & 1 is restaged at c + 2
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int tt = t0 + warp + kFqWarps * u;
+      if (tt < ntiles) {
+        const int ub = tt >> 3, tm = (tt >> 2) & 1, tn = tt & 3;
+        double* W = Gb + ub * kFqBlk;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = 16 * tm + g + ((q & 2) ? 8 : 0), j = 8 * tn + 2 * t + (q & 1);
+          W[i + j * kInvPitch] = acc[u][q];
+          if (a.G0) {
+            const int64_t gi = 32 * tI[u] + i, gj = 32 * tJ[u] + j;
+            double* G0 = a.G0 + b * static_cast<int64_t>(ellp) * ellp;
+            G0[gi + gj * ellp] = acc[u][q];
+            G0[gj + gi * ellp] = acc[u][q];
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. pivot floor, rank; blocked Cholesky in shared memory ---------------
+  if (warp == 0) {
+    double mx = 0.0;
+    for (int i = lane; i < ell; i += 32) mx = fmax(mx, blk(i >> 5, i >> 5)[(i & 31) * (kInvPitch + 1)]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0) {
+      s_thresh = a.tau * mx;
+      s_rank = mx > 0.0 ? ell : 0;
+    }
+  }
+  __syncthreads();
+  const double thresh = s_thresh;
+  for (int J = 0; J < nbk; ++J) {
+    if (32 * J >= s_rank) break;
+    if (warp == 0) {
+      double* W = blk(J, J);
+      double av[32];
+      const bool colok = 32 * J + lane < ell;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        av[i] = (colok && 32 * J + i < ell) ? W[i + lane * kInvPitch] : (i == lane ? 1.0 : 0.0);
+      const int brk = factor_diag_block(av, W, kInvPitch, ell - 32 * J, 0, thresh, Rd, Dt, lane);
+      double* D = Dst + J * kFqBlk;
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) D[lane * kInvPitch + k] = Dt[lane * kInvPitch + k];
+      if (lane == 0 && brk < 32 && 32 * J + brk < s_rank) s_rank = 32 * J + brk;
+    }
+    __syncthreads();
+    if (s_rank < 32 * (J + 1)) break;  // broke down inside block J
+    const int nr = nbk - J - 1;
+    const double* D = Dst + J * kFqBlk;
+    for (int c = J + 1 + warp; c < nbk; c += kFqWarps) {  // R_J,c = D_J^T G_J,c
+      double* W = blk(J, c);
+      double ac[2][4][4];
+      zero_acc(ac);
+      warp_mma32(ac, [&](int i, int k) { return D[k * kInvPitch + i]; },
+                 [&](int k, int cc) { return W[k + cc * kInvPitch]; }, g, t);
+      __syncwarp();
+      store_acc(ac, [&](int i, int cc, double v) { W[i + cc * kInvPitch] = v; }, g, t);
+    }
+    __syncthreads();
+    const int ntr = nr * (nr + 1) / 2;
+    for (int task = warp; task < ntr; task += kFqWarps) {  // G_c,c' -= R_J,c^T R_J,c'
+      int idx = task, cp = 0;
+      while (idx > cp) idx -= ++cp;
+      const int c = J + 1 + idx, c2 = J + 1 + cp;
+      const double* Rc = blk(J, c);
+      const double* Rc2 = blk(J, c2);
+      double* W = blk(c, c2);
+      double ac[2][4][4];
+      zero_acc(ac);
+      warp_mma32(ac, [&](int i, int k) { return Rc[k + i * kInvPitch]; },
+                 [&](int k, int cc) { return Rc2[k + cc * kInvPitch]; }, g, t);
+      store_acc(ac, [&](int i, int cc, double v) { W[i + cc * kInvPitch] -= v; }, g, t);
+    }
+    __syncthreads();
+  }
+  const int r = s_rank;
+  const int nbr = (r + 31) / 32;  // block columns with live R / D
+
+  // ---- 3. outputs: rank, Rf; W_IJ = R_IJ D_J in place ---------------------------
+  if (tid == 0) a.rank[b] = r;
+  if (a.Rf) {
+    double* Rf = a.Rf + b * static_cast<int64_t>(ellp) * ellp;
+    for (int e = tid; e < ellp * ellp; e += kFqThreads) {
+      const int i = e % ellp, j = e / ellp;
+      double v = 0.0;
+      if (i < r && i <= j && j < ell) v = blk(i >> 5, j >> 5)[(i & 31) + (j & 31) * kInvPitch];
+      Rf[e] = v;
+    }
+    __syncthreads();
+  }
+  {
+    const int nw = nbr * (nbr - 1) / 2;
+    for (int task = warp; task < nw; task += kFqWarps) {
+      int I = task, J = 1;
+      while (I >= J) I -= J++;
+      double* W = blk(I, J);
+      const double* D = Dst + J * kFqBlk;
+      double ac[2][4][4];
+      zero_acc(ac);
+      warp_mma32(ac, [&](int i, int k) { return W[i + k * kInvPitch]; },
+                 [&](int k, int cc) { return D[k * kInvPitch + cc]; }, g, t);
+      __syncwarp();
+      store_acc(ac, [&](int i, int cc, double v) { W[i + cc * kInvPitch] = v; }, g, t);
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. Q = Y R^-1, 16-row slabs per warp, block columns in order -----------
+  for (int r0 = 16 * warp; r0 < rows; r0 += 16 * kFqWarps) {
+    const int ra = r0 + g, rb = r0 + g + 8;
+    for (int J = 0; J < nbk; ++J) {
+      double ac[4][4];
+#pragma unroll
+      for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ac[n][q] = 0.0;
+      if (J < nbr) {
+        const double* D = Dst + J * kFqBlk;
+        const double* Yj = Y + static_cast<int64_t>(32 * J) * a.ldy;
+#pragma unroll 2
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          const int k = k0 + t;
+          const bool okc = 32 * J + k < ell;
+          const double a0 = (okc && ra < rows) ? __ldcg(Yj + ra + static_cast<int64_t>(k) * a.ldy) : 0.0;
+          const double a1 = (okc && rb < rows) ? __ldcg(Yj + rb + static_cast<int64_t>(k) * a.ldy) : 0.0;
+#pragma unroll
+          for (int n = 0; n < 4; ++n) dmma_16x8x4(ac[n], a0, a1, D[k * kInvPitch + n * 8 + g]);
+        }
+        for (int I = 0; I < J; ++I) {
+          const double* W = blk(I, J);
+          const double* Qi = Q + static_cast<int64_t>(32 * I) * a.ldq;
+#pragma unroll 2
+          for (int k0 = 0; k0 < 32; k0 += 4) {
+            const int k = k0 + t;
+            const double a0 = ra < rows ? __ldcg(Qi + ra + static_cast<int64_t>(k) * a.ldq) : 0.0;
+            const double a1 = rb < rows ? __ldcg(Qi + rb + static_cast<int64_t>(k) * a.ldq) : 0.0;
+#pragma unroll
+            for (int n = 0; n < 4; ++n) dmma_16x8x4(ac[n], a0, a1, -W[k + (n * 8 + g) * kInvPitch]);
+          }
+        }
+      }
+      double* Qj = Q + static_cast<int64_t>(32 * J) * a.ldq;
+#pragma unroll
+      for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = (q & 2) ? rb : ra, col = n * 8 + 2 * t + (q & 1);
+          if (row < rows) Qj[row + static_cast<int64_t>(col) * a.ldq] = (32 * J + col < r) ? ac[n][q] : 0.0;
+        }
+      __syncwarp();
+      __threadfence_block();
+    }
+  }
+}
+
 }  // namespace
 
 // Per item 2 l_p^2 (trailing buffers / inverse), plus a tail of PB x (l_p + 20)
@@ -1212,6 +1509,35 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
       G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp), tau,
       pivot ? (opts && opts->pairs ? 2 : 1) : 0, opts ? opts->mask : nullptr, rpg);
   RSVD_LAUNCH("pchol_kernel");
+}
+
+
+// Fused CholeskyQR pass (fcqr_kernel) for l_p <= 160; false when it does not
+// apply (the caller runs the unfused Gram / gchol / apply sequence).
+bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
+                      int64_t strideQ, double* G0, double* Rf, int* rank, int64_t rows,
+                      int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st) {
+  if (batch <= 0) return true;
+  if (ellp % 32 != 0 || ellp > 160 || rows < 1 || rows > (1 << 30)) return false;
+  const int64_t nbk = ellp / 32, nub = nbk * (nbk + 1) / 2;
+  const int64_t gbytes = nub * kFqBlk * 8, dbytes = (nbk + 2) * kFqBlk * 8;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device());
+  const int64_t cap = std::max(0, optin - 256);  // room for the kernel's static shared memory
+  int cr = 64;
+  while (cr > 16 && gbytes + std::max<int64_t>(2 * ellp * (cr + 4) * 8, dbytes) > cap) cr -= 16;
+  const int64_t bytes = gbytes + std::max<int64_t>(2 * ellp * (cr + 4) * 8, dbytes);
+  if (bytes > cap) return false;
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
+    RSVD_CUDA(cudaFuncSetAttribute(fcqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(cap)));
+  });
+  FcqrArgs fa{Y, ldy, strideY, Q, ldq, strideQ, G0, Rf, rank, static_cast<int>(rows),
+              static_cast<int>(ell), static_cast<int>(ellp), cr, tau};
+  fcqr_kernel<<<static_cast<unsigned>(batch), kFqThreads, bytes, st>>>(fa);
+  RSVD_LAUNCH("fcqr_kernel");
+  return true;
 }
 
 }  // namespace rsvd

@@ -146,6 +146,14 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
                   cudaStream_t st, const CholOpts* opts = nullptr);
 
+// chol.cu -- one fused CholeskyQR pass for l_p <= 160 (Gram, Cholesky with
+// breakdown -> rank, Q = Y R^-1): Q columns >= rank are zero (completion is the
+// caller's); G0 (full symmetric Gram) and Rf (R, zero below / beyond rank) are
+// written when non-null.  Returns false when the shape does not qualify.
+bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
+                      int64_t strideQ, double* G0, double* Rf, int* rank, int64_t rows,
+                      int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st);
+
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.
 // flags: jacobi_flag_elems(batch) unsigned ints of workspace.

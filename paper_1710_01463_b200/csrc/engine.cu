@@ -370,6 +370,9 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
+  // Small real bases: one fused CholeskyQR kernel per pass (chol.cu fcqr_kernel).
+  static const bool no_fused = std::getenv("RSVD_NO_FUSED_CQR") != nullptr;
+  const bool fused = !no_fused && !cplx && !sharded && lp <= 160;
   auto gram = [&](const MatRef& in, const int* mask) {
     Scope sc(P, kStGram, st);
     GemmOpts sym;
@@ -395,30 +398,45 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
     const MatRef& out = pass == 0 ? Tm : Y;
     double* Rf = Rt ? (pass == 0 ? B.Rf1 : B.Rf2) : nullptr;
     int* rk = pass == 0 ? B.rank1 : B.rank2;
-    bool pivot = false;
-    gram(in, nullptr);
-    {
-      Scope sc(P, kStChol, st);
-      if (pass == 0)
-        RSVD_CUDA(cudaMemcpyAsync(B.G0, B.G, sizeof(double) * b * lp * lp,
-                                  cudaMemcpyDeviceToDevice, st));
-      // Unpivoted everywhere (grid-parallel gchol; breakdown -> numerical
-      // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
-      // Jacobi) measured no fewer sweeps (r01 and r02, C2 8 / C4 7 sweeps).
-      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
-      if (pass == 0) {  // shifted retry of the items that stopped short of full rank
-        CholOpts o;
-        o.gate_rank = rk;
-        o.ill_out = B.ill;
-        o.Gsrc = B.G0;
-        o.shift_coef = 11.0 *
-                       (static_cast<double>(rows_global) * s.ell +
-                        static_cast<double>(s.ell) * (s.ell + 1)) *
-                       1.1102230246251565e-16;
-        launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, false, b, st, &o);
+    const bool pivot = false;
+    auto shifted_retry = [&] {  // the items that stopped short of full rank
+      CholOpts o;
+      o.gate_rank = rk;
+      o.ill_out = B.ill;
+      o.Gsrc = B.G0;
+      o.shift_coef = 11.0 *
+                     (static_cast<double>(rows_global) * s.ell +
+                      static_cast<double>(s.ell) * (s.ell + 1)) *
+                     1.1102230246251565e-16;
+      launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, false, b, st, &o);
+    };
+    if (fused) {
+      // One fused kernel per pass (Gram, Cholesky, Q = Y R^-1; G0 saved on the
+      // first pass); the ill items are then redone from G0 as before.
+      {
+        Scope sc(P, kStChol, st);
+        if (!launch_fused_cqr(in.base, rows, rows * lp, out.base, rows, rows * lp,
+                              pass == 0 ? B.G0 : nullptr, Rf, rk, rows, s.ell, lp, kPivotTau, b, st))
+          throw CudaError("orth: fused CholeskyQR does not fit this shape");
+        if (pass == 0) shifted_retry();
       }
-    }
-    {
+      Scope sc(P, kStApply, st);
+      if (pass == 0) apply(in, out, B.ill, pivot);
+      launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global,
+                            st);
+    } else {
+      gram(in, nullptr);
+      {
+        Scope sc(P, kStChol, st);
+        if (pass == 0)
+          RSVD_CUDA(cudaMemcpyAsync(B.G0, B.G, sizeof(double) * b * lp * lp,
+                                    cudaMemcpyDeviceToDevice, st));
+        // Unpivoted everywhere (grid-parallel gchol; breakdown -> numerical
+        // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
+        // Jacobi) measured no fewer sweeps (r01 and r02, C2 8 / C4 7 sweeps).
+        launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
+        if (pass == 0) shifted_retry();
+      }
       Scope sc(P, kStApply, st);
       apply(in, out, nullptr, pivot);
       launch_complete_basis(out, rows, s.ell, rk, B.seeds, tag + pass, b, row_off, rows_global,
