@@ -1138,15 +1138,16 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   auto blk = [&](int I, int J) { return Gb + fq_ub(I, J) * kFqBlk; };
 
   // ---- 1. Gram (upper blocks) ------------------------------------------------
-  // 8 DMMA tiles (16 x 8) per warp per round; l_p > 128 takes two rounds over Y.
+  // Up to 15 DMMA tiles (16 x 8) per warp, accumulated over all row chunks.
   const int ntiles = 8 * nub;
   // 16-byte copies need 16-byte aligned columns (even ld, aligned base);
   // otherwise (odd row counts) 8-byte copies.
   const bool vec16 = (a.ldy % 2 == 0) && (a.sY % 2 == 0) &&
                      ((reinterpret_cast<uintptr_t>(a.Y) & 15u) == 0);
+  double* const Sbuf = sm;  // the Gram phase stages Y over the whole shared memory
   auto stage = [&](int c, int buf) {
     const int r0 = c * CR;
-    double* dst = U + buf * ellp * CRP;
+    double* dst = Sbuf + buf * ellp * CRP;
     if (vec16) {
       const int per = CR / 2;
       for (int e = tid; e < ellp * per; e += kFqThreads) {
@@ -1175,60 +1176,57 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   const int nch = (rows + CR - 1) / CR;
-  for (int t0 = 0; t0 < ntiles; t0 += 8 * kFqWarps) {
-    double acc[8][4];
+  constexpr int kT = 15;  // tiles per warp: 8 warps x 15 >= 8 x 15 upper blocks (l_p = 160)
+  double acc[kT][4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < kT; ++u)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-    int tI[8], tJ[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int ub = (t0 + warp + kFqWarps * u) >> 3;
-      int J = 0;
-      while ((J + 1) * (J + 2) / 2 <= ub) ++J;
-      tJ[u] = J;
-      tI[u] = ub - J * (J + 1) / 2;
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      stage(c + 1, (c + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    stage(0, 0);
-    for (int c = 0; c < nch; ++c) {
-      if (c + 1 < nch) {
-        stage(c + 1, (c + 1) & 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      }
-      __syncthreads();
-      const double* Yc = U + (c & 1) * ellp * CRP;
+    __syncthreads();
+    const double* Yc = Sbuf + (c & 1) * ellp * CRP;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int tt = t0 + warp + kFqWarps * u;
-        if (tt < ntiles) {
-          const int tm = (tt >> 2) & 1, tn = tt & 3;
-          const double* ap0 = Yc + (32 * tI[u] + 16 * tm + g) * CRP + t;
-          const double* ap1 = ap0 + 8 * CRP;
-          const double* bp = Yc + (32 * tJ[u] + 8 * tn + g) * CRP + t;
-          for (int k0 = 0; k0 < CR; k0 += 4) dmma_16x8x4(acc[u], ap0[k0], ap1[k0], bp[k0]);
-        }
-      }
-      __syncthreads();  // buffer c & 1 is restaged at c + 2
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int tt = t0 + warp + kFqWarps * u;
+    for (int u = 0; u < kT; ++u) {
+      const int tt = warp + kFqWarps * u;
       if (tt < ntiles) {
         const int ub = tt >> 3, tm = (tt >> 2) & 1, tn = tt & 3;
-        double* W = Gb + ub * kFqBlk;
+        int J = 0;
+        while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+        const int I = ub - J * (J + 1) / 2;
+        const double* ap0 = Yc + (32 * I + 16 * tm + g) * CRP + t;
+        const double* ap1 = ap0 + 8 * CRP;
+        const double* bp = Yc + (32 * J + 8 * tn + g) * CRP + t;
+#pragma unroll 4
+        for (int k0 = 0; k0 < CR; k0 += 4) dmma_16x8x4(acc[u], ap0[k0], ap1[k0], bp[k0]);
+      }
+    }
+    __syncthreads();  // buffer c & 1 is restaged at c + 2; the last one frees the G blocks
+  }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = 16 * tm + g + ((q & 2) ? 8 : 0), j = 8 * tn + 2 * t + (q & 1);
-          W[i + j * kInvPitch] = acc[u][q];
-          if (a.G0) {
-            const int64_t gi = 32 * tI[u] + i, gj = 32 * tJ[u] + j;
-            double* G0 = a.G0 + b * static_cast<int64_t>(ellp) * ellp;
-            G0[gi + gj * ellp] = acc[u][q];
-            G0[gj + gi * ellp] = acc[u][q];
-          }
+  for (int u = 0; u < kT; ++u) {
+    const int tt = warp + kFqWarps * u;
+    if (tt < ntiles) {
+      const int ub = tt >> 3, tm = (tt >> 2) & 1, tn = tt & 3;
+      int J = 0;
+      while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+      const int I = ub - J * (J + 1) / 2;
+      double* W = Gb + ub * kFqBlk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = 16 * tm + g + ((q & 2) ? 8 : 0), j = 8 * tn + 2 * t + (q & 1);
+        W[i + j * kInvPitch] = acc[u][q];
+        if (a.G0) {
+          const int64_t gi = 32 * I + i, gj = 32 * J + j;
+          double* G0 = a.G0 + b * static_cast<int64_t>(ellp) * ellp;
+          G0[gi + gj * ellp] = acc[u][q];
+          G0[gj + gi * ellp] = acc[u][q];
         }
       }
     }
@@ -1248,24 +1246,27 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   }
   __syncthreads();
   const double thresh = s_thresh;
-  for (int J = 0; J < nbk; ++J) {
-    if (32 * J >= s_rank) break;
-    if (warp == 0) {
-      double* W = blk(J, J);
-      double av[32];
-      const bool colok = 32 * J + lane < ell;
+  // Factor the diagonal block J by warp 0 (R_JJ in place, D_J = R_JJ^-1,
+  // breakdown -> rank).
+  auto factor = [&](int J) {
+    double* W = blk(J, J);
+    double av[32];
+    const bool colok = 32 * J + lane < ell;
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        av[i] = (colok && 32 * J + i < ell) ? W[i + lane * kInvPitch] : (i == lane ? 1.0 : 0.0);
-      const int brk = factor_diag_block(av, W, kInvPitch, ell - 32 * J, 0, thresh, Rd, Dt, lane);
-      double* D = Dst + J * kFqBlk;
+    for (int i = 0; i < 32; ++i)
+      av[i] = (colok && 32 * J + i < ell) ? W[i + lane * kInvPitch] : (i == lane ? 1.0 : 0.0);
+    const int brk = factor_diag_block(av, W, kInvPitch, ell - 32 * J, 0, thresh, Rd, Dt, lane);
+    double* D = Dst + J * kFqBlk;
 #pragma unroll 4
-      for (int k = 0; k < 32; ++k) D[lane * kInvPitch + k] = Dt[lane * kInvPitch + k];
-      if (lane == 0 && brk < 32 && 32 * J + brk < s_rank) s_rank = 32 * J + brk;
-    }
-    __syncthreads();
-    if (s_rank < 32 * (J + 1)) break;  // broke down inside block J
+    for (int k = 0; k < 32; ++k) D[lane * kInvPitch + k] = Dt[lane * kInvPitch + k];
+    if (lane == 0 && brk < 32 && 32 * J + brk < s_rank) s_rank = 32 * J + brk;
+  };
+  if (warp == 0 && s_rank > 0) factor(0);
+  __syncthreads();
+  for (int J = 0; J < nbk; ++J) {
+    if (s_rank < 32 * (J + 1)) break;  // broke down in or before block J
     const int nr = nbk - J - 1;
+    if (nr == 0) break;
     const double* D = Dst + J * kFqBlk;
     for (int c = J + 1 + warp; c < nbk; c += kFqWarps) {  // R_J,c = D_J^T G_J,c
       double* W = blk(J, c);
@@ -1277,11 +1278,9 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       store_acc(ac, [&](int i, int cc, double v) { W[i + cc * kInvPitch] = v; }, g, t);
     }
     __syncthreads();
-    const int ntr = nr * (nr + 1) / 2;
-    for (int task = warp; task < ntr; task += kFqWarps) {  // G_c,c' -= R_J,c^T R_J,c'
-      int idx = task, cp = 0;
-      while (idx > cp) idx -= ++cp;
-      const int c = J + 1 + idx, c2 = J + 1 + cp;
+    // G_c,c' -= R_J,c^T R_J,c' (J < c <= c'); warp 0 takes (J+1, J+1) and then
+    // factors block J+1 while the other warps finish the trailing tiles.
+    auto trail = [&](int c, int c2) {
       const double* Rc = blk(J, c);
       const double* Rc2 = blk(J, c2);
       double* W = blk(c, c2);
@@ -1290,6 +1289,18 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       warp_mma32(ac, [&](int i, int k) { return Rc[k + i * kInvPitch]; },
                  [&](int k, int cc) { return Rc2[k + cc * kInvPitch]; }, g, t);
       store_acc(ac, [&](int i, int cc, double v) { W[i + cc * kInvPitch] -= v; }, g, t);
+    };
+    if (warp == 0) {
+      trail(J + 1, J + 1);
+      __syncwarp();
+      if (32 * (J + 1) < s_rank) factor(J + 1);
+    } else {
+      const int ntr = nr * (nr + 1) / 2;
+      for (int task = 1 + (warp - 1); task < ntr; task += kFqWarps - 1) {
+        int idx = task, cp = 0;
+        while (idx > cp) idx -= ++cp;
+        trail(J + 1 + idx, J + 1 + cp);
+      }
     }
     __syncthreads();
   }
@@ -1335,28 +1346,37 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) ac[n][q] = 0.0;
       if (J < nbr) {
+        // All 8 k-steps' fragments of a 32-column block are loaded before
+        // their DMMAs: one L2 round trip per block instead of four.
         const double* D = Dst + J * kFqBlk;
         const double* Yj = Y + static_cast<int64_t>(32 * J) * a.ldy;
-#pragma unroll 2
-        for (int k0 = 0; k0 < 32; k0 += 4) {
-          const int k = k0 + t;
-          const bool okc = 32 * J + k < ell;
-          const double a0 = (okc && ra < rows) ? __ldcg(Yj + ra + static_cast<int64_t>(k) * a.ldy) : 0.0;
-          const double a1 = (okc && rb < rows) ? __ldcg(Yj + rb + static_cast<int64_t>(k) * a.ldy) : 0.0;
+        double a0v[8], a1v[8];
 #pragma unroll
-          for (int n = 0; n < 4; ++n) dmma_16x8x4(ac[n], a0, a1, D[k * kInvPitch + n * 8 + g]);
+        for (int kq = 0; kq < 8; ++kq) {
+          const int k = 4 * kq + t;
+          const bool okc = 32 * J + k < ell;
+          a0v[kq] = (okc && ra < rows) ? __ldcg(Yj + ra + static_cast<int64_t>(k) * a.ldy) : 0.0;
+          a1v[kq] = (okc && rb < rows) ? __ldcg(Yj + rb + static_cast<int64_t>(k) * a.ldy) : 0.0;
         }
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+          for (int n = 0; n < 4; ++n)
+            dmma_16x8x4(ac[n], a0v[kq], a1v[kq], D[(4 * kq + t) * kInvPitch + n * 8 + g]);
         for (int I = 0; I < J; ++I) {
           const double* W = blk(I, J);
           const double* Qi = Q + static_cast<int64_t>(32 * I) * a.ldq;
-#pragma unroll 2
-          for (int k0 = 0; k0 < 32; k0 += 4) {
-            const int k = k0 + t;
-            const double a0 = ra < rows ? __ldcg(Qi + ra + static_cast<int64_t>(k) * a.ldq) : 0.0;
-            const double a1 = rb < rows ? __ldcg(Qi + rb + static_cast<int64_t>(k) * a.ldq) : 0.0;
 #pragma unroll
-            for (int n = 0; n < 4; ++n) dmma_16x8x4(ac[n], a0, a1, -W[k + (n * 8 + g) * kInvPitch]);
+          for (int kq = 0; kq < 8; ++kq) {
+            const int k = 4 * kq + t;
+            a0v[kq] = ra < rows ? __ldcg(Qi + ra + static_cast<int64_t>(k) * a.ldq) : 0.0;
+            a1v[kq] = rb < rows ? __ldcg(Qi + rb + static_cast<int64_t>(k) * a.ldq) : 0.0;
           }
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq)
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+              dmma_16x8x4(ac[n], a0v[kq], a1v[kq], -W[(4 * kq + t) + (n * 8 + g) * kInvPitch]);
         }
       }
       double* Qj = Q + static_cast<int64_t>(32 * J) * a.ldq;
@@ -1524,9 +1544,11 @@ bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, 
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device());
   const int64_t cap = std::max(0, optin - 256);  // room for the kernel's static shared memory
+  // The Gram phase stages Y over the whole allocation (the G blocks are
+  // written only after its last chunk): CR rows x l_p, double buffered.
   int cr = 64;
-  while (cr > 16 && gbytes + std::max<int64_t>(2 * ellp * (cr + 4) * 8, dbytes) > cap) cr -= 16;
-  const int64_t bytes = gbytes + std::max<int64_t>(2 * ellp * (cr + 4) * 8, dbytes);
+  while (cr > 16 && 2 * ellp * (cr + 4) * 8 > std::max<int64_t>(gbytes + dbytes, cap / 2)) cr -= 16;
+  const int64_t bytes = std::max<int64_t>(gbytes + dbytes, 2 * ellp * (cr + 4) * 8);
   if (bytes > cap) return false;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
