@@ -1119,12 +1119,25 @@ struct FcqrArgs {
 
 __device__ __forceinline__ int fq_ub(int I, int J) { return J * (J + 1) / 2 + I; }  // I <= J
 
+// CLU: the item is owned by a thread-block cluster of S CTAs that split its
+// rows; the partial Grams are summed through DSMEM in rank order (each CTA
+// reduces every S-th block into CTA 0), CTA 0 factors, and every CTA copies
+// D_J / W_IJ back from CTA 0 and applies them to its own rows -- for single
+// or few items, whose Gram and apply would otherwise run on one SM.
+template <bool CLU>
 __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_red[kFqWarps];
   __shared__ int s_rank;
   __shared__ double s_thresh;
-  const int64_t b = blockIdx.x;
+  int S = 1, q = 0;
+  int64_t b = blockIdx.x;
+  if constexpr (CLU) {
+    S = static_cast<int>(cg::this_cluster().num_blocks());
+    q = static_cast<int>(cg::this_cluster().block_rank());
+    b = blockIdx.x / S;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ell = a.ell, ellp = a.ellp, rows = a.rows, CR = a.cr, CRP = a.cr + 4;
   const int nbk = ellp / 32, nub = nbk * (nbk + 1) / 2;
@@ -1136,6 +1149,9 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   const double* Y = a.Y + b * a.sY;
   double* Q = a.Q + b * a.sQ;
   auto blk = [&](int I, int J) { return Gb + fq_ub(I, J) * kFqBlk; };
+  // this CTA's rows [row0, row0 + nrow)
+  const int rpc = ((rows + S - 1) / S + 15) & ~15;  // multiple of 16: aligned 16-byte row pairs
+  const int row0 = q * rpc, nrow = max(0, min(rows, row0 + rpc) - row0);
 
   // ---- 1. Gram (upper blocks) ------------------------------------------------
   // Up to 15 DMMA tiles (16 x 8) per warp, accumulated over all row chunks.
@@ -1146,7 +1162,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
                      ((reinterpret_cast<uintptr_t>(a.Y) & 15u) == 0);
   double* const Sbuf = sm;  // the Gram phase stages Y over the whole shared memory
   auto stage = [&](int c, int buf) {
-    const int r0 = c * CR;
+    const int r0 = row0 + c * CR;
     double* dst = Sbuf + buf * ellp * CRP;
     if (vec16) {
       const int per = CR / 2;
@@ -1155,8 +1171,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
         const int gr = r0 + r;
         int bytes = 0;
         const double* src = Y;
-        if (col < ell && gr < rows) {
-          bytes = min(16, (rows - gr) * 8);
+        if (col < ell && gr < row0 + nrow) {
+          bytes = min(16, (row0 + nrow - gr) * 8);
           src = Y + gr + static_cast<int64_t>(col) * a.ldy;
         }
         cpa16(dst + r + col * CRP, src, bytes);
@@ -1165,7 +1181,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       for (int e = tid; e < ellp * CR; e += kFqThreads) {
         const int col = e / CR, r = e - col * CR;
         const int gr = r0 + r;
-        const bool ok = col < ell && gr < rows;
+        const bool ok = col < ell && gr < row0 + nrow;
         const double* src = ok ? Y + gr + static_cast<int64_t>(col) * a.ldy : Y;
         const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + r + col * CRP));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
@@ -1175,14 +1191,14 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  const int nch = (rows + CR - 1) / CR;
+  const int nch = (nrow + CR - 1) / CR;
   constexpr int kT = 15;  // tiles per warp: 8 warps x 15 >= 8 x 15 upper blocks (l_p = 160)
   double acc[kT][4];
 #pragma unroll
   for (int u = 0; u < kT; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  stage(0, 0);
+  if (nch > 0) stage(0, 0);
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) {
       stage(c + 1, (c + 1) & 1);
@@ -1222,7 +1238,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       for (int q = 0; q < 4; ++q) {
         const int i = 16 * tm + g + ((q & 2) ? 8 : 0), j = 8 * tn + 2 * t + (q & 1);
         W[i + j * kInvPitch] = acc[u][q];
-        if (a.G0) {
+        if (!CLU && a.G0) {
           const int64_t gi = 32 * I + i, gj = 32 * J + j;
           double* G0 = a.G0 + b * static_cast<int64_t>(ellp) * ellp;
           G0[gi + gj * ellp] = acc[u][q];
@@ -1232,8 +1248,35 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     }
   }
   __syncthreads();
+  if constexpr (CLU) {
+    // Sum the S partial Grams into CTA 0, block ub by CTA ub mod S, ranks in
+    // order (bit-identical to any schedule).
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    double* G0 = a.G0 ? a.G0 + b * static_cast<int64_t>(ellp) * ellp : nullptr;
+    double* dst0 = cl.map_shared_rank(Gb, 0);
+    for (int ub = q; ub < nub; ub += S) {
+      int J = 0;
+      while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+      const int I = ub - J * (J + 1) / 2;
+      for (int e = tid; e < 1024; e += kFqThreads) {
+        const int i = e & 31, j = e >> 5;
+        const int off = ub * kFqBlk + i + j * kInvPitch;
+        double v = 0.0;
+        for (int r = 0; r < S; ++r) v += cl.map_shared_rank(Gb, r)[off];
+        dst0[off] = v;
+        if (G0) {
+          const int64_t gi = 32 * I + i, gj = 32 * J + j;
+          G0[gi + gj * ellp] = v;
+          G0[gj + gi * ellp] = v;
+        }
+      }
+    }
+    cl.sync();
+  }
 
   // ---- 2. pivot floor, rank; blocked Cholesky in shared memory ---------------
+  if (q == 0) {
   if (warp == 0) {
     double mx = 0.0;
     for (int i = lane; i < ell; i += 32) mx = fmax(mx, blk(i >> 5, i >> 5)[(i & 31) * (kInvPitch + 1)]);
@@ -1335,9 +1378,24 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     }
   }
   __syncthreads();
+  }  // q == 0
+  if constexpr (CLU) {
+    // every CTA takes D_J, W_IJ and the rank from CTA 0
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (q != 0) {
+      const double* src = cl.map_shared_rank(sm, 0);
+      for (int e = tid; e < (nub + nbk) * kFqBlk; e += kFqThreads) sm[e] = src[e];
+      if (tid == 0) s_rank = *cl.map_shared_rank(&s_rank, 0);
+    }
+    cl.sync();  // CTA 0's shared memory stays alive until every copy is done
+  }
+  const int r = s_rank;
+  const int nbr = (r + 31) / 32;
 
   // ---- 4. Q = Y R^-1, 16-row slabs per warp, block columns in order -----------
-  for (int r0 = 16 * warp; r0 < rows; r0 += 16 * kFqWarps) {
+  const int rend = row0 + nrow;
+  for (int r0 = row0 + 16 * warp; r0 < rend; r0 += 16 * kFqWarps) {
     const int ra = r0 + g, rb = r0 + g + 8;
     for (int J = 0; J < nbk; ++J) {
       double ac[4][4];
@@ -1355,8 +1413,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
         for (int kq = 0; kq < 8; ++kq) {
           const int k = 4 * kq + t;
           const bool okc = 32 * J + k < ell;
-          a0v[kq] = (okc && ra < rows) ? __ldcg(Yj + ra + static_cast<int64_t>(k) * a.ldy) : 0.0;
-          a1v[kq] = (okc && rb < rows) ? __ldcg(Yj + rb + static_cast<int64_t>(k) * a.ldy) : 0.0;
+          a0v[kq] = (okc && ra < rend) ? __ldcg(Yj + ra + static_cast<int64_t>(k) * a.ldy) : 0.0;
+          a1v[kq] = (okc && rb < rend) ? __ldcg(Yj + rb + static_cast<int64_t>(k) * a.ldy) : 0.0;
         }
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq)
@@ -1369,8 +1427,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
 #pragma unroll
           for (int kq = 0; kq < 8; ++kq) {
             const int k = 4 * kq + t;
-            a0v[kq] = ra < rows ? __ldcg(Qi + ra + static_cast<int64_t>(k) * a.ldq) : 0.0;
-            a1v[kq] = rb < rows ? __ldcg(Qi + rb + static_cast<int64_t>(k) * a.ldq) : 0.0;
+            a0v[kq] = ra < rend ? __ldcg(Qi + ra + static_cast<int64_t>(k) * a.ldq) : 0.0;
+            a1v[kq] = rb < rend ? __ldcg(Qi + rb + static_cast<int64_t>(k) * a.ldq) : 0.0;
           }
 #pragma unroll
           for (int kq = 0; kq < 8; ++kq)
@@ -1385,7 +1443,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int row = (q & 2) ? rb : ra, col = n * 8 + 2 * t + (q & 1);
-          if (row < rows) Qj[row + static_cast<int64_t>(col) * a.ldq] = (32 * J + col < r) ? ac[n][q] : 0.0;
+          if (row < rend) Qj[row + static_cast<int64_t>(col) * a.ldq] = (32 * J + col < r) ? ac[n][q] : 0.0;
         }
       __syncwarp();
       __threadfence_block();
@@ -1552,12 +1610,36 @@ bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, 
   if (bytes > cap) return false;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
-    RSVD_CUDA(cudaFuncSetAttribute(fcqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RSVD_CUDA(cudaFuncSetAttribute(fcqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(cap)));
   });
   FcqrArgs fa{Y, ldy, strideY, Q, ldq, strideQ, G0, Rf, rank, static_cast<int>(rows),
               static_cast<int>(ell), static_cast<int>(ellp), cr, tau};
-  fcqr_kernel<<<static_cast<unsigned>(batch), kFqThreads, bytes, st>>>(fa);
+  // Few items: split each item's rows over a cluster (up to 8 CTAs, >= 64 rows each).
+  int S = 1;
+  while (S < 8 && batch * S * 2 <= num_sms() && rows >= 64 * S * 2) S *= 2;
+  if (S > 1) {
+    static std::atomic<uint64_t> attr2{0};
+    once_per_device(attr2, [&] {
+      RSVD_CUDA(cudaFuncSetAttribute(fcqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(cap)));
+    });
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(S);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(batch * S));
+    cfg.blockDim = dim3(kFqThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RSVD_CUDA(cudaLaunchKernelEx(&cfg, fcqr_kernel<true>, fa));
+  } else {
+    fcqr_kernel<false><<<static_cast<unsigned>(batch), kFqThreads, bytes, st>>>(fa);
+  }
   RSVD_LAUNCH("fcqr_kernel");
   return true;
 }

@@ -370,11 +370,10 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
   const MatRef Y{Yb, rows, rows * lp}, Tm{Tmp, rows, rows * lp};
   const MatRef G{B.G, lp, lp * lp}, T{B.T, lp, lp * lp};
   Prof* P = B.prof;
-  // Batches of small real bases: one fused CholeskyQR kernel per pass
-  // (chol.cu fcqr_kernel, one CTA per item; C2 orth 5.4 -> 3.9 ms).  A few
-  // large-row items would leave most SMs idle (C1: 146 -> 219 us per pass),
-  // so those keep the GPU-wide Gram / gchol / apply sequence.
-  const bool fused = !cplx && !sharded && lp <= 160 && 2 * b >= num_sms();
+  // Small real bases: one fused CholeskyQR kernel per pass (chol.cu
+  // fcqr_kernel: one CTA per item for batches, a row-split cluster of up to 8
+  // CTAs per item for single / few items).
+  const bool fused = !cplx && !sharded && lp <= 160;
   auto gram = [&](const MatRef& in, const int* mask) {
     Scope sc(P, kStGram, st);
     GemmOpts sym;

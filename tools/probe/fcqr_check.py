@@ -2,7 +2,7 @@ import sys, os, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_1710_01463_b200 import _lib as L, tsvd
 h = L.default_handle()
-for (m, n) in [(3, 3), (4, 3), (5, 3), (7, 3), (8, 3), (9, 3), (12, 3), (16, 3), (17, 3), (24, 3), (33, 3), (40, 3), (6, 6), (10, 10)]:
+for (m, n) in [(300, 96), (300, 90), (256, 50), (600, 96), (1024, 74), (1024, 96), (301, 40), (5000, 160), (3, 3), (17, 3)]:
     rng = np.random.default_rng(m + n)
     a = rng.standard_normal((m, n))
     X = torch.from_numpy(a.T.copy()).cuda().t()
