@@ -321,7 +321,10 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
   const int64_t target = 2 * num_sms();  // two resident CTAs per SM
   int64_t splits = 1;
-  if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / 256));
+  // Few output tiles (single small matrices, C1): split K down to 64 per CTA
+  // so that the GEMM spreads over the GPU; otherwise keep >= 256 of K.
+  const int64_t kmin = (tiles * 8 <= num_sms() && K >= 1024) ? 64 : 256;
+  if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / kmin));
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
   int64_t kps = round_up(ceil_div(K, splits), kBK);
   splits = ceil_div(K, kps);
