@@ -327,6 +327,16 @@ unsigned grid1(int64_t work, int threads, int cap_per_sm = 8) {
       std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, threads), cap_per_sm * num_sms())));
 }
 
+// x-extent of a (x, batch) grid whose items usually exit at once (completion
+// of full-rank bases, masked copies, unit scales): about two CTAs per SM in
+// total instead of one per 256 elements, so the no-op case launches a few
+// hundred CTAs rather than tens of thousands.
+unsigned grid_items(int64_t work, int threads, int64_t batch, int per_sm = 2) {
+  return static_cast<unsigned>(std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(work, threads),
+                           ceil_div(static_cast<int64_t>(per_sm) * num_sms(), std::max<int64_t>(batch, 1)))));
+}
+
 }  // namespace
 
 void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
@@ -334,7 +344,7 @@ void launch_complete_basis(MatRef Q, int64_t rows, int64_t ell, const int* rank,
                            int64_t row_offset, int64_t rows_global, cudaStream_t st,
                            const int* mask) {
   if (batch <= 0 || rows <= 0) return;
-  dim3 grid(grid1(rows * ell, 256, 2), static_cast<unsigned>(batch));
+  dim3 grid(grid_items(rows * ell, 256, batch), static_cast<unsigned>(batch));
   complete_basis_kernel<<<grid, 256, 0, st>>>(Q.base, Q.ld, Q.stride, rows, ell, rank, seeds_dev,
                                               tag, row_offset, rows_global, mask);
   RSVD_LAUNCH("complete_basis_kernel");
@@ -361,7 +371,7 @@ void launch_set_identity_rect(MatRef out, int64_t rows, int64_t cols, int64_t ba
 void launch_masked_copy(const int* mask, CMatRef src, MatRef dst, int64_t rows, int64_t cols,
                         int64_t batch, cudaStream_t st) {
   if (batch <= 0 || rows <= 0 || cols <= 0) return;
-  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  dim3 grid(grid_items(rows * cols, 256, batch), static_cast<unsigned>(batch));
   masked_copy_kernel<<<grid, 256, 0, st>>>(mask, src.base, src.ld, src.stride, dst.base, dst.ld,
                                            dst.stride, rows, cols);
   RSVD_LAUNCH("masked_copy_kernel");
@@ -385,7 +395,7 @@ void launch_choose_scale(CMatRef X, int64_t rows, int64_t cols, double* scale, i
 void launch_apply_scale(MatRef X, int64_t rows, int64_t cols, const double* scale,
                         int inverse_power, int64_t batch, cudaStream_t st) {
   if (batch <= 0 || rows <= 0 || cols <= 0) return;
-  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  dim3 grid(grid_items(rows * cols, 256, batch, 8), static_cast<unsigned>(batch));
   apply_scale_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, scale,
                                            inverse_power);
   RSVD_LAUNCH("apply_scale_kernel");
@@ -423,7 +433,7 @@ void launch_gather_scale_columns(const double* src, int64_t ld_src, int64_t stri
 void launch_zero_columns_from_rank(MatRef X, int64_t rows, int64_t cols, const int* rank,
                                    int64_t batch, cudaStream_t st) {
   if (batch <= 0 || rows <= 0 || cols <= 0) return;
-  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  dim3 grid(grid_items(rows * cols, 256, batch, 4), static_cast<unsigned>(batch));
   zero_cols_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, rank);
   RSVD_LAUNCH("zero_cols_kernel");
 }
@@ -431,7 +441,7 @@ void launch_zero_columns_from_rank(MatRef X, int64_t rows, int64_t cols, const i
 void launch_zero_rows_from_rank(MatRef X, int64_t rows, int64_t cols, const int* rank,
                                 int64_t batch, cudaStream_t st) {
   if (batch <= 0 || rows <= 0 || cols <= 0) return;
-  dim3 grid(grid1(rows * cols, 256, 2), static_cast<unsigned>(batch));
+  dim3 grid(grid_items(rows * cols, 256, batch, 4), static_cast<unsigned>(batch));
   zero_rows_kernel<<<grid, 256, 0, st>>>(X.base, X.ld, X.stride, rows, cols, rank);
   RSVD_LAUNCH("zero_rows_kernel");
 }
