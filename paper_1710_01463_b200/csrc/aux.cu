@@ -117,9 +117,9 @@ __global__ void finalize_spectrum_kernel(const double* __restrict__ HJ, int64_t 
   __syncthreads();
   if (threadIdx.x == 0) {
     // sorted values, in order
-    double smax = 0.0;
-    for (int c = 0; c < ell; ++c)
-      if (s_pos[c] == 0) smax = s_sig[c];
+    // perm (global, written above by this block) maps positions to columns
+    const int* pb = perm + b * ellp;
+    const double smax = ell > 0 ? s_sig[pb[0]] : 0.0;
     int nr = 0;
     if (smax > 0.0) {
       const double cut = static_cast<double>(m > n ? m : n) * DBL_EPSILON * smax;
@@ -130,11 +130,8 @@ __global__ void finalize_spectrum_kernel(const double* __restrict__ HJ, int64_t 
     // discarded weight in descending order of the tail (as the reference's loop)
     double dw = 0.0;
     for (int pos = r; pos < ell; ++pos) {
-      for (int c = 0; c < ell; ++c)
-        if (s_pos[c] == pos) {
-          dw += s_sig[c] * s_sig[c];
-          break;
-        }
+      const double v = s_sig[pb[pos]];
+      dw += v * v;
     }
     dw_out[b] = dw;
   }

@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kCholThreads)
 // holds in a[0..31] (column c), writes R_JJ (upper) to W and Rd and its
 // inverse to Dt; returns the in-block breakdown index (32 = none).  Columns
 // at or beyond `ell` arrive as identity columns.
-__device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld, int ell, int o,
+__device__ __forceinline__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld, int ell, int o,
                                  double thresh, double* Rd, double* Dt, int lane) {
   // Cholesky of the 32 x 32 block (lane = column, a[i] = row i) and, in the
   // same sweep, Z = R^{-T} by forward substitution (lane j holds column j of
@@ -427,16 +427,21 @@ __device__ int factor_diag_block(double (&a)[32], double* __restrict__ W, int ld
       rk = (lane == k) ? 1.0 : 0.0;  // beyond the breakdown: keep R_JJ invertible
     }
     a[k] = rk;
+    // Lookahead: the next pivot (lane k + 1's a[k + 1]) is updated first
+    // from the lane's own r_k,k+1, so the pivot chain shfl -> rsqrt -> fma
+    // does not wait for the row broadcast below.
+    if (k + 1 < 32 && lane == k + 1) a[k + 1] = fma(-rk, rk, a[k + 1]);
     Rd[k * kInvPitch + lane] = rk;
     Dt[lane * kInvPitch + k] = rk;
     __syncwarp();
     const double rkm = lane > k ? rk : 0.0;
+    const double rkn = lane > k + 1 ? rk : 0.0;  // element k + 1: lane k + 1 already done
     const double2* row = reinterpret_cast<const double2*>(Rd + k * kInvPitch);
 #pragma unroll
     for (int i2 = (k + 1) / 2; i2 < 16; ++i2) {
       const double2 v = row[i2];
-      if (2 * i2 > k) a[2 * i2] = fma(-v.x, rkm, a[2 * i2]);
-      if (2 * i2 + 1 > k) a[2 * i2 + 1] = fma(-v.y, rkm, a[2 * i2 + 1]);
+      if (2 * i2 > k) a[2 * i2] = fma(-v.x, 2 * i2 == k + 1 ? rkn : rkm, a[2 * i2]);
+      if (2 * i2 + 1 > k) a[2 * i2 + 1] = fma(-v.y, 2 * i2 + 1 == k + 1 ? rkn : rkm, a[2 * i2 + 1]);
     }
     const double2* col = reinterpret_cast<const double2*>(Dt + k * kInvPitch);
     double s0 = 0.0, s1 = 0.0;
@@ -1112,6 +1117,7 @@ struct FcqrArgs {
   int64_t ldq, sQ;
   double* G0;  // full symmetric Gram (l_p x l_p, ld l_p) per item, or null
   double* Rf;  // R (l_p x l_p, ld l_p, upper, zero below / beyond rank), or null
+  double* xs;  // CLU: per item (nub + nbk) blocks of kFqBlk doubles (D_J / W_IJ exchange)
   int* rank;
   int rows, ell, ellp, cr;  // cr: staged rows per chunk (multiple of 16)
   double tau;
@@ -1124,6 +1130,19 @@ __device__ __forceinline__ int fq_ub(int I, int J) { return J * (J + 1) / 2 + I;
 // reduces every S-th block into CTA 0), CTA 0 factors, and every CTA copies
 // D_J / W_IJ back from CTA 0 and applies them to its own rows -- for single
 // or few items, whose Gram and apply would otherwise run on one SM.
+#ifdef RSVD_FCQR_TRACE
+__device__ unsigned long long g_fq_trace[64];
+#define FQ_TRACE(i)                                                                        \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_fq_trace[i] = t_;                                                                  \
+    }                                                                                      \
+  } while (0)
+#else
+#define FQ_TRACE(i) do {} while (0)
+#endif
 template <bool CLU>
 __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   namespace cg = cooperative_groups;
@@ -1152,10 +1171,9 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   // this CTA's rows [row0, row0 + nrow)
   const int rpc = ((rows + S - 1) / S + 15) & ~15;  // multiple of 16: aligned 16-byte row pairs
   const int row0 = q * rpc, nrow = max(0, min(rows, row0 + rpc) - row0);
+  FQ_TRACE(0);
 
   // ---- 1. Gram (upper blocks) ------------------------------------------------
-  // Up to 15 DMMA tiles (16 x 8) per warp, accumulated over all row chunks.
-  const int ntiles = 8 * nub;
   // 16-byte copies need 16-byte aligned columns (even ld, aligned base);
   // otherwise (odd row counts) 8-byte copies.
   const bool vec16 = (a.ldy % 2 == 0) && (a.sY % 2 == 0) &&
@@ -1192,12 +1210,23 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   const int nch = (nrow + CR - 1) / CR;
-  constexpr int kT = 15;  // tiles per warp: 8 warps x 15 >= 8 x 15 upper blocks (l_p = 160)
-  double acc[kT][4];
+  // Whole upper 32 x 32 blocks per warp (block ub = warp, warp + 8: at most 2
+  // for l_p <= 160), register-blocked like warp_mma32: per k-step 8 fragment
+  // loads feed 8 independent DMMAs (per-tile operands would need 3 loads per
+  // DMMA and leave the Gram shared-memory bound).
+  constexpr int kGB = 2;
+  int bI[kGB], bJ[kGB];
 #pragma unroll
-  for (int u = 0; u < kT; ++u)
+  for (int v = 0; v < kGB; ++v) {
+    const int ub = warp + kFqWarps * v;
+    int J = 0;
+    while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+    bJ[v] = J;
+    bI[v] = ub - J * (J + 1) / 2;
+  }
+  double acc[kGB][2][4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  for (int v = 0; v < kGB; ++v) zero_acc(acc[v]);
   if (nch > 0) stage(0, 0);
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) {
@@ -1207,44 +1236,49 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
+    if (c == 0) FQ_TRACE(14);
     const double* Yc = Sbuf + (c & 1) * ellp * CRP;
 #pragma unroll
-    for (int u = 0; u < kT; ++u) {
-      const int tt = warp + kFqWarps * u;
-      if (tt < ntiles) {
-        const int ub = tt >> 3, tm = (tt >> 2) & 1, tn = tt & 3;
-        int J = 0;
-        while ((J + 1) * (J + 2) / 2 <= ub) ++J;
-        const int I = ub - J * (J + 1) / 2;
-        const double* ap0 = Yc + (32 * I + 16 * tm + g) * CRP + t;
-        const double* ap1 = ap0 + 8 * CRP;
-        const double* bp = Yc + (32 * J + 8 * tn + g) * CRP + t;
-#pragma unroll 4
-        for (int k0 = 0; k0 < CR; k0 += 4) dmma_16x8x4(acc[u], ap0[k0], ap1[k0], bp[k0]);
+    for (int v = 0; v < kGB; ++v) {
+      if (warp + kFqWarps * v < nub) {
+        const double* Ab = Yc + (32 * bI[v] + g) * CRP + t;
+        const double* Bb = Yc + (32 * bJ[v] + g) * CRP + t;
+#pragma unroll 2
+        for (int k0 = 0; k0 < CR; k0 += 4) {
+          double av[2][2], bv[4];
+#pragma unroll
+          for (int a2 = 0; a2 < 2; ++a2) {
+            av[a2][0] = Ab[(16 * a2) * CRP + k0];
+            av[a2][1] = Ab[(16 * a2 + 8) * CRP + k0];
+          }
+#pragma unroll
+          for (int n = 0; n < 4; ++n) bv[n] = Bb[(8 * n) * CRP + k0];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            dmma_16x8x4(acc[v][0][n], av[0][0], av[0][1], bv[n]);
+            dmma_16x8x4(acc[v][1][n], av[1][0], av[1][1], bv[n]);
+          }
+        }
       }
     }
     __syncthreads();  // buffer c & 1 is restaged at c + 2; the last one frees the G blocks
+    if (c == 0) FQ_TRACE(15);
   }
 #pragma unroll
-  for (int u = 0; u < kT; ++u) {
-    const int tt = warp + kFqWarps * u;
-    if (tt < ntiles) {
-      const int ub = tt >> 3, tm = (tt >> 2) & 1, tn = tt & 3;
-      int J = 0;
-      while ((J + 1) * (J + 2) / 2 <= ub) ++J;
-      const int I = ub - J * (J + 1) / 2;
+  for (int v = 0; v < kGB; ++v) {
+    const int ub = warp + kFqWarps * v;
+    if (ub < nub) {
       double* W = Gb + ub * kFqBlk;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = 16 * tm + g + ((q & 2) ? 8 : 0), j = 8 * tn + 2 * t + (q & 1);
-        W[i + j * kInvPitch] = acc[u][q];
-        if (!CLU && a.G0) {
+      double* G0 = (!CLU && a.G0) ? a.G0 + b * static_cast<int64_t>(ellp) * ellp : nullptr;
+      const int I = bI[v], J = bJ[v];
+      store_acc(acc[v], [&](int i, int j, double x) {
+        W[i + j * kInvPitch] = x;
+        if (G0) {
           const int64_t gi = 32 * I + i, gj = 32 * J + j;
-          double* G0 = a.G0 + b * static_cast<int64_t>(ellp) * ellp;
-          G0[gi + gj * ellp] = acc[u][q];
-          G0[gj + gi * ellp] = acc[u][q];
+          G0[gi + gj * ellp] = x;
+          G0[gj + gi * ellp] = x;
         }
-      }
+      }, g, t);
     }
   }
   __syncthreads();
@@ -1274,6 +1308,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     }
     cl.sync();
   }
+  FQ_TRACE(2);
 
   // ---- 2. pivot floor, rank; blocked Cholesky in shared memory ---------------
   if (q == 0) {
@@ -1306,6 +1341,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   };
   if (warp == 0 && s_rank > 0) factor(0);
   __syncthreads();
+  FQ_TRACE(3);
   for (int J = 0; J < nbk; ++J) {
     if (s_rank < 32 * (J + 1)) break;  // broke down in or before block J
     const int nr = nbk - J - 1;
@@ -1346,7 +1382,9 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       }
     }
     __syncthreads();
+    FQ_TRACE(4 + J);
   }
+  FQ_TRACE(10);
   const int r = s_rank;
   const int nbr = (r + 31) / 32;  // block columns with live R / D
 
@@ -1378,17 +1416,38 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
     }
   }
   __syncthreads();
+  FQ_TRACE(11);
   }  // q == 0
   if constexpr (CLU) {
-    // every CTA takes D_J, W_IJ and the rank from CTA 0
+    // Every CTA takes D_J, W_IJ (I < J) and the rank from CTA 0 through L2:
+    // CTA 0 writes them to xs, the others stage them back with 16-byte
+    // cp.async (reading them through DSMEM serialises on CTA 0's SM).
     cg::cluster_group cl = cg::this_cluster();
+    constexpr int per = kFqBlk / 2;
+    const int nw = nbk * (nbk - 1) / 2, nblk = nw + nbk;
+    auto off = [&](int e) {  // e-th double2 of the exchange -> its shared-memory index
+      const int bi = e / per, w = e - bi * per;
+      if (bi < nw) {
+        int I = bi, J = 1;
+        while (I >= J) I -= J++;
+        return fq_ub(I, J) * per + w;
+      }
+      return (nub + bi - nw) * per + w;
+    };
+    double2* xg = reinterpret_cast<double2*>(a.xs + b * static_cast<int64_t>(nub + nbk) * kFqBlk);
+    if (q == 0) {
+      const double2* s2 = reinterpret_cast<const double2*>(sm);
+      for (int e = tid; e < nblk * per; e += kFqThreads) __stcg(xg + e, s2[off(e)]);
+      __threadfence();
+    }
     cl.sync();
     if (q != 0) {
-      const double* src = cl.map_shared_rank(sm, 0);
-      for (int e = tid; e < (nub + nbk) * kFqBlk; e += kFqThreads) sm[e] = src[e];
+      for (int e = tid; e < nblk * per; e += kFqThreads) cpa16(sm + 2 * off(e), xg + e, 16);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
       if (tid == 0) s_rank = *cl.map_shared_rank(&s_rank, 0);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    cl.sync();  // CTA 0's shared memory stays alive until every copy is done
+    cl.sync();  // CTA 0's s_rank stays alive until every CTA has read it
   }
   const int r = s_rank;
   const int nbr = (r + 31) / 32;
@@ -1449,6 +1508,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
       __threadfence_block();
     }
   }
+  FQ_TRACE(13);
 }
 
 }  // namespace
@@ -1461,6 +1521,10 @@ bool panel_in_global(int64_t ellp) {
   const int64_t big = std::max<int64_t>(PB * (ellp + 20), kInvSmem);
   return big * 8 + 3 * ellp * 8 + 2 * ellp * 4 + 64 > kSmemCap ||
          big * 8 + 2 * 32 * kInvPitch * 8 + 64 > kSmemCap;
+}
+int64_t fcqr_xscratch_elems(int64_t ellp, int64_t batch) {
+  const int64_t nbk = ellp / 32;
+  return (nbk * (nbk + 1) / 2 + nbk) * kFqBlk * batch;
 }
 int64_t pchol_scratch_elems(int64_t ellp, int64_t batch) {
   return 2 * ellp * ellp * batch + (panel_in_global(ellp) ? batch * PB * (ellp + 20) : 0);
@@ -1593,8 +1657,9 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 // Fused CholeskyQR pass (fcqr_kernel) for l_p <= 160; false when it does not
 // apply (the caller runs the unfused Gram / gchol / apply sequence).
 bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
-                      int64_t strideQ, double* G0, double* Rf, int* rank, int64_t rows,
-                      int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st) {
+                      int64_t strideQ, double* G0, double* Rf, double* xscratch, int* rank,
+                      int64_t rows, int64_t ell, int64_t ellp, double tau, int64_t batch,
+                      cudaStream_t st) {
   if (batch <= 0) return true;
   if (ellp % 32 != 0 || ellp > 160 || rows < 1 || rows > (1 << 30)) return false;
   const int64_t nbk = ellp / 32, nub = nbk * (nbk + 1) / 2;
@@ -1613,11 +1678,11 @@ bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, 
     RSVD_CUDA(cudaFuncSetAttribute(fcqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(cap)));
   });
-  FcqrArgs fa{Y, ldy, strideY, Q, ldq, strideQ, G0, Rf, rank, static_cast<int>(rows),
+  FcqrArgs fa{Y, ldy, strideY, Q, ldq, strideQ, G0, Rf, xscratch, rank, static_cast<int>(rows),
               static_cast<int>(ell), static_cast<int>(ellp), cr, tau};
   // Few items: split each item's rows over a cluster (up to 8 CTAs, >= 64 rows each).
   int S = 1;
-  while (S < 8 && batch * S * 2 <= num_sms() && rows >= 64 * S * 2) S *= 2;
+  while (xscratch && S < 8 && batch * S * 2 <= num_sms() && rows >= 64 * S * 2) S *= 2;
   if (S > 1) {
     static std::atomic<uint64_t> attr2{0};
     once_per_device(attr2, [&] {

@@ -150,9 +150,13 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 // breakdown -> rank, Q = Y R^-1): Q columns >= rank are zero (completion is the
 // caller's); G0 (full symmetric Gram) and Rf (R, zero below / beyond rank) are
 // written when non-null.  Returns false when the shape does not qualify.
+// xscratch: fcqr_xscratch_elems(ellp, batch) doubles (row-split cluster mode;
+// null disables it).
 bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
-                      int64_t strideQ, double* G0, double* Rf, int* rank, int64_t rows,
-                      int64_t ell, int64_t ellp, double tau, int64_t batch, cudaStream_t st);
+                      int64_t strideQ, double* G0, double* Rf, double* xscratch, int* rank,
+                      int64_t rows, int64_t ell, int64_t ellp, double tau, int64_t batch,
+                      cudaStream_t st);
+int64_t fcqr_xscratch_elems(int64_t ellp, int64_t batch);
 
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.

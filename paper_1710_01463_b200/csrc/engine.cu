@@ -307,7 +307,9 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   B.T = c.take<double>(b * lp * lp);
   B.Rf1 = c.take<double>(b * lp * lp);
   B.Rf2 = c.take<double>(b * lp * lp);
-  B.cscratch = c.take<double>(pchol_scratch_elems(lp, b));
+  // Cholesky scratch; also the fused CholeskyQR's cluster exchange (l_p <= 160)
+  B.cscratch = c.take<double>(std::max(pchol_scratch_elems(lp, b),
+                                       lp <= 160 ? fcqr_xscratch_elems(lp, b) : int64_t(0)));
   B.rank1 = c.take<int>(b);
   B.rank2 = c.take<int>(b);
   B.perm = c.take<int>(b * lp);
@@ -417,7 +419,8 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
       {
         Scope sc(P, kStChol, st);
         if (!launch_fused_cqr(in.base, rows, rows * lp, out.base, rows, rows * lp,
-                              pass == 0 ? B.G0 : nullptr, Rf, rk, rows, s.ell, lp, kPivotTau, b, st))
+                              pass == 0 ? B.G0 : nullptr, Rf, B.cscratch, rk, rows, s.ell, lp, kPivotTau,
+                              b, st))
           throw CudaError("orth: fused CholeskyQR does not fit this shape");
         if (pass == 0) shifted_retry();
       }

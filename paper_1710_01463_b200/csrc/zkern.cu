@@ -450,9 +450,9 @@ __global__ void zfinalize_kernel(const double2* __restrict__ W, int64_t lp, int 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double smax = 0.0;
-    for (int c = 0; c < ell; ++c)
-      if (s_pos[c] == 0) smax = s_sig[c];
+    // perm (global, written above by this block) maps positions to columns
+    const int* pb = perm + b * lp;
+    const double smax = ell > 0 ? s_sig[pb[0]] : 0.0;
     int nr = 0;
     if (smax > 0.0) {
       const double cut = static_cast<double>(m > n ? m : n) * DBL_EPSILON * smax;
@@ -461,12 +461,10 @@ __global__ void zfinalize_kernel(const double2* __restrict__ W, int64_t lp, int 
     const int r = static_cast<int>(nr < k ? nr : k);
     rank_out[b] = r;
     double dw = 0.0;
-    for (int pos = r; pos < ell; ++pos)
-      for (int c = 0; c < ell; ++c)
-        if (s_pos[c] == pos) {
-          dw += s_sig[c] * s_sig[c];
-          break;
-        }
+    for (int pos = r; pos < ell; ++pos) {
+      const double v = s_sig[pb[pos]];
+      dw += v * v;
+    }
     dw_out[b] = dw;
   }
   __syncthreads();
