@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(512, 1)
           const int p = rr_player(k, phase - 1, nb), qq = rr_player(nb - 1 - k, phase - 1, nb);
           bp = min(p, qq), bq = max(p, qq);
         }
-        if (bp * W >= ell) continue;
+        // a block-pair task whose second block is all padding has no pair
+        // that can rotate (and intra-block pairs belong to the diagonal phase)
+        if (bp * W >= ell || (!diag && bq * W >= ell)) continue;
         double* Hg = H + item * sq;
         double* Jg = J + item * sq;
         auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
@@ -199,13 +201,17 @@ __global__ void __launch_bounds__(512, 1)
         __syncthreads();
         if (warp < 8) {  // partial Gram of the local rows (DMMA)
           const int tm = warp >> 2, tn = warp & 3;
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          double acc[4] = {0.0, 0.0, 0.0, 0.0}, acc2[4] = {0.0, 0.0, 0.0, 0.0};
           const double* a0p = Hs + (16 * tm + g) * PITCH;
           const double* a1p = Hs + (16 * tm + g + 8) * PITCH;
           const double* b0p = Hs + (8 * tn + g) * PITCH;
-#pragma unroll 8
-          for (int k0 = 0; k0 < ROWS; k0 += 4)
+#pragma unroll 4
+          for (int k0 = 0; k0 < ROWS; k0 += 8) {  // two accumulators: half the DMMA chain
             dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+            dmma_16x8x4(acc2, a0p[k0 + 4 + t4], a1p[k0 + 4 + t4], b0p[k0 + 4 + t4]);
+          }
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) acc[qq] += acc2[qq];
           const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
           Gp[r0 + c0 * GP] = acc[0];
           Gp[r0 + (c0 + 1) * GP] = acc[1];
@@ -453,6 +459,27 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
 // friendly).  Workspace (jacobi_flag_elems): per item 3 rotating "rotated"
 // flags, 3 rotating "big rotation" flags, a completion counter and a
 // converged flag; then the task counter and the converged-item count.
+#ifdef RSVD_JDF_TRACE
+// Phase sums of CTA 0 (ns): pull + dependency wait, Gram, rotation steps,
+// X/J update, bookkeeping; task count (tools/probe/jdf_trace.cu).
+__device__ unsigned long long g_jdf_trace[8];
+__device__ __forceinline__ unsigned long long jdf_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define JDF_MARK(slot)                                         \
+  do {                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                 \
+      const unsigned long long n_ = jdf_now();                 \
+      jdf_acc[slot] += n_ - jdf_last;                          \
+      jdf_last = n_;                                           \
+    }                                                          \
+  } while (0)
+#else
+#define JDF_MARK(slot) do {} while (0)
+#endif
+
 template <int RC, int MINB>
 __global__ void __launch_bounds__(256, MINB)
     jacobi_df_kernel(double* __restrict__ H, double* __restrict__ J, int ell, int ellp, int nb,
@@ -486,6 +513,10 @@ __global__ void __launch_bounds__(256, MINB)
   const int64_t per_phase = batch * half;
   const int64_t total = static_cast<int64_t>(max_sweeps) * nb * per_phase;
   const int slabs = (ell + 15) / 16;
+#ifdef RSVD_JDF_TRACE
+  unsigned long long jdf_acc[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long jdf_last = jdf_now();
+#endif
   for (;;) {
     if (tid == 0) {
       long long t = -1;
@@ -538,14 +569,20 @@ __global__ void __launch_bounds__(256, MINB)
         fl3[slot * batch + item] = 0u;
         mx3[slot * batch + item] = 0ull;
       }
-      if (work == 1 && bp * W >= ell) work = 0;
+      // a block-pair task whose second block is all padding has no pair that
+      // can rotate (intra-block pairs belong to the diagonal phase)
+      if (work == 1 && (bp * W >= ell || (!diag && bq * W >= ell))) work = 0;
       s_work = work;
       s_rot = 0;
       s_mx = 0ull;
     }
     __syncthreads();
+    JDF_MARK(0);
     const int work = s_work;
     if (work == 1) {
+#ifdef RSVD_JDF_TRACE
+      if (blockIdx.x == 0 && threadIdx.x == 0) jdf_acc[5] += 1;
+#endif
       double* Hg = H + item * sq;
       double* Jg = J + item * sq;
       auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };
@@ -571,7 +608,8 @@ __global__ void __launch_bounds__(256, MINB)
       }
       // ---- G = X^T X over row chunks (cp.async double buffer, DMMA) ----
       const int tm = warp >> 2, tn = warp & 3;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      // two accumulators (even / odd k-steps): half the dependent DMMA chain
+      double acc[4] = {0.0, 0.0, 0.0, 0.0}, acc2[4] = {0.0, 0.0, 0.0, 0.0};
       stage(0, 0);
       for (int c = 0; c < nch; ++c) {
         if (c + 1 < nch) {
@@ -585,11 +623,15 @@ __global__ void __launch_bounds__(256, MINB)
         const double* a0p = Xb + (16 * tm + g) * PITCH;
         const double* a1p = Xb + (16 * tm + g + 8) * PITCH;
         const double* b0p = Xb + (8 * tn + g) * PITCH;
-#pragma unroll 8
-        for (int k0 = 0; k0 < RC; k0 += 4)
+#pragma unroll 4
+        for (int k0 = 0; k0 < RC; k0 += 8) {
           dmma_16x8x4(acc, a0p[k0 + t4], a1p[k0 + t4], b0p[k0 + t4]);
+          dmma_16x8x4(acc2, a0p[k0 + 4 + t4], a1p[k0 + 4 + t4], b0p[k0 + 4 + t4]);
+        }
         __syncthreads();  // buffer c & 1 is restaged at c + 2
       }
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) acc[qq] += acc2[qq];
       {
         const int r0 = 16 * tm + g, c0 = 8 * tn + 2 * t4;
         Gs[r0 + c0 * GP] = acc[0];
@@ -598,6 +640,7 @@ __global__ void __launch_bounds__(256, MINB)
         Gs[r0 + 8 + (c0 + 1) * GP] = acc[3];
       }
       __syncthreads();
+      JDF_MARK(1);
       // ---- rotation steps on G and V ----
       // A step's 16 disjoint pairs act on G as G <- R^T G R with R a
       // permuted direct sum of 2 x 2 rotations, so every 2 x 2 block
@@ -699,6 +742,7 @@ __global__ void __launch_bounds__(256, MINB)
         if (big) atomicMax(&s_mx, 1ull);
       }
       __syncthreads();
+      JDF_MARK(2);
       if (s_rot) {
         // ---- X <- X V and J <- J V, in place, 16-row slab per warp ----
         for (int job = warp; job < 2 * slabs; job += NW) {
@@ -733,6 +777,7 @@ __global__ void __launch_bounds__(256, MINB)
         }
       }
       __syncthreads();
+      JDF_MARK(3);
       if (tid == 0 && s_rot) {
         const int slot = sweep % 3;
         atomicOr(fl3 + slot * batch + item, 1u);
@@ -743,7 +788,12 @@ __global__ void __launch_bounds__(256, MINB)
       __threadfence();
       atomicAdd(cnt + item, 1u);
     }
+    JDF_MARK(4);
   }
+#ifdef RSVD_JDF_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 0; i < 6; ++i) g_jdf_trace[i] = jdf_acc[i];
+#endif
 }
 
 // J = I per item, sweeps = max_sweeps (overwritten on convergence), flags,

@@ -699,7 +699,9 @@ __global__ void __launch_bounds__(512, MINB)
           const int p = zrr(k, phase - 1, nb), q = zrr(nb - 1 - k, phase - 1, nb);
           bp = min(p, q), bq = max(p, q);
         }
-        if (bp * W >= ell) continue;
+        // a block-pair task whose second block is all padding has no pair
+        // that can rotate (intra-block pairs belong to the diagonal phase)
+        if (bp * W >= ell || (!diag && bq * W >= ell)) continue;
         double2* Hg = H + item * sq;
         double2* Jg = J + item * sq;
         auto gcol = [&](int c) { return c < W ? bp * W + c : bq * W + (c - W); };

@@ -57,8 +57,7 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
   }
   unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #ifdef RSVD_JDF_TRACE
-  if (which == 0) cudaMemcpyFromSymbol(tr, g_dfw_trace, sizeof(tr));
-  else cudaMemcpyFromSymbol(tr, g_jdf_trace, sizeof(tr));
+  cudaMemcpyFromSymbol(tr, g_jdf_trace, sizeof(tr));
 #endif
   int sw = 0;
   cudaMemcpy(&sw, sweeps, 4, cudaMemcpyDeviceToHost);
@@ -104,12 +103,8 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
 
 int main() {
   run(138, 160, 256, 5, 0);  // C2
-  run(138, 160, 256, 5, 1);
   run(276, 288, 32, 5, 0);   // C4
-  run(276, 288, 32, 5, 2);
   run(138, 160, 64, 5, 0);
-  run(138, 160, 64, 5, 1);
   run(40, 64, 512, 5, 0);
-  run(40, 64, 512, 5, 2);
   return 0;
 }
