@@ -702,7 +702,11 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   Carver cv{h->arena.base};
   layout(cv);
   cudaStream_t cs[4] = {st, h->s_c2, h->s_c3, h->s_c4};
-  constexpr int nstreams = 3;  // 3 compute streams measured best on C4 (2: 295, 3: 319 trunc/s)
+  // 3 compute streams measured best on C4 (2: 295, 3: 319 trunc/s); uneven
+  // chunk sizes (small first / last chunks) and 4 streams measured no better
+  // (100.5-103.5 ms against 100.9 per call): the chunked GPU work, not the
+  // pipeline fill, is the limit (tools/probe/e2e_probe.py).
+  constexpr int nstreams = 3;
   // Order the side streams after whatever the caller queued on its stream.
   RSVD_CUDA(cudaEventRecord(h->ev_in, st));
   RSVD_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_in, 0));
@@ -717,10 +721,19 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                h->s_in);
     RSVD_CUDA(cudaEventRecord(h->ev_slot_in[c], h->s_in));
   }
+#ifdef RSVD_PIPE_TRACE
+  // Timeline of the chunks (make EXTRA=-DRSVD_PIPE_TRACE; tools/probe/e2e_probe.py).
+  std::vector<cudaEvent_t> tev(4 * nchunks + 1);
+  for (auto& e : tev) cudaEventCreate(&e);
+  cudaEventRecord(tev[0], h->s_in);
+#endif
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t b0 = off[c], nb = sizes[c];
     cudaStream_t q = cs[c % nstreams];
     RSVD_CUDA(cudaStreamWaitEvent(q, h->ev_slot_in[c], 0));
+#ifdef RSVD_PIPE_TRACE
+    cudaEventRecord(tev[1 + 4 * c], q);
+#endif
     Shape s = sc;
     s.batch = nb;
     Buffers Bq = B[c];
@@ -730,7 +743,13 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                               cudaMemcpyHostToDevice, q));
     const CMatRef Ad{Ah[c], m, m * n};
     range_finder(s, Bq, Ad, q);
+#ifdef RSVD_PIPE_TRACE
+    cudaEventRecord(tev[2 + 4 * c], q);
+#endif
     svd_stage(s, Bq, Ad, MatRef{Uh[c], m, m * k}, Sh[c], k, MatRef{Vh[c], k, k * n}, q);
+#ifdef RSVD_PIPE_TRACE
+    cudaEventRecord(tev[3 + 4 * c], q);
+#endif
     RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + b0, B[c].rankF, sizeof(int) * nb,
                               cudaMemcpyDeviceToHost, q));
     RSVD_CUDA(cudaMemcpyAsync(h->pin.ints + batch + b0, B[c].sweeps, sizeof(int) * nb,
@@ -745,8 +764,21 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
                cudaMemcpyDeviceToHost, h->s_out);
     copy_batch(S + b0 * strideS, k, strideS, Sh[c], k, k, k, 1, nb, cudaMemcpyDeviceToHost,
                h->s_out);
+#ifdef RSVD_PIPE_TRACE
+    cudaEventRecord(tev[4 + 4 * c], h->s_out);
+#endif
   }
   RSVD_CUDA(cudaStreamSynchronize(h->s_out));
+#ifdef RSVD_PIPE_TRACE
+  cudaDeviceSynchronize();
+  for (int64_t c = 0; c < nchunks; ++c) {
+    float t[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[1 + 4 * c + i]);
+    std::fprintf(stderr, "chunk %lld (%lld items): in %.1f  range %.1f  svd %.1f  out %.1f ms\n",
+                 static_cast<long long>(c), static_cast<long long>(sizes[c]), t[0], t[1], t[2], t[3]);
+  }
+  for (auto& e : tev) cudaEventDestroy(e);
+#endif
   RSVD_CUDA(cudaStreamSynchronize(st));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c2));
   RSVD_CUDA(cudaStreamSynchronize(h->s_c3));
