@@ -824,6 +824,23 @@ __device__ void gc_factor_diag(const GcholArgs& a, int64_t b, int J, double* Rd,
 // = item, block barriers only, no co-residency needed) -- for small l_p,
 // where an item's whole factorization is a few dozen warp tasks and the
 // grid / cluster barriers would dominate.
+#ifdef RSVD_GCHOL_TRACE
+// %globaltimer stamps of CTA 0, thread 0: [0] start, [1] before block 0's
+// factor, [2 + 2 J] phase B of block J starts, [3 + 2 J] phase C starts
+// (tools/probe/gchol_trace.cu).
+__device__ unsigned long long g_gc_trace[160];
+#define GC_TRACE(i)                                                                        \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 160) {                               \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_gc_trace[i] = t_;                                                                  \
+    }                                                                                      \
+  } while (0)
+#else
+#define GC_TRACE(i) do {} while (0)
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_in) {
   namespace cg = cooperative_groups;
@@ -863,6 +880,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
   const int64_t sq = static_cast<int64_t>(ld) * ld;
   const int64_t batch = a.batch;
   const int nb = (ell + 31) / 32;
+  GC_TRACE(0);
   const int64_t gw = static_cast<int64_t>(cta) * kGcWarps + warp;
   const int64_t nw = static_cast<int64_t>(ncta) * kGcWarps;
   const int64_t gtid = static_cast<int64_t>(cta) * blockDim.x + tid;
@@ -893,16 +911,18 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
     go_of(b)[0] = go ? 1.0 : 0.0;
   }
   grid.sync();
-  // Per item (flag read once), 16-byte stores: sq is a multiple of 1024.
-  for (int64_t b = cta; b < batch; b += ncta) {
+  // Per item (flag read once), 16-byte stores (sq is a multiple of 1024),
+  // spread over the whole grid: one CTA per item left single matrices with
+  // ~40 us of zeroing on one SM (l_p = 544).
+  for (int64_t b = 0; b < batch; ++b) {
     if (go_of(b)[0] == 0.0) continue;
     double2* t2 = reinterpret_cast<double2*>(a.T + b * sq);
     const double2 z = make_double2(0.0, 0.0);
-    for (int64_t e = tid; e < sq / 2; e += blockDim.x) t2[e] = z;
+    for (int64_t e = gtid; e < sq / 2; e += gstride) t2[e] = z;
     if (a.o.Gsrc) {
       const double2* s2 = reinterpret_cast<const double2*>(a.o.Gsrc + b * sq);
       double2* g2 = reinterpret_cast<double2*>(a.G + b * sq);
-      for (int64_t e = tid; e < sq / 2; e += blockDim.x) g2[e] = s2[e];
+      for (int64_t e = gtid; e < sq / 2; e += gstride) g2[e] = s2[e];
     }
   }
   grid.sync();
@@ -939,6 +959,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
   // Items whose diagonal factorizations this warp owns.
   const int64_t d0 = static_cast<int64_t>(cta) + static_cast<int64_t>(warp) * ncta;
   const int64_t dstep = static_cast<int64_t>(ncta) * kGcDiagWarps;
+  GC_TRACE(1);
   if (diag_warp)
     for (int64_t b = d0; b < batch; b += dstep)
       if (go_of(b)[0] != 0.0 && a.rank[b] > 0) gc_factor_diag(a, b, 0, Rd, Dt, lane);
@@ -949,6 +970,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
   for (int J = 0; J < nb; ++J) {
     const int o = J * 32;
     const int nr = nb - J - 1;  // blocks right of J
+    GC_TRACE(2 + 2 * J);
     // ---- Phase B ----------------------------------------------------------
     {
       const int per = nr + J;
@@ -990,6 +1012,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
       }
     }
     grid.sync();
+    GC_TRACE(3 + 2 * J);
     if (nr == 0) break;
     // ---- Phase C (+ lookahead factor of block J+1) -----------------------
     if (diag_warp) {

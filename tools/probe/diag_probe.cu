@@ -60,6 +60,20 @@ __global__ void kdiag(const double* G, double* out, long long* cyc, int mode, in
   out[lane] = acc;
 }
 
+__global__ void kcheck(const double* G, double* Rout, double* Dout) {
+  __shared__ double W[32 * kInvPitch], Rd[32 * kInvPitch], Dt[32 * kInvPitch];
+  const int lane = threadIdx.x;
+  double a[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = G[i + lane * 32];
+  factor_diag_block(a, W, kInvPitch, 32, 0, 1e-300, Rd, Dt, lane);
+  __syncwarp();
+  for (int i = 0; i < 32; ++i) {
+    Rout[i + lane * 32] = i <= lane ? W[i + lane * kInvPitch] : 0.0;
+    Dout[i + lane * 32] = Dt[i * kInvPitch + lane];  // D(i, lane)
+  }
+}
+
 __global__ void klat(double x0, double* out, long long* cyc) {
   __shared__ double sh[64];
   const int lane = threadIdx.x;
@@ -121,6 +135,29 @@ int main() {
   cudaMalloc(&dout, 32 * 8);
   cudaMalloc(&dc, 8);
   cudaMemcpy(dG, G.data(), 32 * 32 * 8, cudaMemcpyHostToDevice);
+  {  // check: R^T R = G and R D = I for the factor_diag_block outputs
+    double *dW, *dD;
+    cudaMalloc(&dW, 32 * 32 * 8);
+    cudaMalloc(&dD, 32 * 32 * 8);
+    kcheck<<<1, 32>>>(dG, dW, dD);
+    cudaDeviceSynchronize();
+    std::vector<double> R(1024), D(1024);
+    cudaMemcpy(R.data(), dW, 1024 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(D.data(), dD, 1024 * 8, cudaMemcpyDeviceToHost);
+    double e1 = 0, e2 = 0, gmax = 0;
+    for (int i = 0; i < 32; ++i)
+      for (int j = 0; j < 32; ++j) {
+        double s1 = 0, s2 = 0;
+        for (int k = 0; k < 32; ++k) {
+          s1 += (k <= i ? R[k + i * 32] : 0) * (k <= j ? R[k + j * 32] : 0);
+          s2 += (k >= i ? R[i + k * 32] : 0) * D[k + j * 32];
+        }
+        gmax = std::max(gmax, std::fabs(G[i + j * 32]));
+        e1 = std::max(e1, std::fabs(s1 - G[i + j * 32]));
+        e2 = std::max(e2, std::fabs(s2 - (i == j ? 1.0 : 0.0)));
+      }
+    printf("maxerr |R^T R - G|/max|G| %.2e, |R D - I| %.2e\n", e1 / gmax, e2);
+  }
   for (int mode = 0; mode < 2; ++mode) {
     kdiag<<<1, 32>>>(dG, dout, dc, mode, 20);
     cudaDeviceSynchronize();
