@@ -249,7 +249,7 @@ __global__ void hermitize_kernel(double* __restrict__ G, int64_t lp, const int* 
 // h_q' = s e h_p + c h_q; J accumulates the same unitary 2 x 2.  Rotation test
 // |gamma| > sqrt(l) eps sqrt(alpha beta) (dgesvj's); round-robin ordering,
 // every pair once per sweep; stops after a sweep with no rotation or whose
-// largest rotated ratio was below 1e-9 (quadratic convergence).
+// largest rotated ratio was below 1e-7 (quadratic convergence).
 // Each item is owned by a thread-block cluster of S CTAs (S = 1 for large
 // batches): the l/2 disjoint pairs of a round-robin step are spread over the
 // S x 16 warps, one cluster barrier per step; H and J live in global scratch
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(512) zjacobi_kernel(const double* __restrict__
     sync_all();
     if (tid == 0) s_max = 0ull, s_rot = 0;
     sync_all();
-    if (!any || mx < 1e-9) {
+    if (!any || mx < 1e-7) {
       ++sweep;
       break;
     }
@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(512, MINB)
           const bool rot = al > 0.0 && be > 0.0 && gg > tol2 * ab;
           double c = 1.0, sn = 0.0, tt = 0.0, gm = 0.0, er = 1.0, ei = 0.0;
           if (rot) {
-            big |= gg >= 1e-18 * ab;
+            big |= gg >= 1e-14 * ab;
             gm = sqrt(gg);
             er = ga.x / gm, ei = ga.y / gm;
             const double d = be - al, g2 = 2.0 * gm;
