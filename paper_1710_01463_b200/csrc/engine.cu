@@ -653,8 +653,10 @@ int64_t host_chunks(int64_t batch, int64_t m, int64_t n) {
   // Each chunk has its own staging, so the H2D stream never waits for a slot.
   // C4 (4.3 GB): 7 chunks (5,5,5,5,5,5,2) on three compute streams measured
   // 319 trunc/s against 295 for 4 chunks on two (tools/probe/e2e_probe.py).
+  // C2 (256 x 256^2, 134 MB): 2 chunks 18.7k trunc/s against 16.0k unchunked
+  // (3: 18.4k, 4: 15.6k).
   const int64_t per = m * n * 8;
-  if (batch < 2 || per * batch < (int64_t(256) << 20)) return 1;
+  if (batch < 2 || per * batch < (int64_t(64) << 20)) return 1;
   const int64_t by_size = std::max<int64_t>(1, per * batch / (int64_t(512) << 20));
   return std::max<int64_t>(2, std::min<int64_t>({by_size, batch, 7}));
 }

@@ -53,6 +53,23 @@ static void run(int ell, int ellp, int batch, int reps) {
     cudaEventElapsedTime(&ms, e0, e1);
     if (r >= 2) tot += ms;
   }
+  {  // item `batch - 1`: R^T R = G0 and R T = I (upper parts)
+    const size_t off = sq * (batch - 1);
+    std::vector<double> R(sq), Tm(sq);
+    cudaMemcpy(R.data(), G + off, sq * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(Tm.data(), T + off, sq * 8, cudaMemcpyDeviceToHost);
+    double e1 = 0, e2 = 0, gm = 0;
+    for (int i = 0; i < ell; ++i)
+      for (int j = i; j < ell; ++j) {
+        double s1 = 0, s2 = 0;
+        for (int k = 0; k <= i; ++k) s1 += R[k + i * ellp] * R[k + j * ellp];
+        for (int k = i; k <= j; ++k) s2 += R[i + k * ellp] * Tm[k + j * ellp];
+        gm = std::max(gm, std::fabs(h[off + i + j * ellp]));
+        e1 = std::max(e1, std::fabs(s1 - h[off + i + j * ellp]));
+        e2 = std::max(e2, std::fabs(s2 - (i == j ? 1.0 : 0.0)));
+      }
+    printf("   check: |R^T R - G|/max|G| %.2e, |R T - I| %.2e\n", e1 / gm, e2);
+  }
   unsigned long long tr[160];
   cudaMemcpyFromSymbol(tr, g_gc_trace, sizeof(tr));
   int rk = 0;
@@ -84,5 +101,6 @@ int main() {
   run(544, 544, 1, 5);   // C5
   run(276, 288, 32, 5);  // C4
   run(276, 288, 5, 5);   // C4 host chunk
+  run(90, 96, 3, 5);     // one CTA per item (MODE 2)
   return 0;
 }
