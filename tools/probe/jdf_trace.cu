@@ -9,6 +9,7 @@
 #endif
 
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 #include <vector>
 
@@ -44,7 +45,7 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
   for (int r = 0; r < reps + 2; ++r) {
     cudaMemcpyAsync(H, H0, n * 8, cudaMemcpyDeviceToDevice, st);
     cudaEventRecord(e0, st);
-    if (which == 0) launch_jacobi(H, J, ell, ellp, 30, sweeps, flags, batch, st);
+    if (which == 0 || which == 3) launch_jacobi(H, J, ell, ellp, 30, sweeps, flags, batch, st);
 #ifndef JSRC
     else if (which == 1) launch_df_t<144, 4>(H, J, ell, ellp, 30, sweeps, flags, batch, st);
     else launch_df_t<96, 3>(H, J, ell, ellp, 30, sweeps, flags, batch, st);
@@ -58,6 +59,14 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
   unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #ifdef RSVD_JDF_TRACE
   cudaMemcpyFromSymbol(tr, g_jdf_trace, sizeof(tr));
+#endif
+#ifdef RSVD_JCLU_TRACE
+  if (which == 3) {
+    cudaMemcpyFromSymbol(tr, g_jclu_trace, sizeof(tr));
+    const double nt = tr[5] ? double(tr[5]) : 1.0;
+    printf("   clug CTA0: %llu tasks; per task us: stage %.2f gram+reduce %.2f rot %.2f apply %.2f grid-barrier %.2f\n",
+           tr[5], tr[0] / nt / 1e3, tr[1] / nt / 1e3, tr[2] / nt / 1e3, tr[3] / nt / 1e3, tr[4] / nt / 1e3);
+  }
 #endif
   int sw = 0;
   cudaMemcpy(&sw, sweeps, 4, cudaMemcpyDeviceToHost);
@@ -102,6 +111,12 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
 }
 
 int main() {
+  if (getenv("JDF_ONLY_CLU")) {
+    run(272, 288, 1, 5, 3);  // C3 (cluster kernel)
+    run(544, 544, 1, 3, 3);  // C5
+    run(74, 96, 1, 5, 3);    // C1
+    return 0;
+  }
   run(138, 160, 256, 5, 0);  // C2
   run(276, 288, 32, 5, 0);   // C4
   run(138, 160, 64, 5, 0);
