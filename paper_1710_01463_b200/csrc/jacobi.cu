@@ -47,6 +47,21 @@ __device__ __forceinline__ int rr_player(int slot, int s, int nn) {
   return 1 + (slot - 1 + s) % (nn - 1);
 }
 
+// tan of the Jacobi angle, t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), with
+// a hardware reciprocal refined by two Newton steps instead of the IEEE
+// division (~1e-15 relative instead of 0.5 ulp): t only decides how well the
+// pair is annihilated, while c = (1 + t^2)^-1/2 and s = c t stay orthonormal
+// to working precision whatever t is.  Saves ~60 cycles of the rotation
+// chain per step.
+__device__ __forceinline__ double jacobi_tan(double d, double g2) {
+  const double den = fabs(d) + sqrt(fma(d, d, g2 * g2));
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+  r = r * fma(-den, r, 2.0);
+  r = r * fma(-den, r, 2.0);
+  return copysign(1.0, d) * g2 * r;
+}
+
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(512, 1)
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             if (mag > 1e-140 && mag < 1e140) {
-              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+              tt = jacobi_tan(d, g2);
             } else {
               const double zeta = d / g2;
               tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(256, MINB)
             const double d = be - al, g2 = 2.0 * ga;
             const double mag = fmax(fabs(d), fabs(g2));
             if (mag > 1e-140 && mag < 1e140) {
-              tt = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+              tt = jacobi_tan(d, g2);
             } else {
               const double zeta = d / g2;
               tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
