@@ -111,10 +111,22 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
 }
 
 int main() {
+  if (getenv("JDF_SMALL")) {
+    run(74, 96, 1, 5, 0);    // C1 (shared-memory kernel)
+    run(74, 96, 1, 5, 3);
+    run(40, 64, 512, 5, 0);
+    run(96, 96, 64, 5, 0);
+    run(20, 32, 1000, 5, 0);
+    run(5, 32, 3, 5, 0);
+    return 0;
+  }
   if (getenv("JDF_ONLY_CLU")) {
     run(272, 288, 1, 5, 3);  // C3 (cluster kernel)
     run(544, 544, 1, 3, 3);  // C5
     run(74, 96, 1, 5, 3);    // C1
+    run(74, 96, 1, 5, 2);    // C1 through the dataflow kernel
+    run(74, 96, 1, 5, 1);
+    run(272, 288, 1, 5, 2);  // C3 through the dataflow kernel
     return 0;
   }
   run(138, 160, 256, 5, 0);  // C2
