@@ -107,11 +107,6 @@ class SymmetricMPS:
         return g, lam
 
 
-def _floored_inverse(lam):
-    torch = _torch()
-    return 1.0 / torch.clamp(lam, min=LAMBDA_FLOOR)
-
-
 class _BondPlan:
     """Everything the update of one bond needs between its assembly and its
     gauge update (sector offsets, the assembled theta', QR factors)."""
@@ -124,6 +119,44 @@ def _colmajor(rows: int, cols: int, like):
     return torch.empty((cols, rows), dtype=like.dtype, device=like.device).t()
 
 
+class _Blk:
+    """A strided matrix by address -- (ptr, row stride, column stride, rows,
+    cols) in elements -- and the tensor owning its storage.  Sub-blocks are
+    address arithmetic, so building the launch tables creates no torch views
+    (a view costs microseconds of host time; a layer builds thousands)."""
+
+    __slots__ = ("p", "rs", "cs", "r", "c", "owner", "es")
+
+    def __init__(self, p, rs, cs, r, c, owner, es):
+        self.p, self.rs, self.cs, self.r, self.c, self.owner, self.es = p, rs, cs, r, c, owner, es
+
+    @staticmethod
+    def of(t):
+        return _Blk(t.data_ptr(), t.stride(0), t.stride(1), t.shape[0], t.shape[1], t,
+                    t.element_size())
+
+    def sub(self, r0, r1, c0, c1):
+        return _Blk(self.p + (r0 * self.rs + c0 * self.cs) * self.es, self.rs, self.cs, r1 - r0,
+                    c1 - c0, self.owner, self.es)
+
+
+class _Arena:
+    """One device allocation carved into column-major matrices (the layer's
+    intermediate operands)."""
+
+    def __init__(self, total, like):
+        torch = _torch()
+        self.buf = torch.empty(max(int(total), 1), dtype=like.dtype, device=like.device)
+        self.base = self.buf.data_ptr()
+        self.es = self.buf.element_size()
+        self.off = 0
+
+    def take(self, rows, cols):
+        b = _Blk(self.base + self.off * self.es, 1, max(rows, 1), rows, cols, self.buf, self.es)
+        self.off += rows * cols
+        return b
+
+
 class _Tables:
     """Host job tables of one launch of the engine's table-driven bond-update
     kernels (rsvd_combine_blocks / rsvd_grouped_gemm / rsvd_block_sqnorms)."""
@@ -132,41 +165,30 @@ class _Tables:
         self.jobs, self.terms, self.gemms = [], [], []
         self.keep = []  # tensors whose storage the tables point to
 
-    @staticmethod
-    def _view(t):
-        return t.data_ptr(), t.stride(0), t.stride(1)
-
     def combine(self, dst, terms):
-        """dst = sum_t coef * diag(row_scale) src diag(col_scale); terms =
-        [(src, row_scale or None, col_scale or None, coef)]."""
-        rows, cols = dst.shape
-        if rows == 0 or cols == 0:
+        """dst = sum_t coef * diag(row_scale) src diag(col_scale); dst and the
+        sources are _Blk, terms = [(src, row_scale_ptr or 0, col_scale_ptr or 0,
+        coef)]."""
+        if dst.r == 0 or dst.c == 0:
             return
         begin = len(self.terms)
         for src, rsc, csc, coef in terms:
             if coef == 0:
                 continue
-            sp, srs, scs = self._view(src)
             c = complex(coef)
-            self.terms.append((sp, srs, scs, rsc.data_ptr() if rsc is not None else 0,
-                               csc.data_ptr() if csc is not None else 0, c.real, c.imag))
-            self.keep.append(src)
-        dp, drs, dcs = self._view(dst)
-        self.jobs.append((dp, drs, dcs, rows, cols, begin, len(self.terms) - begin))
-        self.keep.append(dst)
+            self.terms.append((src.p, src.rs, src.cs, rsc, csc, c.real, c.imag))
+            self.keep.append(src.owner)
+        self.jobs.append((dst.p, dst.rs, dst.cs, dst.r, dst.c, begin, len(self.terms) - begin))
+        self.keep.append(dst.owner)
 
     def gemm(self, c, a, b):
-        if c.shape[0] == 0 or c.shape[1] == 0:
+        if c.r == 0 or c.c == 0:
             return
-        if a.shape[1] == 0:
+        if a.c == 0:
             self.combine(c, [])
             return
-        ap, ars, acs = self._view(a)
-        bp, brs, bcs = self._view(b)
-        cp, crs, ccs = self._view(c)
-        self.gemms.append((ap, ars, acs, bp, brs, bcs, cp, crs, ccs, c.shape[0], c.shape[1],
-                           a.shape[1]))
-        self.keep += [a, b, c]
+        self.gemms.append((a.p, a.rs, a.cs, b.p, b.rs, b.cs, c.p, c.rs, c.cs, c.r, c.c, a.c))
+        self.keep += [a.owner, b.owner, c.owner]
 
     def run_combine(self, h, cplx: bool):
         lib = _lib.load()
@@ -186,6 +208,10 @@ class _Tables:
         g = np.array(self.gemms, dtype=_lib.GEMM_JOB)
         _lib.raise_for(lib.rsvd_grouped_gemm(h.raw, int(cplx), len(g), g.ctypes.data), h.raw)
         self.gemms = []
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else 0
 
 
 def _bond_sizes(psi: SymmetricMPS, bond: int, gate: TwoSiteGate) -> _BondPlan:
@@ -239,39 +265,74 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
     st1, st2, st3 = _Tables(), _Tables(), _Tables()
     qr_groups = {}  # (rows, fused) -> [(plan, sp, x, y)]
     lifted_y = []   # (plan, sp, x, y) multiplied directly (no QR)
+    # One allocation for every block-form intermediate (A_mu, B_mu, theta_mu)
+    # of the layer, and the theta' outputs (handed to the factorization as
+    # tensors) carved from a second one.
+    need = 0
+    need_out = 0
+    for pl in plans:
+        if pl.gate.form == GateForm.block:
+            for mu in (0, 1):
+                if pl.nm[mu]:
+                    need += pl.rows[mu] * pl.nm[mu] + pl.nm[mu] * pl.cols[mu] + \
+                        pl.rows[mu] * pl.cols[mu]
+            need_out += pl.rows[0] * pl.cols[0] + pl.rows[1] * pl.cols[1]
+    arena = _Arena(need, ref)
+    outbuf = torch.empty(max(need_out, 1), dtype=ref.dtype, device=dev)
+    out_off = 0
+    blk_cache = {}
+
+    def blk(t):  # _Blk of a state tensor, cached for the layer
+        k = id(t)
+        v = blk_cache.get(k)
+        if v is None:
+            v = _Blk.of(t)
+            blk_cache[k] = v
+        return v
+
     for pl in plans:
         bond = pl.bond
         lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
         g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
         nl, nm, nr, rows, cols = pl.nl, pl.nm, pl.nr, pl.rows, pl.cols
+        row_off, col_off = pl.row_off, pl.col_off
         gate = pl.gate
         if gate.form == GateForm.block:
             pl.lifted = False
             theta = [None, None]
+            pll = [_ptr(lam_l[0]), _ptr(lam_l[1])]
+            plm = [_ptr(lam_m[0]), _ptr(lam_m[1])]
+            plr = [_ptr(lam_r[0]), _ptr(lam_r[1])]
             for mu in (0, 1):
                 if nm[mu] == 0:
                     continue
-                A = _colmajor(rows[mu], nm[mu], ref)
-                B = _colmajor(nm[mu], cols[mu], ref)
+                A = arena.take(rows[mu], nm[mu])
+                B = arena.take(nm[mu], cols[mu])
                 for m in range(d):
                     a = mu ^ p[m]
-                    st1.combine(A[pl.row_off[mu][m]:pl.row_off[mu][m] + nl[a]],
-                                [(g1[m][a], lam_l[a], lam_m[mu], 1.0)])
-                    c = mu ^ p[m]
-                    st1.combine(B[:, pl.col_off[mu][m]:pl.col_off[mu][m] + nr[c]],
-                                [(g2[m][mu], None, lam_r[c], 1.0)])
-                theta[mu] = _colmajor(rows[mu], cols[mu], ref)
+                    st1.combine(A.sub(row_off[mu][m], row_off[mu][m] + nl[a], 0, nm[mu]),
+                                [(blk(g1[m][a]), pll[a], plm[mu], 1.0)])
+                    st1.combine(B.sub(0, nm[mu], col_off[mu][m], col_off[mu][m] + nr[a]),
+                                [(blk(g2[m][mu]), 0, plr[a], 1.0)])
+                theta[mu] = arena.take(rows[mu], cols[mu])
                 st2.gemm(theta[mu], A, B)
             gb = gate.block
-            thetap = [_colmajor(rows[sp], cols[sp], ref) for sp in (0, 1)]
+            thetap, tpb = [], []
+            for sp in (0, 1):
+                n_ = rows[sp] * cols[sp]
+                t_ = outbuf.narrow(0, out_off, n_).view(cols[sp], rows[sp]).t()
+                out_off += n_
+                thetap.append(t_)
+                tpb.append(_Blk(t_.data_ptr(), 1, max(rows[sp], 1), rows[sp], cols[sp], outbuf,
+                                arena.es))
             for sp in (0, 1):
                 for m1 in range(d):
                     a = sp ^ p[m1]
                     for m2 in range(d):
                         c = sp ^ p[m2]
                         q = p[m1] ^ p[m2]
-                        out = thetap[sp][pl.row_off[sp][m1]:pl.row_off[sp][m1] + nl[a],
-                                         pl.col_off[sp][m2]:pl.col_off[sp][m2] + nr[c]]
+                        out = tpb[sp].sub(row_off[sp][m1], row_off[sp][m1] + nl[a],
+                                          col_off[sp][m2], col_off[sp][m2] + nr[c])
                         terms = []
                         for i1 in range(d):
                             for i2 in range(d):
@@ -281,9 +342,9 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
                                 mu = a ^ p[i1]
                                 if coef == 0.0 or theta[mu] is None:
                                     continue
-                                src = theta[mu][pl.row_off[mu][i1]:pl.row_off[mu][i1] + nl[a],
-                                                pl.col_off[mu][i2]:pl.col_off[mu][i2] + nr[c]]
-                                terms.append((src, None, None, coef))
+                                src = theta[mu].sub(row_off[mu][i1], row_off[mu][i1] + nl[a],
+                                                    col_off[mu][i2], col_off[mu][i2] + nr[c])
+                                terms.append((src, 0, 0, coef))
                         st3.combine(out, terms)
             pl.thetap = thetap
         else:
@@ -295,6 +356,7 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
                     fused += nm[sp ^ t.charge]
                 x = _colmajor(rows[sp], fused, ref)
                 y = _colmajor(fused, cols[sp], ref)
+                xb, yb = _Blk.of(x), _Blk.of(y)
                 for k, t in enumerate(gate.terms):
                     mu = sp ^ t.charge
                     w = nm[mu]
@@ -302,15 +364,16 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
                         continue
                     for m1p in range(d):
                         a = sp ^ p[m1p]
-                        st1.combine(x[pl.row_off[sp][m1p]:pl.row_off[sp][m1p] + nl[a],
-                                      koff[k]:koff[k] + w],
-                                    [(g1[m1][a], lam_l[a], lam_m[mu], float(t.left[m1p, m1]))
+                        st1.combine(xb.sub(row_off[sp][m1p], row_off[sp][m1p] + nl[a],
+                                           koff[k], koff[k] + w),
+                                    [(blk(g1[m1][a]), _ptr(lam_l[a]), _ptr(lam_m[mu]),
+                                      float(t.left[m1p, m1]))
                                      for m1 in range(d) if t.left[m1p, m1] != 0.0])
                     for m2p in range(d):
                         c = sp ^ p[m2p]
-                        st1.combine(y[koff[k]:koff[k] + w,
-                                      pl.col_off[sp][m2p]:pl.col_off[sp][m2p] + nr[c]],
-                                    [(g2[m2][mu], None, lam_r[c], float(t.right[m2p, m2]))
+                        st1.combine(yb.sub(koff[k], koff[k] + w,
+                                           col_off[sp][m2p], col_off[sp][m2p] + nr[c]),
+                                    [(blk(g2[m2][mu]), 0, _ptr(lam_r[c]), float(t.right[m2p, m2]))
                                      for m2 in range(d) if t.right[m2p, m2] != 0.0])
                 if rows[sp] == 0 or fused == 0:  # mps.cpp:256-258
                     pl.qfac[sp] = torch.zeros(rows[sp], 0, dtype=ref.dtype, device=dev)
@@ -343,9 +406,9 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
             for i, (pl, sp, _, y) in enumerate(members):
                 pl.qfac[sp] = Qb[i]
                 pl.thetap[sp] = _colmajor(n, pl.cols[sp], ref)
-                st2.gemm(pl.thetap[sp], Rb[i], y)
+                st2.gemm(_Blk.of(pl.thetap[sp]), _Blk.of(Rb[i]), _Blk.of(y))
         for pl, sp, x, y in lifted_y:
-            st2.gemm(pl.thetap[sp], x, y)
+            st2.gemm(_Blk.of(pl.thetap[sp]), _Blk.of(x), _Blk.of(y))
         # (2) theta_mu = Astack Bstack, R y, x y
         st2.run_gemm(h, cplx)
         # (3) gate mixing
@@ -355,8 +418,8 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
         for pl in plans:
             for tp in pl.thetap:
                 if tp is not None and tp.numel():
-                    dp_, rs_, cs_ = _Tables._view(tp)
-                    blocks.append((dp_, rs_, cs_, tp.shape[0], tp.shape[1], 0, 0))
+                    blocks.append((tp.data_ptr(), tp.stride(0), tp.stride(1), tp.shape[0],
+                                   tp.shape[1], 0, 0))
             begin.append(len(blocks))
         out = torch.empty(len(plans), dtype=torch.float64, device=dev)
         bt = np.array(blocks if blocks else [(0, 0, 0, 0, 0, 0, 0)], dtype=_lib.BLOCK_JOB)
@@ -368,7 +431,7 @@ def _assemble_layer(psi: SymmetricMPS, plans: List[_BondPlan], handle) -> None:
     # keep every table operand alive until the stream has consumed it
     for pl, v in zip(plans, vals):
         pl.total_sq = float(v)
-        pl._keep = (st1.keep, st2.keep, st3.keep)
+        pl._keep = (st1.keep, st2.keep, st3.keep, arena)
         if not (pl.total_sq > 0.0):
             raise RuntimeError("apply_gate: evolved wavefunction vanished")
 
@@ -415,41 +478,55 @@ def _finish_layer(psi: SymmetricMPS, plans, fs, seconds, handle) -> List[GateSta
                     continue  # qfac = I: theta' was x y itself
                 left = factors[sp].left
                 lifted = _colmajor(q.shape[0], left.shape[1], left)
-                lift.gemm(lifted, q, left)
+                lift.gemm(_Blk.of(lifted), _Blk.of(q), _Blk.of(left))
                 factors[sp].left = lifted
         plan.kept_sq = kept_sq
         cplx = cplx or factors[0].left.is_complex()
     with _lib.on_torch_stream(h):
         lift.run_gemm(h, cplx)
-    for plan, f in zip(plans, fs):
+    # 1 / max(lambda, floor) of every outer bond of the layer in one pass (the
+    # outer bonds of disjoint gates are not updated by this layer)
+    outer = []
+    for plan in plans:  # (plans is never empty: apply_gate_layer takes >= 1 bond)
+        outer += [psi.lambdas[plan.bond][0], psi.lambdas[plan.bond][1],
+                  psi.lambdas[plan.bond + 2][0], psi.lambdas[plan.bond + 2][1]]
+    inv_all = torch.split(1.0 / torch.clamp(torch.cat(outer), min=LAMBDA_FLOOR),
+                          [t.numel() for t in outer])
+    for pi, (plan, f) in enumerate(zip(plans, fs)):
         factors = f.factors
         bond = plan.bond
-        lam_l, lam_m, lam_r = psi.lambdas[bond], psi.lambdas[bond + 1], psi.lambdas[bond + 2]
+        lam_m = psi.lambdas[bond + 1]
         inv_norm = 1.0 / np.sqrt(plan.kept_sq)
         for s in (0, 1):
             lam_m[s] = factors[s].sigma * inv_norm
-        linv = [_floored_inverse(lam_l[0]), _floored_inverse(lam_l[1])]
-        rinv = [_floored_inverse(lam_r[0]), _floored_inverse(lam_r[1])]
+        linv = inv_all[4 * pi:4 * pi + 2]
+        rinv = inv_all[4 * pi + 2:4 * pi + 4]
+        pli = [_ptr(linv[0]), _ptr(linv[1])]
+        pri = [_ptr(rinv[0]), _ptr(rinv[1])]
         g1, g2 = psi.gammas[bond], psi.gammas[bond + 1]
         nl, nr = plan.nl, plan.nr
+        lb = [_Blk.of(factors[0].left), _Blk.of(factors[1].left)]
+        rb = [_Blk.of(factors[0].right_adj), _Blk.of(factors[1].right_adj)]
         for m in range(d):
             for a in (0, 1):
                 s = a ^ p[m]
-                left = factors[s].left
-                lrows = left[plan.row_off[s][m]:plan.row_off[s][m] + nl[a], :]
-                g1[m][a] = _colmajor(nl[a], left.shape[1], left)
-                gauge.combine(g1[m][a], [(lrows, linv[a], None, 1.0)])
-                ra = factors[a].right_adj
+                L = lb[s]
+                g1[m][a] = _colmajor(nl[a], L.c, factors[s].left)
+                gauge.combine(_Blk.of(g1[m][a]),
+                              [(L.sub(plan.row_off[s][m], plan.row_off[s][m] + nl[a], 0, L.c),
+                                pli[a], 0, 1.0)])
+                R = rb[a]
                 c = a ^ p[m]
-                rcols = ra[:, plan.col_off[a][m]:plan.col_off[a][m] + nr[c]]
-                g2[m][a] = _colmajor(ra.shape[0], nr[c], ra)
-                gauge.combine(g2[m][a], [(rcols, None, rinv[c], 1.0)])
+                g2[m][a] = _colmajor(R.r, nr[c], factors[a].right_adj)
+                gauge.combine(_Blk.of(g2[m][a]),
+                              [(R.sub(0, R.r, plan.col_off[a][m], plan.col_off[a][m] + nr[c]), 0,
+                                pri[c], 1.0)])
         out = GateStats()
         out.discarded_weight = max(0.0, 1.0 - plan.kept_sq / plan.total_sq)
         out.factorize_seconds = seconds / max(len(plans), 1)
         out.mid_rank = int(lam_m[0].numel() + lam_m[1].numel())
         stats.append(out)
-        plan._keep_gauge = (linv, rinv)
+        plan._keep_gauge = (linv, rinv, inv_all)
     with _lib.on_torch_stream(h):
         gauge.run_combine(h, cplx)
     # the table operands (factors, inverse lambdas) must outlive the launch
