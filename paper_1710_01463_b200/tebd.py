@@ -481,6 +481,7 @@ def _finish_layer(psi: SymmetricMPS, plans, fs, seconds, handle) -> List[GateSta
                 lift.gemm(_Blk.of(lifted), _Blk.of(q), _Blk.of(left))
                 factors[sp].left = lifted
         plan.kept_sq = kept_sq
+        plan.sig_host = sh
         cplx = cplx or factors[0].left.is_complex()
     with _lib.on_torch_stream(h):
         lift.run_gemm(h, cplx)
@@ -492,13 +493,35 @@ def _finish_layer(psi: SymmetricMPS, plans, fs, seconds, handle) -> List[GateSta
                   psi.lambdas[plan.bond + 2][0], psi.lambdas[plan.bond + 2][1]]
     inv_all = torch.split(1.0 / torch.clamp(torch.cat(outer), min=LAMBDA_FLOOR),
                           [t.numel() for t in outer])
+    # The new inner lambdas sigma / ||kept|| of the whole layer from the host
+    # copies of sigma, uploaded in one transfer (the same IEEE products).
+    lam_vals, lam_dst = [], []
+    # The new Gamma blocks of the layer: one allocation, column-major blocks.
+    gsize = 0
+    for plan, f in zip(plans, fs):
+        for m in range(d):
+            for a in (0, 1):
+                gsize += plan.nl[a] * f.factors[a ^ p[m]].left.shape[1]
+                gsize += f.factors[a].right_adj.shape[0] * plan.nr[a ^ p[m]]
+    like = fs[0].factors[0].left
+    garena = torch.empty(max(gsize, 1), dtype=like.dtype, device=like.device)
+    goff = 0
+
+    def gtake(rows, cols):
+        nonlocal goff
+        n_ = rows * cols
+        t_ = garena.narrow(0, goff, n_).view(cols, rows).t()
+        goff += n_
+        return t_
+
     for pi, (plan, f) in enumerate(zip(plans, fs)):
         factors = f.factors
         bond = plan.bond
         lam_m = psi.lambdas[bond + 1]
         inv_norm = 1.0 / np.sqrt(plan.kept_sq)
         for s in (0, 1):
-            lam_m[s] = factors[s].sigma * inv_norm
+            lam_vals.append(np.asarray(plan.sig_host[s], dtype=np.float64) * inv_norm)
+            lam_dst.append((lam_m, s))
         linv = inv_all[4 * pi:4 * pi + 2]
         rinv = inv_all[4 * pi + 2:4 * pi + 4]
         pli = [_ptr(linv[0]), _ptr(linv[1])]
@@ -511,22 +534,25 @@ def _finish_layer(psi: SymmetricMPS, plans, fs, seconds, handle) -> List[GateSta
             for a in (0, 1):
                 s = a ^ p[m]
                 L = lb[s]
-                g1[m][a] = _colmajor(nl[a], L.c, factors[s].left)
+                g1[m][a] = gtake(nl[a], L.c)
                 gauge.combine(_Blk.of(g1[m][a]),
                               [(L.sub(plan.row_off[s][m], plan.row_off[s][m] + nl[a], 0, L.c),
                                 pli[a], 0, 1.0)])
                 R = rb[a]
                 c = a ^ p[m]
-                g2[m][a] = _colmajor(R.r, nr[c], factors[a].right_adj)
+                g2[m][a] = gtake(R.r, nr[c])
                 gauge.combine(_Blk.of(g2[m][a]),
                               [(R.sub(0, R.r, plan.col_off[a][m], plan.col_off[a][m] + nr[c]), 0,
                                 pri[c], 1.0)])
         out = GateStats()
         out.discarded_weight = max(0.0, 1.0 - plan.kept_sq / plan.total_sq)
         out.factorize_seconds = seconds / max(len(plans), 1)
-        out.mid_rank = int(lam_m[0].numel() + lam_m[1].numel())
+        out.mid_rank = int(len(plan.sig_host[0]) + len(plan.sig_host[1]))  # the new lambdas
         stats.append(out)
         plan._keep_gauge = (linv, rinv, inv_all)
+    allv = torch.from_numpy(np.concatenate(lam_vals)).to(like.device)
+    for (lst, s_), piece in zip(lam_dst, torch.split(allv, [len(v) for v in lam_vals])):
+        lst[s_] = piece
     with _lib.on_torch_stream(h):
         gauge.run_combine(h, cplx)
     # the table operands (factors, inverse lambdas) must outlive the launch
