@@ -319,12 +319,25 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   else c.bn = (8 * w96 <= 9 * w64) ? 96 : 64;
   c.bm = (M <= 64) ? 64 : 128;
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
-  const int64_t target = 2 * num_sms();  // two resident CTAs per SM
+  const int64_t slots = 2 * num_sms();  // two resident CTAs per SM
   int64_t splits = 1;
-  // Few output tiles (single small matrices, C1): split K down to 64 per CTA
-  // so that the GEMM spreads over the GPU; otherwise keep >= 256 of K.
-  const int64_t kmin = (tiles * 8 <= num_sms() && K >= 1024) ? 64 : 256;
-  if (tiles < target) splits = std::min<int64_t>(ceil_div(target, tiles), std::max<int64_t>(1, K / kmin));
+  // Fewer than ~4 waves of output tiles: split K so that the last wave is as
+  // full as possible (fewer splits among nearly equal), each split keeping
+  // >= 256 of K -- or 64 for very few tiles (single small matrices, C1) --
+  // and >= 512 once the tiles alone fill a wave.  (C3 / C5's A^T Q: 96 tiles
+  // -> 3 splits, 0.97 of a wave instead of 4 splits, 1.3 waves; a 4-item C4
+  // batch, 384 tiles -> 3 splits.)
+  if (tiles < 4 * slots) {
+    const int64_t kmin = (tiles * 8 <= num_sms() && K >= 1024) ? 64 : (tiles < slots ? 256 : 512);
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / kmin));
+    double best_eff = -1.0;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int64_t ctas = tiles * sp;
+      const double eff = static_cast<double>(ctas) / static_cast<double>(ceil_div(ctas, slots) * slots);
+      if (eff > best_eff * 1.02) best_eff = eff, splits = sp;
+      if (ctas >= 4 * slots) break;
+    }
+  }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 64));
   int64_t kps = round_up(ceil_div(K, splits), kBK);
   splits = ceil_div(K, kps);
