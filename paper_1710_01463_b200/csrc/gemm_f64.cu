@@ -306,7 +306,7 @@ struct Choice {
   int64_t kps;
 };
 
-Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
+Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch, bool allow80 = true) {
   Choice c{128, 64, 1, 0};
   // Prefer a BN that covers N with little padding waste.
   // The 128 x 96 tile (TMA path) is the efficient one: take it unless 64-wide
@@ -318,6 +318,10 @@ Choice choose(int64_t M, int64_t N, int64_t K, int64_t batch) {
   // 12.5% padding (N = 256: lift 1.97 -> 1.70 ms on C4).
   else c.bn = (8 * w96 <= 9 * w64) ? 96 : 64;
   c.bm = (M <= 64) ? 64 : 128;
+  // 128 x 80 TMA tiles where they cut the padding by more than 12.5%
+  // (l_p = 160, C2 / TEBD sectors: 160 columns instead of 192).
+  const int64_t w80 = round_up(N, 80);
+  if (allow80 && N > 64 && c.bm == 128 && 9 * w80 < 8 * std::min(w96, w64)) c.bn = 80;
   const int64_t tiles = ceil_div(M, c.bm) * ceil_div(N, c.bn) * batch;
   const int64_t slots = 2 * num_sms();  // two resident CTAs per SM
   int64_t splits = 1;
@@ -406,7 +410,11 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
               int64_t batch, double* partial, int64_t partial_capacity, const GemmOpts& opt,
               cudaStream_t st) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
-  Choice c = choose(M, N, K, batch);
+  // 16-byte aligned operands with even strides: the TMA tiles can take them.
+  const bool tma_ok = aligned16(A.base) && aligned16(B.base) && A.ld % 2 == 0 && B.ld % 2 == 0 &&
+                      (batch == 1 || (A.stride % 2 == 0 && B.stride % 2 == 0)) && !opt.colmapA &&
+                      (trans_a || M % 16 == 0);
+  Choice c = choose(M, N, K, batch, tma_ok);
   // Symmetric Gram of a 96-multiple width: 96 x 96 TMA tiles (the 128 x 96
   // tile leaves a partial row tile and computes ~40% more than the upper half).
   // (Only when the TMA path can take the operands: an odd row count, e.g. a
@@ -448,11 +456,12 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
   const bool vec2 = aligned16(A.base) && aligned16(B.base) && (A.ld % 2 == 0) &&
                     (B.ld % 2 == 0) && (A.stride % 2 == 0) && (B.stride % 2 == 0) &&
                     (trans_a ? true : (M % 2 == 0)) && (K % 2 == 0) && (c.kps % 2 == 0);
-  const bool tma_done = !a.colmapA && ((c.bm == 128 && c.bn == 96) || sq96) &&
-                        dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits,
-                                  c.kps, a.c_upper != 0, opt.item_mask, a.b_upper != 0, st,
-                                  sq96 ? 1 : 0);
+  const bool tma_done =
+      !a.colmapA && ((c.bm == 128 && (c.bn == 96 || c.bn == 80)) || sq96) &&
+      dgemm_tma(trans_a, M, N, K, A, B, a.C, a.ldc, a.strideC, batch, c.splits, c.kps,
+                a.c_upper != 0, opt.item_mask, a.b_upper != 0, st, sq96 ? 1 : (c.bn == 80 ? 2 : 0));
   if (sq96 && !tma_done) throw CudaError("dgemm: 96x96 Gram tile needs the TMA path");
+  if (c.bn == 80 && !tma_done) throw CudaError("dgemm: 128x80 tile needs the TMA path");
   if (tma_done) {
   } else if (trans_a) {
     if (vec2) dispatch<true, 2>(c, a, st);

@@ -273,8 +273,9 @@ bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
                const int* item_mask, bool b_upper, cudaStream_t st, int tile) {
   // tile 0: 128 x 96 (8 warps as 4 x 2); tile 1: 96 x 96 (2 x 4 warps) for the
-  // symmetric Gram of a 96-multiple l_p (no partial 128-row tiles).
-  const int bm = tile == 1 ? 96 : kBM, bn = tile == 1 ? 96 : kBN;
+  // symmetric Gram of a 96-multiple l_p (no partial 128-row tiles); tile 2:
+  // 128 x 80 (4 x 2 warps of 32 x 40) for 160-wide operands.
+  const int bm = tile == 1 ? 96 : kBM, bn = tile == 1 ? 96 : (tile == 2 ? 80 : kBN);
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al16(A.base) || !al16(B.base)) return false;
   if (A.ld % 2 || B.ld % 2 || A.stride % 2 || B.stride % 2) return false;
@@ -310,6 +311,11 @@ bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef
   if (tile == 1) {
     if (trans_a) launch<3, true, 96, 96, 2, 4>(ma, mb, a, st);
     else launch<3, false, 96, 96, 2, 4>(ma, mb, a, st);
+    return true;
+  }
+  if (tile == 2) {
+    if (trans_a) launch<kTmaStages, true, 128, 80, 4, 2>(ma, mb, a, st);
+    else launch<kTmaStages, false, 128, 80, 4, 2>(ma, mb, a, st);
     return true;
   }
   if (trans_a) launch<kTmaStages, true>(ma, mb, a, st);
