@@ -161,7 +161,7 @@ int64_t fcqr_xscratch_elems(int64_t ellp, int64_t batch);
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`
 // columns live), accumulating J; sweeps until converged.
 // flags: jacobi_flag_elems(batch) unsigned ints of workspace.
-int64_t jacobi_flag_elems(int64_t batch);
+int64_t jacobi_flag_elems(int64_t batch, int64_t ellp);
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,
                    unsigned* flags, int64_t batch, cudaStream_t st);
 

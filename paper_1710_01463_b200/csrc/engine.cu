@@ -325,7 +325,7 @@ Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
     B.rankF = c.take<int>(b);
     B.permS = c.take<int>(b * lp);
     B.sweeps = c.take<int>(b);
-    B.jflags = c.take<unsigned>(jacobi_flag_elems(b));
+    B.jflags = c.take<unsigned>(jacobi_flag_elems(b, lp));
   }
   B.partial_cap = partial_need(s);
   B.partial = c.take<double>(std::max<int64_t>(B.partial_cap, 1));

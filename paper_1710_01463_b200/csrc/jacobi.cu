@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(256, MINB)
   unsigned* convg = cnt + batch;
   unsigned long long* next = reinterpret_cast<unsigned long long*>(convg + batch);
   unsigned* nconv = reinterpret_cast<unsigned*>(next + 1);
+  unsigned* bdone = nconv + 2;  // [item][block]: phases the block has completed
 
   const int half = nb / 2;
   const int64_t per_phase = batch * half;
@@ -559,13 +560,20 @@ __global__ void __launch_bounds__(256, MINB)
       const int p = rr_player(k, phase - 1, nb), q = rr_player(nb - 1 - k, phase - 1, nb);
       bp = min(p, q), bq = max(p, q);
     }
+    const unsigned gph = static_cast<unsigned>(static_cast<int64_t>(sweep) * nb + phase);
+    unsigned* bd = bdone + item * nb;
     if (tid == 0) {
       // 1: do the task; 0: count it without work; -1: item converged, skip
       int work = 1;
-      const unsigned need = static_cast<unsigned>((static_cast<int64_t>(sweep) * nb + phase) * half);
       volatile unsigned* vc = convg + item;
-      unsigned c;
-      while ((c = ld_acquire(cnt + item)) < need && *vc == 0u) __nanosleep(100);
+      if (diag) {
+        // the item's whole previous sweep (its flags decide convergence)
+        const unsigned need = static_cast<unsigned>(static_cast<int64_t>(sweep) * nb * half);
+        while (ld_acquire(cnt + item) < need && *vc == 0u) __nanosleep(100);
+      } else {
+        // only the two tasks of the previous phase that held blocks bp, bq
+        while ((ld_acquire(bd + bp) < gph || ld_acquire(bd + bq) < gph) && *vc == 0u) __nanosleep(100);
+      }
       if (*vc != 0u) {
         work = -1;
       } else if (diag && sweep > 0) {
@@ -802,6 +810,8 @@ __global__ void __launch_bounds__(256, MINB)
     }
     if (tid == 0 && work >= 0) {
       __threadfence();
+      atomicMax(bd + bp, gph + 1);
+      atomicMax(bd + bq, gph + 1);
       atomicAdd(cnt + item, 1u);
     }
     JDF_MARK(4);
@@ -846,7 +856,7 @@ void launch_df_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps
   // One CTA per task of a phase at most: extra CTAs would only spin on the
   // next phase's dependencies (C4: 5.2 -> 6.1 ms with twice the grid).
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(per_phase, per_sm * num_sms())));
-  const int64_t nflags = jacobi_flag_elems(batch);
+  const int64_t nflags = jacobi_flag_elems(batch, ellp);
   const int64_t init_work = std::max<int64_t>(ellp * ellp * batch, nflags);
   jacobi_df_init_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(init_work, 256), 8 * num_sms())),
                           256, 0, st>>>(J, static_cast<int>(ellp), batch, max_sweeps, flags, nflags,
@@ -862,10 +872,12 @@ void launch_df_t(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps
 // Per item: 3 rotating "rotated" flags, then (8-byte aligned) 3 rotating
 // "a rotation with g^2 >= c_stop_ratio2 alpha beta" flags.
 
-int64_t jacobi_flag_elems(int64_t batch) {
+int64_t jacobi_flag_elems(int64_t batch, int64_t ellp) {
   // + per-item completion counter and converged flag, task counter (8 B) and
-  // converged-item count for jacobi_df_kernel
-  return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch + 2 * batch + 4;
+  // converged-item count for jacobi_df_kernel, then its per (item, 16-column
+  // block) phase counters
+  const int64_t nbk = (ellp + 15) / 16 + 2;
+  return ((3 * batch + 1) & ~int64_t(1)) + 6 * batch + 2 * batch + 4 + batch * nbk;
 }
 
 void launch_jacobi(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps, int* sweeps,

@@ -33,7 +33,7 @@ static void run(int ell, int ellp, int batch, int reps, int which = 0) {
   cudaMalloc(&H0, n * 8);
   cudaMalloc(&H, n * 8);
   cudaMalloc(&J, n * 8);
-  cudaMalloc(&flags, jacobi_flag_elems(batch) * 4);
+  cudaMalloc(&flags, jacobi_flag_elems(batch, ellp) * 4);
   cudaMalloc(&sweeps, batch * 4);
   cudaMemcpy(H0, h.data(), n * 8, cudaMemcpyHostToDevice);
   cudaStream_t st;
