@@ -458,10 +458,12 @@ bool launch_clu(double* H, double* J, int64_t ell, int64_t ellp, int max_sweeps,
 // Same sweep order, rotation formula, thresholds and convergence rule as
 // jacobi_gram_kernel, but
 //   * no grid-wide barrier: tasks (sweep, phase, item, block pair) are pulled
-//     in that order from one atomic counter by a persistent grid, and a task
-//     waits only for its OWN item's previous phase (a per-item completion
-//     counter, release/acquire) -- items, and the pairs of a phase, never wait
-//     for each other, so uneven task times and converged items cost nothing;
+//     in that order from one atomic counter by a persistent grid, and a
+//     block-pair task waits only for the two previous-phase tasks of its OWN
+//     item that held its blocks (per item-block phase counters), a phase-0 task
+//     for the item's previous sweep (release/acquire) -- items, and the pairs
+//     of a phase, never wait for each other, so uneven task times and
+//     converged items cost nothing;
 //   * the convergence decision for sweep s of an item is taken by its phase-0
 //     tasks of sweep s + 1 from that sweep's final flags;
 //   * nothing scales with l in shared memory: G = X^T X of the task's 32
