@@ -705,6 +705,15 @@ __global__ void __launch_bounds__(kCholThreads)
 // all products on DMMA (mma.sync m16n8k4 f64), operands from L2, with grid-wide
 // barriers between the phases.  Same outputs and breakdown rule as uchol_kernel.
 
+// Repeat CholeskyQR passes (the second pass of CholeskyQR2 / 3) factor a Gram
+// G = I + E of an already orthonormal-to-O(u kappa^2) basis.  With F = triu(E)
+// (diagonal halved), R' = I + F has R'^T R' = G + F^T F and Q = Y (I - F) has
+// ||Q^T Q - I|| = O(||F||^2): for ||F||_F^2 <= 1e-16 ~ u that is the exact
+// factor's own orthogonality, without the latency-bound factorization.  Items
+// with a larger F (ill-conditioned first passes) take the exact path.
+// (gchol: CholOpts::lin; fcqr: FcqrArgs::lin.)
+constexpr double kLinTol2 = 1e-16;
+
 constexpr int kGcThreads = 256;  // 8 warps: <= 255 registers, so the diagonal factor stays in registers
 constexpr int kGcWarps = kGcThreads / 32;
 constexpr int kGcDiagWarps = 2;  // warps per CTA with diagonal-factor smem
@@ -886,8 +895,10 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
   const int64_t gtid = static_cast<int64_t>(cta) * blockDim.x + tid;
   const int64_t gstride = static_cast<int64_t>(ncta) * blockDim.x;
   // scratch per item: [0, 1024) D_J; [sq, 2 sq) Acc (strictly upper blocks);
-  // [2 sq - 2] go flag, [2 sq - 1] pivot floor (a diagonal block of Acc).
+  // [2 sq - 3] ||F||_F^2 (lin), [2 sq - 2] go flag, [2 sq - 1] pivot floor
+  // (a diagonal block of Acc).
   auto go_of = [&](int64_t b) -> double* { return gc_item_scratch(a, b) + 2 * sq - 2; };
+  const bool lin = a.o.lin;
   auto gate = [&](int64_t b) {
     int go = 1;
     if (a.o.gate_rank) go = a.o.gate_rank[b] < ell;
@@ -909,6 +920,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
     const int go = gate(b);
     if (a.o.ill_out) a.o.ill_out[b] = (a.o.gate_rank && a.o.gate_rank[b] < ell) ? 1 : 0;
     go_of(b)[0] = go ? 1.0 : 0.0;
+    if (lin) go_of(b)[-1] = 0.0;
   }
   grid.sync();
   // Per item (flag read once), 16-byte stores (sq is a multiple of 1024),
@@ -919,6 +931,26 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
     double2* t2 = reinterpret_cast<double2*>(a.T + b * sq);
     const double2 z = make_double2(0.0, 0.0);
     for (int64_t e = gtid; e < sq / 2; e += gstride) t2[e] = z;
+    if (lin) {  // ||F||_F^2 over the upper triangle, grid-wide
+      __shared__ double s_f;
+      if (tid == 0) s_f = 0.0;
+      __syncthreads();
+      const double* W = a.G + b * sq;
+      double f2 = 0.0;
+      for (int64_t e = gtid; e < sq; e += gstride) {
+        const int i = static_cast<int>(e % ld), j = static_cast<int>(e / ld);
+        if (i <= j && j < ell) {
+          const double v = __ldcg(W + e);
+          const double f = i == j ? 0.5 * (v - 1.0) : v;
+          f2 = fma(f, f, f2);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) f2 += __shfl_xor_sync(0xffffffffu, f2, off);
+      if (lane == 0) atomicAdd(&s_f, f2);
+      __syncthreads();
+      if (tid == 0) atomicAdd(go_of(b) - 1, s_f);
+    }
     if (a.o.Gsrc) {
       const double2* s2 = reinterpret_cast<const double2*>(a.o.Gsrc + b * sq);
       double2* g2 = reinterpret_cast<double2*>(a.G + b * sq);
@@ -926,8 +958,35 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
     }
   }
   grid.sync();
+  if (lin) {
+    // Items with ||F||_F^2 <= kLinTol2: T = I - F, Rfull = I + F, rank = ell,
+    // written grid-wide; their go flag is cleared below (gate() and the sum
+    // are stable in this phase, the flag is not).
+    for (int64_t b = 0; b < batch; ++b) {
+      if (!gate(b) || !(__ldcg(go_of(b) - 1) <= kLinTol2)) continue;
+      const double* W = a.G + b * sq;
+      double* Tb = a.T + b * sq;
+      for (int64_t e = gtid; e < sq; e += gstride) {
+        const int i = static_cast<int>(e % ld), j = static_cast<int>(e / ld);
+        const bool up = i <= j && j < ell;
+        const double v = up ? __ldcg(W + e) : 0.0;
+        if (up) Tb[e] = i == j ? fma(-0.5, v, 1.5) : -v;
+        if (a.Rfull) a.Rfull[b * sq + e] = up ? (i == j ? fma(0.5, v, 0.5) : v) : 0.0;
+      }
+      if (a.perm)
+        for (int64_t e = gtid; e < ld; e += gstride) a.perm[b * ld + e] = static_cast<int>(e);
+    }
+  }
   for (int64_t b = gw; b < batch; b += nw) {  // shift, pivot floor, initial rank
     if (go_of(b)[0] == 0.0) continue;
+    if (lin && __ldcg(go_of(b) - 1) <= kLinTol2) {
+      __syncwarp();
+      if (lane == 0) {
+        a.rank[b] = ell;
+        go_of(b)[0] = 0.0;
+      }
+      continue;
+    }
     double* W = a.G + b * sq;
     double tr = 0.0, mx = 0.0;
     for (int i = lane; i < ell; i += 32) {
@@ -952,6 +1011,14 @@ __global__ void __launch_bounds__(kGcThreads, 1) gchol_kernel(const GcholArgs a_
     }
   }
   grid.sync();
+  if (lin) {  // every item took the first-order factor: all CTAs leave together
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int64_t b = tid; b < batch; b += blockDim.x)
+      if (__ldcg(go_of(b)) != 0.0) s_any = 1;
+    __syncthreads();
+    if (!s_any) return;
+  }
 
   const bool diag_warp = warp < kGcDiagWarps;
   double* Rd = sm + (diag_warp ? warp : 0) * 2 * 32 * kInvPitch;
@@ -1144,6 +1211,7 @@ struct FcqrArgs {
   int* rank;
   int rows, ell, ellp, cr;  // cr: staged rows per chunk (multiple of 16)
   double tau;
+  int lin;  // repeat pass: first-order factor when ||triu(G - I)||_F^2 <= kLinTol2
 };
 
 __device__ __forceinline__ int fq_ub(int I, int J) { return J * (J + 1) / 2 + I; }  // I <= J
@@ -1333,8 +1401,75 @@ __global__ void __launch_bounds__(kFqThreads, 1) fcqr_kernel(const FcqrArgs a) {
   }
   FQ_TRACE(2);
 
-  // ---- 2. pivot floor, rank; blocked Cholesky in shared memory ---------------
+  // ---- 1b. repeat pass: first-order factor when G = I + small E -------------
+  __shared__ int s_lin;
+  __shared__ double s_ef[kFqWarps];
   if (q == 0) {
+    if (a.lin) {
+      double ef = 0.0;  // ||F||_F^2, F = triu(E) with diag(E) / 2
+      for (int ub = warp; ub < nub; ub += kFqWarps) {
+        int J = 0;
+        while ((J + 1) * (J + 2) / 2 <= ub) ++J;
+        const int I = ub - J * (J + 1) / 2;
+        const double* Wb = blk(I, J);
+        for (int e = lane; e < 1024; e += 32) {
+          const int i = e & 31, j = e >> 5, gi = 32 * I + i, gj = 32 * J + j;
+          if (gi <= gj && gj < ell) {
+            const double v = Wb[i + j * kInvPitch];
+            const double f = gi == gj ? 0.5 * (v - 1.0) : v;
+            ef = fma(f, f, ef);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ef += __shfl_xor_sync(0xffffffffu, ef, off);
+      if (lane == 0) s_ef[warp] = ef;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kFqWarps; ++w) t += s_ef[w];
+        s_lin = t <= kLinTol2 ? 1 : 0;  // NaN fails
+      }
+    } else if (tid == 0) {
+      s_lin = 0;
+    }
+    __syncthreads();
+  }
+  // ---- 2. pivot floor, rank; blocked Cholesky in shared memory ---------------
+  if (q == 0 && s_lin) {
+    // R = I + F: W_IJ = R_IJ D_J = F_IJ + O(E^2) = G_IJ (already in place),
+    // D_J = I - F_JJ, rank = ell; Rf = I + F when requested.
+    for (int J = 0; J < nbk; ++J) {
+      const double* Gj = blk(J, J);
+      double* D = Dst + J * kFqBlk;
+      for (int e = tid; e < 1024; e += kFqThreads) {
+        const int i = e >> 5, j = e & 31, gi = 32 * J + i, gj = 32 * J + j;
+        double v = (i == j) ? 1.0 : 0.0;
+        if (gi < ell && gj < ell) {
+          if (i < j) v = -Gj[i + j * kInvPitch];
+          else if (i == j) v = fma(-0.5, Gj[i + j * kInvPitch], 1.5);
+        }
+        D[i * kInvPitch + j] = v;  // row-major, as the apply reads it
+      }
+    }
+    if (tid == 0) {
+      s_rank = ell;
+      a.rank[b] = ell;
+    }
+    if (a.Rf) {
+      double* Rf = a.Rf + b * static_cast<int64_t>(ellp) * ellp;
+      for (int e = tid; e < ellp * ellp; e += kFqThreads) {
+        const int i = e % ellp, j = e / ellp;
+        double v = 0.0;
+        if (i <= j && j < ell) {
+          const double gv = blk(i >> 5, j >> 5)[(i & 31) + (j & 31) * kInvPitch];
+          v = (i < j) ? gv : fma(0.5, gv, 0.5);
+        }
+        Rf[e] = v;
+      }
+    }
+    __syncthreads();
+  } else if (q == 0) {
   if (warp == 0) {
     double mx = 0.0;
     for (int i = lane; i < ell; i += 32) mx = fmax(mx, blk(i >> 5, i >> 5)[(i & 31) * (kInvPitch + 1)]);
@@ -1565,7 +1700,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
   // ill-conditioned fallback (usually no item active) use the one-CTA-per-item
   // kernel: cooperative launches replayed from a CUDA graph cost ~1 ms each
   // even when every CTA exits at once (C2: 44.6 -> 24.3 ms per step).
-  if (!pivot && !opts) {
+  if (!pivot && (!opts || opts->lin)) {
     GcholArgs ga{G, T, Rfull, scratch, rank, perm, static_cast<int>(ell), static_cast<int>(ellp),
                  tau, batch, opts ? *opts : CholOpts{}};
     const int bytes = kGcDiagWarps * 2 * 32 * kInvPitch * 8;
@@ -1682,7 +1817,7 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
                       int64_t strideQ, double* G0, double* Rf, double* xscratch, int* rank,
                       int64_t rows, int64_t ell, int64_t ellp, double tau, int64_t batch,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool lin) {
   if (batch <= 0) return true;
   if (ellp % 32 != 0 || ellp > 160 || rows < 1 || rows > (1 << 30)) return false;
   const int64_t nbk = ellp / 32, nub = nbk * (nbk + 1) / 2;
@@ -1702,7 +1837,7 @@ bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, 
                                    static_cast<int>(cap)));
   });
   FcqrArgs fa{Y, ldy, strideY, Q, ldq, strideQ, G0, Rf, xscratch, rank, static_cast<int>(rows),
-              static_cast<int>(ell), static_cast<int>(ellp), cr, tau};
+              static_cast<int>(ell), static_cast<int>(ellp), cr, tau, lin ? 1 : 0};
   // Few items: split each item's rows over a cluster (up to 8 CTAs, >= 64 rows each).
   int S = 1;
   while (xscratch && S < 8 && batch * S * 2 <= num_sms() && rows >= 64 * S * 2) S *= 2;

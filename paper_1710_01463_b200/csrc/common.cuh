@@ -141,6 +141,10 @@ struct CholOpts {
   const double* Gsrc = nullptr;
   double shift_coef = 0.0;
   bool pairs = false;  // pivoted kernel: pivot complex columns (2a, 2a+1) together
+  // Repeat CholeskyQR pass (unpivoted, alone): items whose Gram is I + E with
+  // ||triu(E)||_F^2 <= 1e-16 (diagonal halved) get the first-order factor
+  // R = I + F, T = I - F, rank = ell; the rest are factored exactly.
+  bool lin = false;
 };
 void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* rank, int* perm,
                   int64_t ell, int64_t ellp, double tau, bool pivot, int64_t batch,
@@ -151,11 +155,13 @@ void launch_pchol(double* G, double* T, double* Rfull, double* scratch, int* ran
 // caller's); G0 (full symmetric Gram) and Rf (R, zero below / beyond rank) are
 // written when non-null.  Returns false when the shape does not qualify.
 // xscratch: fcqr_xscratch_elems(ellp, batch) doubles (row-split cluster mode;
-// null disables it).
+// null disables it).  lin (repeat passes): items whose Gram is within 1e-8 of I
+// take the first-order factor R = I + triu(G - I) / (1 + [diag]) instead of the
+// exact Cholesky (rank = ell); the others are factored exactly.
 bool launch_fused_cqr(const double* Y, int64_t ldy, int64_t strideY, double* Q, int64_t ldq,
                       int64_t strideQ, double* G0, double* Rf, double* xscratch, int* rank,
                       int64_t rows, int64_t ell, int64_t ellp, double tau, int64_t batch,
-                      cudaStream_t st);
+                      cudaStream_t st, bool lin = false);
 int64_t fcqr_xscratch_elems(int64_t ellp, int64_t batch);
 
 // jacobi.cu — one-sided Jacobi on H (ellp x ellp per item; first `ell`

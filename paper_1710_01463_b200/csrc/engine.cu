@@ -420,7 +420,7 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
         Scope sc(P, kStChol, st);
         if (!launch_fused_cqr(in.base, rows, rows * lp, out.base, rows, rows * lp,
                               pass == 0 ? B.G0 : nullptr, Rf, B.cscratch, rk, rows, s.ell, lp, kPivotTau,
-                              b, st))
+                              b, st, pass > 0))
           throw CudaError("orth: fused CholeskyQR does not fit this shape");
         if (pass == 0) shifted_retry();
       }
@@ -438,7 +438,12 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
         // Unpivoted everywhere (grid-parallel gchol; breakdown -> numerical
         // rank).  Pivoting the first pass on B^T (QRCP grading of Rt for the
         // Jacobi) measured no fewer sweeps (r01 and r02, C2 8 / C4 7 sweeps).
-        launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st);
+        // Repeat passes: first-order factor for the items already orthonormal
+        // to ~1e-8 (chol.cu kLinTol2), exact gchol for the rest.
+        CholOpts lo;
+        lo.lin = pass > 0 && !cplx;
+        launch_pchol(B.G, B.T, Rf, B.cscratch, rk, B.perm, s.ell, lp, kPivotTau, pivot, b, st,
+                     lo.lin ? &lo : nullptr);
         if (pass == 0) shifted_retry();
       }
       Scope sc(P, kStApply, st);
