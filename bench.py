@@ -15,8 +15,10 @@ under torch.distributed.run with N ranks (127.0.0.1).
            (CUDA events on the launching stream, max over ranks).
   e2e    : same metric through the public API with pinned HOST buffers
            (H2D of A and D2H of U, S, Vt inside every timed step).
-  roofline: the dominant kernel (the DMMA A-pass GEMM) against the measured
-           FP64 tensor peak.
+  roofline: the dominant kernel, the A-pass GEMM: on C4 / C5 the emulated-FP64
+           INT8 tensor-core GEMM (ozaki.cu) against the measured tcgen05 kind::i8
+           peak; on the smaller configs the DMMA GEMM against the measured FP64
+           tensor peak.
   cpu_baseline: the reference's own rsvd (proj/src/factorize.cpp + lapack.cpp
            compiled unmodified into oracle/_ref/librlftn_ref.so, OpenBLAS
            LAPACK) on the host cores, rank 0 at N=1, on a bounded sample.
@@ -38,6 +40,11 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+INT8_PEAK_TOPS = 8186 * 148 * 2 * 1.965e9 / 1e12  # tcgen05.mma kind::i8 rate, profiles/r02_umma_rate.txt
+INT8_PEAK_SOURCE = ("measured tcgen05.mma.kind::i8 issue rate, 8186 MAC/clk/SM for N >= 128 "
+                    "(profiles/r02_umma_rate.txt) x 148 SMs x 2 x the 1965 MHz max SM clock; "
+                    "MEASURED_PEAKS.json has no INT8 figure")
+OZ_SLICE_PRODUCTS = 36  # 8 slices per operand, products p + q < 8 (ozaki.cu)
 FP64_PEAK_TFLOPS = 37.1  # measured: mma.sync f64 probe, profiles/r01_fp64_peak.txt
 FP64_PEAK_SOURCE = ("measured DMMA (mma.sync .f64) throughput on this pool's B200, "
                     "profiles/r01_fp64_peak.txt; MEASURED_PEAKS.json has no FP64 figure "
@@ -524,18 +531,45 @@ def run_ours(args, rank, world, local_rank):
                     "note": "tsvd_batched: CholeskyQR3 of A^T + one-sided Jacobi on the full "
                             "min(m, n) factor (row-streamed dataflow / cluster kernels), 1 call"}
         del ft, At
+    gemm_path = _lib.last_gemm_path(h)
+    slice_ms = prof.get("apass_slice", (0.0, 0))[0]  # nested inside the A-pass stages
     ap_ms = prof["apass_nn"][0] + prof["apass_tn"][0]
     ap_calls = prof["apass_nn"][1] + prof["apass_tn"][1]
+    gemm_ms = ap_ms - slice_ms
     ap_flops_per_launch = 2.0 * cfg.m * cfg.n * cfg.ell * B  # algorithmic: one pass over A per item
-    achieved = ap_flops_per_launch / (ap_ms / ap_calls / 1000.0) / 1e12 if ap_calls else None
-    step_ms_prof = sum(v[0] for v in prof.values()) / prof_steps
+    fp64_equiv = ap_flops_per_launch / (gemm_ms / ap_calls / 1000.0) / 1e12 if ap_calls else None
+    step_ms_prof = (sum(v[0] for v in prof.values()) - slice_ms) / prof_steps
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("apass_dram_bytes_per_launch")
+            key = "oz_gemm_dram_bytes_per_launch" if gemm_path == "ozaki" else "apass_dram_bytes_per_launch"
+            traffic = json.load(open(tpath)).get(key)
         except (OSError, ValueError):
             traffic = None
+    if gemm_path == "ozaki":
+        ops_per_launch = OZ_SLICE_PRODUCTS * ap_flops_per_launch  # INT8 ops of the slice products
+        achieved = ops_per_launch / (gemm_ms / ap_calls / 1000.0) / 1e12 if ap_calls else None
+        roof = {"bound": "tensor", "achieved": achieved, "peak": INT8_PEAK_TOPS, "unit": "TOP/s",
+                "frac": (achieved / INT8_PEAK_TOPS) if achieved else None, "traffic": traffic,
+                "kernel": "oz_gemm_kernel A-pass (Y=A X / Z=A^T Y): FP64 emulated from 8 x 8 "
+                          "signed 7-bit slices on tcgen05.mma.kind::i8, TMA-fed, TMEM accumulators",
+                "algorithmic_ops_per_launch": ops_per_launch,
+                "algorithmic_fp64_flops_per_launch": ap_flops_per_launch,
+                "fp64_equivalent_tflops": fp64_equiv,
+                "fp64_equivalent_vs_dmma_peak": (fp64_equiv / FP64_PEAK_TFLOPS) if fp64_equiv else None,
+                "peak_source": INT8_PEAK_SOURCE,
+                "slice_ms_per_step": slice_ms / prof_steps,
+                "apass_share_of_step": gemm_ms / prof_steps / step_ms_prof}
+    else:
+        roof = {"bound": "tensor", "achieved": fp64_equiv, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s",
+                "frac": (fp64_equiv / FP64_PEAK_TFLOPS) if fp64_equiv else None,
+                "traffic": traffic,
+                "kernel": "dgemm_tma_kernel A-pass (Y=A X / Z=A^T Y; TMA-fed DMMA), batched over the step",
+                "algorithmic_flops_per_launch": ap_flops_per_launch,
+                "peak_source": FP64_PEAK_SOURCE,
+                "apass_share_of_step": gemm_ms / prof_steps / step_ms_prof}
 
     # ---- end-to-end through the public API with pinned host buffers ---
     try:
@@ -593,14 +627,8 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": "truncations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "host_memory": "pinned" if e2e_pinned else "pageable"},
             "gpu_launches": launches,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
-                         "traffic": traffic,
-                         "kernel": "dgemm_tma_kernel A-pass (Y=A X / Z=A^T Y; TMA-fed DMMA), batched over the step",
-                         "algorithmic_flops_per_launch": ap_flops_per_launch,
-                         "peak_source": FP64_PEAK_SOURCE,
-                         "apass_share_of_step": ap_ms / prof_steps / step_ms_prof},
+            "roofline": roof,
+            "gemm_path": gemm_path,
             "pipeline": {"tflops_alg": falg * total * args.steps / (ms / 1000) / 1e12 / world,
                          "frac_fp64_peak": falg * B * args.steps / (ms / 1000) / 1e12 / FP64_PEAK_TFLOPS,
                          "stage_ms_per_step": {k2: v[0] / prof_steps for k2, v in prof.items()},

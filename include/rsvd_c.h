@@ -201,6 +201,9 @@ int rsvd_profile_enable(rsvd_handle handle, int on);
 int rsvd_profile_read(rsvd_handle handle, double* ms, int64_t* calls, int n);
 const char* rsvd_profile_stage_name(int i);
 int rsvd_last_jacobi_sweeps(rsvd_handle handle);
+/* Which FP64 GEMM ran the last rsvd's A-passes: 0 the DMMA (mma.sync .f64)
+ * GEMM, 1 the emulated-FP64 GEMM on the INT8 tensor cores (ozaki.cu). */
+int rsvd_last_gemm_path(rsvd_handle handle);
 
 /* rlftn::block_factorize<double>(a, chi, request, method) (blocks.cpp:38-118):
  * truncated factorization of a block-diagonal matrix with one dense block per
@@ -287,6 +290,14 @@ int rsvd_testing_dgemm(rsvd_handle handle, int trans_a, int64_t M, int64_t N, in
                        const double* A, int64_t lda, int64_t strideA, const double* B,
                        int64_t ldb, int64_t strideB, double* C, int64_t ldc, int64_t strideC,
                        int64_t batch);
+
+/* Testing hook: the emulated-FP64 GEMM of the A-passes (Ozaki slices on the
+ * INT8 tensor cores), same arguments as rsvd_testing_dgemm.  Needs M, N, K
+ * multiples of 16 and K <= 65536 (RSVD_ERR_INVALID otherwise). */
+int rsvd_testing_ozaki_gemm(rsvd_handle handle, int trans_a, int64_t M, int64_t N, int64_t K,
+                            const double* A, int64_t lda, int64_t strideA, const double* B,
+                            int64_t ldb, int64_t strideB, double* C, int64_t ldc, int64_t strideC,
+                            int64_t batch);
 
 #ifdef __cplusplus
 }

@@ -86,7 +86,13 @@ SIGNATURES = {
                                    ctypes.POINTER(_c_i64), _c_int]),
     "rsvd_profile_stage_name": (ctypes.c_char_p, [_c_int]),
     "rsvd_last_jacobi_sweeps": (_c_int, [_c_vp]),
+    "rsvd_last_gemm_path": (_c_int, [_c_vp]),
     "rsvd_testing_dgemm": (
+        _c_int,
+        [_c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
+         _c_i64, _c_i64, _c_i64],
+    ),
+    "rsvd_testing_ozaki_gemm": (
         _c_int,
         [_c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp, _c_i64, _c_i64, _c_dp,
          _c_i64, _c_i64, _c_i64],
@@ -285,3 +291,8 @@ def profile_read(handle: Handle) -> dict:
 
 def last_jacobi_sweeps(handle: Handle) -> int:
     return int(load().rsvd_last_jacobi_sweeps(handle.raw))
+
+
+def last_gemm_path(handle: Handle) -> str:
+    """'ozaki' (emulated FP64 on the INT8 tensor cores) or 'dmma'."""
+    return "ozaki" if load().rsvd_last_gemm_path(handle.raw) == 1 else "dmma"

@@ -119,6 +119,21 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
               cudaStream_t st);
 // gemm_tma.cu — TMA/mbarrier-fed variant of the 128 x 96 tile (no column map);
 // returns false (nothing launched) when the operands do not qualify.
+// ozaki.cu — FP64 GEMM emulated on the tcgen05 INT8 tensor cores.
+// oz_prepare_a slices A (rows x cols, column-major) once: sR row-major with
+// per-row exponents eRow (operand of C = A B), sC column-major with per-column
+// exponents eCol (operand of C = A^T B); each oz_slice_bytes(rows, cols, batch).
+// oz_slice_b slices the right operand B (K x N column-major) into sB / eB
+// (oz_slice_bytes(K, N, batch) bytes, N * batch ints); oz_gemm: C (M x N) =
+// op(A) B from the slices of op(A) (sA / eA, M x K, K-major) and of B.
+bool oz_supported(int64_t rows, int64_t cols, int64_t K);
+int64_t oz_slice_bytes(int64_t rows, int64_t cols, int64_t batch);
+void oz_prepare_a(CMatRef A, int64_t rows, int64_t cols, int64_t batch, int8_t* sR, int8_t* sC,
+                  int* eRow, int* eCol, cudaStream_t st);
+void oz_slice_b(CMatRef B, int64_t K, int64_t N, int64_t batch, int8_t* sB, int* eB,
+                cudaStream_t st);
+void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, const int8_t* sB,
+             const int* eB, MatRef C, int64_t batch, cudaStream_t st);
 bool dgemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef B, double* C,
                int64_t ldc, int64_t strideC, int64_t batch, int splits, int64_t kps, bool c_upper,
                const int* item_mask,

@@ -96,10 +96,12 @@ enum Stage : int {
   kStApply,       // Y T, completion, Rf2 Rf1
   kStJacobi,      // one-sided Jacobi on the l x l factor
   kStLift,        // spectrum, gathers, U = Q U~, V = Qb J, transposes
+  kStSlice,       // INT8 slicing of A and of the A-pass right operands (nested
+                  // inside apass_nn / apass_tn: subtract it for the GEMM alone)
   kNumStages
 };
 const char* const kStageNames[kNumStages] = {"omega", "apass_nn", "apass_tn", "gram",
-                                             "chol",  "apply",    "jacobi",   "lift"};
+                                             "chol",  "apply",    "jacobi",   "lift", "apass_slice"};
 
 struct Prof {
   bool on = false;
@@ -237,6 +239,7 @@ struct rsvd_context {
     s_in = s_out = nullptr;
   }
   int last_sweeps = 0;
+  int last_gemm_path = 0;  // 1: the last rsvd's A-passes ran on the emulated-FP64 INT8 path
   void drop_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -268,6 +271,12 @@ struct Buffers {
   unsigned* jflags;
   double* partial;
   int64_t partial_cap;
+  // Emulated-FP64 A-passes (ozaki.cu): slices of A in both K-major layouts,
+  // slices of the right operand, exponents (rows of A, columns of A, columns
+  // of the right operand).  ozR == nullptr: the A-passes run on DMMA.
+  int8_t *ozR, *ozC, *ozB;
+  int *ozErow, *ozEcol, *ozEb;
+  bool oz_ready;  // A sliced for this call
   // staging for host-pointer calls
   double *Ah, *Uh, *Vth, *Sh;
   Prof* prof;
@@ -292,9 +301,35 @@ int64_t partial_need(const Shape& s) {
   return need;
 }
 
+// The A-passes run on the INT8 tensor cores (Ozaki slices, ozaki.cu) when
+// the 128 x 64 output tiles of both directions fill the GPU (>= 90% of one
+// wave, last wave >= 3/4 full: C4, C5, 5-item C4 chunks).  Smaller shapes (C1,
+// C2, and C3's 160 tiles = two thin waves) stay on the split-K DMMA GEMM.
+// RSVD_FP64_GEMM=dmma forces the DMMA path (tests compare both).
+bool oz_wanted(const Shape& s) {
+  static const bool off = [] {
+    const char* e = std::getenv("RSVD_FP64_GEMM");
+    return e && std::string(e) == "dmma";
+  }();
+  if (off || !oz_supported(s.m, s.n, s.ellp) || s.m > 65536 || s.n > 65536) return false;
+  const int64_t nt = ceil_div(s.ellp, 64), sm = num_sms();
+  auto fills = [&](int64_t tiles) {
+    return tiles * 10 >= sm * 9 && tiles * 4 >= ceil_div(tiles, sm) * sm * 3;
+  };
+  return fills(ceil_div(s.m, 128) * nt * s.batch) && fills(ceil_div(s.n, 128) * nt * s.batch);
+}
+
 Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {
   Buffers B{};
   const int64_t b = s.batch, lp = s.ellp;
+  if (oz_wanted(s)) {
+    B.ozR = c.take<int8_t>(oz_slice_bytes(s.m, s.n, b));
+    B.ozC = c.take<int8_t>(oz_slice_bytes(s.m, s.n, b));
+    B.ozB = c.take<int8_t>(oz_slice_bytes(std::max(s.m, s.n), lp, b));
+    B.ozErow = c.take<int>(s.m * b);
+    B.ozEcol = c.take<int>(s.n * b);
+    B.ozEb = c.take<int>(lp * b);
+  }
   B.seeds = c.take<uint64_t>(b);
   B.scale = c.take<double>(b);
   B.X = c.take<double>(b * s.n * lp);
@@ -491,6 +526,29 @@ void orth(const Shape& s, Buffers& B, double*& Yb, double*& Tmp, int64_t rows, d
   if (passes % 2 == 1) std::swap(Yb, Tmp);
 }
 
+// A-pass with the caller's A: C = A X (NN: m x l_p, K = n) or C = A^T Y (TN:
+// n x l_p, K = m).  On the emulated-FP64 path A is sliced once per call, at
+// its first pass.  (A null slice buffer in a chunk's Buffers is the host
+// pipeline's measuring carve: never launched.)
+void apass(const Shape& s, Buffers& B, CMatRef A, bool trans, CMatRef R, MatRef C, cudaStream_t st) {
+  const int64_t lp = s.ellp, b = s.batch;
+  if (B.ozR) {
+    const int64_t M = trans ? s.n : s.m, K = trans ? s.m : s.n;
+    {
+      Scope sc(B.prof, kStSlice, st);
+      if (!B.oz_ready) {
+        oz_prepare_a(A, s.m, s.n, b, B.ozR, B.ozC, B.ozErow, B.ozEcol, st);
+        B.oz_ready = true;
+      }
+      oz_slice_b(R, K, lp, b, B.ozB, B.ozEb, st);
+    }
+    oz_gemm(M, lp, K, trans ? B.ozC : B.ozR, trans ? B.ozEcol : B.ozErow, B.ozB, B.ozEb, C, b, st);
+    return;
+  }
+  if (trans) dgemm(true, s.n, lp, s.m, A, R, C, b, B.partial, B.partial_cap, st);
+  else dgemm(false, s.m, lp, s.n, A, R, C, b, B.partial, B.partial_cap, st);
+}
+
 // randomized_range (factorize.cpp:52-74): leaves Q (orthonormal) in B.Y.
 void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
   const int64_t lp = s.ellp, b = s.batch;
@@ -506,8 +564,7 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
   const bool do_scale = !B.red;
   auto nn = [&] {
     Scope sc(P, kStApassNN, st);
-    dgemm(false, s.m, lp, s.n, A, MatRef{B.X, s.n, s.n * lp}, MatRef{B.Y, s.m, s.m * lp}, b,
-          B.partial, B.partial_cap, st);
+    apass(s, B, A, false, MatRef{B.X, s.n, s.n * lp}, MatRef{B.Y, s.m, s.m * lp}, st);
     if (do_scale) {
       if (!B.scaled) {
         launch_choose_scale(MatRef{B.Y, s.m, s.m * lp}, s.m, s.ell, B.scale, b, st);
@@ -518,12 +575,12 @@ void range_finder(const Shape& s, Buffers& B, CMatRef A, cudaStream_t st) {
   };
   auto tn = [&] {
     Scope sc(P, kStApassTN, st);
-    dgemm(true, s.n, lp, s.m, A, MatRef{B.Y, s.m, s.m * lp}, MatRef{B.X, s.n, s.n * lp}, b,
-          B.partial, B.partial_cap, st);
+    apass(s, B, A, true, MatRef{B.Y, s.m, s.m * lp}, MatRef{B.X, s.n, s.n * lp}, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // Z = sum_p A_p^T Q_p
     if (do_scale) launch_apply_scale(MatRef{B.X, s.n, s.n * lp}, s.n, lp, B.scale, 0, b, st);
   };
   B.scaled = false;
+  B.oz_ready = false;
   nn();
   uint64_t tag = kCompletionTag;
   // Only the last orthonormalisation feeds B = Q^T A and U = Q U~; the
@@ -555,7 +612,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
   // B^T = A^T Q (n x ellp), then B^T = Qb Rt.
   {
     Scope sc(P, kStApassTN, st);
-    dgemm(true, s.n, lp, s.m, A, Y, X, b, B.partial, B.partial_cap, st);
+    apass(s, B, A, true, Y, X, st);
     if (B.red) B.red->allreduce_sum(B.X, b * s.n * lp, st);  // B^T = sum_p A_p^T Q_p
     if (!B.red) {
       if (!B.scaled) {  // tsvd (Q = I): choose the scale from B^T = A_e^T
@@ -571,7 +628,7 @@ void svd_stage(const Shape& s, Buffers& B, CMatRef A, MatRef U, double* S, int64
     Scope sc(P, kStJacobi, st);
     if (exact_h) {
       RSVD_CUDA(cudaMemsetAsync(B.H, 0, sizeof(double) * b * lp * lp, st));
-      dgemm(false, s.m, lp, s.n, A, Qb, MatRef{B.H, lp, lp * lp}, b, B.partial, B.partial_cap, st);
+      apass(s, B, A, false, Qb, MatRef{B.H, lp, lp * lp}, st);
       if (!B.red && B.scaled) launch_apply_scale(MatRef{B.H, lp, lp * lp}, s.m, lp, B.scale, 0, b, st);
     } else {
       launch_transpose(MatRef{B.Rt, lp, lp * lp}, lp, lp, MatRef{B.H, lp, lp * lp}, b, st);
@@ -708,6 +765,7 @@ void rsvd_host_pipelined(rsvd_context* h, const Shape& full, int64_t nchunks, co
   if (h->arena.base != before) h->drop_graphs();
   Carver cv{h->arena.base};
   layout(cv);
+  h->last_gemm_path = B[0].ozR ? 1 : 0;
   cudaStream_t cs[4] = {st, h->s_c2, h->s_c3, h->s_c4};
   // 3 compute streams measured best on C4 (2: 295, 3: 319 trunc/s); uneven
   // chunk sizes (small first / last chunks) and 4 streams measured no better
@@ -915,6 +973,7 @@ void rsvd_batched_impl(rsvd_context* h, int64_t batch, const double* A, int64_t 
   if (h->arena.base != arena_before) h->drop_graphs();
   Carver cv{h->arena.base};
   Buffers B = carve(cv, s, host, true);
+  h->last_gemm_path = B.ozR ? 1 : 0;
 
   if (h->pin.reserve(batch)) h->drop_graphs();
   std::memcpy(h->pin.seeds, seeds, sizeof(uint64_t) * batch);
@@ -1327,6 +1386,7 @@ const char* rsvd_profile_stage_name(int i) {
 }
 
 int rsvd_last_jacobi_sweeps(rsvd_handle h) { return h ? h->last_sweeps : -1; }
+int rsvd_last_gemm_path(rsvd_handle h) { return h ? h->last_gemm_path : -1; }
 
 int rsvd_destroy(rsvd_handle h) {
   if (!h) return RSVD_ERR_INVALID;
@@ -1521,6 +1581,36 @@ int rsvd_testing_dgemm(rsvd_handle h, int trans_a, int64_t M, int64_t N, int64_t
     rsvd::dgemm(trans_a != 0, M, N, K, rsvd::CMatRef{A, lda, strideA},
                 rsvd::CMatRef{B, ldb, strideB}, rsvd::MatRef{C, ldc, strideC}, batch,
                 reinterpret_cast<double*>(h->arena.base), need, h->stream);
+    RSVD_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int rsvd_testing_ozaki_gemm(rsvd_handle h, int trans_a, int64_t M, int64_t N, int64_t K,
+                            const double* A, int64_t lda, int64_t strideA, const double* B,
+                            int64_t ldb, int64_t strideB, double* C, int64_t ldc, int64_t strideC,
+                            int64_t batch) {
+  return rsvd::guarded(h, [&] {
+    RSVD_CUDA(cudaSetDevice(h->device));
+    if (!rsvd::oz_supported(M, N, K) || batch < 1)
+      throw rsvd::InvalidArgument("ozaki_gemm: M, N, K must be multiples of 16, K <= 65536");
+    // stored A: M x K (NN) or K x M (TN)
+    const int64_t rows = trans_a ? K : M, cols = trans_a ? M : K;
+    const int64_t sa = rsvd::oz_slice_bytes(rows, cols, batch), sb = rsvd::oz_slice_bytes(K, N, batch);
+    const int64_t ints = (rows + cols + N) * batch;
+    const size_t bytes = 2 * sa + sb + sizeof(int) * ints + 1024;
+    h->arena.reserve(bytes);
+    char* base = reinterpret_cast<char*>(h->arena.base);
+    int8_t* sR = reinterpret_cast<int8_t*>(base);
+    int8_t* sC = sR + sa;
+    int8_t* sB = sC + sa;
+    int* eRow = reinterpret_cast<int*>(base + ((2 * sa + sb + 255) / 256) * 256);
+    int* eCol = eRow + rows * batch;
+    int* eB = eCol + cols * batch;
+    rsvd::oz_prepare_a(rsvd::CMatRef{A, lda, strideA}, rows, cols, batch, sR, sC, eRow, eCol,
+                       h->stream);
+    rsvd::oz_slice_b(rsvd::CMatRef{B, ldb, strideB}, K, N, batch, sB, eB, h->stream);
+    rsvd::oz_gemm(M, N, K, trans_a ? sC : sR, trans_a ? eCol : eRow, sB, eB,
+                  rsvd::MatRef{C, ldc, strideC}, batch, h->stream);
     RSVD_CUDA(cudaStreamSynchronize(h->stream));
   });
 }

@@ -1,0 +1,497 @@
+// FP64 GEMM emulated on the tcgen05 INT8 tensor cores (Ozaki scheme, split
+// into signed 7-bit slices), for the RSVD A-passes Y = A X and Z = A^T Y
+// (factorize.cpp:68, 70, 71, 86).
+//
+// B200 has no tcgen05 f64 kind: the warp-level DMMA path (gemm_tma.cu) tops
+// out at ~37 TFLOP/s.  The INT8 tensor cores run ~4.5 POPS dense, so an FP64
+// product rebuilt from exact integer products of short slices is faster even
+// after paying for the slice products:
+//   x = 2^e * sum_{p<S} s_p 2^(-6-7p),   s_p in [-64, 64]  (exact split, e per
+//       row of op(A) / per column of B; S = 8 slices = 55 bits below 2^e)
+//   (A B)_ij = 2^(eA_i + eB_j - 12) * sum_{d<S} 2^(-7d) * sum_{p+q=d} (A_p B_q)_ij
+// Every slice product is exact in INT32 (|s| <= 64, K <= 65536, <= 8 terms
+// per diagonal); the terms with p + q >= S are below 2^-56 of the row/column
+// maxima and are dropped, which leaves a normwise error of the order of an
+// FP64 GEMM's.
+//
+// Layout.  A is sliced ONCE per rsvd call into both K-major layouts:
+//   R: slices of A with per-row exponents, row-major  [item][p][row][col]
+//      (the K-major operand of the NN pass  Y = A X)
+//   C: slices of A with per-column exponents, col-major [item][p][col][row]
+//      (the K-major operand of the TN pass  Z = A^T Y)
+// The small right operand (X or Y, K x N column-major = K-major) is sliced per
+// pass.  A CTA owns a 128 x BN output tile and keeps the S diagonal sums in
+// TMEM (S * BN = 512 columns); per 32-byte K step one TMA box brings the S
+// slices of each operand (32B swizzle), and one thread issues the S(S+1)/2
+// tcgen05.mma.kind::i8 of that step.  The epilogue folds the diagonals in
+// FP64 (Horner in 2^-7) and writes C column-major.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <climits>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace rsvd {
+namespace {
+
+constexpr int kOzS = 8;       // slices per operand
+constexpr int kOzBM = 128;    // UMMA M
+constexpr int kOzBN = 64;     // UMMA N (S * BN = 512 TMEM columns)
+constexpr int kOzKC = 32;     // K bytes per stage = one MMA K step = one 32B swizzle row
+constexpr int kOzStages = 4;  // 4 x 48 KB ring
+constexpr int kExpNone = INT_MIN;
+
+__device__ __forceinline__ uint32_t sm_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mb_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "OZW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra OZW_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                       int c3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_c),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// K-major operand tile of `rows` x 32 bytes with the 32-byte swizzle: 8-row
+// core groups 256 bytes apart (SBO), LBO unused, descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(6) << 61);
+}
+
+__device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }
+
+// Signed 7-bit slices of x * 2^-e (|x| < 2^e): exact.
+template <int S>
+__device__ __forceinline__ void split_value(double x, int e, int8_t (&s)[S]) {
+  double v = ldexp(x, 6 - e);  // in (-64, 64)
+#pragma unroll
+  for (int p = 0; p < S; ++p) {
+    const double t = rint(v);
+    s[p] = static_cast<int8_t>(static_cast<int>(t));
+    v = (v - t) * 128.0;
+  }
+}
+
+// Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16 bytes.
+template <class Get>
+__device__ __forceinline__ void pack16(Get get, int e, uint4 (&out)[kOzS]) {
+  uint32_t w[kOzS][4];
+#pragma unroll
+  for (int p = 0; p < kOzS; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[p][q] = 0u;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    int8_t s[kOzS];
+    split_value<kOzS>(get(u), e, s);
+#pragma unroll
+    for (int p = 0; p < kOzS; ++p)
+      w[p][u >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(s[p])) << (8 * (u & 3));
+  }
+#pragma unroll
+  for (int p = 0; p < kOzS; ++p) out[p] = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+__device__ __forceinline__ int exp_of_max(double amax) {
+  int e;
+  frexp(amax, &e);
+  return e;  // amax < 2^e
+}
+
+// Per-row and per-column exponents of A (rows x cols, column-major): 64 x 64
+// tiles, atomicMax into eRow / eCol (pre-set to kExpNone).
+__global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ A, int64_t lda,
+                                                     int64_t sA, int rows, int cols, int* eRow,
+                                                     int* eCol) {
+  __shared__ double rmax[4][64];
+  __shared__ double cmax[2][64];
+  const int item = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Ab = A + item * sA;
+  const int i = i0 + tx;
+  double rm = 0.0;
+  for (int c = ty; c < 64; c += 4) {
+    const int j = j0 + c;
+    double v = 0.0;
+    if (i < rows && j < cols) v = fabs(Ab[i + static_cast<int64_t>(j) * lda]);
+    rm = fmax(rm, v);
+    double w = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+    if (lane == 0) cmax[(warp & 1)][c] = w;  // warps 2t, 2t+1 hold rows 0-31 / 32-63 of column c
+    __syncwarp();
+  }
+  rmax[ty][tx] = rm;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const double r = fmax(fmax(rmax[0][tx], rmax[1][tx]), fmax(rmax[2][tx], rmax[3][tx]));
+    if (i < rows && r > 0.0) atomicMax(&eRow[static_cast<int64_t>(item) * rows + i], exp_of_max(r));
+  } else if (threadIdx.x < 128) {
+    const int c = threadIdx.x - 64, j = j0 + c;
+    const double r = fmax(cmax[0][c], cmax[1][c]);
+    if (j < cols && r > 0.0) atomicMax(&eCol[static_cast<int64_t>(item) * cols + j], exp_of_max(r));
+  }
+}
+
+// Slices of A in both K-major layouts (rows, cols multiples of 16):
+//   sR[item][p][i][j] with eRow[i]   and   sC[item][p][j][i] with eCol[j].
+__global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restrict__ A, int64_t lda,
+                                                         int64_t sA, int rows, int cols,
+                                                         const int* __restrict__ eRow,
+                                                         const int* __restrict__ eCol,
+                                                         int8_t* __restrict__ sR,
+                                                         int8_t* __restrict__ sC) {
+  __shared__ double tile[64][65];  // [col][row]
+  const int item = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const double* Ab = A + item * sA;
+  for (int t = threadIdx.x; t < 64 * 64; t += 256) {
+    const int r = t & 63, c = t >> 6;
+    const int i = i0 + r, j = j0 + c;
+    tile[c][r] = (i < rows && j < cols) ? Ab[i + static_cast<int64_t>(j) * lda] : 0.0;
+  }
+  __syncthreads();
+  const int64_t plane = static_cast<int64_t>(rows) * cols;
+  const int a = threadIdx.x >> 2, part = (threadIdx.x & 3) * 16;
+  // column-major slices: column j0 + a, rows i0 + part .. +15
+  {
+    const int j = j0 + a;
+    if (j < cols && i0 + part < rows) {
+      const int e = usable_exp(eCol[static_cast<int64_t>(item) * cols + j]);
+      uint4 out[kOzS];
+      pack16([&](int u) { return tile[a][part + u]; }, e, out);
+      int8_t* dst = sC + item * kOzS * plane + static_cast<int64_t>(j) * rows + i0 + part;
+#pragma unroll
+      for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
+    }
+  }
+  // row-major slices: row i0 + a, columns j0 + part .. +15
+  {
+    const int i = i0 + a;
+    if (i < rows && j0 + part < cols) {
+      const int e = usable_exp(eRow[static_cast<int64_t>(item) * rows + i]);
+      uint4 out[kOzS];
+      pack16([&](int u) { return tile[part + u][a]; }, e, out);
+      int8_t* dst = sR + item * kOzS * plane + static_cast<int64_t>(i) * cols + j0 + part;
+#pragma unroll
+      for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
+    }
+  }
+}
+
+// Slices of the right operand B (K x N column-major, K % 16 == 0) with one
+// exponent per column: sB[item][p][j][k], eB[item][j].  One CTA per column.
+__global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restrict__ B, int64_t ldb,
+                                                         int64_t sBst, int K, int N,
+                                                         int8_t* __restrict__ sB, int* eB) {
+  __shared__ double red[8];
+  __shared__ int eshared;
+  const int j = blockIdx.x, item = blockIdx.y;
+  const double* col = B + item * sBst + static_cast<int64_t>(j) * ldb;
+  double m = 0.0;
+  for (int k = threadIdx.x; k < K; k += 256) m = fmax(m, fabs(col[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = red[0];
+    for (int w = 1; w < 8; ++w) r = fmax(r, red[w]);
+    const int e = r > 0.0 ? exp_of_max(r) : 0;
+    eshared = e;
+    eB[static_cast<int64_t>(item) * N + j] = e;
+  }
+  __syncthreads();
+  const int e = eshared;
+  const int64_t plane = static_cast<int64_t>(N) * K;
+  int8_t* dst = sB + item * kOzS * plane + static_cast<int64_t>(j) * K;
+  for (int k0 = threadIdx.x * 16; k0 < K; k0 += 256 * 16) {
+    uint4 out[kOzS];
+    pack16([&](int u) { return col[k0 + u]; }, e, out);
+#pragma unroll
+    for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane + k0) = out[p];
+  }
+}
+
+struct OzArgs {
+  int M, N, K;
+  double* C;
+  int64_t ldc, strideC;
+  const int* eA;  // per row of op(A): eA[item * M + i]
+  const int* eB;  // per column of B:  eB[item * N + j]
+};
+
+constexpr int kOzBytesA = kOzS * kOzBM * kOzKC;
+constexpr int kOzBytesB = kOzS * kOzBN * kOzKC;
+constexpr int kOzStage = kOzBytesA + kOzBytesB;
+constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 256;
+
+// One 128 x BN tile of C per CTA.  Warp 0 lane 0: TMA producer; warp 1 lane 0:
+// MMA issuer; warp 2 owns the TMEM allocation; all four warps drain TMEM
+// (warp w reads lanes 32w..32w+31 = tile rows).
+__global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const OzArgs p) {
+  extern __shared__ __align__(1024) unsigned char oz_smem[];
+  const uint32_t raw = sm_addr(oz_smem);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* sgen = oz_smem + (sbase - raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sgen + kOzStages * kOzStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kOzStages + 1);
+  const uint32_t bar0 = sm_addr(bars);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kOzStages + s); };
+  const uint32_t done_bar = bar0 + 8u * (2 * kOzStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kOzBN, m0 = blockIdx.y * kOzBM, item = blockIdx.z;
+  const int nk = (p.K + kOzKC - 1) / kOzKC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      mb_init(full_bar(s), 1);
+      mb_init(empty_bar(s), 1);
+    }
+    mb_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     sm_addr(tmem_slot)),
+                 "r"(kOzS * kOzBN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int kc = 0; kc < nk; ++kc) {
+      const int s = kc % kOzStages;
+      if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
+      const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
+      mb_expect_tx(full_bar(s), kOzStage);
+      tma_4d(dA, &tmA, kc * kOzKC, m0, 0, item, full_bar(s));
+      tma_4d(dB, &tmB, kc * kOzKC, n0, 0, item, full_bar(s));
+    }
+  } else if (warp == 1 && lane == 0) {
+    // kind::i8: D s32 (bits 4-5 = 2), A/B signed (bits 7, 10), K-major, N >> 3 at 17, M >> 4 at 24.
+    // The S slices of B sit back to back in shared memory (slice q = rows
+    // q*BN .. q*BN+BN-1 of one K-major tile) and diagonal d's accumulator at
+    // TMEM columns d*BN, so A_p times slices q0 .. q0+nq-1 is ONE MMA of
+    // N = nq*BN into columns (p+q0)*BN onward: up to 256-wide MMAs, which keep
+    // the tensor core's shared-memory operand reads under the SM's bandwidth
+    // (a 128 x 64 x 32 MMA is smem-bound at 48 cycles, 256-wide runs at N/2).
+    constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) |
+                                (static_cast<uint32_t>(kOzBM >> 4) << 24);
+    constexpr int kQ = 256 / kOzBN;  // B slices per MMA
+    for (int kc = 0; kc < nk; ++kc) {
+      const int s = kc % kOzStages;
+      mb_wait(full_bar(s), (kc / kOzStages) & 1);
+      tc_fence_after();
+      const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
+#pragma unroll
+      for (int pa = 0; pa < kOzS; ++pa) {
+        const uint64_t da = umma_desc_sw32(dA + pa * (kOzBM * kOzKC));
+#pragma unroll
+        for (int q0 = 0; q0 < kOzS - pa; q0 += kQ) {
+          const int nq = (kOzS - pa - q0) < kQ ? (kOzS - pa - q0) : kQ;
+          const uint64_t db = umma_desc_sw32(dB + q0 * (kOzBN * kOzKC));
+          const uint32_t idesc = idesc0 | (static_cast<uint32_t>((nq * kOzBN) >> 3) << 17);
+          tc_mma_i8(tmem + static_cast<uint32_t>((pa + q0) * kOzBN), da, db, idesc,
+                    (kc > 0 || pa > 0) ? 1u : 0u);
+        }
+      }
+      tc_commit(empty_bar(s));
+    }
+    tc_commit(done_bar);
+  }
+  __syncwarp();
+  mb_wait(done_bar, 0);
+  __syncwarp();
+  tc_fence_after();
+
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < p.M;
+  const int ea = row_ok ? usable_exp(p.eA[static_cast<int64_t>(item) * p.M + row]) : 0;
+  double* Cb = p.C + item * p.strideC;
+  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+  for (int c0 = 0; c0 < kOzBN; c0 += 16) {
+    if (n0 + c0 >= p.N) break;
+    double t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = 0.0;
+#pragma unroll 1
+    for (int d = kOzS - 1; d >= 0; --d) {
+      uint32_t r[16];
+      tc_ld16(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        t[j] = fma(t[j], 0.0078125, static_cast<double>(static_cast<int>(r[j])));
+    }
+    if (row_ok) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = n0 + c0 + j;
+        if (col < p.N) {
+          const int eb = usable_exp(p.eB[static_cast<int64_t>(item) * p.N + col]);
+          Cb[row + static_cast<int64_t>(col) * p.ldc] = ldexp(t[j], ea + eb - 12);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(kOzS * kOzBN)
+                 : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r{};
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &q, 12000, cudaEnableDefault,
+                                         &r) == cudaSuccess &&
+        r == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(q);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// [item][p][rows][K] int8 slices, K contiguous; box {32 K, box_rows, S, 1}.
+bool oz_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64_t batch,
+            int box_rows) {
+  auto fn = oz_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(kOzS), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K * rows),
+                             static_cast<cuuint64_t>(K * rows * kOzS)};
+  const cuuint32_t box[4] = {kOzKC, static_cast<cuuint32_t>(box_rows), kOzS, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool oz_supported(int64_t rows, int64_t cols, int64_t K) {
+  return rows % 16 == 0 && cols % 16 == 0 && K % 16 == 0 && K <= 65536 && rows < (1ll << 31) &&
+         cols < (1ll << 31);
+}
+
+int64_t oz_slice_bytes(int64_t rows, int64_t cols, int64_t batch) {
+  return kOzS * rows * cols * batch;
+}
+
+void oz_prepare_a(CMatRef A, int64_t rows, int64_t cols, int64_t batch, int8_t* sR, int8_t* sC,
+                  int* eRow, int* eCol, cudaStream_t st) {
+  RSVD_CUDA(cudaMemsetAsync(eRow, 0x80, sizeof(int) * rows * batch, st));
+  RSVD_CUDA(cudaMemsetAsync(eCol, 0x80, sizeof(int) * cols * batch, st));
+  // 0x80808080 < any frexp exponent; usable_exp maps it to 0 (an all-zero line).
+  dim3 grid(static_cast<unsigned>(ceil_div(cols, 64)), static_cast<unsigned>(ceil_div(rows, 64)),
+            static_cast<unsigned>(batch));
+  oz_exp_kernel<<<grid, 256, 0, st>>>(A.base, A.ld, A.stride, static_cast<int>(rows),
+                                      static_cast<int>(cols), eRow, eCol);
+  RSVD_LAUNCH("oz_exp_kernel");
+  oz_slice_a_kernel<<<grid, 256, 0, st>>>(A.base, A.ld, A.stride, static_cast<int>(rows),
+                                          static_cast<int>(cols), eRow, eCol, sR, sC);
+  RSVD_LAUNCH("oz_slice_a_kernel");
+}
+
+void oz_slice_b(CMatRef B, int64_t K, int64_t N, int64_t batch, int8_t* sB, int* eB,
+                cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(N), static_cast<unsigned>(batch));
+  oz_slice_b_kernel<<<grid, 256, 0, st>>>(B.base, B.ld, B.stride, static_cast<int>(K),
+                                          static_cast<int>(N), sB, eB);
+  RSVD_LAUNCH("oz_slice_b_kernel");
+}
+
+void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, const int8_t* sB,
+             const int* eB, MatRef C, int64_t batch, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  if (!oz_map(&ma, sA, K, M, batch, kOzBM) || !oz_map(&mb, sB, K, N, batch, kOzBN))
+    throw CudaError("oz_gemm: cuTensorMapEncodeTiled failed");
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
+    RSVD_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kOzSmem));
+  });
+  OzArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), C.base, C.ld, C.stride,
+           eA, eB};
+  dim3 grid(static_cast<unsigned>(ceil_div(N, kOzBN)), static_cast<unsigned>(ceil_div(M, kOzBM)),
+            static_cast<unsigned>(batch));
+  oz_gemm_kernel<<<grid, 128, kOzSmem, st>>>(ma, mb, a);
+  RSVD_LAUNCH("oz_gemm_kernel");
+}
+
+}  // namespace rsvd

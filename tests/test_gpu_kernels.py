@@ -46,7 +46,7 @@ def test_device_gaussian_large_stream_vs_oracle(cuda, oracle_mod):
     assert np.mean(d == 0) > 0.5
 
 
-def _dgemm(trans_a, A, B, M, N, K, batch, lda, ldb, sA, sB):
+def _dgemm(trans_a, A, B, M, N, K, batch, lda, ldb, sA, sB, fn="rsvd_testing_dgemm"):
     import torch
     from paper_1710_01463_b200 import _lib
 
@@ -55,8 +55,8 @@ def _dgemm(trans_a, A, B, M, N, K, batch, lda, ldb, sA, sB):
     lib = _lib.load()
     lib.rsvd_set_stream(h.raw, ctypes.c_void_p(_lib.torch_stream_ptr()))
     try:
-        rc = lib.rsvd_testing_dgemm(h.raw, int(trans_a), M, N, K, A.data_ptr(), lda, sA,
-                                    B.data_ptr(), ldb, sB, C.data_ptr(), M, M * N, batch)
+        rc = getattr(lib, fn)(h.raw, int(trans_a), M, N, K, A.data_ptr(), lda, sA,
+                              B.data_ptr(), ldb, sB, C.data_ptr(), M, M * N, batch)
     finally:
         lib.rsvd_set_stream(h.raw, None)
     _lib.raise_for(rc, h.raw)
@@ -101,3 +101,61 @@ def test_dgemm_odd_leading_dimension(cuda):
     C = _dgemm(False, A2, B, M, N, K, 1, M, K, 0, 0)[0]
     ref = A2.t() @ B.t()
     assert (C - ref).abs().max().item() < 1e-12
+
+
+@pytest.mark.parametrize("trans_a", [False, True])
+@pytest.mark.parametrize(
+    "M,N,K,batch,grade",
+    [(128, 64, 32, 1, 0), (128, 48, 64, 2, 0), (256, 288, 512, 3, 0), (1024, 80, 1024, 1, 0),
+     (1024, 96, 2048, 2, 12), (4096, 288, 4096, 2, 0), (2048, 544, 32768, 1, 0),
+     (512, 64, 256, 1, 300)],
+)
+def test_ozaki_gemm_vs_torch(cuda, trans_a, M, N, K, batch, grade):
+    """Emulated FP64 (8 signed 7-bit slices per operand on the INT8 tensor
+    cores, ozaki.cu) against torch float64: elementwise within 8e-15 of
+    |op(A)| |B| (an FP64 GEMM's K u |A||B| bound is ~1e-12 here), normwise
+    within 1e-14; `grade` spreads the K columns of op(A) over 10^-grade
+    (per-row exponents keep the small entries), 300 = extreme magnitudes."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(M * 5 + N * 11 + K)
+    opA = torch.randn(batch, M, K, dtype=torch.float64, device=cuda, generator=g)
+    if grade == 300:
+        opA = opA * 1e-300
+    elif grade:
+        opA = opA * torch.logspace(0, -grade, K, dtype=torch.float64, device=cuda)
+    if trans_a:
+        Aflat, lda = opA.contiguous(), K  # stored K x M column-major
+    else:
+        Aflat, lda = opA.transpose(1, 2).contiguous(), M  # stored M x K
+    B = torch.randn(batch, N, K, dtype=torch.float64, device=cuda, generator=g)
+    if grade == 300:
+        B = B * 1e250
+    C = _dgemm(trans_a, Aflat, B, M, N, K, batch, lda, K, M * K, N * K, fn="rsvd_testing_ozaki_gemm")
+    ref = torch.matmul(opA, B.transpose(1, 2))
+    bound = torch.matmul(opA.abs(), B.abs().transpose(1, 2))
+    assert ((C - ref).abs() <= 8e-15 * bound).all(), ((C - ref).abs() / bound).max().item()
+    assert ((C - ref).norm() / ref.norm()).item() < 1e-14
+
+
+def test_ozaki_gemm_zero_lines_and_rejects(cuda):
+    """All-zero rows / columns (no exponent) give exact zeros; shapes off the
+    16-multiple grid are refused with InvalidArgument."""
+    import torch
+
+    from paper_1710_01463_b200 import InvalidArgument
+
+    M, N, K = 256, 64, 128
+    opA = torch.randn(1, M, K, dtype=torch.float64, device=cuda)
+    opA[:, 5, :] = 0
+    opA[:, :, 7] = 0
+    B = torch.randn(1, N, K, dtype=torch.float64, device=cuda)
+    B[:, 3, :] = 0
+    C = _dgemm(False, opA.transpose(1, 2).contiguous(), B, M, N, K, 1, M, K, M * K, N * K,
+               fn="rsvd_testing_ozaki_gemm")
+    ref = torch.matmul(opA, B.transpose(1, 2))
+    assert (C[0, 5, :] == 0).all() and (C[0, :, 3] == 0).all()
+    assert ((C - ref).abs().max() <= 1e-13 * ref.abs().max()).item()
+    with pytest.raises(InvalidArgument):
+        _dgemm(False, opA.transpose(1, 2).contiguous(), B, M, N, K - 8, 1, M, K, M * K, N * K,
+               fn="rsvd_testing_ozaki_gemm")

@@ -355,3 +355,48 @@ def test_graph_replay_equals_direct_launches(cuda, tmp_path):
                        check=True, env=env, timeout=300)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+_GEMM_PATH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1710_01463_b200 import RsvdParams, rsvd_batched, synth
+cfg = synth.CONFIGS["C4"]
+A = synth.make_batch(cfg, device="cuda:0")[:8].contiguous()
+seeds = synth.omega_seeds(cfg)[:8]
+f = rsvd_batched(A, RsvdParams(cfg.rank, cfg.ell, cfg.power, 0), seeds)
+torch.cuda.synchronize()
+r = min(f.ranks)
+np.savez({out!r}, s=f.sigma[:, :r].cpu().numpy(), u=f.left[:, :, :r].cpu().numpy(),
+         dw=np.array(f.discarded_weight))
+"""
+
+
+def test_ozaki_and_dmma_a_passes_agree(cuda, tmp_path):
+    """The emulated-FP64 A-passes (INT8 tensor cores, the default for C4-sized
+    batches) and RSVD_FP64_GEMM=dmma give the same factorization of 8 C4 items
+    to the north_star tolerances (sigma 1e-10 relative, U to 1e-8 in subspace
+    distance on the gapped prefix, discarded weight 1e-8)."""
+    import os
+    import subprocess
+    import sys
+
+    from tests.helpers import subspace_distance
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for path in ("ozaki", "dmma"):
+        out = str(tmp_path / f"{path}.npz")
+        env = dict(os.environ)
+        env.pop("RSVD_FP64_GEMM", None)
+        if path == "dmma":
+            env["RSVD_FP64_GEMM"] = "dmma"
+        subprocess.run([sys.executable, "-c", _GEMM_PATH_SCRIPT.format(root=root, out=out)],
+                       check=True, env=env, timeout=600)
+        res[path] = np.load(out)
+    s0, s1 = res["ozaki"]["s"], res["dmma"]["s"]
+    assert np.max(np.abs(s0 - s1) / s1[:, :1]) < 1e-12
+    assert np.max(np.abs(s0 - s1) / s1) < 1e-10
+    for b in range(s0.shape[0]):
+        assert subspace_distance(res["ozaki"]["u"][b, :, :200], res["dmma"]["u"][b, :, :200]) < 1e-8
+    assert np.allclose(res["ozaki"]["dw"], res["dmma"]["dw"], rtol=1e-8, atol=0)
