@@ -44,7 +44,7 @@ INT8_PEAK_TOPS = 8186 * 148 * 2 * 1.965e9 / 1e12  # tcgen05.mma kind::i8 rate, p
 INT8_PEAK_SOURCE = ("measured tcgen05.mma.kind::i8 issue rate, 8186 MAC/clk/SM for N >= 128 "
                     "(profiles/r02_umma_rate.txt) x 148 SMs x 2 x the 1965 MHz max SM clock; "
                     "MEASURED_PEAKS.json has no INT8 figure")
-OZ_SLICE_PRODUCTS = 36  # 8 slices per operand, products p + q < 8 (ozaki.cu)
+OZ_SLICE_PRODUCTS = 28  # 7 slices per operand, products p + q < 7 (ozaki.cu)
 FP64_PEAK_TFLOPS = 37.1  # measured: mma.sync f64 probe, profiles/r01_fp64_peak.txt
 FP64_PEAK_SOURCE = ("measured DMMA (mma.sync .f64) throughput on this pool's B200, "
                     "profiles/r01_fp64_peak.txt; MEASURED_PEAKS.json has no FP64 figure "
@@ -552,8 +552,8 @@ def run_ours(args, rank, world, local_rank):
         achieved = ops_per_launch / (gemm_ms / ap_calls / 1000.0) / 1e12 if ap_calls else None
         roof = {"bound": "tensor", "achieved": achieved, "peak": INT8_PEAK_TOPS, "unit": "TOP/s",
                 "frac": (achieved / INT8_PEAK_TOPS) if achieved else None, "traffic": traffic,
-                "kernel": "oz_gemm_kernel A-pass (Y=A X / Z=A^T Y): FP64 emulated from 8 x 8 "
-                          "signed 7-bit slices on tcgen05.mma.kind::i8, TMA-fed, TMEM accumulators",
+                "kernel": "oz_gemm_kernel A-pass (Y=A X / Z=A^T Y): FP64 emulated from 7 x 7 "
+                          "signed 8-bit slices on tcgen05.mma.kind::i8, TMA-fed, TMEM accumulators",
                 "algorithmic_ops_per_launch": ops_per_launch,
                 "algorithmic_fp64_flops_per_launch": ap_flops_per_launch,
                 "fp64_equivalent_tflops": fp64_equiv,

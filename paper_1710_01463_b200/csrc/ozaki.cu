@@ -1,18 +1,19 @@
 // FP64 GEMM emulated on the tcgen05 INT8 tensor cores (Ozaki scheme, split
-// into signed 7-bit slices), for the RSVD A-passes Y = A X and Z = A^T Y
+// into signed 8-bit slices), for the RSVD A-passes Y = A X and Z = A^T Y
 // (factorize.cpp:68, 70, 71, 86).
 //
 // B200 has no tcgen05 f64 kind: the warp-level DMMA path (gemm_tma.cu) tops
 // out at ~37 TFLOP/s.  The INT8 tensor cores run ~4.5 POPS dense, so an FP64
 // product rebuilt from exact integer products of short slices is faster even
 // after paying for the slice products:
-//   x = 2^e * sum_{p<S} s_p 2^(-6-7p),   s_p in [-64, 64]  (exact split, e per
-//       row of op(A) / per column of B; S = 8 slices = 55 bits below 2^e)
-//   (A B)_ij = 2^(eA_i + eB_j - 12) * sum_{d<S} 2^(-7d) * sum_{p+q=d} (A_p B_q)_ij
-// Every slice product is exact in INT32 (|s| <= 64, K <= 65536, <= 8 terms
-// per diagonal); the terms with p + q >= S are below 2^-56 of the row/column
-// maxima and are dropped, which leaves a normwise error of the order of an
-// FP64 GEMM's.
+//   x = 2^e * sum_{p<S} s_p 2^(-6-8p),   s_0 in [-65, 65], s_p in [-128, 127]
+//       (balanced base-256 digits of rint(x 2^(54-e)); e per row of op(A) /
+//       per column of B; S = 7 slices = 54 bits below 2^e)
+//   (A B)_ij = 2^(eA_i + eB_j - 12) * sum_{d<S} 2^(-8d) * sum_{p+q=d} (A_p B_q)_ij
+// Every slice product is exact in INT32 (|s| <= 128, <= 7 terms per diagonal,
+// K chunks of <= 16384 per launch); the terms with p + q >= S are below 2^-54
+// of the row/column maxima and are dropped, which leaves a normwise error of
+// the order of an FP64 GEMM's.
 //
 // Layout.  A is sliced ONCE per rsvd call into both K-major layouts:
 //   R: slices of A with per-row exponents, row-major  [item][p][row][col]
@@ -21,10 +22,11 @@
 //      (the K-major operand of the TN pass  Z = A^T Y)
 // The small right operand (X or Y, K x N column-major = K-major) is sliced per
 // pass.  A CTA owns a 128 x BN output tile and keeps the S diagonal sums in
-// TMEM (S * BN = 512 columns); per 32-byte K step one TMA box brings the S
-// slices of each operand (32B swizzle), and one thread issues the S(S+1)/2
-// tcgen05.mma.kind::i8 of that step.  The epilogue folds the diagonals in
-// FP64 (Horner in 2^-7) and writes C column-major.
+// TMEM (S * BN = 448 columns); per 32-byte K step one TMA box brings the S
+// slices of each operand (32B swizzle), and one thread issues the S(S+1)/2 =
+// 28 slice products of that step as 10 stacked tcgen05.mma.kind::i8.  The
+// epilogue folds the diagonals in FP64 (Horner in 2^-8) and writes (or adds
+// to, for the later K chunks) C column-major.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -36,11 +38,13 @@
 namespace rsvd {
 namespace {
 
-constexpr int kOzS = 8;       // slices per operand
+constexpr int kOzS = 7;       // slices per operand
 constexpr int kOzBM = 128;    // UMMA M
-constexpr int kOzBN = 64;     // UMMA N (S * BN = 512 TMEM columns)
+constexpr int kOzBN = 64;     // UMMA N (S * BN = 448 of the 512 TMEM columns)
 constexpr int kOzKC = 32;     // K bytes per stage = one MMA K step = one 32B swizzle row
-constexpr int kOzStages = 4;  // 4 x 48 KB ring
+constexpr int kOzStages = 5;  // 5 x 42 KB ring
+constexpr int kOzKChunk = 16384;  // K per launch: 7 * 16384 * 128^2 < 2^31
+constexpr int kOzTmemCols = 512;
 constexpr int kExpNone = INT_MIN;
 
 __device__ __forceinline__ uint32_t sm_addr(const void* p) {
@@ -115,21 +119,45 @@ __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
 
 __device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }
 
-// Signed 7-bit slices of x * 2^-e (|x| < 2^e): exact.
-template <int S>
-__device__ __forceinline__ void split_value(double x, int e, int8_t (&s)[S]) {
-  double v = ldexp(x, 6 - e);  // in (-64, 64)
+// Signed 8-bit slices of x (|x| < 2^e): V = rint(x 2^(54-e)), |V| <= 2^54, as
+// 7 balanced base-256 digits d_0 (most significant, |d_0| <= 65) .. d_6 (in
+// [-128, 127]), V = sum_p d_p 256^(6-p): x = 2^e sum_p d_p 2^(-6-8p) up to the
+// rounding of V.  Two halves (24 bits, 30 bits) in int32, so the digit loop
+// is integer-only.  sc_lo * sc_hi = 2^(54-e), split to stay finite for tiny e.
+__device__ __forceinline__ void split_digits(double x, double sc_lo, double sc_hi,
+                                             int (&d)[kOzS]) {
+  const double v = (x * sc_lo) * sc_hi;
+  const double hd = rint(v * 0x1p-24);
+  int lo = static_cast<int>(rint(fma(hd, -0x1p24, v)));  // |lo| <= 2^23, exact
+  int hi = static_cast<int>(hd);                          // |hi| <= 2^30
 #pragma unroll
-  for (int p = 0; p < S; ++p) {
-    const double t = rint(v);
-    s[p] = static_cast<int8_t>(static_cast<int>(t));
-    v = (v - t) * 128.0;
+  for (int p = kOzS - 1; p >= 4; --p) {
+    const int t = ((lo + 128) & 255) - 128;
+    d[p] = t;
+    lo = (lo - t) >> 8;
   }
+  hi += lo;
+#pragma unroll
+  for (int p = 3; p >= 1; --p) {
+    const int t = ((hi + 128) & 255) - 128;
+    d[p] = t;
+    hi = (hi - t) >> 8;
+  }
+  d[0] = hi;
 }
+
+struct SliceScale {
+  double lo, hi;
+  __device__ explicit SliceScale(int e) {
+    const int t = 54 - e, a = t / 2;
+    lo = ldexp(1.0, a);
+    hi = ldexp(1.0, t - a);
+  }
+};
 
 // Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16 bytes.
 template <class Get>
-__device__ __forceinline__ void pack16(Get get, int e, uint4 (&out)[kOzS]) {
+__device__ __forceinline__ void pack16(Get get, const SliceScale& sc, uint4 (&out)[kOzS]) {
   uint32_t w[kOzS][4];
 #pragma unroll
   for (int p = 0; p < kOzS; ++p)
@@ -137,11 +165,11 @@ __device__ __forceinline__ void pack16(Get get, int e, uint4 (&out)[kOzS]) {
     for (int q = 0; q < 4; ++q) w[p][q] = 0u;
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
-    int8_t s[kOzS];
-    split_value<kOzS>(get(u), e, s);
+    int d[kOzS];
+    split_digits(get(u), sc.lo, sc.hi, d);
 #pragma unroll
     for (int p = 0; p < kOzS; ++p)
-      w[p][u >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(s[p])) << (8 * (u & 3));
+      w[p][u >> 2] |= (static_cast<uint32_t>(d[p]) & 0xFFu) << (8 * (u & 3));
   }
 #pragma unroll
   for (int p = 0; p < kOzS; ++p) out[p] = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
@@ -154,39 +182,42 @@ __device__ __forceinline__ int exp_of_max(double amax) {
 }
 
 // Per-row and per-column exponents of A (rows x cols, column-major): 64 x 64
-// tiles, atomicMax into eRow / eCol (pre-set to kExpNone).
+// tiles, atomicMax into eRow / eCol (pre-set to kExpNone).  Rows reduce in
+// registers (16 columns per thread) and shared memory; columns from a shared
+// copy of |A| (16 rows per thread, then 4 lanes).
 __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ A, int64_t lda,
                                                      int64_t sA, int rows, int cols, int* eRow,
                                                      int* eCol) {
   __shared__ double rmax[4][64];
-  __shared__ double cmax[2][64];
+  __shared__ double tile[64][65];  // [col][row] of |A|
   const int item = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* Ab = A + item * sA;
   const int i = i0 + tx;
   double rm = 0.0;
+#pragma unroll 4
   for (int c = ty; c < 64; c += 4) {
     const int j = j0 + c;
     double v = 0.0;
     if (i < rows && j < cols) v = fabs(Ab[i + static_cast<int64_t>(j) * lda]);
     rm = fmax(rm, v);
-    double w = v;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
-    if (lane == 0) cmax[(warp & 1)][c] = w;  // warps 2t, 2t+1 hold rows 0-31 / 32-63 of column c
-    __syncwarp();
+    tile[c][tx] = v;
   }
   rmax[ty][tx] = rm;
   __syncthreads();
+  const int c = threadIdx.x >> 2, part = (threadIdx.x & 3) * 16;
+  double cm = 0.0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) cm = fmax(cm, tile[c][part + u]);
+  cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+  cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+  const int j = j0 + c;
+  if ((threadIdx.x & 3) == 0 && j < cols && cm > 0.0)
+    atomicMax(&eCol[static_cast<int64_t>(item) * cols + j], exp_of_max(cm));
   if (threadIdx.x < 64) {
     const double r = fmax(fmax(rmax[0][tx], rmax[1][tx]), fmax(rmax[2][tx], rmax[3][tx]));
     if (i < rows && r > 0.0) atomicMax(&eRow[static_cast<int64_t>(item) * rows + i], exp_of_max(r));
-  } else if (threadIdx.x < 128) {
-    const int c = threadIdx.x - 64, j = j0 + c;
-    const double r = fmax(cmax[0][c], cmax[1][c]);
-    if (j < cols && r > 0.0) atomicMax(&eCol[static_cast<int64_t>(item) * cols + j], exp_of_max(r));
   }
 }
 
@@ -214,9 +245,9 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
   {
     const int j = j0 + a;
     if (j < cols && i0 + part < rows) {
-      const int e = usable_exp(eCol[static_cast<int64_t>(item) * cols + j]);
+      const SliceScale sc(usable_exp(eCol[static_cast<int64_t>(item) * cols + j]));
       uint4 out[kOzS];
-      pack16([&](int u) { return tile[a][part + u]; }, e, out);
+      pack16([&](int u) { return tile[a][part + u]; }, sc, out);
       int8_t* dst = sC + item * kOzS * plane + static_cast<int64_t>(j) * rows + i0 + part;
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
@@ -226,9 +257,9 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
   {
     const int i = i0 + a;
     if (i < rows && j0 + part < cols) {
-      const int e = usable_exp(eRow[static_cast<int64_t>(item) * rows + i]);
+      const SliceScale sc(usable_exp(eRow[static_cast<int64_t>(item) * rows + i]));
       uint4 out[kOzS];
-      pack16([&](int u) { return tile[part + u][a]; }, e, out);
+      pack16([&](int u) { return tile[part + u][a]; }, sc, out);
       int8_t* dst = sR + item * kOzS * plane + static_cast<int64_t>(i) * cols + j0 + part;
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
@@ -259,12 +290,12 @@ __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restric
     eB[static_cast<int64_t>(item) * N + j] = e;
   }
   __syncthreads();
-  const int e = eshared;
+  const SliceScale sc(eshared);
   const int64_t plane = static_cast<int64_t>(N) * K;
   int8_t* dst = sB + item * kOzS * plane + static_cast<int64_t>(j) * K;
   for (int k0 = threadIdx.x * 16; k0 < K; k0 += 256 * 16) {
     uint4 out[kOzS];
-    pack16([&](int u) { return col[k0 + u]; }, e, out);
+    pack16([&](int u) { return col[k0 + u]; }, sc, out);
 #pragma unroll
     for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane + k0) = out[p];
   }
@@ -272,6 +303,8 @@ __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restric
 
 struct OzArgs {
   int M, N, K;
+  int k_begin;     // this launch's K range: [k_begin, k_begin + K)
+  int accumulate;  // C += (later K chunks) instead of C =
   double* C;
   int64_t ldc, strideC;
   const int* eA;  // per row of op(A): eA[item * M + i]
@@ -317,7 +350,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      sm_addr(tmem_slot)),
-                 "r"(kOzS * kOzBN)
+                 "r"(kOzTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
@@ -332,8 +365,8 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
       mb_expect_tx(full_bar(s), kOzStage);
-      tma_4d(dA, &tmA, kc * kOzKC, m0, 0, item, full_bar(s));
-      tma_4d(dB, &tmB, kc * kOzKC, n0, 0, item, full_bar(s));
+      tma_4d(dA, &tmA, p.k_begin + kc * kOzKC, m0, 0, item, full_bar(s));
+      tma_4d(dB, &tmB, p.k_begin + kc * kOzKC, n0, 0, item, full_bar(s));
     }
   } else if (warp == 1 && lane == 0) {
     // kind::i8: D s32 (bits 4-5 = 2), A/B signed (bits 7, 10), K-major, N >> 3 at 17, M >> 4 at 24.
@@ -389,7 +422,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       tc_ld16(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        t[j] = fma(t[j], 0.0078125, static_cast<double>(static_cast<int>(r[j])));
+        t[j] = fma(t[j], 0.00390625, static_cast<double>(static_cast<int>(r[j])));
     }
     if (row_ok) {
 #pragma unroll
@@ -397,7 +430,9 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
         const int col = n0 + c0 + j;
         if (col < p.N) {
           const int eb = usable_exp(p.eB[static_cast<int64_t>(item) * p.N + col]);
-          Cb[row + static_cast<int64_t>(col) * p.ldc] = ldexp(t[j], ea + eb - 12);
+          double* c = Cb + row + static_cast<int64_t>(col) * p.ldc;
+          const double v = ldexp(t[j], ea + eb - 12);
+          *c = p.accumulate ? *c + v : v;
         }
       }
     }
@@ -406,7 +441,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(kOzS * kOzBN)
+                 "r"(kOzTmemCols)
                  : "memory");
   }
 }
@@ -445,7 +480,7 @@ bool oz_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64
 }  // namespace
 
 bool oz_supported(int64_t rows, int64_t cols, int64_t K) {
-  return rows % 16 == 0 && cols % 16 == 0 && K % 16 == 0 && K <= 65536 && rows < (1ll << 31) &&
+  return rows % 16 == 0 && cols % 16 == 0 && K % 16 == 0 && rows < (1ll << 31) &&
          cols < (1ll << 31);
 }
 
@@ -486,12 +521,14 @@ void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, c
     RSVD_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kOzSmem));
   });
-  OzArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), C.base, C.ld, C.stride,
-           eA, eB};
   dim3 grid(static_cast<unsigned>(ceil_div(N, kOzBN)), static_cast<unsigned>(ceil_div(M, kOzBM)),
             static_cast<unsigned>(batch));
-  oz_gemm_kernel<<<grid, 128, kOzSmem, st>>>(ma, mb, a);
-  RSVD_LAUNCH("oz_gemm_kernel");
+  for (int64_t k0 = 0; k0 < K; k0 += kOzKChunk) {
+    OzArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(std::min<int64_t>(kOzKChunk, K - k0)),
+             static_cast<int>(k0), k0 > 0 ? 1 : 0, C.base, C.ld, C.stride, eA, eB};
+    oz_gemm_kernel<<<grid, 128, kOzSmem, st>>>(ma, mb, a);
+    RSVD_LAUNCH("oz_gemm_kernel");
+  }
 }
 
 }  // namespace rsvd

@@ -111,7 +111,7 @@ def test_dgemm_odd_leading_dimension(cuda):
      (512, 64, 256, 1, 300)],
 )
 def test_ozaki_gemm_vs_torch(cuda, trans_a, M, N, K, batch, grade):
-    """Emulated FP64 (8 signed 7-bit slices per operand on the INT8 tensor
+    """Emulated FP64 (7 signed 8-bit slices per operand on the INT8 tensor
     cores, ozaki.cu) against torch float64: elementwise within 8e-15 of
     |op(A)| |B| (an FP64 GEMM's K u |A||B| bound is ~1e-12 here), normwise
     within 1e-14; `grade` spreads the K columns of op(A) over 10^-grade
