@@ -109,12 +109,20 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// K-major operand tile of `rows` x 32 bytes with the 32-byte swizzle: 8-row
-// core groups 256 bytes apart (SBO), LBO unused, descriptor version 1.
-__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
-         (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
-         (static_cast<uint64_t>(6) << 61);
+// K-major operand tile of `rows` x 32 bytes in the canonical no-swizzle
+// ("interleaved") layout: 8 x 16-byte core matrices of 128 contiguous bytes,
+// the two of one K step 128 bytes apart (LBO), 8-row groups 256 bytes apart
+// (SBO), descriptor version 1.  This is also the layout of the slices in
+// global memory (tile_off), so a TMA box row is 256 contiguous bytes.
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(128 >> 4) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46);
+}
+
+// Byte offset of the 16-byte chunk (row r, K bytes 16c .. 16c+15) inside one
+// slice plane of `R` rows x `K` bytes: [r / 8][c][r % 8][16].
+__device__ __forceinline__ int64_t tile_off(int r, int c, int K) {
+  return (static_cast<int64_t>(r >> 3) * (K >> 4) + c) * 128 + (r & 7) * 16;
 }
 
 __device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
       const SliceScale sc(usable_exp(eCol[static_cast<int64_t>(item) * cols + j]));
       uint4 out[kOzS];
       pack16([&](int u) { return tile[a][part + u]; }, sc, out);
-      int8_t* dst = sC + item * kOzS * plane + static_cast<int64_t>(j) * rows + i0 + part;
+      int8_t* dst = sC + item * kOzS * plane + tile_off(j, (i0 + part) >> 4, rows);
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
     }
@@ -260,44 +268,49 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
       const SliceScale sc(usable_exp(eRow[static_cast<int64_t>(item) * rows + i]));
       uint4 out[kOzS];
       pack16([&](int u) { return tile[part + u][a]; }, sc, out);
-      int8_t* dst = sR + item * kOzS * plane + static_cast<int64_t>(i) * cols + j0 + part;
+      int8_t* dst = sR + item * kOzS * plane + tile_off(i, (j0 + part) >> 4, cols);
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
     }
   }
 }
 
-// Slices of the right operand B (K x N column-major, K % 16 == 0) with one
-// exponent per column: sB[item][p][j][k], eB[item][j].  One CTA per column.
+// Slices of the right operand B (K x N column-major, K % 16 == 0, N % 8 == 0)
+// with one exponent per column: sB[item][p] in the tiled layout (tile_off with
+// row = column j of B), eB[item][j].  One CTA per 8 columns (one row group):
+// warp w reduces column w's maximum, then lane (r, c) of every warp packs the
+// 16-byte chunk (column r, K chunk c), so a warp stores whole 128-byte lines.
 __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restrict__ B, int64_t ldb,
                                                          int64_t sBst, int K, int N,
                                                          int8_t* __restrict__ sB, int* eB) {
-  __shared__ double red[8];
-  __shared__ int eshared;
-  const int j = blockIdx.x, item = blockIdx.y;
-  const double* col = B + item * sBst + static_cast<int64_t>(j) * ldb;
-  double m = 0.0;
-  for (int k = threadIdx.x; k < K; k += 256) m = fmax(m, fabs(col[k]));
+  __shared__ int eshared[8];
+  const int j0 = blockIdx.x * 8, item = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Bb = B + item * sBst;
+  {
+    const double* col = Bb + static_cast<int64_t>(j0 + warp) * ldb;
+    double m = 0.0;
+    for (int k = lane; k < K; k += 32) m = fmax(m, fabs(col[k]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r = red[0];
-    for (int w = 1; w < 8; ++w) r = fmax(r, red[w]);
-    const int e = r > 0.0 ? exp_of_max(r) : 0;
-    eshared = e;
-    eB[static_cast<int64_t>(item) * N + j] = e;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      const int e = m > 0.0 ? exp_of_max(m) : 0;
+      eshared[warp] = e;
+      eB[static_cast<int64_t>(item) * N + j0 + warp] = e;
+    }
   }
   __syncthreads();
-  const SliceScale sc(eshared);
+  const int r = threadIdx.x & 7;
+  const SliceScale sc(eshared[r]);
+  const double* col = Bb + static_cast<int64_t>(j0 + r) * ldb;
   const int64_t plane = static_cast<int64_t>(N) * K;
-  int8_t* dst = sB + item * kOzS * plane + static_cast<int64_t>(j) * K;
-  for (int k0 = threadIdx.x * 16; k0 < K; k0 += 256 * 16) {
+  int8_t* dst = sB + item * kOzS * plane;
+  for (int c = threadIdx.x >> 3; c < (K >> 4); c += 32) {
     uint4 out[kOzS];
-    pack16([&](int u) { return col[k0 + u]; }, sc, out);
+    pack16([&](int u) { return col[c * 16 + u]; }, sc, out);
+    int8_t* d = dst + tile_off(j0 + r, c, K);
 #pragma unroll
-    for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane + k0) = out[p];
+    for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(d + p * plane) = out[p];
   }
 }
 
@@ -365,8 +378,8 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
       mb_expect_tx(full_bar(s), kOzStage);
-      tma_4d(dA, &tmA, p.k_begin + kc * kOzKC, m0, 0, item, full_bar(s));
-      tma_4d(dB, &tmB, p.k_begin + kc * kOzKC, n0, 0, item, full_bar(s));
+      tma_4d(dA, &tmA, 8 * (p.k_begin + kc * kOzKC), m0 >> 3, 0, item, full_bar(s));
+      tma_4d(dB, &tmB, 8 * (p.k_begin + kc * kOzKC), n0 >> 3, 0, item, full_bar(s));
     }
   } else if (warp == 1 && lane == 0) {
     // kind::i8: D s32 (bits 4-5 = 2), A/B signed (bits 7, 10), K-major, N >> 3 at 17, M >> 4 at 24.
@@ -386,11 +399,11 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
 #pragma unroll
       for (int pa = 0; pa < kOzS; ++pa) {
-        const uint64_t da = umma_desc_sw32(dA + pa * (kOzBM * kOzKC));
+        const uint64_t da = umma_desc_kmajor(dA + pa * (kOzBM * kOzKC));
 #pragma unroll
         for (int q0 = 0; q0 < kOzS - pa; q0 += kQ) {
           const int nq = (kOzS - pa - q0) < kQ ? (kOzS - pa - q0) : kQ;
-          const uint64_t db = umma_desc_sw32(dB + q0 * (kOzBN * kOzKC));
+          const uint64_t db = umma_desc_kmajor(dB + q0 * (kOzBN * kOzKC));
           const uint32_t idesc = idesc0 | (static_cast<uint32_t>((nq * kOzBN) >> 3) << 17);
           tc_mma_i8(tmem + static_cast<uint32_t>((pa + q0) * kOzBN), da, db, idesc,
                     (kc > 0 || pa > 0) ? 1u : 0u);
@@ -461,19 +474,23 @@ PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
   return fn;
 }
 
-// [item][p][rows][K] int8 slices, K contiguous; box {32 K, box_rows, S, 1}.
+// Slices in the tiled layout [item][p][rows / 8][K / 16][8][16 bytes]: as a
+// tensor of bytes {8 K (one row group, contiguous), rows / 8, S, batch}; a box
+// {256 bytes = the two core matrices of one K step, box_rows / 8, S, 1} lands
+// in shared memory exactly as umma_desc_kmajor expects.  No swizzle: every box
+// row is 256 contiguous bytes of global memory (two full lines per request).
 bool oz_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64_t batch,
             int box_rows) {
   auto fn = oz_encode_fn();
   if (!fn) return false;
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows),
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(8 * K), static_cast<cuuint64_t>(rows / 8),
                               static_cast<cuuint64_t>(kOzS), static_cast<cuuint64_t>(batch)};
-  const cuuint64_t str[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K * rows),
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(8 * K), static_cast<cuuint64_t>(K * rows),
                              static_cast<cuuint64_t>(K * rows * kOzS)};
-  const cuuint32_t box[4] = {kOzKC, static_cast<cuuint32_t>(box_rows), kOzS, 1};
+  const cuuint32_t box[4] = {8 * kOzKC, static_cast<cuuint32_t>(box_rows / 8), kOzS, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -505,7 +522,7 @@ void oz_prepare_a(CMatRef A, int64_t rows, int64_t cols, int64_t batch, int8_t* 
 
 void oz_slice_b(CMatRef B, int64_t K, int64_t N, int64_t batch, int8_t* sB, int* eB,
                 cudaStream_t st) {
-  dim3 grid(static_cast<unsigned>(N), static_cast<unsigned>(batch));
+  dim3 grid(static_cast<unsigned>(N / 8), static_cast<unsigned>(batch));
   oz_slice_b_kernel<<<grid, 256, 0, st>>>(B.base, B.ld, B.stride, static_cast<int>(K),
                                           static_cast<int>(N), sB, eB);
   RSVD_LAUNCH("oz_slice_b_kernel");

@@ -1,6 +1,7 @@
 """Per-kernel SASS instruction counts of librsvd_b200.so (cuobjdump -sass):
 the evidence that the GEMMs are TMA-fed (UTMALDG) and run on the FP64 tensor
-pipe (DMMA), and which kernels use cp.async (LDGSTS), DSMEM / cluster
+pipe (DMMA) or, for the emulated-FP64 A-pass, on tcgen05 (UTCIMMA = tcgen05.mma
+kind::i8, LDTM = tcgen05.ld), and which kernels use cp.async (LDGSTS), DSMEM / cluster
 barriers, etc.  Usage: python tools/sass_summary.py [lib.so] > profiles/..."""
 import collections
 import re
@@ -8,7 +9,7 @@ import subprocess
 import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1710_01463_b200/librsvd_b200.so"
-KEYS = ["DMMA", "UTMALDG", "SYNCS", "LDGSTS", "DFMA", "MUFU", "BAR", "LDS", "LDG", "STG", "SHFL",
+KEYS = ["DMMA", "UTCIMMA", "LDTM", "UTMALDG", "SYNCS", "LDGSTS", "DFMA", "MUFU", "BAR", "LDS", "LDG", "STG", "SHFL",
         "ATOM", "RED", "UCGABAR", "CCTL"]
 
 
