@@ -45,7 +45,8 @@ constexpr int kOzKC = 32;     // K bytes per stage = one MMA K step = one 32B sw
 constexpr int kOzStages = 5;  // 5 x 42 KB ring
 constexpr int kOzKChunk = 16384;  // K per launch: 7 * 16384 * 128^2 < 2^31
 constexpr int kOzTmemCols = 512;
-constexpr int kExpNone = INT_MIN;
+constexpr int kOzPF = 12;       // L2 prefetch distance of the A boxes, in K steps
+constexpr int kExpNone = static_cast<int>(0x80808080u);  // cudaMemset(0x80): below any frexp exponent
 
 __device__ __forceinline__ uint32_t sm_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -75,6 +76,13 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int
       "%3, %4, %5}], [%6];\n" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -125,19 +133,35 @@ __device__ __forceinline__ int64_t tile_off(int r, int c, int K) {
   return (static_cast<int64_t>(r >> 3) * (K >> 4) + c) * 128 + (r & 7) * 16;
 }
 
-__device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }
+// Exact int32 -> double on the FP64 pipe (I2F.F64 runs on the conversion unit
+// at a few per clock per SM: 448 per thread made the TMEM drain ~10% of a
+// tile): 2^52 + 2^31 + v has the low word v ^ 0x80000000.
+__device__ __forceinline__ double i32_to_f64(uint32_t v) {
+  return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
+}
 
-// Signed 8-bit slices of x (|x| < 2^e): V = rint(x 2^(54-e)), |V| <= 2^54, as
+__device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }  // all-zero line
+
+// Signed 8-bit slices of x (|x| < 2^e): V = round(x 2^(54-e)), |V| <= 2^54, as
 // 7 balanced base-256 digits d_0 (most significant, |d_0| <= 65) .. d_6 (in
 // [-128, 127]), V = sum_p d_p 256^(6-p): x = 2^e sum_p d_p 2^(-6-8p) up to the
-// rounding of V.  Two halves (24 bits, 30 bits) in int32, so the digit loop
-// is integer-only.  sc_lo * sc_hi = 2^(54-e), split to stay finite for tiny e.
-__device__ __forceinline__ void split_digits(double x, double sc_lo, double sc_hi,
-                                             int (&d)[kOzS]) {
-  const double v = (x * sc_lo) * sc_hi;
-  const double hd = rint(v * 0x1p-24);
-  int lo = static_cast<int>(rint(fma(hd, -0x1p24, v)));  // |lo| <= 2^23, exact
-  int hi = static_cast<int>(hd);                          // |hi| <= 2^30
+// rounding of V (half away from zero, <= 2^(e-55)).  Integer-only: V is the
+// 53-bit significand shifted by e + 1021 - (biased exponent) >= -1 bits (the
+// FP64 conversions F2I / FRND run at a few per clock per SM and bounded the
+// slicing kernels; ncu: XU pipe saturated), then split into a 24-bit and a
+// signed 31-bit half so the digit loop runs on 32-bit integers.
+__device__ __forceinline__ void split_digits(double x, int e, int (&d)[kOzS]) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  int ef = static_cast<int>(b >> 52) & 0x7FF;
+  unsigned long long m = b & 0xFFFFFFFFFFFFFull;
+  if (ef) m |= 1ull << 52; else ef = 1;  // subnormal: no implicit bit
+  // V = round(2 m / 2^s), s = sh + 1 in [0, 63]: branch-free, the rounding
+  // term (1 << s) >> 1 vanishes for s = 0.
+  const int s = min(e + 1022 - ef, 63);
+  const unsigned long long v = ((m << 1) + ((1ull << s) >> 1)) >> s;
+  const long long sv = (b >> 63) ? -static_cast<long long>(v) : static_cast<long long>(v);
+  int lo = static_cast<int>(sv & 0xFFFFFF);  // [0, 2^24)
+  int hi = static_cast<int>(sv >> 24);       // |hi| <= 2^30
 #pragma unroll
   for (int p = kOzS - 1; p >= 4; --p) {
     const int t = ((lo + 128) & 255) - 128;
@@ -155,12 +179,8 @@ __device__ __forceinline__ void split_digits(double x, double sc_lo, double sc_h
 }
 
 struct SliceScale {
-  double lo, hi;
-  __device__ explicit SliceScale(int e) {
-    const int t = 54 - e, a = t / 2;
-    lo = ldexp(1.0, a);
-    hi = ldexp(1.0, t - a);
-  }
+  int e;
+  __device__ explicit SliceScale(int e_) : e(e_) {}
 };
 
 // Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16 bytes.
@@ -174,7 +194,7 @@ __device__ __forceinline__ void pack16(Get get, const SliceScale& sc, uint4 (&ou
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     int d[kOzS];
-    split_digits(get(u), sc.lo, sc.hi, d);
+    split_digits(get(u), sc.e, d);
 #pragma unroll
     for (int p = 0; p < kOzS; ++p)
       w[p][u >> 2] |= (static_cast<uint32_t>(d[p]) & 0xFFu) << (8 * (u & 3));
@@ -275,43 +295,42 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
   }
 }
 
-// Slices of the right operand B (K x N column-major, K % 16 == 0, N % 8 == 0)
-// with one exponent per column: sB[item][p] in the tiled layout (tile_off with
-// row = column j of B), eB[item][j].  One CTA per 8 columns (one row group):
-// warp w reduces column w's maximum, then lane (r, c) of every warp packs the
-// 16-byte chunk (column r, K chunk c), so a warp stores whole 128-byte lines.
+// Exponents of the right operand B (K x N column-major): eB[item][j] (pre-set
+// to kExpNone) by atomicMax over K ranges of kOzBK; one warp per column, one
+// CTA per 8 columns and K range.
+constexpr int kOzBK = 512;  // K per CTA of the B kernels (32 chunks of 16 x 8 columns = 256 threads)
+
+__global__ void __launch_bounds__(256) oz_exp_b_kernel(const double* __restrict__ B, int64_t ldb,
+                                                       int64_t sBst, int K, int N, int* eB) {
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), item = blockIdx.z, lane = threadIdx.x & 31;
+  const int k0 = blockIdx.y * kOzBK, k1 = min(K, k0 + kOzBK);
+  const double* col = B + item * sBst + static_cast<int64_t>(j) * ldb;
+  double m = 0.0;
+  for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs(col[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0 && m > 0.0) atomicMax(&eB[static_cast<int64_t>(item) * N + j], exp_of_max(m));
+}
+
+// Slices of the right operand B (K % 16 == 0, N % 8 == 0) with eB's exponent
+// per column: sB[item][p] in the tiled layout (tile_off with row = column j of
+// B).  One CTA per 8 columns (one row group) and K range; thread (r, c) packs
+// the 16-byte chunk (column r, K chunk c), so a warp stores whole 128-byte lines.
 __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restrict__ B, int64_t ldb,
                                                          int64_t sBst, int K, int N,
-                                                         int8_t* __restrict__ sB, int* eB) {
-  __shared__ int eshared[8];
-  const int j0 = blockIdx.x * 8, item = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* Bb = B + item * sBst;
-  {
-    const double* col = Bb + static_cast<int64_t>(j0 + warp) * ldb;
-    double m = 0.0;
-    for (int k = lane; k < K; k += 32) m = fmax(m, fabs(col[k]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      const int e = m > 0.0 ? exp_of_max(m) : 0;
-      eshared[warp] = e;
-      eB[static_cast<int64_t>(item) * N + j0 + warp] = e;
-    }
-  }
-  __syncthreads();
-  const int r = threadIdx.x & 7;
-  const SliceScale sc(eshared[r]);
-  const double* col = Bb + static_cast<int64_t>(j0 + r) * ldb;
+                                                         int8_t* __restrict__ sB,
+                                                         const int* __restrict__ eB) {
+  const int j = blockIdx.x * 8 + (threadIdx.x & 7), item = blockIdx.z;
+  const int c = blockIdx.y * (kOzBK / 16) + (threadIdx.x >> 3);
+  if (c >= (K >> 4)) return;
+  const SliceScale sc(usable_exp(eB[static_cast<int64_t>(item) * N + j]));
+  const double* src = B + item * sBst + static_cast<int64_t>(j) * ldb + c * 16;
   const int64_t plane = static_cast<int64_t>(N) * K;
-  int8_t* dst = sB + item * kOzS * plane;
-  for (int c = threadIdx.x >> 3; c < (K >> 4); c += 32) {
-    uint4 out[kOzS];
-    pack16([&](int u) { return col[c * 16 + u]; }, sc, out);
-    int8_t* d = dst + tile_off(j0 + r, c, K);
+  uint4 out[kOzS];
+  pack16([&](int u) { return src[u]; }, sc, out);
+  int8_t* d = sB + item * kOzS * plane + tile_off(j, c, K);
 #pragma unroll
-    for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(d + p * plane) = out[p];
-  }
+  for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(d + p * plane) = out[p];
 }
 
 struct OzArgs {
@@ -373,8 +392,17 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
+    // The CTAs of one M tile (blockIdx.x = N tile) run side by side and read
+    // the same A boxes: the first of them pulls the boxes kOzPF steps ahead
+    // into L2, so the ring only has to cover the L2 hit latency, not DRAM's.
+    const bool pf = blockIdx.x == 0;
+    if (pf)
+      for (int kc = 0; kc < kOzPF && kc < nk; ++kc)
+        tma_prefetch_4d(&tmA, 8 * (p.k_begin + kc * kOzKC), m0 >> 3, 0, item);
     for (int kc = 0; kc < nk; ++kc) {
       const int s = kc % kOzStages;
+      if (pf && kc + kOzPF < nk)
+        tma_prefetch_4d(&tmA, 8 * (p.k_begin + (kc + kOzPF) * kOzKC), m0 >> 3, 0, item);
       if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
       mb_expect_tx(full_bar(s), kOzStage);
@@ -435,7 +463,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       tc_ld16(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        t[j] = fma(t[j], 0.00390625, static_cast<double>(static_cast<int>(r[j])));
+        t[j] = fma(t[j], 0.00390625, i32_to_f64(r[j]));
     }
     if (row_ok) {
 #pragma unroll
@@ -509,7 +537,6 @@ void oz_prepare_a(CMatRef A, int64_t rows, int64_t cols, int64_t batch, int8_t* 
                   int* eRow, int* eCol, cudaStream_t st) {
   RSVD_CUDA(cudaMemsetAsync(eRow, 0x80, sizeof(int) * rows * batch, st));
   RSVD_CUDA(cudaMemsetAsync(eCol, 0x80, sizeof(int) * cols * batch, st));
-  // 0x80808080 < any frexp exponent; usable_exp maps it to 0 (an all-zero line).
   dim3 grid(static_cast<unsigned>(ceil_div(cols, 64)), static_cast<unsigned>(ceil_div(rows, 64)),
             static_cast<unsigned>(batch));
   oz_exp_kernel<<<grid, 256, 0, st>>>(A.base, A.ld, A.stride, static_cast<int>(rows),
@@ -522,7 +549,12 @@ void oz_prepare_a(CMatRef A, int64_t rows, int64_t cols, int64_t batch, int8_t* 
 
 void oz_slice_b(CMatRef B, int64_t K, int64_t N, int64_t batch, int8_t* sB, int* eB,
                 cudaStream_t st) {
-  dim3 grid(static_cast<unsigned>(N / 8), static_cast<unsigned>(batch));
+  RSVD_CUDA(cudaMemsetAsync(eB, 0x80, sizeof(int) * N * batch, st));
+  dim3 grid(static_cast<unsigned>(N / 8), static_cast<unsigned>(ceil_div(K, kOzBK)),
+            static_cast<unsigned>(batch));
+  oz_exp_b_kernel<<<grid, 256, 0, st>>>(B.base, B.ld, B.stride, static_cast<int>(K),
+                                        static_cast<int>(N), eB);
+  RSVD_LAUNCH("oz_exp_b_kernel");
   oz_slice_b_kernel<<<grid, 256, 0, st>>>(B.base, B.ld, B.stride, static_cast<int>(K),
                                           static_cast<int>(N), sB, eB);
   RSVD_LAUNCH("oz_slice_b_kernel");
