@@ -1588,6 +1588,14 @@ int rsvd_testing_dgemm(rsvd_handle h, int trans_a, int64_t M, int64_t N, int64_t
   });
 }
 
+#ifdef RSVD_OZ_TRACE
+int rsvd_testing_oz_trace_read(unsigned long long* out, int64_t n) {
+  cudaDeviceSynchronize();
+  rsvd::oz_trace_read(out, n);
+  return 0;
+}
+#endif
+
 int rsvd_testing_ozaki_gemm(rsvd_handle h, int trans_a, int64_t M, int64_t N, int64_t K,
                             const double* A, int64_t lda, int64_t strideA, const double* B,
                             int64_t ldb, int64_t strideB, double* C, int64_t ldc, int64_t strideC,

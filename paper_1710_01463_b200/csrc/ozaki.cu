@@ -45,7 +45,6 @@ constexpr int kOzKC = 32;     // K bytes per stage = one MMA K step = one 32B sw
 constexpr int kOzStages = 5;  // 5 x 42 KB ring
 constexpr int kOzKChunk = 16384;  // K per launch: 7 * 16384 * 128^2 < 2^31
 constexpr int kOzTmemCols = 512;
-constexpr int kOzPF = 12;       // L2 prefetch distance of the A boxes, in K steps
 constexpr int kExpNone = static_cast<int>(0x80808080u);  // cudaMemset(0x80): below any frexp exponent
 
 __device__ __forceinline__ uint32_t sm_addr(const void* p) {
@@ -77,13 +76,6 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
-                                                int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
@@ -106,13 +98,10 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_c, uint64_t da, uint64_t
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
@@ -138,6 +127,17 @@ __device__ __forceinline__ int64_t tile_off(int r, int c, int K) {
 // tile): 2^52 + 2^31 + v has the low word v ^ 0x80000000.
 __device__ __forceinline__ double i32_to_f64(uint32_t v) {
   return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// x 2^e for |x| < 2^35 and any e the exponents of two doubles can add up to:
+// two multiplies by normal powers of two built from their exponent bits
+// (branch-free and a handful of instructions: an inlined ldexp per element made
+// the TMEM drain ~70 KB of straight-line code that ran from L2 at every tile,
+// 9 us of an 88 us tile).  Below 2^-2040 the product underflows to 0 either way.
+__device__ __forceinline__ double scale_pow2(double x, int e) {
+  e = max(e, -2040);
+  const int e1 = e >> 1, e2 = e - e1;
+  return (x * __hiloint2double((1023 + e1) << 20, 0)) * __hiloint2double((1023 + e2) << 20, 0);
 }
 
 __device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }  // all-zero line
@@ -333,6 +333,27 @@ __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restric
   for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(d + p * plane) = out[p];
 }
 
+#ifdef RSVD_OZ_TRACE
+// Per-CTA %globaltimer stamps (ns): entry, setup done, first stage landed,
+// accumulators complete, exit.  Read by tools/probe/oz_trace.py.
+constexpr int kOzTraceCtas = 8192;
+__device__ unsigned long long g_oz_trace[kOzTraceCtas * 8];
+__device__ __forceinline__ unsigned long long oz_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+#define OZ_STAMP(i)                                                                       \
+  do {                                                                                    \
+    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);  \
+    if (lin < kOzTraceCtas) g_oz_trace[lin * 8 + (i)] = oz_now();                         \
+  } while (0)
+#else
+#define OZ_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
 struct OzArgs {
   int M, N, K;
   int k_begin;     // this launch's K range: [k_begin, k_begin + K)
@@ -346,7 +367,7 @@ struct OzArgs {
 constexpr int kOzBytesA = kOzS * kOzBM * kOzKC;
 constexpr int kOzBytesB = kOzS * kOzBN * kOzKC;
 constexpr int kOzStage = kOzBytesA + kOzBytesB;
-constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 256;
+constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 512;
 
 // One 128 x BN tile of C per CTA.  Warp 0 lane 0: TMA producer; warp 1 lane 0:
 // MMA issuer; warp 2 owns the TMEM allocation; all four warps drain TMEM
@@ -360,6 +381,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   unsigned char* sgen = oz_smem + (sbase - raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sgen + kOzStages * kOzStage);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kOzStages + 1);
+  int* seb = reinterpret_cast<int*>(bars + 2 * kOzStages + 2);  // eB - 12 of the tile's columns
   const uint32_t bar0 = sm_addr(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kOzStages + s); };
@@ -367,6 +389,12 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kOzBN, m0 = blockIdx.y * kOzBM, item = blockIdx.z;
+  if (threadIdx.x == 0) OZ_STAMP(0);
+  if (threadIdx.x >= 64) {
+    const int col = n0 + static_cast<int>(threadIdx.x) - 64;
+    seb[threadIdx.x - 64] =
+        (col < p.N ? usable_exp(p.eB[static_cast<int64_t>(item) * p.N + col]) : 0) - 12;
+  }
   const int nk = (p.K + kOzKC - 1) / kOzKC;
 
   if (threadIdx.x == 0) {
@@ -390,19 +418,11 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) OZ_STAMP(1);
 
   if (warp == 0 && lane == 0) {
-    // The CTAs of one M tile (blockIdx.x = N tile) run side by side and read
-    // the same A boxes: the first of them pulls the boxes kOzPF steps ahead
-    // into L2, so the ring only has to cover the L2 hit latency, not DRAM's.
-    const bool pf = blockIdx.x == 0;
-    if (pf)
-      for (int kc = 0; kc < kOzPF && kc < nk; ++kc)
-        tma_prefetch_4d(&tmA, 8 * (p.k_begin + kc * kOzKC), m0 >> 3, 0, item);
     for (int kc = 0; kc < nk; ++kc) {
       const int s = kc % kOzStages;
-      if (pf && kc + kOzPF < nk)
-        tma_prefetch_4d(&tmA, 8 * (p.k_begin + (kc + kOzPF) * kOzKC), m0 >> 3, 0, item);
       if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
       mb_expect_tx(full_bar(s), kOzStage);
@@ -423,6 +443,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
     for (int kc = 0; kc < nk; ++kc) {
       const int s = kc % kOzStages;
       mb_wait(full_bar(s), (kc / kOzStages) & 1);
+      if (kc == 0) OZ_STAMP(2);
       tc_fence_after();
       const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
 #pragma unroll
@@ -445,38 +466,49 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   mb_wait(done_bar, 0);
   __syncwarp();
   tc_fence_after();
+  if (threadIdx.x == 0) OZ_STAMP(3);
 
   const int row = m0 + warp * 32 + lane;
   const bool row_ok = row < p.M;
   const int ea = row_ok ? usable_exp(p.eA[static_cast<int64_t>(item) * p.M + row]) : 0;
-  double* Cb = p.C + item * p.strideC;
+  double* Crow = p.C + item * p.strideC + row;
   const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  // Two halves of 32 columns: 7 TMEM loads each (x32), Horner over the
+  // diagonals, one scaling by 2^(eA + eB - 12) built from its exponent bits
+  // (ldexp only outside the normal range), then the stores (the values of a
+  // later K chunk's C are read up front, 32 independent loads).
 #pragma unroll 1
-  for (int c0 = 0; c0 < kOzBN; c0 += 16) {
+  for (int c0 = 0; c0 < kOzBN; c0 += 32) {
     if (n0 + c0 >= p.N) break;
-    double t[16];
+    double t[32];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) t[j] = 0.0;
+    for (int j = 0; j < 32; ++j) t[j] = 0.0;
 #pragma unroll 1
     for (int d = kOzS - 1; d >= 0; --d) {
-      uint32_t r[16];
-      tc_ld16(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
+      uint32_t r[32];
+      tc_ld32(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        t[j] = fma(t[j], 0.00390625, i32_to_f64(r[j]));
+      for (int j = 0; j < 32; ++j) t[j] = fma(t[j], 0.00390625, i32_to_f64(r[j]));
     }
+    if (threadIdx.x == 0) OZ_STAMP(c0 ? 6 : 4);
     if (row_ok) {
+      double* cp = Crow + static_cast<int64_t>(n0 + c0) * p.ldc;
+      const int nc = min(min(32, kOzBN - c0), p.N - n0 - c0);
+      if (p.accumulate) {
+        double cv[32];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + c0 + j;
-        if (col < p.N) {
-          const int eb = usable_exp(p.eB[static_cast<int64_t>(item) * p.N + col]);
-          double* c = Cb + row + static_cast<int64_t>(col) * p.ldc;
-          const double v = ldexp(t[j], ea + eb - 12);
-          *c = p.accumulate ? *c + v : v;
-        }
+        for (int j = 0; j < 32; ++j) cv[j] = j < nc ? cp[j * p.ldc] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t[j] = cv[j] + scale_pow2(t[j], ea + seb[c0 + j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t[j] = scale_pow2(t[j], ea + seb[c0 + j]);
       }
+#pragma unroll
+      for (int j = 0; j < 32; ++j, cp += p.ldc)
+        if (j < nc) *cp = t[j];
     }
+    if (threadIdx.x == 0 && c0 == 0) OZ_STAMP(5);
   }
   tc_fence_before();
   __syncthreads();
@@ -485,6 +517,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
                  "r"(kOzTmemCols)
                  : "memory");
   }
+  if (threadIdx.x == 0) OZ_STAMP(7);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
@@ -523,6 +556,12 @@ bool oz_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64
 }
 
 }  // namespace
+
+#ifdef RSVD_OZ_TRACE
+void oz_trace_read(unsigned long long* out, int64_t n) {
+  RSVD_CUDA(cudaMemcpyFromSymbol(out, g_oz_trace, sizeof(unsigned long long) * n));
+}
+#endif
 
 bool oz_supported(int64_t rows, int64_t cols, int64_t K) {
   return rows % 16 == 0 && cols % 16 == 0 && K % 16 == 0 && rows < (1ll << 31) &&
