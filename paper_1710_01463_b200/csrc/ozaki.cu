@@ -145,37 +145,24 @@ __device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e;
 // Signed 8-bit slices of x (|x| < 2^e): V = round(x 2^(54-e)), |V| <= 2^54, as
 // 7 balanced base-256 digits d_0 (most significant, |d_0| <= 65) .. d_6 (in
 // [-128, 127]), V = sum_p d_p 256^(6-p): x = 2^e sum_p d_p 2^(-6-8p) up to the
-// rounding of V (half away from zero, <= 2^(e-55)).  Integer-only: V is the
-// 53-bit significand shifted by e + 1021 - (biased exponent) >= -1 bits (the
-// FP64 conversions F2I / FRND run at a few per clock per SM and bounded the
-// slicing kernels; ncu: XU pipe saturated), then split into a 24-bit and a
-// signed 31-bit half so the digit loop runs on 32-bit integers.
-__device__ __forceinline__ void split_digits(double x, int e, int (&d)[kOzS]) {
+// rounding of V (half away from zero, <= 2^(e-55)).  Integer-only (FP64
+// conversions run at a few per clock per SM): V is the 53-bit significand
+// shifted by e + 1021 - (biased exponent) >= -1 bits.  Adding the bias
+// B = sum_p 128 * 256^p turns the balanced digits into the plain bytes of
+// V + B (d_p + 128 in [0, 255]), and flipping each byte's top bit gives d_p as
+// int8: the 7 digits are the low 7 bytes of (V + B) ^ B, byte 6 - p = d_p.
+__device__ __forceinline__ unsigned long long digit_bytes(double x, int e) {
   const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
   int ef = static_cast<int>(b >> 52) & 0x7FF;
   unsigned long long m = b & 0xFFFFFFFFFFFFFull;
   if (ef) m |= 1ull << 52; else ef = 1;  // subnormal: no implicit bit
-  // V = round(2 m / 2^s), s = sh + 1 in [0, 63]: branch-free, the rounding
-  // term (1 << s) >> 1 vanishes for s = 0.
+  // V = round(2 m / 2^s), s in [0, 63]: branch-free, the rounding term
+  // (1 << s) >> 1 vanishes for s = 0.
   const int s = min(e + 1022 - ef, 63);
   const unsigned long long v = ((m << 1) + ((1ull << s) >> 1)) >> s;
-  const long long sv = (b >> 63) ? -static_cast<long long>(v) : static_cast<long long>(v);
-  int lo = static_cast<int>(sv & 0xFFFFFF);  // [0, 2^24)
-  int hi = static_cast<int>(sv >> 24);       // |hi| <= 2^30
-#pragma unroll
-  for (int p = kOzS - 1; p >= 4; --p) {
-    const int t = ((lo + 128) & 255) - 128;
-    d[p] = t;
-    lo = (lo - t) >> 8;
-  }
-  hi += lo;
-#pragma unroll
-  for (int p = 3; p >= 1; --p) {
-    const int t = ((hi + 128) & 255) - 128;
-    d[p] = t;
-    hi = (hi - t) >> 8;
-  }
-  d[0] = hi;
+  const unsigned long long sv = (b >> 63) ? 0ull - v : v;
+  constexpr unsigned long long kBias = 0x0080808080808080ull;
+  return (sv + kBias) ^ kBias;
 }
 
 struct SliceScale {
@@ -183,21 +170,32 @@ struct SliceScale {
   __device__ explicit SliceScale(int e_) : e(e_) {}
 };
 
-// Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16 bytes.
+// Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16
+// bytes: a byte transpose of the 16 digit words, 15 PRMT per 4 values (one
+// PRMT gathers two digit positions of two values, one more joins two pairs).
 template <class Get>
 __device__ __forceinline__ void pack16(Get get, const SliceScale& sc, uint4 (&out)[kOzS]) {
   uint32_t w[kOzS][4];
 #pragma unroll
-  for (int p = 0; p < kOzS; ++p)
+  for (int g = 0; g < 4; ++g) {
+    uint32_t lo[4], hi[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) w[p][q] = 0u;
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    int d[kOzS];
-    split_digits(get(u), sc.e, d);
-#pragma unroll
-    for (int p = 0; p < kOzS; ++p)
-      w[p][u >> 2] |= (static_cast<uint32_t>(d[p]) & 0xFFu) << (8 * (u & 3));
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long d = digit_bytes(get(4 * g + u), sc.e);
+      lo[u] = static_cast<uint32_t>(d);        // d_6, d_5, d_4, d_3
+      hi[u] = static_cast<uint32_t>(d >> 32);  // d_2, d_1, d_0, 0
+    }
+    const uint32_t l01a = __byte_perm(lo[0], lo[1], 0x5140), l01c = __byte_perm(lo[2], lo[3], 0x5140);
+    const uint32_t l23a = __byte_perm(lo[0], lo[1], 0x7362), l23c = __byte_perm(lo[2], lo[3], 0x7362);
+    const uint32_t h01a = __byte_perm(hi[0], hi[1], 0x5140), h01c = __byte_perm(hi[2], hi[3], 0x5140);
+    const uint32_t h23a = __byte_perm(hi[0], hi[1], 0x7362), h23c = __byte_perm(hi[2], hi[3], 0x7362);
+    w[6][g] = __byte_perm(l01a, l01c, 0x5410);
+    w[5][g] = __byte_perm(l01a, l01c, 0x7632);
+    w[4][g] = __byte_perm(l23a, l23c, 0x5410);
+    w[3][g] = __byte_perm(l23a, l23c, 0x7632);
+    w[2][g] = __byte_perm(h01a, h01c, 0x5410);
+    w[1][g] = __byte_perm(h01a, h01c, 0x7632);
+    w[0][g] = __byte_perm(h23a, h23c, 0x5410);
   }
 #pragma unroll
   for (int p = 0; p < kOzS; ++p) out[p] = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
@@ -250,32 +248,49 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
 }
 
 // Slices of A in both K-major layouts (rows, cols multiples of 16):
-//   sR[item][p][i][j] with eRow[i]   and   sC[item][p][j][i] with eCol[j].
+//   sR[item][p] (tile_off with row i, K = cols) with eRow[i]   and
+//   sC[item][p] (tile_off with row j, K = rows) with eCol[j].
+// 64 x 64 tiles through shared memory, [col][row] with pitch 72 and 2 doubles
+// of padding after every 16 rows: the column pass (thread = column, 16-row
+// chunk; 16-byte reads) and the row pass (a warp = 32 consecutive rows of one
+// 16-column chunk) are both bank-conflict free, and every warp stores whole
+// 128-byte lines of the tiled layout.
+constexpr int kOzTP = 72;
+__device__ __forceinline__ int oz_tile_idx(int c, int r) { return c * kOzTP + r + 2 * (r >> 4); }
+
 __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restrict__ A, int64_t lda,
                                                          int64_t sA, int rows, int cols,
                                                          const int* __restrict__ eRow,
                                                          const int* __restrict__ eCol,
                                                          int8_t* __restrict__ sR,
                                                          int8_t* __restrict__ sC) {
-  __shared__ double tile[64][65];  // [col][row]
+  __shared__ __align__(16) double tile[64 * kOzTP];
   const int item = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const double* Ab = A + item * sA;
   for (int t = threadIdx.x; t < 64 * 64; t += 256) {
     const int r = t & 63, c = t >> 6;
     const int i = i0 + r, j = j0 + c;
-    tile[c][r] = (i < rows && j < cols) ? Ab[i + static_cast<int64_t>(j) * lda] : 0.0;
+    tile[oz_tile_idx(c, r)] = (i < rows && j < cols) ? Ab[i + static_cast<int64_t>(j) * lda] : 0.0;
   }
   __syncthreads();
   const int64_t plane = static_cast<int64_t>(rows) * cols;
-  const int a = threadIdx.x >> 2, part = (threadIdx.x & 3) * 16;
   // column-major slices: column j0 + a, rows i0 + part .. +15
   {
+    const int a = threadIdx.x >> 2, part = (threadIdx.x & 3) * 16;
     const int j = j0 + a;
     if (j < cols && i0 + part < rows) {
       const SliceScale sc(usable_exp(eCol[static_cast<int64_t>(item) * cols + j]));
+      const double2* src = reinterpret_cast<const double2*>(&tile[oz_tile_idx(a, part)]);
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2 q = src[u];
+        v[2 * u] = q.x;
+        v[2 * u + 1] = q.y;
+      }
       uint4 out[kOzS];
-      pack16([&](int u) { return tile[a][part + u]; }, sc, out);
+      pack16([&](int u) { return v[u]; }, sc, out);
       int8_t* dst = sC + item * kOzS * plane + tile_off(j, (i0 + part) >> 4, rows);
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
@@ -283,11 +298,12 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
   }
   // row-major slices: row i0 + a, columns j0 + part .. +15
   {
+    const int a = threadIdx.x & 63, part = (threadIdx.x >> 6) * 16;
     const int i = i0 + a;
     if (i < rows && j0 + part < cols) {
       const SliceScale sc(usable_exp(eRow[static_cast<int64_t>(item) * rows + i]));
       uint4 out[kOzS];
-      pack16([&](int u) { return tile[part + u][a]; }, sc, out);
+      pack16([&](int u) { return tile[oz_tile_idx(part + u, a)]; }, sc, out);
       int8_t* dst = sR + item * kOzS * plane + tile_off(i, (j0 + part) >> 4, cols);
 #pragma unroll
       for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(dst + p * plane) = out[p];
