@@ -127,6 +127,7 @@ void dgemm_ex(bool trans_a, int64_t M, int64_t N, int64_t K, CMatRef A, CMatRef 
 // (oz_slice_bytes(K, N, batch) bytes, N * batch ints); oz_gemm: C (M x N) =
 // op(A) B from the slices of op(A) (sA / eA, M x K, K-major) and of B.
 bool oz_supported(int64_t rows, int64_t cols, int64_t K);
+double oz_grid_efficiency(int64_t M, int64_t N, int64_t batch);
 #ifdef RSVD_OZ_TRACE
 void oz_trace_read(unsigned long long* out, int64_t n);  // tools/probe/oz_trace.py
 #endif

@@ -302,12 +302,12 @@ int64_t partial_need(const Shape& s) {
 }
 
 // The A-passes run on the INT8 tensor cores (Ozaki slices, ozaki.cu) when
-// the 128 x 64 output tiles of both directions fill the GPU (>= 90% of one
-// wave, last wave >= 3/4 full: C4, C5, 5-item C4 chunks) and both K extents
-// are >= 1024 (a tile's prologue / TMEM drain is ~10 K steps: C2's K = 256
-// measured 22.2k against 25.4k trunc/s on DMMA).  Smaller shapes (C1, C2, and
-// C3's 160 tiles = two thin waves) stay on the split-K DMMA GEMM.
-// RSVD_FP64_GEMM=dmma forces the DMMA path (tests compare both).
+// the one-CTA-per-SM output tiles of both directions keep >= 72% of their
+// SM-waves busy (128 x 64 tiles, or 128 x 32 for grids of one or two thin
+// waves: C3, C4, C5, C4 chunks of >= 2 items) and both K extents are >= 1024
+// (a tile's prologue / TMEM drain is ~10 K steps: C2's K = 256 measured 22.2k
+// against 25.4k trunc/s on DMMA).  C1 (24 tiles) and C2 stay on the split-K
+// DMMA GEMM.  RSVD_FP64_GEMM=dmma forces the DMMA path (tests compare both).
 bool oz_wanted(const Shape& s) {
   static const bool off = [] {
     const char* e = std::getenv("RSVD_FP64_GEMM");
@@ -315,11 +315,8 @@ bool oz_wanted(const Shape& s) {
   }();
   if (off || !oz_supported(s.m, s.n, s.ellp) || s.m > 65536 || s.n > 65536) return false;
   if (s.m < 1024 || s.n < 1024) return false;
-  const int64_t nt = ceil_div(s.ellp, 64), sm = num_sms();
-  auto fills = [&](int64_t tiles) {
-    return tiles * 10 >= sm * 9 && tiles * 4 >= ceil_div(tiles, sm) * sm * 3;
-  };
-  return fills(ceil_div(s.m, 128) * nt * s.batch) && fills(ceil_div(s.n, 128) * nt * s.batch);
+  return oz_grid_efficiency(s.m, s.ellp, s.batch) >= 0.72 &&
+         oz_grid_efficiency(s.n, s.ellp, s.batch) >= 0.72;
 }
 
 Buffers carve(Carver& c, const Shape& s, bool host_io, bool want_svd) {

@@ -40,11 +40,11 @@ namespace {
 
 constexpr int kOzS = 7;       // slices per operand
 constexpr int kOzBM = 128;    // UMMA M
-constexpr int kOzBN = 64;     // UMMA N (S * BN = 448 of the 512 TMEM columns)
+constexpr int kOzBN = 64;     // UMMA N of the wide tile (S * BN = 448 of the 512 TMEM columns)
+constexpr int kOzBNs = 32;    // narrow tile for grids of one or two thin waves (C3: 288 tiles)
 constexpr int kOzKC = 32;     // K bytes per stage = one MMA K step = one 32B swizzle row
 constexpr int kOzStages = 5;  // 5 x 42 KB ring
 constexpr int kOzKChunk = 16384;  // K per launch: 7 * 16384 * 128^2 < 2^31
-constexpr int kOzTmemCols = 512;
 constexpr int kExpNone = static_cast<int>(0x80808080u);  // cudaMemset(0x80): below any frexp exponent
 
 __device__ __forceinline__ uint32_t sm_addr(const void* p) {
@@ -222,13 +222,18 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
   const double* Ab = A + item * sA;
   const int i = i0 + tx;
   double rm = 0.0;
-#pragma unroll 4
-  for (int c = ty; c < 64; c += 4) {
-    const int j = j0 + c;
-    double v = 0.0;
-    if (i < rows && j < cols) v = fabs(Ab[i + static_cast<int64_t>(j) * lda]);
-    rm = fmax(rm, v);
-    tile[c][tx] = v;
+  {
+    double v[16];  // all 16 loads in flight
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int j = j0 + ty + 4 * k;
+      v[k] = (i < rows && j < cols) ? fabs(__ldg(Ab + i + static_cast<int64_t>(j) * lda)) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      rm = fmax(rm, v[k]);
+      tile[ty + 4 * k][tx] = v[k];
+    }
   }
   rmax[ty][tx] = rm;
   __syncthreads();
@@ -268,10 +273,17 @@ __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restric
   const int item = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const double* Ab = A + item * sA;
-  for (int t = threadIdx.x; t < 64 * 64; t += 256) {
-    const int r = t & 63, c = t >> 6;
-    const int i = i0 + r, j = j0 + c;
-    tile[oz_tile_idx(c, r)] = (i < rows && j < cols) ? Ab[i + static_cast<int64_t>(j) * lda] : 0.0;
+  {
+    // all 16 loads of the thread in flight before the first shared-memory store
+    const int r = threadIdx.x & 63, c0 = threadIdx.x >> 6;
+    const double* src = Ab + (i0 + r) + static_cast<int64_t>(j0 + c0) * lda;
+    const bool rok = i0 + r < rows;
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      v[k] = (rok && j0 + c0 + 4 * k < cols) ? __ldg(src + static_cast<int64_t>(4 * k) * lda) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[oz_tile_idx(c0 + 4 * k, r)] = v[k];
   }
   __syncthreads();
   const int64_t plane = static_cast<int64_t>(rows) * cols;
@@ -381,21 +393,27 @@ struct OzArgs {
 };
 
 constexpr int kOzBytesA = kOzS * kOzBM * kOzKC;
-constexpr int kOzBytesB = kOzS * kOzBN * kOzKC;
-constexpr int kOzStage = kOzBytesA + kOzBytesB;
-constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 512;
+template <int BN>
+struct OzTile {
+  static constexpr int kBytesB = kOzS * BN * kOzKC;
+  static constexpr int kStage = kOzBytesA + kBytesB;
+  static constexpr int kSmem = kOzStages * kStage + 1024 + 512;
+  static constexpr int kTmemCols = kOzS * BN > 256 ? 512 : 256;
+};
 
 // One 128 x BN tile of C per CTA.  Warp 0 lane 0: TMA producer; warp 1 lane 0:
 // MMA issuer; warp 2 owns the TMEM allocation; all four warps drain TMEM
 // (warp w reads lanes 32w..32w+31 = tile rows).
+template <int BN>
 __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
                                                          const OzArgs p) {
+  constexpr int kStage = OzTile<BN>::kStage, kTmemCols = OzTile<BN>::kTmemCols;
   extern __shared__ __align__(1024) unsigned char oz_smem[];
   const uint32_t raw = sm_addr(oz_smem);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   unsigned char* sgen = oz_smem + (sbase - raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sgen + kOzStages * kOzStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sgen + kOzStages * kStage);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kOzStages + 1);
   int* seb = reinterpret_cast<int*>(bars + 2 * kOzStages + 2);  // eB - 12 of the tile's columns
   const uint32_t bar0 = sm_addr(bars);
@@ -404,7 +422,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   const uint32_t done_bar = bar0 + 8u * (2 * kOzStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kOzBN, m0 = blockIdx.y * kOzBM, item = blockIdx.z;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kOzBM, item = blockIdx.z;
   if (threadIdx.x == 0) OZ_STAMP(0);
   if (threadIdx.x >= 64) {
     const int col = n0 + static_cast<int>(threadIdx.x) - 64;
@@ -426,7 +444,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      sm_addr(tmem_slot)),
-                 "r"(kOzTmemCols)
+                 "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
@@ -440,8 +458,8 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
     for (int kc = 0; kc < nk; ++kc) {
       const int s = kc % kOzStages;
       if (kc >= kOzStages) mb_wait(empty_bar(s), ((kc / kOzStages) - 1) & 1);
-      const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
-      mb_expect_tx(full_bar(s), kOzStage);
+      const uint32_t dA = sbase + s * kStage, dB = dA + kOzBytesA;
+      mb_expect_tx(full_bar(s), kStage);
       tma_4d(dA, &tmA, 8 * (p.k_begin + kc * kOzKC), m0 >> 3, 0, item, full_bar(s));
       tma_4d(dB, &tmB, 8 * (p.k_begin + kc * kOzKC), n0 >> 3, 0, item, full_bar(s));
     }
@@ -455,22 +473,22 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
     // (a 128 x 64 x 32 MMA is smem-bound at 48 cycles, 256-wide runs at N/2).
     constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) |
                                 (static_cast<uint32_t>(kOzBM >> 4) << 24);
-    constexpr int kQ = 256 / kOzBN;  // B slices per MMA
+    constexpr int kQ = 256 / BN;  // B slices per MMA
     for (int kc = 0; kc < nk; ++kc) {
       const int s = kc % kOzStages;
       mb_wait(full_bar(s), (kc / kOzStages) & 1);
       if (kc == 0) OZ_STAMP(2);
       tc_fence_after();
-      const uint32_t dA = sbase + s * kOzStage, dB = dA + kOzBytesA;
+      const uint32_t dA = sbase + s * kStage, dB = dA + kOzBytesA;
 #pragma unroll
       for (int pa = 0; pa < kOzS; ++pa) {
         const uint64_t da = umma_desc_kmajor(dA + pa * (kOzBM * kOzKC));
 #pragma unroll
         for (int q0 = 0; q0 < kOzS - pa; q0 += kQ) {
           const int nq = (kOzS - pa - q0) < kQ ? (kOzS - pa - q0) : kQ;
-          const uint64_t db = umma_desc_kmajor(dB + q0 * (kOzBN * kOzKC));
-          const uint32_t idesc = idesc0 | (static_cast<uint32_t>((nq * kOzBN) >> 3) << 17);
-          tc_mma_i8(tmem + static_cast<uint32_t>((pa + q0) * kOzBN), da, db, idesc,
+          const uint64_t db = umma_desc_kmajor(dB + q0 * (BN * kOzKC));
+          const uint32_t idesc = idesc0 | (static_cast<uint32_t>((nq * BN) >> 3) << 17);
+          tc_mma_i8(tmem + static_cast<uint32_t>((pa + q0) * BN), da, db, idesc,
                     (kc > 0 || pa > 0) ? 1u : 0u);
         }
       }
@@ -494,7 +512,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   // (ldexp only outside the normal range), then the stores (the values of a
   // later K chunk's C are read up front, 32 independent loads).
 #pragma unroll 1
-  for (int c0 = 0; c0 < kOzBN; c0 += 32) {
+  for (int c0 = 0; c0 < BN; c0 += 32) {
     if (n0 + c0 >= p.N) break;
     double t[32];
 #pragma unroll
@@ -502,14 +520,14 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
 #pragma unroll 1
     for (int d = kOzS - 1; d >= 0; --d) {
       uint32_t r[32];
-      tc_ld32(lane_base + static_cast<uint32_t>(d * kOzBN + c0), r);
+      tc_ld32(lane_base + static_cast<uint32_t>(d * BN + c0), r);
 #pragma unroll
       for (int j = 0; j < 32; ++j) t[j] = fma(t[j], 0.00390625, i32_to_f64(r[j]));
     }
     if (threadIdx.x == 0) OZ_STAMP(c0 ? 6 : 4);
     if (row_ok) {
       double* cp = Crow + static_cast<int64_t>(n0 + c0) * p.ldc;
-      const int nc = min(min(32, kOzBN - c0), p.N - n0 - c0);
+      const int nc = min(min(32, BN - c0), p.N - n0 - c0);
       if (p.accumulate) {
         double cv[32];
 #pragma unroll
@@ -530,7 +548,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(kOzTmemCols)
+                 "r"(kTmemCols)
                  : "memory");
   }
   if (threadIdx.x == 0) OZ_STAMP(7);
@@ -615,24 +633,58 @@ void oz_slice_b(CMatRef B, int64_t K, int64_t N, int64_t batch, int8_t* sB, int*
   RSVD_LAUNCH("oz_slice_b_kernel");
 }
 
-void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, const int8_t* sB,
-             const int* eB, MatRef C, int64_t batch, cudaStream_t st) {
+namespace {
+
+template <int BN>
+void oz_gemm_launch(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA,
+                    const int8_t* sB, const int* eB, MatRef C, int64_t batch, cudaStream_t st) {
   CUtensorMap ma, mb;
-  if (!oz_map(&ma, sA, K, M, batch, kOzBM) || !oz_map(&mb, sB, K, N, batch, kOzBN))
+  if (!oz_map(&ma, sA, K, M, batch, kOzBM) || !oz_map(&mb, sB, K, N, batch, BN))
     throw CudaError("oz_gemm: cuTensorMapEncodeTiled failed");
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
-    RSVD_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kOzSmem));
+    RSVD_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   OzTile<BN>::kSmem));
   });
-  dim3 grid(static_cast<unsigned>(ceil_div(N, kOzBN)), static_cast<unsigned>(ceil_div(M, kOzBM)),
+  dim3 grid(static_cast<unsigned>(ceil_div(N, BN)), static_cast<unsigned>(ceil_div(M, kOzBM)),
             static_cast<unsigned>(batch));
   for (int64_t k0 = 0; k0 < K; k0 += kOzKChunk) {
     OzArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(std::min<int64_t>(kOzKChunk, K - k0)),
              static_cast<int>(k0), k0 > 0 ? 1 : 0, C.base, C.ld, C.stride, eA, eB};
-    oz_gemm_kernel<<<grid, 128, kOzSmem, st>>>(ma, mb, a);
+    oz_gemm_kernel<BN><<<grid, 128, OzTile<BN>::kSmem, st>>>(ma, mb, a);
     RSVD_LAUNCH("oz_gemm_kernel");
   }
+}
+
+// Fraction of the SM-waves a grid of `tiles` one-CTA-per-SM tiles keeps busy.
+double oz_fill(int64_t tiles) {
+  const int64_t sm = num_sms();
+  return static_cast<double>(tiles) / static_cast<double>(ceil_div(tiles, sm) * sm);
+}
+
+}  // namespace
+
+// Output tile width for an M x N product over `batch` items: 64 columns (the
+// most work per byte of A) unless the grid is a few thin waves that 32-wide
+// tiles fill better (a 32-wide tile costs ~7% more tensor time per column).
+int oz_tile_n(int64_t M, int64_t N, int64_t batch) {
+  const int64_t mt = ceil_div(M, kOzBM) * batch;
+  const double f64 = oz_fill(mt * ceil_div(N, kOzBN)), f32 = 0.93 * oz_fill(mt * ceil_div(N, kOzBNs));
+  return f32 > f64 ? kOzBNs : kOzBN;
+}
+
+// Tensor-time efficiency of the grid oz_gemm would launch (1 = full waves of wide tiles).
+double oz_grid_efficiency(int64_t M, int64_t N, int64_t batch) {
+  const int64_t mt = ceil_div(M, kOzBM) * batch;
+  return std::max(oz_fill(mt * ceil_div(N, kOzBN)), 0.93 * oz_fill(mt * ceil_div(N, kOzBNs)));
+}
+
+void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, const int8_t* sB,
+             const int* eB, MatRef C, int64_t batch, cudaStream_t st) {
+  if (oz_tile_n(M, N, batch) == kOzBNs)
+    oz_gemm_launch<kOzBNs>(M, N, K, sA, eA, sB, eB, C, batch, st);
+  else
+    oz_gemm_launch<kOzBN>(M, N, K, sA, eA, sB, eB, C, batch, st);
 }
 
 }  // namespace rsvd
