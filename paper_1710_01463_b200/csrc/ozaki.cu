@@ -222,18 +222,13 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
   const double* Ab = A + item * sA;
   const int i = i0 + tx;
   double rm = 0.0;
-  {
-    double v[16];  // all 16 loads in flight
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int j = j0 + ty + 4 * k;
-      v[k] = (i < rows && j < cols) ? fabs(__ldg(Ab + i + static_cast<int64_t>(j) * lda)) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      rm = fmax(rm, v[k]);
-      tile[ty + 4 * k][tx] = v[k];
-    }
+#pragma unroll 4
+  for (int c = ty; c < 64; c += 4) {
+    const int j = j0 + c;
+    double v = 0.0;
+    if (i < rows && j < cols) v = fabs(Ab[i + static_cast<int64_t>(j) * lda]);
+    rm = fmax(rm, v);
+    tile[c][tx] = v;
   }
   rmax[ty][tx] = rm;
   __syncthreads();
