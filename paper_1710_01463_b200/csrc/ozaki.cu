@@ -400,9 +400,8 @@ struct OzTile {
 // MMA issuer; warp 2 owns the TMEM allocation; all four warps drain TMEM
 // (warp w reads lanes 32w..32w+31 = tile rows).
 template <int BN>
-__global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                         const __grid_constant__ CUtensorMap tmB,
-                                                         const OzArgs p) {
+__device__ __forceinline__ void oz_tile(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                        const OzArgs& p, const int n0) {
   constexpr int kStage = OzTile<BN>::kStage, kTmemCols = OzTile<BN>::kTmemCols;
   extern __shared__ __align__(1024) unsigned char oz_smem[];
   const uint32_t raw = sm_addr(oz_smem);
@@ -417,7 +416,7 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   const uint32_t done_bar = bar0 + 8u * (2 * kOzStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kOzBM, item = blockIdx.z;
+  const int m0 = blockIdx.y * kOzBM, item = blockIdx.z;
   if (threadIdx.x == 0) OZ_STAMP(0);
   if (threadIdx.x >= 64) {
     const int col = n0 + static_cast<int>(threadIdx.x) - 64;
@@ -549,6 +548,25 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   if (threadIdx.x == 0) OZ_STAMP(7);
 }
 
+template <int BN>
+__global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const OzArgs p) {
+  oz_tile<BN>(tmA, tmB, p, static_cast<int>(blockIdx.x) * BN);
+}
+
+// `wide` 64-column tiles and one 32-column tile for a remainder of N of at
+// most 32 columns (l_p = 288 = 4 x 64 + 32: a fifth wide tile would be half
+// padding, 10% of the launch).
+__global__ void __launch_bounds__(128, 1) oz_gemm_mixed_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBw,
+    const __grid_constant__ CUtensorMap tmBn, const OzArgs p, const int wide) {
+  if (static_cast<int>(blockIdx.x) < wide)
+    oz_tile<kOzBN>(tmA, tmBw, p, static_cast<int>(blockIdx.x) * kOzBN);
+  else
+    oz_tile<kOzBNs>(tmA, tmBn, p, wide * kOzBN);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -676,10 +694,33 @@ double oz_grid_efficiency(int64_t M, int64_t N, int64_t batch) {
 
 void oz_gemm(int64_t M, int64_t N, int64_t K, const int8_t* sA, const int* eA, const int8_t* sB,
              const int* eB, MatRef C, int64_t batch, cudaStream_t st) {
-  if (oz_tile_n(M, N, batch) == kOzBNs)
+  if (oz_tile_n(M, N, batch) == kOzBNs) {
     oz_gemm_launch<kOzBNs>(M, N, K, sA, eA, sB, eB, C, batch, st);
-  else
+    return;
+  }
+  const int64_t wide = N / kOzBN, rem = N - wide * kOzBN;
+  if (wide == 0 || rem == 0 || rem > kOzBNs) {
     oz_gemm_launch<kOzBN>(M, N, K, sA, eA, sB, eB, C, batch, st);
+    return;
+  }
+  CUtensorMap ma, mbw, mbn;
+  if (!oz_map(&ma, sA, K, M, batch, kOzBM) || !oz_map(&mbw, sB, K, N, batch, kOzBN) ||
+      !oz_map(&mbn, sB, K, N, batch, kOzBNs))
+    throw CudaError("oz_gemm: cuTensorMapEncodeTiled failed");
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
+    RSVD_CUDA(cudaFuncSetAttribute(oz_gemm_mixed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   OzTile<kOzBN>::kSmem));
+  });
+  dim3 grid(static_cast<unsigned>(wide + 1), static_cast<unsigned>(ceil_div(M, kOzBM)),
+            static_cast<unsigned>(batch));
+  for (int64_t k0 = 0; k0 < K; k0 += kOzKChunk) {
+    OzArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(std::min<int64_t>(kOzKChunk, K - k0)),
+             static_cast<int>(k0), k0 > 0 ? 1 : 0, C.base, C.ld, C.stride, eA, eB};
+    oz_gemm_mixed_kernel<<<grid, 128, OzTile<kOzBN>::kSmem, st>>>(ma, mbw, mbn, a,
+                                                                  static_cast<int>(wide));
+    RSVD_LAUNCH("oz_gemm_mixed_kernel");
+  }
 }
 
 }  // namespace rsvd

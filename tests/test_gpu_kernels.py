@@ -108,14 +108,17 @@ def test_dgemm_odd_leading_dimension(cuda):
     "M,N,K,batch,grade",
     [(128, 64, 32, 1, 0), (128, 48, 64, 2, 0), (256, 288, 512, 3, 0), (1024, 80, 1024, 1, 0),
      (1024, 96, 2048, 2, 12), (4096, 288, 4096, 2, 0), (2048, 544, 32768, 1, 0),
-     (512, 64, 256, 1, 300)],
+     (512, 64, 256, 1, 300), (4096, 288, 2048, 8, 6), (4096, 256, 1024, 8, 0)],
 )
 def test_ozaki_gemm_vs_torch(cuda, trans_a, M, N, K, batch, grade):
     """Emulated FP64 (7 signed 8-bit slices per operand on the INT8 tensor
     cores, ozaki.cu) against torch float64: elementwise within 8e-15 of
     |op(A)| |B| (an FP64 GEMM's K u |A||B| bound is ~1e-12 here), normwise
     within 1e-14; `grade` spreads the K columns of op(A) over 10^-grade
-    (per-row exponents keep the small entries), 300 = extreme magnitudes."""
+    (per-row exponents keep the small entries), 300 = extreme magnitudes.
+    The shapes cover the three launch forms: 128 x 32 tiles (small grids),
+    128 x 64 tiles (8 x 4096 x 256), and the mixed grid of 64-wide tiles plus
+    one 32-wide remainder tile (544 columns; 288 columns on 8 items)."""
     import torch
 
     g = torch.Generator(device=cuda).manual_seed(M * 5 + N * 11 + K)
