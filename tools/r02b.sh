@@ -27,10 +27,10 @@ full() {  # name config kernel-regex [launch-skip]
   timeout 900 $NCU --set full --import-source on -k "regex:$3" --launch-skip ${4:-0} -c 1 \
     -o $out/$1 python tools/probe/one_call.py $2 > $out/$1.log 2>&1
 }
-full ozgemm_c4 C4 oz_gemm_kernel 0
-full ozgemm_tn_c4 C4 oz_gemm_kernel 1
+full ozgemm_c4 C4 oz_gemm 0
+full ozgemm_tn_c4 C4 oz_gemm 1
 full ozslicea_c4 C4 oz_slice_a_kernel 0
 full ozsliceb_c4 C4 oz_slice_b_kernel 0
 full ozexp_c4 C4 oz_exp_kernel 0
-full ozgemm_c5 C5 oz_gemm_kernel 0
+full ozgemm_c5 C5 oz_gemm 0
 ls -la $out
