@@ -629,6 +629,11 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches,
             "roofline": roof,
             "gemm_path": gemm_path,
+            "precision": ("f64 in and out; A-pass products rebuilt exactly from 7 x 7 signed 8-bit "
+                          "slice products (54-bit operands, INT32 / FP64 accumulation): elementwise "
+                          "within 8e-15 |A||B| of torch f64 (tests/test_gpu_kernels.py), parity with "
+                          "the reference build at this size in tests/test_gpu_configs.py"
+                          if gemm_path == "ozaki" else "f64 (DMMA) throughout"),
             "pipeline": {"tflops_alg": falg * total * args.steps / (ms / 1000) / 1e12 / world,
                          "frac_fp64_peak": falg * B * args.steps / (ms / 1000) / 1e12 / FP64_PEAK_TFLOPS,
                          "stage_ms_per_step": {k2: v[0] / prof_steps for k2, v in prof.items()},
