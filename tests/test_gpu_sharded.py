@@ -14,11 +14,12 @@ pytestmark = pytest.mark.gpu
 def run_sharded(A, params, world):
     import torch
 
-    from paper_1710_01463_b200 import Handle, sharding
+    from paper_1710_01463_b200 import Handle, _lib, sharding
 
     m = A.shape[0]
     group = sharding.Group(world)
     results = [None] * world
+    run_sharded.gemm_paths = [None] * world
     errors = []
 
     def worker(rank):
@@ -32,6 +33,7 @@ def run_sharded(A, params, world):
                 f = sharding.rsvd_rowsharded(a_loc, m, first, params, h)
                 torch.cuda.synchronize()
             results[rank] = (first, count, f)
+            run_sharded.gemm_paths[rank] = _lib.last_gemm_path(h)
         except Exception as e:  # pragma: no cover - surfaced below
             errors.append(e)
 
@@ -75,6 +77,36 @@ def test_rowsharded_matches_unsharded_and_oracle(cuda, oracle_mod, world, ref_mo
     er = np.linalg.norm(a - (ref[0] * ref[1]) @ ref[2])
     assert abs(e - er) / er < 1e-10
     assert subspace_distance(U[:, :20], ref[0][:, :20]) < 1e-8
+    assert f0.discarded_weight == pytest.approx(ref[3], rel=1e-8)
+
+
+def test_rowsharded_on_the_int8_path(cuda, oracle_mod, ref_mod):
+    """Two row shards of a 4096 x 2048 matrix: each rank's 2048 x 2048 shard
+    is large enough for the emulated-FP64 A-passes (INT8 tensor cores, per-rank
+    row / column exponents of its own shard), the all-reduced A^T Q panels and
+    Grams are FP64.  Same tolerances against the reference build."""
+    import torch
+
+    from paper_1710_01463_b200 import RsvdParams
+
+    m, n, k, ell, q, seed = 4096, 2048, 256, 276, 1, 0xBEEF
+    a = matrix_with_spectrum(oracle_mod, 5, m, n, np.exp(-np.arange(n) / 60.0))
+    A = torch.from_numpy(a).to(cuda).t().contiguous().t()
+    res = run_sharded(A, RsvdParams(k, ell, q, seed), 2)
+    assert run_sharded.gemm_paths == ["ozaki", "ozaki"]
+    ref = ref_mod.rsvd(a, k, ell, q, seed)
+    f0 = res[0][2]
+    U = np.zeros((m, f0.rank()))
+    for first, count, f in res:
+        assert torch.equal(f.sigma, f0.sigma) and torch.equal(f.right_adj, f0.right_adj)
+        U[first:first + count] = f.left.cpu().numpy()
+    S, Vt = f0.sigma.cpu().numpy(), f0.right_adj.cpu().numpy()
+    assert len(S) == len(ref[1]) == k
+    assert rel_sigma_err(S, ref[1]) < 1e-10
+    assert isometry_err(U) < 1e-12 and isometry_err(Vt.T) < 1e-12
+    e = np.linalg.norm(a - (U * S) @ Vt)
+    er = np.linalg.norm(a - (ref[0] * ref[1]) @ ref[2])
+    assert abs(e - er) / er < 1e-10
     assert f0.discarded_weight == pytest.approx(ref[3], rel=1e-8)
 
 
