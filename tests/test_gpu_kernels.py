@@ -108,7 +108,8 @@ def test_dgemm_odd_leading_dimension(cuda):
     "M,N,K,batch,grade",
     [(128, 64, 32, 1, 0), (128, 48, 64, 2, 0), (256, 288, 512, 3, 0), (1024, 80, 1024, 1, 0),
      (1024, 96, 2048, 2, 12), (4096, 288, 4096, 2, 0), (2048, 544, 32768, 1, 0),
-     (512, 64, 256, 1, 300), (4096, 288, 2048, 8, 6), (4096, 256, 1024, 8, 0)],
+     (512, 64, 256, 1, 300), (4096, 288, 2048, 8, 6), (4096, 256, 1024, 8, 0),
+     (272, 96, 1040, 2, 0)],
 )
 def test_ozaki_gemm_vs_torch(cuda, trans_a, M, N, K, batch, grade):
     """Emulated FP64 (7 signed 8-bit slices per operand on the INT8 tensor
