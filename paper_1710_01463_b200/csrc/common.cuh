@@ -76,6 +76,18 @@ inline int num_sms() {
   }
   return v;
 }
+// Total memory of the current device in bytes (cached per device ordinal).
+inline int64_t device_total_memory() {
+  static std::atomic<int64_t> cache[kMaxDevices];
+  const int d = current_device();
+  int64_t v = cache[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    size_t fr = 0, tot = 0;
+    v = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? static_cast<int64_t>(tot) : (int64_t{180} << 30);
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 // Function attributes (e.g. the dynamic shared-memory opt-in) are per device
 // context: `mask` (one per kernel instantiation) records the devices on which
 // `apply` already ran.  apply() is idempotent, so a race only repeats it.

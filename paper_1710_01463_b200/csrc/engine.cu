@@ -315,6 +315,12 @@ bool oz_wanted(const Shape& s) {
   }();
   if (off || !oz_supported(s.m, s.n, s.ellp) || s.m > 65536 || s.n > 65536) return false;
   if (s.m < 1024 || s.n < 1024) return false;
+  // The slice copies (14 bytes per entry of A + the thin operand's) must leave
+  // room for the input and the rest of the workspace: beyond half of the
+  // device's memory the call stays on DMMA instead of failing its allocation.
+  const int64_t need = 2 * oz_slice_bytes(s.m, s.n, s.batch) +
+                       oz_slice_bytes(std::max(s.m, s.n), s.ellp, s.batch);
+  if (need > device_total_memory() / 2) return false;
   return oz_grid_efficiency(s.m, s.ellp, s.batch) >= 0.72 &&
          oz_grid_efficiency(s.n, s.ellp, s.batch) >= 0.72;
 }
