@@ -44,6 +44,22 @@ INT8_PEAK_TOPS = 8186 * 148 * 2 * 1.965e9 / 1e12  # tcgen05.mma kind::i8 rate, p
 INT8_PEAK_SOURCE = ("measured tcgen05.mma.kind::i8 issue rate, 8186 MAC/clk/SM for N >= 128 "
                     "(profiles/r02_umma_rate.txt) x 148 SMs x 2 x the 1965 MHz max SM clock; "
                     "MEASURED_PEAKS.json has no INT8 figure")
+def int8_vs_measured_bf16(achieved_tops):
+    """Context for the INT8 roofline: MEASURED_PEAKS.json (driver-written) has the dense bf16
+    cuBLAS throughput of this pool's B200s; INT8 tensor work runs at twice the bf16 rate, so
+    2 x that figure is what a library GEMM would sustain under the same power limit."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        burst, sus = 2.0 * mp["bf16_tflops"], 2.0 * mp.get("bf16_tflops_sustained", mp["bf16_tflops"])
+    except (OSError, ValueError, KeyError):
+        return {}
+    out = {"int8_tops_from_measured_bf16": {"burst": burst, "sustained": sus,
+                                            "source": "2 x MEASURED_PEAKS.json bf16_tflops / bf16_tflops_sustained"}}
+    if achieved_tops:
+        out["frac_of_2x_measured_bf16_sustained"] = achieved_tops / sus
+    return out
+
+
 OZ_SLICE_PRODUCTS = 28  # 7 slices per operand, products p + q < 7 (ozaki.cu)
 FP64_PEAK_TFLOPS = 37.1  # measured: mma.sync f64 probe, profiles/r01_fp64_peak.txt
 FP64_PEAK_SOURCE = ("measured DMMA (mma.sync .f64) throughput on this pool's B200, "
@@ -560,6 +576,7 @@ def run_ours(args, rank, world, local_rank):
                 "fp64_equivalent_vs_dmma_peak": (fp64_equiv / FP64_PEAK_TFLOPS) if fp64_equiv else None,
                 "peak_source": INT8_PEAK_SOURCE,
                 "slice_ms_per_step": slice_ms / prof_steps,
+                **int8_vs_measured_bf16(achieved),
                 "apass_share_of_step": gemm_ms / prof_steps / step_ms_prof}
     else:
         roof = {"bound": "tensor", "achieved": fp64_equiv, "peak": FP64_PEAK_TFLOPS,
