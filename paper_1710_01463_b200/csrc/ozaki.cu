@@ -142,36 +142,41 @@ __device__ __forceinline__ double scale_pow2(double x, int e) {
 
 __device__ __forceinline__ int usable_exp(int e) { return e == kExpNone ? 0 : e; }  // all-zero line
 
-// Signed 8-bit slices of x (|x| < 2^e): V = round(x 2^(54-e)), |V| <= 2^54, as
+// Signed 8-bit slices of x (|x| < 2^e): V = rint(x 2^(54-e)), |V| <= 2^54, as
 // 7 balanced base-256 digits d_0 (most significant, |d_0| <= 65) .. d_6 (in
 // [-128, 127]), V = sum_p d_p 256^(6-p): x = 2^e sum_p d_p 2^(-6-8p) up to the
-// rounding of V (half away from zero, <= 2^(e-55)).  Integer-only (FP64
-// conversions run at a few per clock per SM): V is the 53-bit significand
-// shifted by e + 1021 - (biased exponent) >= -1 bits.  Adding the bias
-// B = sum_p 128 * 256^p turns the balanced digits into the plain bytes of
-// V + B (d_p + 128 in [0, 255]), and flipping each byte's top bit gives d_p as
-// int8: the 7 digits are the low 7 bytes of (V + B) ^ B, byte 6 - p = d_p.
-__device__ __forceinline__ unsigned long long digit_bytes(double x, int e) {
-  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-  int ef = static_cast<int>(b >> 52) & 0x7FF;
-  unsigned long long m = b & 0xFFFFFFFFFFFFFull;
-  if (ef) m |= 1ull << 52; else ef = 1;  // subnormal: no implicit bit
-  // V = round(2 m / 2^s), s in [0, 63]: branch-free, the rounding term
-  // (1 << s) >> 1 vanishes for s = 0.
-  const int s = min(e + 1022 - ef, 63);
-  const unsigned long long v = ((m << 1) + ((1ull << s) >> 1)) >> s;
-  const unsigned long long sv = (b >> 63) ? 0ull - v : v;
-  constexpr unsigned long long kBias = 0x0080808080808080ull;
-  return (sv + kBias) ^ kBias;
+// rounding of V (<= 2^(e-55)).  No FP64 <-> integer conversion instruction
+// (they run at a few per clock per SM) and no 64-bit integer shifts: V is
+// split into hi = rint(v 2^-24) and lo = rint(v - hi 2^24) with the 1.5 * 2^52
+// trick, which leaves both integers in the low words of two doubles.  Adding
+// the bias 128 * (256^k - 1) / 255 turns balanced digits into plain bytes
+// (d + 128 in [0, 255]): the returned words hold d_6, d_5, d_4 (+128 each) in
+// bytes 0-2 of .x (byte 3 is the carry, unused) and d_3 .. d_0 (+128) in .y;
+// pack16 flips the top bits after the byte transpose.
+__device__ __forceinline__ uint2 digit_bytes(double x, double sc_lo, double sc_hi) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double v = (x * sc_lo) * sc_hi;           // exact: powers of two
+  const double th = fma(v, 0x1p-24, kMagic);
+  const double hd = th - kMagic;                  // rint(v 2^-24), |hd| <= 2^30
+  const double tl = fma(hd, -0x1p24, v) + kMagic;  // v - hd 2^24 is exact, |.| <= 2^23
+  const uint32_t lo = static_cast<uint32_t>(__double2loint(tl)) + 0x808080u;
+  const uint32_t hi = static_cast<uint32_t>(__double2loint(th)) + 0x80808080u + (lo >> 24);
+  return make_uint2(lo, hi);
 }
 
+// 2^(54 - e) as two finite powers of two (e is a frexp exponent: any int in
+// [-1073, 1024]).
 struct SliceScale {
-  int e;
-  __device__ explicit SliceScale(int e_) : e(e_) {}
+  double lo, hi;
+  __device__ explicit SliceScale(int e) {
+    const int t = 54 - e, a = t / 2;
+    lo = __hiloint2double((1023 + a) << 20, 0);
+    hi = __hiloint2double((1023 + t - a) << 20, 0);
+  }
 };
 
 // Slices of 16 consecutive values (get(u), u < 16) packed per slice into 16
-// bytes: a byte transpose of the 16 digit words, 15 PRMT per 4 values (one
+// bytes: a byte transpose of the 16 digit words, 14 PRMT per 4 values (one
 // PRMT gathers two digit positions of two values, one more joins two pairs).
 template <class Get>
 __device__ __forceinline__ void pack16(Get get, const SliceScale& sc, uint4 (&out)[kOzS]) {
@@ -181,21 +186,21 @@ __device__ __forceinline__ void pack16(Get get, const SliceScale& sc, uint4 (&ou
     uint32_t lo[4], hi[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const unsigned long long d = digit_bytes(get(4 * g + u), sc.e);
-      lo[u] = static_cast<uint32_t>(d);        // d_6, d_5, d_4, d_3
-      hi[u] = static_cast<uint32_t>(d >> 32);  // d_2, d_1, d_0, 0
+      const uint2 d = digit_bytes(get(4 * g + u), sc.lo, sc.hi);
+      lo[u] = d.x;  // d_6, d_5, d_4, carry
+      hi[u] = d.y;  // d_3, d_2, d_1, d_0
     }
     const uint32_t l01a = __byte_perm(lo[0], lo[1], 0x5140), l01c = __byte_perm(lo[2], lo[3], 0x5140);
-    const uint32_t l23a = __byte_perm(lo[0], lo[1], 0x7362), l23c = __byte_perm(lo[2], lo[3], 0x7362);
+    const uint32_t l2a = __byte_perm(lo[0], lo[1], 0x7362), l2c = __byte_perm(lo[2], lo[3], 0x7362);
     const uint32_t h01a = __byte_perm(hi[0], hi[1], 0x5140), h01c = __byte_perm(hi[2], hi[3], 0x5140);
     const uint32_t h23a = __byte_perm(hi[0], hi[1], 0x7362), h23c = __byte_perm(hi[2], hi[3], 0x7362);
-    w[6][g] = __byte_perm(l01a, l01c, 0x5410);
-    w[5][g] = __byte_perm(l01a, l01c, 0x7632);
-    w[4][g] = __byte_perm(l23a, l23c, 0x5410);
-    w[3][g] = __byte_perm(l23a, l23c, 0x7632);
-    w[2][g] = __byte_perm(h01a, h01c, 0x5410);
-    w[1][g] = __byte_perm(h01a, h01c, 0x7632);
-    w[0][g] = __byte_perm(h23a, h23c, 0x5410);
+    w[6][g] = __byte_perm(l01a, l01c, 0x5410) ^ 0x80808080u;
+    w[5][g] = __byte_perm(l01a, l01c, 0x7632) ^ 0x80808080u;
+    w[4][g] = __byte_perm(l2a, l2c, 0x5410) ^ 0x80808080u;
+    w[3][g] = __byte_perm(h01a, h01c, 0x5410) ^ 0x80808080u;
+    w[2][g] = __byte_perm(h01a, h01c, 0x7632) ^ 0x80808080u;
+    w[1][g] = __byte_perm(h23a, h23c, 0x5410) ^ 0x80808080u;
+    w[0][g] = __byte_perm(h23a, h23c, 0x7632) ^ 0x80808080u;
   }
 #pragma unroll
   for (int p = 0; p < kOzS; ++p) out[p] = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
