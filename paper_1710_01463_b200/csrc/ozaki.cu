@@ -212,6 +212,12 @@ __device__ __forceinline__ int exp_of_max(double amax) {
   return e;  // amax < 2^e
 }
 
+// 64 x 64 staging tile [col][row] with pitch 72 and 2 doubles of padding after
+// every 16 rows: 16-byte reads of (column, 16-row chunk) by thread pairs and
+// row reads by 32 consecutive rows are both bank-conflict free.
+constexpr int kOzTP = 72;
+__device__ __forceinline__ int oz_tile_idx(int c, int r) { return c * kOzTP + r + 2 * (r >> 4); }
+
 // Per-row and per-column exponents of A (rows x cols, column-major): 64 x 64
 // tiles, atomicMax into eRow / eCol (pre-set to kExpNone).  Rows reduce in
 // registers (16 columns per thread) and shared memory; columns from a shared
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
                                                      int64_t sA, int rows, int cols, int* eRow,
                                                      int* eCol) {
   __shared__ double rmax[4][64];
-  __shared__ double tile[64][65];  // [col][row] of |A|
+  __shared__ __align__(16) double tile[64 * kOzTP];  // [col][row] of |A|
   const int item = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
@@ -233,14 +239,18 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
     double v = 0.0;
     if (i < rows && j < cols) v = fabs(Ab[i + static_cast<int64_t>(j) * lda]);
     rm = fmax(rm, v);
-    tile[c][tx] = v;
+    tile[oz_tile_idx(c, tx)] = v;
   }
   rmax[ty][tx] = rm;
   __syncthreads();
   const int c = threadIdx.x >> 2, part = (threadIdx.x & 3) * 16;
+  const double2* colp = reinterpret_cast<const double2*>(&tile[oz_tile_idx(c, part)]);
   double cm = 0.0;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) cm = fmax(cm, tile[c][part + u]);
+  for (int u = 0; u < 8; ++u) {
+    const double2 q = colp[u];
+    cm = fmax(cm, fmax(q.x, q.y));
+  }
   cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
   cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
   const int j = j0 + c;
@@ -260,8 +270,6 @@ __global__ void __launch_bounds__(256) oz_exp_kernel(const double* __restrict__ 
 // chunk; 16-byte reads) and the row pass (a warp = 32 consecutive rows of one
 // 16-column chunk) are both bank-conflict free, and every warp stores whole
 // 128-byte lines of the tiled layout.
-constexpr int kOzTP = 72;
-__device__ __forceinline__ int oz_tile_idx(int c, int r) { return c * kOzTP + r + 2 * (r >> 4); }
 
 __global__ void __launch_bounds__(256) oz_slice_a_kernel(const double* __restrict__ A, int64_t lda,
                                                          int64_t sA, int rows, int cols,
@@ -342,20 +350,49 @@ __global__ void __launch_bounds__(256) oz_exp_b_kernel(const double* __restrict_
 
 // Slices of the right operand B (K % 16 == 0, N % 8 == 0) with eB's exponent
 // per column: sB[item][p] in the tiled layout (tile_off with row = column j of
-// B).  One CTA per 8 columns (one row group) and K range; thread (r, c) packs
-// the 16-byte chunk (column r, K chunk c), so a warp stores whole 128-byte lines.
+// B).  One CTA per 8 columns (one row group) and K range: the 8 x 512 block
+// is staged through shared memory (coalesced loads along K; pitch 578 with 2
+// doubles of padding per 16 keeps the 16-byte reads conflict free), then
+// thread (r, c) packs the 16-byte chunk (column r, K chunk c), so a warp
+// stores whole 128-byte lines.
+constexpr int kOzBP = kOzBK + 2 * (kOzBK / 16) + 2;
+
 __global__ void __launch_bounds__(256) oz_slice_b_kernel(const double* __restrict__ B, int64_t ldb,
                                                          int64_t sBst, int K, int N,
                                                          int8_t* __restrict__ sB,
                                                          const int* __restrict__ eB) {
-  const int j = blockIdx.x * 8 + (threadIdx.x & 7), item = blockIdx.z;
-  const int c = blockIdx.y * (kOzBK / 16) + (threadIdx.x >> 3);
+  __shared__ __align__(16) double tile[8 * kOzBP];
+  const int j0 = blockIdx.x * 8, k0 = blockIdx.y * kOzBK, item = blockIdx.z;
+  const double* Bb = B + item * sBst + static_cast<int64_t>(j0) * ldb + k0;
+  {
+    double v[16];  // all 16 loads in flight
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int r = t >> 1, kk = (t & 1) * 256 + static_cast<int>(threadIdx.x);
+      v[t] = (k0 + kk < K) ? __ldg(Bb + static_cast<int64_t>(r) * ldb + kk) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int r = t >> 1, kk = (t & 1) * 256 + static_cast<int>(threadIdx.x);
+      tile[r * kOzBP + kk + 2 * (kk >> 4)] = v[t];
+    }
+  }
+  __syncthreads();
+  const int r = threadIdx.x & 7, cl = threadIdx.x >> 3;
+  const int j = j0 + r, c = blockIdx.y * (kOzBK / 16) + cl;
   if (c >= (K >> 4)) return;
   const SliceScale sc(usable_exp(eB[static_cast<int64_t>(item) * N + j]));
-  const double* src = B + item * sBst + static_cast<int64_t>(j) * ldb + c * 16;
+  const double2* src = reinterpret_cast<const double2*>(&tile[r * kOzBP + 18 * cl]);
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double2 q = src[u];
+    v[2 * u] = q.x;
+    v[2 * u + 1] = q.y;
+  }
   const int64_t plane = static_cast<int64_t>(N) * K;
   uint4 out[kOzS];
-  pack16([&](int u) { return src[u]; }, sc, out);
+  pack16([&](int u) { return v[u]; }, sc, out);
   int8_t* d = sB + item * kOzS * plane + tile_off(j, c, K);
 #pragma unroll
   for (int p = 0; p < kOzS; ++p) *reinterpret_cast<uint4*>(d + p * plane) = out[p];
